@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark: sample-wise LP forward+backward on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config NAME] [--impl b200|reference]
+
+A step is one LP forward + backward (lp_forward_tv then lp_backward_tv with
+the forward's carry tape, i.e. what ``LPTV`` autograd runs) over one batch of
+synthetic D1 input already resident in HBM.  The default
+workload is config 3 of BASELINE.json (B=64, T=48000, M=22, fp32) per GPU;
+with N GPUs (torchrun, one process per GPU) every rank filters its own 64
+sequences with no collective in the filter (batch sharding, weak scaling);
+the timed region is bracketed by a barrier and synchronisation and the
+reported time is the max over ranks.
+
+Besides the device-resident ``value`` the line carries:
+  e2e          the same metric through the public API from pinned HOST
+               buffers: per step H2D of (e, A, grad_s), forward, backward, D2H
+               of (s, grad_e, grad_A), all inside the timed region;
+  roofline     the dominant kernel's algorithmic bytes / its CUDA-event
+               duration (profiling pass over the same K steps) vs the measured
+               HBM copy bandwidth in MEASURED_PEAKS.json, plus the whole step;
+  cpu_baseline the oracle (C port of the reference LP path, oracle/) timed on
+               this host's cores on a bounded sample (rank 0, N=1 only).
+``--impl reference`` times that CPU port alone (the reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LP fwd+bwd audio samples/sec and HBM GB/s vs roofline at 1/2/4/8 B200"
+UNIT = "samples/s"
+
+CONFIGS = {
+    # name: kind, B (per GPU), T, M[, hop]
+    "tv_b64_t48000": dict(kind="tv", B=64, T=48000, M=22, baseline_cfg=3),
+    "tv_b4_t24000": dict(kind="tv", B=4, T=24000, M=22, baseline_cfg=1),
+    "framewise_b32_t48000": dict(kind="framewise", B=32, T=48000, M=22, hop=240, baseline_cfg=2),
+    "tv_b1_t14400000": dict(kind="tv", B=1, T=14_400_000, M=22, baseline_cfg=4),
+}
+DEFAULT = "tv_b64_t48000"
+
+
+def algorithmic_bytes_per_sample(cfg):
+    """TV fwd 4(M+2) + bwd 4(2M+3) = 4(3M+5); frame-wise ~21.1."""
+    M = cfg["M"]
+    if cfg["kind"] == "tv":
+        return 4 * (3 * M + 5)
+    return 21.1
+
+
+# per-kernel algorithmic bytes per sample (what each launch must move at least)
+def kernel_bytes_per_sample(name, M):
+    return {
+        "basis": 4 * (M + 1),          # A, e in
+        "apply_fwd": 4 * (M + 2),      # A, e in; s out
+        "adjoint_zs": 4 * (M + 1),     # A, g_s in
+        "adjoint_apply": 4 * (M + 2),  # A, g_s in; g_e out
+        "grad_A": 4 * (M + 2),         # g_e, s in; g_A out
+    }.get(name)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for n, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle (C port of the reference path), threaded
+# ---------------------------------------------------------------------------
+
+def cpu_baseline(cfg, seconds=10.0):
+    import oracle
+    from paper_2406_05128_b200 import data
+
+    nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    T, M = cfg["T"], cfg["M"]
+    if cfg["kind"] == "tv":
+        T_s = min(T, 480_000)
+        B_s = max(1, min(cfg["B"], 4 * nthreads)) if T <= 480_000 else nthreads
+        e, A, g = data.d1_batch(1000, B_s, T_s, M)
+        kind = "tv"
+    else:
+        T_s = T
+        B_s = max(1, min(cfg["B"], 4 * nthreads))
+        e, A, g = data.d1_frames_batch(1000, B_s, T_s, M, cfg["hop"])
+        kind = "framewise"
+    oracle.batch_fwd_bwd(kind, e[:1], A[:1], g[:1], nthreads=1)  # warm (page-in)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while True:
+        t0 = time.perf_counter()
+        oracle.batch_fwd_bwd(kind, e, A, g, nthreads=nthreads, hop=cfg.get("hop", 240))
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 3 and time.perf_counter() > t_end:
+            break
+        if len(times) >= 50:
+            break
+    med = float(np.median(times))
+    return {"value": B_s * T_s / med, "unit": UNIT, "cores": nthreads, "kind": "port",
+            "sample": f"{B_s} x {T_s} samples (M={M}, D1) fwd+bwd per repeat, median of "
+                      f"{len(times)} repeats, {nthreads} threads, oracle/tvlp_oracle.c"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_b200(args, cfg, rank, world, dist):
+    import torch
+
+    from paper_2406_05128_b200 import _native as N
+    from paper_2406_05128_b200 import data, lpc, params
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    lpc.set_validation("lazy")
+    lib = N.load()
+    B, T, M = cfg["B"], cfg["T"], cfg["M"]
+    kind = cfg["kind"]
+    if kind == "tv":
+        e, A, g = data.d1_batch_torch(rank * B, B, T, M, device=dev)
+
+        def step(e=e, A=A, g=g):
+            s, carry = lpc._forward(False, e, A, None, return_carry=True)
+            ge, gA = lpc._backward(False, g, A, s, None, carry)
+            return s, ge, gA
+    else:
+        ev, fr, gv = data.d1_frames_batch(rank * B, B, T, M, cfg["hop"])
+        e = torch.from_numpy(ev).to(dev)
+        A = torch.from_numpy(fr).to(dev)
+        g = torch.from_numpy(gv).to(dev)
+        plan = params.FramePlan.raised_cosine(cfg["hop"])
+
+        def step(e=e, A=A, g=g):
+            y, seg = params.framewise_forward(e, A, plan)
+            ge, gf = params.framewise_backward(g, A, seg, plan)
+            return y, ge, gf
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = lib.tvlp_launch_count()
+    with Clocks(dev.index) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.tvlp_launch_count() - n0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    lpc.check_nonfinite(dev)
+    samples = B * T * world
+    value = samples / (ms * 1e-3)
+
+    # profiling pass: per-kernel CUDA-event durations over K steps
+    N.profile_dump()
+    lib.tvlp_profile_enable(1)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    lib.tvlp_profile_enable(0)
+    prof = N.profile_dump()
+    hbm, peak_kind = peaks()
+    per_kernel = {}
+    for name, (cnt, tot) in prof.items():
+        avg_ms = tot / max(cnt, 1)
+        per_kernel[name] = {"launches": cnt, "avg_us": round(avg_ms * 1e3, 2),
+                            "share": None}
+    tot_all = sum(v[1] for v in prof.values()) or 1.0
+    for name, (cnt, tot) in prof.items():
+        per_kernel[name]["share"] = round(tot / tot_all, 4)
+    dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
+    roof = None
+    if dom is not None:
+        bps = kernel_bytes_per_sample(dom, M)
+        cnt, tot = prof[dom]
+        avg_s = tot / cnt * 1e-3
+        if bps is not None:
+            ach = bps * B * T / avg_s / 1e9
+            roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm,
+                    "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
+                    "peak_source": peak_kind,
+                    "bytes_per_launch": bps * B * T, "avg_launch_us": round(avg_s * 1e6, 2)}
+        else:
+            roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": hbm,
+                    "unit": "GB/s", "frac": None, "traffic": None}
+    step_gbs = algorithmic_bytes_per_sample(cfg) * B * T / (ms * 1e-3) / 1e9
+
+    # e2e: pinned host buffers through the public API
+    eh, Ah, gh = (x.cpu().pin_memory() for x in (e, A, g))
+    outs = step()
+    oh = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+    h2d = sum(x.numel() * x.element_size() for x in (eh, Ah, gh))
+    d2h = sum(x.numel() * x.element_size() for x in oh)
+
+    def e2e_step():
+        ed = eh.to(dev, non_blocking=True)
+        Ad = Ah.to(dev, non_blocking=True)
+        gd = gh.to(dev, non_blocking=True)
+        res = step(ed, Ad, gd)
+        for o, r in zip(oh, res):
+            o.copy_(r, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = ev0.elapsed_time(ev1) / args.steps
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic D1 (SURVEY.md §8(d)); inputs resident in HBM; working set "
+                f"{round(algorithmic_bytes_per_sample(cfg) * B * T / 1e6)} MB > 126 MB L2 "
+                "(no flush needed)",
+        "config": {"workload": args.config, "baseline_config": cfg["baseline_cfg"],
+                   "kind": kind, "B_per_gpu": B, "T": T, "M": M,
+                   "global_B": B * world, "parallelism": f"batch-shard x{world}",
+                   "carry_precision": lpc.carry_precision(),
+                   "subchunk": int(lib.tvlp_subchunk_len(T, M)) if kind == "tv" else None,
+                   "l2": "inputs larger than L2"},
+        "gbs_algorithmic_step": round(step_gbs, 1),
+        "step_roofline_frac": round(step_gbs / hbm, 4),
+        "roofline": roof,
+        "kernels": per_kernel,
+        "e2e": {"value": round(samples / (e2e_ms * 1e-3), 1), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    return line
+
+
+def run_reference(args, cfg):
+    base = cpu_baseline(cfg, seconds=max(5.0, min(60.0, 2.0 * args.steps)))
+    return {
+        "metric": METRIC, "value": round(base["value"], 1), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic D1 (SURVEY.md §8(d))",
+        "config": {"workload": args.config, "baseline_config": cfg["baseline_cfg"],
+                   "kind": cfg["kind"], "B_per_gpu": cfg["B"], "T": cfg["T"], "M": cfg["M"]},
+        "impl": "reference",
+        "cpu_baseline": base,
+        "e2e": {"value": round(base["value"], 1), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=DEFAULT, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, cfg)), flush=True)
+        return 0
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    line = run_b200(args, cfg, rank, world, dist)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,135 @@
+/*
+ * tvlp.h -- C ABI of the B200-native differentiable linear-prediction kernels
+ * (libtvlp_b200.so).  Plain pointers and sizes only; every pointer is a CUDA
+ * device pointer unless stated otherwise; `stream` is a cudaStream_t (NULL =
+ * legacy default stream).  All calls are asynchronous on `stream`, never
+ * synchronise the host, and return a TVLP_* status (TVLP_ERR_CUDA carries a
+ * launch error; see tvlp_last_cuda_error()).
+ *
+ * Each entry point replaces one function of the reference tvlp 0.1.0 LP path
+ * (files under pkg/src/tvlp/ of arxiv/paper_2406_05128), with a leading batch
+ * axis added (the reference is 1-D only):
+ *
+ *   tvlp_lp_forward_tv       lpc.py:101-117  lp_forward_tv(e, A, zi)   (+ _lp_kernel_tv lpc.py:36-47)
+ *   tvlp_lp_backward_tv      lpc.py:152-173  lp_backward_tv(grad_s, A, s, zi)
+ *   tvlp_lp_forward_ti       lpc.py:82-98    lp_forward_ti(e, a, zi)   (+ _lp_kernel_ti lpc.py:50-61)
+ *   tvlp_lp_backward_ti      lpc.py:176-195  lp_backward_ti(grad_s, a, s, zi)
+ *   tvlp_shift_coeffs        lpc.py:120-135  shift_coeffs(A)
+ *   tvlp_lagged_signal_matrix lpc.py:138-149 lagged_signal_matrix(s, M, zi)
+ *   tvlp_framewise_forward   params.py:220-239 _framewise_forward(e, frames, plan)
+ *   tvlp_framewise_backward  params.py:259-273 _framewise_vjp(grad, e, frames, plan, segs)
+ *
+ * The tape-op contract of lpc.py:202-223 (forward saves the output s and A,
+ * backward returns (grad_e, grad_A), no gradient for zi) is kept: the forward
+ * may additionally emit the "carry tape" (the per-sub-chunk transition
+ * matrices) that the backward reuses instead of recomputing.
+ *
+ * Layouts (C-contiguous): e, s, grad_s, grad_e [B, T]; A, grad_A [B, T, M];
+ * zi [B, M] (nullable = zeros); a, grad_a [B, M]; frames, grad_frames
+ * [B, F, M]; window [frame_size] (the reference's float64 window cast to the
+ * I/O dtype); seg [B, frame_size, n_frames].  dtype: TVLP_F32 or TVLP_F64 for
+ * every floating-point array of the call.
+ */
+#ifndef TVLP_B200_H
+#define TVLP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TVLP_ABI_VERSION 1
+
+#define TVLP_F32 0
+#define TVLP_F64 1
+
+#define TVLP_OK 0
+#define TVLP_ERR_ARG 1       /* bad shape / null pointer / unsupported dtype */
+#define TVLP_ERR_ORDER 2     /* M outside [1, tvlp_max_order()] */
+#define TVLP_ERR_WORKSPACE 3 /* workspace smaller than tvlp_workspace_bytes() */
+#define TVLP_ERR_CUDA 4      /* a CUDA launch failed */
+
+/* precision of the sub-chunk transition matrices ("carries") */
+#define TVLP_CARRY_F64 0 /* fp64 chains, default: matches the fp64 oracle to 1e-4 on resonant tracks */
+#define TVLP_CARRY_F32 1 /* fp32 chains: faster, ~1e-3 relative on near-unit-circle poles */
+
+/* workspace op codes */
+#define TVLP_OP_FWD_TV 0
+#define TVLP_OP_BWD_TV 1
+#define TVLP_OP_FWD_TI 2
+#define TVLP_OP_BWD_TI 3
+#define TVLP_OP_FW_FWD 4
+#define TVLP_OP_FW_BWD 5
+
+int tvlp_abi_version(void);
+const char* tvlp_status_string(int status);
+int tvlp_last_cuda_error(void);
+int32_t tvlp_max_order(void);
+
+/* Number of float32 elements of the carry tape for (B, T, M). */
+int64_t tvlp_carry_elems(int64_t B, int64_t T, int32_t M);
+/* Sub-chunk length used for (T, M) (diagnostics / tests). */
+int64_t tvlp_subchunk_len(int64_t T, int32_t M);
+/* Device workspace bytes needed by `op`; F/frame_size/hop only for frame-wise ops. */
+size_t tvlp_workspace_bytes(int32_t op, int32_t dtype, int64_t B, int64_t T, int32_t M, int64_t F,
+                            int32_t frame_size, int32_t hop);
+/* Number of frames (lead-in included) of the frame-wise plan (params.py:203-217). */
+int64_t tvlp_framewise_nframes(int64_t T, int64_t F, int32_t frame_size, int32_t hop);
+
+/* s = LP_A(e).  carry (nullable): receives tvlp_carry_elems() floats for the
+ * backward.  nonfinite (nullable, device int32): OR-ed with 1 when e or A holds
+ * a non-finite value (lpc.py:64-70, 111-112 reject those; the flag lets the
+ * caller raise without a synchronising check inside the call). */
+int tvlp_lp_forward_tv(int32_t dtype, const void* e, const void* A, const void* zi, void* s,
+                       int64_t B, int64_t T, int32_t M, float* carry, int32_t carry_prec,
+                       void* workspace, size_t workspace_bytes, int32_t* nonfinite, void* stream);
+
+/* (grad_e, grad_A) of lp_forward_tv given the saved output s.  carry: the
+ * tape written by the forward for the same (A, B, T, M), or NULL to recompute. */
+int tvlp_lp_backward_tv(int32_t dtype, const void* grad_s, const void* A, const void* s,
+                        const void* zi, void* grad_e, void* grad_A, int64_t B, int64_t T,
+                        int32_t M, const float* carry, int32_t carry_prec, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* Time-invariant special case: a [B, M] constant row per sequence. */
+int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,
+                       int64_t B, int64_t T, int32_t M, float* carry, int32_t carry_prec,
+                       void* workspace, size_t workspace_bytes, int32_t* nonfinite, void* stream);
+int tvlp_lp_backward_ti(int32_t dtype, const void* grad_s, const void* a, const void* s,
+                        const void* zi, void* grad_e, void* grad_a, int64_t B, int64_t T,
+                        int32_t M, const float* carry, int32_t carry_prec, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+int tvlp_shift_coeffs(int32_t dtype, const void* A, void* out, int64_t B, int64_t T, int32_t M,
+                      void* stream);
+int tvlp_lagged_signal_matrix(int32_t dtype, const void* s, const void* zi, void* out, int64_t B,
+                              int64_t T, int32_t M, void* stream);
+
+/* Frame-wise TI LP with overlap-add.  cola = window.sum()/hop (params.py:199-201).
+ * seg [B, frame_size, tvlp_framewise_nframes()] receives the per-frame outputs
+ * (the reference's seg_outputs), which the backward consumes. */
+int tvlp_framewise_forward(int32_t dtype, const void* e, const void* frames, const void* window,
+                           double cola, void* out, void* seg, int64_t B, int64_t T, int64_t F,
+                           int32_t M, int32_t frame_size, int32_t hop, void* workspace,
+                           size_t workspace_bytes, void* stream);
+int tvlp_framewise_backward(int32_t dtype, const void* grad_out, const void* frames,
+                            const void* window, double cola, const void* seg, void* grad_e,
+                            void* grad_frames, int64_t B, int64_t T, int64_t F, int32_t M,
+                            int32_t frame_size, int32_t hop, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
+/* Instrumentation (bench.py): number of kernels this library has launched,
+ * and optional CUDA-event timing of every launch (off by default; when on,
+ * each launch is bracketed by two events on its stream).  tvlp_profile_dump
+ * writes "name launches total_ms" lines (it synchronises on the recorded
+ * events) and resets the table; returns the number of bytes written. */
+int64_t tvlp_launch_count(void);
+void tvlp_profile_enable(int32_t on);
+int32_t tvlp_profile_dump(char* buf, int32_t buflen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TVLP_B200_H */

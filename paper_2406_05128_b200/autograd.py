@@ -1,0 +1,90 @@
+"""``torch.autograd.Function``s for the LP operators -- the B200 replacement
+of the reference's tape-op registrations (pkg/src/tvlp/lpc.py:202-223 and
+params.py:348-360, contract at tape.py:54-65).
+
+The reference contract is kept: the forward saves its OUTPUT ``s`` and the
+coefficients ``A`` (not ``e``), the backward returns
+``(grad_e, grad_A)`` and nothing for ``zi``.  The forward also
+keeps the carry tape (per-sub-chunk transition matrices) in ``ctx`` so the
+backward does not recompute it.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import lpc
+from . import params as _params
+
+__all__ = ["LPTV", "LPTI", "LPFramewise", "lp_tv", "lp_ti", "framewise"]
+
+
+class LPTV(torch.autograd.Function):
+    """s = LP_A(e) with the analytic adjoint (lpc.py:202-209)."""
+
+    @staticmethod
+    def forward(ctx, e, A, zi=None):
+        A = A.to(e.dtype)
+        s, carry = lpc._forward(False, e.detach(), A.detach(),
+                                None if zi is None else zi.detach(), return_carry=True)
+        ctx.save_for_backward(A, s, zi)
+        ctx.carry = carry
+        return s
+
+    @staticmethod
+    def backward(ctx, grad_s):
+        A, s, zi = ctx.saved_tensors
+        ge, gA = lpc._backward(False, grad_s.contiguous(), A, s, zi, ctx.carry)
+        return ge, gA, None
+
+
+class LPTI(torch.autograd.Function):
+    """Time-invariant filter with the single-filter adjoint (lpc.py:212-219)."""
+
+    @staticmethod
+    def forward(ctx, e, a, zi=None):
+        a = a.to(e.dtype)
+        s, carry = lpc._forward(True, e.detach(), a.detach(),
+                                None if zi is None else zi.detach(), return_carry=True)
+        ctx.save_for_backward(a, s, zi)
+        ctx.carry = carry
+        return s
+
+    @staticmethod
+    def backward(ctx, grad_s):
+        a, s, zi = ctx.saved_tensors
+        ge, ga = lpc._backward(True, grad_s.contiguous(), a, s, zi, ctx.carry)
+        return ge, ga.reshape(a.shape), None
+
+
+class LPFramewise(torch.autograd.Function):
+    """Frame-wise LP with overlap-add (params.py:348-357); saves the frame
+    outputs like the reference's ctx['seg_outputs']."""
+
+    @staticmethod
+    def forward(ctx, e, frames, plan):
+        frames = frames.to(e.dtype)
+        out, seg = _params.framewise_forward(e.detach(), frames.detach(), plan)
+        ctx.save_for_backward(frames, seg)
+        ctx.plan = plan
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        frames, seg = ctx.saved_tensors
+        ge, gf = _params.framewise_backward(grad_out.contiguous(), frames, seg, ctx.plan)
+        return ge, gf, None
+
+
+def lp_tv(e, A, zi=None):
+    """Differentiable sample-wise LP filter."""
+    return LPTV.apply(e, A, zi)
+
+
+def lp_ti(e, a, zi=None):
+    """Differentiable time-invariant LP filter."""
+    return LPTI.apply(e, a, zi)
+
+
+def framewise(e, frames, plan):
+    """Differentiable frame-wise LP with overlap-add."""
+    return LPFramewise.apply(e, frames, plan)

@@ -1,0 +1,664 @@
+// capi.cu -- the C ABI (include/tvlp.h): argument checks, workspace carving,
+// layout normalisation (T padded to a multiple of 4, M padded to a compiled
+// order, 16-byte alignment) and the launch sequences of each operation.
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tvlp.h"
+#include "framewise_launch.cuh"
+#include "lp_scan.cuh"
+#include "scan_launch.cuh"
+
+namespace tvlp {
+namespace {
+
+thread_local int g_last_cuda = 0;
+
+inline int fail_cuda(cudaError_t e) {
+    g_last_cuda = (int)e;
+    return TVLP_ERR_CUDA;
+}
+#define TVLP_CK(x)                                   \
+    do {                                             \
+        cudaError_t e__ = (x);                       \
+        if (e__ != cudaSuccess) return fail_cuda(e__); \
+    } while (0)
+
+constexpr int kMaxOrder = 30;
+
+// ---------------------------------------------------------------- instrumentation
+std::atomic<int64_t> g_launches{0};
+std::atomic<int> g_prof_on{0};
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof;
+
+// Run a launcher, count its kernels and (if enabled) bracket it with events.
+template <typename F>
+cudaError_t tracked(const char* name, int nkernels, cudaStream_t st, F&& launch) {
+    g_launches += nkernels;
+    if (!g_prof_on.load()) return launch();
+    ProfRec r{name, nullptr, nullptr};
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, st);
+    cudaError_t err = launch();
+    cudaEventRecord(r.b, st);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back(r);
+    return err;
+}
+#define TVLP_RUN(name, nk, st, call) TVLP_CK(tracked(name, nk, st, [&]() { return (call); }))
+
+// ---------------------------------------------------------------- geometry
+struct Plan {
+    int64_t B = 0, T = 0, Tp = 0;
+    int M = 0, Mp = 0;
+    int Ls = 0, nsub = 0;
+};
+
+int64_t choose_ls(int64_t Tp, int Mp) {
+    const int unit = ls_unit(Mp);
+    int64_t target = 512;
+    if (const char* env = std::getenv("TVLP_SUBCHUNK")) {
+        const long v = std::atol(env);
+        if (v > 0) target = v;
+    }
+    int64_t k = (target + unit / 2) / unit;
+    if (k < 1) k = 1;
+    int64_t Ls = unit * k;
+    const int64_t single = (Tp + unit - 1) / unit * unit;
+    return Ls < single ? Ls : single;
+}
+
+bool make_plan(int64_t B, int64_t T, int M, Plan& p) {
+    if (B < 1 || T < 1 || M < 1 || M > kMaxOrder) return false;
+    p.B = B;
+    p.T = T;
+    p.Tp = (T + 3) / 4 * 4;
+    p.M = M;
+    p.Mp = padded_order(M);
+    p.Ls = (int)choose_ls(p.Tp, p.Mp);
+    p.nsub = (int)((p.Tp + p.Ls - 1) / p.Ls);
+    return true;
+}
+
+ScanArgs scan_args(const Plan& p) {
+    ScanArgs g;
+    g.B = p.B;
+    g.T = p.Tp;
+    g.Ls = p.Ls;
+    g.nsub = p.nsub;
+    return g;
+}
+
+int64_t carry_elems(const Plan& p) { return p.B * (int64_t)p.nsub * (p.Mp + 1) * p.Mp; }
+
+// bump allocator over the caller's workspace (nullptr base = sizing pass)
+struct Carver {
+    unsigned char* base;
+    size_t used = 0;
+    explicit Carver(void* b) : base(static_cast<unsigned char*>(b)) {}
+    void* take(size_t bytes) {
+        used = (used + 255) / 256 * 256;
+        void* p = base ? base + used : nullptr;
+        used += bytes;
+        return p;
+    }
+};
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------- pack kernels
+// dst[b, t, c] (Tp x Mp, zero-filled) <- src[b, t, c] (T x M)
+template <typename IO>
+__global__ void k_pack(const IO* __restrict__ src, IO* __restrict__ dst, int64_t B, int64_t T,
+                       int M, int64_t Tp, int Mp) {
+    const int64_t n = B * Tp * Mp;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % Mp);
+        const int64_t bt = i / Mp;
+        const int64_t t = bt % Tp, b = bt / Tp;
+        dst[i] = (t < T && c < M) ? src[(b * T + t) * M + c] : (IO)0;
+    }
+}
+template <typename IO>
+__global__ void k_unpack(const IO* __restrict__ src, IO* __restrict__ dst, int64_t B, int64_t T,
+                         int M, int64_t Tp, int Mp) {
+    const int64_t n = B * T * M;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % M);
+        const int64_t bt = i / M;
+        const int64_t t = bt % T, b = bt / T;
+        dst[i] = src[(b * Tp + t) * Mp + c];
+    }
+}
+inline unsigned grid_for(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    if (g > 148 * 64) g = 148 * 64;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+template <typename IO>
+cudaError_t pack(const void* src, void* dst, int64_t B, int64_t T, int M, int64_t Tp, int Mp,
+                 cudaStream_t st) {
+    g_launches += 1;
+    k_pack<IO><<<grid_for(B * Tp * Mp), 256, 0, st>>>(static_cast<const IO*>(src),
+                                                       static_cast<IO*>(dst), B, T, M, Tp, Mp);
+    return cudaGetLastError();
+}
+template <typename IO>
+cudaError_t unpack(const void* src, void* dst, int64_t B, int64_t T, int M, int64_t Tp, int Mp,
+                   cudaStream_t st) {
+    g_launches += 1;
+    k_unpack<IO><<<grid_for(B * T * M), 256, 0, st>>>(static_cast<const IO*>(src),
+                                                       static_cast<IO*>(dst), B, T, M, Tp, Mp);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- small ops
+template <typename IO>
+__global__ void k_shift(const IO* __restrict__ A, IO* __restrict__ out, int64_t B, int64_t T,
+                        int M) {
+    const int64_t n = B * T * M;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % M);
+        const int64_t bt = i / M;
+        const int64_t t = bt % T, b = bt / T;
+        const int64_t src = t + c + 1;  // A_hat[t, i-1] = A[t+i, i-1], i = c+1
+        out[i] = src < T ? A[(b * T + src) * M + c] : (IO)0;
+    }
+}
+template <typename IO>
+__global__ void k_lag(const IO* __restrict__ s, const IO* __restrict__ zi, IO* __restrict__ out,
+                      int64_t B, int64_t T, int M) {
+    const int64_t n = B * T * M;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % M);
+        const int64_t bt = i / M;
+        const int64_t t = bt % T, b = bt / T;
+        const int64_t src = t - c - 1;
+        out[i] = src >= 0 ? s[b * T + src] : (zi ? zi[b * M + (c - t)] : (IO)0);
+    }
+}
+
+// ---------------------------------------------------------------- TV / TI
+template <typename IO>
+int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s, const Plan& p,
+                 float* carry, int prec, void* ws, size_t ws_bytes, int32_t* nonfinite,
+                 cudaStream_t st, size_t* need) {
+    const size_t sz = sizeof(IO);
+    const bool packed = p.Tp != p.T || p.Mp != p.M || !aligned16(e) || !aligned16(A) ||
+                        !aligned16(s) || (zi && !aligned16(zi));
+    const int64_t nsc = p.B * p.nsub;
+    Carver c(ws);
+    float* phiz = carry ? carry : static_cast<float*>(c.take(carry_elems(p) * 4));
+    float* xin = static_cast<float*>(c.take(nsc * p.Mp * 4));
+    const IO* e_p = static_cast<const IO*>(e);
+    const IO* A_p = static_cast<const IO*>(A);
+    const IO* zi_p = static_cast<const IO*>(zi);
+    IO* s_p = static_cast<IO*>(s);
+    void *pe = nullptr, *pA = nullptr, *ps = nullptr, *pz = nullptr;
+    if (packed) {
+        pe = c.take(p.B * p.Tp * sz);
+        pA = c.take((ti ? p.B : p.B * p.Tp) * p.Mp * sz);
+        ps = c.take(p.B * p.Tp * sz);
+        if (zi) pz = c.take(p.B * p.Mp * sz);
+    }
+    if (need) {
+        *need = c.used;
+        return TVLP_OK;
+    }
+    if (ws_bytes < c.used) return TVLP_ERR_WORKSPACE;
+    const ScanArgs g = scan_args(p);
+    if (packed) {
+        TVLP_CK(pack<IO>(e, pe, p.B, p.T, 1, p.Tp, 1, st));
+        if (ti)
+            TVLP_CK(pack<IO>(A, pA, p.B, 1, p.M, 1, p.Mp, st));
+        else
+            TVLP_CK(pack<IO>(A, pA, p.B, p.T, p.M, p.Tp, p.Mp, st));
+        if (zi) TVLP_CK(pack<IO>(zi, pz, p.B, 1, p.M, 1, p.Mp, st));
+        e_p = static_cast<const IO*>(pe);
+        A_p = static_cast<const IO*>(pA);
+        zi_p = static_cast<const IO*>(pz);
+        s_p = static_cast<IO*>(ps);
+    }
+    TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, e_p, A_p, phiz, g, st)));
+    TVLP_RUN("carry_fwd", 1, st, (launch_carry_fwd(p.Mp, phiz, zi_p, sizeof(IO) == 8, xin, g, st)));
+    TVLP_RUN("apply_fwd", 1, st, (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, g, st)));
+    if (packed) TVLP_CK(unpack<IO>(ps, s, p.B, p.T, 1, p.Tp, 1, st));
+    return TVLP_OK;
+}
+
+inline int grad_a_chunks(const Plan& p) {
+    int64_t n = p.Tp / 2048;
+    if (n < 1) n = 1;
+    if (n > 256) n = 256;
+    return (int)n;
+}
+
+template <typename IO>
+int backward_impl(bool ti, const void* gs, const void* A, const void* s, const void* zi, void* ge,
+                  void* gA, const Plan& p, const float* carry, int prec, void* ws,
+                  size_t ws_bytes, cudaStream_t st, size_t* need) {
+    const size_t sz = sizeof(IO);
+    const bool packed = p.Tp != p.T || p.Mp != p.M || !aligned16(gs) || !aligned16(A) ||
+                        !aligned16(s) || !aligned16(ge) || (!ti && !aligned16(gA)) ||
+                        (zi && !aligned16(zi));
+    const int64_t nsc = p.B * p.nsub;
+    Carver c(ws);
+    float* phiz_own = carry ? nullptr : static_cast<float*>(c.take(carry_elems(p) * 4));
+    float* nu = static_cast<float*>(c.take(nsc * p.Mp * 4));
+    float* mu = static_cast<float*>(c.take(nsc * p.Mp * 4));
+    const int nchunk = grad_a_chunks(p);
+    IO* part = ti ? static_cast<IO*>(c.take(p.B * (int64_t)nchunk * p.Mp * sz)) : nullptr;
+    IO* ga_p = (ti && p.Mp != p.M) ? static_cast<IO*>(c.take(p.B * p.Mp * sz)) : nullptr;
+    const IO* gs_p = static_cast<const IO*>(gs);
+    const IO* A_p = static_cast<const IO*>(A);
+    const IO* s_p = static_cast<const IO*>(s);
+    const IO* zi_p = static_cast<const IO*>(zi);
+    IO* ge_p = static_cast<IO*>(ge);
+    IO* gA_p = static_cast<IO*>(gA);
+    void *pgs = nullptr, *pA = nullptr, *ps = nullptr, *pz = nullptr, *pge = nullptr,
+         *pgA = nullptr;
+    if (packed) {
+        pgs = c.take(p.B * p.Tp * sz);
+        pA = c.take((ti ? p.B : p.B * p.Tp) * p.Mp * sz);
+        ps = c.take(p.B * p.Tp * sz);
+        if (zi) pz = c.take(p.B * p.Mp * sz);
+        pge = c.take(p.B * p.Tp * sz);
+        if (!ti) pgA = c.take(p.B * p.Tp * p.Mp * sz);
+    }
+    if (need) {
+        *need = c.used;
+        return TVLP_OK;
+    }
+    if (ws_bytes < c.used) return TVLP_ERR_WORKSPACE;
+    const ScanArgs g = scan_args(p);
+    if (packed) {
+        TVLP_CK(pack<IO>(gs, pgs, p.B, p.T, 1, p.Tp, 1, st));
+        if (ti)
+            TVLP_CK(pack<IO>(A, pA, p.B, 1, p.M, 1, p.Mp, st));
+        else
+            TVLP_CK(pack<IO>(A, pA, p.B, p.T, p.M, p.Tp, p.Mp, st));
+        TVLP_CK(pack<IO>(s, ps, p.B, p.T, 1, p.Tp, 1, st));
+        if (zi) TVLP_CK(pack<IO>(zi, pz, p.B, 1, p.M, 1, p.Mp, st));
+        gs_p = static_cast<const IO*>(pgs);
+        A_p = static_cast<const IO*>(pA);
+        s_p = static_cast<const IO*>(ps);
+        zi_p = static_cast<const IO*>(pz);
+        ge_p = static_cast<IO*>(pge);
+        gA_p = static_cast<IO*>(pgA);
+    }
+    const float* phiz = carry;
+    if (!phiz) {
+        // transition matrices only (the zero-state row is unused here; s is a
+        // valid stand-in for e of the same shape)
+        TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, s_p, A_p, phiz_own, g, st)));
+        phiz = phiz_own;
+    }
+    TVLP_RUN("adjoint_zs", 1, st, (launch_adjoint<IO>(p.Mp, ti, 0, gs_p, A_p, nullptr, nu, nullptr, g, st)));
+    TVLP_RUN("carry_bwd", 1, st, (launch_carry_bwd(p.Mp, phiz, nu, mu, g, st)));
+    TVLP_RUN("adjoint_apply", 1, st, (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, g, st)));
+    if (ti) {
+        IO* ga_out = ga_p ? ga_p : static_cast<IO*>(gA);
+        TVLP_RUN("grad_a", 2, st, (launch_grad_a<IO>(p.Mp, ge_p, s_p, zi_p, part, ga_out, p.B, p.Tp, nchunk, st)));
+        if (ga_p) TVLP_CK(unpack<IO>(ga_p, gA, p.B, 1, p.M, 1, p.Mp, st));
+    } else {
+        TVLP_RUN("grad_A", 1, st, (launch_grad_A<IO>(p.Mp, ge_p, s_p, zi_p, gA_p, p.B, p.Tp, st)));
+    }
+    if (packed) {
+        TVLP_CK(unpack<IO>(pge, ge, p.B, p.T, 1, p.Tp, 1, st));
+        if (!ti) TVLP_CK(unpack<IO>(pgA, gA, p.B, p.T, p.M, p.Tp, p.Mp, st));
+    }
+    return TVLP_OK;
+}
+
+// ---------------------------------------------------------------- frame-wise
+bool fw_args(int64_t B, int64_t T, int64_t F, int M, int size, int hop, double cola, FwArgs& a) {
+    if (B < 1 || T < 1 || M < 1 || M > kMaxOrder || size < 1 || hop < 1) return false;
+    if (F != (T - 1) / hop + 1) return false;  // params.py:223-227
+    a.B = B;
+    a.T = T;
+    a.F = (int)F;
+    a.size = size;
+    a.hop = hop;
+    a.n_lead = (size - 1) / hop;  // params.py:203-207
+    a.nfr = (int)(F + a.n_lead);
+    a.cola = cola;
+    return true;
+}
+
+template <typename IO>
+int fw_forward_impl(const void* e, const void* frames, const void* win, void* out, void* seg,
+                    const FwArgs& a, int M, void* ws, size_t ws_bytes, cudaStream_t st,
+                    size_t* need) {
+    const int Mp = padded_order(M);
+    Carver c(ws);
+    void* fp = (Mp != M) ? c.take(a.B * (int64_t)a.F * Mp * sizeof(IO)) : nullptr;
+    if (need) {
+        *need = c.used;
+        return TVLP_OK;
+    }
+    if (ws_bytes < c.used) return TVLP_ERR_WORKSPACE;
+    const IO* fr = static_cast<const IO*>(frames);
+    if (fp) {
+        TVLP_CK(pack<IO>(frames, fp, a.B, a.F, M, a.F, Mp, st));
+        fr = static_cast<const IO*>(fp);
+    }
+    TVLP_RUN("fw_forward", 2, st,
+             (launch_fw_forward<IO>(Mp, static_cast<const IO*>(e), fr, static_cast<const IO*>(win),
+                                    static_cast<IO*>(seg), static_cast<IO*>(out), a, st)));
+    return TVLP_OK;
+}
+
+template <typename IO>
+int fw_backward_impl(const void* gout, const void* frames, const void* win, const void* seg,
+                     void* ge, void* gf, const FwArgs& a, int M, void* ws, size_t ws_bytes,
+                     cudaStream_t st, size_t* need) {
+    const int Mp = padded_order(M);
+    Carver c(ws);
+    void* fp = (Mp != M) ? c.take(a.B * (int64_t)a.F * Mp * sizeof(IO)) : nullptr;
+    void* gfp = (Mp != M) ? c.take(a.B * (int64_t)a.F * Mp * sizeof(IO)) : nullptr;
+    IO* gew = static_cast<IO*>(c.take(a.B * (int64_t)a.size * a.nfr * sizeof(IO)));
+    IO* gap = static_cast<IO*>(c.take(a.B * (int64_t)a.nfr * Mp * sizeof(IO)));
+    if (need) {
+        *need = c.used;
+        return TVLP_OK;
+    }
+    if (ws_bytes < c.used) return TVLP_ERR_WORKSPACE;
+    const IO* fr = static_cast<const IO*>(frames);
+    if (fp) {
+        TVLP_CK(pack<IO>(frames, fp, a.B, a.F, M, a.F, Mp, st));
+        fr = static_cast<const IO*>(fp);
+    }
+    IO* gf_out = gfp ? static_cast<IO*>(gfp) : static_cast<IO*>(gf);
+    TVLP_RUN("fw_backward", 3, st,
+             (launch_fw_backward<IO>(Mp, M, static_cast<const IO*>(gout), fr,
+                                     static_cast<const IO*>(win), static_cast<const IO*>(seg), gew,
+                                     gap, static_cast<IO*>(ge), gf_out, a, st)));
+    if (gfp) TVLP_CK(unpack<IO>(gfp, gf, a.B, a.F, M, a.F, Mp, st));
+    return TVLP_OK;
+}
+
+}  // namespace
+}  // namespace tvlp
+
+using namespace tvlp;
+
+extern "C" {
+
+int tvlp_abi_version(void) { return TVLP_ABI_VERSION; }
+
+const char* tvlp_status_string(int status) {
+    switch (status) {
+        case TVLP_OK: return "ok";
+        case TVLP_ERR_ARG: return "invalid argument";
+        case TVLP_ERR_ORDER: return "unsupported filter order";
+        case TVLP_ERR_WORKSPACE: return "workspace too small";
+        case TVLP_ERR_CUDA: return cudaGetErrorString((cudaError_t)g_last_cuda);
+        default: return "unknown status";
+    }
+}
+
+int tvlp_last_cuda_error(void) { return g_last_cuda; }
+
+int32_t tvlp_max_order(void) { return kMaxOrder; }
+
+int64_t tvlp_launch_count(void) { return g_launches.load(); }
+
+void tvlp_profile_enable(int32_t on) { g_prof_on.store(on ? 1 : 0); }
+
+int32_t tvlp_profile_dump(char* buf, int32_t buflen) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    std::vector<std::string> names;
+    std::vector<double> ms;
+    std::vector<long> cnt;
+    for (auto& r : g_prof) {
+        cudaEventSynchronize(r.b);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        size_t k = 0;
+        while (k < names.size() && names[k] != r.name) ++k;
+        if (k == names.size()) {
+            names.emplace_back(r.name);
+            ms.push_back(0.0);
+            cnt.push_back(0);
+        }
+        ms[k] += t;
+        cnt[k] += 1;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+    std::string out;
+    char line[160];
+    for (size_t k = 0; k < names.size(); ++k) {
+        std::snprintf(line, sizeof(line), "%s %ld %.6f\n", names[k].c_str(), cnt[k], ms[k]);
+        out += line;
+    }
+    if (buf && buflen > 0) {
+        const int n = (int)std::min<size_t>(out.size(), (size_t)buflen - 1);
+        std::memcpy(buf, out.data(), n);
+        buf[n] = 0;
+        return n;
+    }
+    return (int32_t)out.size();
+}
+
+int64_t tvlp_carry_elems(int64_t B, int64_t T, int32_t M) {
+    Plan p;
+    if (!make_plan(B, T, M, p)) return -1;
+    return carry_elems(p);
+}
+
+int64_t tvlp_subchunk_len(int64_t T, int32_t M) {
+    Plan p;
+    if (!make_plan(1, T, M, p)) return -1;
+    return p.Ls;
+}
+
+int64_t tvlp_framewise_nframes(int64_t T, int64_t F, int32_t frame_size, int32_t hop) {
+    FwArgs a;
+    if (!fw_args(1, T, F, 1, frame_size, hop, 1.0, a)) return -1;
+    return a.nfr;
+}
+
+static int check_common(int32_t dtype, int32_t M) {
+    if (dtype != TVLP_F32 && dtype != TVLP_F64) return TVLP_ERR_ARG;
+    if (M < 1 || M > kMaxOrder) return TVLP_ERR_ORDER;
+    return TVLP_OK;
+}
+
+size_t tvlp_workspace_bytes(int32_t op, int32_t dtype, int64_t B, int64_t T, int32_t M,
+                            int64_t F, int32_t frame_size, int32_t hop) {
+    if (check_common(dtype, M) != TVLP_OK) return 0;
+    size_t need = 0;
+    const bool f64 = dtype == TVLP_F64;
+    // sizing pass: fake non-null, unaligned pointers force the packed layout
+    const void* any = reinterpret_cast<const void*>(uintptr_t(1));
+    if (op <= TVLP_OP_BWD_TI) {
+        Plan p;
+        if (!make_plan(B, T, M, p)) return 0;
+        const bool ti = op == TVLP_OP_FWD_TI || op == TVLP_OP_BWD_TI;
+        if (op == TVLP_OP_FWD_TV || op == TVLP_OP_FWD_TI) {
+            if (f64)
+                forward_impl<double>(ti, any, any, any, (void*)any, p, nullptr, 0, nullptr, 0,
+                                     nullptr, 0, &need);
+            else
+                forward_impl<float>(ti, any, any, any, (void*)any, p, nullptr, 0, nullptr, 0,
+                                    nullptr, 0, &need);
+        } else {
+            if (f64)
+                backward_impl<double>(ti, any, any, any, any, (void*)any, (void*)any, p, nullptr,
+                                      0, nullptr, 0, 0, &need);
+            else
+                backward_impl<float>(ti, any, any, any, any, (void*)any, (void*)any, p, nullptr,
+                                     0, nullptr, 0, 0, &need);
+        }
+        return need;
+    }
+    FwArgs a;
+    if (!fw_args(B, T, F, M, frame_size, hop, 1.0, a)) return 0;
+    if (op == TVLP_OP_FW_FWD) {
+        if (f64)
+            fw_forward_impl<double>(any, any, any, (void*)any, (void*)any, a, M, nullptr, 0, 0,
+                                    &need);
+        else
+            fw_forward_impl<float>(any, any, any, (void*)any, (void*)any, a, M, nullptr, 0, 0,
+                                   &need);
+    } else if (op == TVLP_OP_FW_BWD) {
+        if (f64)
+            fw_backward_impl<double>(any, any, any, any, (void*)any, (void*)any, a, M, nullptr, 0,
+                                     0, &need);
+        else
+            fw_backward_impl<float>(any, any, any, any, (void*)any, (void*)any, a, M, nullptr, 0,
+                                    0, &need);
+    }
+    return need;
+}
+
+static int fwd_entry(bool ti, int32_t dtype, const void* e, const void* A, const void* zi,
+                     void* s, int64_t B, int64_t T, int32_t M, float* carry, int32_t prec,
+                     void* ws, size_t ws_bytes, int32_t* nonfinite, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!e || !A || !s) return TVLP_ERR_ARG;
+    Plan p;
+    if (!make_plan(B, T, M, p)) return TVLP_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64)
+        return forward_impl<double>(ti, e, A, zi, s, p, carry, TVLP_CARRY_F64, ws, ws_bytes,
+                                    nonfinite, st, nullptr);
+    return forward_impl<float>(ti, e, A, zi, s, p, carry, prec, ws, ws_bytes, nonfinite, st,
+                               nullptr);
+}
+
+static int bwd_entry(bool ti, int32_t dtype, const void* gs, const void* A, const void* s,
+                     const void* zi, void* ge, void* gA, int64_t B, int64_t T, int32_t M,
+                     const float* carry, int32_t prec, void* ws, size_t ws_bytes, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!gs || !A || !s || !ge || !gA) return TVLP_ERR_ARG;
+    Plan p;
+    if (!make_plan(B, T, M, p)) return TVLP_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64)
+        return backward_impl<double>(ti, gs, A, s, zi, ge, gA, p, carry, TVLP_CARRY_F64, ws,
+                                     ws_bytes, st, nullptr);
+    return backward_impl<float>(ti, gs, A, s, zi, ge, gA, p, carry, prec, ws, ws_bytes, st,
+                                nullptr);
+}
+
+int tvlp_lp_forward_tv(int32_t dtype, const void* e, const void* A, const void* zi, void* s,
+                       int64_t B, int64_t T, int32_t M, float* carry, int32_t carry_prec,
+                       void* workspace, size_t workspace_bytes, int32_t* nonfinite, void* stream) {
+    return fwd_entry(false, dtype, e, A, zi, s, B, T, M, carry, carry_prec, workspace,
+                     workspace_bytes, nonfinite, stream);
+}
+
+int tvlp_lp_backward_tv(int32_t dtype, const void* grad_s, const void* A, const void* s,
+                        const void* zi, void* grad_e, void* grad_A, int64_t B, int64_t T,
+                        int32_t M, const float* carry, int32_t carry_prec, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    return bwd_entry(false, dtype, grad_s, A, s, zi, grad_e, grad_A, B, T, M, carry, carry_prec,
+                     workspace, workspace_bytes, stream);
+}
+
+int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,
+                       int64_t B, int64_t T, int32_t M, float* carry, int32_t carry_prec,
+                       void* workspace, size_t workspace_bytes, int32_t* nonfinite, void* stream) {
+    return fwd_entry(true, dtype, e, a, zi, s, B, T, M, carry, carry_prec, workspace,
+                     workspace_bytes, nonfinite, stream);
+}
+
+int tvlp_lp_backward_ti(int32_t dtype, const void* grad_s, const void* a, const void* s,
+                        const void* zi, void* grad_e, void* grad_a, int64_t B, int64_t T,
+                        int32_t M, const float* carry, int32_t carry_prec, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    return bwd_entry(true, dtype, grad_s, a, s, zi, grad_e, grad_a, B, T, M, carry, carry_prec,
+                     workspace, workspace_bytes, stream);
+}
+
+int tvlp_shift_coeffs(int32_t dtype, const void* A, void* out, int64_t B, int64_t T, int32_t M,
+                      void* stream) {
+    if (dtype != TVLP_F32 && dtype != TVLP_F64) return TVLP_ERR_ARG;
+    if (!A || !out || B < 1 || T < 1 || M < 1) return TVLP_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = grid_for(B * T * M);
+    if (dtype == TVLP_F64)
+        k_shift<double><<<grid, 256, 0, st>>>(static_cast<const double*>(A),
+                                              static_cast<double*>(out), B, T, M);
+    else
+        k_shift<float><<<grid, 256, 0, st>>>(static_cast<const float*>(A),
+                                             static_cast<float*>(out), B, T, M);
+    TVLP_CK(cudaGetLastError());
+    return TVLP_OK;
+}
+
+int tvlp_lagged_signal_matrix(int32_t dtype, const void* s, const void* zi, void* out, int64_t B,
+                              int64_t T, int32_t M, void* stream) {
+    if (dtype != TVLP_F32 && dtype != TVLP_F64) return TVLP_ERR_ARG;
+    if (!s || !out || B < 1 || T < 1 || M < 1) return TVLP_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = grid_for(B * T * M);
+    if (dtype == TVLP_F64)
+        k_lag<double><<<grid, 256, 0, st>>>(static_cast<const double*>(s),
+                                            static_cast<const double*>(zi),
+                                            static_cast<double*>(out), B, T, M);
+    else
+        k_lag<float><<<grid, 256, 0, st>>>(static_cast<const float*>(s),
+                                           static_cast<const float*>(zi),
+                                           static_cast<float*>(out), B, T, M);
+    TVLP_CK(cudaGetLastError());
+    return TVLP_OK;
+}
+
+int tvlp_framewise_forward(int32_t dtype, const void* e, const void* frames, const void* window,
+                           double cola, void* out, void* seg, int64_t B, int64_t T, int64_t F,
+                           int32_t M, int32_t frame_size, int32_t hop, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!e || !frames || !window || !out || !seg) return TVLP_ERR_ARG;
+    FwArgs a;
+    if (!fw_args(B, T, F, M, frame_size, hop, cola, a)) return TVLP_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64)
+        return fw_forward_impl<double>(e, frames, window, out, seg, a, M, workspace,
+                                       workspace_bytes, st, nullptr);
+    return fw_forward_impl<float>(e, frames, window, out, seg, a, M, workspace, workspace_bytes,
+                                  st, nullptr);
+}
+
+int tvlp_framewise_backward(int32_t dtype, const void* grad_out, const void* frames,
+                            const void* window, double cola, const void* seg, void* grad_e,
+                            void* grad_frames, int64_t B, int64_t T, int64_t F, int32_t M,
+                            int32_t frame_size, int32_t hop, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!grad_out || !frames || !window || !seg || !grad_e || !grad_frames) return TVLP_ERR_ARG;
+    FwArgs a;
+    if (!fw_args(B, T, F, M, frame_size, hop, cola, a)) return TVLP_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64)
+        return fw_backward_impl<double>(grad_out, frames, window, seg, grad_e, grad_frames, a, M,
+                                        workspace, workspace_bytes, st, nullptr);
+    return fw_backward_impl<float>(grad_out, frames, window, seg, grad_e, grad_frames, a, M,
+                                   workspace, workspace_bytes, st, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,152 @@
+// common.cuh -- sm_100a helpers shared by the LP kernels.
+//
+// 1-D bulk TMA (cp.async.bulk) global<->shared copies completed on mbarriers,
+// compile-time-aligned vector row loads, warp reductions.
+#pragma once
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+
+namespace tvlp {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---------------------------------------------------------------- mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// ---------------------------------------------------------------- bulk TMA
+// global -> shared, completion signalled as tx bytes on `bar`.
+// src, dst and bytes must be multiples of 16.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// shared -> global, tracked by the issuing thread's bulk groups.
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// order generic-proxy shared accesses before subsequent async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- warp utils
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// round `bytes` up to 16 and make (bytes/16) odd: per-lane slot strides with an
+// odd number of 16-byte granules keep 8 consecutive lanes' 16-B accesses in
+// distinct bank groups.
+constexpr int odd16_stride(int bytes) {
+    int b = (bytes + 15) / 16 * 16;
+    return ((b / 16) % 2 == 0) ? b + 16 : b;
+}
+constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+constexpr int clcm(int a, int b) { return a / cgcd(a, b) * b; }
+
+// ---------------------------------------------------------------- row loads
+// Load M consecutive T values from shared memory at `p` into registers, using
+// the widest vector accesses the compile-time alignment OFF (= address mod 16)
+// allows.
+template <typename T, int M, int I, int OFF>
+struct RowLoad {
+    static __device__ __forceinline__ void run(const T* p, T* a) {
+        if constexpr (I < M) {
+            constexpr int off = (OFF + I * (int)sizeof(T)) & 15;
+            if constexpr (sizeof(T) == 4 && off == 0 && I + 4 <= M) {
+                float4 v = *reinterpret_cast<const float4*>(p + I);
+                a[I] = v.x;
+                a[I + 1] = v.y;
+                a[I + 2] = v.z;
+                a[I + 3] = v.w;
+                RowLoad<T, M, I + 4, OFF>::run(p, a);
+            } else if constexpr (sizeof(T) == 4 && (off & 7) == 0 && I + 2 <= M) {
+                float2 v = *reinterpret_cast<const float2*>(p + I);
+                a[I] = v.x;
+                a[I + 1] = v.y;
+                RowLoad<T, M, I + 2, OFF>::run(p, a);
+            } else if constexpr (sizeof(T) == 8 && off == 0 && I + 2 <= M) {
+                double2 v = *reinterpret_cast<const double2*>(p + I);
+                a[I] = v.x;
+                a[I + 1] = v.y;
+                RowLoad<T, M, I + 2, OFF>::run(p, a);
+            } else {
+                a[I] = p[I];
+                RowLoad<T, M, I + 1, OFF>::run(p, a);
+            }
+        }
+    }
+};
+template <typename T, int M, int OFF>
+__device__ __forceinline__ void load_row(const T* p, T (&a)[M]) {
+    RowLoad<T, M, 0, OFF>::run(p, a);
+}
+
+// Same, with the alignment given as a value that is a compile-time constant
+// after loop unrolling (the switch folds away).
+template <typename T, int M>
+__device__ __forceinline__ void load_row_at(const T* p, T (&a)[M], int off) {
+    switch (off & 15) {
+        case 0: load_row<T, M, 0>(p, a); break;
+        case 4: load_row<T, M, 4>(p, a); break;
+        case 8: load_row<T, M, 8>(p, a); break;
+        default: load_row<T, M, 12>(p, a); break;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ bool is_finite_val(T x) {
+    return isfinite(x);
+}
+
+}  // namespace tvlp

@@ -1,0 +1,24 @@
+// framewise_launch.cuh -- host launchers for the frame-wise LP kernels (internal).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tvlp {
+
+struct FwArgs {
+    int64_t B, T;
+    int F, nfr, size, hop, n_lead;
+    double cola;
+};
+
+// seg: [B, size, nfr] saved frame outputs; out: [B, T]
+template <typename IO>
+cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* win, IO* seg,
+                              IO* out, const FwArgs& a, cudaStream_t st);
+// gew: [B, size, nfr] scratch, gapart: [B, nfr, Mp] scratch; ge: [B, T]; gf: [B, F, Mp]
+template <typename IO>
+cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, const IO* win,
+                               const IO* seg, IO* gew, IO* gapart, IO* ge, IO* gf,
+                               const FwArgs& a, cudaStream_t st);
+
+}  // namespace tvlp

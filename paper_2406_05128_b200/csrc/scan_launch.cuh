@@ -1,0 +1,43 @@
+// scan_launch.cuh -- host launchers for the chunked-scan kernels (internal).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tvlp {
+
+struct ScanArgs;
+
+// Orders with compiled kernels; other orders are zero-padded up to the next
+// one by the C ABI (exact: padded coefficients are 0).
+constexpr int kNumOrders = 9;
+constexpr int kOrders[kNumOrders] = {2, 4, 6, 8, 12, 16, 22, 24, 30};
+inline int padded_order(int M) {
+    for (int i = 0; i < kNumOrders; ++i)
+        if (kOrders[i] >= M) return kOrders[i];
+    return -1;
+}
+int ls_unit(int Mp);  // sub-chunk length granularity for order Mp
+
+enum Prec : int { kPrecF64Chains = 0, kPrecF32Chains = 1 };
+
+template <typename IO>
+cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, float* PhiZ,
+                         const ScanArgs& g, cudaStream_t st);
+cudaError_t launch_carry_fwd(int Mp, const float* PhiZ, const void* zi, bool zi_double,
+                             float* Xin, const ScanArgs& g, cudaStream_t st);
+cudaError_t launch_carry_bwd(int Mp, const float* PhiZ, const float* Nu, float* Mu,
+                             const ScanArgs& g, cudaStream_t st);
+template <typename IO>
+cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const float* Xin, IO* s,
+                             int* flag, const ScanArgs& g, cudaStream_t st);
+template <typename IO>
+cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const float* Mu,
+                           float* Nu, IO* ge, const ScanArgs& g, cudaStream_t st);
+template <typename IO>
+cudaError_t launch_grad_A(int Mp, const IO* ge, const IO* s, const IO* zi, IO* gA, int64_t B,
+                          int64_t T, cudaStream_t st);
+template <typename IO>
+cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* part, IO* ga,
+                          int64_t B, int64_t T, int nchunk, cudaStream_t st);
+
+}  // namespace tvlp

@@ -1,0 +1,321 @@
+"""Sample-wise all-pole filtering on B200 -- the reference ``tvlp.lpc`` API.
+
+Drop-in for pkg/src/tvlp/lpc.py (reference tvlp 0.1.0): same function names,
+argument order, validation messages and return values, with an optional
+leading batch axis.  Arrays may be CUDA tensors (results stay on the device)
+or numpy arrays (moved to ``cuda:0`` and returned as numpy).  All arithmetic
+runs in the sm_100a kernels of libtvlp_b200.so; there is no CPU path.
+
+    s(t) = e(t) - sum_{i=1..M} A[t, i-1] s(t-i)          (lpc.py:1-13)
+
+Shapes: e [T] or [B, T]; A [T, M] or [B, T, M]; a [M] or [B, M]; zi [M] or
+[B, M] with zi[i-1] = s(-i).  dtype float32 (production) or float64
+(gradient checking); A is cast to e's dtype (lpc.py:113).
+
+Non-finite e/A raise ``ValueError`` like lpc.py:68-69/111-112.  The check is
+fused into the forward kernel (a device flag); ``set_validation("eager")``
+(default) reads the flag after each forward (one 4-byte device->host read),
+``"lazy"`` accumulates it until :func:`check_nonfinite`, ``"off"`` skips it.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+__all__ = [
+    "lp_forward_ti",
+    "lp_forward_tv",
+    "lp_backward_ti",
+    "lp_backward_tv",
+    "shift_coeffs",
+    "lagged_signal_matrix",
+    "set_validation",
+    "check_nonfinite",
+    "set_carry_precision",
+    "carry_precision",
+]
+
+_VALIDATION = os.environ.get("TVLP_VALIDATION", "eager")
+_CARRY = os.environ.get("TVLP_CARRY", "fp64")
+_pending_flags = {}
+
+
+def set_validation(mode):
+    """'eager' (reference semantics), 'lazy' (check_nonfinite()) or 'off'."""
+    global _VALIDATION
+    if mode not in ("eager", "lazy", "off"):
+        raise ValueError(f"unknown validation mode {mode!r}")
+    _VALIDATION = mode
+
+
+def set_carry_precision(p):
+    """'fp64' (default; sub-chunk transition matrices from float64 chains) or
+    'fp32' (faster; ~1e-3 relative error on near-unit-circle poles)."""
+    global _CARRY
+    if p not in ("fp64", "fp32"):
+        raise ValueError(f"unknown carry precision {p!r}")
+    _CARRY = p
+
+
+def carry_precision():
+    return _CARRY
+
+
+def _carry_code(p=None):
+    return N.CARRY_F32 if (p or _CARRY) == "fp32" else N.CARRY_F64
+
+
+def check_nonfinite(device=None):
+    """Raise ValueError if a lazily validated forward saw non-finite input."""
+    devs = list(_pending_flags) if device is None else [torch.device(device)]
+    for d in devs:
+        flag = _pending_flags.get(d)
+        if flag is not None and int(flag.item()) != 0:
+            flag.zero_()
+            raise ValueError("e or A contains non-finite values")
+
+
+# ---------------------------------------------------------------------------
+# argument handling
+# ---------------------------------------------------------------------------
+
+class _Conv:
+    """numpy <-> CUDA tensor bridge: numpy in, numpy out."""
+
+    def __init__(self, *xs):
+        self.numpy = any(isinstance(x, np.ndarray) for x in xs if x is not None)
+        dev = None
+        for x in xs:
+            if isinstance(x, torch.Tensor):
+                dev = x.device
+                break
+        if dev is None:
+            dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() \
+                else torch.device("cuda")
+        if dev.type != "cuda":
+            raise RuntimeError(
+                "the B200 LP kernels run on CUDA tensors only (no CPU fallback); "
+                f"got a tensor on {dev}")
+        self.device = dev
+
+    def t(self, x, dtype=None):
+        if x is None:
+            return None
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(np.ascontiguousarray(x))
+        elif not isinstance(x, torch.Tensor):
+            x = torch.as_tensor(np.asarray(x))
+        if x.device != self.device:
+            x = x.to(self.device)
+        if dtype is not None and x.dtype != dtype:
+            x = x.to(dtype)
+        return x.contiguous()
+
+    def out(self, x):
+        return x.cpu().numpy() if self.numpy else x
+
+
+def _signal(x, name):
+    if x.dim() not in (1, 2) or x.shape[-1] < 1 or x.numel() == 0:
+        raise ValueError(f"{name} must be a 1-d signal of length >= 1")
+    if x.dtype not in (torch.float32, torch.float64):
+        x = x.to(torch.float64 if x.dtype == torch.float64 else torch.float32)
+    return x
+
+
+def _zi(zi, M, B, batched, dtype, conv):
+    if zi is None:
+        return None
+    zi = conv.t(zi, dtype)
+    want = (B, M) if batched else (M,)
+    if tuple(zi.shape) != want:
+        if batched and tuple(zi.shape) == (M,):
+            zi = zi.expand(B, M)
+        else:
+            raise ValueError(f"zi must have shape ({M},), got {tuple(zi.shape)}")
+    return zi.reshape(B, M).contiguous()
+
+
+def _flag(device):
+    if _VALIDATION == "off":
+        return None
+    if _VALIDATION == "lazy":
+        f = _pending_flags.get(device)
+        if f is None:
+            f = torch.zeros(1, dtype=torch.int32, device=device)
+            _pending_flags[device] = f
+        return f
+    return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def _raise_nonfinite(flag, e, A, a_name="A"):
+    if flag is None or _VALIDATION != "eager":
+        return
+    if int(flag.item()) != 0:
+        if not bool(torch.isfinite(e).all()):
+            raise ValueError("e contains non-finite values")
+        raise ValueError(f"{a_name} contains non-finite values")
+
+
+# ---------------------------------------------------------------------------
+# forward
+# ---------------------------------------------------------------------------
+
+def _forward(ti, e, A, zi, carry_prec=None, return_carry=False):
+    conv = _Conv(e, A, zi)
+    e = _signal(conv.t(e), "e")
+    A = conv.t(A)
+    batched = e.dim() == 2
+    B = e.shape[0] if batched else 1
+    T = e.shape[-1]
+    if ti:
+        if A.dim() not in (1, 2) or A.shape[-1] < 1:
+            raise ValueError("a must be a 1-d coefficient row of order >= 1")
+        if A.dim() == 2 and not batched:
+            raise ValueError("a must be a 1-d coefficient row of order >= 1")
+        M = A.shape[-1]
+        A = A.to(e.dtype).expand(B, M).contiguous() if A.dim() == 1 else A.to(e.dtype)
+        if batched and A.shape[0] != B:
+            raise ValueError(f"a has {A.shape[0]} rows but the batch has {B} signals")
+    else:
+        if A.dim() != e.dim() + 1:
+            raise ValueError("A must be a (T+1, M) coefficient track")
+        if A.shape[-2] != T or (batched and A.shape[0] != B):
+            raise ValueError(
+                f"coefficient track has {A.shape[-2]} rows but the signal has {T} samples")
+        M = A.shape[-1]
+        A = A.to(e.dtype).contiguous()
+    if M > N.load().tvlp_max_order():
+        raise ValueError(f"order M={M} exceeds the kernels' maximum {N.load().tvlp_max_order()}")
+    zi = _zi(zi, M, B, batched, e.dtype, conv)
+    e = e.contiguous()
+    dt = N.dtype_code(e.dtype)
+    lib = N.load()
+    s = torch.empty_like(e)
+    ncarry = lib.tvlp_carry_elems(B, T, M)
+    carry = torch.empty(ncarry, dtype=torch.float32, device=conv.device)
+    op = N.OP_FWD_TI if ti else N.OP_FWD_TV
+    ws, nws = N.workspace(lib.tvlp_workspace_bytes(op, dt, B, T, M, 0, 0, 0), conv.device)
+    flag = _flag(conv.device)
+    fn = lib.tvlp_lp_forward_ti if ti else lib.tvlp_lp_forward_tv
+    cp = _carry_code(carry_prec)
+    with torch.cuda.device(conv.device):
+        N.check(fn(dt, N.ptr(e), N.ptr(A), N.ptr(zi), N.ptr(s), B, T, M, N.ptr(carry), cp,
+                   N.ptr(ws), nws, N.ptr(flag), N.stream_ptr(conv.device)))
+    _raise_nonfinite(flag, e, A, "a" if ti else "A")
+    out = conv.out(s)
+    if return_carry:
+        return out, carry
+    return out
+
+
+def lp_forward_tv(e, A, zi=None, *, carry_precision=None):
+    """Sample-wise all-pole filter ``s(t) = e(t) - sum_i A[t, i-1] s(t-i)``
+    (lpc.py:101-117)."""
+    return _forward(False, e, A, zi, carry_precision)
+
+
+def lp_forward_ti(e, a, zi=None, *, carry_precision=None):
+    """Time-invariant all-pole filter (lpc.py:82-98).  Unstable ``a`` is not
+    rejected; overflow is a legitimate outcome."""
+    return _forward(True, e, a, zi, carry_precision)
+
+
+# ---------------------------------------------------------------------------
+# backward
+# ---------------------------------------------------------------------------
+
+def _backward(ti, grad_s, A, s, zi, carry=None, carry_prec=None):
+    conv = _Conv(grad_s, A, s, zi)
+    grad_s = conv.t(grad_s)
+    if grad_s.dtype not in (torch.float32, torch.float64):
+        grad_s = grad_s.to(torch.float32)
+    dtype = grad_s.dtype
+    A = conv.t(A, dtype)
+    s = conv.t(s, dtype)
+    batched = grad_s.dim() == 2
+    B = grad_s.shape[0] if batched else 1
+    T = grad_s.shape[-1]
+    if ti:
+        M = A.shape[-1]
+        if s.shape[-1] != T:
+            raise ValueError("grad_s and s must share the same length")
+        A = A.expand(B, M).contiguous() if A.dim() == 1 else A
+    else:
+        if not (T == A.shape[-2] == s.shape[-1]):
+            raise ValueError("grad_s, A and s must share the same length")
+        M = A.shape[-1]
+    zi = _zi(zi, M, B, batched, dtype, conv)
+    dt = N.dtype_code(dtype)
+    lib = N.load()
+    ge = torch.empty_like(grad_s)
+    gA = torch.empty((B, M) if ti else A.shape, dtype=dtype, device=conv.device)
+    if ti and not batched:
+        gA = gA.reshape(M)
+    op = N.OP_BWD_TI if ti else N.OP_BWD_TV
+    ws, nws = N.workspace(lib.tvlp_workspace_bytes(op, dt, B, T, M, 0, 0, 0), conv.device)
+    if carry is not None and carry.numel() != lib.tvlp_carry_elems(B, T, M):
+        carry = None
+    fn = lib.tvlp_lp_backward_ti if ti else lib.tvlp_lp_backward_tv
+    with torch.cuda.device(conv.device):
+        N.check(fn(dt, N.ptr(grad_s), N.ptr(A), N.ptr(s), N.ptr(zi), N.ptr(ge), N.ptr(gA), B, T,
+                   M, N.ptr(carry), _carry_code(carry_prec), N.ptr(ws), nws,
+                   N.stream_ptr(conv.device)))
+    return conv.out(ge), conv.out(gA)
+
+
+def lp_backward_tv(grad_s, A, s, zi=None, *, carry=None, carry_precision=None):
+    """Adjoints of :func:`lp_forward_tv` given the saved output ``s``
+    (lpc.py:152-173): returns ``(grad_e, grad_A)`` with
+    ``grad_A[t, i-1] = -grad_e(t) s(t-i)``.  No gradient for ``zi``.
+    ``carry`` is the optional tape of the forward (skips recomputing it)."""
+    return _backward(False, grad_s, A, s, zi, carry, carry_precision)
+
+
+def lp_backward_ti(grad_s, a, s, zi=None, *, carry=None, carry_precision=None):
+    """Adjoints of :func:`lp_forward_ti` (lpc.py:176-195):
+    ``grad_a[i-1] = -sum_t grad_e(t) s(t-i)``."""
+    return _backward(True, grad_s, a, s, zi, carry, carry_precision)
+
+
+# ---------------------------------------------------------------------------
+# helpers of the reference API
+# ---------------------------------------------------------------------------
+
+def shift_coeffs(A):
+    """``A_hat[t, i-1] = A[t+i, i-1]``, zero past the end (lpc.py:120-135)."""
+    conv = _Conv(A)
+    A = conv.t(A)
+    if A.dim() not in (2, 3):
+        raise ValueError("A must be a (T+1, M) coefficient track")
+    if A.dtype not in (torch.float32, torch.float64):
+        A = A.to(torch.float64)
+    B = A.shape[0] if A.dim() == 3 else 1
+    T, M = A.shape[-2], A.shape[-1]
+    out = torch.empty_like(A)
+    with torch.cuda.device(conv.device):
+        N.check(N.load().tvlp_shift_coeffs(N.dtype_code(A.dtype), N.ptr(A), N.ptr(out), B, T, M,
+                                           N.stream_ptr(conv.device)))
+    return conv.out(out)
+
+
+def lagged_signal_matrix(s, M, zi=None):
+    """``L[t, i-1] = s(t-i)`` with ``s(-i)`` from ``zi`` (lpc.py:138-149)."""
+    conv = _Conv(s, zi)
+    s = conv.t(s)
+    if s.dtype not in (torch.float32, torch.float64):
+        s = s.to(torch.float64)
+    batched = s.dim() == 2
+    B = s.shape[0] if batched else 1
+    T = s.shape[-1]
+    zi = None if zi is None else conv.t(zi, s.dtype).expand(B, M).contiguous()
+    out = torch.empty(s.shape + (M,), dtype=s.dtype, device=conv.device)
+    with torch.cuda.device(conv.device):
+        N.check(N.load().tvlp_lagged_signal_matrix(N.dtype_code(s.dtype), N.ptr(s), N.ptr(zi),
+                                                   N.ptr(out), B, T, M,
+                                                   N.stream_ptr(conv.device)))
+    return conv.out(out)

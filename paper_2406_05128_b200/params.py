@@ -1,0 +1,176 @@
+"""Frame-wise time-invariant LP with overlap-add -- the reference
+``tvlp.params`` frame-wise API (pkg/src/tvlp/params.py:102-273) on B200.
+
+``FramePlan`` mirrors params.py:157-217 exactly (it is host-side metadata);
+``framewise_lp`` runs the per-frame recursions, the overlap-add and (through
+:class:`paper_2406_05128_b200.autograd.LPFramewise`) the VJP in the sm_100a
+kernels of libtvlp_b200.so.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .lpc import _Conv
+
+__all__ = [
+    "expected_frame_count",
+    "raised_cosine_window",
+    "FramePlan",
+    "framewise_lp",
+    "framewise_forward",
+    "framewise_backward",
+]
+
+
+def expected_frame_count(T, hop):
+    """Frame count whose centers ``f*hop`` tile ``0..T`` (params.py:102-104)."""
+    return T // hop + 1
+
+
+def raised_cosine_window(n):
+    """Periodic raised-cosine window of length ``n`` (params.py:152-154)."""
+    return 0.5 - 0.5 * np.cos(2.0 * np.pi * np.arange(n) / n)
+
+
+@dataclass
+class FramePlan:
+    """Windowed framing grid for overlap-add processing (params.py:157-217)."""
+
+    frame_size: int
+    hop: int
+    window: np.ndarray = field(repr=False)
+
+    @classmethod
+    def raised_cosine(cls, hop, overlap=0.75):
+        denom = 1.0 - overlap
+        size = hop / denom
+        if abs(size - round(size)) > 1e-9:
+            raise ValueError(f"hop {hop} and overlap {overlap} give a non-integer frame size")
+        size = int(round(size))
+        return cls(frame_size=size, hop=hop, window=raised_cosine_window(size))
+
+    @classmethod
+    def rectangular(cls, frame_size, hop=None):
+        hop = frame_size if hop is None else hop
+        return cls(frame_size=frame_size, hop=hop, window=np.ones(frame_size))
+
+    @property
+    def overlap(self):
+        return 1.0 - self.hop / self.frame_size
+
+    def ola_deviation(self):
+        reps = self.frame_size // self.hop + 2
+        acc = np.zeros(self.frame_size + reps * self.hop)
+        for f in range(reps):
+            acc[f * self.hop: f * self.hop + self.frame_size] += self.window
+        interior = acc[self.frame_size: self.frame_size + self.hop]
+        return float(np.max(np.abs(interior - np.median(interior))))
+
+    def validate_cola(self, tol=1e-6):
+        dev = self.ola_deviation()
+        if dev > tol:
+            raise ValueError(f"window does not satisfy constant overlap-add; deviation {dev:.3e}")
+
+    def cola_constant(self):
+        return float(self.window.sum() / self.hop)
+
+    def n_lead_in(self):
+        return (self.frame_size - 1) // self.hop
+
+    def iter_frames(self, length, n_frames):
+        for f in range(-self.n_lead_in(), n_frames):
+            start = f * self.hop
+            sig_lo, sig_hi = max(start, 0), min(start + self.frame_size, length)
+            if sig_hi <= sig_lo:
+                continue
+            yield max(f, 0), sig_lo, sig_hi, sig_lo - start, sig_hi - start
+
+    # device copy of the window in the I/O dtype (params.py:232, 266: astype(e.dtype))
+    def _window_tensor(self, dtype, device):
+        cache = self.__dict__.setdefault("_wcache", {})
+        key = (dtype, str(device), id(self.window))
+        w = cache.get(key)
+        if w is None:
+            np_dt = np.float32 if dtype == torch.float32 else np.float64
+            w = torch.from_numpy(np.ascontiguousarray(self.window.astype(np_dt))).to(device)
+            cache[key] = w
+        return w
+
+
+def _check(e, frames, plan):
+    T1 = e.shape[-1]
+    F = frames.shape[-2]
+    if F != expected_frame_count(T1 - 1, plan.hop):
+        raise ValueError(
+            f"got {F} coefficient frames but length {T1} at hop {plan.hop} "
+            f"requires {expected_frame_count(T1 - 1, plan.hop)}")
+    plan.validate_cola()
+
+
+def framewise_forward(e, frames, plan):
+    """Returns ``(out, seg)``; ``seg`` [B, frame_size, n_frames] holds the
+    per-frame outputs the VJP needs (the reference's ``seg_outputs``)."""
+    conv = _Conv(e, frames)
+    e = conv.t(e)
+    if e.dtype not in (torch.float32, torch.float64):
+        e = e.to(torch.float32)
+    frames = conv.t(frames, e.dtype)
+    _check(e, frames, plan)
+    batched = e.dim() == 2
+    B = e.shape[0] if batched else 1
+    T = e.shape[-1]
+    F, M = frames.shape[-2], frames.shape[-1]
+    lib = N.load()
+    nfr = lib.tvlp_framewise_nframes(T, F, plan.frame_size, plan.hop)
+    out = torch.empty_like(e)
+    seg = torch.empty((B, plan.frame_size, nfr), dtype=e.dtype, device=conv.device)
+    w = plan._window_tensor(e.dtype, conv.device)
+    dt = N.dtype_code(e.dtype)
+    ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FW_FWD, dt, B, T, M, F, plan.frame_size,
+                                                   plan.hop), conv.device)
+    with torch.cuda.device(conv.device):
+        N.check(lib.tvlp_framewise_forward(dt, N.ptr(e), N.ptr(frames), N.ptr(w),
+                                           plan.cola_constant(), N.ptr(out), N.ptr(seg), B, T, F,
+                                           M, plan.frame_size, plan.hop, N.ptr(ws), nws,
+                                           N.stream_ptr(conv.device)))
+    return conv.out(out), seg
+
+
+def framewise_backward(grad_out, frames, seg, plan):
+    """VJP of :func:`framewise_forward` (params.py:259-273):
+    returns ``(grad_e, grad_frames)``."""
+    conv = _Conv(grad_out, frames, seg)
+    g = conv.t(grad_out)
+    if g.dtype not in (torch.float32, torch.float64):
+        g = g.to(torch.float32)
+    frames = conv.t(frames, g.dtype)
+    seg = conv.t(seg, g.dtype)
+    batched = g.dim() == 2
+    B = g.shape[0] if batched else 1
+    T = g.shape[-1]
+    F, M = frames.shape[-2], frames.shape[-1]
+    lib = N.load()
+    ge = torch.empty_like(g)
+    gf = torch.empty(frames.shape, dtype=g.dtype, device=conv.device)
+    w = plan._window_tensor(g.dtype, conv.device)
+    dt = N.dtype_code(g.dtype)
+    ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FW_BWD, dt, B, T, M, F, plan.frame_size,
+                                                   plan.hop), conv.device)
+    with torch.cuda.device(conv.device):
+        N.check(lib.tvlp_framewise_backward(dt, N.ptr(g), N.ptr(frames), N.ptr(w),
+                                            plan.cola_constant(), N.ptr(seg), N.ptr(ge),
+                                            N.ptr(gf), B, T, F, M, plan.frame_size, plan.hop,
+                                            N.ptr(ws), nws, N.stream_ptr(conv.device)))
+    return conv.out(ge), conv.out(gf)
+
+
+def framewise_lp(e, frames, plan):
+    """Frame-wise time-invariant LP with overlap-add (params.py:242-256):
+    each windowed frame is filtered from a zero state with its own row, the
+    outputs are overlap-added and divided by the COLA constant."""
+    out, _ = framewise_forward(e, frames, plan)
+    return out

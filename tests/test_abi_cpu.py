@@ -1,0 +1,67 @@
+"""CPU-side checks of the C ABI and host logic (no GPU, no kernel launches)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2406_05128_b200 import _native as N
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "tvlp.h")).read()
+    return sorted(set(re.findall(r"\b(tvlp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.load()
+    declared = _declared()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(N.EXPORTS) == declared
+
+
+def test_abi_queries_without_gpu():
+    lib = N.load()
+    assert lib.tvlp_abi_version() == 1
+    assert lib.tvlp_max_order() >= 22
+    Ls = lib.tvlp_subchunk_len(48000, 22)
+    assert Ls % 88 == 0 and 256 <= Ls <= 1024
+    nsub = -(-48000 // Ls)
+    assert lib.tvlp_carry_elems(64, 48000, 22) == 64 * nsub * 23 * 22
+    for op in range(4):
+        assert lib.tvlp_workspace_bytes(op, 0, 64, 48000, 22, 0, 0, 0) > 0
+    assert lib.tvlp_framewise_nframes(48000, 200, 960, 240) == 203
+    assert lib.tvlp_workspace_bytes(5, 0, 32, 48000, 22, 200, 960, 240) > 0
+    # odd orders pad to a compiled order; too-large orders are rejected
+    assert lib.tvlp_carry_elems(1, 100, 5) == 1 * 7 * 6
+    assert lib.tvlp_carry_elems(1, 100, 99) == -1
+    assert lib.tvlp_workspace_bytes(0, 0, 1, 100, 99, 0, 0, 0) == 0
+
+
+def test_status_strings():
+    lib = N.load()
+    assert lib.tvlp_status_string(0) == b"ok"
+    assert b"workspace" in lib.tvlp_status_string(3)
+    with pytest.raises(N.TVLPError, match="order"):
+        N.check(2)
+
+
+def test_frameplan_host_logic():
+    from paper_2406_05128_b200.params import FramePlan, expected_frame_count
+
+    plan = FramePlan.raised_cosine(240)
+    assert plan.frame_size == 960 and plan.n_lead_in() == 3
+    assert plan.ola_deviation() < 1e-12
+    assert plan.cola_constant() == pytest.approx(2.0)
+    frames = list(plan.iter_frames(48000, expected_frame_count(47999, 240)))
+    assert len(frames) == 203
+    assert frames[0] == (0, 0, 240, 720, 960)
+    bad = FramePlan(frame_size=256, hop=100, window=np.hanning(256))
+    with pytest.raises(ValueError, match="deviation"):
+        bad.validate_cola()
+    with pytest.raises(ValueError, match="non-integer"):
+        FramePlan.raised_cosine(7, overlap=0.7)

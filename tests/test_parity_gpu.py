@@ -1,0 +1,323 @@
+"""GPU parity of the B200 kernels against the pinned CPU oracle.
+
+Protocol: inputs are generated once in float32; the oracle
+(float64, the reference's arithmetic restated in C and pinned bit-exactly to
+the reference by tests/golden/) runs on the SAME float32 values upcast, and
+each output is compared per batch item with the reference's own metric
+``gradcheck_error`` (oracle.py:228-234) against TOL = 1e-4 (the north star's
+"max relative error 1e-4 against the reference evaluated in float64").
+float64 kernels are checked against the float64 golden vectors at 1e-9.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2406_05128_b200 import data
+
+pytestmark = pytest.mark.gpu
+
+TOL32 = 1e-4   # float32 kernels vs float64 oracle on identical inputs
+TOL64 = 1e-9   # float64 kernels vs float64 reference golden vectors
+
+lpc = pytest.importorskip("paper_2406_05128_b200.lpc")
+
+
+def _cuda(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _err(a, b):
+    return oracle.gradcheck_error(a, b)
+
+
+def _golden_cases(d, well_conditioned=True):
+    n = int(d["n_cases"])
+    for i in range(n):
+        k = f"c{i}_"
+        c = {name[len(k):]: d[name] for name in d.files if name.startswith(k)}
+        finite = all(np.all(np.isfinite(c[x])) for x in ("s", "ge", "gA", "s_ti", "ge_ti", "ga_ti"))
+        mx = max(np.abs(c["s"]).max(), np.abs(c["s_ti"]).max())
+        if well_conditioned and (not finite or mx > 1e4):
+            continue
+        yield i, c
+
+
+# ---------------------------------------------------------------------------
+# golden vectors from the reference itself
+# ---------------------------------------------------------------------------
+
+def test_golden_tv_ti(golden_lpc):
+    checked = 0
+    for i, c in _golden_cases(golden_lpc):
+        dt = c["e"].dtype
+        tol = TOL64 if dt == np.float64 else TOL32
+        zi = c.get("zi")
+        e, A, g = _cuda(c["e"]), _cuda(c["A"]), _cuda(c["g"])
+        z = None if zi is None else _cuda(zi)
+        s = lpc.lp_forward_tv(e, A, z)
+        ref_s = c["s"] if dt == np.float64 else oracle.lp_forward_tv(
+            c["e"].astype(np.float64), c["A"].astype(np.float64),
+            None if zi is None else zi.astype(np.float64))
+        assert _err(_np(s), ref_s) < tol, (i, "s")
+        ge, gA = lpc.lp_backward_tv(g, A, s, z)
+        if dt == np.float64:
+            ref_ge, ref_gA = c["ge"], c["gA"]
+        else:
+            ref_ge, ref_gA = oracle.lp_backward_tv(
+                c["g"].astype(np.float64), c["A"].astype(np.float64), ref_s,
+                None if zi is None else zi.astype(np.float64))
+        assert _err(_np(ge), ref_ge) < tol, (i, "ge")
+        assert _err(_np(gA), ref_gA) < tol, (i, "gA")
+        a = A[0].contiguous()
+        s_ti = lpc.lp_forward_ti(e, a, z)
+        ref = c["s_ti"] if dt == np.float64 else oracle.lp_forward_ti(
+            c["e"].astype(np.float64), c["A"][0].astype(np.float64),
+            None if zi is None else zi.astype(np.float64))
+        assert _err(_np(s_ti), ref) < tol, (i, "s_ti")
+        ge_ti, ga_ti = lpc.lp_backward_ti(g, a, s_ti, z)
+        if dt == np.float64:
+            r_ge, r_ga = c["ge_ti"], c["ga_ti"]
+        else:
+            r_ge, r_ga = oracle.lp_backward_ti(c["g"].astype(np.float64),
+                                               c["A"][0].astype(np.float64), ref,
+                                               None if zi is None else zi.astype(np.float64))
+        assert _err(_np(ge_ti), r_ge) < tol, (i, "ge_ti")
+        assert _err(_np(ga_ti), r_ga) < tol, (i, "ga_ti")
+        np.testing.assert_array_equal(_np(lpc.shift_coeffs(A)), c["Ahat"])
+        np.testing.assert_array_equal(_np(lpc.lagged_signal_matrix(s, A.shape[1], z)),
+                                      oracle.lagged_signal_matrix(_np(s), A.shape[1], zi))
+        checked += 1
+    assert checked >= 40
+
+
+def test_golden_framewise(golden_framewise):
+    from paper_2406_05128_b200 import params
+
+    d = golden_framewise
+    for i in range(int(d["n_cases"])):
+        k = f"f{i}_"
+        T1, hop, M = (int(x) for x in d[k + "cfg"])
+        e, fr, g = d[k + "e"], d[k + "frames"], d[k + "g"]
+        dt = e.dtype
+        plan = params.FramePlan.raised_cosine(hop)
+        y, seg = params.framewise_forward(_cuda(e), _cuda(fr), plan)
+        ge, gf = params.framewise_backward(_cuda(g), _cuda(fr), seg, plan)
+        if dt == np.float64:
+            ry, rge, rgf = d[k + "y"], d[k + "ge"], d[k + "gf"]
+            tol = TOL64
+        else:
+            ry, rsegs = oracle.framewise_forward(e.astype(np.float64), fr.astype(np.float64), hop)
+            rge, rgf = oracle.framewise_backward(g.astype(np.float64), fr.astype(np.float64),
+                                                 rsegs, hop)
+            tol = TOL32
+        assert _err(_np(y), ry) < tol, (i, "y")
+        assert _err(_np(ge), rge) < tol, (i, "ge")
+        assert _err(_np(gf), rgf) < tol, (i, "gf")
+
+
+# ---------------------------------------------------------------------------
+# reference known-answer tests (pkg/tests/test_lpc.py) on the GPU path
+# ---------------------------------------------------------------------------
+
+def test_kat_one_pole():  # test_lpc.py:10-12
+    s = lpc.lp_forward_ti(np.array([1.0, 0, 0, 0]), np.array([-0.5]))
+    np.testing.assert_allclose(s, [1.0, 0.5, 0.25, 0.125])
+
+
+def test_kat_hand_recursion_and_worked_backward():  # test_lpc.py:43-46, 95-100
+    A = np.array([[0.0], [-1.0], [-0.5]])
+    s = lpc.lp_forward_tv(np.ones(3), A)
+    np.testing.assert_allclose(s, [1.0, 2.0, 2.0])
+    ge, gA = lpc.lp_backward_tv(np.array([0.0, 0.0, 1.0]), A, s)
+    np.testing.assert_allclose(ge, [0.5, 0.5, 1.0])
+    np.testing.assert_allclose(gA[:, 0], [0.0, -0.5, -2.0])
+
+
+def test_kat_ti_backward_quadratic():  # test_lpc.py:153-160
+    a = np.array([-0.5])
+    s = lpc.lp_forward_ti(np.array([1.0, 0, 0, 0]), a)
+    ge, ga = lpc.lp_backward_ti(np.array([0.0, 0, 1.0, 0]), a, s)
+    assert ga[0] == pytest.approx(-1.0)
+    np.testing.assert_allclose(ge, [0.25, 0.5, 1.0, 0.0])
+
+
+def test_exact_structure(rng):  # test_lpc.py:48-57, 102-115; 16-20
+    e = rng.standard_normal(640)
+    np.testing.assert_array_equal(lpc.lp_forward_tv(e, np.zeros((640, 22))), e)
+    np.testing.assert_array_equal(lpc.lp_forward_ti(np.zeros(8), np.array([0.4, -0.2])),
+                                  np.zeros(8))
+    gs = rng.standard_normal(12)
+    ge, _ = lpc.lp_backward_tv(gs, np.zeros((12, 2)), rng.standard_normal(12))
+    np.testing.assert_array_equal(ge, gs)
+    ge, gA = lpc.lp_backward_tv(np.zeros(9), rng.uniform(-0.4, 0.4, (9, 2)),
+                                rng.standard_normal(9))
+    assert not ge.any() and not gA.any()
+    # constant rows: TV equals TI (same kernels, same arithmetic) bit-exactly
+    for dt in (np.float64, np.float32):
+        e = rng.standard_normal(2000).astype(dt)
+        a = data.stress_row(3, 22).astype(dt)
+        np.testing.assert_array_equal(lpc.lp_forward_tv(e, np.repeat(a[None], 2000, 0)),
+                                      lpc.lp_forward_ti(e, a))
+
+
+def test_initial_state_continuation(rng):  # test_lpc.py:31-39 (the chunk-carry invariant)
+    e = rng.standard_normal(4000)
+    a = np.array([0.5, -0.3, 0.1])
+    full = lpc.lp_forward_ti(e, a)
+    s1 = lpc.lp_forward_ti(e[:2500], a)
+    s2 = lpc.lp_forward_ti(e[2500:], a, zi=s1[-1:-4:-1])
+    np.testing.assert_allclose(np.concatenate([s1, s2]), full, atol=1e-12)
+
+
+def test_unstable_not_rejected():  # test_lpc.py:22-25
+    s = lpc.lp_forward_ti(np.ones(32), np.array([-2.0]))
+    assert np.all(np.isfinite(s)) and abs(s[-1]) > 1e8
+
+
+def test_nonfinite_and_shape_errors():  # test_lpc.py:27-29, 59-61, 117-119
+    with pytest.raises(ValueError, match="non-finite"):
+        lpc.lp_forward_ti(np.array([1.0, np.nan]), np.array([0.5]))
+    A = np.zeros((5, 2))
+    A[3, 1] = np.inf
+    with pytest.raises(ValueError, match="A contains non-finite"):
+        lpc.lp_forward_tv(np.ones(5), A)
+    with pytest.raises(ValueError, match="rows"):
+        lpc.lp_forward_tv(np.ones(5), np.zeros((4, 1)))
+    with pytest.raises(ValueError, match="length"):
+        lpc.lp_backward_tv(np.ones(4), np.zeros((5, 1)), np.ones(5))
+
+
+def test_no_cpu_fallback():
+    with pytest.raises(RuntimeError, match="CUDA"):
+        lpc.lp_forward_tv(torch.ones(8), torch.zeros(8, 2))
+
+
+def test_dtype_preserved(rng):  # test_lpc.py:237-243
+    e = rng.standard_normal(32).astype(np.float32)
+    A = rng.uniform(-0.3, 0.3, (32, 4)).astype(np.float32)
+    s = lpc.lp_forward_tv(e, A)
+    assert s.dtype == np.float32
+    ge, gA = lpc.lp_backward_tv(s.copy(), A, s)
+    assert ge.dtype == np.float32 and gA.dtype == np.float32
+
+
+# ---------------------------------------------------------------------------
+# production shapes: D1 and the resonant stress set
+# ---------------------------------------------------------------------------
+
+def _tv_parity(e, A, g, tol=TOL32, zi=None, precision=None):
+    B = e.shape[0]
+    et, At, gt = _cuda(e), _cuda(A), _cuda(g)
+    zt = None if zi is None else _cuda(zi)
+    s = lpc.lp_forward_tv(et, At, zt, carry_precision=precision)
+    ge, gA = lpc.lp_backward_tv(gt, At, s, zt, carry_precision=precision)
+    s, ge, gA = _np(s), _np(ge), _np(gA)
+    worst = 0.0
+    for b in range(B):
+        z64 = None if zi is None else zi[b].astype(np.float64)
+        rs = oracle.lp_forward_tv(e[b].astype(np.float64), A[b].astype(np.float64), z64)
+        rge, rgA = oracle.lp_backward_tv(g[b].astype(np.float64), A[b].astype(np.float64), rs, z64)
+        errs = (_err(s[b], rs), _err(ge[b], rge), _err(gA[b], rgA))
+        worst = max(worst, *errs)
+        assert max(errs) < tol, (b, errs)
+    return worst
+
+
+def test_config1_d1_and_stress():
+    """Config 1: B=4, T=24000, M=22, D1 + stress, seeds 0-3."""
+    e, A, g = data.d1_batch(0, 4, 24000)
+    _tv_parity(e, A, g)
+    items = [data.stress_item(s, 24000) for s in range(4)]
+    e = np.stack([x[0] for x in items])
+    A = np.stack([x[1] for x in items])
+    g = np.stack([x[2] for x in items])
+    _tv_parity(e, A, g)
+
+
+def test_config3_shape_d1():
+    """Config 3 geometry (T=48000, many sub-chunks per item), 8 of its 64 items."""
+    e, A, g = data.d1_batch(0, 8, 48000)
+    assert _tv_parity(e, A, g) < 1e-5
+
+
+def test_long_sequence_d1():
+    """Long single sequence (config 4 pattern): 1.44 M samples, ~2700 sub-chunks."""
+    e, A, g = data.d1_batch(7, 1, 1_440_000)
+    assert _tv_parity(e, A, g) < 1e-5
+
+
+def test_zi_and_odd_lengths(rng):
+    for T1, M in [(37, 3), (1001, 22), (4099, 5), (6, 22), (1, 4)]:
+        e, A, g = data.d1_batch(3, 2, T1, M, hop=7)
+        zi = rng.standard_normal((2, M)).astype(np.float32)
+        _tv_parity(e, A, g, zi=zi)
+
+
+def test_fp32_carries_option_on_d1():
+    e, A, g = data.d1_batch(11, 2, 24000)
+    _tv_parity(e, A, g, precision="fp32")
+
+
+# ---------------------------------------------------------------------------
+# autograd
+# ---------------------------------------------------------------------------
+
+def test_autograd_matches_functional():
+    from paper_2406_05128_b200 import autograd as ag
+
+    e, A, g = data.d1_batch(2, 3, 5000)
+    et = _cuda(e).requires_grad_()
+    At = _cuda(A).requires_grad_()
+    s = ag.lp_tv(et, At)
+    s.backward(_cuda(g))
+    ge, gA = lpc.lp_backward_tv(_cuda(g), _cuda(A), s.detach())
+    torch.testing.assert_close(et.grad, ge, rtol=0, atol=0)
+    torch.testing.assert_close(At.grad, gA, rtol=0, atol=0)
+
+
+def test_torch_gradcheck_fp64():  # C1-style finite-difference check (test_lpc.py:209-235)
+    from paper_2406_05128_b200 import autograd as ag
+
+    rng = np.random.default_rng(101)
+    for T1, M in [(17, 3), (40, 6), (64, 2)]:
+        A = oracle.lp_forward_tv  # noqa: F841  (keeps the oracle import explicit)
+        frames = data.reflection_to_lpc(rng.uniform(-0.9, 0.9, (4, M)))
+        A = data.upsample_linear(frames, max(1, (T1 - 1) // 3), T1)
+        e = torch.tensor(rng.standard_normal((2, T1)), device="cuda", requires_grad=True)
+        At = torch.tensor(np.stack([A, A[::-1].copy()]), device="cuda", requires_grad=True)
+        assert torch.autograd.gradcheck(lambda x, y: ag.lp_tv(x, y), (e, At), eps=1e-6,
+                                        atol=1e-7, rtol=1e-5)
+        a = torch.tensor(frames[:2], device="cuda", requires_grad=True)
+        assert torch.autograd.gradcheck(lambda x, y: ag.lp_ti(x, y), (e, a), eps=1e-6,
+                                        atol=1e-7, rtol=1e-5)
+
+
+def test_framewise_production_shape():
+    from paper_2406_05128_b200 import params
+
+    e, fr, g = data.d1_frames_batch(0, 3, 48000)
+    plan = params.FramePlan.raised_cosine(240)
+    y, seg = params.framewise_forward(_cuda(e), _cuda(fr), plan)
+    ge, gf = params.framewise_backward(_cuda(g), _cuda(fr), seg, plan)
+    for b in range(3):
+        ry, rseg = oracle.framewise_forward(e[b].astype(np.float64), fr[b].astype(np.float64), 240)
+        rge, rgf = oracle.framewise_backward(g[b].astype(np.float64), fr[b].astype(np.float64),
+                                             rseg, 240)
+        assert _err(_np(y[b]), ry) < TOL32
+        assert _err(_np(ge[b]), rge) < TOL32
+        assert _err(_np(gf[b]), rgf) < TOL32
+
+
+def test_framewise_single_rect_frame_equals_ti(rng):  # test_params.py:123-128
+    from paper_2406_05128_b200 import params
+
+    e = rng.standard_normal(200)
+    a = np.array([[-0.5, 0.2, 0.1]])
+    plan = params.FramePlan.rectangular(200)
+    out = params.framewise_lp(e, a, plan)
+    np.testing.assert_array_equal(out, lpc.lp_forward_ti(e, a[0]))
