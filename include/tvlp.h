@@ -22,7 +22,7 @@
  * The tape-op contract of lpc.py:202-223 (forward saves the output s and A,
  * backward returns (grad_e, grad_A), no gradient for zi) is kept: the forward
  * may additionally emit the "carry tape" (the per-sub-chunk transition
- * matrices) that the backward reuses instead of recomputing.
+ * matrices, in the I/O dtype) that the backward reuses instead of recomputing.
  *
  * Layouts (C-contiguous): e, s, grad_s, grad_e [B, T]; A, grad_A [B, T, M];
  * zi [B, M] (nullable = zeros); a, grad_a [B, M]; frames, grad_frames
@@ -68,7 +68,7 @@ const char* tvlp_status_string(int status);
 int tvlp_last_cuda_error(void);
 int32_t tvlp_max_order(void);
 
-/* Number of float32 elements of the carry tape for (B, T, M). */
+/* Number of elements (of the call dtype) of the carry tape for (B, T, M). */
 int64_t tvlp_carry_elems(int64_t B, int64_t T, int32_t M);
 /* Sub-chunk length used for (T, M) (diagnostics / tests). */
 int64_t tvlp_subchunk_len(int64_t T, int32_t M);
@@ -78,28 +78,28 @@ size_t tvlp_workspace_bytes(int32_t op, int32_t dtype, int64_t B, int64_t T, int
 /* Number of frames (lead-in included) of the frame-wise plan (params.py:203-217). */
 int64_t tvlp_framewise_nframes(int64_t T, int64_t F, int32_t frame_size, int32_t hop);
 
-/* s = LP_A(e).  carry (nullable): receives tvlp_carry_elems() floats for the
+/* s = LP_A(e).  carry (nullable): receives tvlp_carry_elems() values for the
  * backward.  nonfinite (nullable, device int32): OR-ed with 1 when e or A holds
  * a non-finite value (lpc.py:64-70, 111-112 reject those; the flag lets the
  * caller raise without a synchronising check inside the call). */
 int tvlp_lp_forward_tv(int32_t dtype, const void* e, const void* A, const void* zi, void* s,
-                       int64_t B, int64_t T, int32_t M, float* carry, int32_t carry_prec,
+                       int64_t B, int64_t T, int32_t M, void* carry, int32_t carry_prec,
                        void* workspace, size_t workspace_bytes, int32_t* nonfinite, void* stream);
 
 /* (grad_e, grad_A) of lp_forward_tv given the saved output s.  carry: the
  * tape written by the forward for the same (A, B, T, M), or NULL to recompute. */
 int tvlp_lp_backward_tv(int32_t dtype, const void* grad_s, const void* A, const void* s,
                         const void* zi, void* grad_e, void* grad_A, int64_t B, int64_t T,
-                        int32_t M, const float* carry, int32_t carry_prec, void* workspace,
+                        int32_t M, const void* carry, int32_t carry_prec, void* workspace,
                         size_t workspace_bytes, void* stream);
 
 /* Time-invariant special case: a [B, M] constant row per sequence. */
 int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,
-                       int64_t B, int64_t T, int32_t M, float* carry, int32_t carry_prec,
+                       int64_t B, int64_t T, int32_t M, void* carry, int32_t carry_prec,
                        void* workspace, size_t workspace_bytes, int32_t* nonfinite, void* stream);
 int tvlp_lp_backward_ti(int32_t dtype, const void* grad_s, const void* a, const void* s,
                         const void* zi, void* grad_e, void* grad_a, int64_t B, int64_t T,
-                        int32_t M, const float* carry, int32_t carry_prec, void* workspace,
+                        int32_t M, const void* carry, int32_t carry_prec, void* workspace,
                         size_t workspace_bytes, void* stream);
 
 int tvlp_shift_coeffs(int32_t dtype, const void* A, void* out, int64_t B, int64_t T, int32_t M,

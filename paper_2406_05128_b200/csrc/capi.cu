@@ -197,15 +197,16 @@ __global__ void k_lag(const IO* __restrict__ s, const IO* __restrict__ zi, IO* _
 // ---------------------------------------------------------------- TV / TI
 template <typename IO>
 int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s, const Plan& p,
-                 float* carry, int prec, void* ws, size_t ws_bytes, int32_t* nonfinite,
+                 void* carry_v, int prec, void* ws, size_t ws_bytes, int32_t* nonfinite,
                  cudaStream_t st, size_t* need) {
     const size_t sz = sizeof(IO);
+    IO* carry = static_cast<IO*>(carry_v);
     const bool packed = p.Tp != p.T || p.Mp != p.M || !aligned16(e) || !aligned16(A) ||
                         !aligned16(s) || (zi && !aligned16(zi));
     const int64_t nsc = p.B * p.nsub;
     Carver c(ws);
-    float* phiz = carry ? carry : static_cast<float*>(c.take(carry_elems(p) * 4));
-    float* xin = static_cast<float*>(c.take(nsc * p.Mp * 4));
+    IO* phiz = carry ? carry : static_cast<IO*>(c.take(carry_elems(p) * sz));
+    IO* xin = static_cast<IO*>(c.take(nsc * p.Mp * sz));
     const IO* e_p = static_cast<const IO*>(e);
     const IO* A_p = static_cast<const IO*>(A);
     const IO* zi_p = static_cast<const IO*>(zi);
@@ -236,7 +237,7 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
         s_p = static_cast<IO*>(ps);
     }
     TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, e_p, A_p, phiz, g, st)));
-    TVLP_RUN("carry_fwd", 1, st, (launch_carry_fwd(p.Mp, phiz, zi_p, sizeof(IO) == 8, xin, g, st)));
+    TVLP_RUN("carry_fwd", 1, st, (launch_carry_fwd<IO>(p.Mp, phiz, zi_p, xin, g, st)));
     TVLP_RUN("apply_fwd", 1, st, (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, g, st)));
     if (packed) TVLP_CK(unpack<IO>(ps, s, p.B, p.T, 1, p.Tp, 1, st));
     return TVLP_OK;
@@ -251,17 +252,18 @@ inline int grad_a_chunks(const Plan& p) {
 
 template <typename IO>
 int backward_impl(bool ti, const void* gs, const void* A, const void* s, const void* zi, void* ge,
-                  void* gA, const Plan& p, const float* carry, int prec, void* ws,
+                  void* gA, const Plan& p, const void* carry_v, int prec, void* ws,
                   size_t ws_bytes, cudaStream_t st, size_t* need) {
     const size_t sz = sizeof(IO);
+    const IO* carry = static_cast<const IO*>(carry_v);
     const bool packed = p.Tp != p.T || p.Mp != p.M || !aligned16(gs) || !aligned16(A) ||
                         !aligned16(s) || !aligned16(ge) || (!ti && !aligned16(gA)) ||
                         (zi && !aligned16(zi));
     const int64_t nsc = p.B * p.nsub;
     Carver c(ws);
-    float* phiz_own = carry ? nullptr : static_cast<float*>(c.take(carry_elems(p) * 4));
-    float* nu = static_cast<float*>(c.take(nsc * p.Mp * 4));
-    float* mu = static_cast<float*>(c.take(nsc * p.Mp * 4));
+    IO* phiz_own = carry ? nullptr : static_cast<IO*>(c.take(carry_elems(p) * sz));
+    IO* nu = static_cast<IO*>(c.take(nsc * p.Mp * sz));
+    IO* mu = static_cast<IO*>(c.take(nsc * p.Mp * sz));
     const int nchunk = grad_a_chunks(p);
     IO* part = ti ? static_cast<IO*>(c.take(p.B * (int64_t)nchunk * p.Mp * sz)) : nullptr;
     IO* ga_p = (ti && p.Mp != p.M) ? static_cast<IO*>(c.take(p.B * p.Mp * sz)) : nullptr;
@@ -302,7 +304,7 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
         ge_p = static_cast<IO*>(pge);
         gA_p = static_cast<IO*>(pgA);
     }
-    const float* phiz = carry;
+    const IO* phiz = carry;
     if (!phiz) {
         // transition matrices only (the zero-state row is unused here; s is a
         // valid stand-in for e of the same shape)
@@ -310,7 +312,7 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
         phiz = phiz_own;
     }
     TVLP_RUN("adjoint_zs", 1, st, (launch_adjoint<IO>(p.Mp, ti, 0, gs_p, A_p, nullptr, nu, nullptr, g, st)));
-    TVLP_RUN("carry_bwd", 1, st, (launch_carry_bwd(p.Mp, phiz, nu, mu, g, st)));
+    TVLP_RUN("carry_bwd", 1, st, (launch_carry_bwd<IO>(p.Mp, phiz, nu, mu, g, st)));
     TVLP_RUN("adjoint_apply", 1, st, (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, g, st)));
     if (ti) {
         IO* ga_out = ga_p ? ga_p : static_cast<IO*>(gA);
@@ -531,7 +533,7 @@ size_t tvlp_workspace_bytes(int32_t op, int32_t dtype, int64_t B, int64_t T, int
 }
 
 static int fwd_entry(bool ti, int32_t dtype, const void* e, const void* A, const void* zi,
-                     void* s, int64_t B, int64_t T, int32_t M, float* carry, int32_t prec,
+                     void* s, int64_t B, int64_t T, int32_t M, void* carry, int32_t prec,
                      void* ws, size_t ws_bytes, int32_t* nonfinite, void* stream) {
     int rc = check_common(dtype, M);
     if (rc != TVLP_OK) return rc;
@@ -548,7 +550,7 @@ static int fwd_entry(bool ti, int32_t dtype, const void* e, const void* A, const
 
 static int bwd_entry(bool ti, int32_t dtype, const void* gs, const void* A, const void* s,
                      const void* zi, void* ge, void* gA, int64_t B, int64_t T, int32_t M,
-                     const float* carry, int32_t prec, void* ws, size_t ws_bytes, void* stream) {
+                     const void* carry, int32_t prec, void* ws, size_t ws_bytes, void* stream) {
     int rc = check_common(dtype, M);
     if (rc != TVLP_OK) return rc;
     if (!gs || !A || !s || !ge || !gA) return TVLP_ERR_ARG;
@@ -563,7 +565,7 @@ static int bwd_entry(bool ti, int32_t dtype, const void* gs, const void* A, cons
 }
 
 int tvlp_lp_forward_tv(int32_t dtype, const void* e, const void* A, const void* zi, void* s,
-                       int64_t B, int64_t T, int32_t M, float* carry, int32_t carry_prec,
+                       int64_t B, int64_t T, int32_t M, void* carry, int32_t carry_prec,
                        void* workspace, size_t workspace_bytes, int32_t* nonfinite, void* stream) {
     return fwd_entry(false, dtype, e, A, zi, s, B, T, M, carry, carry_prec, workspace,
                      workspace_bytes, nonfinite, stream);
@@ -571,14 +573,14 @@ int tvlp_lp_forward_tv(int32_t dtype, const void* e, const void* A, const void* 
 
 int tvlp_lp_backward_tv(int32_t dtype, const void* grad_s, const void* A, const void* s,
                         const void* zi, void* grad_e, void* grad_A, int64_t B, int64_t T,
-                        int32_t M, const float* carry, int32_t carry_prec, void* workspace,
+                        int32_t M, const void* carry, int32_t carry_prec, void* workspace,
                         size_t workspace_bytes, void* stream) {
     return bwd_entry(false, dtype, grad_s, A, s, zi, grad_e, grad_A, B, T, M, carry, carry_prec,
                      workspace, workspace_bytes, stream);
 }
 
 int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,
-                       int64_t B, int64_t T, int32_t M, float* carry, int32_t carry_prec,
+                       int64_t B, int64_t T, int32_t M, void* carry, int32_t carry_prec,
                        void* workspace, size_t workspace_bytes, int32_t* nonfinite, void* stream) {
     return fwd_entry(true, dtype, e, a, zi, s, B, T, M, carry, carry_prec, workspace,
                      workspace_bytes, nonfinite, stream);
@@ -586,7 +588,7 @@ int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* 
 
 int tvlp_lp_backward_ti(int32_t dtype, const void* grad_s, const void* a, const void* s,
                         const void* zi, void* grad_e, void* grad_a, int64_t B, int64_t T,
-                        int32_t M, const float* carry, int32_t carry_prec, void* workspace,
+                        int32_t M, const void* carry, int32_t carry_prec, void* workspace,
                         size_t workspace_bytes, void* stream) {
     return bwd_entry(true, dtype, grad_s, a, s, zi, grad_e, grad_a, B, T, M, carry, carry_prec,
                      workspace, workspace_bytes, stream);

@@ -20,8 +20,8 @@
 //
 // Data layout in HBM (all row-major, batch-major):
 //   e, s, g_s, g_e : [B, T]          A, g_A : [B, T, M]     zi : [B, M]
-//   PhiZ : [B*nsub, M+1, M] fp32     (row c < M: column c of Phi_j; row M: z_j)
-//   Xin, Nu, Mu : [B*nsub, M] fp32
+//   PhiZ : [B*nsub, M+1, M]          (row c < M: column c of Phi_j; row M: z_j)
+//   Xin, Nu, Mu : [B*nsub, M]        (all in the I/O dtype)
 // Preconditions (enforced by the C ABI, which pads otherwise): T % 4 == 0,
 // Ls % lcm(M,4,8) == 0, all pointers 16-byte aligned.
 #pragma once
@@ -69,7 +69,7 @@ struct BasisSmem {
 
 template <typename IO, typename ACC, int M, bool TI, int NW>
 __global__ void __launch_bounds__(NW * 32)
-k_basis(const IO* __restrict__ e, const IO* __restrict__ A, float* __restrict__ PhiZ,
+k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ PhiZ,
         ScanArgs g) {
     using S = BasisSmem<IO, ACC, M, TI, NW>;
     constexpr int WR = S::WR;
@@ -190,34 +190,30 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, float* __restrict__ 
         ACC tmp[M];
 #pragma unroll
         for (int p = 0; p < M; ++p) tmp[p] = R[p];
-        float* out = PhiZ + (gid * (M + 1) + lane) * M;
+        IO* out = PhiZ + (gid * (M + 1) + lane) * M;
         const int last = (len - 1) % M;
-        for (int i = 0; i < M; ++i) out[i] = (float)tmp[(last - i + M) % M];
+        for (int i = 0; i < M; ++i) out[i] = (IO)tmp[(last - i + M) % M];
     }
 }
 
 // ============================================================================
 // Carry kernels: one warp per sequence, lane r holds component r.
 // ============================================================================
-template <int M, typename ACC>
+template <int M, typename ACC, typename CT>
 __global__ void __launch_bounds__(128)
-k_carry_fwd(const float* __restrict__ PhiZ, const void* __restrict__ zi, int zi_is_double,
-            float* __restrict__ Xin, ScanArgs g) {
+k_carry_fwd(const CT* __restrict__ PhiZ, const CT* __restrict__ zi, CT* __restrict__ Xin,
+            ScanArgs g) {
     __shared__ ACC xs[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * 4 + warp;
     if (b >= g.B) return;
     ACC x = (ACC)0;
-    if (zi != nullptr && lane < M) {
-        const int64_t off = b * M + lane;
-        x = zi_is_double ? (ACC) reinterpret_cast<const double*>(zi)[off]
-                         : (ACC) reinterpret_cast<const float*>(zi)[off];
-    }
+    if (zi != nullptr && lane < M) x = (ACC)zi[b * M + lane];
     const int64_t g0 = b * g.nsub;
     for (int j = 0; j < g.nsub; ++j) {
-        if (lane < M) Xin[(g0 + j) * M + lane] = (float)x;
+        if (lane < M) Xin[(g0 + j) * M + lane] = (CT)x;
         if (j == g.nsub - 1) break;
-        const float* W = PhiZ + (g0 + j) * (M + 1) * M;
+        const CT* W = PhiZ + (g0 + j) * (M + 1) * M;
         xs[warp][lane] = x;
         __syncwarp();
         if (lane < M) {
@@ -239,10 +235,10 @@ k_carry_fwd(const float* __restrict__ PhiZ, const void* __restrict__ zi, int zi_
 }
 
 // mu(j-1) = Phi_j^T mu(j) + nu_j ;  Mu[j] = carry into sub-chunk j from the right.
-template <int M, typename ACC>
+template <int M, typename ACC, typename CT>
 __global__ void __launch_bounds__(128)
-k_carry_bwd(const float* __restrict__ PhiZ, const float* __restrict__ Nu,
-            float* __restrict__ Mu, ScanArgs g) {
+k_carry_bwd(const CT* __restrict__ PhiZ, const CT* __restrict__ Nu, CT* __restrict__ Mu,
+            ScanArgs g) {
     __shared__ ACC ms[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * 4 + warp;
@@ -250,9 +246,9 @@ k_carry_bwd(const float* __restrict__ PhiZ, const float* __restrict__ Nu,
     ACC mu = (ACC)0;
     const int64_t g0 = b * g.nsub;
     for (int j = g.nsub - 1; j >= 0; --j) {
-        if (lane < M) Mu[(g0 + j) * M + lane] = (float)mu;
+        if (lane < M) Mu[(g0 + j) * M + lane] = (CT)mu;
         if (j == 0) break;
-        const float* W = PhiZ + (g0 + j) * (M + 1) * M;  // W[c][r] = Phi[r][c]
+        const CT* W = PhiZ + (g0 + j) * (M + 1) * M;  // W[c][r] = Phi[r][c]
         ms[warp][lane] = mu;
         __syncwarp();
         if (lane < M) {
@@ -349,7 +345,7 @@ struct LaneStream {
 // ---------------------------------------------------------------- apply fwd
 template <typename IO, int M, bool TI>
 __global__ void __launch_bounds__(32)
-k_apply_fwd(const IO* __restrict__ e, const IO* __restrict__ A, const float* __restrict__ Xin,
+k_apply_fwd(const IO* __restrict__ e, const IO* __restrict__ A, const IO* __restrict__ Xin,
             IO* __restrict__ s, int* __restrict__ flag, ScanArgs g) {
     using S = LaneSmem<IO, M, TI>;
     using LS = LaneStream<IO, M, TI, +1>;
@@ -450,8 +446,8 @@ k_apply_fwd(const IO* __restrict__ e, const IO* __restrict__ A, const float* __r
 //   lambda += u0 g_s(t);  g_e(t) = lambda_0;  lambda = C(t)^T lambda.
 template <typename IO, int M, bool TI, int MODE>
 __global__ void __launch_bounds__(32)
-k_adjoint(const IO* __restrict__ gs, const IO* __restrict__ A, const float* __restrict__ Mu,
-          float* __restrict__ Nu, IO* __restrict__ ge, ScanArgs g) {
+k_adjoint(const IO* __restrict__ gs, const IO* __restrict__ A, const IO* __restrict__ Mu,
+          IO* __restrict__ Nu, IO* __restrict__ ge, ScanArgs g) {
     using S = LaneSmem<IO, M, TI>;
     using LS = LaneStream<IO, M, TI, -1>;
     constexpr int W = S::W;
@@ -530,7 +526,7 @@ k_adjoint(const IO* __restrict__ gs, const IO* __restrict__ A, const float* __re
     if (MODE == 1) bulk_wait<0>();
     if (MODE == 0 && ls.active) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) Nu[gid * M + i] = (float)lam[i];
+        for (int i = 0; i < M; ++i) Nu[gid * M + i] = lam[i];
     }
 }
 

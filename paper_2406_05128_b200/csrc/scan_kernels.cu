@@ -15,7 +15,7 @@ cudaError_t ensure_smem(K kernel, int bytes) {
 constexpr int kBasisWarps = 4;
 
 template <typename IO, typename ACC, int M, bool TI>
-cudaError_t basis_impl(const IO* e, const IO* A, float* PhiZ, const ScanArgs& g,
+cudaError_t basis_impl(const IO* e, const IO* A, IO* PhiZ, const ScanArgs& g,
                        cudaStream_t st) {
     using S = BasisSmem<IO, ACC, M, TI, kBasisWarps>;
     auto k = k_basis<IO, ACC, M, TI, kBasisWarps>;
@@ -28,7 +28,7 @@ cudaError_t basis_impl(const IO* e, const IO* A, float* PhiZ, const ScanArgs& g,
 }
 
 template <typename IO, int M, bool TI>
-cudaError_t apply_impl(const IO* e, const IO* A, const float* Xin, IO* s, int* flag,
+cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag,
                        const ScanArgs& g, cudaStream_t st) {
     using S = LaneSmem<IO, M, TI>;
     auto k = k_apply_fwd<IO, M, TI>;
@@ -40,7 +40,7 @@ cudaError_t apply_impl(const IO* e, const IO* A, const float* Xin, IO* s, int* f
 }
 
 template <typename IO, int M, bool TI, int MODE>
-cudaError_t adjoint_impl(const IO* gs, const IO* A, const float* Mu, float* Nu, IO* ge,
+cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge,
                          const ScanArgs& g, cudaStream_t st) {
     using S = LaneSmem<IO, M, TI>;
     auto k = k_adjoint<IO, M, TI, MODE>;
@@ -79,7 +79,7 @@ int ls_unit(int Mp) {
 }
 
 template <typename IO>
-cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, float* PhiZ,
+cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO* PhiZ,
                          const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
         if constexpr (std::is_same<IO, float>::value) {
@@ -92,25 +92,26 @@ cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, fl
     })
 }
 
-cudaError_t launch_carry_fwd(int Mp, const float* PhiZ, const void* zi, bool zi_double,
-                             float* Xin, const ScanArgs& g, cudaStream_t st) {
+template <typename IO>
+cudaError_t launch_carry_fwd(int Mp, const IO* PhiZ, const IO* zi, IO* Xin, const ScanArgs& g,
+                             cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
-        k_carry_fwd<M_, double><<<(unsigned)((g.B + 3) / 4), 128, 0, st>>>(
-            PhiZ, zi, zi_double ? 1 : 0, Xin, g);
-        return cudaGetLastError();
-    })
-}
-
-cudaError_t launch_carry_bwd(int Mp, const float* PhiZ, const float* Nu, float* Mu,
-                             const ScanArgs& g, cudaStream_t st) {
-    TVLP_DISPATCH_M(Mp, {
-        k_carry_bwd<M_, double><<<(unsigned)((g.B + 3) / 4), 128, 0, st>>>(PhiZ, Nu, Mu, g);
+        k_carry_fwd<M_, double, IO><<<(unsigned)((g.B + 3) / 4), 128, 0, st>>>(PhiZ, zi, Xin, g);
         return cudaGetLastError();
     })
 }
 
 template <typename IO>
-cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const float* Xin, IO* s,
+cudaError_t launch_carry_bwd(int Mp, const IO* PhiZ, const IO* Nu, IO* Mu, const ScanArgs& g,
+                             cudaStream_t st) {
+    TVLP_DISPATCH_M(Mp, {
+        k_carry_bwd<M_, double, IO><<<(unsigned)((g.B + 3) / 4), 128, 0, st>>>(PhiZ, Nu, Mu, g);
+        return cudaGetLastError();
+    })
+}
+
+template <typename IO>
+cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO* Xin, IO* s,
                              int* flag, const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
         return ti ? apply_impl<IO, M_, true>(e, A, Xin, s, flag, g, st)
@@ -119,8 +120,8 @@ cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const fl
 }
 
 template <typename IO>
-cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const float* Mu,
-                           float* Nu, IO* ge, const ScanArgs& g, cudaStream_t st) {
+cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const IO* Mu,
+                           IO* Nu, IO* ge, const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
         if (mode == 0)
             return ti ? adjoint_impl<IO, M_, true, 0>(gs, A, Mu, Nu, ge, g, st)
@@ -152,12 +153,16 @@ cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* pa
 }
 
 #define TVLP_INST(IO)                                                                            \
-    template cudaError_t launch_basis<IO>(int, bool, int, const IO*, const IO*, float*,          \
+    template cudaError_t launch_basis<IO>(int, bool, int, const IO*, const IO*, IO*,             \
                                           const ScanArgs&, cudaStream_t);                        \
-    template cudaError_t launch_apply_fwd<IO>(int, bool, const IO*, const IO*, const float*,     \
-                                              IO*, int*, const ScanArgs&, cudaStream_t);         \
-    template cudaError_t launch_adjoint<IO>(int, bool, int, const IO*, const IO*, const float*,  \
-                                            float*, IO*, const ScanArgs&, cudaStream_t);         \
+    template cudaError_t launch_carry_fwd<IO>(int, const IO*, const IO*, IO*, const ScanArgs&,   \
+                                              cudaStream_t);                                     \
+    template cudaError_t launch_carry_bwd<IO>(int, const IO*, const IO*, IO*, const ScanArgs&,   \
+                                              cudaStream_t);                                     \
+    template cudaError_t launch_apply_fwd<IO>(int, bool, const IO*, const IO*, const IO*, IO*,   \
+                                              int*, const ScanArgs&, cudaStream_t);              \
+    template cudaError_t launch_adjoint<IO>(int, bool, int, const IO*, const IO*, const IO*,     \
+                                            IO*, IO*, const ScanArgs&, cudaStream_t);            \
     template cudaError_t launch_grad_A<IO>(int, const IO*, const IO*, const IO*, IO*, int64_t,   \
                                            int64_t, cudaStream_t);                               \
     template cudaError_t launch_grad_a<IO>(int, const IO*, const IO*, const IO*, IO*, IO*,       \

@@ -21,18 +21,20 @@ int ls_unit(int Mp);  // sub-chunk length granularity for order Mp
 enum Prec : int { kPrecF64Chains = 0, kPrecF32Chains = 1 };
 
 template <typename IO>
-cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, float* PhiZ,
+cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO* PhiZ,
                          const ScanArgs& g, cudaStream_t st);
-cudaError_t launch_carry_fwd(int Mp, const float* PhiZ, const void* zi, bool zi_double,
-                             float* Xin, const ScanArgs& g, cudaStream_t st);
-cudaError_t launch_carry_bwd(int Mp, const float* PhiZ, const float* Nu, float* Mu,
-                             const ScanArgs& g, cudaStream_t st);
 template <typename IO>
-cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const float* Xin, IO* s,
+cudaError_t launch_carry_fwd(int Mp, const IO* PhiZ, const IO* zi, IO* Xin, const ScanArgs& g,
+                             cudaStream_t st);
+template <typename IO>
+cudaError_t launch_carry_bwd(int Mp, const IO* PhiZ, const IO* Nu, IO* Mu, const ScanArgs& g,
+                             cudaStream_t st);
+template <typename IO>
+cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO* Xin, IO* s,
                              int* flag, const ScanArgs& g, cudaStream_t st);
 template <typename IO>
-cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const float* Mu,
-                           float* Nu, IO* ge, const ScanArgs& g, cudaStream_t st);
+cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const IO* Mu,
+                           IO* Nu, IO* ge, const ScanArgs& g, cudaStream_t st);
 template <typename IO>
 cudaError_t launch_grad_A(int Mp, const IO* ge, const IO* s, const IO* zi, IO* gA, int64_t B,
                           int64_t T, cudaStream_t st);

@@ -181,6 +181,8 @@ def _forward(ti, e, A, zi, carry_prec=None, return_carry=False):
         A = A.to(e.dtype).expand(B, M).contiguous() if A.dim() == 1 else A.to(e.dtype)
         if batched and A.shape[0] != B:
             raise ValueError(f"a has {A.shape[0]} rows but the batch has {B} signals")
+        if _VALIDATION == "eager" and not bool(torch.isfinite(A).all()):  # lpc.py:92-93
+            raise ValueError("a contains non-finite values")
     else:
         if A.dim() != e.dim() + 1:
             raise ValueError("A must be a (T+1, M) coefficient track")
@@ -197,7 +199,7 @@ def _forward(ti, e, A, zi, carry_prec=None, return_carry=False):
     lib = N.load()
     s = torch.empty_like(e)
     ncarry = lib.tvlp_carry_elems(B, T, M)
-    carry = torch.empty(ncarry, dtype=torch.float32, device=conv.device)
+    carry = torch.empty(ncarry, dtype=e.dtype, device=conv.device)
     op = N.OP_FWD_TI if ti else N.OP_FWD_TV
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(op, dt, B, T, M, 0, 0, 0), conv.device)
     flag = _flag(conv.device)
