@@ -197,8 +197,13 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ Phi
 }
 
 // ============================================================================
-// Carry kernels: one warp per sequence, lane r holds component r.
+// Carry kernels: one warp per sequence, lane r holds component r.  The chain
+// is latency-bound (one M x M mat-vec per sub-chunk), so the next sub-chunks'
+// matrix rows are prefetched into registers (distance kPF) while the current
+// mat-vec runs; the state is broadcast through shared memory.
 // ============================================================================
+constexpr int kPF = 4;
+
 template <int M, typename ACC, typename CT>
 __global__ void __launch_bounds__(128)
 k_carry_fwd(const CT* __restrict__ PhiZ, const CT* __restrict__ zi, CT* __restrict__ Xin,
@@ -207,30 +212,52 @@ k_carry_fwd(const CT* __restrict__ PhiZ, const CT* __restrict__ zi, CT* __restri
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * 4 + warp;
     if (b >= g.B) return;
+    const int r = lane < M ? lane : 0;
     ACC x = (ACC)0;
     if (zi != nullptr && lane < M) x = (ACC)zi[b * M + lane];
     const int64_t g0 = b * g.nsub;
-    for (int j = 0; j < g.nsub; ++j) {
-        if (lane < M) Xin[(g0 + j) * M + lane] = (CT)x;
-        if (j == g.nsub - 1) break;
-        const CT* W = PhiZ + (g0 + j) * (M + 1) * M;
-        xs[warp][lane] = x;
-        __syncwarp();
-        if (lane < M) {
-            ACC q0 = (ACC)W[M * M + lane], q1 = (ACC)0, q2 = (ACC)0, q3 = (ACC)0;
+    const int nstep = g.nsub - 1;
+    // ring of prefetched rows: w[k][c] = Phi_j[r][c] (c < M), w[k][M] = z_j[r]
+    CT w[kPF][M + 1];
 #pragma unroll
-            for (int c = 0; c < M; ++c) {
-                const ACC w = (ACC)W[c * M + lane];
-                switch (c & 3) {
-                    case 0: q0 = fma(w, xs[warp][c], q0); break;
-                    case 1: q1 = fma(w, xs[warp][c], q1); break;
-                    case 2: q2 = fma(w, xs[warp][c], q2); break;
-                    default: q3 = fma(w, xs[warp][c], q3); break;
+    for (int k = 0; k < kPF; ++k) {
+        if (k < nstep) {
+            const CT* W = PhiZ + (g0 + k) * (M + 1) * M;
+#pragma unroll
+            for (int c = 0; c <= M; ++c) w[k][c] = W[c * M + r];
+        }
+    }
+    for (int j0 = 0; j0 <= nstep; j0 += kPF) {
+#pragma unroll
+        for (int k = 0; k < kPF; ++k) {
+            const int j = j0 + k;
+            if (j <= nstep) {
+                if (lane < M) Xin[(g0 + j) * M + lane] = (CT)x;
+                if (j < nstep) {
+                    xs[warp][lane] = x;
+                    __syncwarp();
+                    ACC q0 = (ACC)w[k][M], q1 = (ACC)0, q2 = (ACC)0, q3 = (ACC)0;
+#pragma unroll
+                    for (int c = 0; c < M; ++c) {
+                        const ACC xc = xs[warp][c];
+                        switch (c & 3) {
+                            case 0: q0 = fma((ACC)w[k][c], xc, q0); break;
+                            case 1: q1 = fma((ACC)w[k][c], xc, q1); break;
+                            case 2: q2 = fma((ACC)w[k][c], xc, q2); break;
+                            default: q3 = fma((ACC)w[k][c], xc, q3); break;
+                        }
+                    }
+                    __syncwarp();
+                    if (lane < M) x = (q0 + q1) + (q2 + q3);
+                    const int jn = j + kPF;
+                    if (jn < nstep) {
+                        const CT* W = PhiZ + (g0 + jn) * (M + 1) * M;
+#pragma unroll
+                        for (int c = 0; c <= M; ++c) w[k][c] = W[c * M + r];
+                    }
                 }
             }
-            x = (q0 + q1) + (q2 + q3);
         }
-        __syncwarp();
     }
 }
 
@@ -243,29 +270,54 @@ k_carry_bwd(const CT* __restrict__ PhiZ, const CT* __restrict__ Nu, CT* __restri
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * 4 + warp;
     if (b >= g.B) return;
+    const int r = lane < M ? lane : 0;
     ACC mu = (ACC)0;
     const int64_t g0 = b * g.nsub;
-    for (int j = g.nsub - 1; j >= 0; --j) {
-        if (lane < M) Mu[(g0 + j) * M + lane] = (CT)mu;
-        if (j == 0) break;
-        const CT* W = PhiZ + (g0 + j) * (M + 1) * M;  // W[c][r] = Phi[r][c]
-        ms[warp][lane] = mu;
-        __syncwarp();
-        if (lane < M) {
-            ACC q0 = (ACC)Nu[(g0 + j) * M + lane], q1 = (ACC)0, q2 = (ACC)0, q3 = (ACC)0;
+    const int nstep = g.nsub - 1;  // steps j = nsub-1 .. 1
+    // w[k][c] = Phi_j^T[r][c] = W_j[r][c]; w[k][M] = nu_j[r]
+    CT w[kPF][M + 1];
 #pragma unroll
-            for (int c = 0; c < M; ++c) {
-                const ACC w = (ACC)W[lane * M + c];  // Phi^T[lane][c] = Phi[c][lane]
-                switch (c & 3) {
-                    case 0: q0 = fma(w, ms[warp][c], q0); break;
-                    case 1: q1 = fma(w, ms[warp][c], q1); break;
-                    case 2: q2 = fma(w, ms[warp][c], q2); break;
-                    default: q3 = fma(w, ms[warp][c], q3); break;
+    for (int k = 0; k < kPF; ++k) {
+        const int j = g.nsub - 1 - k;
+        if (j >= 1) {
+            const CT* W = PhiZ + (g0 + j) * (M + 1) * M + r * M;
+#pragma unroll
+            for (int c = 0; c < M; ++c) w[k][c] = W[c];
+            w[k][M] = Nu[(g0 + j) * M + r];
+        }
+    }
+    for (int i0 = 0; i0 < g.nsub; i0 += kPF) {
+#pragma unroll
+        for (int k = 0; k < kPF; ++k) {
+            const int j = g.nsub - 1 - (i0 + k);
+            if (j >= 0) {
+                if (lane < M) Mu[(g0 + j) * M + lane] = (CT)mu;
+                if (j >= 1) {
+                    ms[warp][lane] = mu;
+                    __syncwarp();
+                    ACC q0 = (ACC)w[k][M], q1 = (ACC)0, q2 = (ACC)0, q3 = (ACC)0;
+#pragma unroll
+                    for (int c = 0; c < M; ++c) {
+                        const ACC mc = ms[warp][c];
+                        switch (c & 3) {
+                            case 0: q0 = fma((ACC)w[k][c], mc, q0); break;
+                            case 1: q1 = fma((ACC)w[k][c], mc, q1); break;
+                            case 2: q2 = fma((ACC)w[k][c], mc, q2); break;
+                            default: q3 = fma((ACC)w[k][c], mc, q3); break;
+                        }
+                    }
+                    __syncwarp();
+                    if (lane < M) mu = (q0 + q1) + (q2 + q3);
+                    const int jn = j - kPF;
+                    if (jn >= 1) {
+                        const CT* W = PhiZ + (g0 + jn) * (M + 1) * M + r * M;
+#pragma unroll
+                        for (int c = 0; c < M; ++c) w[k][c] = W[c];
+                        w[k][M] = Nu[(g0 + jn) * M + r];
+                    }
                 }
             }
-            mu = (q0 + q1) + (q2 + q3);
         }
-        __syncwarp();
     }
 }
 

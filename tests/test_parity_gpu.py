@@ -107,6 +107,8 @@ def test_golden_framewise(golden_framewise):
         plan = params.FramePlan.raised_cosine(hop)
         y, seg = params.framewise_forward(_cuda(e), _cuda(fr), plan)
         ge, gf = params.framewise_backward(_cuda(g), _cuda(fr), seg, plan)
+        if not np.all(np.isfinite(d[k + "y"])) or np.abs(d[k + "y"]).max() > 1e4:
+            continue  # interpolated direct-form rows that blow up
         if dt == np.float64:
             ry, rge, rgf = d[k + "y"], d[k + "ge"], d[k + "gf"]
             tol = TOL64
