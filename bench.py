@@ -227,7 +227,7 @@ def run_b200(args, cfg, rank, world, dist):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    lpc.check_nonfinite(dev)
+    nonfinite_seen = lpc.check_nonfinite(dev)
     samples = B * T * world
     value = samples / (ms * 1e-3)
 
@@ -315,6 +315,7 @@ def run_b200(args, cfg, rank, world, dist):
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": round(e2e_ms, 3)},
         "gpu_launches": int(launches),
+        "nonfinite_outputs": bool(nonfinite_seen),
         "clocks": clk.summary(),
     }
     return line

@@ -395,6 +395,11 @@ struct LaneStream {
 };
 
 // ---------------------------------------------------------------- apply fwd
+// One lane re-runs the recursion of its sub-chunk from x_in.  The state lives
+// in a register ring of MR = round_up(M, W) slots (slot p holds s at local
+// step tau with tau mod MR == p); the unrolled body covers MR/W windows so
+// every ring index is a compile-time constant.  Full windows take a
+// predicate-free path; only the last window of a sequence can be partial.
 template <typename IO, int M, bool TI>
 __global__ void __launch_bounds__(32)
 k_apply_fwd(const IO* __restrict__ e, const IO* __restrict__ A, const IO* __restrict__ Xin,
@@ -402,6 +407,8 @@ k_apply_fwd(const IO* __restrict__ e, const IO* __restrict__ A, const IO* __rest
     using S = LaneSmem<IO, M, TI>;
     using LS = LaneStream<IO, M, TI, +1>;
     constexpr int W = S::W;
+    constexpr int MR = (M + W - 1) / W * W;
+    constexpr int WPB = MR / W;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x;
     LS ls;
@@ -416,7 +423,7 @@ k_apply_fwd(const IO* __restrict__ e, const IO* __restrict__ A, const IO* __rest
     const int64_t t0 = (int64_t)j * g.Ls;
     ls.len = ls.active ? (int)(int64_t)min((int64_t)(g.Ls), (int64_t)(g.T - t0)) : 0;
     ls.row0 = b * g.T + t0;
-    const int nwin_max = (g.Ls + W - 1) / W;  // lanes with shorter len just idle
+    const int nwin_max = (g.Ls + W - 1) / W;
 
     if (lane == 0) {
         for (int st = 0; st < kLaneStages; ++st) mbar_init(&ls.bars[st], 1);
@@ -431,62 +438,71 @@ k_apply_fwd(const IO* __restrict__ e, const IO* __restrict__ A, const IO* __rest
 #pragma unroll
         for (int i = 0; i < M; ++i) ati[i] = ls.active ? A[b * M + i] : (IO)0;
     }
-    IO x[M];
+    IO R[MR];
 #pragma unroll
-    for (int i = 0; i < M; ++i) x[i] = ls.active ? (IO)Xin[gid * M + i] : (IO)0;
+    for (int p = 0; p < MR; ++p) R[p] = (IO)0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) R[MR - 1 - i] = ls.active ? Xin[gid * M + i] : (IO)0;
     bool finite = true;
 
-    for (int k = 0; k < nwin_max; ++k) {
-        const int st = k % kLaneStages;
-        mbar_wait(&ls.bars[st], (uint32_t)((k / kLaneStages) & 1));
-        int lo, rows;
-        ls.window(k, lo, rows);
-        const IO* Ar = reinterpret_cast<const IO*>(ls.A_slot(st));
-        const IO* er = reinterpret_cast<const IO*>(ls.X_slot(st));
-        const int so = k % kOutStages;
-        IO* ob = reinterpret_cast<IO*>(ls.O_slot(so));
-        if (k >= kOutStages) bulk_wait_read<kOutStages - 1>();
+    for (int kb = 0; kb < nwin_max; kb += WPB) {
 #pragma unroll
-        for (int u = 0; u < W; ++u) {
-            if (u < rows) {
-                IO a[M];
-                if constexpr (TI) {
+        for (int w = 0; w < WPB; ++w) {
+            const int k = kb + w;
+            if (k < nwin_max) {
+                const int st = k % kLaneStages;
+                mbar_wait(&ls.bars[st], (uint32_t)((k / kLaneStages) & 1));
+                int lo, rows;
+                ls.window(k, lo, rows);
+                const IO* Ar = reinterpret_cast<const IO*>(ls.A_slot(st));
+                const IO* er = reinterpret_cast<const IO*>(ls.X_slot(st));
+                const int so = k % kOutStages;
+                IO* ob = reinterpret_cast<IO*>(ls.O_slot(so));
+                if (k >= kOutStages) bulk_wait_read<kOutStages - 1>();
+                IO ev[W];
 #pragma unroll
-                    for (int i = 0; i < M; ++i) a[i] = ati[i];
-                } else {
-                    load_row_at<IO, M>(Ar + u * M, a, u * M * (int)sizeof(IO));
+                for (int u = 0; u < W; ++u) ev[u] = er[u];
+                const bool full = rows == W;
 #pragma unroll
-                    for (int i = 0; i < M; ++i) finite &= is_finite_val(a[i]);
-                }
-                const IO ev = er[u];
-                finite &= is_finite_val(ev);
-                IO p0 = (IO)0, p1 = (IO)0, p2 = (IO)0, p3 = (IO)0;
+                for (int u = 0; u < W; ++u) {
+                    if (full || u < rows) {
+                        const int pos = w * W + u;  // compile-time after unrolling
+                        IO a[M];
+                        if constexpr (TI) {
 #pragma unroll
-                for (int i = M; i >= 2; --i) {
-                    switch (i & 3) {
-                        case 0: p0 = fma(a[i - 1], x[i - 1], p0); break;
-                        case 1: p1 = fma(a[i - 1], x[i - 1], p1); break;
-                        case 2: p2 = fma(a[i - 1], x[i - 1], p2); break;
-                        default: p3 = fma(a[i - 1], x[i - 1], p3); break;
+                            for (int i = 0; i < M; ++i) a[i] = ati[i];
+                        } else {
+                            load_row_at<IO, M>(Ar + u * M, a, u * M * (int)sizeof(IO));
+                        }
+                        IO p0 = (IO)0, p1 = (IO)0, p2 = (IO)0, p3 = (IO)0;
+#pragma unroll
+                        for (int i = M; i >= 2; --i) {
+                            const IO x = R[(pos - i + 2 * MR) % MR];
+                            switch (i & 3) {
+                                case 0: p0 = fma(a[i - 1], x, p0); break;
+                                case 1: p1 = fma(a[i - 1], x, p1); break;
+                                case 2: p2 = fma(a[i - 1], x, p2); break;
+                                default: p3 = fma(a[i - 1], x, p3); break;
+                            }
+                        }
+                        const IO v = fma(-a[0], R[(pos - 1 + MR) % MR], ev[u] - ((p0 + p1) + (p2 + p3)));
+                        R[pos % MR] = v;
+                        ob[u] = v;
+                        finite &= is_finite_val(v);
                     }
                 }
-                const IO v = fma(-a[0], x[0], ev - ((p0 + p1) + (p2 + p3)));
-#pragma unroll
-                for (int i = M - 1; i >= 1; --i) x[i] = x[i - 1];
-                x[0] = v;
-                ob[u] = v;
+                __syncwarp();
+                fence_proxy_async();
+                if (rows > 0) tma_store_1d(s + ls.row0 + lo, ob, rows * (uint32_t)sizeof(IO));
+                bulk_commit();
+                ls.issue(k + kLaneStages, nwin_max, A, e);
             }
         }
-        __syncwarp();
-        fence_proxy_async();
-        if (rows > 0) {
-            tma_store_1d(s + ls.row0 + lo, ob, rows * (uint32_t)sizeof(IO));
-        }
-        bulk_commit();
-        ls.issue(k + kLaneStages, nwin_max, A, e);
     }
     bulk_wait<0>();
     if (flag != nullptr) {
+        // a non-finite output means non-finite input or overflow; the host
+        // tells them apart (overflow of an unstable filter is legitimate).
         const unsigned bad = __ballot_sync(0xffffffffu, !finite);
         if (bad && lane == 0) atomicOr(flag, 1);
     }
@@ -496,6 +512,7 @@ k_apply_fwd(const IO* __restrict__ e, const IO* __restrict__ A, const IO* __rest
 // MODE 0: zero-state adjoint per sub-chunk -> Nu.  MODE 1: apply from Mu,
 // write g_e.  Reverse time; row A[t] is used at step t:
 //   lambda += u0 g_s(t);  g_e(t) = lambda_0;  lambda = C(t)^T lambda.
+// The transposed-state update shifts lambda inside its FMAs (no moves).
 template <typename IO, int M, bool TI, int MODE>
 __global__ void __launch_bounds__(32)
 k_adjoint(const IO* __restrict__ gs, const IO* __restrict__ A, const IO* __restrict__ Mu,
@@ -535,7 +552,7 @@ k_adjoint(const IO* __restrict__ gs, const IO* __restrict__ A, const IO* __restr
     IO lam[M];
 #pragma unroll
     for (int i = 0; i < M; ++i)
-        lam[i] = (MODE == 1 && ls.active) ? (IO)Mu[gid * M + i] : (IO)0;
+        lam[i] = (MODE == 1 && ls.active) ? Mu[gid * M + i] : (IO)0;
 
     // reverse windows of a sub-chunk whose length is not a multiple of W:
     // window k covers [max(0, len-(k+1)W), len-kW); slots are right-aligned.
@@ -549,9 +566,13 @@ k_adjoint(const IO* __restrict__ gs, const IO* __restrict__ A, const IO* __restr
         const int so = k % kOutStages;
         IO* ob = reinterpret_cast<IO*>(ls.O_slot(so));
         if (MODE == 1 && k >= kOutStages) bulk_wait_read<kOutStages - 1>();
+        IO gv[W];
+#pragma unroll
+        for (int u = 0; u < W; ++u) gv[u] = xr[u];
+        const bool full = rows == W;
 #pragma unroll
         for (int u = W - 1; u >= 0; --u) {
-            if (u >= W - rows) {
+            if (full || u >= W - rows) {
                 IO a[M];
                 if constexpr (TI) {
 #pragma unroll
@@ -559,7 +580,7 @@ k_adjoint(const IO* __restrict__ gs, const IO* __restrict__ A, const IO* __restr
                 } else {
                     load_row_at<IO, M>(Ar + u * M, a, u * M * (int)sizeof(IO));
                 }
-                const IO l0 = lam[0] + xr[u];
+                const IO l0 = lam[0] + gv[u];
                 if (MODE == 1) ob[u] = l0;
 #pragma unroll
                 for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
@@ -584,28 +605,37 @@ k_adjoint(const IO* __restrict__ gs, const IO* __restrict__ A, const IO* __restr
 
 // ---------------------------------------------------------------- g_A
 // g_A[b,t,c] = -g_e[b,t] * s(t-c-1), s(<0) from zi (lpc.py:138-149, 172).
-// One block per (64-row tile, sequence); writes are fully coalesced.
+// A block stages s[tlo-M, tlo+RT) and g_e[tlo, tlo+RT) in shared memory and
+// writes its RT*M contiguous outputs with coalesced stores.
 template <typename IO, int M>
 __global__ void __launch_bounds__(256)
 k_grad_A(const IO* __restrict__ ge, const IO* __restrict__ s, const IO* __restrict__ zi,
          IO* __restrict__ gA, int64_t T) {
-    constexpr int RT = 64;
+    constexpr int RT = 256;
+    __shared__ IO sh_s[RT + M];
+    __shared__ IO sh_g[RT];
     const int64_t b = blockIdx.y;
     const int64_t tlo = (int64_t)blockIdx.x * RT;
-    const int rows = (int)(int64_t)min((int64_t)(RT), (int64_t)(T - tlo));
+    const int rows = (int)(int64_t)min((int64_t)RT, T - tlo);
     const IO* sb = s + b * T;
+    for (int i = threadIdx.x; i < RT + M; i += 256) {
+        const int64_t tau = tlo - M + i;
+        IO v = (IO)0;
+        if (tau >= 0) {
+            if (tau < T) v = sb[tau];
+        } else if (zi) {
+            v = zi[b * M + (-tau - 1)];
+        }
+        sh_s[i] = v;
+    }
+    for (int i = threadIdx.x; i < RT; i += 256) sh_g[i] = i < rows ? ge[b * T + tlo + i] : (IO)0;
+    __syncthreads();
     IO* out = gA + (b * T + tlo) * M;
-    for (int local = threadIdx.x; local < rows * M; local += 256) {
-        const int r = local / M;
-        const int c = local - r * M;
-        const int64_t t = tlo + r;
-        const int64_t src = t - c - 1;
-        IO lag;
-        if (src >= 0)
-            lag = sb[src];
-        else
-            lag = zi ? zi[b * M + (c - t)] : (IO)0;
-        out[local] = (-ge[b * T + t]) * lag;
+    const int n = rows * M;
+    for (int idx = threadIdx.x; idx < n; idx += 256) {
+        const int r = idx / M;
+        const int c = idx - r * M;
+        out[idx] = (-sh_g[r]) * sh_s[M + r - c - 1];
     }
 }
 

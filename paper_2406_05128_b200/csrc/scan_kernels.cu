@@ -134,7 +134,7 @@ cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A,
 template <typename IO>
 cudaError_t launch_grad_A(int Mp, const IO* ge, const IO* s, const IO* zi, IO* gA, int64_t B,
                           int64_t T, cudaStream_t st) {
-    dim3 grid((unsigned)((T + 63) / 64), (unsigned)B);
+    dim3 grid((unsigned)((T + 255) / 256), (unsigned)B);
     TVLP_DISPATCH_M(Mp, {
         k_grad_A<IO, M_><<<grid, 256, 0, st>>>(ge, s, zi, gA, T);
         return cudaGetLastError();

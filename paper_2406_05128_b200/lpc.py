@@ -70,13 +70,16 @@ def _carry_code(p=None):
 
 
 def check_nonfinite(device=None):
-    """Raise ValueError if a lazily validated forward saw non-finite input."""
+    """Lazy mode: returns True if a forward since the last call produced a
+    non-finite output (non-finite input or overflow; re-run eagerly to tell)."""
     devs = list(_pending_flags) if device is None else [torch.device(device)]
+    seen = False
     for d in devs:
         flag = _pending_flags.get(d)
         if flag is not None and int(flag.item()) != 0:
             flag.zero_()
-            raise ValueError("e or A contains non-finite values")
+            seen = True
+    return seen
 
 
 # ---------------------------------------------------------------------------
@@ -153,12 +156,16 @@ def _flag(device):
 
 
 def _raise_nonfinite(flag, e, A, a_name="A"):
+    """The kernel flags a non-finite OUTPUT: either non-finite input (an error,
+    lpc.py:68-69/111-112) or overflow of an unstable filter (legitimate,
+    lpc.py:86-87).  Only then are the inputs scanned to tell them apart."""
     if flag is None or _VALIDATION != "eager":
         return
     if int(flag.item()) != 0:
         if not bool(torch.isfinite(e).all()):
             raise ValueError("e contains non-finite values")
-        raise ValueError(f"{a_name} contains non-finite values")
+        if not bool(torch.isfinite(A).all()):
+            raise ValueError(f"{a_name} contains non-finite values")
 
 
 # ---------------------------------------------------------------------------
