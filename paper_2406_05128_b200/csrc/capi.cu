@@ -65,29 +65,41 @@ struct Plan {
     int Ls = 0, nsub = 0;
 };
 
-int64_t choose_ls(int64_t Tp, int Mp) {
-    const int unit = ls_unit(Mp);
+// Sub-chunk length: a multiple of 8 dividing T (so all sub-chunks are full and
+// uniformly strided for the 2-D tensor TMA), closest to the target (512, or
+// $TVLP_SUBCHUNK); if T has no such divisor, T is padded up to a multiple.
+int64_t choose_ls(int64_t T, int64_t* Tp) {
     int64_t target = 512;
     if (const char* env = std::getenv("TVLP_SUBCHUNK")) {
         const long v = std::atol(env);
-        if (v > 0) target = v;
+        if (v >= 8) target = v;
     }
-    int64_t k = (target + unit / 2) / unit;
-    if (k < 1) k = 1;
-    int64_t Ls = unit * k;
-    const int64_t single = (Tp + unit - 1) / unit * unit;
-    return Ls < single ? Ls : single;
+    if (T >= 256) {
+        int64_t best = -1;
+        for (int64_t d = 256; d <= 1024; d += 8)
+            if (T % d == 0 && (best < 0 || std::llabs(d - target) < std::llabs(best - target)))
+                best = d;
+        if (best > 0) {
+            *Tp = T;
+            return best;
+        }
+        const int64_t Ls = (target + 7) / 8 * 8;
+        *Tp = (T + Ls - 1) / Ls * Ls;
+        return Ls;
+    }
+    const int64_t Ls = (T + 7) / 8 * 8;
+    *Tp = Ls;
+    return Ls;
 }
 
 bool make_plan(int64_t B, int64_t T, int M, Plan& p) {
     if (B < 1 || T < 1 || M < 1 || M > kMaxOrder) return false;
     p.B = B;
     p.T = T;
-    p.Tp = (T + 3) / 4 * 4;
     p.M = M;
     p.Mp = padded_order(M);
-    p.Ls = (int)choose_ls(p.Tp, p.Mp);
-    p.nsub = (int)((p.Tp + p.Ls - 1) / p.Ls);
+    p.Ls = (int)choose_ls(T, &p.Tp);
+    p.nsub = (int)(p.Tp / p.Ls);
     return true;
 }
 

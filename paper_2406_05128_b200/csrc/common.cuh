@@ -5,6 +5,7 @@
 #pragma once
 #include <cstdint>
 #include <type_traits>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace tvlp {
@@ -54,6 +55,28 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         "[%3];" ::"r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+// 2-D tiled tensor copies (CUtensorMap passed as a __grid_constant__ kernel
+// parameter).  smem boxes must be 128-byte aligned; out-of-bounds elements of
+// a load box are zero-filled, out-of-bounds elements of a store box are
+// skipped.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+        "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1,
+                                             const void* src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     map),
+                 "r"(c0), "r"(c1), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 // shared -> global, tracked by the issuing thread's bulk groups.
 __device__ __forceinline__ void tma_store_1d(void* dst, const void* src, uint32_t bytes) {

@@ -22,8 +22,8 @@
 //   e, s, g_s, g_e : [B, T]          A, g_A : [B, T, M]     zi : [B, M]
 //   PhiZ : [B*nsub, M+1, M]          (row c < M: column c of Phi_j; row M: z_j)
 //   Xin, Nu, Mu : [B*nsub, M]        (all in the I/O dtype)
-// Preconditions (enforced by the C ABI, which pads otherwise): T % 4 == 0,
-// Ls % lcm(M,4,8) == 0, all pointers 16-byte aligned.
+// Preconditions (enforced by the C ABI, which pads otherwise): Ls % 8 == 0,
+// T % Ls == 0 (all sub-chunks full), all pointers 16-byte aligned.
 #pragma once
 #include "common.cuh"
 
@@ -197,6 +197,139 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ Phi
 }
 
 // ============================================================================
+// fp32 basis with packed FFMA2: one warp = two sub-chunks (half-warps); lane q
+// of a half runs the chain pair (2q, 2q+1) as one float2, the coefficient is
+// broadcast into both halves of the FFMA2 (SASS: FFMA2 Rd, Ra.F32, Rb.F32x2,
+// Rc.F32x2).  Chain M is the zero-state chain; chains > M are idle slots.
+// ============================================================================
+template <int M, bool TI, int NW>
+struct Basis2Smem {
+    static constexpr int WR = Geo<M>::WR;
+    static constexpr int NSTB = 2;
+    static constexpr int A_BYTES = TI ? 0 : WR * M * 4;
+    static constexpr int STAGE_BYTES = (A_BYTES + WR * 4 + 15) / 16 * 16;
+    static constexpr int HALF_BYTES = NSTB * STAGE_BYTES;
+    static constexpr int BYTES = NW * 2 * HALF_BYTES + NW * 2 * NSTB * 8;
+};
+
+template <int M, bool TI, int NW>
+__global__ void __launch_bounds__(NW * 32)
+k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
+         ScanArgs g) {
+    using S = Basis2Smem<M, TI, NW>;
+    constexpr int WR = S::WR;
+    constexpr int NSTB = S::NSTB;
+    static_assert(M + 1 <= 32, "order M must be <= 31");
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int half = lane >> 4, q = lane & 15;
+    const int slot = warp * 2 + half;
+    unsigned char* hbase = smem + slot * S::HALF_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NW * 2 * S::HALF_BYTES) + slot * NSTB;
+
+    const int64_t nsc = g.B * g.nsub;
+    const int64_t gid0 = ((int64_t)blockIdx.x * NW + warp) * 2;
+    if (gid0 >= nsc) return;  // warp-uniform
+    const int64_t gid = gid0 + half;
+    const bool active = gid < nsc;
+    const int64_t gg = active ? gid : gid0;  // an idle half shadows its sibling's rows
+    const int64_t b = gg / g.nsub;
+    const int j = (int)(gg % g.nsub);
+    const int64_t t0 = (int64_t)j * g.Ls;
+    const int len = g.Ls;  // all sub-chunks are full (T % Ls == 0)
+    const int nwin = (len + WR - 1) / WR;
+    const int64_t row0 = b * g.T + t0;
+
+    if (q == 0) {
+        for (int s2 = 0; s2 < NSTB; ++s2) mbar_init(&bars[s2], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    auto stage_ptr = [&](int st) { return hbase + st * S::STAGE_BYTES; };
+    auto issue = [&](int k) {
+        if (k >= nwin || q != 0) return;
+        const int st = k % NSTB;
+        const int rows = min(WR, len - k * WR);
+        mbar_arrive_expect_tx(&bars[st], rows * ((TI ? 0 : M) + 1) * 4);
+        const int64_t r = row0 + (int64_t)k * WR;
+        unsigned char* p = stage_ptr(st);
+        if (!TI) tma_load_1d(p, A + r * M, rows * M * 4, &bars[st]);
+        tma_load_1d(p + S::A_BYTES, e + r, rows * 4, &bars[st]);
+    };
+#pragma unroll
+    for (int k = 0; k < NSTB; ++k) issue(k);
+
+    float ati[M];
+    if (TI) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) ati[i] = A[b * M + i];
+    }
+    const int cx = 2 * q, cy = 2 * q + 1;  // chain ids of the pair
+    float2 R[M];
+#pragma unroll
+    for (int p = 0; p < M; ++p)
+        R[p] = make_float2((cx < M && M - 1 - p == cx) ? 1.f : 0.f,
+                           (cy < M && M - 1 - p == cy) ? 1.f : 0.f);
+    const float mx = (cx == M) ? 1.f : 0.f, my = (cy == M) ? 1.f : 0.f;
+
+    for (int k = 0; k < nwin; ++k) {
+        const int st = k % NSTB;
+        mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
+        const int rows = min(WR, len - k * WR);
+        const float* Ar = reinterpret_cast<const float*>(stage_ptr(st));
+        const float* er = reinterpret_cast<const float*>(stage_ptr(st) + S::A_BYTES);
+#pragma unroll
+        for (int u = 0; u < WR; ++u) {
+            if (u < rows) {  // warp-uniform: only the last window can be short
+                float a[M];
+                if constexpr (TI) {
+#pragma unroll
+                    for (int i = 0; i < M; ++i) a[i] = ati[i];
+                } else {
+                    load_row_at<float, M>(Ar + u * M, a, u * M * 4);
+                }
+                const float ev = er[u];
+                const float2 ein = make_float2(ev * mx, ev * my);
+                float2 p0 = make_float2(0.f, 0.f), p1 = p0, p2 = p0, p3 = p0;
+#pragma unroll
+                for (int i = M; i >= 2; --i) {
+                    const float2 x = R[(u - i + 2 * M) % M];
+                    const float2 ai = make_float2(a[i - 1], a[i - 1]);
+                    switch (i & 3) {
+                        case 0: p0 = __ffma2_rn(ai, x, p0); break;
+                        case 1: p1 = __ffma2_rn(ai, x, p1); break;
+                        case 2: p2 = __ffma2_rn(ai, x, p2); break;
+                        default: p3 = __ffma2_rn(ai, x, p3); break;
+                    }
+                }
+                const float2 sum = __fadd2_rn(__fadd2_rn(p0, p1), __fadd2_rn(p2, p3));
+                const float2 part = __fadd2_rn(ein, make_float2(-sum.x, -sum.y));
+                const float2 na0 = make_float2(-a[0], -a[0]);
+                R[u % M] = __ffma2_rn(na0, R[(u - 1 + M) % M], part);
+            }
+        }
+        __syncwarp();
+        fence_proxy_async();
+        issue(k + NSTB);
+    }
+
+    // final state x[i] = s(t1 - i) = R[(len-1-i) mod M]
+    if (active && cx <= M) {
+        float2 tmp[M];
+#pragma unroll
+        for (int p = 0; p < M; ++p) tmp[p] = R[p];
+        const int last = (len - 1) % M;
+        float* ox = PhiZ + (gid * (M + 1) + cx) * M;
+        float* oy = PhiZ + (gid * (M + 1) + cy) * M;
+        for (int i = 0; i < M; ++i) {
+            const float2 v = tmp[(last - i + M) % M];
+            ox[i] = v.x;
+            if (cy <= M) oy[i] = v.y;
+        }
+    }
+}
+
+// ============================================================================
 // Carry kernels: one warp per sequence, lane r holds component r.  The chain
 // is latency-bound (one M x M mat-vec per sub-chunk), so the next sub-chunks'
 // matrix rows are prefetched into registers (distance kPF) while the current
@@ -323,187 +456,152 @@ k_carry_bwd(const CT* __restrict__ PhiZ, const CT* __restrict__ Nu, CT* __restri
 
 // ============================================================================
 // Lane-per-sub-chunk streaming kernels (apply fwd, adjoint zero-state, apply
-// bwd).  One warp = 32 consecutive sub-chunks; lane l streams its own rows in
-// windows of W = 8 through a 3-stage shared ring (each lane issues its own
-// 1-D bulk copies; the stage mbarrier expects the warp's total bytes).
-// Outputs are staged per lane and written back by bulk TMA stores.
+// bwd).  One warp = 32 consecutive sub-chunks; lane l runs the recursion of
+// sub-chunk g0+l.  Sub-chunks are full and uniformly strided (the C ABI picks
+// Ls | T or pads T), so the inputs of one window (W rows of all 32 lanes) are
+// ONE 2-D box of the view [B*nsub, Ls*M] (resp. [B*nsub, Ls]) and arrive with
+// a single tensor TMA per operand; outputs leave the same way.  Box rows are
+// padded to an odd number of 16-byte granules so the 32 lanes' vector reads of
+// the same row offset hit distinct bank groups (the pad columns are the next
+// window's first values, or zero-filled past the sub-chunk end).
 // ============================================================================
 template <typename IO, int M, bool TI>
 struct LaneSmem {
     static constexpr int W = kLaneWin;
-    static constexpr int ASTR = TI ? 0 : odd16_stride(W * M * (int)sizeof(IO));
-    static constexpr int XSTR = odd16_stride(W * (int)sizeof(IO));
-    static constexpr int STAGE = 32 * (ASTR + XSTR);
-    static constexpr int OSTR = odd16_stride(W * (int)sizeof(IO));
-    static constexpr int OUT = 32 * OSTR;
-    static constexpr int BYTES = kLaneStages * STAGE + kOutStages * OUT + kLaneStages * 8;
+    static constexpr int SZ = (int)sizeof(IO);
+    static constexpr int AROW = TI ? 0 : odd16_stride(W * M * SZ) / SZ;  // elements per lane
+    static constexpr int XROW = odd16_stride(W * SZ) / SZ;
+    static constexpr int A_BYTES = (32 * AROW * SZ + 127) / 128 * 128;
+    static constexpr int X_BYTES = (32 * XROW * SZ + 127) / 128 * 128;
+    static constexpr int STAGE = A_BYTES + X_BYTES;
+    static constexpr int OUT = (32 * W * SZ + 127) / 128 * 128;
+    static constexpr int BYTES = kLaneStages * STAGE + kOutStages * OUT + 128;
+    static constexpr uint32_t TX = 32u * (AROW + XROW) * SZ;  // bytes landed per stage
 };
 
-// direction: +1 forward windows from t0, -1 reverse windows from t1.
-template <typename IO, int M, bool TI, int DIR>
-struct LaneStream {
-    using S = LaneSmem<IO, M, TI>;
-    static constexpr int W = S::W;
-    unsigned char* base;
-    uint64_t* bars;
-    int lane;
-    bool active;
-    int len;
-    int64_t row0;  // flat row of t0
-    int nwin;
-
-    __device__ __forceinline__ unsigned char* A_slot(int st) const {
-        return base + st * S::STAGE + lane * S::ASTR;
-    }
-    __device__ __forceinline__ unsigned char* X_slot(int st) const {
-        return base + st * S::STAGE + 32 * S::ASTR + lane * S::XSTR;
-    }
-    __device__ __forceinline__ unsigned char* O_slot(int so) const {
-        return base + kLaneStages * S::STAGE + so * S::OUT + lane * S::OSTR;
-    }
-    // window k: rows [lo, lo+rows) relative to t0
-    __device__ __forceinline__ void window(int k, int& lo, int& rows) const {
-        if (DIR > 0) {
-            lo = k * W;
-            rows = active ? max(0, min(W, len - lo)) : 0;
-        } else {
-            const int hi = len - k * W;
-            lo = max(0, hi - W);
-            rows = active ? max(0, hi - lo) : 0;
-        }
-    }
-    __device__ __forceinline__ void issue(int k, int nwin_max, const IO* A, const IO* X) {
-        if (k >= nwin_max) return;
-        const int st = k % kLaneStages;
-        int lo, rows;
-        window(k, lo, rows);
-        const uint32_t mine = rows * ((TI ? 0 : M) + 1) * (uint32_t)sizeof(IO);
-        const uint32_t tot = warp_sum_u32(mine);
-        if (lane == 0) mbar_arrive_expect_tx(&bars[st], tot);
-        __syncwarp();
-        if (rows > 0) {
-            const int64_t r = row0 + lo;
-            // reverse windows may be short at t0: place rows at the window end
-            const int pad = (DIR > 0) ? 0 : (W - rows);
-            if (!TI)
-                tma_load_1d(A_slot(st) + pad * M * (int)sizeof(IO), A + r * M,
-                            rows * M * (uint32_t)sizeof(IO), &bars[st]);
-            tma_load_1d(X_slot(st) + pad * (int)sizeof(IO), X + r, rows * (uint32_t)sizeof(IO),
-                        &bars[st]);
-        }
-    }
+struct LaneMaps {
+    CUtensorMap A;  // [B*nsub, Ls*M] box {AROW, 32}   (unused for TI)
+    CUtensorMap X;  // [B*nsub, Ls]   box {XROW, 32}   (e or g_s)
+    CUtensorMap O;  // [B*nsub, Ls]   box {W, 32}      (s or g_e)
 };
 
 // ---------------------------------------------------------------- apply fwd
 // One lane re-runs the recursion of its sub-chunk from x_in.  The state lives
 // in a register ring of MR = round_up(M, W) slots (slot p holds s at local
 // step tau with tau mod MR == p); the unrolled body covers MR/W windows so
-// every ring index is a compile-time constant.  Full windows take a
-// predicate-free path; only the last window of a sequence can be partial.
+// every ring index is a compile-time constant.
 template <typename IO, int M, bool TI>
 __global__ void __launch_bounds__(32)
-k_apply_fwd(const IO* __restrict__ e, const IO* __restrict__ A, const IO* __restrict__ Xin,
-            IO* __restrict__ s, int* __restrict__ flag, ScanArgs g) {
+k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
+            const IO* __restrict__ Xin, int* __restrict__ flag, ScanArgs g) {
     using S = LaneSmem<IO, M, TI>;
-    using LS = LaneStream<IO, M, TI, +1>;
     constexpr int W = S::W;
     constexpr int MR = (M + W - 1) / W * W;
     constexpr int WPB = MR / W;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x;
-    LS ls;
-    ls.base = smem;
-    ls.bars = reinterpret_cast<uint64_t*>(smem + kLaneStages * S::STAGE + kOutStages * S::OUT);
-    ls.lane = lane;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kLaneStages * S::STAGE + kOutStages * S::OUT);
     const int64_t nsc = g.B * g.nsub;
-    const int64_t gid = (int64_t)blockIdx.x * 32 + lane;
-    ls.active = gid < nsc;
-    const int64_t b = ls.active ? gid / g.nsub : 0;
-    const int j = ls.active ? (int)(gid % g.nsub) : 0;
-    const int64_t t0 = (int64_t)j * g.Ls;
-    ls.len = ls.active ? (int)(int64_t)min((int64_t)(g.Ls), (int64_t)(g.T - t0)) : 0;
-    ls.row0 = b * g.T + t0;
-    const int nwin_max = (g.Ls + W - 1) / W;
+    const int g0 = blockIdx.x * 32;
+    const int64_t gid = (int64_t)g0 + lane;
+    const bool active = gid < nsc;
+    const int nwin = g.Ls / W;
 
     if (lane == 0) {
-        for (int st = 0; st < kLaneStages; ++st) mbar_init(&ls.bars[st], 1);
+        prefetch_tmap(&maps.A);
+        prefetch_tmap(&maps.X);
+        prefetch_tmap(&maps.O);
+        for (int st = 0; st < kLaneStages; ++st) mbar_init(&bars[st], 1);
         fence_mbar_init();
     }
     __syncwarp();
+    auto issue = [&](int k) {
+        if (k < nwin && lane == 0) {
+            const int st = k % kLaneStages;
+            unsigned char* base = smem + st * S::STAGE;
+            mbar_arrive_expect_tx(&bars[st], S::TX);
+            if (!TI) tma_load_2d(base, &maps.A, k * W * M, g0, &bars[st]);
+            tma_load_2d(base + S::A_BYTES, &maps.X, k * W, g0, &bars[st]);
+        }
+    };
 #pragma unroll
-    for (int k = 0; k < kLaneStages; ++k) ls.issue(k, nwin_max, A, e);
+    for (int k = 0; k < kLaneStages; ++k) issue(k);
 
     IO ati[M];
     if (TI) {
+        const int64_t b = active ? gid / g.nsub : 0;
 #pragma unroll
-        for (int i = 0; i < M; ++i) ati[i] = ls.active ? A[b * M + i] : (IO)0;
+        for (int i = 0; i < M; ++i) ati[i] = active ? ati_ptr[b * M + i] : (IO)0;
     }
     IO R[MR];
 #pragma unroll
     for (int p = 0; p < MR; ++p) R[p] = (IO)0;
 #pragma unroll
-    for (int i = 0; i < M; ++i) R[MR - 1 - i] = ls.active ? Xin[gid * M + i] : (IO)0;
+    for (int i = 0; i < M; ++i) R[MR - 1 - i] = active ? Xin[gid * M + i] : (IO)0;
     bool finite = true;
 
-    for (int kb = 0; kb < nwin_max; kb += WPB) {
+    for (int kb = 0; kb < nwin; kb += WPB) {
 #pragma unroll
         for (int w = 0; w < WPB; ++w) {
             const int k = kb + w;
-            if (k < nwin_max) {
+            if (k < nwin) {
                 const int st = k % kLaneStages;
-                mbar_wait(&ls.bars[st], (uint32_t)((k / kLaneStages) & 1));
-                int lo, rows;
-                ls.window(k, lo, rows);
-                const IO* Ar = reinterpret_cast<const IO*>(ls.A_slot(st));
-                const IO* er = reinterpret_cast<const IO*>(ls.X_slot(st));
+                mbar_wait(&bars[st], (uint32_t)((k / kLaneStages) & 1));
+                const unsigned char* base = smem + st * S::STAGE;
+                const IO* Ar = reinterpret_cast<const IO*>(base) + lane * S::AROW;
+                const IO* er = reinterpret_cast<const IO*>(base + S::A_BYTES) + lane * S::XROW;
                 const int so = k % kOutStages;
-                IO* ob = reinterpret_cast<IO*>(ls.O_slot(so));
-                if (k >= kOutStages) bulk_wait_read<kOutStages - 1>();
+                IO* obox = reinterpret_cast<IO*>(smem + kLaneStages * S::STAGE + so * S::OUT);
+                IO* ob = obox + lane * W;
+                if (k >= kOutStages) {
+                    if (lane == 0) bulk_wait_read<kOutStages - 1>();
+                    __syncwarp();
+                }
                 IO ev[W];
 #pragma unroll
                 for (int u = 0; u < W; ++u) ev[u] = er[u];
-                const bool full = rows == W;
 #pragma unroll
                 for (int u = 0; u < W; ++u) {
-                    if (full || u < rows) {
-                        const int pos = w * W + u;  // compile-time after unrolling
-                        IO a[M];
-                        if constexpr (TI) {
+                    const int pos = w * W + u;  // compile-time after unrolling
+                    IO a[M];
+                    if constexpr (TI) {
 #pragma unroll
-                            for (int i = 0; i < M; ++i) a[i] = ati[i];
-                        } else {
-                            load_row_at<IO, M>(Ar + u * M, a, u * M * (int)sizeof(IO));
-                        }
-                        IO p0 = (IO)0, p1 = (IO)0, p2 = (IO)0, p3 = (IO)0;
-#pragma unroll
-                        for (int i = M; i >= 2; --i) {
-                            const IO x = R[(pos - i + 2 * MR) % MR];
-                            switch (i & 3) {
-                                case 0: p0 = fma(a[i - 1], x, p0); break;
-                                case 1: p1 = fma(a[i - 1], x, p1); break;
-                                case 2: p2 = fma(a[i - 1], x, p2); break;
-                                default: p3 = fma(a[i - 1], x, p3); break;
-                            }
-                        }
-                        const IO v = fma(-a[0], R[(pos - 1 + MR) % MR], ev[u] - ((p0 + p1) + (p2 + p3)));
-                        R[pos % MR] = v;
-                        ob[u] = v;
-                        finite &= is_finite_val(v);
+                        for (int i = 0; i < M; ++i) a[i] = ati[i];
+                    } else {
+                        load_row_at<IO, M>(Ar + u * M, a, (lane * S::AROW + u * M) * S::SZ);
                     }
+                    IO p0 = (IO)0, p1 = (IO)0, p2 = (IO)0, p3 = (IO)0;
+#pragma unroll
+                    for (int i = M; i >= 2; --i) {
+                        const IO x = R[(pos - i + 2 * MR) % MR];
+                        switch (i & 3) {
+                            case 0: p0 = fma(a[i - 1], x, p0); break;
+                            case 1: p1 = fma(a[i - 1], x, p1); break;
+                            case 2: p2 = fma(a[i - 1], x, p2); break;
+                            default: p3 = fma(a[i - 1], x, p3); break;
+                        }
+                    }
+                    const IO v =
+                        fma(-a[0], R[(pos - 1 + MR) % MR], ev[u] - ((p0 + p1) + (p2 + p3)));
+                    R[pos % MR] = v;
+                    ob[u] = v;
+                    finite &= is_finite_val(v);
                 }
-                __syncwarp();
                 fence_proxy_async();
-                if (rows > 0) tma_store_1d(s + ls.row0 + lo, ob, rows * (uint32_t)sizeof(IO));
-                bulk_commit();
-                ls.issue(k + kLaneStages, nwin_max, A, e);
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&maps.O, k * W, g0, obox);
+                    bulk_commit();
+                }
+                issue(k + kLaneStages);
             }
         }
     }
-    bulk_wait<0>();
+    if (lane == 0) bulk_wait<0>();
     if (flag != nullptr) {
         // a non-finite output means non-finite input or overflow; the host
         // tells them apart (overflow of an unstable filter is legitimate).
-        const unsigned bad = __ballot_sync(0xffffffffu, !finite);
+        const unsigned bad = __ballot_sync(0xffffffffu, active && !finite);
         if (bad && lane == 0) atomicOr(flag, 1);
     }
 }
@@ -515,89 +613,95 @@ k_apply_fwd(const IO* __restrict__ e, const IO* __restrict__ A, const IO* __rest
 // The transposed-state update shifts lambda inside its FMAs (no moves).
 template <typename IO, int M, bool TI, int MODE>
 __global__ void __launch_bounds__(32)
-k_adjoint(const IO* __restrict__ gs, const IO* __restrict__ A, const IO* __restrict__ Mu,
-          IO* __restrict__ Nu, IO* __restrict__ ge, ScanArgs g) {
+k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
+          const IO* __restrict__ Mu, IO* __restrict__ Nu, ScanArgs g) {
     using S = LaneSmem<IO, M, TI>;
-    using LS = LaneStream<IO, M, TI, -1>;
     constexpr int W = S::W;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x;
-    LS ls;
-    ls.base = smem;
-    ls.bars = reinterpret_cast<uint64_t*>(smem + kLaneStages * S::STAGE + kOutStages * S::OUT);
-    ls.lane = lane;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kLaneStages * S::STAGE + kOutStages * S::OUT);
     const int64_t nsc = g.B * g.nsub;
-    const int64_t gid = (int64_t)blockIdx.x * 32 + lane;
-    ls.active = gid < nsc;
-    const int64_t b = ls.active ? gid / g.nsub : 0;
-    const int j = ls.active ? (int)(gid % g.nsub) : 0;
-    const int64_t t0 = (int64_t)j * g.Ls;
-    ls.len = ls.active ? (int)(int64_t)min((int64_t)(g.Ls), (int64_t)(g.T - t0)) : 0;
-    ls.row0 = b * g.T + t0;
-    const int nwin_max = (g.Ls + W - 1) / W;
+    const int g0 = blockIdx.x * 32;
+    const int64_t gid = (int64_t)g0 + lane;
+    const bool active = gid < nsc;
+    const int nwin = g.Ls / W;
 
     if (lane == 0) {
-        for (int st = 0; st < kLaneStages; ++st) mbar_init(&ls.bars[st], 1);
+        prefetch_tmap(&maps.A);
+        prefetch_tmap(&maps.X);
+        if (MODE == 1) prefetch_tmap(&maps.O);
+        for (int st = 0; st < kLaneStages; ++st) mbar_init(&bars[st], 1);
         fence_mbar_init();
     }
     __syncwarp();
+    // reverse window k covers rows [Ls-(k+1)W, Ls-kW)
+    auto issue = [&](int k) {
+        if (k < nwin && lane == 0) {
+            const int st = k % kLaneStages;
+            unsigned char* base = smem + st * S::STAGE;
+            const int wr = nwin - 1 - k;
+            mbar_arrive_expect_tx(&bars[st], S::TX);
+            if (!TI) tma_load_2d(base, &maps.A, wr * W * M, g0, &bars[st]);
+            tma_load_2d(base + S::A_BYTES, &maps.X, wr * W, g0, &bars[st]);
+        }
+    };
 #pragma unroll
-    for (int k = 0; k < kLaneStages; ++k) ls.issue(k, nwin_max, A, gs);
+    for (int k = 0; k < kLaneStages; ++k) issue(k);
 
     IO ati[M];
     if (TI) {
+        const int64_t b = active ? gid / g.nsub : 0;
 #pragma unroll
-        for (int i = 0; i < M; ++i) ati[i] = ls.active ? A[b * M + i] : (IO)0;
+        for (int i = 0; i < M; ++i) ati[i] = active ? ati_ptr[b * M + i] : (IO)0;
     }
     IO lam[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i)
-        lam[i] = (MODE == 1 && ls.active) ? Mu[gid * M + i] : (IO)0;
+    for (int i = 0; i < M; ++i) lam[i] = (MODE == 1 && active) ? Mu[gid * M + i] : (IO)0;
 
-    // reverse windows of a sub-chunk whose length is not a multiple of W:
-    // window k covers [max(0, len-(k+1)W), len-kW); slots are right-aligned.
-    for (int k = 0; k < nwin_max; ++k) {
+    for (int k = 0; k < nwin; ++k) {
         const int st = k % kLaneStages;
-        mbar_wait(&ls.bars[st], (uint32_t)((k / kLaneStages) & 1));
-        int lo, rows;
-        ls.window(k, lo, rows);
-        const IO* Ar = reinterpret_cast<const IO*>(ls.A_slot(st));
-        const IO* xr = reinterpret_cast<const IO*>(ls.X_slot(st));
+        mbar_wait(&bars[st], (uint32_t)((k / kLaneStages) & 1));
+        const unsigned char* base = smem + st * S::STAGE;
+        const IO* Ar = reinterpret_cast<const IO*>(base) + lane * S::AROW;
+        const IO* xr = reinterpret_cast<const IO*>(base + S::A_BYTES) + lane * S::XROW;
         const int so = k % kOutStages;
-        IO* ob = reinterpret_cast<IO*>(ls.O_slot(so));
-        if (MODE == 1 && k >= kOutStages) bulk_wait_read<kOutStages - 1>();
+        IO* obox = reinterpret_cast<IO*>(smem + kLaneStages * S::STAGE + so * S::OUT);
+        IO* ob = obox + lane * W;
+        if (MODE == 1 && k >= kOutStages) {
+            if (lane == 0) bulk_wait_read<kOutStages - 1>();
+            __syncwarp();
+        }
         IO gv[W];
 #pragma unroll
         for (int u = 0; u < W; ++u) gv[u] = xr[u];
-        const bool full = rows == W;
 #pragma unroll
         for (int u = W - 1; u >= 0; --u) {
-            if (full || u >= W - rows) {
-                IO a[M];
-                if constexpr (TI) {
+            IO a[M];
+            if constexpr (TI) {
 #pragma unroll
-                    for (int i = 0; i < M; ++i) a[i] = ati[i];
-                } else {
-                    load_row_at<IO, M>(Ar + u * M, a, u * M * (int)sizeof(IO));
-                }
-                const IO l0 = lam[0] + gv[u];
-                if (MODE == 1) ob[u] = l0;
-#pragma unroll
-                for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
-                lam[M - 1] = -a[M - 1] * l0;
+                for (int i = 0; i < M; ++i) a[i] = ati[i];
+            } else {
+                load_row_at<IO, M>(Ar + u * M, a, (lane * S::AROW + u * M) * S::SZ);
             }
+            const IO l0 = lam[0] + gv[u];
+            if (MODE == 1) ob[u] = l0;
+#pragma unroll
+            for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
+            lam[M - 1] = -a[M - 1] * l0;
         }
         if (MODE == 1) {
-            __syncwarp();
             fence_proxy_async();
-            if (rows > 0)
-                tma_store_1d(ge + ls.row0 + lo, ob + (W - rows), rows * (uint32_t)sizeof(IO));
-            bulk_commit();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&maps.O, (nwin - 1 - k) * W, g0, obox);
+                bulk_commit();
+            }
         }
-        ls.issue(k + kLaneStages, nwin_max, A, gs);
+        __syncwarp();
+        issue(k + kLaneStages);
     }
-    if (MODE == 1) bulk_wait<0>();
-    if (MODE == 0 && ls.active) {
+    if (MODE == 1 && lane == 0) bulk_wait<0>();
+    if (MODE == 0 && active) {
 #pragma unroll
         for (int i = 0; i < M; ++i) Nu[gid * M + i] = lam[i];
     }

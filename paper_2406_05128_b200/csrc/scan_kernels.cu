@@ -1,4 +1,8 @@
 // scan_kernels.cu -- instantiations and launchers of the chunked-scan kernels.
+#include <cstring>
+
+#include <cudaTypedefs.h>
+
 #include "lp_scan.cuh"
 #include "scan_launch.cuh"
 
@@ -27,6 +31,63 @@ cudaError_t basis_impl(const IO* e, const IO* A, IO* PhiZ, const ScanArgs& g,
     return cudaGetLastError();
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D row-major view [dim1, dim0] of `base`, box {box0, box1}
+cudaError_t map2d(CUtensorMap* m, const void* base, int sz, uint64_t dim0, uint64_t dim1,
+                  uint32_t box0, uint32_t box1) {
+    std::memset(m, 0, sizeof(*m));
+    if (base == nullptr) return cudaSuccess;
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    cuuint64_t gdim[2] = {dim0, dim1};
+    cuuint64_t gstr[1] = {dim0 * (uint64_t)sz};
+    cuuint32_t box[2] = {box0, box1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, sz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                    2, const_cast<void*>(base), gdim, gstr, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <typename IO, int M, bool TI>
+cudaError_t lane_maps(LaneMaps& mp, const IO* A, const IO* X, const IO* O, const ScanArgs& g) {
+    using S = LaneSmem<IO, M, TI>;
+    const uint64_t rows = (uint64_t)g.B * g.nsub;
+    cudaError_t err = cudaSuccess;
+    if (!TI) err = map2d(&mp.A, A, S::SZ, (uint64_t)g.Ls * M, rows, S::AROW, 32);
+    else std::memset(&mp.A, 0, sizeof(mp.A));
+    if (err == cudaSuccess) err = map2d(&mp.X, X, S::SZ, (uint64_t)g.Ls, rows, S::XROW, 32);
+    if (err == cudaSuccess) err = map2d(&mp.O, O, S::SZ, (uint64_t)g.Ls, rows, S::W, 32);
+    return err;
+}
+
+template <int M, bool TI>
+cudaError_t basis2_impl(const float* e, const float* A, float* PhiZ, const ScanArgs& g,
+                        cudaStream_t st) {
+    using S = Basis2Smem<M, TI, kBasisWarps>;
+    auto k = k_basis2<M, TI, kBasisWarps>;
+    cudaError_t err = ensure_smem(k, S::BYTES);
+    if (err != cudaSuccess) return err;
+    const int64_t nsc = g.B * g.nsub;
+    const int64_t per_block = 2 * kBasisWarps;
+    k<<<(unsigned)((nsc + per_block - 1) / per_block), kBasisWarps * 32, S::BYTES, st>>>(e, A,
+                                                                                      PhiZ, g);
+    return cudaGetLastError();
+}
+
 template <typename IO, int M, bool TI>
 cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag,
                        const ScanArgs& g, cudaStream_t st) {
@@ -34,8 +95,11 @@ cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag
     auto k = k_apply_fwd<IO, M, TI>;
     cudaError_t err = ensure_smem(k, S::BYTES);
     if (err != cudaSuccess) return err;
+    LaneMaps mp;
+    err = lane_maps<IO, M, TI>(mp, TI ? nullptr : A, e, s, g);
+    if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
-    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(e, A, Xin, s, flag, g);
+    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Xin, flag, g);
     return cudaGetLastError();
 }
 
@@ -46,8 +110,11 @@ cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge
     auto k = k_adjoint<IO, M, TI, MODE>;
     cudaError_t err = ensure_smem(k, S::BYTES);
     if (err != cudaSuccess) return err;
+    LaneMaps mp;
+    err = lane_maps<IO, M, TI>(mp, TI ? nullptr : A, gs, MODE == 1 ? ge : nullptr, g);
+    if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
-    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(gs, A, Mu, Nu, ge, g);
+    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Mu, Nu, g);
     return cudaGetLastError();
 }
 
@@ -67,25 +134,14 @@ cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge
 
 }  // namespace
 
-int ls_unit(int Mp) {
-    switch (Mp) {
-#define TVLP_LSU(m) \
-    case m: return Geo<m>::LsUnit;
-        TVLP_LSU(2) TVLP_LSU(4) TVLP_LSU(6) TVLP_LSU(8) TVLP_LSU(12) TVLP_LSU(16) TVLP_LSU(22)
-        TVLP_LSU(24) TVLP_LSU(30)
-#undef TVLP_LSU
-        default: return -1;
-    }
-}
-
 template <typename IO>
 cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO* PhiZ,
                          const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
         if constexpr (std::is_same<IO, float>::value) {
             if (prec == kPrecF32Chains)
-                return ti ? basis_impl<IO, float, M_, true>(e, A, PhiZ, g, st)
-                          : basis_impl<IO, float, M_, false>(e, A, PhiZ, g, st);
+                return ti ? basis2_impl<M_, true>(e, A, PhiZ, g, st)
+                          : basis2_impl<M_, false>(e, A, PhiZ, g, st);
         }
         return ti ? basis_impl<IO, double, M_, true>(e, A, PhiZ, g, st)
                   : basis_impl<IO, double, M_, false>(e, A, PhiZ, g, st);

@@ -16,7 +16,6 @@ inline int padded_order(int M) {
         if (kOrders[i] >= M) return kOrders[i];
     return -1;
 }
-int ls_unit(int Mp);  // sub-chunk length granularity for order Mp
 
 enum Prec : int { kPrecF64Chains = 0, kPrecF32Chains = 1 };
 

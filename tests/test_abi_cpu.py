@@ -29,7 +29,7 @@ def test_abi_queries_without_gpu():
     assert lib.tvlp_abi_version() == 1
     assert lib.tvlp_max_order() >= 22
     Ls = lib.tvlp_subchunk_len(48000, 22)
-    assert Ls % 88 == 0 and 256 <= Ls <= 1024
+    assert Ls % 8 == 0 and 48000 % Ls == 0 and 256 <= Ls <= 1024
     nsub = -(-48000 // Ls)
     assert lib.tvlp_carry_elems(64, 48000, 22) == 64 * nsub * 23 * 22
     for op in range(4):
