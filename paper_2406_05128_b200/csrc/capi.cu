@@ -112,7 +112,7 @@ ScanArgs scan_args(const Plan& p) {
     return g;
 }
 
-int64_t carry_elems(const Plan& p) { return p.B * (int64_t)p.nsub * (p.Mp + 1) * p.Mp; }
+int64_t carry_elems(const Plan& p) { return p.B * (int64_t)p.nsub * tape_elems(p.Mp); }
 
 // bump allocator over the caller's workspace (nullptr base = sizing pass)
 struct Carver {

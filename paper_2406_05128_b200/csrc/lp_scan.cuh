@@ -44,6 +44,18 @@ struct ScanArgs {
     int Ls, nsub;
 };
 
+// Carry tape of one sub-chunk (I/O dtype), rows padded to MP4 = round_up(M,4):
+//   rows 0..M-1   W[c] = column c of Phi_j      (read by the adjoint carry)
+//   row  M        z_j  (zero-state final state) (forward carry)
+//   rows M+1..2M  R[i] = row i of Phi_j         (forward carry)
+template <int M>
+struct Tape {
+    static constexpr int MP4 = (M + 3) / 4 * 4;
+    static constexpr int Z_ROW = M;
+    static constexpr int R_ROW = M + 1;
+    static constexpr int SIZE = (2 * M + 1) * MP4;
+};
+
 // ============================================================================
 // Basis kernel: one warp per sub-chunk; lane c < M runs the unit chain c,
 // lane M runs the zero-state chain driven by e.  ACC is the chain precision
@@ -190,9 +202,14 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ Phi
         ACC tmp[M];
 #pragma unroll
         for (int p = 0; p < M; ++p) tmp[p] = R[p];
-        IO* out = PhiZ + (gid * (M + 1) + lane) * M;
+        IO* tape = PhiZ + gid * Tape<M>::SIZE;
+        IO* out = tape + lane * Tape<M>::MP4;  // W[lane] (or z for lane M)
         const int last = (len - 1) % M;
-        for (int i = 0; i < M; ++i) out[i] = (IO)tmp[(last - i + M) % M];
+        for (int i = 0; i < M; ++i) {
+            const IO v = (IO)tmp[(last - i + M) % M];
+            out[i] = v;
+            if (lane < M) tape[(Tape<M>::R_ROW + i) * Tape<M>::MP4 + lane] = v;  // R[i][lane]
+        }
     }
 }
 
@@ -204,10 +221,11 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ Phi
 // ============================================================================
 template <int M, bool TI, int NW>
 struct Basis2Smem {
-    static constexpr int WR = Geo<M>::WR;
+    static_assert(M % 2 == 0, "even orders only (odd orders are padded)");
+    static constexpr int WR = M;  // window = M rows: 4*M*M bytes, 16-B aligned for even M
     static constexpr int NSTB = 2;
-    static constexpr int A_BYTES = TI ? 0 : WR * M * 4;
-    static constexpr int STAGE_BYTES = (A_BYTES + WR * 4 + 15) / 16 * 16;
+    static constexpr int A_BYTES = TI ? 16 : WR * M * 4;
+    static constexpr int STAGE_BYTES = (A_BYTES + 15) / 16 * 16;
     static constexpr int HALF_BYTES = NSTB * STAGE_BYTES;
     static constexpr int BYTES = NW * 2 * HALF_BYTES + NW * 2 * NSTB * 8;
 };
@@ -239,22 +257,20 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
     const int len = g.Ls;  // all sub-chunks are full (T % Ls == 0)
     const int nwin = (len + WR - 1) / WR;
     const int64_t row0 = b * g.T + t0;
+    const float* eb = e + row0;
 
-    if (q == 0) {
+    if (!TI && q == 0) {
         for (int s2 = 0; s2 < NSTB; ++s2) mbar_init(&bars[s2], 1);
         fence_mbar_init();
     }
     __syncwarp();
     auto stage_ptr = [&](int st) { return hbase + st * S::STAGE_BYTES; };
     auto issue = [&](int k) {
-        if (k >= nwin || q != 0) return;
+        if (TI || k >= nwin || q != 0) return;
         const int st = k % NSTB;
         const int rows = min(WR, len - k * WR);
-        mbar_arrive_expect_tx(&bars[st], rows * ((TI ? 0 : M) + 1) * 4);
-        const int64_t r = row0 + (int64_t)k * WR;
-        unsigned char* p = stage_ptr(st);
-        if (!TI) tma_load_1d(p, A + r * M, rows * M * 4, &bars[st]);
-        tma_load_1d(p + S::A_BYTES, e + r, rows * 4, &bars[st]);
+        mbar_arrive_expect_tx(&bars[st], rows * M * 4);
+        tma_load_1d(stage_ptr(st), A + (row0 + (int64_t)k * WR) * M, rows * M * 4, &bars[st]);
     };
 #pragma unroll
     for (int k = 0; k < NSTB; ++k) issue(k);
@@ -274,10 +290,10 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
 
     for (int k = 0; k < nwin; ++k) {
         const int st = k % NSTB;
-        mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
+        if (!TI) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
         const int rows = min(WR, len - k * WR);
         const float* Ar = reinterpret_cast<const float*>(stage_ptr(st));
-        const float* er = reinterpret_cast<const float*>(stage_ptr(st) + S::A_BYTES);
+        const float* ek = eb + k * WR;  // excitation (zero-state chain only), L1/L2 broadcast
 #pragma unroll
         for (int u = 0; u < WR; ++u) {
             if (u < rows) {  // warp-uniform: only the last window can be short
@@ -288,7 +304,7 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
                 } else {
                     load_row_at<float, M>(Ar + u * M, a, u * M * 4);
                 }
-                const float ev = er[u];
+                const float ev = __ldg(ek + u);
                 const float2 ein = make_float2(ev * mx, ev * my);
                 float2 p0 = make_float2(0.f, 0.f), p1 = p0, p2 = p0, p3 = p0;
 #pragma unroll
@@ -319,74 +335,116 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
 #pragma unroll
         for (int p = 0; p < M; ++p) tmp[p] = R[p];
         const int last = (len - 1) % M;
-        float* ox = PhiZ + (gid * (M + 1) + cx) * M;
-        float* oy = PhiZ + (gid * (M + 1) + cy) * M;
+        float* tape = PhiZ + gid * Tape<M>::SIZE;
+        float* ox = tape + cx * Tape<M>::MP4;
+        float* oy = tape + cy * Tape<M>::MP4;
+        float* rr = tape + Tape<M>::R_ROW * Tape<M>::MP4;
         for (int i = 0; i < M; ++i) {
             const float2 v = tmp[(last - i + M) % M];
             ox[i] = v.x;
+            if (cx < M) rr[i * Tape<M>::MP4 + cx] = v.x;
             if (cy <= M) oy[i] = v.y;
+            if (cy < M) rr[i * Tape<M>::MP4 + cy] = v.y;
         }
     }
 }
 
 // ============================================================================
 // Carry kernels: one warp per sequence, lane r holds component r.  The chain
-// is latency-bound (one M x M mat-vec per sub-chunk), so the next sub-chunks'
-// matrix rows are prefetched into registers (distance kPF) while the current
-// mat-vec runs; the state is broadcast through shared memory.
+// is latency-bound (one M x M mat-vec per sub-chunk): the lane's matrix row is
+// prefetched kPF sub-chunks ahead into registers with 16-byte loads, and the
+// state vector is broadcast through shared memory as float4/double2 reads, so
+// a step is ~M FMAs + M/4 vector loads on the critical path.
 // ============================================================================
 constexpr int kPF = 4;
 
-template <int M, typename ACC, typename CT>
-__global__ void __launch_bounds__(128)
-k_carry_fwd(const CT* __restrict__ PhiZ, const CT* __restrict__ zi, CT* __restrict__ Xin,
-            ScanArgs g) {
-    __shared__ ACC xs[4][32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t b = (int64_t)blockIdx.x * 4 + warp;
-    if (b >= g.B) return;
-    const int r = lane < M ? lane : 0;
-    ACC x = (ACC)0;
-    if (zi != nullptr && lane < M) x = (ACC)zi[b * M + lane];
-    const int64_t g0 = b * g.nsub;
-    const int nstep = g.nsub - 1;
-    // ring of prefetched rows: w[k][c] = Phi_j[r][c] (c < M), w[k][M] = z_j[r]
-    CT w[kPF][M + 1];
+template <typename CT, int N>
+__device__ __forceinline__ void load_vec(const CT* p, CT (&v)[N]) {
+    static_assert(N % 4 == 0, "padded rows");
+    if constexpr (sizeof(CT) == 4) {
 #pragma unroll
-    for (int k = 0; k < kPF; ++k) {
-        if (k < nstep) {
-            const CT* W = PhiZ + (g0 + k) * (M + 1) * M;
+        for (int i = 0; i < N; i += 4) {
+            const float4 q = *reinterpret_cast<const float4*>(p + i);
+            v[i] = q.x;
+            v[i + 1] = q.y;
+            v[i + 2] = q.z;
+            v[i + 3] = q.w;
+        }
+    } else {
 #pragma unroll
-            for (int c = 0; c <= M; ++c) w[k][c] = W[c * M + r];
+        for (int i = 0; i < N; i += 2) {
+            const double2 q = *reinterpret_cast<const double2*>(p + i);
+            v[i] = q.x;
+            v[i + 1] = q.y;
         }
     }
-    for (int j0 = 0; j0 <= nstep; j0 += kPF) {
+}
+
+template <int M, typename CT>
+__device__ __forceinline__ CT dot_rows(const CT (&w)[Tape<M>::MP4], const CT (&x)[Tape<M>::MP4],
+                                       CT init) {
+    CT q0 = init, q1 = (CT)0, q2 = (CT)0, q3 = (CT)0;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+        switch (c & 3) {
+            case 0: q0 = fma(w[c], x[c], q0); break;
+            case 1: q1 = fma(w[c], x[c], q1); break;
+            case 2: q2 = fma(w[c], x[c], q2); break;
+            default: q3 = fma(w[c], x[c], q3); break;
+        }
+    }
+    return (q0 + q1) + (q2 + q3);
+}
+
+// Forward carry over segments: segment s = (sequence b, first sub-chunk k0,
+// count n); x(k0) = x0[s] (or zi / zero), x(k+1) = Phi_k x(k) + z_k.  Writes
+// Xin[k] for every sub-chunk of the segment.
+template <int M, typename CT>
+__global__ void __launch_bounds__(128)
+k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, CT* __restrict__ Xin,
+            int64_t nseg, int seglen, int nsub) {
+    using TP = Tape<M>;
+    constexpr int MP4 = TP::MP4;
+    __shared__ __align__(16) CT xs[4][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t sidx = (int64_t)blockIdx.x * 4 + warp;
+    if (sidx >= nseg) return;
+    const int nper = (nsub + seglen - 1) / seglen;  // segments per sequence
+    const int64_t b = sidx / nper;
+    const int k0 = (int)(sidx % nper) * seglen;
+    const int n = min(seglen, nsub - k0);
+    const int64_t base = b * nsub + k0;
+    const int r = lane < M ? lane : 0;
+    CT x = (x0 != nullptr && lane < M) ? x0[sidx * M + lane] : (CT)0;
+    CT w[kPF][MP4];
+    CT z[kPF];
+#pragma unroll
+    for (int k = 0; k < kPF; ++k) {
+        if (k < n - 1) {
+            const CT* t = tape + (base + k) * TP::SIZE;
+            load_vec<CT, MP4>(t + (TP::R_ROW + r) * MP4, w[k]);
+            z[k] = t[TP::Z_ROW * MP4 + r];
+        }
+    }
+    for (int i0 = 0; i0 < n; i0 += kPF) {
 #pragma unroll
         for (int k = 0; k < kPF; ++k) {
-            const int j = j0 + k;
-            if (j <= nstep) {
-                if (lane < M) Xin[(g0 + j) * M + lane] = (CT)x;
-                if (j < nstep) {
-                    xs[warp][lane] = x;
+            const int i = i0 + k;
+            if (i < n) {
+                if (lane < M) Xin[(base + i) * M + lane] = x;
+                if (i < n - 1) {
+                    xs[warp][lane] = lane < M ? x : (CT)0;
                     __syncwarp();
-                    ACC q0 = (ACC)w[k][M], q1 = (ACC)0, q2 = (ACC)0, q3 = (ACC)0;
-#pragma unroll
-                    for (int c = 0; c < M; ++c) {
-                        const ACC xc = xs[warp][c];
-                        switch (c & 3) {
-                            case 0: q0 = fma((ACC)w[k][c], xc, q0); break;
-                            case 1: q1 = fma((ACC)w[k][c], xc, q1); break;
-                            case 2: q2 = fma((ACC)w[k][c], xc, q2); break;
-                            default: q3 = fma((ACC)w[k][c], xc, q3); break;
-                        }
-                    }
+                    CT xv[MP4];
+                    load_vec<CT, MP4>(&xs[warp][0], xv);
+                    const CT xn = dot_rows<M, CT>(w[k], xv, z[k]);
                     __syncwarp();
-                    if (lane < M) x = (q0 + q1) + (q2 + q3);
-                    const int jn = j + kPF;
-                    if (jn < nstep) {
-                        const CT* W = PhiZ + (g0 + jn) * (M + 1) * M;
-#pragma unroll
-                        for (int c = 0; c <= M; ++c) w[k][c] = W[c * M + r];
+                    x = xn;
+                    const int in = i + kPF;
+                    if (in < n - 1) {
+                        const CT* t = tape + (base + in) * TP::SIZE;
+                        load_vec<CT, MP4>(t + (TP::R_ROW + r) * MP4, w[k]);
+                        z[k] = t[TP::Z_ROW * MP4 + r];
                     }
                 }
             }
@@ -394,59 +452,57 @@ k_carry_fwd(const CT* __restrict__ PhiZ, const CT* __restrict__ zi, CT* __restri
     }
 }
 
-// mu(j-1) = Phi_j^T mu(j) + nu_j ;  Mu[j] = carry into sub-chunk j from the right.
-template <int M, typename ACC, typename CT>
+// Adjoint carry over segments (right to left): mu(k_last) = m0[s] (or zero),
+// mu(k-1) = Phi_k^T mu(k) + nu_k.  Writes Mu[k] = carry into sub-chunk k.
+template <int M, typename CT>
 __global__ void __launch_bounds__(128)
-k_carry_bwd(const CT* __restrict__ PhiZ, const CT* __restrict__ Nu, CT* __restrict__ Mu,
-            ScanArgs g) {
-    __shared__ ACC ms[4][32];
+k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __restrict__ m0,
+            CT* __restrict__ Mu, int64_t nseg, int seglen, int nsub) {
+    using TP = Tape<M>;
+    constexpr int MP4 = TP::MP4;
+    __shared__ __align__(16) CT ms[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t b = (int64_t)blockIdx.x * 4 + warp;
-    if (b >= g.B) return;
+    const int64_t sidx = (int64_t)blockIdx.x * 4 + warp;
+    if (sidx >= nseg) return;
+    const int nper = (nsub + seglen - 1) / seglen;
+    const int64_t b = sidx / nper;
+    const int k0 = (int)(sidx % nper) * seglen;
+    const int n = min(seglen, nsub - k0);
+    const int64_t base = b * nsub + k0;
     const int r = lane < M ? lane : 0;
-    ACC mu = (ACC)0;
-    const int64_t g0 = b * g.nsub;
-    const int nstep = g.nsub - 1;  // steps j = nsub-1 .. 1
-    // w[k][c] = Phi_j^T[r][c] = W_j[r][c]; w[k][M] = nu_j[r]
-    CT w[kPF][M + 1];
+    CT mu = (m0 != nullptr && lane < M) ? m0[sidx * M + lane] : (CT)0;
+    CT w[kPF][MP4];
+    CT nu[kPF];
+    // step i handles sub-chunk k = n-1-i (it needs Phi_k, nu_k for k >= 1)
 #pragma unroll
     for (int k = 0; k < kPF; ++k) {
-        const int j = g.nsub - 1 - k;
-        if (j >= 1) {
-            const CT* W = PhiZ + (g0 + j) * (M + 1) * M + r * M;
-#pragma unroll
-            for (int c = 0; c < M; ++c) w[k][c] = W[c];
-            w[k][M] = Nu[(g0 + j) * M + r];
+        const int kk = n - 1 - k;
+        if (kk >= 1) {
+            const CT* t = tape + (base + kk) * TP::SIZE;
+            load_vec<CT, MP4>(t + r * MP4, w[k]);
+            nu[k] = Nu[(base + kk) * M + r];
         }
     }
-    for (int i0 = 0; i0 < g.nsub; i0 += kPF) {
+    for (int i0 = 0; i0 < n; i0 += kPF) {
 #pragma unroll
         for (int k = 0; k < kPF; ++k) {
-            const int j = g.nsub - 1 - (i0 + k);
-            if (j >= 0) {
-                if (lane < M) Mu[(g0 + j) * M + lane] = (CT)mu;
-                if (j >= 1) {
-                    ms[warp][lane] = mu;
+            const int i = i0 + k;
+            const int kk = n - 1 - i;
+            if (kk >= 0) {
+                if (lane < M) Mu[(base + kk) * M + lane] = mu;
+                if (kk >= 1) {
+                    ms[warp][lane] = lane < M ? mu : (CT)0;
                     __syncwarp();
-                    ACC q0 = (ACC)w[k][M], q1 = (ACC)0, q2 = (ACC)0, q3 = (ACC)0;
-#pragma unroll
-                    for (int c = 0; c < M; ++c) {
-                        const ACC mc = ms[warp][c];
-                        switch (c & 3) {
-                            case 0: q0 = fma((ACC)w[k][c], mc, q0); break;
-                            case 1: q1 = fma((ACC)w[k][c], mc, q1); break;
-                            case 2: q2 = fma((ACC)w[k][c], mc, q2); break;
-                            default: q3 = fma((ACC)w[k][c], mc, q3); break;
-                        }
-                    }
+                    CT mv[MP4];
+                    load_vec<CT, MP4>(&ms[warp][0], mv);
+                    const CT mn = dot_rows<M, CT>(w[k], mv, nu[k]);
                     __syncwarp();
-                    if (lane < M) mu = (q0 + q1) + (q2 + q3);
-                    const int jn = j - kPF;
-                    if (jn >= 1) {
-                        const CT* W = PhiZ + (g0 + jn) * (M + 1) * M + r * M;
-#pragma unroll
-                        for (int c = 0; c < M; ++c) w[k][c] = W[c];
-                        w[k][M] = Nu[(g0 + jn) * M + r];
+                    mu = mn;
+                    const int kn = kk - kPF;
+                    if (kn >= 1) {
+                        const CT* t = tape + (base + kn) * TP::SIZE;
+                        load_vec<CT, MP4>(t + r * MP4, w[k]);
+                        nu[k] = Nu[(base + kn) * M + r];
                     }
                 }
             }

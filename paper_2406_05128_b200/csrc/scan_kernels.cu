@@ -148,20 +148,33 @@ cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO
     })
 }
 
+int tape_elems(int Mp) {
+    switch (Mp) {
+#define TVLP_TE(m) \
+    case m: return Tape<m>::SIZE;
+        TVLP_TE(2) TVLP_TE(4) TVLP_TE(6) TVLP_TE(8) TVLP_TE(12) TVLP_TE(16) TVLP_TE(22) TVLP_TE(24)
+        TVLP_TE(30)
+#undef TVLP_TE
+        default: return -1;
+    }
+}
+
 template <typename IO>
-cudaError_t launch_carry_fwd(int Mp, const IO* PhiZ, const IO* zi, IO* Xin, const ScanArgs& g,
+cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, const ScanArgs& g,
                              cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
-        k_carry_fwd<M_, double, IO><<<(unsigned)((g.B + 3) / 4), 128, 0, st>>>(PhiZ, zi, Xin, g);
+        k_carry_fwd<M_, IO><<<(unsigned)((g.B + 3) / 4), 128, 0, st>>>(tape, zi, Xin, g.B, g.nsub,
+                                                                       g.nsub);
         return cudaGetLastError();
     })
 }
 
 template <typename IO>
-cudaError_t launch_carry_bwd(int Mp, const IO* PhiZ, const IO* Nu, IO* Mu, const ScanArgs& g,
+cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, const ScanArgs& g,
                              cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
-        k_carry_bwd<M_, double, IO><<<(unsigned)((g.B + 3) / 4), 128, 0, st>>>(PhiZ, Nu, Mu, g);
+        k_carry_bwd<M_, IO><<<(unsigned)((g.B + 3) / 4), 128, 0, st>>>(tape, Nu, nullptr, Mu,
+                                                                       g.B, g.nsub, g.nsub);
         return cudaGetLastError();
     })
 }

@@ -22,11 +22,12 @@ enum Prec : int { kPrecF64Chains = 0, kPrecF32Chains = 1 };
 template <typename IO>
 cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO* PhiZ,
                          const ScanArgs& g, cudaStream_t st);
+int tape_elems(int Mp);  // carry-tape elements per sub-chunk
 template <typename IO>
-cudaError_t launch_carry_fwd(int Mp, const IO* PhiZ, const IO* zi, IO* Xin, const ScanArgs& g,
+cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, const ScanArgs& g,
                              cudaStream_t st);
 template <typename IO>
-cudaError_t launch_carry_bwd(int Mp, const IO* PhiZ, const IO* Nu, IO* Mu, const ScanArgs& g,
+cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, const ScanArgs& g,
                              cudaStream_t st);
 template <typename IO>
 cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO* Xin, IO* s,
