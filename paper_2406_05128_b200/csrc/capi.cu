@@ -113,6 +113,7 @@ ScanArgs scan_args(const Plan& p) {
 }
 
 int64_t carry_elems(const Plan& p) { return p.B * (int64_t)p.nsub * tape_elems(p.Mp); }
+inline int64_t mp4(const Plan& p) { return (p.Mp + 3) / 4 * 4; }
 
 // bump allocator over the caller's workspace (nullptr base = sizing pass)
 struct Carver {
@@ -218,7 +219,7 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     const int64_t nsc = p.B * p.nsub;
     Carver c(ws);
     IO* phiz = carry ? carry : static_cast<IO*>(c.take(carry_elems(p) * sz));
-    IO* xin = static_cast<IO*>(c.take(nsc * p.Mp * sz));
+    IO* xin = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
     const IO* e_p = static_cast<const IO*>(e);
     const IO* A_p = static_cast<const IO*>(A);
     const IO* zi_p = static_cast<const IO*>(zi);
@@ -274,8 +275,8 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     const int64_t nsc = p.B * p.nsub;
     Carver c(ws);
     IO* phiz_own = carry ? nullptr : static_cast<IO*>(c.take(carry_elems(p) * sz));
-    IO* nu = static_cast<IO*>(c.take(nsc * p.Mp * sz));
-    IO* mu = static_cast<IO*>(c.take(nsc * p.Mp * sz));
+    IO* nu = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
+    IO* mu = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
     const int nchunk = grad_a_chunks(p);
     IO* part = ti ? static_cast<IO*>(c.take(p.B * (int64_t)nchunk * p.Mp * sz)) : nullptr;
     IO* ga_p = (ti && p.Mp != p.M) ? static_cast<IO*>(c.take(p.B * p.Mp * sz)) : nullptr;

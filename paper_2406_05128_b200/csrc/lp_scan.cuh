@@ -350,13 +350,15 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
 }
 
 // ============================================================================
-// Carry kernels: one warp per sequence, lane r holds component r.  The chain
-// is latency-bound (one M x M mat-vec per sub-chunk): the lane's matrix row is
-// prefetched kPF sub-chunks ahead into registers with 16-byte loads, and the
-// state vector is broadcast through shared memory as float4/double2 reads, so
-// a step is ~M FMAs + M/4 vector loads on the critical path.
+// Carry kernels: one warp per segment of consecutive sub-chunks (a whole
+// sequence, or a group in the two-level scheme), lane r holds component r.
+// The chain is latency-bound (one M x M mat-vec per sub-chunk): the tape rows
+// it needs stream into a kCS-deep shared-memory ring by bulk TMA (one copy per
+// sub-chunk, issued kCS steps ahead), the lane's matrix row and the broadcast
+// state are read as 16-byte vectors, and the dot product runs on 4 partial
+// accumulators.
 // ============================================================================
-constexpr int kPF = 4;
+constexpr int kCS = 16;  // carry ring depth (sub-chunks in flight)
 
 template <typename CT, int N>
 __device__ __forceinline__ void load_vec(const CT* p, CT (&v)[N]) {
@@ -396,17 +398,29 @@ __device__ __forceinline__ CT dot_rows(const CT (&w)[Tape<M>::MP4], const CT (&x
     return (q0 + q1) + (q2 + q3);
 }
 
+template <int M, typename CT>
+struct CarrySmem {
+    static constexpr int MP4 = Tape<M>::MP4;
+    static constexpr int STAGE = (M + 1) * MP4 * (int)sizeof(CT);  // z+R (fwd) or W+nu (bwd)
+    static constexpr int WARP = kCS * STAGE + 32 * (int)sizeof(CT) + kCS * 8;
+    static constexpr int BYTES = 4 * WARP;
+};
+
 // Forward carry over segments: segment s = (sequence b, first sub-chunk k0,
-// count n); x(k0) = x0[s] (or zi / zero), x(k+1) = Phi_k x(k) + z_k.  Writes
-// Xin[k] for every sub-chunk of the segment.
+// count n); x(k0) = x0[s] (or zero), x(k+1) = Phi_k x(k) + z_k.  Writes
+// Xin[k] (row stride MP4) for every sub-chunk of the segment.
 template <int M, typename CT>
 __global__ void __launch_bounds__(128)
-k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, CT* __restrict__ Xin,
-            int64_t nseg, int seglen, int nsub) {
+k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_stride,
+            CT* __restrict__ Xin, int64_t nseg, int seglen, int nsub) {
     using TP = Tape<M>;
+    using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
-    __shared__ __align__(16) CT xs[4][32];
+    extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* wb = smem + warp * SM::WARP;
+    CT* xs = reinterpret_cast<CT*>(wb + kCS * SM::STAGE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wb + kCS * SM::STAGE + 32 * sizeof(CT));
     const int64_t sidx = (int64_t)blockIdx.x * 4 + warp;
     if (sidx >= nseg) return;
     const int nper = (nsub + seglen - 1) / seglen;  // segments per sequence
@@ -415,53 +429,55 @@ k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, CT* __restri
     const int n = min(seglen, nsub - k0);
     const int64_t base = b * nsub + k0;
     const int r = lane < M ? lane : 0;
-    CT x = (x0 != nullptr && lane < M) ? x0[sidx * M + lane] : (CT)0;
-    CT w[kPF][MP4];
-    CT z[kPF];
-#pragma unroll
-    for (int k = 0; k < kPF; ++k) {
-        if (k < n - 1) {
-            const CT* t = tape + (base + k) * TP::SIZE;
-            load_vec<CT, MP4>(t + (TP::R_ROW + r) * MP4, w[k]);
-            z[k] = t[TP::Z_ROW * MP4 + r];
-        }
+    if (lane == 0) {
+        for (int i = 0; i < kCS; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
     }
-    for (int i0 = 0; i0 < n; i0 += kPF) {
-#pragma unroll
-        for (int k = 0; k < kPF; ++k) {
-            const int i = i0 + k;
-            if (i < n) {
-                if (lane < M) Xin[(base + i) * M + lane] = x;
-                if (i < n - 1) {
-                    xs[warp][lane] = lane < M ? x : (CT)0;
-                    __syncwarp();
-                    CT xv[MP4];
-                    load_vec<CT, MP4>(&xs[warp][0], xv);
-                    const CT xn = dot_rows<M, CT>(w[k], xv, z[k]);
-                    __syncwarp();
-                    x = xn;
-                    const int in = i + kPF;
-                    if (in < n - 1) {
-                        const CT* t = tape + (base + in) * TP::SIZE;
-                        load_vec<CT, MP4>(t + (TP::R_ROW + r) * MP4, w[k]);
-                        z[k] = t[TP::Z_ROW * MP4 + r];
-                    }
-                }
-            }
+    __syncwarp();
+    auto issue = [&](int i) {
+        if (lane == 0 && i < n - 1) {
+            const int st = i % kCS;
+            mbar_arrive_expect_tx(&bars[st], SM::STAGE);
+            tma_load_1d(wb + st * SM::STAGE, tape + (base + i) * TP::SIZE + TP::Z_ROW * MP4,
+                        SM::STAGE, &bars[st]);
         }
+    };
+    for (int i = 0; i < kCS; ++i) issue(i);
+    CT x = (x0 != nullptr && lane < M) ? x0[sidx * x0_stride + lane] : (CT)0;
+    for (int i = 0; i < n; ++i) {
+        if (lane < M) Xin[(base + i) * MP4 + lane] = x;
+        if (i == n - 1) break;
+        const int st = i % kCS;
+        xs[lane] = lane < M ? x : (CT)0;
+        mbar_wait(&bars[st], (uint32_t)((i / kCS) & 1));
+        __syncwarp();
+        const CT* sg = reinterpret_cast<const CT*>(wb + st * SM::STAGE);
+        CT w[MP4], xv[MP4];
+        load_vec<CT, MP4>(sg + (1 + r) * MP4, w);
+        load_vec<CT, MP4>(xs, xv);
+        const CT xn = dot_rows<M, CT>(w, xv, sg[r]);
+        __syncwarp();
+        x = xn;
+        fence_proxy_async();
+        issue(i + kCS);
     }
 }
 
 // Adjoint carry over segments (right to left): mu(k_last) = m0[s] (or zero),
 // mu(k-1) = Phi_k^T mu(k) + nu_k.  Writes Mu[k] = carry into sub-chunk k.
+// Nu/Mu rows have stride MP4.
 template <int M, typename CT>
 __global__ void __launch_bounds__(128)
 k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __restrict__ m0,
-            CT* __restrict__ Mu, int64_t nseg, int seglen, int nsub) {
+            int m0_stride, CT* __restrict__ Mu, int64_t nseg, int seglen, int nsub) {
     using TP = Tape<M>;
+    using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
-    __shared__ __align__(16) CT ms[4][32];
+    extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* wb = smem + warp * SM::WARP;
+    CT* ms = reinterpret_cast<CT*>(wb + kCS * SM::STAGE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wb + kCS * SM::STAGE + 32 * sizeof(CT));
     const int64_t sidx = (int64_t)blockIdx.x * 4 + warp;
     if (sidx >= nseg) return;
     const int nper = (nsub + seglen - 1) / seglen;
@@ -470,43 +486,42 @@ k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __
     const int n = min(seglen, nsub - k0);
     const int64_t base = b * nsub + k0;
     const int r = lane < M ? lane : 0;
-    CT mu = (m0 != nullptr && lane < M) ? m0[sidx * M + lane] : (CT)0;
-    CT w[kPF][MP4];
-    CT nu[kPF];
-    // step i handles sub-chunk k = n-1-i (it needs Phi_k, nu_k for k >= 1)
-#pragma unroll
-    for (int k = 0; k < kPF; ++k) {
-        const int kk = n - 1 - k;
-        if (kk >= 1) {
-            const CT* t = tape + (base + kk) * TP::SIZE;
-            load_vec<CT, MP4>(t + r * MP4, w[k]);
-            nu[k] = Nu[(base + kk) * M + r];
-        }
+    if (lane == 0) {
+        for (int i = 0; i < kCS; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
     }
-    for (int i0 = 0; i0 < n; i0 += kPF) {
-#pragma unroll
-        for (int k = 0; k < kPF; ++k) {
-            const int i = i0 + k;
-            const int kk = n - 1 - i;
-            if (kk >= 0) {
-                if (lane < M) Mu[(base + kk) * M + lane] = mu;
-                if (kk >= 1) {
-                    ms[warp][lane] = lane < M ? mu : (CT)0;
-                    __syncwarp();
-                    CT mv[MP4];
-                    load_vec<CT, MP4>(&ms[warp][0], mv);
-                    const CT mn = dot_rows<M, CT>(w[k], mv, nu[k]);
-                    __syncwarp();
-                    mu = mn;
-                    const int kn = kk - kPF;
-                    if (kn >= 1) {
-                        const CT* t = tape + (base + kn) * TP::SIZE;
-                        load_vec<CT, MP4>(t + r * MP4, w[k]);
-                        nu[k] = Nu[(base + kn) * M + r];
-                    }
-                }
-            }
+    __syncwarp();
+    // step i handles sub-chunk kk = n-1-i and needs W rows of Phi_kk and nu_kk
+    auto issue = [&](int i) {
+        const int kk = n - 1 - i;
+        if (lane == 0 && kk >= 1) {
+            const int st = i % kCS;
+            unsigned char* dst = wb + st * SM::STAGE;
+            mbar_arrive_expect_tx(&bars[st], SM::STAGE);
+            tma_load_1d(dst, tape + (base + kk) * TP::SIZE, M * MP4 * sizeof(CT), &bars[st]);
+            tma_load_1d(dst + M * MP4 * sizeof(CT), Nu + (base + kk) * MP4, MP4 * sizeof(CT),
+                        &bars[st]);
         }
+    };
+    for (int i = 0; i < kCS; ++i) issue(i);
+    CT mu = (m0 != nullptr && lane < M) ? m0[sidx * m0_stride + lane] : (CT)0;
+    for (int i = 0; i < n; ++i) {
+        const int kk = n - 1 - i;
+        if (lane < M) Mu[(base + kk) * MP4 + lane] = mu;
+        if (kk == 0) break;
+        const int st = i % kCS;
+        ms[lane] = lane < M ? mu : (CT)0;
+        mbar_wait(&bars[st], (uint32_t)((i / kCS) & 1));
+        __syncwarp();
+        const CT* sg = reinterpret_cast<const CT*>(wb + st * SM::STAGE);
+        CT w[MP4], mv[MP4];
+        load_vec<CT, MP4>(sg + r * MP4, w);
+        load_vec<CT, MP4>(ms, mv);
+        const CT mn = dot_rows<M, CT>(w, mv, sg[M * MP4 + r]);
+        __syncwarp();
+        mu = mn;
+        fence_proxy_async();
+        issue(i + kCS);
     }
 }
 
@@ -593,7 +608,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 #pragma unroll
     for (int p = 0; p < MR; ++p) R[p] = (IO)0;
 #pragma unroll
-    for (int i = 0; i < M; ++i) R[MR - 1 - i] = active ? Xin[gid * M + i] : (IO)0;
+    for (int i = 0; i < M; ++i) R[MR - 1 - i] = active ? Xin[gid * Tape<M>::MP4 + i] : (IO)0;
     bool finite = true;
 
     for (int kb = 0; kb < nwin; kb += WPB) {
@@ -712,7 +727,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     }
     IO lam[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) lam[i] = (MODE == 1 && active) ? Mu[gid * M + i] : (IO)0;
+    for (int i = 0; i < M; ++i) lam[i] = (MODE == 1 && active) ? Mu[gid * Tape<M>::MP4 + i] : (IO)0;
 
     for (int k = 0; k < nwin; ++k) {
         const int st = k % kLaneStages;
@@ -759,7 +774,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     if (MODE == 1 && lane == 0) bulk_wait<0>();
     if (MODE == 0 && active) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) Nu[gid * M + i] = lam[i];
+        for (int i = 0; i < M; ++i) Nu[gid * Tape<M>::MP4 + i] = lam[i];
     }
 }
 

@@ -159,13 +159,35 @@ int tape_elems(int Mp) {
     }
 }
 
+template <int M, typename IO>
+cudaError_t carry_fwd_impl(const IO* tape, const IO* x0, int x0s, IO* Xin, int64_t nseg,
+                           int seglen, int nsub, cudaStream_t st) {
+    using SM = CarrySmem<M, IO>;
+    auto k = k_carry_fwd<M, IO>;
+    cudaError_t err = ensure_smem(k, SM::BYTES);
+    if (err != cudaSuccess) return err;
+    k<<<(unsigned)((nseg + 3) / 4), 128, SM::BYTES, st>>>(tape, x0, x0s, Xin, nseg, seglen,
+                                                           nsub);
+    return cudaGetLastError();
+}
+
+template <int M, typename IO>
+cudaError_t carry_bwd_impl(const IO* tape, const IO* Nu, const IO* m0, int m0s, IO* Mu,
+                           int64_t nseg, int seglen, int nsub, cudaStream_t st) {
+    using SM = CarrySmem<M, IO>;
+    auto k = k_carry_bwd<M, IO>;
+    cudaError_t err = ensure_smem(k, SM::BYTES);
+    if (err != cudaSuccess) return err;
+    k<<<(unsigned)((nseg + 3) / 4), 128, SM::BYTES, st>>>(tape, Nu, m0, m0s, Mu, nseg,
+                                                           seglen, nsub);
+    return cudaGetLastError();
+}
+
 template <typename IO>
 cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, const ScanArgs& g,
                              cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
-        k_carry_fwd<M_, IO><<<(unsigned)((g.B + 3) / 4), 128, 0, st>>>(tape, zi, Xin, g.B, g.nsub,
-                                                                       g.nsub);
-        return cudaGetLastError();
+        return carry_fwd_impl<M_, IO>(tape, zi, Mp, Xin, g.B, g.nsub, g.nsub, st);
     })
 }
 
@@ -173,9 +195,7 @@ template <typename IO>
 cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, const ScanArgs& g,
                              cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
-        k_carry_bwd<M_, IO><<<(unsigned)((g.B + 3) / 4), 128, 0, st>>>(tape, Nu, nullptr, Mu,
-                                                                       g.B, g.nsub, g.nsub);
-        return cudaGetLastError();
+        return carry_bwd_impl<M_, IO>(tape, Nu, nullptr, 0, Mu, g.B, g.nsub, g.nsub, st);
     })
 }
 
