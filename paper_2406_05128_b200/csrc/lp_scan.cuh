@@ -288,12 +288,18 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
                            (cy < M && M - 1 - p == cy) ? 1.f : 0.f);
     const float mx = (cx == M) ? 1.f : 0.f, my = (cy == M) ? 1.f : 0.f;
 
+    // excitation (read by the zero-state chain only): lane q of a half holds
+    // e[w*WR + q] and e[w*WR + 16 + q] of window w, loaded one window ahead;
+    // step u takes it with a 16-lane shuffle (off the recursion's chain).
+    static_assert(WR <= 32, "window fits two registers per lane");
+    auto eload = [&](int w, int u) { const int t = w * WR + u; return (u < WR && t < len) ? __ldg(eb + t) : 0.f; };
+    float ec0 = eload(0, q), ec1 = eload(0, 16 + q);
     for (int k = 0; k < nwin; ++k) {
         const int st = k % NSTB;
+        const float en0 = eload(k + 1, q), en1 = eload(k + 1, 16 + q);
         if (!TI) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
         const int rows = min(WR, len - k * WR);
         const float* Ar = reinterpret_cast<const float*>(stage_ptr(st));
-        const float* ek = eb + k * WR;  // excitation (zero-state chain only), L1/L2 broadcast
 #pragma unroll
         for (int u = 0; u < WR; ++u) {
             if (u < rows) {  // warp-uniform: only the last window can be short
@@ -304,7 +310,7 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
                 } else {
                     load_row_at<float, M>(Ar + u * M, a, u * M * 4);
                 }
-                const float ev = __ldg(ek + u);
+                const float ev = __shfl_sync(0xffffffffu, u < 16 ? ec0 : ec1, u & 15, 16);
                 const float2 ein = make_float2(ev * mx, ev * my);
                 float2 p0 = make_float2(0.f, 0.f), p1 = p0, p2 = p0, p3 = p0;
 #pragma unroll
@@ -327,6 +333,8 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
         __syncwarp();
         fence_proxy_async();
         issue(k + NSTB);
+        ec0 = en0;
+        ec1 = en1;
     }
 
     // final state x[i] = s(t1 - i) = R[(len-1-i) mod M]
@@ -358,7 +366,8 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
 // state are read as 16-byte vectors, and the dot product runs on 4 partial
 // accumulators.
 // ============================================================================
-constexpr int kCS = 16;  // carry ring depth (sub-chunks in flight)
+constexpr int kCB = 4;   // sub-chunks per carry ring stage (one wait / copy per stage)
+constexpr int kCS = 4;   // carry ring stages (kCB*kCS sub-chunks in flight)
 
 template <typename CT, int N>
 __device__ __forceinline__ void load_vec(const CT* p, CT (&v)[N]) {
@@ -401,27 +410,28 @@ __device__ __forceinline__ CT dot_rows(const CT (&w)[Tape<M>::MP4], const CT (&x
 template <int M, typename CT>
 struct CarrySmem {
     static constexpr int MP4 = Tape<M>::MP4;
-    static constexpr int STAGE = (M + 1) * MP4 * (int)sizeof(CT);  // z+R (fwd) or W+nu (bwd)
-    static constexpr int WARP = kCS * STAGE + 32 * (int)sizeof(CT) + kCS * 8;
-    static constexpr int BYTES = 4 * WARP;
+    static constexpr int SUB = Tape<M>::SIZE * (int)sizeof(CT);  // one sub-chunk's tape
+    static constexpr int STAGE = kCB * SUB;
+    static constexpr int NU = kCB * MP4 * (int)sizeof(CT);        // bwd: nu of the stage
+    static constexpr int BYTES = kCS * (STAGE + NU) + 32 * (int)sizeof(CT) + kCS * 8;
 };
 
 // Forward carry over segments: segment s = (sequence b, first sub-chunk k0,
 // count n); x(k0) = x0[s] (or zero), x(k+1) = Phi_k x(k) + z_k.  Writes
-// Xin[k] (row stride MP4) for every sub-chunk of the segment.
+// Xin[k] (row stride MP4) for every sub-chunk of the segment.  One warp per
+// CTA; whole tapes of kCB consecutive sub-chunks arrive per bulk copy.
 template <int M, typename CT>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(32)
 k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_stride,
             CT* __restrict__ Xin, int64_t nseg, int seglen, int nsub) {
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
     extern __shared__ __align__(128) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char* wb = smem + warp * SM::WARP;
-    CT* xs = reinterpret_cast<CT*>(wb + kCS * SM::STAGE);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wb + kCS * SM::STAGE + 32 * sizeof(CT));
-    const int64_t sidx = (int64_t)blockIdx.x * 4 + warp;
+    const int lane = threadIdx.x;
+    CT* xs = reinterpret_cast<CT*>(smem + kCS * (SM::STAGE + SM::NU));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kCS * (SM::STAGE + SM::NU) + 32 * sizeof(CT));
+    const int64_t sidx = blockIdx.x;
     if (sidx >= nseg) return;
     const int nper = (nsub + seglen - 1) / seglen;  // segments per sequence
     const int64_t b = sidx / nper;
@@ -429,56 +439,66 @@ k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_strid
     const int n = min(seglen, nsub - k0);
     const int64_t base = b * nsub + k0;
     const int r = lane < M ? lane : 0;
+    const int nsteps = n - 1;  // mat-vecs needed
+    const int nst = (nsteps + kCB - 1) / kCB;
     if (lane == 0) {
         for (int i = 0; i < kCS; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     __syncwarp();
-    auto issue = [&](int i) {
-        if (lane == 0 && i < n - 1) {
-            const int st = i % kCS;
-            mbar_arrive_expect_tx(&bars[st], SM::STAGE);
-            tma_load_1d(wb + st * SM::STAGE, tape + (base + i) * TP::SIZE + TP::Z_ROW * MP4,
-                        SM::STAGE, &bars[st]);
+    auto issue = [&](int sg) {  // stage sg: sub-chunks sg*kCB .. +kCB-1
+        if (lane == 0 && sg < nst) {
+            const int st = sg % kCS;
+            const int cnt = min(kCB, nsteps - sg * kCB);
+            mbar_arrive_expect_tx(&bars[st], cnt * SM::SUB);
+            tma_load_1d(smem + st * (SM::STAGE + SM::NU), tape + (base + sg * kCB) * TP::SIZE,
+                        cnt * SM::SUB, &bars[st]);
         }
     };
     for (int i = 0; i < kCS; ++i) issue(i);
     CT x = (x0 != nullptr && lane < M) ? x0[sidx * x0_stride + lane] : (CT)0;
-    for (int i = 0; i < n; ++i) {
-        if (lane < M) Xin[(base + i) * MP4 + lane] = x;
-        if (i == n - 1) break;
-        const int st = i % kCS;
-        xs[lane] = lane < M ? x : (CT)0;
-        mbar_wait(&bars[st], (uint32_t)((i / kCS) & 1));
-        __syncwarp();
-        const CT* sg = reinterpret_cast<const CT*>(wb + st * SM::STAGE);
-        CT w[MP4], xv[MP4];
-        load_vec<CT, MP4>(sg + (1 + r) * MP4, w);
-        load_vec<CT, MP4>(xs, xv);
-        const CT xn = dot_rows<M, CT>(w, xv, sg[r]);
-        __syncwarp();
-        x = xn;
+    for (int sg = 0; sg < nst; ++sg) {
+        const int st = sg % kCS;
+        mbar_wait(&bars[st], (uint32_t)((sg / kCS) & 1));
+        const CT* sgb = reinterpret_cast<const CT*>(smem + st * (SM::STAGE + SM::NU));
+#pragma unroll
+        for (int u = 0; u < kCB; ++u) {
+            const int i = sg * kCB + u;
+            if (i < nsteps) {
+                if (lane < M) Xin[(base + i) * MP4 + lane] = x;
+                xs[lane] = lane < M ? x : (CT)0;
+                __syncwarp();
+                const CT* tp = sgb + u * TP::SIZE;
+                CT w[MP4], xv[MP4];
+                load_vec<CT, MP4>(tp + (TP::R_ROW + r) * MP4, w);
+                load_vec<CT, MP4>(xs, xv);
+                const CT xn = dot_rows<M, CT>(w, xv, tp[TP::Z_ROW * MP4 + r]);
+                __syncwarp();
+                x = xn;
+            }
+        }
         fence_proxy_async();
-        issue(i + kCS);
+        __syncwarp();
+        issue(sg + kCS);
     }
+    if (lane < M) Xin[(base + n - 1) * MP4 + lane] = x;
 }
 
 // Adjoint carry over segments (right to left): mu(k_last) = m0[s] (or zero),
 // mu(k-1) = Phi_k^T mu(k) + nu_k.  Writes Mu[k] = carry into sub-chunk k.
 // Nu/Mu rows have stride MP4.
 template <int M, typename CT>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(32)
 k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __restrict__ m0,
             int m0_stride, CT* __restrict__ Mu, int64_t nseg, int seglen, int nsub) {
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
     extern __shared__ __align__(128) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char* wb = smem + warp * SM::WARP;
-    CT* ms = reinterpret_cast<CT*>(wb + kCS * SM::STAGE);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wb + kCS * SM::STAGE + 32 * sizeof(CT));
-    const int64_t sidx = (int64_t)blockIdx.x * 4 + warp;
+    const int lane = threadIdx.x;
+    CT* ms = reinterpret_cast<CT*>(smem + kCS * (SM::STAGE + SM::NU));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kCS * (SM::STAGE + SM::NU) + 32 * sizeof(CT));
+    const int64_t sidx = blockIdx.x;
     if (sidx >= nseg) return;
     const int nper = (nsub + seglen - 1) / seglen;
     const int64_t b = sidx / nper;
@@ -486,43 +506,59 @@ k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __
     const int n = min(seglen, nsub - k0);
     const int64_t base = b * nsub + k0;
     const int r = lane < M ? lane : 0;
+    // mat-vec i (i = 0..n-2) uses sub-chunk kk = n-1-i; stage sg holds
+    // sub-chunks kk = n-1-sg*kCB-u for u = 0..kCB-1 (descending), i.e. the
+    // contiguous tape range [hi-cnt+1, hi] with hi = n-1-sg*kCB.
+    const int nsteps = n - 1;
+    const int nst = (nsteps + kCB - 1) / kCB;
     if (lane == 0) {
         for (int i = 0; i < kCS; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     __syncwarp();
-    // step i handles sub-chunk kk = n-1-i and needs W rows of Phi_kk and nu_kk
-    auto issue = [&](int i) {
-        const int kk = n - 1 - i;
-        if (lane == 0 && kk >= 1) {
-            const int st = i % kCS;
-            unsigned char* dst = wb + st * SM::STAGE;
-            mbar_arrive_expect_tx(&bars[st], SM::STAGE);
-            tma_load_1d(dst, tape + (base + kk) * TP::SIZE, M * MP4 * sizeof(CT), &bars[st]);
-            tma_load_1d(dst + M * MP4 * sizeof(CT), Nu + (base + kk) * MP4, MP4 * sizeof(CT),
+    auto issue = [&](int sg) {
+        if (lane == 0 && sg < nst) {
+            const int st = sg % kCS;
+            const int cnt = min(kCB, nsteps - sg * kCB);
+            const int lo = n - sg * kCB - cnt;  // lowest sub-chunk of the stage
+            unsigned char* dst = smem + st * (SM::STAGE + SM::NU);
+            mbar_arrive_expect_tx(&bars[st], cnt * (SM::SUB + MP4 * (int)sizeof(CT)));
+            tma_load_1d(dst, tape + (base + lo) * TP::SIZE, cnt * SM::SUB, &bars[st]);
+            tma_load_1d(dst + SM::STAGE, Nu + (base + lo) * MP4, cnt * MP4 * sizeof(CT),
                         &bars[st]);
         }
     };
     for (int i = 0; i < kCS; ++i) issue(i);
     CT mu = (m0 != nullptr && lane < M) ? m0[sidx * m0_stride + lane] : (CT)0;
-    for (int i = 0; i < n; ++i) {
-        const int kk = n - 1 - i;
-        if (lane < M) Mu[(base + kk) * MP4 + lane] = mu;
-        if (kk == 0) break;
-        const int st = i % kCS;
-        ms[lane] = lane < M ? mu : (CT)0;
-        mbar_wait(&bars[st], (uint32_t)((i / kCS) & 1));
-        __syncwarp();
-        const CT* sg = reinterpret_cast<const CT*>(wb + st * SM::STAGE);
-        CT w[MP4], mv[MP4];
-        load_vec<CT, MP4>(sg + r * MP4, w);
-        load_vec<CT, MP4>(ms, mv);
-        const CT mn = dot_rows<M, CT>(w, mv, sg[M * MP4 + r]);
-        __syncwarp();
-        mu = mn;
+    for (int sg = 0; sg < nst; ++sg) {
+        const int st = sg % kCS;
+        mbar_wait(&bars[st], (uint32_t)((sg / kCS) & 1));
+        const unsigned char* dst = smem + st * (SM::STAGE + SM::NU);
+        const int cnt = min(kCB, nsteps - sg * kCB);
+#pragma unroll
+        for (int u = 0; u < kCB; ++u) {
+            const int i = sg * kCB + u;
+            if (i < nsteps) {
+                const int kk = n - 1 - i;
+                if (lane < M) Mu[(base + kk) * MP4 + lane] = mu;
+                ms[lane] = lane < M ? mu : (CT)0;
+                __syncwarp();
+                const int slot = cnt - 1 - u;  // position of kk inside the stage
+                const CT* tp = reinterpret_cast<const CT*>(dst) + slot * TP::SIZE;
+                const CT* nu = reinterpret_cast<const CT*>(dst + SM::STAGE) + slot * MP4;
+                CT w[MP4], mv[MP4];
+                load_vec<CT, MP4>(tp + r * MP4, w);
+                load_vec<CT, MP4>(ms, mv);
+                const CT mn = dot_rows<M, CT>(w, mv, nu[r]);
+                __syncwarp();
+                mu = mn;
+            }
+        }
         fence_proxy_async();
-        issue(i + kCS);
+        __syncwarp();
+        issue(sg + kCS);
     }
+    if (lane < M) Mu[base * MP4 + lane] = mu;
 }
 
 // ============================================================================

@@ -166,8 +166,7 @@ cudaError_t carry_fwd_impl(const IO* tape, const IO* x0, int x0s, IO* Xin, int64
     auto k = k_carry_fwd<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
-    k<<<(unsigned)((nseg + 3) / 4), 128, SM::BYTES, st>>>(tape, x0, x0s, Xin, nseg, seglen,
-                                                           nsub);
+    k<<<(unsigned)nseg, 32, SM::BYTES, st>>>(tape, x0, x0s, Xin, nseg, seglen, nsub);
     return cudaGetLastError();
 }
 
@@ -178,8 +177,7 @@ cudaError_t carry_bwd_impl(const IO* tape, const IO* Nu, const IO* m0, int m0s, 
     auto k = k_carry_bwd<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
-    k<<<(unsigned)((nseg + 3) / 4), 128, SM::BYTES, st>>>(tape, Nu, m0, m0s, Mu, nseg,
-                                                           seglen, nsub);
+    k<<<(unsigned)nseg, 32, SM::BYTES, st>>>(tape, Nu, m0, m0s, Mu, nseg, seglen, nsub);
     return cudaGetLastError();
 }
 
