@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libtvlp_b200.so")
 
 F32, F64 = 0, 1
-CARRY_F64, CARRY_F32 = 0, 1
+CARRY_F64, CARRY_F32, CARRY_AUTO = 0, 1, 2
 OP_FWD_TV, OP_BWD_TV, OP_FWD_TI, OP_BWD_TI, OP_FW_FWD, OP_FW_BWD = range(6)
 
 _lib = None

@@ -220,6 +220,10 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     Carver c(ws);
     IO* phiz = carry ? carry : static_cast<IO*>(c.take(carry_elems(p) * sz));
     IO* xin = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
+    // precision "auto": fp32 chains + boundary-defect check + refinement
+    const bool refine = prec == kPrecAuto && sizeof(IO) == 4;
+    IO* xend = refine ? static_cast<IO*>(c.take(nsc * mp4(p) * sz)) : nullptr;
+    int* flags = refine ? static_cast<int*>(c.take(p.B * sizeof(int))) : nullptr;
     const IO* e_p = static_cast<const IO*>(e);
     const IO* A_p = static_cast<const IO*>(A);
     const IO* zi_p = static_cast<const IO*>(zi);
@@ -251,7 +255,13 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     }
     TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, e_p, A_p, phiz, g, st)));
     TVLP_RUN("carry_fwd", 1, st, (launch_carry_fwd<IO>(p.Mp, phiz, zi_p, xin, g, st)));
-    TVLP_RUN("apply_fwd", 1, st, (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, g, st)));
+    TVLP_RUN("apply_fwd", 1, st,
+             (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, xend, nullptr, g, st)));
+    if (refine) {
+        TVLP_RUN("refine_fwd", 1, st, (launch_refine<IO>(p.Mp, true, phiz, xin, xend, flags, g, st)));
+        TVLP_RUN("apply_fwd_refined", 1, st,
+                 (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nullptr, nullptr, flags, g, st)));
+    }
     if (packed) TVLP_CK(unpack<IO>(ps, s, p.B, p.T, 1, p.Tp, 1, st));
     return TVLP_OK;
 }
@@ -277,6 +287,9 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     IO* phiz_own = carry ? nullptr : static_cast<IO*>(c.take(carry_elems(p) * sz));
     IO* nu = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
     IO* mu = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
+    const bool refine = prec == kPrecAuto && sizeof(IO) == 4;
+    IO* kout = refine ? static_cast<IO*>(c.take(nsc * mp4(p) * sz)) : nullptr;
+    int* flags = refine ? static_cast<int*>(c.take(p.B * sizeof(int))) : nullptr;
     const int nchunk = grad_a_chunks(p);
     IO* part = ti ? static_cast<IO*>(c.take(p.B * (int64_t)nchunk * p.Mp * sz)) : nullptr;
     IO* ga_p = (ti && p.Mp != p.M) ? static_cast<IO*>(c.take(p.B * p.Mp * sz)) : nullptr;
@@ -324,9 +337,16 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
         TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, s_p, A_p, phiz_own, g, st)));
         phiz = phiz_own;
     }
-    TVLP_RUN("adjoint_zs", 1, st, (launch_adjoint<IO>(p.Mp, ti, 0, gs_p, A_p, nullptr, nu, nullptr, g, st)));
+    TVLP_RUN("adjoint_zs", 1, st,
+             (launch_adjoint<IO>(p.Mp, ti, 0, gs_p, A_p, nullptr, nu, nullptr, nullptr, g, st)));
     TVLP_RUN("carry_bwd", 1, st, (launch_carry_bwd<IO>(p.Mp, phiz, nu, mu, g, st)));
-    TVLP_RUN("adjoint_apply", 1, st, (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, g, st)));
+    TVLP_RUN("adjoint_apply", 1, st,
+             (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, kout, ge_p, nullptr, g, st)));
+    if (refine) {
+        TVLP_RUN("refine_bwd", 1, st, (launch_refine<IO>(p.Mp, false, phiz, mu, kout, flags, g, st)));
+        TVLP_RUN("adjoint_apply_refined", 1, st,
+                 (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, flags, g, st)));
+    }
     if (ti) {
         IO* ga_out = ga_p ? ga_p : static_cast<IO*>(gA);
         TVLP_RUN("grad_a", 2, st, (launch_grad_a<IO>(p.Mp, ge_p, s_p, zi_p, part, ga_out, p.B, p.Tp, nchunk, st)));

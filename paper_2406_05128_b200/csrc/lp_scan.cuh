@@ -600,7 +600,8 @@ struct LaneMaps {
 template <typename IO, int M, bool TI>
 __global__ void __launch_bounds__(32)
 k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
-            const IO* __restrict__ Xin, int* __restrict__ flag, ScanArgs g) {
+            const IO* __restrict__ Xin, int* __restrict__ flag, IO* __restrict__ Xend,
+            const int* __restrict__ only, ScanArgs g) {
     using S = LaneSmem<IO, M, TI>;
     constexpr int W = S::W;
     constexpr int MR = (M + W - 1) / W * W;
@@ -613,6 +614,9 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
     const int64_t gid = (int64_t)g0 + lane;
     const bool active = gid < nsc;
     const int nwin = g.Ls / W;
+    // refinement pass: only warps holding a flagged sequence recompute (the
+    // others would reproduce their first-pass outputs bit-for-bit)
+    if (only != nullptr && !__any_sync(0xffffffffu, active && only[gid / g.nsub] != 0)) return;
 
     if (lane == 0) {
         prefetch_tmap(&maps.A);
@@ -711,6 +715,15 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
         const unsigned bad = __ballot_sync(0xffffffffu, active && !finite);
         if (bad && lane == 0) atomicOr(flag, 1);
     }
+    if (Xend != nullptr && active) {
+        // end state x[i] = s(t1 - i): the defect check compares it with the
+        // carry's x_in of the next sub-chunk
+        IO tmp[MR];
+#pragma unroll
+        for (int p = 0; p < MR; ++p) tmp[p] = R[p];
+        const int last = (g.Ls - 1) % MR;
+        for (int i = 0; i < M; ++i) Xend[gid * Tape<M>::MP4 + i] = tmp[(last - i + MR) % MR];
+    }
 }
 
 // ---------------------------------------------------------------- adjoint
@@ -721,7 +734,8 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 template <typename IO, int M, bool TI, int MODE>
 __global__ void __launch_bounds__(32)
 k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
-          const IO* __restrict__ Mu, IO* __restrict__ Nu, ScanArgs g) {
+          const IO* __restrict__ Mu, IO* __restrict__ Nu, const int* __restrict__ only,
+          ScanArgs g) {
     using S = LaneSmem<IO, M, TI>;
     constexpr int W = S::W;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -732,6 +746,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     const int64_t gid = (int64_t)g0 + lane;
     const bool active = gid < nsc;
     const int nwin = g.Ls / W;
+    if (only != nullptr && !__any_sync(0xffffffffu, active && only[gid / g.nsub] != 0)) return;
 
     if (lane == 0) {
         prefetch_tmap(&maps.A);
@@ -808,9 +823,114 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
         issue(k + kLaneStages);
     }
     if (MODE == 1 && lane == 0) bulk_wait<0>();
-    if (MODE == 0 && active) {
+    // MODE 0: Nu = zero-state carry-out.  MODE 1: Nu (if given) = the carry-out
+    // C(t0)^T lambda(t0) obtained from Mu, which the defect check compares with
+    // the carry chain's Mu of the previous sub-chunk.
+    if (active && Nu != nullptr) {
 #pragma unroll
         for (int i = 0; i < M; ++i) Nu[gid * Tape<M>::MP4 + i] = lam[i];
+    }
+}
+
+// ---------------------------------------------------------------- refinement
+// A-posteriori check of the fp32-chain carries (precision "auto").  For a
+// sequence, d_j = Xend_j - Xin_{j+1} is the boundary defect between the state
+// the apply pass actually reached at the end of sub-chunk j (a plain fp32
+// recursion from Xin_j) and the carry's prediction for sub-chunk j+1.  With
+// exact carries d_j is fp32 rounding noise.  If max|d| > tau * max|x| the
+// carries are corrected by e_{j+1} = Phi_j e_j + d_j (e_0 = 0, Xin += e): the
+// correction is linear and small, so the fp32 Phi_j (relative error ~1e-5
+// after cancellation) contracts the error by ~1e-4 per pass.
+constexpr float kDefectTol = 2e-5f;
+
+template <typename CT>
+__device__ __forceinline__ CT warp_max(CT v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <int M, typename CT>
+__global__ void __launch_bounds__(32)
+k_refine_fwd(const CT* __restrict__ tape, CT* __restrict__ Xin, const CT* __restrict__ Xend,
+             int* __restrict__ flags, int nsub, int64_t B) {
+    using TP = Tape<M>;
+    constexpr int MP4 = TP::MP4;
+    __shared__ __align__(16) CT es[32];
+    const int lane = threadIdx.x;
+    const int64_t b = blockIdx.x;
+    if (b >= B) return;
+    const int64_t base = b * nsub;
+    const int r = lane < M ? lane : 0;
+    CT dmax = (CT)0, xmax = (CT)0;
+    for (int j = 0; j + 1 < nsub; ++j) {
+        if (lane < M) {
+            const CT xe = Xend[(base + j) * MP4 + r], xi = Xin[(base + j + 1) * MP4 + r];
+            dmax = max(dmax, fabs(xe - xi));
+            xmax = max(xmax, max(fabs(xe), fabs(xi)));
+        }
+    }
+    dmax = warp_max(dmax);
+    xmax = warp_max(xmax);
+    const bool bad = dmax > (CT)kDefectTol * xmax || !(dmax == dmax);
+    if (lane == 0) flags[b] = bad ? 1 : 0;
+    if (!bad) return;
+    CT e = (CT)0;  // correction of Xin_j, component r
+    for (int j = 0; j + 1 < nsub; ++j) {
+        const CT* t = tape + (base + j) * TP::SIZE;
+        es[lane] = lane < M ? e : (CT)0;
+        __syncwarp();
+        CT w[MP4], ev[MP4];
+        load_vec<CT, MP4>(t + (TP::R_ROW + r) * MP4, w);
+        load_vec<CT, MP4>(es, ev);
+        const CT d = lane < M ? Xend[(base + j) * MP4 + r] - Xin[(base + j + 1) * MP4 + r] : (CT)0;
+        const CT en = dot_rows<M, CT>(w, ev, d);
+        __syncwarp();
+        e = en;
+        if (lane < M) Xin[(base + j + 1) * MP4 + r] += e;
+    }
+}
+
+// Adjoint analogue: K_j = carry-out of sub-chunk j computed by the apply pass
+// from Mu_j; d_j = K_j - Mu_{j-1};  e_{j-1} = Phi_j^T e_j + d_j (e_last = 0).
+template <int M, typename CT>
+__global__ void __launch_bounds__(32)
+k_refine_bwd(const CT* __restrict__ tape, CT* __restrict__ Mu, const CT* __restrict__ K,
+             int* __restrict__ flags, int nsub, int64_t B) {
+    using TP = Tape<M>;
+    constexpr int MP4 = TP::MP4;
+    __shared__ __align__(16) CT es[32];
+    const int lane = threadIdx.x;
+    const int64_t b = blockIdx.x;
+    if (b >= B) return;
+    const int64_t base = b * nsub;
+    const int r = lane < M ? lane : 0;
+    CT dmax = (CT)0, xmax = (CT)0;
+    for (int j = 1; j < nsub; ++j) {
+        if (lane < M) {
+            const CT kj = K[(base + j) * MP4 + r], mj = Mu[(base + j - 1) * MP4 + r];
+            dmax = max(dmax, fabs(kj - mj));
+            xmax = max(xmax, max(fabs(kj), fabs(mj)));
+        }
+    }
+    dmax = warp_max(dmax);
+    xmax = warp_max(xmax);
+    const bool bad = dmax > (CT)kDefectTol * xmax || !(dmax == dmax);
+    if (lane == 0) flags[b] = bad ? 1 : 0;
+    if (!bad) return;
+    CT e = (CT)0;
+    for (int j = nsub - 1; j >= 1; --j) {
+        const CT* t = tape + (base + j) * TP::SIZE;
+        es[lane] = lane < M ? e : (CT)0;
+        __syncwarp();
+        CT w[MP4], ev[MP4];
+        load_vec<CT, MP4>(t + r * MP4, w);
+        load_vec<CT, MP4>(es, ev);
+        const CT d = lane < M ? K[(base + j) * MP4 + r] - Mu[(base + j - 1) * MP4 + r] : (CT)0;
+        const CT en = dot_rows<M, CT>(w, ev, d);
+        __syncwarp();
+        e = en;
+        if (lane < M) Mu[(base + j - 1) * MP4 + r] += e;
     }
 }
 

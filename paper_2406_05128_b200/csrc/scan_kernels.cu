@@ -89,8 +89,8 @@ cudaError_t basis2_impl(const float* e, const float* A, float* PhiZ, const ScanA
 }
 
 template <typename IO, int M, bool TI>
-cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag,
-                       const ScanArgs& g, cudaStream_t st) {
+cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag, IO* Xend,
+                       const int* only, const ScanArgs& g, cudaStream_t st) {
     using S = LaneSmem<IO, M, TI>;
     auto k = k_apply_fwd<IO, M, TI>;
     cudaError_t err = ensure_smem(k, S::BYTES);
@@ -99,13 +99,14 @@ cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag
     err = lane_maps<IO, M, TI>(mp, TI ? nullptr : A, e, s, g);
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
-    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Xin, flag, g);
+    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Xin, flag, Xend,
+                                                        only, g);
     return cudaGetLastError();
 }
 
 template <typename IO, int M, bool TI, int MODE>
 cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge,
-                         const ScanArgs& g, cudaStream_t st) {
+                         const int* only, const ScanArgs& g, cudaStream_t st) {
     using S = LaneSmem<IO, M, TI>;
     auto k = k_adjoint<IO, M, TI, MODE>;
     cudaError_t err = ensure_smem(k, S::BYTES);
@@ -114,7 +115,7 @@ cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge
     err = lane_maps<IO, M, TI>(mp, TI ? nullptr : A, gs, MODE == 1 ? ge : nullptr, g);
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
-    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Mu, Nu, g);
+    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Mu, Nu, only, g);
     return cudaGetLastError();
 }
 
@@ -139,7 +140,7 @@ cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO
                          const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
         if constexpr (std::is_same<IO, float>::value) {
-            if (prec == kPrecF32Chains)
+            if (prec == kPrecF32Chains || prec == kPrecAuto)
                 return ti ? basis2_impl<M_, true>(e, A, PhiZ, g, st)
                           : basis2_impl<M_, false>(e, A, PhiZ, g, st);
         }
@@ -199,22 +200,35 @@ cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, const
 
 template <typename IO>
 cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO* Xin, IO* s,
-                             int* flag, const ScanArgs& g, cudaStream_t st) {
+                             int* flag, IO* Xend, const int* only, const ScanArgs& g,
+                             cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
-        return ti ? apply_impl<IO, M_, true>(e, A, Xin, s, flag, g, st)
-                  : apply_impl<IO, M_, false>(e, A, Xin, s, flag, g, st);
+        return ti ? apply_impl<IO, M_, true>(e, A, Xin, s, flag, Xend, only, g, st)
+                  : apply_impl<IO, M_, false>(e, A, Xin, s, flag, Xend, only, g, st);
+    })
+}
+
+template <typename IO>
+cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xend, int* flags,
+                          const ScanArgs& g, cudaStream_t st) {
+    TVLP_DISPATCH_M(Mp, {
+        if (fwd)
+            k_refine_fwd<M_, IO><<<(unsigned)g.B, 32, 0, st>>>(tape, X, Xend, flags, g.nsub, g.B);
+        else
+            k_refine_bwd<M_, IO><<<(unsigned)g.B, 32, 0, st>>>(tape, X, Xend, flags, g.nsub, g.B);
+        return cudaGetLastError();
     })
 }
 
 template <typename IO>
 cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const IO* Mu,
-                           IO* Nu, IO* ge, const ScanArgs& g, cudaStream_t st) {
+                           IO* Nu, IO* ge, const int* only, const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
         if (mode == 0)
-            return ti ? adjoint_impl<IO, M_, true, 0>(gs, A, Mu, Nu, ge, g, st)
-                      : adjoint_impl<IO, M_, false, 0>(gs, A, Mu, Nu, ge, g, st);
-        return ti ? adjoint_impl<IO, M_, true, 1>(gs, A, Mu, Nu, ge, g, st)
-                  : adjoint_impl<IO, M_, false, 1>(gs, A, Mu, Nu, ge, g, st);
+            return ti ? adjoint_impl<IO, M_, true, 0>(gs, A, Mu, Nu, ge, only, g, st)
+                      : adjoint_impl<IO, M_, false, 0>(gs, A, Mu, Nu, ge, only, g, st);
+        return ti ? adjoint_impl<IO, M_, true, 1>(gs, A, Mu, Nu, ge, only, g, st)
+                  : adjoint_impl<IO, M_, false, 1>(gs, A, Mu, Nu, ge, only, g, st);
     })
 }
 
@@ -247,9 +261,12 @@ cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* pa
     template cudaError_t launch_carry_bwd<IO>(int, const IO*, const IO*, IO*, const ScanArgs&,   \
                                               cudaStream_t);                                     \
     template cudaError_t launch_apply_fwd<IO>(int, bool, const IO*, const IO*, const IO*, IO*,   \
-                                              int*, const ScanArgs&, cudaStream_t);              \
+                                              int*, IO*, const int*, const ScanArgs&,            \
+                                              cudaStream_t);                                     \
     template cudaError_t launch_adjoint<IO>(int, bool, int, const IO*, const IO*, const IO*,     \
-                                            IO*, IO*, const ScanArgs&, cudaStream_t);            \
+                                            IO*, IO*, const int*, const ScanArgs&, cudaStream_t);\
+    template cudaError_t launch_refine<IO>(int, bool, const IO*, IO*, const IO*, int*,           \
+                                           const ScanArgs&, cudaStream_t);                       \
     template cudaError_t launch_grad_A<IO>(int, const IO*, const IO*, const IO*, IO*, int64_t,   \
                                            int64_t, cudaStream_t);                               \
     template cudaError_t launch_grad_a<IO>(int, const IO*, const IO*, const IO*, IO*, IO*,       \

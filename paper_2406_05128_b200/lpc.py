@@ -40,7 +40,7 @@ __all__ = [
 ]
 
 _VALIDATION = os.environ.get("TVLP_VALIDATION", "eager")
-_CARRY = os.environ.get("TVLP_CARRY", "fp64")
+_CARRY = os.environ.get("TVLP_CARRY", "auto")
 _pending_flags = {}
 
 
@@ -53,10 +53,13 @@ def set_validation(mode):
 
 
 def set_carry_precision(p):
-    """'fp64' (default; sub-chunk transition matrices from float64 chains) or
-    'fp32' (faster; ~1e-3 relative error on near-unit-circle poles)."""
+    """Precision of the sub-chunk transition matrices ("carries"):
+    'auto' (default) -- fp32 chains, then an a-posteriori boundary-defect check
+    and a device-side refinement pass for the sequences that fail it;
+    'fp64' -- float64 chains (no check needed); 'fp32' -- fp32 chains without
+    the check (~1e-3 relative error on near-unit-circle poles)."""
     global _CARRY
-    if p not in ("fp64", "fp32"):
+    if p not in ("fp64", "fp32", "auto"):
         raise ValueError(f"unknown carry precision {p!r}")
     _CARRY = p
 
@@ -66,7 +69,7 @@ def carry_precision():
 
 
 def _carry_code(p=None):
-    return N.CARRY_F32 if (p or _CARRY) == "fp32" else N.CARRY_F64
+    return {"fp32": N.CARRY_F32, "fp64": N.CARRY_F64, "auto": N.CARRY_AUTO}[p or _CARRY]
 
 
 def check_nonfinite(device=None):

@@ -230,15 +230,27 @@ def _tv_parity(e, A, g, tol=TOL32, zi=None, precision=None):
     return worst
 
 
-def test_config1_d1_and_stress():
-    """Config 1: B=4, T=24000, M=22, D1 + stress, seeds 0-3."""
+@pytest.mark.parametrize("precision", ["auto", "fp64"])
+def test_config1_d1_and_stress(precision):
+    """Config 1: B=4, T=24000, M=22, D1 + the resonant stress set, seeds 0-3.
+    'auto' must refine the stress sequences (fp32 chains alone fail them)."""
     e, A, g = data.d1_batch(0, 4, 24000)
-    _tv_parity(e, A, g)
+    _tv_parity(e, A, g, precision=precision)
     items = [data.stress_item(s, 24000) for s in range(4)]
     e = np.stack([x[0] for x in items])
     A = np.stack([x[1] for x in items])
     g = np.stack([x[2] for x in items])
-    _tv_parity(e, A, g)
+    _tv_parity(e, A, g, precision=precision)
+
+
+def test_stress_mixed_batch_auto():
+    """Refinement is per sequence: resonant and D1 items in one batch, T=48000."""
+    e1, A1, g1 = data.d1_batch(5, 3, 48000)
+    items = [data.stress_item(s, 48000) for s in (7, 8, 9)]
+    e = np.concatenate([e1, np.stack([x[0] for x in items])])
+    A = np.concatenate([A1, np.stack([x[1] for x in items])])
+    g = np.concatenate([g1, np.stack([x[2] for x in items])])
+    _tv_parity(e, A, g, precision="auto")
 
 
 def test_config3_shape_d1():
