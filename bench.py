@@ -214,6 +214,7 @@ def run_b200(args, cfg, rank, world, dist):
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = lib.tvlp_launch_count()
+    r0 = lib.tvlp_refined_sequences()
     with Clocks(dev.index) as clk:
         barrier()
         ev0.record(stream)
@@ -222,6 +223,7 @@ def run_b200(args, cfg, rank, world, dist):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = lib.tvlp_launch_count() - n0
+    refined = lib.tvlp_refined_sequences() - r0
     ms = ev0.elapsed_time(ev1) / args.steps
     if dist is not None:
         t = torch.tensor([ms], device=dev)
@@ -316,6 +318,7 @@ def run_b200(args, cfg, rank, world, dist):
                 "ms_per_step": round(e2e_ms, 3)},
         "gpu_launches": int(launches),
         "nonfinite_outputs": bool(nonfinite_seen),
+        "refined_sequences": int(refined),
         "clocks": clk.summary(),
     }
     return line

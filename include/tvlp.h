@@ -128,6 +128,9 @@ int tvlp_framewise_backward(int32_t dtype, const void* grad_out, const void* fra
  * writes "name launches total_ms" lines (it synchronises on the recorded
  * events) and resets the table; returns the number of bytes written. */
 int64_t tvlp_launch_count(void);
+/* Sequences whose fp32 carries failed the boundary-defect check and were
+ * refined (precision TVLP_CARRY_AUTO), cumulative; synchronises the device. */
+int64_t tvlp_refined_sequences(void);
 void tvlp_profile_enable(int32_t on);
 int32_t tvlp_profile_dump(char* buf, int32_t buflen);
 

@@ -50,6 +50,7 @@ _SIGS = [
     ("tvlp_framewise_backward", ctypes.c_int,
      [_I32, _P, _P, _P, _D, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _P, _SZ, _P]),
     ("tvlp_launch_count", _I64, []),
+    ("tvlp_refined_sequences", _I64, []),
     ("tvlp_profile_enable", None, [_I32]),
     ("tvlp_profile_dump", _I32, [ctypes.c_char_p, _I32]),
 ]

@@ -224,6 +224,7 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     const bool refine = prec == kPrecAuto && sizeof(IO) == 4;
     IO* xend = refine ? static_cast<IO*>(c.take(nsc * mp4(p) * sz)) : nullptr;
     int* flags = refine ? static_cast<int*>(c.take(p.B * sizeof(int))) : nullptr;
+    unsigned* dstat = refine ? static_cast<unsigned*>(c.take(p.B * 2 * sizeof(unsigned))) : nullptr;
     const IO* e_p = static_cast<const IO*>(e);
     const IO* A_p = static_cast<const IO*>(A);
     const IO* zi_p = static_cast<const IO*>(zi);
@@ -254,13 +255,16 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
         s_p = static_cast<IO*>(ps);
     }
     TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, e_p, A_p, phiz, g, st)));
-    TVLP_RUN("carry_fwd", 1, st, (launch_carry_fwd<IO>(p.Mp, phiz, zi_p, xin, g, st)));
+    TVLP_RUN("carry_fwd", 1, st, (launch_carry_fwd<IO>(p.Mp, phiz, zi_p, xin, dstat, g, st)));
     TVLP_RUN("apply_fwd", 1, st,
-             (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, xend, nullptr, g, st)));
+             (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, xend, dstat, nullptr, g,
+                                   st)));
     if (refine) {
-        TVLP_RUN("refine_fwd", 1, st, (launch_refine<IO>(p.Mp, true, phiz, xin, xend, flags, g, st)));
+        TVLP_RUN("refine_fwd", 1, st,
+                 (launch_refine<IO>(p.Mp, true, phiz, xin, xend, dstat, flags, g, st)));
         TVLP_RUN("apply_fwd_refined", 1, st,
-                 (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nullptr, nullptr, flags, g, st)));
+                 (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nullptr, nullptr, nullptr, flags,
+                                       g, st)));
     }
     if (packed) TVLP_CK(unpack<IO>(ps, s, p.B, p.T, 1, p.Tp, 1, st));
     return TVLP_OK;
@@ -290,6 +294,7 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     const bool refine = prec == kPrecAuto && sizeof(IO) == 4;
     IO* kout = refine ? static_cast<IO*>(c.take(nsc * mp4(p) * sz)) : nullptr;
     int* flags = refine ? static_cast<int*>(c.take(p.B * sizeof(int))) : nullptr;
+    unsigned* dstat = refine ? static_cast<unsigned*>(c.take(p.B * 2 * sizeof(unsigned))) : nullptr;
     const int nchunk = grad_a_chunks(p);
     IO* part = ti ? static_cast<IO*>(c.take(p.B * (int64_t)nchunk * p.Mp * sz)) : nullptr;
     IO* ga_p = (ti && p.Mp != p.M) ? static_cast<IO*>(c.take(p.B * p.Mp * sz)) : nullptr;
@@ -338,14 +343,17 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
         phiz = phiz_own;
     }
     TVLP_RUN("adjoint_zs", 1, st,
-             (launch_adjoint<IO>(p.Mp, ti, 0, gs_p, A_p, nullptr, nu, nullptr, nullptr, g, st)));
-    TVLP_RUN("carry_bwd", 1, st, (launch_carry_bwd<IO>(p.Mp, phiz, nu, mu, g, st)));
+             (launch_adjoint<IO>(p.Mp, ti, 0, gs_p, A_p, nullptr, nu, nullptr, nullptr, nullptr, g,
+                                 st)));
+    TVLP_RUN("carry_bwd", 1, st, (launch_carry_bwd<IO>(p.Mp, phiz, nu, mu, dstat, g, st)));
     TVLP_RUN("adjoint_apply", 1, st,
-             (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, kout, ge_p, nullptr, g, st)));
+             (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, kout, ge_p, dstat, nullptr, g, st)));
     if (refine) {
-        TVLP_RUN("refine_bwd", 1, st, (launch_refine<IO>(p.Mp, false, phiz, mu, kout, flags, g, st)));
+        TVLP_RUN("refine_bwd", 1, st,
+                 (launch_refine<IO>(p.Mp, false, phiz, mu, kout, dstat, flags, g, st)));
         TVLP_RUN("adjoint_apply_refined", 1, st,
-                 (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, flags, g, st)));
+                 (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, nullptr, flags, g,
+                                     st)));
     }
     if (ti) {
         IO* ga_out = ga_p ? ga_p : static_cast<IO*>(gA);
@@ -454,6 +462,8 @@ int32_t tvlp_max_order(void) { return kMaxOrder; }
 
 int64_t tvlp_launch_count(void) { return g_launches.load(); }
 
+int64_t tvlp_refined_sequences(void) { return (int64_t)refined_sequences(); }
+
 void tvlp_profile_enable(int32_t on) { g_prof_on.store(on ? 1 : 0); }
 
 int32_t tvlp_profile_dump(char* buf, int32_t buflen) {
@@ -530,18 +540,18 @@ size_t tvlp_workspace_bytes(int32_t op, int32_t dtype, int64_t B, int64_t T, int
         const bool ti = op == TVLP_OP_FWD_TI || op == TVLP_OP_BWD_TI;
         if (op == TVLP_OP_FWD_TV || op == TVLP_OP_FWD_TI) {
             if (f64)
-                forward_impl<double>(ti, any, any, any, (void*)any, p, nullptr, 0, nullptr, 0,
-                                     nullptr, 0, &need);
+                forward_impl<double>(ti, any, any, any, (void*)any, p, nullptr, kPrecAuto, nullptr,
+                                     0, nullptr, 0, &need);
             else
-                forward_impl<float>(ti, any, any, any, (void*)any, p, nullptr, 0, nullptr, 0,
-                                    nullptr, 0, &need);
+                forward_impl<float>(ti, any, any, any, (void*)any, p, nullptr, kPrecAuto, nullptr,
+                                    0, nullptr, 0, &need);
         } else {
             if (f64)
                 backward_impl<double>(ti, any, any, any, any, (void*)any, (void*)any, p, nullptr,
-                                      0, nullptr, 0, 0, &need);
+                                      kPrecAuto, nullptr, 0, 0, &need);
             else
                 backward_impl<float>(ti, any, any, any, any, (void*)any, (void*)any, p, nullptr,
-                                     0, nullptr, 0, 0, &need);
+                                     kPrecAuto, nullptr, 0, 0, &need);
         }
         return need;
     }

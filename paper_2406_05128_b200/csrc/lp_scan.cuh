@@ -423,7 +423,8 @@ struct CarrySmem {
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_stride,
-            CT* __restrict__ Xin, int64_t nseg, int seglen, int nsub) {
+            CT* __restrict__ Xin, int64_t nseg, int seglen, int nsub,
+            unsigned* __restrict__ dstat) {
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
@@ -456,6 +457,10 @@ k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_strid
         }
     };
     for (int i = 0; i < kCS; ++i) issue(i);
+    if (dstat != nullptr && lane == 0 && k0 == 0) {
+        dstat[2 * b] = 0u;
+        dstat[2 * b + 1] = 0u;
+    }
     CT x = (x0 != nullptr && lane < M) ? x0[sidx * x0_stride + lane] : (CT)0;
     for (int sg = 0; sg < nst; ++sg) {
         const int st = sg % kCS;
@@ -490,7 +495,8 @@ k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_strid
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __restrict__ m0,
-            int m0_stride, CT* __restrict__ Mu, int64_t nseg, int seglen, int nsub) {
+            int m0_stride, CT* __restrict__ Mu, int64_t nseg, int seglen, int nsub,
+            unsigned* __restrict__ dstat) {
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
@@ -529,6 +535,10 @@ k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __
         }
     };
     for (int i = 0; i < kCS; ++i) issue(i);
+    if (dstat != nullptr && lane == 0 && k0 == 0) {
+        dstat[2 * b] = 0u;
+        dstat[2 * b + 1] = 0u;
+    }
     CT mu = (m0 != nullptr && lane < M) ? m0[sidx * m0_stride + lane] : (CT)0;
     for (int sg = 0; sg < nst; ++sg) {
         const int st = sg % kCS;
@@ -601,7 +611,7 @@ template <typename IO, int M, bool TI>
 __global__ void __launch_bounds__(32)
 k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
             const IO* __restrict__ Xin, int* __restrict__ flag, IO* __restrict__ Xend,
-            const int* __restrict__ only, ScanArgs g) {
+            unsigned* __restrict__ dstat, const int* __restrict__ only, ScanArgs g) {
     using S = LaneSmem<IO, M, TI>;
     constexpr int W = S::W;
     constexpr int MR = (M + W - 1) / W * W;
@@ -722,7 +732,23 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 #pragma unroll
         for (int p = 0; p < MR; ++p) tmp[p] = R[p];
         const int last = (g.Ls - 1) % MR;
-        for (int i = 0; i < M; ++i) Xend[gid * Tape<M>::MP4 + i] = tmp[(last - i + MR) % MR];
+        const bool has_next = (gid % g.nsub) + 1 < g.nsub;
+        float dm = 0.f, xm = 0.f;
+        for (int i = 0; i < M; ++i) {
+            const IO v = tmp[(last - i + MR) % MR];
+            Xend[gid * Tape<M>::MP4 + i] = v;
+            if (has_next) {
+                const IO xn = Xin[(gid + 1) * Tape<M>::MP4 + i];
+                dm = fmaxf(dm, (float)fabs(v - xn));
+                xm = fmaxf(xm, fmaxf((float)fabs(v), (float)fabs(xn)));
+            }
+        }
+        if (has_next && dstat != nullptr) {
+            const int64_t b = gid / g.nsub;
+            if (!(dm == dm)) dm = __int_as_float(0x7f800000);  // NaN -> +inf: always refine
+            atomicMax(&dstat[2 * b], __float_as_uint(dm));
+            atomicMax(&dstat[2 * b + 1], __float_as_uint(xm));
+        }
     }
 }
 
@@ -734,8 +760,8 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 template <typename IO, int M, bool TI, int MODE>
 __global__ void __launch_bounds__(32)
 k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
-          const IO* __restrict__ Mu, IO* __restrict__ Nu, const int* __restrict__ only,
-          ScanArgs g) {
+          const IO* __restrict__ Mu, IO* __restrict__ Nu, unsigned* __restrict__ dstat,
+          const int* __restrict__ only, ScanArgs g) {
     using S = LaneSmem<IO, M, TI>;
     constexpr int W = S::W;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -829,6 +855,19 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     if (active && Nu != nullptr) {
 #pragma unroll
         for (int i = 0; i < M; ++i) Nu[gid * Tape<M>::MP4 + i] = lam[i];
+        if (MODE == 1 && dstat != nullptr && (gid % g.nsub) > 0) {
+            float dm = 0.f, xm = 0.f;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const IO mp = Mu[(gid - 1) * Tape<M>::MP4 + i];
+                dm = fmaxf(dm, (float)fabs(lam[i] - mp));
+                xm = fmaxf(xm, fmaxf((float)fabs(lam[i]), (float)fabs(mp)));
+            }
+            const int64_t b = gid / g.nsub;
+            if (!(dm == dm)) dm = __int_as_float(0x7f800000);
+            atomicMax(&dstat[2 * b], __float_as_uint(dm));
+            atomicMax(&dstat[2 * b + 1], __float_as_uint(xm));
+        }
     }
 }
 
@@ -850,31 +889,27 @@ __device__ __forceinline__ CT warp_max(CT v) {
     return v;
 }
 
+__device__ unsigned long long g_refined_sequences = 0;
+
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_refine_fwd(const CT* __restrict__ tape, CT* __restrict__ Xin, const CT* __restrict__ Xend,
-             int* __restrict__ flags, int nsub, int64_t B) {
+             const unsigned* __restrict__ dstat, int* __restrict__ flags, int nsub, int64_t B) {
     using TP = Tape<M>;
     constexpr int MP4 = TP::MP4;
     __shared__ __align__(16) CT es[32];
     const int lane = threadIdx.x;
     const int64_t b = blockIdx.x;
     if (b >= B) return;
+    const float dmax = __uint_as_float(dstat[2 * b]), xmax = __uint_as_float(dstat[2 * b + 1]);
+    const bool bad = dmax > kDefectTol * xmax;
+    if (lane == 0) {
+        flags[b] = bad ? 1 : 0;
+        if (bad) atomicAdd(&g_refined_sequences, 1ull);
+    }
+    if (!bad) return;
     const int64_t base = b * nsub;
     const int r = lane < M ? lane : 0;
-    CT dmax = (CT)0, xmax = (CT)0;
-    for (int j = 0; j + 1 < nsub; ++j) {
-        if (lane < M) {
-            const CT xe = Xend[(base + j) * MP4 + r], xi = Xin[(base + j + 1) * MP4 + r];
-            dmax = max(dmax, fabs(xe - xi));
-            xmax = max(xmax, max(fabs(xe), fabs(xi)));
-        }
-    }
-    dmax = warp_max(dmax);
-    xmax = warp_max(xmax);
-    const bool bad = dmax > (CT)kDefectTol * xmax || !(dmax == dmax);
-    if (lane == 0) flags[b] = bad ? 1 : 0;
-    if (!bad) return;
     CT e = (CT)0;  // correction of Xin_j, component r
     for (int j = 0; j + 1 < nsub; ++j) {
         const CT* t = tape + (base + j) * TP::SIZE;
@@ -896,28 +931,22 @@ k_refine_fwd(const CT* __restrict__ tape, CT* __restrict__ Xin, const CT* __rest
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_refine_bwd(const CT* __restrict__ tape, CT* __restrict__ Mu, const CT* __restrict__ K,
-             int* __restrict__ flags, int nsub, int64_t B) {
+             const unsigned* __restrict__ dstat, int* __restrict__ flags, int nsub, int64_t B) {
     using TP = Tape<M>;
     constexpr int MP4 = TP::MP4;
     __shared__ __align__(16) CT es[32];
     const int lane = threadIdx.x;
     const int64_t b = blockIdx.x;
     if (b >= B) return;
+    const float dmax = __uint_as_float(dstat[2 * b]), xmax = __uint_as_float(dstat[2 * b + 1]);
+    const bool bad = dmax > kDefectTol * xmax;
+    if (lane == 0) {
+        flags[b] = bad ? 1 : 0;
+        if (bad) atomicAdd(&g_refined_sequences, 1ull);
+    }
+    if (!bad) return;
     const int64_t base = b * nsub;
     const int r = lane < M ? lane : 0;
-    CT dmax = (CT)0, xmax = (CT)0;
-    for (int j = 1; j < nsub; ++j) {
-        if (lane < M) {
-            const CT kj = K[(base + j) * MP4 + r], mj = Mu[(base + j - 1) * MP4 + r];
-            dmax = max(dmax, fabs(kj - mj));
-            xmax = max(xmax, max(fabs(kj), fabs(mj)));
-        }
-    }
-    dmax = warp_max(dmax);
-    xmax = warp_max(xmax);
-    const bool bad = dmax > (CT)kDefectTol * xmax || !(dmax == dmax);
-    if (lane == 0) flags[b] = bad ? 1 : 0;
-    if (!bad) return;
     CT e = (CT)0;
     for (int j = nsub - 1; j >= 1; --j) {
         const CT* t = tape + (base + j) * TP::SIZE;

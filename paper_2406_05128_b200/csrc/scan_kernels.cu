@@ -90,7 +90,7 @@ cudaError_t basis2_impl(const float* e, const float* A, float* PhiZ, const ScanA
 
 template <typename IO, int M, bool TI>
 cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag, IO* Xend,
-                       const int* only, const ScanArgs& g, cudaStream_t st) {
+                       unsigned* dstat, const int* only, const ScanArgs& g, cudaStream_t st) {
     using S = LaneSmem<IO, M, TI>;
     auto k = k_apply_fwd<IO, M, TI>;
     cudaError_t err = ensure_smem(k, S::BYTES);
@@ -100,13 +100,13 @@ cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
     k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Xin, flag, Xend,
-                                                        only, g);
+                                                        dstat, only, g);
     return cudaGetLastError();
 }
 
 template <typename IO, int M, bool TI, int MODE>
 cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge,
-                         const int* only, const ScanArgs& g, cudaStream_t st) {
+                         unsigned* dstat, const int* only, const ScanArgs& g, cudaStream_t st) {
     using S = LaneSmem<IO, M, TI>;
     auto k = k_adjoint<IO, M, TI, MODE>;
     cudaError_t err = ensure_smem(k, S::BYTES);
@@ -115,7 +115,8 @@ cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge
     err = lane_maps<IO, M, TI>(mp, TI ? nullptr : A, gs, MODE == 1 ? ge : nullptr, g);
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
-    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Mu, Nu, only, g);
+    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Mu, Nu, dstat,
+                                                        only, g);
     return cudaGetLastError();
 }
 
@@ -162,73 +163,82 @@ int tape_elems(int Mp) {
 
 template <int M, typename IO>
 cudaError_t carry_fwd_impl(const IO* tape, const IO* x0, int x0s, IO* Xin, int64_t nseg,
-                           int seglen, int nsub, cudaStream_t st) {
+                           int seglen, int nsub, unsigned* dstat, cudaStream_t st) {
     using SM = CarrySmem<M, IO>;
     auto k = k_carry_fwd<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
-    k<<<(unsigned)nseg, 32, SM::BYTES, st>>>(tape, x0, x0s, Xin, nseg, seglen, nsub);
+    k<<<(unsigned)nseg, 32, SM::BYTES, st>>>(tape, x0, x0s, Xin, nseg, seglen, nsub, dstat);
     return cudaGetLastError();
 }
 
 template <int M, typename IO>
 cudaError_t carry_bwd_impl(const IO* tape, const IO* Nu, const IO* m0, int m0s, IO* Mu,
-                           int64_t nseg, int seglen, int nsub, cudaStream_t st) {
+                           int64_t nseg, int seglen, int nsub, unsigned* dstat, cudaStream_t st) {
     using SM = CarrySmem<M, IO>;
     auto k = k_carry_bwd<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
-    k<<<(unsigned)nseg, 32, SM::BYTES, st>>>(tape, Nu, m0, m0s, Mu, nseg, seglen, nsub);
+    k<<<(unsigned)nseg, 32, SM::BYTES, st>>>(tape, Nu, m0, m0s, Mu, nseg, seglen, nsub, dstat);
     return cudaGetLastError();
 }
 
 template <typename IO>
-cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, const ScanArgs& g,
-                             cudaStream_t st) {
+cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, unsigned* dstat,
+                             const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
-        return carry_fwd_impl<M_, IO>(tape, zi, Mp, Xin, g.B, g.nsub, g.nsub, st);
+        return carry_fwd_impl<M_, IO>(tape, zi, Mp, Xin, g.B, g.nsub, g.nsub, dstat, st);
     })
 }
 
+unsigned long long refined_sequences() {
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, g_refined_sequences, sizeof(v));
+    return v;
+}
+
 template <typename IO>
-cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, const ScanArgs& g,
-                             cudaStream_t st) {
+cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, unsigned* dstat,
+                             const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
-        return carry_bwd_impl<M_, IO>(tape, Nu, nullptr, 0, Mu, g.B, g.nsub, g.nsub, st);
+        return carry_bwd_impl<M_, IO>(tape, Nu, nullptr, 0, Mu, g.B, g.nsub, g.nsub, dstat, st);
     })
 }
 
 template <typename IO>
 cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO* Xin, IO* s,
-                             int* flag, IO* Xend, const int* only, const ScanArgs& g,
-                             cudaStream_t st) {
+                             int* flag, IO* Xend, unsigned* dstat, const int* only,
+                             const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
-        return ti ? apply_impl<IO, M_, true>(e, A, Xin, s, flag, Xend, only, g, st)
-                  : apply_impl<IO, M_, false>(e, A, Xin, s, flag, Xend, only, g, st);
+        return ti ? apply_impl<IO, M_, true>(e, A, Xin, s, flag, Xend, dstat, only, g, st)
+                  : apply_impl<IO, M_, false>(e, A, Xin, s, flag, Xend, dstat, only, g, st);
     })
 }
 
 template <typename IO>
-cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xend, int* flags,
-                          const ScanArgs& g, cudaStream_t st) {
+cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xend,
+                          const unsigned* dstat, int* flags, const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
         if (fwd)
-            k_refine_fwd<M_, IO><<<(unsigned)g.B, 32, 0, st>>>(tape, X, Xend, flags, g.nsub, g.B);
+            k_refine_fwd<M_, IO><<<(unsigned)g.B, 32, 0, st>>>(tape, X, Xend, dstat, flags, g.nsub,
+                                                               g.B);
         else
-            k_refine_bwd<M_, IO><<<(unsigned)g.B, 32, 0, st>>>(tape, X, Xend, flags, g.nsub, g.B);
+            k_refine_bwd<M_, IO><<<(unsigned)g.B, 32, 0, st>>>(tape, X, Xend, dstat, flags, g.nsub,
+                                                               g.B);
         return cudaGetLastError();
     })
 }
 
 template <typename IO>
 cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const IO* Mu,
-                           IO* Nu, IO* ge, const int* only, const ScanArgs& g, cudaStream_t st) {
+                           IO* Nu, IO* ge, unsigned* dstat, const int* only, const ScanArgs& g,
+                           cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
         if (mode == 0)
-            return ti ? adjoint_impl<IO, M_, true, 0>(gs, A, Mu, Nu, ge, only, g, st)
-                      : adjoint_impl<IO, M_, false, 0>(gs, A, Mu, Nu, ge, only, g, st);
-        return ti ? adjoint_impl<IO, M_, true, 1>(gs, A, Mu, Nu, ge, only, g, st)
-                  : adjoint_impl<IO, M_, false, 1>(gs, A, Mu, Nu, ge, only, g, st);
+            return ti ? adjoint_impl<IO, M_, true, 0>(gs, A, Mu, Nu, ge, dstat, only, g, st)
+                      : adjoint_impl<IO, M_, false, 0>(gs, A, Mu, Nu, ge, dstat, only, g, st);
+        return ti ? adjoint_impl<IO, M_, true, 1>(gs, A, Mu, Nu, ge, dstat, only, g, st)
+                  : adjoint_impl<IO, M_, false, 1>(gs, A, Mu, Nu, ge, dstat, only, g, st);
     })
 }
 
@@ -256,17 +266,18 @@ cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* pa
 #define TVLP_INST(IO)                                                                            \
     template cudaError_t launch_basis<IO>(int, bool, int, const IO*, const IO*, IO*,             \
                                           const ScanArgs&, cudaStream_t);                        \
-    template cudaError_t launch_carry_fwd<IO>(int, const IO*, const IO*, IO*, const ScanArgs&,   \
-                                              cudaStream_t);                                     \
-    template cudaError_t launch_carry_bwd<IO>(int, const IO*, const IO*, IO*, const ScanArgs&,   \
-                                              cudaStream_t);                                     \
+    template cudaError_t launch_carry_fwd<IO>(int, const IO*, const IO*, IO*, unsigned*,         \
+                                              const ScanArgs&, cudaStream_t);                    \
+    template cudaError_t launch_carry_bwd<IO>(int, const IO*, const IO*, IO*, unsigned*,         \
+                                              const ScanArgs&, cudaStream_t);                    \
     template cudaError_t launch_apply_fwd<IO>(int, bool, const IO*, const IO*, const IO*, IO*,   \
-                                              int*, IO*, const int*, const ScanArgs&,            \
+                                              int*, IO*, unsigned*, const int*, const ScanArgs&, \
                                               cudaStream_t);                                     \
     template cudaError_t launch_adjoint<IO>(int, bool, int, const IO*, const IO*, const IO*,     \
-                                            IO*, IO*, const int*, const ScanArgs&, cudaStream_t);\
-    template cudaError_t launch_refine<IO>(int, bool, const IO*, IO*, const IO*, int*,           \
-                                           const ScanArgs&, cudaStream_t);                       \
+                                            IO*, IO*, unsigned*, const int*, const ScanArgs&,    \
+                                            cudaStream_t);                                       \
+    template cudaError_t launch_refine<IO>(int, bool, const IO*, IO*, const IO*,                 \
+                                           const unsigned*, int*, const ScanArgs&, cudaStream_t);\
     template cudaError_t launch_grad_A<IO>(int, const IO*, const IO*, const IO*, IO*, int64_t,   \
                                            int64_t, cudaStream_t);                               \
     template cudaError_t launch_grad_a<IO>(int, const IO*, const IO*, const IO*, IO*, IO*,       \

@@ -24,22 +24,24 @@ cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO
                          const ScanArgs& g, cudaStream_t st);
 int tape_elems(int Mp);  // carry-tape elements per sub-chunk
 template <typename IO>
-cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, const ScanArgs& g,
-                             cudaStream_t st);
+cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, unsigned* dstat,
+                             const ScanArgs& g, cudaStream_t st);
 template <typename IO>
-cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, const ScanArgs& g,
-                             cudaStream_t st);
+cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, unsigned* dstat,
+                             const ScanArgs& g, cudaStream_t st);
+unsigned long long refined_sequences();  // diagnostic counter (synchronising read)
 enum Prec2 : int { kPrecAuto = 2 };
 template <typename IO>
 cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO* Xin, IO* s,
-                             int* flag, IO* Xend, const int* only, const ScanArgs& g,
-                             cudaStream_t st);
+                             int* flag, IO* Xend, unsigned* dstat, const int* only,
+                             const ScanArgs& g, cudaStream_t st);
 template <typename IO>
 cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const IO* Mu,
-                           IO* Nu, IO* ge, const int* only, const ScanArgs& g, cudaStream_t st);
+                           IO* Nu, IO* ge, unsigned* dstat, const int* only, const ScanArgs& g,
+                           cudaStream_t st);
 template <typename IO>
-cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xend, int* flags,
-                          const ScanArgs& g, cudaStream_t st);
+cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xend,
+                          const unsigned* dstat, int* flags, const ScanArgs& g, cudaStream_t st);
 template <typename IO>
 cudaError_t launch_grad_A(int Mp, const IO* ge, const IO* s, const IO* zi, IO* gA, int64_t B,
                           int64_t T, cudaStream_t st);
