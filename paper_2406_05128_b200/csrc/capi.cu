@@ -112,7 +112,10 @@ ScanArgs scan_args(const Plan& p) {
     return g;
 }
 
-int64_t carry_elems(const Plan& p) { return p.B * (int64_t)p.nsub * tape_elems(p.Mp); }
+// carry tape: per-sub-chunk tapes followed by one forward-refinement flag per
+// sequence (an int stored in the first bytes of a B-element trailing region)
+int64_t tape_body(const Plan& p) { return p.B * (int64_t)p.nsub * tape_elems(p.Mp); }
+int64_t carry_elems(const Plan& p) { return tape_body(p) + p.B; }
 inline int64_t mp4(const Plan& p) { return (p.Mp + 3) / 4 * 4; }
 
 // bump allocator over the caller's workspace (nullptr base = sizing pass)
@@ -129,6 +132,7 @@ struct Carver {
 };
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+inline bool base_ok(const void* p) { return p != nullptr; }
 
 // ---------------------------------------------------------------- pack kernels
 // dst[b, t, c] (Tp x Mp, zero-filled) <- src[b, t, c] (T x M)
@@ -223,7 +227,8 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     // precision "auto": fp32 chains + boundary-defect check + refinement
     const bool refine = prec == kPrecAuto && sizeof(IO) == 4;
     IO* xend = refine ? static_cast<IO*>(c.take(nsc * mp4(p) * sz)) : nullptr;
-    int* flags = refine ? static_cast<int*>(c.take(p.B * sizeof(int))) : nullptr;
+    int* fflags = reinterpret_cast<int*>(phiz + tape_body(p));  // lives in the carry tape
+    int* flags = refine ? fflags : nullptr;
     unsigned* dstat = refine ? static_cast<unsigned*>(c.take(p.B * 2 * sizeof(unsigned))) : nullptr;
     const IO* e_p = static_cast<const IO*>(e);
     const IO* A_p = static_cast<const IO*>(A);
@@ -255,13 +260,15 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
         s_p = static_cast<IO*>(ps);
     }
     TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, e_p, A_p, phiz, g, st)));
-    TVLP_RUN("carry_fwd", 1, st, (launch_carry_fwd<IO>(p.Mp, phiz, zi_p, xin, dstat, g, st)));
+    TVLP_RUN("carry_fwd", 1, st,
+             (launch_carry_fwd<IO>(p.Mp, phiz, zi_p, xin, dstat, base_ok(phiz) ? fflags : nullptr,
+                                   g, st)));
     TVLP_RUN("apply_fwd", 1, st,
              (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, xend, dstat, nullptr, g,
                                    st)));
     if (refine) {
         TVLP_RUN("refine_fwd", 1, st,
-                 (launch_refine<IO>(p.Mp, true, phiz, xin, xend, dstat, flags, g, st)));
+                 (launch_refine<IO>(p.Mp, true, phiz, xin, xend, dstat, flags, nullptr, g, st)));
         TVLP_RUN("apply_fwd_refined", 1, st,
                  (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nullptr, nullptr, nullptr, flags,
                                        g, st)));
@@ -291,6 +298,9 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     IO* phiz_own = carry ? nullptr : static_cast<IO*>(c.take(carry_elems(p) * sz));
     IO* nu = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
     IO* mu = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
+    // without the forward's tape (and its per-sequence refinement flags) the
+    // backward recomputes the transition matrices with fp64 chains
+    if (carry == nullptr && prec == kPrecAuto) prec = kPrecF64Chains;
     const bool refine = prec == kPrecAuto && sizeof(IO) == 4;
     IO* kout = refine ? static_cast<IO*>(c.take(nsc * mp4(p) * sz)) : nullptr;
     int* flags = refine ? static_cast<int*>(c.take(p.B * sizeof(int))) : nullptr;
@@ -350,7 +360,10 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
              (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, kout, ge_p, dstat, nullptr, g, st)));
     if (refine) {
         TVLP_RUN("refine_bwd", 1, st,
-                 (launch_refine<IO>(p.Mp, false, phiz, mu, kout, dstat, flags, g, st)));
+                 (launch_refine<IO>(p.Mp, false, phiz, mu, kout, dstat, flags,
+                                    carry ? reinterpret_cast<const int*>(carry + tape_body(p))
+                                          : nullptr,
+                                    g, st)));
         TVLP_RUN("adjoint_apply_refined", 1, st,
                  (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, nullptr, flags, g,
                                      st)));

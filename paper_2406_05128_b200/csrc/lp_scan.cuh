@@ -424,7 +424,7 @@ template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_stride,
             CT* __restrict__ Xin, int64_t nseg, int seglen, int nsub,
-            unsigned* __restrict__ dstat) {
+            unsigned* __restrict__ dstat, int* __restrict__ fflags) {
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
@@ -457,9 +457,12 @@ k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_strid
         }
     };
     for (int i = 0; i < kCS; ++i) issue(i);
-    if (dstat != nullptr && lane == 0 && k0 == 0) {
-        dstat[2 * b] = 0u;
-        dstat[2 * b + 1] = 0u;
+    if (lane == 0 && k0 == 0) {
+        if (dstat != nullptr) {
+            dstat[2 * b] = 0u;
+            dstat[2 * b + 1] = 0u;
+        }
+        if (fflags != nullptr) fflags[b] = 0;  // set by k_refine_fwd in precision "auto"
     }
     CT x = (x0 != nullptr && lane < M) ? x0[sidx * x0_stride + lane] : (CT)0;
     for (int sg = 0; sg < nst; ++sg) {
@@ -856,12 +859,17 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
 #pragma unroll
         for (int i = 0; i < M; ++i) Nu[gid * Tape<M>::MP4 + i] = lam[i];
         if (MODE == 1 && dstat != nullptr && (gid % g.nsub) > 0) {
-            float dm = 0.f, xm = 0.f;
+            // scale: |lambda_0| = |grad_e| at the boundary.  The other adjoint
+            // components are coefficient-weighted sums of future grad_e and can
+            // be orders larger on resonant rows, while a defect in component i
+            // reaches grad_e unamplified i steps later (it shifts into lambda_0).
+            float dm = 0.f;
+            const IO mp0 = Mu[(gid - 1) * Tape<M>::MP4];
+            const float xm = fmaxf((float)fabs(lam[0]), (float)fabs(mp0));
 #pragma unroll
             for (int i = 0; i < M; ++i) {
                 const IO mp = Mu[(gid - 1) * Tape<M>::MP4 + i];
                 dm = fmaxf(dm, (float)fabs(lam[i] - mp));
-                xm = fmaxf(xm, fmaxf((float)fabs(lam[i]), (float)fabs(mp)));
             }
             const int64_t b = gid / g.nsub;
             if (!(dm == dm)) dm = __int_as_float(0x7f800000);
@@ -880,7 +888,8 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
 // carries are corrected by e_{j+1} = Phi_j e_j + d_j (e_0 = 0, Xin += e): the
 // correction is linear and small, so the fp32 Phi_j (relative error ~1e-5
 // after cancellation) contracts the error by ~1e-4 per pass.
-constexpr float kDefectTol = 2e-5f;
+constexpr float kDefectTol = 2e-5f;     // forward: relative to max |x| (samples of s)
+constexpr float kDefectTolBwd = 2e-6f;  // adjoint: relative to max |lambda_0| (= |grad_e|)
 
 template <typename CT>
 __device__ __forceinline__ CT warp_max(CT v) {
@@ -931,7 +940,8 @@ k_refine_fwd(const CT* __restrict__ tape, CT* __restrict__ Xin, const CT* __rest
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_refine_bwd(const CT* __restrict__ tape, CT* __restrict__ Mu, const CT* __restrict__ K,
-             const unsigned* __restrict__ dstat, int* __restrict__ flags, int nsub, int64_t B) {
+             const unsigned* __restrict__ dstat, int* __restrict__ flags, int nsub, int64_t B,
+             const int* __restrict__ fflags) {
     using TP = Tape<M>;
     constexpr int MP4 = TP::MP4;
     __shared__ __align__(16) CT es[32];
@@ -939,7 +949,10 @@ k_refine_bwd(const CT* __restrict__ tape, CT* __restrict__ Mu, const CT* __restr
     const int64_t b = blockIdx.x;
     if (b >= B) return;
     const float dmax = __uint_as_float(dstat[2 * b]), xmax = __uint_as_float(dstat[2 * b + 1]);
-    const bool bad = dmax > kDefectTol * xmax;
+    // a sequence whose forward carries needed refinement has ill-conditioned
+    // transition matrices; its adjoint carries are refined too (defects of the
+    // adjoint can be amplified by the resonance before they reach grad_e)
+    const bool bad = dmax > kDefectTolBwd * xmax || (fflags != nullptr && fflags[b] != 0);
     if (lane == 0) {
         flags[b] = bad ? 1 : 0;
         if (bad) atomicAdd(&g_refined_sequences, 1ull);

@@ -163,12 +163,13 @@ int tape_elems(int Mp) {
 
 template <int M, typename IO>
 cudaError_t carry_fwd_impl(const IO* tape, const IO* x0, int x0s, IO* Xin, int64_t nseg,
-                           int seglen, int nsub, unsigned* dstat, cudaStream_t st) {
+                           int seglen, int nsub, unsigned* dstat, int* fflags, cudaStream_t st) {
     using SM = CarrySmem<M, IO>;
     auto k = k_carry_fwd<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
-    k<<<(unsigned)nseg, 32, SM::BYTES, st>>>(tape, x0, x0s, Xin, nseg, seglen, nsub, dstat);
+    k<<<(unsigned)nseg, 32, SM::BYTES, st>>>(tape, x0, x0s, Xin, nseg, seglen, nsub, dstat,
+                                             fflags);
     return cudaGetLastError();
 }
 
@@ -185,9 +186,9 @@ cudaError_t carry_bwd_impl(const IO* tape, const IO* Nu, const IO* m0, int m0s, 
 
 template <typename IO>
 cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, unsigned* dstat,
-                             const ScanArgs& g, cudaStream_t st) {
+                             int* fflags, const ScanArgs& g, cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
-        return carry_fwd_impl<M_, IO>(tape, zi, Mp, Xin, g.B, g.nsub, g.nsub, dstat, st);
+        return carry_fwd_impl<M_, IO>(tape, zi, Mp, Xin, g.B, g.nsub, g.nsub, dstat, fflags, st);
     })
 }
 
@@ -217,14 +218,15 @@ cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO
 
 template <typename IO>
 cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xend,
-                          const unsigned* dstat, int* flags, const ScanArgs& g, cudaStream_t st) {
+                          const unsigned* dstat, int* flags, const int* fflags, const ScanArgs& g,
+                          cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
         if (fwd)
             k_refine_fwd<M_, IO><<<(unsigned)g.B, 32, 0, st>>>(tape, X, Xend, dstat, flags, g.nsub,
                                                                g.B);
         else
             k_refine_bwd<M_, IO><<<(unsigned)g.B, 32, 0, st>>>(tape, X, Xend, dstat, flags, g.nsub,
-                                                               g.B);
+                                                               g.B, fflags);
         return cudaGetLastError();
     })
 }
@@ -266,7 +268,7 @@ cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* pa
 #define TVLP_INST(IO)                                                                            \
     template cudaError_t launch_basis<IO>(int, bool, int, const IO*, const IO*, IO*,             \
                                           const ScanArgs&, cudaStream_t);                        \
-    template cudaError_t launch_carry_fwd<IO>(int, const IO*, const IO*, IO*, unsigned*,         \
+    template cudaError_t launch_carry_fwd<IO>(int, const IO*, const IO*, IO*, unsigned*, int*,   \
                                               const ScanArgs&, cudaStream_t);                    \
     template cudaError_t launch_carry_bwd<IO>(int, const IO*, const IO*, IO*, unsigned*,         \
                                               const ScanArgs&, cudaStream_t);                    \
@@ -277,7 +279,8 @@ cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* pa
                                             IO*, IO*, unsigned*, const int*, const ScanArgs&,    \
                                             cudaStream_t);                                       \
     template cudaError_t launch_refine<IO>(int, bool, const IO*, IO*, const IO*,                 \
-                                           const unsigned*, int*, const ScanArgs&, cudaStream_t);\
+                                           const unsigned*, int*, const int*, const ScanArgs&,   \
+                                           cudaStream_t);                                        \
     template cudaError_t launch_grad_A<IO>(int, const IO*, const IO*, const IO*, IO*, int64_t,   \
                                            int64_t, cudaStream_t);                               \
     template cudaError_t launch_grad_a<IO>(int, const IO*, const IO*, const IO*, IO*, IO*,       \

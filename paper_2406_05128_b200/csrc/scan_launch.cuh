@@ -25,7 +25,7 @@ cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO
 int tape_elems(int Mp);  // carry-tape elements per sub-chunk
 template <typename IO>
 cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, unsigned* dstat,
-                             const ScanArgs& g, cudaStream_t st);
+                             int* fflags, const ScanArgs& g, cudaStream_t st);
 template <typename IO>
 cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, unsigned* dstat,
                              const ScanArgs& g, cudaStream_t st);
@@ -41,7 +41,8 @@ cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A,
                            cudaStream_t st);
 template <typename IO>
 cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xend,
-                          const unsigned* dstat, int* flags, const ScanArgs& g, cudaStream_t st);
+                          const unsigned* dstat, int* flags, const int* fflags, const ScanArgs& g,
+                          cudaStream_t st);
 template <typename IO>
 cudaError_t launch_grad_A(int Mp, const IO* ge, const IO* s, const IO* zi, IO* gA, int64_t B,
                           int64_t T, cudaStream_t st);

@@ -31,13 +31,14 @@ def test_abi_queries_without_gpu():
     Ls = lib.tvlp_subchunk_len(48000, 22)
     assert Ls % 8 == 0 and 48000 % Ls == 0 and 256 <= Ls <= 1024
     nsub = -(-48000 // Ls)
-    assert lib.tvlp_carry_elems(64, 48000, 22) == 64 * nsub * (2 * 22 + 1) * 24
+    # per-sub-chunk tapes + one forward-refinement flag slot per sequence
+    assert lib.tvlp_carry_elems(64, 48000, 22) == 64 * nsub * (2 * 22 + 1) * 24 + 64
     for op in range(4):
         assert lib.tvlp_workspace_bytes(op, 0, 64, 48000, 22, 0, 0, 0) > 0
     assert lib.tvlp_framewise_nframes(48000, 200, 960, 240) == 203
     assert lib.tvlp_workspace_bytes(5, 0, 32, 48000, 22, 200, 960, 240) > 0
     # odd orders pad to a compiled order; too-large orders are rejected
-    assert lib.tvlp_carry_elems(1, 100, 5) == 1 * (2 * 6 + 1) * 8
+    assert lib.tvlp_carry_elems(1, 100, 5) == 1 * (2 * 6 + 1) * 8 + 1
     assert lib.tvlp_carry_elems(1, 100, 99) == -1
     assert lib.tvlp_workspace_bytes(0, 0, 1, 100, 99, 0, 0, 0) == 0
 
