@@ -289,9 +289,15 @@ def test_autograd_matches_functional():
     At = _cuda(A).requires_grad_()
     s = ag.lp_tv(et, At)
     s.backward(_cuda(g))
-    ge, gA = lpc.lp_backward_tv(_cuda(g), _cuda(A), s.detach())
+    # same forward (and carry tape) through the functional API: bit-identical
+    s2, carry = lpc._forward(False, _cuda(e), _cuda(A), None, return_carry=True)
+    torch.testing.assert_close(s.detach(), s2, rtol=0, atol=0)
+    ge, gA = lpc.lp_backward_tv(_cuda(g), _cuda(A), s2, carry=carry)
     torch.testing.assert_close(et.grad, ge, rtol=0, atol=0)
     torch.testing.assert_close(At.grad, gA, rtol=0, atol=0)
+    # without the tape the backward recomputes it (fp64 chains): same to rounding
+    ge3, gA3 = lpc.lp_backward_tv(_cuda(g), _cuda(A), s2)
+    assert oracle.gradcheck_error(ge3, ge) < 1e-5 and oracle.gradcheck_error(gA3, gA) < 1e-5
 
 
 def test_torch_gradcheck_fp64():  # C1-style finite-difference check (test_lpc.py:209-235)
