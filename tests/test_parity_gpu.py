@@ -297,7 +297,7 @@ def test_autograd_matches_functional():
     torch.testing.assert_close(At.grad, gA, rtol=0, atol=0)
     # without the tape the backward recomputes it (fp64 chains): same to rounding
     ge3, gA3 = lpc.lp_backward_tv(_cuda(g), _cuda(A), s2)
-    assert oracle.gradcheck_error(ge3, ge) < 1e-5 and oracle.gradcheck_error(gA3, gA) < 1e-5
+    assert _err(_np(ge3), _np(ge)) < 1e-5 and _err(_np(gA3), _np(gA)) < 1e-5
 
 
 def test_torch_gradcheck_fp64():  # C1-style finite-difference check (test_lpc.py:209-235)
