@@ -167,6 +167,19 @@ __device__ __forceinline__ void load_row_at(const T* p, T (&a)[M], int off) {
     }
 }
 
+// compile-time loop: f(std::integral_constant<int, I>{}) for I = 0..N-1
+template <int I, int N, typename F>
+__device__ __forceinline__ void static_for_impl(F&& f) {
+    if constexpr (I < N) {
+        f(std::integral_constant<int, I>{});
+        static_for_impl<I + 1, N>(f);
+    }
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+    static_for_impl<0, N>(f);
+}
+
 template <typename T>
 __device__ __forceinline__ bool is_finite_val(T x) {
     return isfinite(x);

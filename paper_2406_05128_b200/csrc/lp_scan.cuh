@@ -286,7 +286,7 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
     for (int p = 0; p < M; ++p)
         R[p] = make_float2((cx < M && M - 1 - p == cx) ? 1.f : 0.f,
                            (cy < M && M - 1 - p == cy) ? 1.f : 0.f);
-    const float mx = (cx == M) ? 1.f : 0.f, my = (cy == M) ? 1.f : 0.f;
+    const bool zsx = cx == M, zsy = cy == M;
 
     // excitation (read by the zero-state chain only): lane q of a half holds
     // e[w*WR + q] and e[w*WR + 16 + q] of window w, loaded one window ahead;
@@ -300,36 +300,36 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
         if (!TI) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
         const int rows = min(WR, len - k * WR);
         const float* Ar = reinterpret_cast<const float*>(stage_ptr(st));
+#define TVLP_BASIS2_STEP(u)                                                              \
+    {                                                                                    \
+        float a[M];                                                                      \
+        if constexpr (TI) {                                                              \
+            _Pragma("unroll") for (int i = 0; i < M; ++i) a[i] = ati[i];                 \
+        } else {                                                                         \
+            load_row_at<float, M>(Ar + (u) * M, a, (u) * M * 4);                         \
+        }                                                                                \
+        const float ev = __shfl_sync(0xffffffffu, (u) < 16 ? ec0 : ec1, (u) & 15, 16);   \
+        /* only the zero-state slot sees the excitation (ALU selects) */                 \
+        const float2 ein = make_float2(zsx ? ev : 0.f, zsy ? ev : 0.f);                  \
+        /* two accumulators over lags M..2, oldest first; freshest lag last */           \
+        float2 p0 = make_float2(0.f, 0.f), p1 = p0;                                      \
+        _Pragma("unroll") for (int i = M; i >= 2; --i) {                                 \
+            const float2 x = R[((u) - i + 2 * M) % M];                                   \
+            const float2 ai = make_float2(a[i - 1], a[i - 1]);                           \
+            if (i & 1)                                                                   \
+                p1 = __ffma2_rn(ai, x, p1);                                              \
+            else                                                                         \
+                p0 = __ffma2_rn(ai, x, p0);                                              \
+        }                                                                                \
+        const float2 sum = __fadd2_rn(p0, p1);                                           \
+        const float2 part = __fadd2_rn(ein, make_float2(-sum.x, -sum.y));                \
+        const float2 na0 = make_float2(-a[0], -a[0]);                                    \
+        R[(u) % M] = __ffma2_rn(na0, R[((u) - 1 + M) % M], part);                        \
+    }
 #pragma unroll
-        for (int u = 0; u < WR; ++u) {
-            if (u < rows) {  // warp-uniform: only the last window can be short
-                float a[M];
-                if constexpr (TI) {
-#pragma unroll
-                    for (int i = 0; i < M; ++i) a[i] = ati[i];
-                } else {
-                    load_row_at<float, M>(Ar + u * M, a, u * M * 4);
-                }
-                const float ev = __shfl_sync(0xffffffffu, u < 16 ? ec0 : ec1, u & 15, 16);
-                const float2 ein = make_float2(ev * mx, ev * my);
-                float2 p0 = make_float2(0.f, 0.f), p1 = p0, p2 = p0, p3 = p0;
-#pragma unroll
-                for (int i = M; i >= 2; --i) {
-                    const float2 x = R[(u - i + 2 * M) % M];
-                    const float2 ai = make_float2(a[i - 1], a[i - 1]);
-                    switch (i & 3) {
-                        case 0: p0 = __ffma2_rn(ai, x, p0); break;
-                        case 1: p1 = __ffma2_rn(ai, x, p1); break;
-                        case 2: p2 = __ffma2_rn(ai, x, p2); break;
-                        default: p3 = __ffma2_rn(ai, x, p3); break;
-                    }
-                }
-                const float2 sum = __fadd2_rn(__fadd2_rn(p0, p1), __fadd2_rn(p2, p3));
-                const float2 part = __fadd2_rn(ein, make_float2(-sum.x, -sum.y));
-                const float2 na0 = make_float2(-a[0], -a[0]);
-                R[u % M] = __ffma2_rn(na0, R[(u - 1 + M) % M], part);
-            }
-        }
+        for (int u = 0; u < WR; ++u)
+            if (u < rows) TVLP_BASIS2_STEP(u)  // warp-uniform: only the last window is short
+#undef TVLP_BASIS2_STEP
         __syncwarp();
         fence_proxy_async();
         issue(k + NSTB);
