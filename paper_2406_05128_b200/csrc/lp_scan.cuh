@@ -300,46 +300,36 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
         if (!TI) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
         const int rows = min(WR, len - k * WR);
         const float* Ar = reinterpret_cast<const float*>(stage_ptr(st));
-        // coefficient rows are software-pipelined one step ahead (the LDS
-        // latency otherwise sits in front of every step's first FFMA2)
-        float acur[M];
-        if constexpr (TI) {
+#define TVLP_BASIS2_STEP(u)                                                              \
+    {                                                                                    \
+        float a[M];                                                                      \
+        if constexpr (TI) {                                                              \
+            _Pragma("unroll") for (int i = 0; i < M; ++i) a[i] = ati[i];                 \
+        } else {                                                                         \
+            load_row_at<float, M>(Ar + (u) * M, a, (u) * M * 4);                         \
+        }                                                                                \
+        const float ev = __shfl_sync(0xffffffffu, (u) < 16 ? ec0 : ec1, (u) & 15, 16);   \
+        /* only the zero-state slot sees the excitation (ALU selects) */                 \
+        const float2 ein = make_float2(zsx ? ev : 0.f, zsy ? ev : 0.f);                  \
+        /* two accumulators over lags M..2, oldest first; freshest lag last */           \
+        float2 p0 = make_float2(0.f, 0.f), p1 = p0;                                      \
+        _Pragma("unroll") for (int i = M; i >= 2; --i) {                                 \
+            const float2 x = R[((u) - i + 2 * M) % M];                                   \
+            const float2 ai = make_float2(a[i - 1], a[i - 1]);                           \
+            if (i & 1)                                                                   \
+                p1 = __ffma2_rn(ai, x, p1);                                              \
+            else                                                                         \
+                p0 = __ffma2_rn(ai, x, p0);                                              \
+        }                                                                                \
+        const float2 sum = __fadd2_rn(p0, p1);                                           \
+        const float2 part = __fadd2_rn(ein, make_float2(-sum.x, -sum.y));                \
+        const float2 na0 = make_float2(-a[0], -a[0]);                                    \
+        R[(u) % M] = __ffma2_rn(na0, R[((u) - 1 + M) % M], part);                        \
+    }
 #pragma unroll
-            for (int i = 0; i < M; ++i) acur[i] = ati[i];
-        } else {
-            load_row_at<float, M>(Ar, acur, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < WR; ++u) {
-            if (u < rows) {  // warp-uniform: only the last window is short
-                float anext[M];
-                if constexpr (!TI) {
-                    if (u + 1 < WR) load_row_at<float, M>(Ar + (u + 1) * M, anext, (u + 1) * M * 4);
-                }
-                const float ev = __shfl_sync(0xffffffffu, u < 16 ? ec0 : ec1, u & 15, 16);
-                // only the zero-state slot sees the excitation (ALU selects)
-                const float2 ein = make_float2(zsx ? ev : 0.f, zsy ? ev : 0.f);
-                // two accumulators over lags M..2, oldest first; freshest lag last
-                float2 p0 = make_float2(0.f, 0.f), p1 = p0;
-#pragma unroll
-                for (int i = M; i >= 2; --i) {
-                    const float2 x = R[(u - i + 2 * M) % M];
-                    const float2 ai = make_float2(acur[i - 1], acur[i - 1]);
-                    if (i & 1)
-                        p1 = __ffma2_rn(ai, x, p1);
-                    else
-                        p0 = __ffma2_rn(ai, x, p0);
-                }
-                const float2 sum = __fadd2_rn(p0, p1);
-                const float2 part = __fadd2_rn(ein, make_float2(-sum.x, -sum.y));
-                const float2 na0 = make_float2(-acur[0], -acur[0]);
-                R[u % M] = __ffma2_rn(na0, R[(u - 1 + M) % M], part);
-                if constexpr (!TI) {
-#pragma unroll
-                    for (int i = 0; i < M; ++i) acur[i] = anext[i];
-                }
-            }
-        }
+        for (int u = 0; u < WR; ++u)
+            if (u < rows) TVLP_BASIS2_STEP(u)  // warp-uniform: only the last window is short
+#undef TVLP_BASIS2_STEP
         __syncwarp();
         fence_proxy_async();
         issue(k + NSTB);
