@@ -242,29 +242,32 @@ def run_b200(args, cfg, rank, world, dist):
     lib.tvlp_profile_enable(0)
     prof = N.profile_dump()
     hbm, peak_kind = peaks()
+    nsteps = max(1, args.steps)
     per_kernel = {}
-    for name, (cnt, tot) in prof.items():
-        avg_ms = tot / max(cnt, 1)
-        per_kernel[name] = {"launches": cnt, "avg_us": round(avg_ms * 1e3, 2),
-                            "share": None}
     tot_all = sum(v[1] for v in prof.values()) or 1.0
     for name, (cnt, tot) in prof.items():
-        per_kernel[name]["share"] = round(tot / tot_all, 4)
+        per_kernel[name] = {"launches_per_step": round(cnt / nsteps, 2),
+                            "us_per_step": round(tot / nsteps * 1e3, 2),
+                            "share": round(tot / tot_all, 4)}
     dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
     roof = None
     if dom is not None:
         bps = kernel_bytes_per_sample(dom, M)
         cnt, tot = prof[dom]
-        avg_s = tot / cnt * 1e-3
-        if bps is not None:
-            ach = bps * B * T / avg_s / 1e9
-            roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm,
-                    "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
-                    "peak_source": peak_kind,
-                    "bytes_per_launch": bps * B * T, "avg_launch_us": round(avg_s * 1e6, 2)}
-        else:
-            roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": hbm,
-                    "unit": "GB/s", "frac": None, "traffic": None}
+        t_step = tot / nsteps * 1e-3  # seconds of this kernel per step (all its slices)
+        ach = (bps * B * T / t_step / 1e9) if bps is not None else None
+        roof = {"bound": "hbm", "kernel": dom,
+                "achieved": None if ach is None else round(ach, 1), "peak": hbm, "unit": "GB/s",
+                "frac": None if ach is None else round(ach / hbm, 4), "traffic": None,
+                "peak_source": peak_kind,
+                "bytes_per_step": None if bps is None else bps * B * T,
+                "us_per_step": round(t_step * 1e6, 2), "launches_per_step": cnt / nsteps}
+        if dom in ("basis",) and kind == "tv":
+            # the basis is FP32-FMA bound: 23 chains x 22 FMA per sample
+            fl = 2.0 * (M + 1) * M * B * T / t_step / 1e12
+            fp32_peak = 148 * 128 * 2 * 1.965e-3  # TFLOP/s at the max SM clock (derived)
+            roof["fp32_tflops"] = round(fl, 2)
+            roof["fp32_frac_of_derived_peak"] = round(fl / fp32_peak, 4)
     step_gbs = algorithmic_bytes_per_sample(cfg) * B * T / (ms * 1e-3) / 1e9
 
     # e2e: pinned host buffers through the public API

@@ -211,6 +211,30 @@ __global__ void k_lag(const IO* __restrict__ s, const IO* __restrict__ zi, IO* _
     }
 }
 
+// ---------------------------------------------------------------- streams
+// One non-blocking auxiliary stream per device for the pipelined forward.
+cudaStream_t aux_stream() {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+    return streams[dev];
+}
+
+// number of batch slices of the pipelined forward ($TVLP_FWD_SLICES overrides)
+int fwd_slices(int64_t B) {
+    int n = B >= 16 ? 4 : 1;
+    if (const char* env = std::getenv("TVLP_FWD_SLICES")) {
+        const int v = std::atoi(env);
+        if (v >= 1) n = v;
+    }
+    if (n > B) n = (int)B;
+    return n;
+}
+
 // ---------------------------------------------------------------- TV / TI
 template <typename IO>
 int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s, const Plan& p,
@@ -259,19 +283,61 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
         zi_p = static_cast<const IO*>(pz);
         s_p = static_cast<IO*>(ps);
     }
-    TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, e_p, A_p, phiz, g, st)));
-    TVLP_RUN("carry_fwd", 1, st,
-             (launch_carry_fwd<IO>(p.Mp, phiz, zi_p, xin, dstat, base_ok(phiz) ? fflags : nullptr,
-                                   g, st)));
-    TVLP_RUN("apply_fwd", 1, st,
-             (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, xend, dstat, nullptr, g,
-                                   st)));
-    if (refine) {
-        TVLP_RUN("refine_fwd", 1, st,
-                 (launch_refine<IO>(p.Mp, true, phiz, xin, xend, dstat, flags, nullptr, g, st)));
-        TVLP_RUN("apply_fwd_refined", 1, st,
-                 (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nullptr, nullptr, nullptr, flags,
-                                       g, st)));
+    // Batch slices pipelined over two streams: the compute-bound basis of
+    // slice k+1 (caller stream) overlaps the latency/HBM-bound carry + apply
+    // of slice k (auxiliary stream).
+    const int nsl = fwd_slices(p.B);
+    cudaStream_t aux = st;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (nsl > 1) {
+        aux = aux_stream();
+        TVLP_CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        TVLP_CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        TVLP_CK(cudaEventRecord(ev_fork, st));
+        TVLP_CK(cudaStreamWaitEvent(aux, ev_fork, 0));
+    }
+    const int64_t mp = mp4(p), TS = tape_elems(p.Mp);
+    for (int sl = 0; sl < nsl; ++sl) {
+        const int64_t b0 = p.B * sl / nsl, b1 = p.B * (sl + 1) / nsl;
+        ScanArgs gs = g;
+        gs.B = b1 - b0;
+        const IO* e_s = e_p + b0 * p.Tp;
+        const IO* A_s = A_p + (ti ? b0 : b0 * p.Tp) * p.Mp;
+        const IO* zi_s = zi_p ? zi_p + b0 * p.Mp : nullptr;
+        IO* s_s = s_p + b0 * p.Tp;
+        IO* tape_s = phiz + b0 * p.nsub * TS;
+        IO* xin_s = xin + b0 * p.nsub * mp;
+        IO* xend_s = xend ? xend + b0 * p.nsub * mp : nullptr;
+        unsigned* dstat_s = dstat ? dstat + 2 * b0 : nullptr;
+        int* flags_s = flags ? flags + b0 : nullptr;
+        int* fflags_s = base_ok(phiz) ? fflags + b0 : nullptr;
+        TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, e_s, A_s, tape_s, gs, st)));
+        if (nsl > 1) {
+            cudaEvent_t ev;
+            TVLP_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            TVLP_CK(cudaEventRecord(ev, st));
+            TVLP_CK(cudaStreamWaitEvent(aux, ev, 0));
+            TVLP_CK(cudaEventDestroy(ev));  // released once the wait has been satisfied
+        }
+        TVLP_RUN("carry_fwd", 1, aux,
+                 (launch_carry_fwd<IO>(p.Mp, tape_s, zi_s, xin_s, dstat_s, fflags_s, gs, aux)));
+        TVLP_RUN("apply_fwd", 1, aux,
+                 (launch_apply_fwd<IO>(p.Mp, ti, e_s, A_s, xin_s, s_s, nonfinite, xend_s, dstat_s,
+                                       nullptr, gs, aux)));
+        if (refine) {
+            TVLP_RUN("refine_fwd", 1, aux,
+                     (launch_refine<IO>(p.Mp, true, tape_s, xin_s, xend_s, dstat_s, flags_s, nullptr,
+                                        gs, aux)));
+            TVLP_RUN("apply_fwd_refined", 1, aux,
+                     (launch_apply_fwd<IO>(p.Mp, ti, e_s, A_s, xin_s, s_s, nullptr, nullptr, nullptr,
+                                           flags_s, gs, aux)));
+        }
+    }
+    if (nsl > 1) {
+        TVLP_CK(cudaEventRecord(ev_join, aux));
+        TVLP_CK(cudaStreamWaitEvent(st, ev_join, 0));
+        TVLP_CK(cudaEventDestroy(ev_fork));
+        TVLP_CK(cudaEventDestroy(ev_join));
     }
     if (packed) TVLP_CK(unpack<IO>(ps, s, p.B, p.T, 1, p.Tp, 1, st));
     return TVLP_OK;

@@ -473,14 +473,17 @@ k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_strid
         for (int u = 0; u < kCB; ++u) {
             const int i = sg * kCB + u;
             if (i < nsteps) {
-                if (lane < M) Xin[(base + i) * MP4 + lane] = x;
-                xs[lane] = lane < M ? x : (CT)0;
-                __syncwarp();
+                // the matrix row does not depend on x: load it before the
+                // broadcast so only STS -> LDS -> FMA chain is serial
                 const CT* tp = sgb + u * TP::SIZE;
                 CT w[MP4], xv[MP4];
                 load_vec<CT, MP4>(tp + (TP::R_ROW + r) * MP4, w);
+                const CT zr = tp[TP::Z_ROW * MP4 + r];
+                if (lane < M) Xin[(base + i) * MP4 + lane] = x;
+                xs[lane] = lane < M ? x : (CT)0;
+                __syncwarp();
                 load_vec<CT, MP4>(xs, xv);
-                const CT xn = dot_rows<M, CT>(w, xv, tp[TP::Z_ROW * MP4 + r]);
+                const CT xn = dot_rows<M, CT>(w, xv, zr);
                 __syncwarp();
                 x = xn;
             }
@@ -553,16 +556,17 @@ k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __
             const int i = sg * kCB + u;
             if (i < nsteps) {
                 const int kk = n - 1 - i;
-                if (lane < M) Mu[(base + kk) * MP4 + lane] = mu;
-                ms[lane] = lane < M ? mu : (CT)0;
-                __syncwarp();
                 const int slot = cnt - 1 - u;  // position of kk inside the stage
                 const CT* tp = reinterpret_cast<const CT*>(dst) + slot * TP::SIZE;
                 const CT* nu = reinterpret_cast<const CT*>(dst + SM::STAGE) + slot * MP4;
                 CT w[MP4], mv[MP4];
                 load_vec<CT, MP4>(tp + r * MP4, w);
+                const CT nur = nu[r];
+                if (lane < M) Mu[(base + kk) * MP4 + lane] = mu;
+                ms[lane] = lane < M ? mu : (CT)0;
+                __syncwarp();
                 load_vec<CT, MP4>(ms, mv);
-                const CT mn = dot_rows<M, CT>(w, mv, nu[r]);
+                const CT mn = dot_rows<M, CT>(w, mv, nur);
                 __syncwarp();
                 mu = mn;
             }
