@@ -224,9 +224,12 @@ cudaStream_t aux_stream() {
     return streams[dev];
 }
 
-// number of batch slices of the pipelined forward ($TVLP_FWD_SLICES overrides)
+// number of batch slices of the pipelined forward ($TVLP_FWD_SLICES
+// overrides).  Measured on B200 at B=64, T=48000: 1 slice 424 us/step, 4
+// slices 631, 8 slices 778 -- the basis kernel is issue-bound per warp, and a
+// quarter batch leaves it latency-bound, so slicing is off by default.
 int fwd_slices(int64_t B) {
-    int n = B >= 16 ? 4 : 1;
+    int n = 1;
     if (const char* env = std::getenv("TVLP_FWD_SLICES")) {
         const int v = std::atoi(env);
         if (v >= 1) n = v;
