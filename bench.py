@@ -47,15 +47,22 @@ CONFIGS = {
     "tv_b4_t24000": dict(kind="tv", B=4, T=24000, M=22, baseline_cfg=1),
     "framewise_b32_t48000": dict(kind="framewise", B=32, T=48000, M=22, hop=240, baseline_cfg=2),
     "tv_b1_t14400000": dict(kind="tv", B=1, T=14_400_000, M=22, baseline_cfg=4),
+    # config 5: HpN decoder's two LPs (H(z) on the glottal source, C(z) on the
+    # noise) grouped into one launch; 256 items over 8 GPUs = 32 items per GPU
+    "hpn_b32_t48000": dict(kind="hpn", B=32, T=48000, M=22, baseline_cfg=5,
+                           encoder_params=6_100_000),
 }
 DEFAULT = "tv_b64_t48000"
 
 
 def algorithmic_bytes_per_sample(cfg):
-    """TV fwd 4(M+2) + bwd 4(2M+3) = 4(3M+5); frame-wise ~21.1."""
+    """SURVEY.md §8(d): TV fwd 4(M+2) + bwd 4(2M+3) = 4(3M+5); frame-wise ~21.1;
+    HpN: two TV LPs per audio sample (568 B)."""
     M = cfg["M"]
     if cfg["kind"] == "tv":
         return 4 * (3 * M + 5)
+    if cfg["kind"] == "hpn":
+        return 2 * 4 * (3 * M + 5)
     return 21.1
 
 
@@ -141,9 +148,10 @@ def cpu_baseline(cfg, seconds=10.0):
 
     nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     T, M = cfg["T"], cfg["M"]
-    if cfg["kind"] == "tv":
+    lps_per_sample = 2 if cfg["kind"] == "hpn" else 1
+    if cfg["kind"] in ("tv", "hpn"):
         T_s = min(T, 480_000)
-        B_s = max(1, min(cfg["B"], 4 * nthreads)) if T <= 480_000 else nthreads
+        B_s = max(1, min(cfg["B"] * lps_per_sample, 4 * nthreads)) if T <= 480_000 else nthreads
         e, A, g = data.d1_batch(1000, B_s, T_s, M)
         kind = "tv"
     else:
@@ -163,8 +171,10 @@ def cpu_baseline(cfg, seconds=10.0):
         if len(times) >= 50:
             break
     med = float(np.median(times))
-    return {"value": B_s * T_s / med, "unit": UNIT, "cores": nthreads, "kind": "port",
-            "sample": f"{B_s} x {T_s} samples (M={M}, D1) fwd+bwd per repeat, median of "
+    return {"value": B_s * T_s / med / lps_per_sample, "unit": UNIT, "cores": nthreads,
+            "kind": "port",
+            "sample": f"{B_s} x {T_s} samples (M={M}, D1) LP fwd+bwd per repeat"
+                      f"{' (2 LPs per audio sample)' if lps_per_sample == 2 else ''}, median of "
                       f"{len(times)} repeats, {nthreads} threads, oracle/tvlp_oracle.c"}
 
 
@@ -177,6 +187,7 @@ def run_b200(args, cfg, rank, world, dist):
 
     from paper_2406_05128_b200 import _native as N
     from paper_2406_05128_b200 import data, lpc, params
+    from paper_2406_05128_b200 import dist as pdist
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
@@ -184,15 +195,30 @@ def run_b200(args, cfg, rank, world, dist):
     lib = N.load()
     B, T, M = cfg["B"], cfg["T"], cfg["M"]
     kind = cfg["kind"]
-    if kind == "tv":
-        e, A, g = data.d1_batch_torch(rank * B, B, T, M, device=dev)
+    lo, hi = pdist.shard(B, rank)
+    allreduce = None
+    if kind in ("tv", "hpn"):
+        if kind == "tv":
+            e, A, g = data.d1_batch_torch(lo, B, T, M, device=dev)
+        else:
+            # grouped launch: rows [0, B) are H(z) on the glottal source, rows
+            # [B, 2B) C(z) on the noise (both D1 tracks, distinct seeds)
+            e, A, g = data.d1_batch_torch(2 * lo, 2 * B, T, M, device=dev)
+            if dist is not None:
+                grad = torch.randn(cfg["encoder_params"], device=dev)
+
+                def allreduce():
+                    return dist.all_reduce(grad, async_op=True)
 
         def step(e=e, A=A, g=g):
             s, carry = lpc._forward(False, e, A, None, return_carry=True)
+            work = allreduce() if allreduce is not None else None
             ge, gA = lpc._backward(False, g, A, s, None, carry)
+            if work is not None:
+                work.wait()
             return s, ge, gA
     else:
-        ev, fr, gv = data.d1_frames_batch(rank * B, B, T, M, cfg["hop"])
+        ev, fr, gv = data.d1_frames_batch(lo, B, T, M, cfg["hop"])
         e = torch.from_numpy(ev).to(dev)
         A = torch.from_numpy(fr).to(dev)
         g = torch.from_numpy(gv).to(dev)
@@ -224,11 +250,7 @@ def run_b200(args, cfg, rank, world, dist):
         torch.cuda.synchronize()
     launches = lib.tvlp_launch_count() - n0
     refined = lib.tvlp_refined_sequences() - r0
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if dist is not None:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = pdist.max_over_ranks(ev0.elapsed_time(ev1) / args.steps, dist, dev)
     nonfinite_seen = lpc.check_nonfinite(dev)
     samples = B * T * world
     value = samples / (ms * 1e-3)
@@ -253,18 +275,19 @@ def run_b200(args, cfg, rank, world, dist):
     roof = None
     if dom is not None:
         bps = kernel_bytes_per_sample(dom, M)
+        lp_rows = 2 * B if kind == "hpn" else B  # LP sequences per GPU
         cnt, tot = prof[dom]
         t_step = tot / nsteps * 1e-3  # seconds of this kernel per step (all its slices)
-        ach = (bps * B * T / t_step / 1e9) if bps is not None else None
+        ach = (bps * lp_rows * T / t_step / 1e9) if bps is not None else None
         roof = {"bound": "hbm", "kernel": dom,
                 "achieved": None if ach is None else round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": None if ach is None else round(ach / hbm, 4), "traffic": None,
                 "peak_source": peak_kind,
-                "bytes_per_step": None if bps is None else bps * B * T,
+                "bytes_per_step": None if bps is None else bps * lp_rows * T,
                 "us_per_step": round(t_step * 1e6, 2), "launches_per_step": cnt / nsteps}
-        if dom in ("basis",) and kind == "tv":
+        if dom in ("basis",) and kind in ("tv", "hpn"):
             # the basis is FP32-FMA bound: 23 chains x 22 FMA per sample
-            fl = 2.0 * (M + 1) * M * B * T / t_step / 1e12
+            fl = 2.0 * (M + 1) * M * lp_rows * T / t_step / 1e12
             fp32_peak = 148 * 128 * 2 * 1.965e-3  # TFLOP/s at the max SM clock (derived)
             roof["fp32_tflops"] = round(fl, 2)
             roof["fp32_frac_of_derived_peak"] = round(fl / fp32_peak, 4)
@@ -293,11 +316,7 @@ def run_b200(args, cfg, rank, world, dist):
         e2e_step()
     ev1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = ev0.elapsed_time(ev1) / args.steps
-    if dist is not None:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = pdist.max_over_ranks(ev0.elapsed_time(ev1) / args.steps, dist, dev)
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
@@ -363,14 +382,9 @@ def main(argv=None):
             print(json.dumps(run_reference(args, cfg)), flush=True)
         return 0
 
-    dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as tdist
+    from paper_2406_05128_b200 import dist as pdist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        tdist.init_process_group("nccl")
-        dist = tdist
+    dist = pdist.init("nccl") if world > 1 else None
     line = run_b200(args, cfg, rank, world, dist)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
