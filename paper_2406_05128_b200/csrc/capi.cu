@@ -115,8 +115,140 @@ ScanArgs scan_args(const Plan& p) {
 // carry tape: per-sub-chunk tapes followed by one forward-refinement flag per
 // sequence (an int stored in the first bytes of a B-element trailing region)
 int64_t tape_body(const Plan& p) { return p.B * (int64_t)p.nsub * tape_elems(p.Mp); }
-int64_t carry_elems(const Plan& p) { return tape_body(p) + p.B; }
 inline int64_t mp4(const Plan& p) { return (p.Mp + 3) / 4 * 4; }
+
+// Hierarchical carry: chains longer than kSerialMax sub-chunks are cut into
+// groups of kGroup whose products P_g form the next level (SURVEY.md §5 "long
+// context"), recursively.  Level-l group tapes live in the carry tape after
+// the level-0 tapes and the per-sequence flag slots, so the backward reuses
+// the forward's group products.
+constexpr int kSerialMax = 256;
+constexpr int kGroup = 32;
+struct Levels {
+    int L = 1;
+    int64_t n[8] = {};
+    int64_t off[8] = {};  // element offset of level-l tapes in the carry tape
+};
+Levels make_levels(const Plan& p) {
+    Levels v;
+    v.n[0] = p.nsub;
+    v.off[0] = 0;
+    int64_t cur = tape_body(p) + p.B;
+    while (v.n[v.L - 1] > kSerialMax && v.L < 8) {
+        v.n[v.L] = (v.n[v.L - 1] + kGroup - 1) / kGroup;
+        v.off[v.L] = cur;
+        cur += p.B * v.n[v.L] * tape_elems(p.Mp);
+        ++v.L;
+    }
+    return v;
+}
+int64_t carry_elems(const Plan& p) {
+    const Levels v = make_levels(p);
+    int64_t tot = tape_body(p) + p.B;
+    for (int l = 1; l < v.L; ++l) tot += p.B * v.n[l] * tape_elems(p.Mp);
+    return tot;
+}
+
+template <typename IO>
+struct Hier {
+    const Plan* p;
+    Levels lv;
+    IO* tape;           // carry tape base
+    IO* U[8] = {};      // per level >= 1: group forcing / tails
+    IO* V[8] = {};      // per level >= 1: group states
+    const int* only = nullptr;
+    cudaStream_t st = nullptr;
+
+    IO* tape_l(int l) const { return tape + lv.off[l]; }
+    CarryArgs<IO> args(int l) const {
+        CarryArgs<IO> a{};
+        a.tape = tape_l(l);
+        a.nsub = (int)lv.n[l];
+        a.only = only;
+        return a;
+    }
+    // x(k+1) = Phi_k x(k) + f_k on level l (f = tape z rows if force == null)
+    cudaError_t fwd(int l, const IO* force, const IO* x0, int64_t x0s, IO* X, unsigned* dstat,
+                    int* fflags) const {
+        const int64_t B = p->B;
+        if (l == lv.L - 1) {
+            CarryArgs<IO> a = args(l);
+            a.force = force;
+            a.x0 = x0;
+            a.x0_stride = x0s;
+            a.X = X;
+            a.nseg = B;
+            a.seglen = a.nsub;
+            a.dstat = dstat;
+            a.fflags = fflags;
+            return launch_carry_fwd<IO>(p->Mp, a, st);
+        }
+        const int TS = tape_elems(p->Mp);
+        CarryArgs<IO> t = args(l);  // group tails (zero-state group outputs)
+        t.force = force;
+        t.nseg = B * lv.n[l + 1];
+        t.seglen = kGroup;
+        t.dstat = dstat;
+        t.fflags = fflags;
+        if (force == nullptr) {
+            t.tail = tape_l(l + 1) + (int64_t)p->Mp * mp4(*p);  // z row (Tape::Z_ROW = M)
+            t.tail_stride = TS;
+        } else {
+            t.tail = U[l + 1];
+            t.tail_stride = mp4(*p);
+        }
+        cudaError_t err = launch_carry_fwd<IO>(p->Mp, t, st);
+        if (err != cudaSuccess) return err;
+        err = fwd(l + 1, force == nullptr ? nullptr : U[l + 1], x0, x0s, V[l + 1], nullptr, nullptr);
+        if (err != cudaSuccess) return err;
+        CarryArgs<IO> e = args(l);  // expansion inside each group
+        e.force = force;
+        e.x0 = V[l + 1];
+        e.x0_stride = mp4(*p);
+        e.X = X;
+        e.nseg = B * lv.n[l + 1];
+        e.seglen = kGroup;
+        return launch_carry_fwd<IO>(p->Mp, e, st);
+    }
+    // mu(k-1) = Phi_k^T mu(k) + nu_k on level l
+    cudaError_t bwd(int l, const IO* nu, IO* X) const {
+        const int64_t B = p->B;
+        if (l == lv.L - 1) {
+            CarryArgs<IO> a = args(l);
+            a.force = nu;
+            a.X = X;
+            a.nseg = B;
+            a.seglen = a.nsub;
+            return launch_carry_bwd<IO>(p->Mp, a, st);
+        }
+        CarryArgs<IO> t = args(l);
+        t.force = nu;
+        t.tail = U[l + 1];
+        t.tail_stride = mp4(*p);
+        t.nseg = B * lv.n[l + 1];
+        t.seglen = kGroup;
+        cudaError_t err = launch_carry_bwd<IO>(p->Mp, t, st);
+        if (err != cudaSuccess) return err;
+        err = bwd(l + 1, U[l + 1], V[l + 1]);
+        if (err != cudaSuccess) return err;
+        CarryArgs<IO> e = args(l);
+        e.force = nu;
+        e.x0 = V[l + 1];
+        e.x0_stride = mp4(*p);
+        e.X = X;
+        e.nseg = B * lv.n[l + 1];
+        e.seglen = kGroup;
+        return launch_carry_bwd<IO>(p->Mp, e, st);
+    }
+    cudaError_t compose() const {  // group products of every level
+        for (int l = 0; l + 1 < lv.L; ++l) {
+            cudaError_t err = launch_group_P<IO>(p->Mp, tape_l(l), tape_l(l + 1),
+                                                 p->B * lv.n[l + 1], kGroup, (int)lv.n[l], only, st);
+            if (err != cudaSuccess) return err;
+        }
+        return cudaSuccess;
+    }
+};
 
 // bump allocator over the caller's workspace (nullptr base = sizing pass)
 struct Carver {
@@ -211,33 +343,6 @@ __global__ void k_lag(const IO* __restrict__ s, const IO* __restrict__ zi, IO* _
     }
 }
 
-// ---------------------------------------------------------------- streams
-// One non-blocking auxiliary stream per device for the pipelined forward.
-cudaStream_t aux_stream() {
-    static std::mutex mu;
-    static cudaStream_t streams[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(mu);
-    if (dev < 0 || dev >= 64) return nullptr;
-    if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-    return streams[dev];
-}
-
-// number of batch slices of the pipelined forward ($TVLP_FWD_SLICES
-// overrides).  Measured on B200 at B=64, T=48000: 1 slice 424 us/step, 4
-// slices 631, 8 slices 778 -- the basis kernel is issue-bound per warp, and a
-// quarter batch leaves it latency-bound, so slicing is off by default.
-int fwd_slices(int64_t B) {
-    int n = 1;
-    if (const char* env = std::getenv("TVLP_FWD_SLICES")) {
-        const int v = std::atoi(env);
-        if (v >= 1) n = v;
-    }
-    if (n > B) n = (int)B;
-    return n;
-}
-
 // ---------------------------------------------------------------- TV / TI
 template <typename IO>
 int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s, const Plan& p,
@@ -248,15 +353,29 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     const bool packed = p.Tp != p.T || p.Mp != p.M || !aligned16(e) || !aligned16(A) ||
                         !aligned16(s) || (zi && !aligned16(zi));
     const int64_t nsc = p.B * p.nsub;
+    const int64_t mp = mp4(p);
+    Hier<IO> h;
+    h.p = &p;
+    h.lv = make_levels(p);
+    h.st = st;
     Carver c(ws);
     IO* phiz = carry ? carry : static_cast<IO*>(c.take(carry_elems(p) * sz));
-    IO* xin = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
-    // precision "auto": fp32 chains + boundary-defect check + refinement
-    const bool refine = prec == kPrecAuto && sizeof(IO) == 4;
-    IO* xend = refine ? static_cast<IO*>(c.take(nsc * mp4(p) * sz)) : nullptr;
-    int* fflags = reinterpret_cast<int*>(phiz + tape_body(p));  // lives in the carry tape
+    h.tape = phiz;
+    IO* xin = static_cast<IO*>(c.take(nsc * mp * sz));
+    for (int l = 1; l < h.lv.L; ++l) {
+        h.U[l] = static_cast<IO*>(c.take(p.B * h.lv.n[l] * mp * sz));
+        h.V[l] = static_cast<IO*>(c.take(p.B * h.lv.n[l] * mp * sz));
+    }
+    // precision "auto": fp32 chains + boundary-defect check + refinement (long,
+    // hierarchical chains are always checked: their group products are fp32)
+    const bool hier = h.lv.L > 1;
+    const bool refine = sizeof(IO) == 4 && (prec == kPrecAuto || hier);
+    IO* xend = refine ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
+    int* fflags = reinterpret_cast<int*>(phiz + tape_body(p));  // flag slots in the carry tape
     int* flags = refine ? fflags : nullptr;
     unsigned* dstat = refine ? static_cast<unsigned*>(c.take(p.B * 2 * sizeof(unsigned))) : nullptr;
+    IO* D0 = (refine && hier) ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
+    IO* E0 = (refine && hier) ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
     const IO* e_p = static_cast<const IO*>(e);
     const IO* A_p = static_cast<const IO*>(A);
     const IO* zi_p = static_cast<const IO*>(zi);
@@ -286,61 +405,39 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
         zi_p = static_cast<const IO*>(pz);
         s_p = static_cast<IO*>(ps);
     }
-    // Batch slices pipelined over two streams: the compute-bound basis of
-    // slice k+1 (caller stream) overlaps the latency/HBM-bound carry + apply
-    // of slice k (auxiliary stream).
-    const int nsl = fwd_slices(p.B);
-    cudaStream_t aux = st;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    if (nsl > 1) {
-        aux = aux_stream();
-        TVLP_CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-        TVLP_CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-        TVLP_CK(cudaEventRecord(ev_fork, st));
-        TVLP_CK(cudaStreamWaitEvent(aux, ev_fork, 0));
-    }
-    const int64_t mp = mp4(p), TS = tape_elems(p.Mp);
-    for (int sl = 0; sl < nsl; ++sl) {
-        const int64_t b0 = p.B * sl / nsl, b1 = p.B * (sl + 1) / nsl;
-        ScanArgs gs = g;
-        gs.B = b1 - b0;
-        const IO* e_s = e_p + b0 * p.Tp;
-        const IO* A_s = A_p + (ti ? b0 : b0 * p.Tp) * p.Mp;
-        const IO* zi_s = zi_p ? zi_p + b0 * p.Mp : nullptr;
-        IO* s_s = s_p + b0 * p.Tp;
-        IO* tape_s = phiz + b0 * p.nsub * TS;
-        IO* xin_s = xin + b0 * p.nsub * mp;
-        IO* xend_s = xend ? xend + b0 * p.nsub * mp : nullptr;
-        unsigned* dstat_s = dstat ? dstat + 2 * b0 : nullptr;
-        int* flags_s = flags ? flags + b0 : nullptr;
-        int* fflags_s = base_ok(phiz) ? fflags + b0 : nullptr;
-        TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, e_s, A_s, tape_s, gs, st)));
-        if (nsl > 1) {
-            cudaEvent_t ev;
-            TVLP_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            TVLP_CK(cudaEventRecord(ev, st));
-            TVLP_CK(cudaStreamWaitEvent(aux, ev, 0));
-            TVLP_CK(cudaEventDestroy(ev));  // released once the wait has been satisfied
+    const int bprec = (prec == kPrecAuto || prec == kPrecF32Chains) ? prec : kPrecF64Chains;
+    TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, bprec, e_p, A_p, phiz, g, st)));
+    if (hier) TVLP_RUN("compose", h.lv.L - 1, st, (h.compose()));
+    TVLP_RUN("carry_fwd", 1, st, (h.fwd(0, nullptr, zi_p, p.Mp, xin, dstat, fflags)));
+    TVLP_RUN("apply_fwd", 1, st,
+             (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, xend, dstat, nullptr, g,
+                                   st)));
+    if (refine) {
+        if (!hier) {
+            TVLP_RUN("refine_fwd", 1, st,
+                     (launch_refine<IO>(p.Mp, true, phiz, xin, xend, dstat, flags, nullptr, g, st)));
+        } else {
+            // decide, defects D = Xend - Xin(next), corrections E through the
+            // same hierarchy (forced by D), Xin += E -- flagged sequences only
+            TVLP_RUN("refine_fwd", 4, st, ([&]() -> cudaError_t {
+                cudaError_t err = launch_refine_helpers<IO>(0, p.Mp, nullptr, nullptr, nullptr,
+                                                            p.nsub, true, nullptr, flags, dstat,
+                                                            nullptr, kDefectTol, p.B, st);
+                if (err != cudaSuccess) return err;
+                err = launch_refine_helpers<IO>(1, p.Mp, xend, xin, D0, p.nsub, true, flags,
+                                                nullptr, nullptr, nullptr, 0.f, p.B, st);
+                if (err != cudaSuccess) return err;
+                Hier<IO> hr = h;
+                hr.only = flags;
+                err = hr.fwd(0, D0, nullptr, 0, E0, nullptr, nullptr);
+                if (err != cudaSuccess) return err;
+                return launch_refine_helpers<IO>(2, p.Mp, xin, E0, nullptr, p.nsub, true, flags,
+                                                 nullptr, nullptr, nullptr, 0.f, p.B, st);
+            }()));
         }
-        TVLP_RUN("carry_fwd", 1, aux,
-                 (launch_carry_fwd<IO>(p.Mp, tape_s, zi_s, xin_s, dstat_s, fflags_s, gs, aux)));
-        TVLP_RUN("apply_fwd", 1, aux,
-                 (launch_apply_fwd<IO>(p.Mp, ti, e_s, A_s, xin_s, s_s, nonfinite, xend_s, dstat_s,
-                                       nullptr, gs, aux)));
-        if (refine) {
-            TVLP_RUN("refine_fwd", 1, aux,
-                     (launch_refine<IO>(p.Mp, true, tape_s, xin_s, xend_s, dstat_s, flags_s, nullptr,
-                                        gs, aux)));
-            TVLP_RUN("apply_fwd_refined", 1, aux,
-                     (launch_apply_fwd<IO>(p.Mp, ti, e_s, A_s, xin_s, s_s, nullptr, nullptr, nullptr,
-                                           flags_s, gs, aux)));
-        }
-    }
-    if (nsl > 1) {
-        TVLP_CK(cudaEventRecord(ev_join, aux));
-        TVLP_CK(cudaStreamWaitEvent(st, ev_join, 0));
-        TVLP_CK(cudaEventDestroy(ev_fork));
-        TVLP_CK(cudaEventDestroy(ev_join));
+        TVLP_RUN("apply_fwd_refined", 1, st,
+                 (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nullptr, nullptr, nullptr, flags,
+                                       g, st)));
     }
     if (packed) TVLP_CK(unpack<IO>(ps, s, p.B, p.T, 1, p.Tp, 1, st));
     return TVLP_OK;
@@ -363,17 +460,29 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
                         !aligned16(s) || !aligned16(ge) || (!ti && !aligned16(gA)) ||
                         (zi && !aligned16(zi));
     const int64_t nsc = p.B * p.nsub;
+    const int64_t mp = mp4(p);
+    Hier<IO> h;
+    h.p = &p;
+    h.lv = make_levels(p);
+    h.st = st;
+    const bool hier = h.lv.L > 1;
     Carver c(ws);
     IO* phiz_own = carry ? nullptr : static_cast<IO*>(c.take(carry_elems(p) * sz));
-    IO* nu = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
-    IO* mu = static_cast<IO*>(c.take(nsc * mp4(p) * sz));
+    IO* nu = static_cast<IO*>(c.take(nsc * mp * sz));
+    IO* mu = static_cast<IO*>(c.take(nsc * mp * sz));
+    for (int l = 1; l < h.lv.L; ++l) {
+        h.U[l] = static_cast<IO*>(c.take(p.B * h.lv.n[l] * mp * sz));
+        h.V[l] = static_cast<IO*>(c.take(p.B * h.lv.n[l] * mp * sz));
+    }
     // without the forward's tape (and its per-sequence refinement flags) the
     // backward recomputes the transition matrices with fp64 chains
     if (carry == nullptr && prec == kPrecAuto) prec = kPrecF64Chains;
-    const bool refine = prec == kPrecAuto && sizeof(IO) == 4;
-    IO* kout = refine ? static_cast<IO*>(c.take(nsc * mp4(p) * sz)) : nullptr;
+    const bool refine = sizeof(IO) == 4 && (prec == kPrecAuto || hier);
+    IO* kout = refine ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
     int* flags = refine ? static_cast<int*>(c.take(p.B * sizeof(int))) : nullptr;
     unsigned* dstat = refine ? static_cast<unsigned*>(c.take(p.B * 2 * sizeof(unsigned))) : nullptr;
+    IO* D0 = (refine && hier) ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
+    IO* E0 = (refine && hier) ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
     const int nchunk = grad_a_chunks(p);
     IO* part = ti ? static_cast<IO*>(c.take(p.B * (int64_t)nchunk * p.Mp * sz)) : nullptr;
     IO* ga_p = (ti && p.Mp != p.M) ? static_cast<IO*>(c.take(p.B * p.Mp * sz)) : nullptr;
@@ -414,32 +523,51 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
         ge_p = static_cast<IO*>(pge);
         gA_p = static_cast<IO*>(pgA);
     }
-    const IO* phiz = carry;
-    if (!phiz) {
+    h.tape = carry ? const_cast<IO*>(carry) : phiz_own;
+    if (!carry) {
         // transition matrices only (the zero-state row is unused here; s is a
         // valid stand-in for e of the same shape)
         TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, s_p, A_p, phiz_own, g, st)));
-        phiz = phiz_own;
+        if (hier) TVLP_RUN("compose", h.lv.L - 1, st, (h.compose()));
     }
     TVLP_RUN("adjoint_zs", 1, st,
              (launch_adjoint<IO>(p.Mp, ti, 0, gs_p, A_p, nullptr, nu, nullptr, nullptr, nullptr, g,
                                  st)));
-    TVLP_RUN("carry_bwd", 1, st, (launch_carry_bwd<IO>(p.Mp, phiz, nu, mu, dstat, g, st)));
+    if (dstat) TVLP_CK(cudaMemsetAsync(dstat, 0, p.B * 2 * sizeof(unsigned), st));
+    TVLP_RUN("carry_bwd", 1, st, (h.bwd(0, nu, mu)));
     TVLP_RUN("adjoint_apply", 1, st,
              (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, kout, ge_p, dstat, nullptr, g, st)));
     if (refine) {
-        TVLP_RUN("refine_bwd", 1, st,
-                 (launch_refine<IO>(p.Mp, false, phiz, mu, kout, dstat, flags,
-                                    carry ? reinterpret_cast<const int*>(carry + tape_body(p))
-                                          : nullptr,
-                                    g, st)));
+        const int* inherit = carry ? reinterpret_cast<const int*>(carry + tape_body(p)) : nullptr;
+        if (!hier) {
+            TVLP_RUN("refine_bwd", 1, st,
+                     (launch_refine<IO>(p.Mp, false, h.tape, mu, kout, dstat, flags, inherit, g,
+                                        st)));
+        } else {
+            TVLP_RUN("refine_bwd", 4, st, ([&]() -> cudaError_t {
+                cudaError_t err = launch_refine_helpers<IO>(0, p.Mp, nullptr, nullptr, nullptr,
+                                                            p.nsub, false, nullptr, flags, dstat,
+                                                            inherit, kDefectTolBwd, p.B, st);
+                if (err != cudaSuccess) return err;
+                err = launch_refine_helpers<IO>(1, p.Mp, kout, mu, D0, p.nsub, false, flags,
+                                                nullptr, nullptr, nullptr, 0.f, p.B, st);
+                if (err != cudaSuccess) return err;
+                Hier<IO> hr = h;
+                hr.only = flags;
+                err = hr.bwd(0, D0, E0);
+                if (err != cudaSuccess) return err;
+                return launch_refine_helpers<IO>(2, p.Mp, mu, E0, nullptr, p.nsub, false, flags,
+                                                 nullptr, nullptr, nullptr, 0.f, p.B, st);
+            }()));
+        }
         TVLP_RUN("adjoint_apply_refined", 1, st,
                  (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, nullptr, flags, g,
                                      st)));
     }
     if (ti) {
         IO* ga_out = ga_p ? ga_p : static_cast<IO*>(gA);
-        TVLP_RUN("grad_a", 2, st, (launch_grad_a<IO>(p.Mp, ge_p, s_p, zi_p, part, ga_out, p.B, p.Tp, nchunk, st)));
+        TVLP_RUN("grad_a", 2, st,
+                 (launch_grad_a<IO>(p.Mp, ge_p, s_p, zi_p, part, ga_out, p.B, p.Tp, nchunk, st)));
         if (ga_p) TVLP_CK(unpack<IO>(ga_p, gA, p.B, 1, p.M, 1, p.Mp, st));
     } else {
         TVLP_RUN("grad_A", 1, st, (launch_grad_A<IO>(p.Mp, ge_p, s_p, zi_p, gA_p, p.B, p.Tp, st)));

@@ -416,15 +416,31 @@ struct CarrySmem {
     static constexpr int BYTES = kCS * (STAGE + NU) + 32 * (int)sizeof(CT) + kCS * 8;
 };
 
-// Forward carry over segments: segment s = (sequence b, first sub-chunk k0,
-// count n); x(k0) = x0[s] (or zero), x(k+1) = Phi_k x(k) + z_k.  Writes
-// Xin[k] (row stride MP4) for every sub-chunk of the segment.  One warp per
-// CTA; whole tapes of kCB consecutive sub-chunks arrive per bulk copy.
+// Arguments of the carry recurrences.  A "segment" is a run of consecutive
+// sub-chunks (or groups) of one sequence: the whole sequence in the one-level
+// scheme, one group in the expansion step of the hierarchical scheme.
+template <typename CT>
+struct CarryArgs {
+    const CT* tape;      // [B*nsub][Tape<M>::SIZE]
+    const CT* force;     // fwd: nullable override of the tape's z rows; bwd: nu. [B*nsub][MP4]
+    const CT* x0;        // nullable initial state per segment (fwd: left end, bwd: right end)
+    int64_t x0_stride;
+    CT* X;               // nullable: fwd state at each sub-chunk start / bwd carry into each sub-chunk
+    CT* tail;            // nullable: state past the segment (fwd: after its last sub-chunk,
+                         // bwd: left of its first sub-chunk), one row per segment
+    int64_t tail_stride;
+    int64_t nseg;
+    int seglen, nsub;
+    unsigned* dstat;     // fwd only: zeroed per sequence (defect statistics of "auto")
+    int* fflags;         // fwd only: zeroed per sequence (forward refinement flags)
+    const int* only;     // nullable: per-sequence flags; other sequences' segments return
+};
+
+// Forward carry: x(k0) = x0 (or zero), x(k+1) = Phi_k x(k) + z_k.  One warp per
+// segment (one CTA); whole tapes of kCB consecutive sub-chunks per bulk copy.
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
-k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_stride,
-            CT* __restrict__ Xin, int64_t nseg, int seglen, int nsub,
-            unsigned* __restrict__ dstat, int* __restrict__ fflags) {
+k_carry_fwd(const CarryArgs<CT> a) {
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
@@ -433,14 +449,15 @@ k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_strid
     CT* xs = reinterpret_cast<CT*>(smem + kCS * (SM::STAGE + SM::NU));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kCS * (SM::STAGE + SM::NU) + 32 * sizeof(CT));
     const int64_t sidx = blockIdx.x;
-    if (sidx >= nseg) return;
-    const int nper = (nsub + seglen - 1) / seglen;  // segments per sequence
+    if (sidx >= a.nseg) return;
+    const int nper = (a.nsub + a.seglen - 1) / a.seglen;  // segments per sequence
     const int64_t b = sidx / nper;
-    const int k0 = (int)(sidx % nper) * seglen;
-    const int n = min(seglen, nsub - k0);
-    const int64_t base = b * nsub + k0;
+    if (a.only != nullptr && a.only[b] == 0) return;
+    const int k0 = (int)(sidx % nper) * a.seglen;
+    const int n = min(a.seglen, a.nsub - k0);
+    const int64_t base = b * a.nsub + k0;
     const int r = lane < M ? lane : 0;
-    const int nsteps = n - 1;  // mat-vecs needed
+    const int nsteps = a.tail != nullptr ? n : n - 1;  // mat-vecs needed
     const int nst = (nsteps + kCB - 1) / kCB;
     if (lane == 0) {
         for (int i = 0; i < kCS; ++i) mbar_init(&bars[i], 1);
@@ -451,24 +468,29 @@ k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_strid
         if (lane == 0 && sg < nst) {
             const int st = sg % kCS;
             const int cnt = min(kCB, nsteps - sg * kCB);
-            mbar_arrive_expect_tx(&bars[st], cnt * SM::SUB);
-            tma_load_1d(smem + st * (SM::STAGE + SM::NU), tape + (base + sg * kCB) * TP::SIZE,
-                        cnt * SM::SUB, &bars[st]);
+            unsigned char* dst = smem + st * (SM::STAGE + SM::NU);
+            mbar_arrive_expect_tx(&bars[st], cnt * (SM::SUB + (a.force ? MP4 * (int)sizeof(CT) : 0)));
+            tma_load_1d(dst, a.tape + (base + sg * kCB) * TP::SIZE, cnt * SM::SUB, &bars[st]);
+            if (a.force)
+                tma_load_1d(dst + SM::STAGE, a.force + (base + sg * kCB) * MP4,
+                            cnt * MP4 * sizeof(CT), &bars[st]);
         }
     };
     for (int i = 0; i < kCS; ++i) issue(i);
     if (lane == 0 && k0 == 0) {
-        if (dstat != nullptr) {
-            dstat[2 * b] = 0u;
-            dstat[2 * b + 1] = 0u;
+        if (a.dstat != nullptr) {
+            a.dstat[2 * b] = 0u;
+            a.dstat[2 * b + 1] = 0u;
         }
-        if (fflags != nullptr) fflags[b] = 0;  // set by k_refine_fwd in precision "auto"
+        if (a.fflags != nullptr) a.fflags[b] = 0;  // set by k_refine_fwd in precision "auto"
     }
-    CT x = (x0 != nullptr && lane < M) ? x0[sidx * x0_stride + lane] : (CT)0;
+    CT x = (a.x0 != nullptr && lane < M) ? a.x0[sidx * a.x0_stride + lane] : (CT)0;
     for (int sg = 0; sg < nst; ++sg) {
         const int st = sg % kCS;
         mbar_wait(&bars[st], (uint32_t)((sg / kCS) & 1));
-        const CT* sgb = reinterpret_cast<const CT*>(smem + st * (SM::STAGE + SM::NU));
+        const unsigned char* dst = smem + st * (SM::STAGE + SM::NU);
+        const CT* sgb = reinterpret_cast<const CT*>(dst);
+        const CT* fgb = reinterpret_cast<const CT*>(dst + SM::STAGE);
 #pragma unroll
         for (int u = 0; u < kCB; ++u) {
             const int i = sg * kCB + u;
@@ -478,8 +500,8 @@ k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_strid
                 const CT* tp = sgb + u * TP::SIZE;
                 CT w[MP4], xv[MP4];
                 load_vec<CT, MP4>(tp + (TP::R_ROW + r) * MP4, w);
-                const CT zr = tp[TP::Z_ROW * MP4 + r];
-                if (lane < M) Xin[(base + i) * MP4 + lane] = x;
+                const CT zr = a.force ? fgb[u * MP4 + r] : tp[TP::Z_ROW * MP4 + r];
+                if (a.X != nullptr && lane < M) a.X[(base + i) * MP4 + lane] = x;
                 xs[lane] = lane < M ? x : (CT)0;
                 __syncwarp();
                 load_vec<CT, MP4>(xs, xv);
@@ -492,17 +514,19 @@ k_carry_fwd(const CT* __restrict__ tape, const CT* __restrict__ x0, int x0_strid
         __syncwarp();
         issue(sg + kCS);
     }
-    if (lane < M) Xin[(base + n - 1) * MP4 + lane] = x;
+    if (lane < M) {
+        if (a.tail != nullptr)
+            a.tail[sidx * a.tail_stride + lane] = x;
+        else if (a.X != nullptr)
+            a.X[(base + n - 1) * MP4 + lane] = x;
+    }
 }
 
-// Adjoint carry over segments (right to left): mu(k_last) = m0[s] (or zero),
-// mu(k-1) = Phi_k^T mu(k) + nu_k.  Writes Mu[k] = carry into sub-chunk k.
-// Nu/Mu rows have stride MP4.
+// Adjoint carry (right to left): mu(k_last) = x0 (or zero),
+// mu(k-1) = Phi_k^T mu(k) + nu_k.  X[k] = carry into sub-chunk k from the right.
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
-k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __restrict__ m0,
-            int m0_stride, CT* __restrict__ Mu, int64_t nseg, int seglen, int nsub,
-            unsigned* __restrict__ dstat) {
+k_carry_bwd(const CarryArgs<CT> a) {
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
@@ -511,17 +535,18 @@ k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __
     CT* ms = reinterpret_cast<CT*>(smem + kCS * (SM::STAGE + SM::NU));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kCS * (SM::STAGE + SM::NU) + 32 * sizeof(CT));
     const int64_t sidx = blockIdx.x;
-    if (sidx >= nseg) return;
-    const int nper = (nsub + seglen - 1) / seglen;
+    if (sidx >= a.nseg) return;
+    const int nper = (a.nsub + a.seglen - 1) / a.seglen;
     const int64_t b = sidx / nper;
-    const int k0 = (int)(sidx % nper) * seglen;
-    const int n = min(seglen, nsub - k0);
-    const int64_t base = b * nsub + k0;
+    if (a.only != nullptr && a.only[b] == 0) return;
+    const int k0 = (int)(sidx % nper) * a.seglen;
+    const int n = min(a.seglen, a.nsub - k0);
+    const int64_t base = b * a.nsub + k0;
     const int r = lane < M ? lane : 0;
-    // mat-vec i (i = 0..n-2) uses sub-chunk kk = n-1-i; stage sg holds
-    // sub-chunks kk = n-1-sg*kCB-u for u = 0..kCB-1 (descending), i.e. the
-    // contiguous tape range [hi-cnt+1, hi] with hi = n-1-sg*kCB.
-    const int nsteps = n - 1;
+    // mat-vec i uses sub-chunk kk = n-1-i (kk >= 1, or >= 0 with a tail);
+    // stage sg holds sub-chunks kk = n-1-sg*kCB-u (descending), i.e. the
+    // contiguous range [hi-cnt+1, hi] with hi = n-1-sg*kCB.
+    const int nsteps = a.tail != nullptr ? n : n - 1;
     const int nst = (nsteps + kCB - 1) / kCB;
     if (lane == 0) {
         for (int i = 0; i < kCS; ++i) mbar_init(&bars[i], 1);
@@ -535,17 +560,13 @@ k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __
             const int lo = n - sg * kCB - cnt;  // lowest sub-chunk of the stage
             unsigned char* dst = smem + st * (SM::STAGE + SM::NU);
             mbar_arrive_expect_tx(&bars[st], cnt * (SM::SUB + MP4 * (int)sizeof(CT)));
-            tma_load_1d(dst, tape + (base + lo) * TP::SIZE, cnt * SM::SUB, &bars[st]);
-            tma_load_1d(dst + SM::STAGE, Nu + (base + lo) * MP4, cnt * MP4 * sizeof(CT),
+            tma_load_1d(dst, a.tape + (base + lo) * TP::SIZE, cnt * SM::SUB, &bars[st]);
+            tma_load_1d(dst + SM::STAGE, a.force + (base + lo) * MP4, cnt * MP4 * sizeof(CT),
                         &bars[st]);
         }
     };
     for (int i = 0; i < kCS; ++i) issue(i);
-    if (dstat != nullptr && lane == 0 && k0 == 0) {
-        dstat[2 * b] = 0u;
-        dstat[2 * b + 1] = 0u;
-    }
-    CT mu = (m0 != nullptr && lane < M) ? m0[sidx * m0_stride + lane] : (CT)0;
+    CT mu = (a.x0 != nullptr && lane < M) ? a.x0[sidx * a.x0_stride + lane] : (CT)0;
     for (int sg = 0; sg < nst; ++sg) {
         const int st = sg % kCS;
         mbar_wait(&bars[st], (uint32_t)((sg / kCS) & 1));
@@ -562,7 +583,7 @@ k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __
                 CT w[MP4], mv[MP4];
                 load_vec<CT, MP4>(tp + r * MP4, w);
                 const CT nur = nu[r];
-                if (lane < M) Mu[(base + kk) * MP4 + lane] = mu;
+                if (a.X != nullptr && lane < M) a.X[(base + kk) * MP4 + lane] = mu;
                 ms[lane] = lane < M ? mu : (CT)0;
                 __syncwarp();
                 load_vec<CT, MP4>(ms, mv);
@@ -575,7 +596,92 @@ k_carry_bwd(const CT* __restrict__ tape, const CT* __restrict__ Nu, const CT* __
         __syncwarp();
         issue(sg + kCS);
     }
-    if (lane < M) Mu[base * MP4 + lane] = mu;
+    if (lane < M) {
+        if (a.tail != nullptr)
+            a.tail[sidx * a.tail_stride + lane] = mu;
+        else if (a.X != nullptr)
+            a.X[base * MP4 + lane] = mu;
+    }
+}
+
+// Group product for the hierarchical carry: P_g = Phi_{k1-1} ... Phi_{k0} over
+// a group of G consecutive sub-chunks, written in the tape layout (W rows =
+// columns, R rows = rows; the z row is filled by a k_carry_fwd tail pass).
+// One warp per group; lane c < M owns column c of the running product, the
+// factor's rows are broadcast from a shared-memory ring.
+template <int M, typename CT>
+__global__ void __launch_bounds__(32)
+k_group_P(const CT* __restrict__ tape, CT* __restrict__ gtape, int64_t ngroups, int G, int nsub,
+          const int* __restrict__ only) {
+    using TP = Tape<M>;
+    using SM = CarrySmem<M, CT>;
+    constexpr int MP4 = TP::MP4;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kCS * (SM::STAGE + SM::NU) + 32 * sizeof(CT));
+    const int64_t gi = blockIdx.x;
+    if (gi >= ngroups) return;
+    const int ng = (nsub + G - 1) / G;
+    const int64_t b = gi / ng;
+    if (only != nullptr && only[b] == 0) return;
+    const int k0 = (int)(gi % ng) * G;
+    const int n = min(G, nsub - k0);
+    const int64_t base = b * nsub + k0;
+    const int nst = (n + kCB - 1) / kCB;
+    if (lane == 0) {
+        for (int i = 0; i < kCS; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    auto issue = [&](int sg) {
+        if (lane == 0 && sg < nst) {
+            const int st = sg % kCS;
+            const int cnt = min(kCB, n - sg * kCB);
+            mbar_arrive_expect_tx(&bars[st], cnt * SM::SUB);
+            tma_load_1d(smem + st * (SM::STAGE + SM::NU), tape + (base + sg * kCB) * TP::SIZE,
+                        cnt * SM::SUB, &bars[st]);
+        }
+    };
+    for (int i = 0; i < kCS; ++i) issue(i);
+    CT col[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) col[i] = (lane == i) ? (CT)1 : (CT)0;
+    for (int sg = 0; sg < nst; ++sg) {
+        const int st = sg % kCS;
+        mbar_wait(&bars[st], (uint32_t)((sg / kCS) & 1));
+        const CT* sgb = reinterpret_cast<const CT*>(smem + st * (SM::STAGE + SM::NU));
+        const int cnt = min(kCB, n - sg * kCB);
+        for (int u = 0; u < cnt; ++u) {
+            const CT* R = sgb + u * TP::SIZE + TP::R_ROW * MP4;
+            CT nc[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                CT row[MP4];
+                load_vec<CT, MP4>(R + i * MP4, row);  // broadcast: all lanes read row i
+                CT q0 = (CT)0, q1 = (CT)0;
+#pragma unroll
+                for (int c = 0; c < M; ++c) {
+                    if (c & 1)
+                        q1 = fma(row[c], col[c], q1);
+                    else
+                        q0 = fma(row[c], col[c], q0);
+                }
+                nc[i] = q0 + q1;
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i) col[i] = nc[i];
+        }
+        fence_proxy_async();
+        __syncwarp();
+        issue(sg + kCS);
+    }
+    if (lane < M) {
+        CT* gt = gtape + gi * TP::SIZE;
+        for (int i = 0; i < M; ++i) {
+            gt[lane * MP4 + i] = col[i];                // W[lane] = column lane
+            gt[(TP::R_ROW + i) * MP4 + lane] = col[i];  // R[i][lane]
+        }
+    }
 }
 
 // ============================================================================
@@ -902,7 +1008,7 @@ __device__ __forceinline__ CT warp_max(CT v) {
     return v;
 }
 
-__device__ unsigned long long g_refined_sequences = 0;
+static __device__ unsigned long long g_refined_sequences = 0;  // launched from scan_kernels.cu only
 
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
@@ -977,6 +1083,52 @@ k_refine_bwd(const CT* __restrict__ tape, CT* __restrict__ Mu, const CT* __restr
         __syncwarp();
         e = en;
         if (lane < M) Mu[(base + j - 1) * MP4 + r] += e;
+    }
+}
+
+// ---------------------------------------------------------------- hierarchical refinement helpers
+// Per-sequence decision of precision "auto" (the long-sequence path; the
+// short path decides inside k_refine_fwd/bwd).
+static __global__ void k_refine_decide(const unsigned* __restrict__ dstat, int* __restrict__ flags,
+                                const int* __restrict__ inherit, float tol, int64_t B) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const float d = __uint_as_float(dstat[2 * b]), x = __uint_as_float(dstat[2 * b + 1]);
+    const bool bad = d > tol * x || (inherit != nullptr && inherit[b] != 0);
+    flags[b] = bad ? 1 : 0;
+    if (bad) atomicAdd(&g_refined_sequences, 1ull);
+}
+
+// D[j] = forcing of the correction recurrence.  fwd: Xend[j] - Xin[j+1]
+// (zero for the last sub-chunk); bwd: K[j] - Mu[j-1] (zero for j = 0).
+template <typename CT>
+__global__ void k_defects(const CT* __restrict__ P, const CT* __restrict__ Q, CT* __restrict__ D,
+                          int nsub, int mp4, int M, bool fwd, const int* __restrict__ only,
+                          int64_t B) {
+    const int64_t n = B * (int64_t)nsub * mp4;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % mp4);
+        const int64_t g = i / mp4;
+        const int j = (int)(g % nsub);
+        const int64_t b = g / nsub;
+        CT v = (CT)0;
+        if (c < M && (only == nullptr || only[b])) {
+            if (fwd && j + 1 < nsub) v = P[g * mp4 + c] - Q[(g + 1) * mp4 + c];
+            if (!fwd && j > 0) v = P[g * mp4 + c] - Q[(g - 1) * mp4 + c];
+        }
+        D[i] = v;
+    }
+}
+
+template <typename CT>
+__global__ void k_add_rows(CT* __restrict__ X, const CT* __restrict__ E, int nsub, int mp4,
+                           const int* __restrict__ only, int64_t B) {
+    const int64_t n = B * (int64_t)nsub * mp4;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / ((int64_t)nsub * mp4);
+        if (only == nullptr || only[b]) X[i] += E[i];
     }
 }
 

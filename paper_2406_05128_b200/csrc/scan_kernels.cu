@@ -162,34 +162,39 @@ int tape_elems(int Mp) {
 }
 
 template <int M, typename IO>
-cudaError_t carry_fwd_impl(const IO* tape, const IO* x0, int x0s, IO* Xin, int64_t nseg,
-                           int seglen, int nsub, unsigned* dstat, int* fflags, cudaStream_t st) {
+cudaError_t carry_fwd_impl(const CarryArgs<IO>& a, cudaStream_t st) {
     using SM = CarrySmem<M, IO>;
     auto k = k_carry_fwd<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
-    k<<<(unsigned)nseg, 32, SM::BYTES, st>>>(tape, x0, x0s, Xin, nseg, seglen, nsub, dstat,
-                                             fflags);
+    k<<<(unsigned)a.nseg, 32, SM::BYTES, st>>>(a);
     return cudaGetLastError();
 }
 
 template <int M, typename IO>
-cudaError_t carry_bwd_impl(const IO* tape, const IO* Nu, const IO* m0, int m0s, IO* Mu,
-                           int64_t nseg, int seglen, int nsub, unsigned* dstat, cudaStream_t st) {
+cudaError_t carry_bwd_impl(const CarryArgs<IO>& a, cudaStream_t st) {
     using SM = CarrySmem<M, IO>;
     auto k = k_carry_bwd<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
-    k<<<(unsigned)nseg, 32, SM::BYTES, st>>>(tape, Nu, m0, m0s, Mu, nseg, seglen, nsub, dstat);
+    k<<<(unsigned)a.nseg, 32, SM::BYTES, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int M, typename IO>
+cudaError_t group_P_impl(const IO* tape, IO* gtape, int64_t ngroups, int G, int nsub,
+                         const int* only, cudaStream_t st) {
+    using SM = CarrySmem<M, IO>;
+    auto k = k_group_P<M, IO>;
+    cudaError_t err = ensure_smem(k, SM::BYTES);
+    if (err != cudaSuccess) return err;
+    k<<<(unsigned)ngroups, 32, SM::BYTES, st>>>(tape, gtape, ngroups, G, nsub, only);
     return cudaGetLastError();
 }
 
 template <typename IO>
-cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, unsigned* dstat,
-                             int* fflags, const ScanArgs& g, cudaStream_t st) {
-    TVLP_DISPATCH_M(Mp, {
-        return carry_fwd_impl<M_, IO>(tape, zi, Mp, Xin, g.B, g.nsub, g.nsub, dstat, fflags, st);
-    })
+cudaError_t launch_carry_fwd(int Mp, const CarryArgs<IO>& a, cudaStream_t st) {
+    TVLP_DISPATCH_M(Mp, { return carry_fwd_impl<M_, IO>(a, st); })
 }
 
 unsigned long long refined_sequences() {
@@ -199,11 +204,33 @@ unsigned long long refined_sequences() {
 }
 
 template <typename IO>
-cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, unsigned* dstat,
-                             const ScanArgs& g, cudaStream_t st) {
-    TVLP_DISPATCH_M(Mp, {
-        return carry_bwd_impl<M_, IO>(tape, Nu, nullptr, 0, Mu, g.B, g.nsub, g.nsub, dstat, st);
-    })
+cudaError_t launch_carry_bwd(int Mp, const CarryArgs<IO>& a, cudaStream_t st) {
+    TVLP_DISPATCH_M(Mp, { return carry_bwd_impl<M_, IO>(a, st); })
+}
+
+template <typename IO>
+cudaError_t launch_group_P(int Mp, const IO* tape, IO* gtape, int64_t ngroups, int G, int nsub,
+                           const int* only, cudaStream_t st) {
+    TVLP_DISPATCH_M(Mp, { return group_P_impl<M_, IO>(tape, gtape, ngroups, G, nsub, only, st); })
+}
+
+// what: 0 = decide, 1 = defects, 2 = add (X=P as mutable, E=Q)
+template <typename IO>
+cudaError_t launch_refine_helpers(int what, int Mp, const IO* P, const IO* Q, IO* D, int nsub,
+                                  bool fwd, const int* only, int* flags, const unsigned* dstat,
+                                  const int* inherit, float tol, int64_t B, cudaStream_t st) {
+    const int mp4 = (Mp + 3) / 4 * 4;
+    const int64_t n = B * (int64_t)nsub * mp4;
+    int64_t grid = (n + 255) / 256;
+    if (grid > 148 * 32) grid = 148 * 32;
+    if (grid < 1) grid = 1;
+    if (what == 0)
+        k_refine_decide<<<(unsigned)((B + 127) / 128), 128, 0, st>>>(dstat, flags, inherit, tol, B);
+    else if (what == 1)
+        k_defects<IO><<<(unsigned)grid, 256, 0, st>>>(P, Q, D, nsub, mp4, Mp, fwd, only, B);
+    else
+        k_add_rows<IO><<<(unsigned)grid, 256, 0, st>>>(const_cast<IO*>(P), Q, nsub, mp4, only, B);
+    return cudaGetLastError();
 }
 
 template <typename IO>
@@ -268,10 +295,13 @@ cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* pa
 #define TVLP_INST(IO)                                                                            \
     template cudaError_t launch_basis<IO>(int, bool, int, const IO*, const IO*, IO*,             \
                                           const ScanArgs&, cudaStream_t);                        \
-    template cudaError_t launch_carry_fwd<IO>(int, const IO*, const IO*, IO*, unsigned*, int*,   \
-                                              const ScanArgs&, cudaStream_t);                    \
-    template cudaError_t launch_carry_bwd<IO>(int, const IO*, const IO*, IO*, unsigned*,         \
-                                              const ScanArgs&, cudaStream_t);                    \
+    template cudaError_t launch_carry_fwd<IO>(int, const CarryArgs<IO>&, cudaStream_t);          \
+    template cudaError_t launch_carry_bwd<IO>(int, const CarryArgs<IO>&, cudaStream_t);          \
+    template cudaError_t launch_group_P<IO>(int, const IO*, IO*, int64_t, int, int, const int*,  \
+                                            cudaStream_t);                                       \
+    template cudaError_t launch_refine_helpers<IO>(int, int, const IO*, const IO*, IO*, int,     \
+                                                   bool, const int*, int*, const unsigned*,      \
+                                                   const int*, float, int64_t, cudaStream_t);    \
     template cudaError_t launch_apply_fwd<IO>(int, bool, const IO*, const IO*, const IO*, IO*,   \
                                               int*, IO*, unsigned*, const int*, const ScanArgs&, \
                                               cudaStream_t);                                     \

@@ -23,12 +23,22 @@ template <typename IO>
 cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO* PhiZ,
                          const ScanArgs& g, cudaStream_t st);
 int tape_elems(int Mp);  // carry-tape elements per sub-chunk
+template <typename CT>
+struct CarryArgs;
+// x(k+1) = Phi_k x(k) + z_k over segments (see CarryArgs in lp_scan.cuh)
 template <typename IO>
-cudaError_t launch_carry_fwd(int Mp, const IO* tape, const IO* zi, IO* Xin, unsigned* dstat,
-                             int* fflags, const ScanArgs& g, cudaStream_t st);
+cudaError_t launch_carry_fwd(int Mp, const CarryArgs<IO>& a, cudaStream_t st);
+// mu(k-1) = Phi_k^T mu(k) + nu_k over segments
 template <typename IO>
-cudaError_t launch_carry_bwd(int Mp, const IO* tape, const IO* Nu, IO* Mu, unsigned* dstat,
-                             const ScanArgs& g, cudaStream_t st);
+cudaError_t launch_carry_bwd(int Mp, const CarryArgs<IO>& a, cudaStream_t st);
+// group products P_g of G consecutive tapes (hierarchical carry)
+template <typename IO>
+cudaError_t launch_group_P(int Mp, const IO* tape, IO* gtape, int64_t ngroups, int G, int nsub,
+                           const int* only, cudaStream_t st);
+template <typename IO>
+cudaError_t launch_refine_helpers(int what, int Mp, const IO* P, const IO* Q, IO* D, int nsub,
+                                  bool fwd, const int* only, int* flags, const unsigned* dstat,
+                                  const int* inherit, float tol, int64_t B, cudaStream_t st);
 unsigned long long refined_sequences();  // diagnostic counter (synchronising read)
 enum Prec2 : int { kPrecAuto = 2 };
 template <typename IO>

@@ -265,6 +265,39 @@ def test_long_sequence_d1():
     assert _tv_parity(e, A, g) < 1e-5
 
 
+def test_hierarchical_carry_two_levels(rng):
+    """nsub > 256 sub-chunks per sequence: group products + expansion (2 levels),
+    with zi, on D1 and on the resonant stress set (which needs refinement)."""
+    T = 480 * 300
+    e, A, g = data.d1_batch(21, 2, T)
+    zi = rng.standard_normal((2, 22)).astype(np.float32)
+    _tv_parity(e, A, g, zi=zi)
+    items = [data.stress_item(s, T) for s in (4, 5)]
+    e = np.stack([x[0] for x in items])
+    A = np.stack([x[1] for x in items])
+    g = np.stack([x[2] for x in items])
+    _tv_parity(e, A, g)
+
+
+def test_hierarchical_carry_three_levels():
+    """4.8 M samples = 10000 sub-chunks: 10000 -> 313 -> 10 (three levels)."""
+    e, A, g = data.d1_batch(33, 1, 4_800_000)
+    assert _tv_parity(e, A, g) < 1e-5
+
+
+def test_hierarchical_fp64_io(rng):
+    T = 480 * 300
+    e, A, g = data.d1_batch(8, 1, T, dtype=np.float64)
+    et, At, gt = _cuda(e), _cuda(A), _cuda(g)
+    s = lpc.lp_forward_tv(et, At)
+    ge, gA = lpc.lp_backward_tv(gt, At, s)
+    rs = oracle.lp_forward_tv(e[0], A[0])
+    rge, rgA = oracle.lp_backward_tv(g[0], A[0], rs)
+    assert _err(_np(s)[0], rs) < 1e-8
+    assert _err(_np(ge)[0], rge) < 1e-8
+    assert _err(_np(gA)[0], rgA) < 1e-8
+
+
 def test_zi_and_odd_lengths(rng):
     for T1, M in [(37, 3), (1001, 22), (4099, 5), (6, 22), (1, 4)]:
         e, A, g = data.d1_batch(3, 2, T1, M, hop=7)
