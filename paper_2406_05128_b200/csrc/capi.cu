@@ -133,7 +133,7 @@ Levels make_levels(const Plan& p) {
     Levels v;
     v.n[0] = p.nsub;
     v.off[0] = 0;
-    int64_t cur = tape_body(p) + p.B;
+    int64_t cur = tape_body(p) + (p.B + 3) / 4 * 4;  // group tapes stay 16-B aligned
     while (v.n[v.L - 1] > kSerialMax && v.L < 8) {
         v.n[v.L] = (v.n[v.L - 1] + kGroup - 1) / kGroup;
         v.off[v.L] = cur;
@@ -144,9 +144,8 @@ Levels make_levels(const Plan& p) {
 }
 int64_t carry_elems(const Plan& p) {
     const Levels v = make_levels(p);
-    int64_t tot = tape_body(p) + p.B;
-    for (int l = 1; l < v.L; ++l) tot += p.B * v.n[l] * tape_elems(p.Mp);
-    return tot;
+    if (v.L == 1) return tape_body(p) + p.B;
+    return v.off[v.L - 1] + p.B * v.n[v.L - 1] * tape_elems(p.Mp);
 }
 
 template <typename IO>
