@@ -61,10 +61,13 @@ class TVLPError(RuntimeError):
     """A C-ABI call failed (launch error, bad workspace, unsupported order)."""
 
 
-def load(path=LIB_PATH):
-    """Load libtvlp_b200.so and declare its signatures (no GPU needed)."""
+def load(path=None):
+    """Load libtvlp_b200.so and declare its signatures (no GPU needed).
+
+    $TVLP_LIB selects a tuning variant built with ``build --define ... --out``."""
     global _lib
     if _lib is None:
+        path = path or os.environ.get("TVLP_LIB") or LIB_PATH
         if not os.path.exists(path):
             raise TVLPError(
                 f"{path} is missing: build the B200 kernels with "

@@ -47,19 +47,25 @@ def up_to_date():
     return all(os.path.getmtime(s) <= t for s in _sources())
 
 
-def build(force=False, verbose=False, jobs=None):
-    """Compile (if stale) and return the path of libtvlp_b200.so."""
-    if not force and up_to_date():
+def build(force=False, verbose=False, jobs=None, defines=(), out=None):
+    """Compile (if stale) and return the path of libtvlp_b200.so.
+
+    ``defines``/``out`` build a tuning variant (extra -D flags) into another
+    path, loaded with TVLP_LIB=<path> (A/B experiments; not the product)."""
+    lib = out or LIB
+    objdir = os.path.join(os.path.dirname(lib), "obj") if out else OBJDIR
+    if not force and not out and up_to_date():
         return LIB
     nvcc = _nvcc()
-    os.makedirs(OBJDIR, exist_ok=True)
+    os.makedirs(objdir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
 
     def compile_unit(unit):
         src = os.path.join(CSRC, unit)
-        obj = os.path.join(OBJDIR, unit.replace(".cu", ".o"))
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+        obj = os.path.join(objdir, unit.replace(".cu", ".o"))
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *dflags, "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
-        log = os.path.join(OBJDIR, unit.replace(".cu", ".log"))
+        log = os.path.join(objdir, unit.replace(".cu", ".log"))
         with open(log, "w") as fh:
             fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
         if res.returncode != 0:
@@ -68,22 +74,25 @@ def build(force=False, verbose=False, jobs=None):
 
     with ThreadPoolExecutor(max_workers=jobs or len(UNITS)) as ex:
         objs = list(ex.map(compile_unit, UNITS))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
-        print(f"built {LIB}")
-    return LIB
+        print(f"built {lib}")
+    return lib
 
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--define", "-D", action="append", default=[],
+                    help="extra preprocessor define for a tuning variant")
+    ap.add_argument("--out", default=None, help="variant library path (with --define)")
     args = ap.parse_args(argv)
-    build(force=args.force, verbose=True)
+    build(force=args.force, verbose=True, defines=args.define, out=args.out)
 
 
 if __name__ == "__main__":

@@ -5,6 +5,7 @@
 #pragma once
 #include <cstdint>
 #include <type_traits>
+#include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
 

@@ -27,6 +27,10 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef TVLP_BASIS_GROUP
+#define TVLP_BASIS_GROUP 2
+#endif
+
 namespace tvlp {
 
 constexpr int kLaneWin = 8;     // rows per TMA window in the lane-per-sub-chunk kernels
@@ -230,14 +234,78 @@ struct Basis2Smem {
     static constexpr int BYTES = NW * 2 * HALF_BYTES + NW * 2 * NSTB * 8;
 };
 
+// One step of the packed chains at ring position U (compile-time): lags are
+// R[(U - i) mod M].  Four accumulators over lags M..2, oldest first, so the
+// freshest lag enters last; the lag-1 term closes the step.
+template <int M, bool TI, int U>
+__device__ __forceinline__ void basis2_step(float2 (&R)[M], const float* __restrict__ Ar,
+                                            const float (&ati)[M], float ec0, float ec1, bool zsx,
+                                            bool zsy) {
+    float a[M];
+    if constexpr (TI) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) a[i] = ati[i];
+    } else {
+        load_row_at<float, M>(Ar + U * M, a, U * M * 4);
+    }
+    const float ev = __shfl_sync(0xffffffffu, U < 16 ? ec0 : ec1, U & 15, 16);
+    const float2 ein = make_float2(zsx ? ev : 0.f, zsy ? ev : 0.f);  // zero-state slot only
+    float2 p[4];
+#pragma unroll
+    for (int i = M; i >= 2; --i) {
+        const float2 x = R[(U - i + 2 * M) % M];
+        const float2 ai = make_float2(a[i - 1], a[i - 1]);
+        const int c = (M - i) & 3;
+        p[c] = (M - i < 4) ? __fmul2_rn(ai, x) : __ffma2_rn(ai, x, p[c]);
+    }
+    const float2 sum = __fadd2_rn(__fadd2_rn(p[0], p[1]), __fadd2_rn(p[2], p[3]));
+    const float2 part = __fadd2_rn(ein, make_float2(-sum.x, -sum.y));
+    const float2 na0 = make_float2(-a[0], -a[0]);
+    R[U % M] = __ffma2_rn(na0, R[(U - 1 + M) % M], part);
+}
+
+// A window of M steps at ring positions 0..M-1.  The first window of a
+// sub-chunk may be partial (it starts at ring position u0): its steps are
+// guarded one by one.  Full windows run in groups of kBasisGroup steps, one
+// basic block per group: steps of a group interleave, and the group boundary
+// bounds how far the scheduler runs ahead (register pressure).
+constexpr int kBasisGroup = TVLP_BASIS_GROUP;
+template <int M, bool TI, int G, int... V>
+__device__ __forceinline__ void basis2_group(std::integer_sequence<int, V...>, float2 (&R)[M],
+                                             const float* __restrict__ Ar,
+                                             const float (&ati)[M], float ec0, float ec1,
+                                             bool zsx, bool zsy) {
+    ((G * kBasisGroup + V < M
+          ? basis2_step<M, TI, (G * kBasisGroup + V) % M>(R, Ar, ati, ec0, ec1, zsx, zsy)
+          : void()),
+     ...);
+}
+template <int M, bool TI, int... G>
+__device__ __forceinline__ void basis2_full(std::integer_sequence<int, G...>, float2 (&R)[M],
+                                            const float* __restrict__ Ar, const float (&ati)[M],
+                                            float ec0, float ec1, bool zsx, bool zsy, int lim) {
+    ((G * kBasisGroup < lim
+          ? basis2_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R, Ar, ati,
+                                   ec0, ec1, zsx, zsy)
+          : void()),
+     ...);
+}
+template <int M, bool TI, int... U>
+__device__ __forceinline__ void basis2_partial(std::integer_sequence<int, U...>, float2 (&R)[M],
+                                               const float* __restrict__ Ar,
+                                               const float (&ati)[M], float ec0, float ec1,
+                                               bool zsx, bool zsy, int u0) {
+    ((U >= u0 ? basis2_step<M, TI, U>(R, Ar, ati, ec0, ec1, zsx, zsy) : void()), ...);
+}
+
 template <int M, bool TI, int NW>
 __global__ void __launch_bounds__(NW * 32)
 k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
          ScanArgs g) {
     using S = Basis2Smem<M, TI, NW>;
-    constexpr int WR = S::WR;
     constexpr int NSTB = S::NSTB;
     static_assert(M + 1 <= 32, "order M must be <= 31");
+    static_assert(M <= 32, "window fits two registers per lane");
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int half = lane >> 4, q = lane & 15;
@@ -255,7 +323,10 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
     const int j = (int)(gg % g.nsub);
     const int64_t t0 = (int64_t)j * g.Ls;
     const int len = g.Ls;  // all sub-chunks are full (T % Ls == 0)
-    const int nwin = (len + WR - 1) / WR;
+    // windows are aligned to the END of the sub-chunk: the first covers ring
+    // positions u0..M-1 (time 0..M-1-u0); u0 is even because M and Ls are
+    const int u0 = (M - len % M) % M;
+    const int nwin = (len + u0) / M;
     const int64_t row0 = b * g.T + t0;
     const float* eb = e + row0;
 
@@ -268,9 +339,12 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
     auto issue = [&](int k) {
         if (TI || k >= nwin || q != 0) return;
         const int st = k % NSTB;
-        const int rows = min(WR, len - k * WR);
+        const int first = k == 0 ? u0 : 0;              // ring position of the first row
+        const int64_t tstart = (int64_t)k * M - u0 + first;  // its time in the sub-chunk
+        const int rows = M - first;
         mbar_arrive_expect_tx(&bars[st], rows * M * 4);
-        tma_load_1d(stage_ptr(st), A + (row0 + (int64_t)k * WR) * M, rows * M * 4, &bars[st]);
+        tma_load_1d(stage_ptr(st) + first * M * 4, A + (row0 + tstart) * M, rows * M * 4,
+                    &bars[st]);
     };
 #pragma unroll
     for (int k = 0; k < NSTB; ++k) issue(k);
@@ -281,55 +355,34 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
         for (int i = 0; i < M; ++i) ati[i] = A[b * M + i];
     }
     const int cx = 2 * q, cy = 2 * q + 1;  // chain ids of the pair
+    // initial state x_c = s(t0 - 1 - c) = unit for chain c sits at ring (u0 - 1 - c) mod M
     float2 R[M];
 #pragma unroll
-    for (int p = 0; p < M; ++p)
-        R[p] = make_float2((cx < M && M - 1 - p == cx) ? 1.f : 0.f,
-                           (cy < M && M - 1 - p == cy) ? 1.f : 0.f);
+    for (int p = 0; p < M; ++p) {
+        const int c = ((u0 - 1 - p) % M + M) % M;  // the state component at ring p
+        R[p] = make_float2(c == cx ? 1.f : 0.f, c == cy ? 1.f : 0.f);
+    }
     const bool zsx = cx == M, zsy = cy == M;
 
     // excitation (read by the zero-state chain only): lane q of a half holds
-    // e[w*WR + q] and e[w*WR + 16 + q] of window w, loaded one window ahead;
-    // step u takes it with a 16-lane shuffle (off the recursion's chain).
-    static_assert(WR <= 32, "window fits two registers per lane");
-    auto eload = [&](int w, int u) { const int t = w * WR + u; return (u < WR && t < len) ? __ldg(eb + t) : 0.f; };
+    // the values of ring positions q and 16 + q of window w, loaded one window
+    // ahead; a step takes it with a 16-lane shuffle (off the recursion's chain)
+    auto eload = [&](int w, int u) {
+        const int t = w * M + u - u0;
+        return (u < M && t >= 0 && t < len) ? __ldg(eb + t) : 0.f;
+    };
     float ec0 = eload(0, q), ec1 = eload(0, 16 + q);
     for (int k = 0; k < nwin; ++k) {
         const int st = k % NSTB;
         const float en0 = eload(k + 1, q), en1 = eload(k + 1, 16 + q);
         if (!TI) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
-        const int rows = min(WR, len - k * WR);
         const float* Ar = reinterpret_cast<const float*>(stage_ptr(st));
-#define TVLP_BASIS2_STEP(u)                                                              \
-    {                                                                                    \
-        float a[M];                                                                      \
-        if constexpr (TI) {                                                              \
-            _Pragma("unroll") for (int i = 0; i < M; ++i) a[i] = ati[i];                 \
-        } else {                                                                         \
-            load_row_at<float, M>(Ar + (u) * M, a, (u) * M * 4);                         \
-        }                                                                                \
-        const float ev = __shfl_sync(0xffffffffu, (u) < 16 ? ec0 : ec1, (u) & 15, 16);   \
-        /* only the zero-state slot sees the excitation (ALU selects) */                 \
-        const float2 ein = make_float2(zsx ? ev : 0.f, zsy ? ev : 0.f);                  \
-        /* two accumulators over lags M..2, oldest first; freshest lag last */           \
-        float2 p0 = make_float2(0.f, 0.f), p1 = p0;                                      \
-        _Pragma("unroll") for (int i = M; i >= 2; --i) {                                 \
-            const float2 x = R[((u) - i + 2 * M) % M];                                   \
-            const float2 ai = make_float2(a[i - 1], a[i - 1]);                           \
-            if (i & 1)                                                                   \
-                p1 = __ffma2_rn(ai, x, p1);                                              \
-            else                                                                         \
-                p0 = __ffma2_rn(ai, x, p0);                                              \
-        }                                                                                \
-        const float2 sum = __fadd2_rn(p0, p1);                                           \
-        const float2 part = __fadd2_rn(ein, make_float2(-sum.x, -sum.y));                \
-        const float2 na0 = make_float2(-a[0], -a[0]);                                    \
-        R[(u) % M] = __ffma2_rn(na0, R[((u) - 1 + M) % M], part);                        \
-    }
-#pragma unroll
-        for (int u = 0; u < WR; ++u)
-            if (u < rows) TVLP_BASIS2_STEP(u)  // warp-uniform: only the last window is short
-#undef TVLP_BASIS2_STEP
+        if (k == 0 && u0 != 0)
+            basis2_partial<M, TI>(std::make_integer_sequence<int, M>{}, R, Ar, ati, ec0, ec1, zsx,
+                                  zsy, u0);
+        else
+            basis2_full<M, TI>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
+                               R, Ar, ati, ec0, ec1, zsx, zsy, g.Ls);
         __syncwarp();
         fence_proxy_async();
         issue(k + NSTB);
@@ -337,18 +390,207 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
         ec1 = en1;
     }
 
-    // final state x[i] = s(t1 - i) = R[(len-1-i) mod M]
+    // final state x[i] = s(t1 - i) = R[(M - 1 - i) mod M] (the last window is full)
     if (active && cx <= M) {
-        float2 tmp[M];
-#pragma unroll
-        for (int p = 0; p < M; ++p) tmp[p] = R[p];
-        const int last = (len - 1) % M;
         float* tape = PhiZ + gid * Tape<M>::SIZE;
         float* ox = tape + cx * Tape<M>::MP4;
         float* oy = tape + cy * Tape<M>::MP4;
         float* rr = tape + Tape<M>::R_ROW * Tape<M>::MP4;
+#pragma unroll
         for (int i = 0; i < M; ++i) {
-            const float2 v = tmp[(last - i + M) % M];
+            const float2 v = R[M - 1 - i];
+            ox[i] = v.x;
+            if (cx < M) rr[i * Tape<M>::MP4 + cx] = v.x;
+            if (cy <= M) oy[i] = v.y;
+            if (cy < M) rr[i * Tape<M>::MP4 + cy] = v.y;
+        }
+    }
+}
+
+// ============================================================================
+// fp32 basis, lane-packed: a sub-chunk needs M/2+1 = P lanes (chain pairs,
+// the last pair holds the zero-state chain), and the CTA packs S = 32W/P
+// sub-chunks into W warps so no lane idles (M = 22: P = 12, 8 sub-chunks per
+// 3 warps; k_basis2's half-warp mapping left 25% of the lanes idle).  A step
+// is 1 FMUL2 + (M-2) FFMA2 + 1 FADD2 + 1 FFMA2 on the FMA pipe: the
+// excitation enters as the initial value of one accumulator and the
+// coefficients are negated in the FFMA2 operand (-Ra.F32).
+// ============================================================================
+constexpr int basis3_best_w(int P) {
+    int bw = 1, bn = 0, bd = 1;  // best lane efficiency S*P / (32 W) as a fraction
+    for (int w = 1; w <= 4; ++w) {
+        const int s = 32 * w / P;
+        if (s * P * bd > bn * 32 * w) {
+            bw = w;
+            bn = s * P;
+            bd = 32 * w;
+        }
+    }
+    return bw;
+}
+template <int M, bool TI>
+struct Basis3Cfg {
+    static_assert(M % 2 == 0, "even orders only (odd orders are padded)");
+    static constexpr int P = M / 2 + 1;
+    static constexpr int W = basis3_best_w(P);
+    static constexpr int S = 32 * W / P;
+    static constexpr int NSTB = 2;
+    static constexpr int ROWS_BYTES = TI ? 0 : (M * M * 4 + 15) / 16 * 16;
+    static constexpr int E_OFF = ROWS_BYTES;
+    static constexpr int STAGE = ROWS_BYTES + 128;  // + the window's excitation (<= 32 floats)
+    static constexpr int BAR_OFF = S * NSTB * STAGE;
+    static constexpr int BYTES = BAR_OFF + S * NSTB * 8;
+};
+
+template <int M, bool TI, int U>
+__device__ __forceinline__ void basis3_step(float2 (&R)[M], const float* __restrict__ Ar,
+                                            const float* __restrict__ es, const float (&ati)[M],
+                                            bool zsx, bool zsy) {
+    float a[M];
+    if constexpr (TI) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) a[i] = ati[i];
+    } else {
+        load_row_at<float, M>(Ar + U * M, a, U * M * 4);
+    }
+    const float ev = es[U];
+    float2 pa = make_float2(zsx ? ev : 0.f, zsy ? ev : 0.f);  // zero-state slot only
+    float2 pb = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = M; i >= 2; --i) {  // lags M..2, oldest first
+        const float2 x = R[(U - i + 2 * M) % M];
+        const float2 na = make_float2(-a[i - 1], -a[i - 1]);
+        if ((M - i) & 1)
+            pb = (M - i == 1) ? __fmul2_rn(na, x) : __ffma2_rn(na, x, pb);
+        else
+            pa = __ffma2_rn(na, x, pa);
+    }
+    const float2 part = M > 2 ? __fadd2_rn(pa, pb) : pa;
+    R[U % M] = __ffma2_rn(make_float2(-a[0], -a[0]), R[(U - 1 + M) % M], part);
+}
+template <int M, bool TI, int G, int... V>
+__device__ __forceinline__ void basis3_group(std::integer_sequence<int, V...>, float2 (&R)[M],
+                                             const float* __restrict__ Ar,
+                                             const float* __restrict__ es, const float (&ati)[M],
+                                             bool zsx, bool zsy) {
+    ((G * kBasisGroup + V < M
+          ? basis3_step<M, TI, (G * kBasisGroup + V) % M>(R, Ar, es, ati, zsx, zsy)
+          : void()),
+     ...);
+}
+template <int M, bool TI, int... G>
+__device__ __forceinline__ void basis3_full(std::integer_sequence<int, G...>, float2 (&R)[M],
+                                            const float* __restrict__ Ar,
+                                            const float* __restrict__ es, const float (&ati)[M],
+                                            bool zsx, bool zsy, int lim) {
+    ((G * kBasisGroup < lim
+          ? basis3_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R, Ar, es, ati,
+                                   zsx, zsy)
+          : void()),
+     ...);
+}
+template <int M, bool TI, int... U>
+__device__ __forceinline__ void basis3_partial(std::integer_sequence<int, U...>, float2 (&R)[M],
+                                               const float* __restrict__ Ar,
+                                               const float* __restrict__ es,
+                                               const float (&ati)[M], bool zsx, bool zsy, int u0) {
+    ((U >= u0 ? basis3_step<M, TI, U>(R, Ar, es, ati, zsx, zsy) : void()), ...);
+}
+
+template <int M, bool TI>
+__global__ void __launch_bounds__(Basis3Cfg<M, TI>::W * 32)
+k_basis3(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
+         ScanArgs g) {
+    using C = Basis3Cfg<M, TI>;
+    constexpr int P = C::P, S = C::S, NSTB = C::NSTB;
+    static_assert(M + 1 <= 32, "order M must be <= 31");
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x;
+    const int q = tid % P;
+    const bool lane_used = tid / P < S;
+    const int sc = lane_used ? tid / P : S - 1;
+    const int64_t nsc = g.B * g.nsub;
+    const int64_t gid = (int64_t)blockIdx.x * S + sc;
+    const bool valid = lane_used && gid < nsc;  // idle lanes compute on garbage, never wait
+    const int64_t gg = gid < nsc ? gid : nsc - 1;
+    const int64_t b = gg / g.nsub;
+    const int j = (int)(gg % g.nsub);
+    const int len = g.Ls;  // all sub-chunks are full (T % Ls == 0)
+    const int u0 = (M - len % M) % M;  // first window covers ring positions u0..M-1
+    const int nwin = (len + u0) / M;
+    const int64_t row0 = b * g.T + (int64_t)j * g.Ls;
+    const float* eb = e + row0;
+    auto stage = [&](int st) { return smem + (sc * NSTB + st) * C::STAGE; };
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF) + sc * NSTB;
+    const bool leader = valid && q == 0;
+
+    auto issue = [&](int k) {
+        if (TI || !leader || k >= nwin) return;
+        const int st = k % NSTB;
+        const int first = k == 0 ? u0 : 0;
+        const int64_t tstart = (int64_t)k * M - u0 + first;
+        const int rows = M - first;
+        mbar_arrive_expect_tx(&bars[st], rows * M * 4);
+        tma_load_1d(stage(st) + first * M * 4, A + (row0 + tstart) * M, rows * M * 4, &bars[st]);
+    };
+    auto eload = [&](int w, int u) {
+        const int t = w * M + u - u0;
+        return (valid && u < M && t >= 0 && t < len) ? __ldg(eb + t) : 0.f;
+    };
+    auto estore = [&](int st, float v0, float v1) {
+        float* es = reinterpret_cast<float*>(stage(st) + C::E_OFF);
+        if (q < M) es[q] = v0;
+        if (q + P < M) es[q + P] = v1;
+    };
+    if (leader && !TI) {
+        for (int st = 0; st < NSTB; ++st) mbar_init(&bars[st], 1);
+        fence_mbar_init();
+    }
+    estore(0, eload(0, q), eload(0, q + P));
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NSTB; ++k) issue(k);
+
+    float ati[M];
+    if (TI) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) ati[i] = A[b * M + i];
+    }
+    const int cx = 2 * q, cy = 2 * q + 1;
+    float2 R[M];
+#pragma unroll
+    for (int p = 0; p < M; ++p) {
+        const int c = ((u0 - 1 - p) % M + M) % M;  // state component held at ring position p
+        R[p] = make_float2(c == cx ? 1.f : 0.f, c == cy ? 1.f : 0.f);
+    }
+    const bool zsx = cx == M, zsy = cy == M;
+
+    for (int k = 0; k < nwin; ++k) {
+        const int st = k % NSTB;
+        const float en0 = eload(k + 1, q), en1 = eload(k + 1, q + P);
+        if (!TI && valid) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
+        const float* Ar = reinterpret_cast<const float*>(stage(st));
+        const float* es = reinterpret_cast<const float*>(stage(st) + C::E_OFF);
+        if (k == 0 && u0 != 0)
+            basis3_partial<M, TI>(std::make_integer_sequence<int, M>{}, R, Ar, es, ati, zsx, zsy,
+                                  u0);
+        else
+            basis3_full<M, TI>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
+                               R, Ar, es, ati, zsx, zsy, len);
+        estore((k + 1) % NSTB, en0, en1);
+        fence_proxy_async();
+        __syncthreads();  // every lane is done with stage st; window k+1's excitation is visible
+        issue(k + NSTB);
+    }
+
+    if (valid && cx <= M) {
+        float* tape = PhiZ + gid * Tape<M>::SIZE;
+        float* ox = tape + cx * Tape<M>::MP4;
+        float* oy = tape + cy * Tape<M>::MP4;
+        float* rr = tape + Tape<M>::R_ROW * Tape<M>::MP4;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const float2 v = R[M - 1 - i];
             ox[i] = v.x;
             if (cx < M) rr[i * Tape<M>::MP4 + cx] = v.x;
             if (cy <= M) oy[i] = v.y;

@@ -16,7 +16,10 @@ cudaError_t ensure_smem(K kernel, int bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-constexpr int kBasisWarps = 4;
+#ifndef TVLP_BASIS_WARPS
+#define TVLP_BASIS_WARPS 2
+#endif
+constexpr int kBasisWarps = TVLP_BASIS_WARPS;
 
 template <typename IO, typename ACC, int M, bool TI>
 cudaError_t basis_impl(const IO* e, const IO* A, IO* PhiZ, const ScanArgs& g,
@@ -88,6 +91,18 @@ cudaError_t basis2_impl(const float* e, const float* A, float* PhiZ, const ScanA
     return cudaGetLastError();
 }
 
+template <int M, bool TI>
+cudaError_t basis3_impl(const float* e, const float* A, float* PhiZ, const ScanArgs& g,
+                        cudaStream_t st) {
+    using C = Basis3Cfg<M, TI>;
+    auto k = k_basis3<M, TI>;
+    cudaError_t err = ensure_smem(k, C::BYTES);
+    if (err != cudaSuccess) return err;
+    const int64_t nsc = g.B * g.nsub;
+    k<<<(unsigned)((nsc + C::S - 1) / C::S), C::W * 32, C::BYTES, st>>>(e, A, PhiZ, g);
+    return cudaGetLastError();
+}
+
 template <typename IO, int M, bool TI>
 cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag, IO* Xend,
                        unsigned* dstat, const int* only, const ScanArgs& g, cudaStream_t st) {
@@ -142,8 +157,8 @@ cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO
     TVLP_DISPATCH_M(Mp, {
         if constexpr (std::is_same<IO, float>::value) {
             if (prec == kPrecF32Chains || prec == kPrecAuto)
-                return ti ? basis2_impl<M_, true>(e, A, PhiZ, g, st)
-                          : basis2_impl<M_, false>(e, A, PhiZ, g, st);
+                return ti ? basis3_impl<M_, true>(e, A, PhiZ, g, st)
+                          : basis3_impl<M_, false>(e, A, PhiZ, g, st);
         }
         return ti ? basis_impl<IO, double, M_, true>(e, A, PhiZ, g, st)
                   : basis_impl<IO, double, M_, false>(e, A, PhiZ, g, st);
