@@ -27,6 +27,12 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef TVLP_BASIS4_WARPS
+#define TVLP_BASIS4_WARPS 2
+#endif
+#ifndef TVLP_BASIS3_MINCTAS
+#define TVLP_BASIS3_MINCTAS 6
+#endif
 #ifndef TVLP_BASIS_GROUP
 #define TVLP_BASIS_GROUP 2
 #endif
@@ -412,9 +418,8 @@ k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __rest
 // the last pair holds the zero-state chain), and the CTA packs S = 32W/P
 // sub-chunks into W warps so no lane idles (M = 22: P = 12, 8 sub-chunks per
 // 3 warps; k_basis2's half-warp mapping left 25% of the lanes idle).  A step
-// is 1 FMUL2 + (M-2) FFMA2 + 1 FADD2 + 1 FFMA2 on the FMA pipe: the
-// excitation enters as the initial value of one accumulator and the
-// coefficients are negated in the FFMA2 operand (-Ra.F32).
+// is 2M scalar FMA-pipe ops per lane: the excitation enters as the initial
+// value of one accumulator and the coefficients are negated in the operand.
 // ============================================================================
 constexpr int basis3_best_w(int P) {
     int bw = 1, bn = 0, bd = 1;  // best lane efficiency S*P / (32 W) as a fraction
@@ -440,6 +445,10 @@ struct Basis3Cfg {
     static constexpr int STAGE = ROWS_BYTES + 128;  // + the window's excitation (<= 32 floats)
     static constexpr int BAR_OFF = S * NSTB * STAGE;
     static constexpr int BYTES = BAR_OFF + S * NSTB * 8;
+    // resident CTAs per SM the register budget is sized for (M = 22: 7 -> <= 96
+    // registers, i.e. 5 warps per SM sub-partition, so that 6 CTAs x 8
+    // sub-chunks x 148 SMs >= 6400 sub-chunks of config 3 run in one wave)
+    static constexpr int MIN_CTAS = TVLP_BASIS3_MINCTAS;
 };
 
 template <int M, bool TI, int U>
@@ -454,19 +463,29 @@ __device__ __forceinline__ void basis3_step(float2 (&R)[M], const float* __restr
         load_row_at<float, M>(Ar + U * M, a, U * M * 4);
     }
     const float ev = es[U];
-    float2 pa = make_float2(zsx ? ev : 0.f, zsy ? ev : 0.f);  // zero-state slot only
-    float2 pb = make_float2(0.f, 0.f);
+    // scalar FFMA: with register operands FFMA2 issues at half the FFMA rate
+    // (tools/micro/ffma2_regs.cu: 14-18 vs 35 TFMA/s), so the pair is two
+    // independent scalar chains, each split over two accumulators
+    float xa = zsx ? ev : 0.f, ya = zsy ? ev : 0.f;  // the zero-state slot takes e
+    float xb = 0.f, yb = 0.f;
 #pragma unroll
     for (int i = M; i >= 2; --i) {  // lags M..2, oldest first
-        const float2 x = R[(U - i + 2 * M) % M];
-        const float2 na = make_float2(-a[i - 1], -a[i - 1]);
-        if ((M - i) & 1)
-            pb = (M - i == 1) ? __fmul2_rn(na, x) : __ffma2_rn(na, x, pb);
-        else
-            pa = __ffma2_rn(na, x, pa);
+        const float2 v = R[(U - i + 2 * M) % M];
+        const float na = -a[i - 1];
+        if ((M - i) & 1) {
+            xb = (M - i == 1) ? na * v.x : fmaf(na, v.x, xb);
+            yb = (M - i == 1) ? na * v.y : fmaf(na, v.y, yb);
+        } else {
+            xa = fmaf(na, v.x, xa);
+            ya = fmaf(na, v.y, ya);
+        }
     }
-    const float2 part = M > 2 ? __fadd2_rn(pa, pb) : pa;
-    R[U % M] = __ffma2_rn(make_float2(-a[0], -a[0]), R[(U - 1 + M) % M], part);
+    if constexpr (M > 2) {
+        xa += xb;
+        ya += yb;
+    }
+    const float2 r1 = R[(U - 1 + M) % M];
+    R[U % M] = make_float2(fmaf(-a[0], r1.x, xa), fmaf(-a[0], r1.y, ya));
 }
 template <int M, bool TI, int G, int... V>
 __device__ __forceinline__ void basis3_group(std::integer_sequence<int, V...>, float2 (&R)[M],
@@ -498,7 +517,7 @@ __device__ __forceinline__ void basis3_partial(std::integer_sequence<int, U...>,
 }
 
 template <int M, bool TI>
-__global__ void __launch_bounds__(Basis3Cfg<M, TI>::W * 32)
+__global__ void __launch_bounds__(Basis3Cfg<M, TI>::W * 32, Basis3Cfg<M, TI>::MIN_CTAS)
 k_basis3(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
          ScanArgs g) {
     using C = Basis3Cfg<M, TI>;
@@ -595,6 +614,194 @@ k_basis3(const float* __restrict__ e, const float* __restrict__ A, float* __rest
             if (cx < M) rr[i * Tape<M>::MP4 + cx] = v.x;
             if (cy <= M) oy[i] = v.y;
             if (cy < M) rr[i * Tape<M>::MP4 + cy] = v.y;
+        }
+    }
+}
+
+// ============================================================================
+// fp32 basis, three chains per lane (scalar FFMA).  A sub-chunk takes
+// P = ceil((M+1)/3) lanes (M = 22: 8 lanes, 24 slots for the M unit chains and
+// the zero-state chain), a warp packs S = 32/P sub-chunks and is independent
+// of every other warp (warp-level sync only).  Each lane's coefficient row
+// loads (7 LDS per step for M = 22) are shared by its three chains, and the
+// three chains are independent FMA streams (ILP) within the step.
+// ============================================================================
+template <int M, bool TI>
+struct Basis4Cfg {
+    static_assert(M % 2 == 0, "even orders only (odd orders are padded)");
+    static constexpr int P = (M + 1 + 2) / 3;
+    static constexpr int S = 32 / P;
+    static constexpr int NW = TVLP_BASIS4_WARPS;  // independent warps per CTA
+    static constexpr int NSTB = 2;
+    static constexpr int ROWS_BYTES = TI ? 0 : (M * M * 4 + 15) / 16 * 16;
+    static constexpr int E_OFF = ROWS_BYTES;
+    static constexpr int STAGE = ROWS_BYTES + 128;  // + the window's excitation (<= 32 floats)
+    static constexpr int WARP_BYTES = S * NSTB * STAGE;
+    static constexpr int BAR_OFF = NW * WARP_BYTES;
+    static constexpr int BYTES = BAR_OFF + NW * S * NSTB * 8;
+};
+
+template <int M, bool TI, int U>
+__device__ __forceinline__ void basis4_step(float (&R0)[M], float (&R1)[M], float (&R2)[M],
+                                            const float* __restrict__ Ar,
+                                            const float* __restrict__ es, const float (&ati)[M],
+                                            int zs) {
+    float a[M];
+    if constexpr (TI) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) a[i] = ati[i];
+    } else {
+        load_row_at<float, M>(Ar + U * M, a, U * M * 4);
+    }
+    const float ev = es[U];
+    float c0 = zs == 0 ? ev : 0.f, c1 = zs == 1 ? ev : 0.f, c2 = zs == 2 ? ev : 0.f;
+#pragma unroll
+    for (int i = M; i >= 2; --i) {  // lags M..2, oldest first
+        const int r = (U - i + 2 * M) % M;
+        const float na = -a[i - 1];
+        c0 = fmaf(na, R0[r], c0);
+        c1 = fmaf(na, R1[r], c1);
+        c2 = fmaf(na, R2[r], c2);
+    }
+    const int r1 = (U - 1 + M) % M;
+    R0[U % M] = fmaf(-a[0], R0[r1], c0);
+    R1[U % M] = fmaf(-a[0], R1[r1], c1);
+    R2[U % M] = fmaf(-a[0], R2[r1], c2);
+}
+template <int M, bool TI, int G, int... V>
+__device__ __forceinline__ void basis4_group(std::integer_sequence<int, V...>, float (&R0)[M],
+                                             float (&R1)[M], float (&R2)[M],
+                                             const float* __restrict__ Ar,
+                                             const float* __restrict__ es, const float (&ati)[M],
+                                             int zs) {
+    ((G * kBasisGroup + V < M
+          ? basis4_step<M, TI, (G * kBasisGroup + V) % M>(R0, R1, R2, Ar, es, ati, zs)
+          : void()),
+     ...);
+}
+template <int M, bool TI, int... G>
+__device__ __forceinline__ void basis4_full(std::integer_sequence<int, G...>, float (&R0)[M],
+                                            float (&R1)[M], float (&R2)[M],
+                                            const float* __restrict__ Ar,
+                                            const float* __restrict__ es, const float (&ati)[M],
+                                            int zs, int lim) {
+    ((G * kBasisGroup < lim
+          ? basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R0, R1, R2, Ar,
+                                   es, ati, zs)
+          : void()),
+     ...);
+}
+template <int M, bool TI, int... U>
+__device__ __forceinline__ void basis4_partial(std::integer_sequence<int, U...>, float (&R0)[M],
+                                               float (&R1)[M], float (&R2)[M],
+                                               const float* __restrict__ Ar,
+                                               const float* __restrict__ es,
+                                               const float (&ati)[M], int zs, int u0) {
+    ((U >= u0 ? basis4_step<M, TI, U>(R0, R1, R2, Ar, es, ati, zs) : void()), ...);
+}
+
+template <int M, bool TI>
+__global__ void __launch_bounds__(Basis4Cfg<M, TI>::NW * 32)
+k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
+         ScanArgs g) {
+    using C = Basis4Cfg<M, TI>;
+    constexpr int P = C::P, S = C::S, NSTB = C::NSTB;
+    static_assert(M + 1 <= 32, "order M must be <= 31");
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = lane % P;
+    const bool lane_used = lane / P < S;
+    const int sc = lane_used ? lane / P : S - 1;
+    const int64_t nsc = g.B * g.nsub;
+    const int64_t gid = ((int64_t)blockIdx.x * C::NW + warp) * S + sc;
+    const bool valid = lane_used && gid < nsc;  // idle lanes compute on garbage, never wait
+    const int64_t gg = gid < nsc ? gid : nsc - 1;
+    const int64_t b = gg / g.nsub;
+    const int j = (int)(gg % g.nsub);
+    const int len = g.Ls;  // all sub-chunks are full (T % Ls == 0)
+    const int u0 = (M - len % M) % M;  // the first window covers ring positions u0..M-1
+    const int nwin = (len + u0) / M;
+    const int64_t row0 = b * g.T + (int64_t)j * g.Ls;
+    const float* eb = e + row0;
+    unsigned char* wbase = smem + warp * C::WARP_BYTES;
+    auto stage = [&](int st) { return wbase + (sc * NSTB + st) * C::STAGE; };
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF) + (warp * S + sc) * NSTB;
+    const bool leader = valid && q == 0;
+
+    auto issue = [&](int k) {
+        if (TI || !leader || k >= nwin) return;
+        const int st = k % NSTB;
+        const int first = k == 0 ? u0 : 0;
+        const int64_t tstart = (int64_t)k * M - u0 + first;
+        const int rows = M - first;
+        mbar_arrive_expect_tx(&bars[st], rows * M * 4);
+        tma_load_1d(stage(st) + first * M * 4, A + (row0 + tstart) * M, rows * M * 4, &bars[st]);
+    };
+    auto eload = [&](int w, int u) {
+        const int t = w * M + u - u0;
+        return (valid && u < M && t >= 0 && t < len) ? __ldg(eb + t) : 0.f;
+    };
+    auto estore = [&](int st, float v0, float v1, float v2) {
+        float* es = reinterpret_cast<float*>(stage(st) + C::E_OFF);
+        if (q < M) es[q] = v0;
+        if (q + P < M) es[q + P] = v1;
+        if (q + 2 * P < M) es[q + 2 * P] = v2;
+    };
+    if (leader && !TI) {
+        for (int st = 0; st < NSTB; ++st) mbar_init(&bars[st], 1);
+        fence_mbar_init();
+    }
+    estore(0, eload(0, q), eload(0, q + P), eload(0, q + 2 * P));
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < NSTB; ++k) issue(k);
+
+    float ati[M];
+    if (TI) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) ati[i] = A[b * M + i];
+    }
+    const int c0 = 3 * q;  // chains c0, c0+1, c0+2 (chain M is the zero-state chain)
+    const int zs = M - c0;  // which of the three is the zero-state chain (0..2), if any
+    float R0[M], R1[M], R2[M];
+#pragma unroll
+    for (int p = 0; p < M; ++p) {
+        const int c = ((u0 - 1 - p) % M + M) % M;  // state component held at ring position p
+        R0[p] = c == c0 ? 1.f : 0.f;
+        R1[p] = c == c0 + 1 ? 1.f : 0.f;
+        R2[p] = c == c0 + 2 ? 1.f : 0.f;
+    }
+
+    for (int k = 0; k < nwin; ++k) {
+        const int st = k % NSTB;
+        const float en0 = eload(k + 1, q), en1 = eload(k + 1, q + P), en2 = eload(k + 1, q + 2 * P);
+        if (!TI && valid) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
+        const float* Ar = reinterpret_cast<const float*>(stage(st));
+        const float* es = reinterpret_cast<const float*>(stage(st) + C::E_OFF);
+        if (k == 0 && u0 != 0)
+            basis4_partial<M, TI>(std::make_integer_sequence<int, M>{}, R0, R1, R2, Ar, es, ati, zs,
+                                  u0);
+        else
+            basis4_full<M, TI>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
+                               R0, R1, R2, Ar, es, ati, zs, len);
+        estore((k + 1) % NSTB, en0, en1, en2);
+        fence_proxy_async();
+        __syncwarp();  // the warp is done with stage st; window k+1's excitation is visible
+        issue(k + NSTB);
+    }
+
+    if (valid) {
+        float* tape = PhiZ + gid * Tape<M>::SIZE;
+        float* rr = tape + Tape<M>::R_ROW * Tape<M>::MP4;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const float v[3] = {R0[M - 1 - i], R1[M - 1 - i], R2[M - 1 - i]};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int ch = c0 + c;
+                if (ch <= M) tape[ch * Tape<M>::MP4 + i] = v[c];  // W column ch / z row
+                if (ch < M) rr[i * Tape<M>::MP4 + ch] = v[c];    // R row i
+            }
         }
     }
 }

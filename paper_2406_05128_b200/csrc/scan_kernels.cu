@@ -103,6 +103,19 @@ cudaError_t basis3_impl(const float* e, const float* A, float* PhiZ, const ScanA
     return cudaGetLastError();
 }
 
+template <int M, bool TI>
+cudaError_t basis4_impl(const float* e, const float* A, float* PhiZ, const ScanArgs& g,
+                        cudaStream_t st) {
+    using C = Basis4Cfg<M, TI>;
+    auto k = k_basis4<M, TI>;
+    cudaError_t err = ensure_smem(k, C::BYTES);
+    if (err != cudaSuccess) return err;
+    const int64_t nsc = g.B * g.nsub;
+    const int64_t per = (int64_t)C::S * C::NW;
+    k<<<(unsigned)((nsc + per - 1) / per), C::NW * 32, C::BYTES, st>>>(e, A, PhiZ, g);
+    return cudaGetLastError();
+}
+
 template <typename IO, int M, bool TI>
 cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag, IO* Xend,
                        unsigned* dstat, const int* only, const ScanArgs& g, cudaStream_t st) {
@@ -157,8 +170,8 @@ cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO
     TVLP_DISPATCH_M(Mp, {
         if constexpr (std::is_same<IO, float>::value) {
             if (prec == kPrecF32Chains || prec == kPrecAuto)
-                return ti ? basis3_impl<M_, true>(e, A, PhiZ, g, st)
-                          : basis3_impl<M_, false>(e, A, PhiZ, g, st);
+                return ti ? basis4_impl<M_, true>(e, A, PhiZ, g, st)
+                          : basis4_impl<M_, false>(e, A, PhiZ, g, st);
         }
         return ti ? basis_impl<IO, double, M_, true>(e, A, PhiZ, g, st)
                   : basis_impl<IO, double, M_, false>(e, A, PhiZ, g, st);

@@ -7,7 +7,7 @@ using namespace tvlp;
 constexpr int M = 22;
 
 template <int MODE>
-__global__ void kb(float* out, int nwin, int lim) {
+__global__ void __launch_bounds__(64, 10) kb(float* out, int nwin, int lim) {
     __shared__ __align__(16) float rows[M * M];
     for (int i = threadIdx.x; i < M * M; i += blockDim.x) rows[i] = 0.01f * ((i % 7) - 3);
     __syncthreads();
@@ -21,7 +21,14 @@ __global__ void kb(float* out, int nwin, int lim) {
     const bool zsx = q == 11, zsy = false;
     float ec0 = 0.5f + q, ec1 = 0.25f * q;
     for (int k = 0; k < nwin; ++k) {
-        if constexpr (MODE == 0) {
+        if constexpr (MODE == 2) {
+            basis3_full<M, false>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
+                                  R, rows, rows + 7, ati, zsx, zsy, lim);
+        } else if constexpr (MODE == 3) {
+            // dependent FFMA2 chain (latency probe)
+#pragma unroll
+            for (int i = 0; i < M; ++i) R[0] = __ffma2_rn(make_float2(rows[0], rows[0]), R[0], R[1]);
+        } else if constexpr (MODE == 0) {
             basis2_full<M, false>(std::make_integer_sequence<int, M>{}, R, rows, ati, ec0, ec1, zsx,
                                   zsy, lim);
         } else {
@@ -45,13 +52,15 @@ int main() {
     int clk;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     const int nwin = 400;
-    for (int mode = 0; mode < 2; ++mode) {
-        for (int wps : {4, 8, 12, 16, 20, 24}) {
+    for (int mode = 0; mode < 4; ++mode) {
+        for (int wps : {2, 4, 8, 12, 16, 20, 24}) {
             const int blocks = 148 * wps / 2;
             for (int rep = 0; rep < 2; ++rep) {
                 cudaEventRecord(e0);
-                if (mode == 0) kb<0><<<blocks, 64>>>(out, nwin, mode == 0 ? M : 0);
-                else kb<1><<<blocks, 64>>>(out, nwin, 0);
+                if (mode == 0) kb<0><<<blocks, 64>>>(out, nwin, M);
+                else if (mode == 1) kb<1><<<blocks, 64>>>(out, nwin, 0);
+                else if (mode == 2) kb<2><<<blocks, 64>>>(out, nwin, M);
+                else kb<3><<<blocks, 64>>>(out, nwin, M);
                 cudaEventRecord(e1);
                 cudaEventSynchronize(e1);
                 float ms;
