@@ -270,6 +270,7 @@ inline bool base_ok(const void* p) { return p != nullptr; }
 template <typename IO>
 __global__ void k_pack(const IO* __restrict__ src, IO* __restrict__ dst, int64_t B, int64_t T,
                        int M, int64_t Tp, int Mp) {
+    grid_dep_wait();
     const int64_t n = B * Tp * Mp;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -282,6 +283,7 @@ __global__ void k_pack(const IO* __restrict__ src, IO* __restrict__ dst, int64_t
 template <typename IO>
 __global__ void k_unpack(const IO* __restrict__ src, IO* __restrict__ dst, int64_t B, int64_t T,
                          int M, int64_t Tp, int Mp) {
+    grid_dep_wait();
     const int64_t n = B * T * M;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -301,7 +303,7 @@ template <typename IO>
 cudaError_t pack(const void* src, void* dst, int64_t B, int64_t T, int M, int64_t Tp, int Mp,
                  cudaStream_t st) {
     g_launches += 1;
-    k_pack<IO><<<grid_for(B * Tp * Mp), 256, 0, st>>>(static_cast<const IO*>(src),
+    launch_pdl(k_pack<IO>, grid_for(B * Tp * Mp), 256, 0, st, static_cast<const IO*>(src),
                                                        static_cast<IO*>(dst), B, T, M, Tp, Mp);
     return cudaGetLastError();
 }
@@ -309,7 +311,7 @@ template <typename IO>
 cudaError_t unpack(const void* src, void* dst, int64_t B, int64_t T, int M, int64_t Tp, int Mp,
                    cudaStream_t st) {
     g_launches += 1;
-    k_unpack<IO><<<grid_for(B * T * M), 256, 0, st>>>(static_cast<const IO*>(src),
+    launch_pdl(k_unpack<IO>, grid_for(B * T * M), 256, 0, st, static_cast<const IO*>(src),
                                                        static_cast<IO*>(dst), B, T, M, Tp, Mp);
     return cudaGetLastError();
 }
@@ -318,6 +320,7 @@ cudaError_t unpack(const void* src, void* dst, int64_t B, int64_t T, int M, int6
 template <typename IO>
 __global__ void k_shift(const IO* __restrict__ A, IO* __restrict__ out, int64_t B, int64_t T,
                         int M) {
+    grid_dep_wait();
     const int64_t n = B * T * M;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -331,6 +334,7 @@ __global__ void k_shift(const IO* __restrict__ A, IO* __restrict__ out, int64_t 
 template <typename IO>
 __global__ void k_lag(const IO* __restrict__ s, const IO* __restrict__ zi, IO* __restrict__ out,
                       int64_t B, int64_t T, int M) {
+    grid_dep_wait();
     const int64_t n = B * T * M;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -853,10 +857,10 @@ int tvlp_shift_coeffs(int32_t dtype, const void* A, void* out, int64_t B, int64_
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const unsigned grid = grid_for(B * T * M);
     if (dtype == TVLP_F64)
-        k_shift<double><<<grid, 256, 0, st>>>(static_cast<const double*>(A),
+        launch_pdl(k_shift<double>, grid, 256, 0, st, static_cast<const double*>(A),
                                               static_cast<double*>(out), B, T, M);
     else
-        k_shift<float><<<grid, 256, 0, st>>>(static_cast<const float*>(A),
+        launch_pdl(k_shift<float>, grid, 256, 0, st, static_cast<const float*>(A),
                                              static_cast<float*>(out), B, T, M);
     TVLP_CK(cudaGetLastError());
     return TVLP_OK;
@@ -869,11 +873,11 @@ int tvlp_lagged_signal_matrix(int32_t dtype, const void* s, const void* zi, void
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const unsigned grid = grid_for(B * T * M);
     if (dtype == TVLP_F64)
-        k_lag<double><<<grid, 256, 0, st>>>(static_cast<const double*>(s),
+        launch_pdl(k_lag<double>, grid, 256, 0, st, static_cast<const double*>(s),
                                             static_cast<const double*>(zi),
                                             static_cast<double*>(out), B, T, M);
     else
-        k_lag<float><<<grid, 256, 0, st>>>(static_cast<const float*>(s),
+        launch_pdl(k_lag<float>, grid, 256, 0, st, static_cast<const float*>(s),
                                            static_cast<const float*>(zi),
                                            static_cast<float*>(out), B, T, M);
     TVLP_CK(cudaGetLastError());

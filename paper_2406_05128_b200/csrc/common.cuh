@@ -5,6 +5,7 @@
 #pragma once
 #include <cstdint>
 #include <type_traits>
+#include <cstdlib>
 #include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -184,6 +185,39 @@ __device__ __forceinline__ void static_for(F&& f) {
 template <typename T>
 __device__ __forceinline__ bool is_finite_val(T x) {
     return isfinite(x);
+}
+
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel is launched with programmatic stream serialization, so its
+// launch (block scheduling, prologue) overlaps the tail of the previous
+// kernel in the stream; griddepcontrol.wait then blocks until that kernel has
+// completed and its writes are visible.  Kernels call it before touching
+// global memory.  Without the launch attribute the wait is a no-op.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("TVLP_PDL");
+        return v == nullptr || v[0] != '0';
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace tvlp

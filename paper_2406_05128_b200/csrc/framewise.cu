@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(128)
 k_fw_forward(const IO* __restrict__ e, const IO* __restrict__ frames, const IO* __restrict__ win,
              IO* __restrict__ seg, int64_t B, int64_t T, int F, int nfr, int size, int hop,
              int n_lead) {
+    grid_dep_wait();
     constexpr int L = FwGeo<M>::L;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = gid < B * nfr;
@@ -72,6 +73,7 @@ k_fw_forward(const IO* __restrict__ e, const IO* __restrict__ frames, const IO* 
 template <typename IO>
 __global__ void k_fw_ola(const IO* __restrict__ seg, IO* __restrict__ out, int64_t B, int64_t T,
                          int nfr, int size, int hop, int n_lead, IO cola) {
+    grid_dep_wait();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= B * T) return;
     const int64_t b = idx / T, t = idx % T;
@@ -97,6 +99,7 @@ k_fw_backward(const IO* __restrict__ gout, const IO* __restrict__ frames,
               const IO* __restrict__ win, const IO* __restrict__ seg, IO* __restrict__ gew,
               IO* __restrict__ gapart, int64_t B, int64_t T, int F, int nfr, int size, int hop,
               int n_lead, IO cola) {
+    grid_dep_wait();
     constexpr int L = FwGeo<M>::L;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = gid < B * nfr;
@@ -158,6 +161,7 @@ k_fw_backward(const IO* __restrict__ gout, const IO* __restrict__ frames,
 template <typename IO>
 __global__ void k_fw_gather_ge(const IO* __restrict__ gew, IO* __restrict__ ge, int64_t B,
                                int64_t T, int nfr, int size, int hop, int n_lead) {
+    grid_dep_wait();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= B * T) return;
     const int64_t b = idx / T, t = idx % T;
@@ -174,6 +178,7 @@ __global__ void k_fw_gather_ge(const IO* __restrict__ gew, IO* __restrict__ ge, 
 template <typename IO>
 __global__ void k_fw_rows(const IO* __restrict__ gapart, IO* __restrict__ gf, int64_t B, int F,
                           int nfr, int M, int n_lead) {
+    grid_dep_wait();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= B * (int64_t)F * M) return;
     const int c = (int)(idx % M);
@@ -209,14 +214,14 @@ cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* w
     const int64_t nl = a.B * a.nfr;
     const unsigned blocks = (unsigned)((nl + 127) / 128);
     TVLP_FW_DISPATCH(Mp, {
-        k_fw_forward<IO, M_><<<blocks, 128, 0, st>>>(e, frames, win, seg, a.B, a.T, a.F, a.nfr,
+        launch_pdl(k_fw_forward<IO, M_>, blocks, 128, 0, st, e, frames, win, seg, a.B, a.T, a.F, a.nfr,
                                                      a.size, a.hop, a.n_lead);
         break;
     })
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     const int64_t n = a.B * a.T;
-    k_fw_ola<IO><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(seg, out, a.B, a.T, a.nfr, a.size,
+    launch_pdl(k_fw_ola<IO>, (unsigned)((n + 255) / 256), 256, 0, st, seg, out, a.B, a.T, a.nfr, a.size,
                                                               a.hop, a.n_lead, (IO)a.cola);
     return cudaGetLastError();
 }
@@ -228,7 +233,7 @@ cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, 
     const int64_t nl = a.B * a.nfr;
     const unsigned blocks = (unsigned)((nl + 127) / 128);
     TVLP_FW_DISPATCH(Mp, {
-        k_fw_backward<IO, M_><<<blocks, 128, 0, st>>>(gout, frames, win, seg, gew, gapart, a.B,
+        launch_pdl(k_fw_backward<IO, M_>, blocks, 128, 0, st, gout, frames, win, seg, gew, gapart, a.B,
                                                       a.T, a.F, a.nfr, a.size, a.hop, a.n_lead,
                                                       (IO)a.cola);
         break;
@@ -236,12 +241,12 @@ cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, 
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     const int64_t n = a.B * a.T;
-    k_fw_gather_ge<IO><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(gew, ge, a.B, a.T, a.nfr,
+    launch_pdl(k_fw_gather_ge<IO>, (unsigned)((n + 255) / 256), 256, 0, st, gew, ge, a.B, a.T, a.nfr,
                                                                     a.size, a.hop, a.n_lead);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     const int64_t nr = a.B * (int64_t)a.F * Mp;
-    k_fw_rows<IO><<<(unsigned)((nr + 255) / 256), 256, 0, st>>>(gapart, gf, a.B, a.F, a.nfr, Mp,
+    launch_pdl(k_fw_rows<IO>, (unsigned)((nr + 255) / 256), 256, 0, st, gapart, gf, a.B, a.F, a.nfr, Mp,
                                                                 a.n_lead);
     (void)M;
     return cudaGetLastError();

@@ -30,9 +30,6 @@
 #ifndef TVLP_BASIS4_WARPS
 #define TVLP_BASIS4_WARPS 2
 #endif
-#ifndef TVLP_BASIS3_MINCTAS
-#define TVLP_BASIS3_MINCTAS 6
-#endif
 #ifndef TVLP_BASIS_GROUP
 #define TVLP_BASIS_GROUP 2
 #endif
@@ -93,6 +90,7 @@ template <typename IO, typename ACC, int M, bool TI, int NW>
 __global__ void __launch_bounds__(NW * 32)
 k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ PhiZ,
         ScanArgs g) {
+    grid_dep_wait();
     using S = BasisSmem<IO, ACC, M, TI, NW>;
     constexpr int WR = S::WR;
     constexpr int NSTB = S::NSTB;
@@ -224,401 +222,6 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ Phi
 }
 
 // ============================================================================
-// fp32 basis with packed FFMA2: one warp = two sub-chunks (half-warps); lane q
-// of a half runs the chain pair (2q, 2q+1) as one float2, the coefficient is
-// broadcast into both halves of the FFMA2 (SASS: FFMA2 Rd, Ra.F32, Rb.F32x2,
-// Rc.F32x2).  Chain M is the zero-state chain; chains > M are idle slots.
-// ============================================================================
-template <int M, bool TI, int NW>
-struct Basis2Smem {
-    static_assert(M % 2 == 0, "even orders only (odd orders are padded)");
-    static constexpr int WR = M;  // window = M rows: 4*M*M bytes, 16-B aligned for even M
-    static constexpr int NSTB = 2;
-    static constexpr int A_BYTES = TI ? 16 : WR * M * 4;
-    static constexpr int STAGE_BYTES = (A_BYTES + 15) / 16 * 16;
-    static constexpr int HALF_BYTES = NSTB * STAGE_BYTES;
-    static constexpr int BYTES = NW * 2 * HALF_BYTES + NW * 2 * NSTB * 8;
-};
-
-// One step of the packed chains at ring position U (compile-time): lags are
-// R[(U - i) mod M].  Four accumulators over lags M..2, oldest first, so the
-// freshest lag enters last; the lag-1 term closes the step.
-template <int M, bool TI, int U>
-__device__ __forceinline__ void basis2_step(float2 (&R)[M], const float* __restrict__ Ar,
-                                            const float (&ati)[M], float ec0, float ec1, bool zsx,
-                                            bool zsy) {
-    float a[M];
-    if constexpr (TI) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) a[i] = ati[i];
-    } else {
-        load_row_at<float, M>(Ar + U * M, a, U * M * 4);
-    }
-    const float ev = __shfl_sync(0xffffffffu, U < 16 ? ec0 : ec1, U & 15, 16);
-    const float2 ein = make_float2(zsx ? ev : 0.f, zsy ? ev : 0.f);  // zero-state slot only
-    float2 p[4];
-#pragma unroll
-    for (int i = M; i >= 2; --i) {
-        const float2 x = R[(U - i + 2 * M) % M];
-        const float2 ai = make_float2(a[i - 1], a[i - 1]);
-        const int c = (M - i) & 3;
-        p[c] = (M - i < 4) ? __fmul2_rn(ai, x) : __ffma2_rn(ai, x, p[c]);
-    }
-    const float2 sum = __fadd2_rn(__fadd2_rn(p[0], p[1]), __fadd2_rn(p[2], p[3]));
-    const float2 part = __fadd2_rn(ein, make_float2(-sum.x, -sum.y));
-    const float2 na0 = make_float2(-a[0], -a[0]);
-    R[U % M] = __ffma2_rn(na0, R[(U - 1 + M) % M], part);
-}
-
-// A window of M steps at ring positions 0..M-1.  The first window of a
-// sub-chunk may be partial (it starts at ring position u0): its steps are
-// guarded one by one.  Full windows run in groups of kBasisGroup steps, one
-// basic block per group: steps of a group interleave, and the group boundary
-// bounds how far the scheduler runs ahead (register pressure).
-constexpr int kBasisGroup = TVLP_BASIS_GROUP;
-template <int M, bool TI, int G, int... V>
-__device__ __forceinline__ void basis2_group(std::integer_sequence<int, V...>, float2 (&R)[M],
-                                             const float* __restrict__ Ar,
-                                             const float (&ati)[M], float ec0, float ec1,
-                                             bool zsx, bool zsy) {
-    ((G * kBasisGroup + V < M
-          ? basis2_step<M, TI, (G * kBasisGroup + V) % M>(R, Ar, ati, ec0, ec1, zsx, zsy)
-          : void()),
-     ...);
-}
-template <int M, bool TI, int... G>
-__device__ __forceinline__ void basis2_full(std::integer_sequence<int, G...>, float2 (&R)[M],
-                                            const float* __restrict__ Ar, const float (&ati)[M],
-                                            float ec0, float ec1, bool zsx, bool zsy, int lim) {
-    ((G * kBasisGroup < lim
-          ? basis2_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R, Ar, ati,
-                                   ec0, ec1, zsx, zsy)
-          : void()),
-     ...);
-}
-template <int M, bool TI, int... U>
-__device__ __forceinline__ void basis2_partial(std::integer_sequence<int, U...>, float2 (&R)[M],
-                                               const float* __restrict__ Ar,
-                                               const float (&ati)[M], float ec0, float ec1,
-                                               bool zsx, bool zsy, int u0) {
-    ((U >= u0 ? basis2_step<M, TI, U>(R, Ar, ati, ec0, ec1, zsx, zsy) : void()), ...);
-}
-
-template <int M, bool TI, int NW>
-__global__ void __launch_bounds__(NW * 32)
-k_basis2(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
-         ScanArgs g) {
-    using S = Basis2Smem<M, TI, NW>;
-    constexpr int NSTB = S::NSTB;
-    static_assert(M + 1 <= 32, "order M must be <= 31");
-    static_assert(M <= 32, "window fits two registers per lane");
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int half = lane >> 4, q = lane & 15;
-    const int slot = warp * 2 + half;
-    unsigned char* hbase = smem + slot * S::HALF_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NW * 2 * S::HALF_BYTES) + slot * NSTB;
-
-    const int64_t nsc = g.B * g.nsub;
-    const int64_t gid0 = ((int64_t)blockIdx.x * NW + warp) * 2;
-    if (gid0 >= nsc) return;  // warp-uniform
-    const int64_t gid = gid0 + half;
-    const bool active = gid < nsc;
-    const int64_t gg = active ? gid : gid0;  // an idle half shadows its sibling's rows
-    const int64_t b = gg / g.nsub;
-    const int j = (int)(gg % g.nsub);
-    const int64_t t0 = (int64_t)j * g.Ls;
-    const int len = g.Ls;  // all sub-chunks are full (T % Ls == 0)
-    // windows are aligned to the END of the sub-chunk: the first covers ring
-    // positions u0..M-1 (time 0..M-1-u0); u0 is even because M and Ls are
-    const int u0 = (M - len % M) % M;
-    const int nwin = (len + u0) / M;
-    const int64_t row0 = b * g.T + t0;
-    const float* eb = e + row0;
-
-    if (!TI && q == 0) {
-        for (int s2 = 0; s2 < NSTB; ++s2) mbar_init(&bars[s2], 1);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    auto stage_ptr = [&](int st) { return hbase + st * S::STAGE_BYTES; };
-    auto issue = [&](int k) {
-        if (TI || k >= nwin || q != 0) return;
-        const int st = k % NSTB;
-        const int first = k == 0 ? u0 : 0;              // ring position of the first row
-        const int64_t tstart = (int64_t)k * M - u0 + first;  // its time in the sub-chunk
-        const int rows = M - first;
-        mbar_arrive_expect_tx(&bars[st], rows * M * 4);
-        tma_load_1d(stage_ptr(st) + first * M * 4, A + (row0 + tstart) * M, rows * M * 4,
-                    &bars[st]);
-    };
-#pragma unroll
-    for (int k = 0; k < NSTB; ++k) issue(k);
-
-    float ati[M];
-    if (TI) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) ati[i] = A[b * M + i];
-    }
-    const int cx = 2 * q, cy = 2 * q + 1;  // chain ids of the pair
-    // initial state x_c = s(t0 - 1 - c) = unit for chain c sits at ring (u0 - 1 - c) mod M
-    float2 R[M];
-#pragma unroll
-    for (int p = 0; p < M; ++p) {
-        const int c = ((u0 - 1 - p) % M + M) % M;  // the state component at ring p
-        R[p] = make_float2(c == cx ? 1.f : 0.f, c == cy ? 1.f : 0.f);
-    }
-    const bool zsx = cx == M, zsy = cy == M;
-
-    // excitation (read by the zero-state chain only): lane q of a half holds
-    // the values of ring positions q and 16 + q of window w, loaded one window
-    // ahead; a step takes it with a 16-lane shuffle (off the recursion's chain)
-    auto eload = [&](int w, int u) {
-        const int t = w * M + u - u0;
-        return (u < M && t >= 0 && t < len) ? __ldg(eb + t) : 0.f;
-    };
-    float ec0 = eload(0, q), ec1 = eload(0, 16 + q);
-    for (int k = 0; k < nwin; ++k) {
-        const int st = k % NSTB;
-        const float en0 = eload(k + 1, q), en1 = eload(k + 1, 16 + q);
-        if (!TI) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
-        const float* Ar = reinterpret_cast<const float*>(stage_ptr(st));
-        if (k == 0 && u0 != 0)
-            basis2_partial<M, TI>(std::make_integer_sequence<int, M>{}, R, Ar, ati, ec0, ec1, zsx,
-                                  zsy, u0);
-        else
-            basis2_full<M, TI>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
-                               R, Ar, ati, ec0, ec1, zsx, zsy, g.Ls);
-        __syncwarp();
-        fence_proxy_async();
-        issue(k + NSTB);
-        ec0 = en0;
-        ec1 = en1;
-    }
-
-    // final state x[i] = s(t1 - i) = R[(M - 1 - i) mod M] (the last window is full)
-    if (active && cx <= M) {
-        float* tape = PhiZ + gid * Tape<M>::SIZE;
-        float* ox = tape + cx * Tape<M>::MP4;
-        float* oy = tape + cy * Tape<M>::MP4;
-        float* rr = tape + Tape<M>::R_ROW * Tape<M>::MP4;
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-            const float2 v = R[M - 1 - i];
-            ox[i] = v.x;
-            if (cx < M) rr[i * Tape<M>::MP4 + cx] = v.x;
-            if (cy <= M) oy[i] = v.y;
-            if (cy < M) rr[i * Tape<M>::MP4 + cy] = v.y;
-        }
-    }
-}
-
-// ============================================================================
-// fp32 basis, lane-packed: a sub-chunk needs M/2+1 = P lanes (chain pairs,
-// the last pair holds the zero-state chain), and the CTA packs S = 32W/P
-// sub-chunks into W warps so no lane idles (M = 22: P = 12, 8 sub-chunks per
-// 3 warps; k_basis2's half-warp mapping left 25% of the lanes idle).  A step
-// is 2M scalar FMA-pipe ops per lane: the excitation enters as the initial
-// value of one accumulator and the coefficients are negated in the operand.
-// ============================================================================
-constexpr int basis3_best_w(int P) {
-    int bw = 1, bn = 0, bd = 1;  // best lane efficiency S*P / (32 W) as a fraction
-    for (int w = 1; w <= 4; ++w) {
-        const int s = 32 * w / P;
-        if (s * P * bd > bn * 32 * w) {
-            bw = w;
-            bn = s * P;
-            bd = 32 * w;
-        }
-    }
-    return bw;
-}
-template <int M, bool TI>
-struct Basis3Cfg {
-    static_assert(M % 2 == 0, "even orders only (odd orders are padded)");
-    static constexpr int P = M / 2 + 1;
-    static constexpr int W = basis3_best_w(P);
-    static constexpr int S = 32 * W / P;
-    static constexpr int NSTB = 2;
-    static constexpr int ROWS_BYTES = TI ? 0 : (M * M * 4 + 15) / 16 * 16;
-    static constexpr int E_OFF = ROWS_BYTES;
-    static constexpr int STAGE = ROWS_BYTES + 128;  // + the window's excitation (<= 32 floats)
-    static constexpr int BAR_OFF = S * NSTB * STAGE;
-    static constexpr int BYTES = BAR_OFF + S * NSTB * 8;
-    // resident CTAs per SM the register budget is sized for (M = 22: 7 -> <= 96
-    // registers, i.e. 5 warps per SM sub-partition, so that 6 CTAs x 8
-    // sub-chunks x 148 SMs >= 6400 sub-chunks of config 3 run in one wave)
-    static constexpr int MIN_CTAS = TVLP_BASIS3_MINCTAS;
-};
-
-template <int M, bool TI, int U>
-__device__ __forceinline__ void basis3_step(float2 (&R)[M], const float* __restrict__ Ar,
-                                            const float* __restrict__ es, const float (&ati)[M],
-                                            bool zsx, bool zsy) {
-    float a[M];
-    if constexpr (TI) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) a[i] = ati[i];
-    } else {
-        load_row_at<float, M>(Ar + U * M, a, U * M * 4);
-    }
-    const float ev = es[U];
-    // scalar FFMA: with register operands FFMA2 issues at half the FFMA rate
-    // (tools/micro/ffma2_regs.cu: 14-18 vs 35 TFMA/s), so the pair is two
-    // independent scalar chains, each split over two accumulators
-    float xa = zsx ? ev : 0.f, ya = zsy ? ev : 0.f;  // the zero-state slot takes e
-    float xb = 0.f, yb = 0.f;
-#pragma unroll
-    for (int i = M; i >= 2; --i) {  // lags M..2, oldest first
-        const float2 v = R[(U - i + 2 * M) % M];
-        const float na = -a[i - 1];
-        if ((M - i) & 1) {
-            xb = (M - i == 1) ? na * v.x : fmaf(na, v.x, xb);
-            yb = (M - i == 1) ? na * v.y : fmaf(na, v.y, yb);
-        } else {
-            xa = fmaf(na, v.x, xa);
-            ya = fmaf(na, v.y, ya);
-        }
-    }
-    if constexpr (M > 2) {
-        xa += xb;
-        ya += yb;
-    }
-    const float2 r1 = R[(U - 1 + M) % M];
-    R[U % M] = make_float2(fmaf(-a[0], r1.x, xa), fmaf(-a[0], r1.y, ya));
-}
-template <int M, bool TI, int G, int... V>
-__device__ __forceinline__ void basis3_group(std::integer_sequence<int, V...>, float2 (&R)[M],
-                                             const float* __restrict__ Ar,
-                                             const float* __restrict__ es, const float (&ati)[M],
-                                             bool zsx, bool zsy) {
-    ((G * kBasisGroup + V < M
-          ? basis3_step<M, TI, (G * kBasisGroup + V) % M>(R, Ar, es, ati, zsx, zsy)
-          : void()),
-     ...);
-}
-template <int M, bool TI, int... G>
-__device__ __forceinline__ void basis3_full(std::integer_sequence<int, G...>, float2 (&R)[M],
-                                            const float* __restrict__ Ar,
-                                            const float* __restrict__ es, const float (&ati)[M],
-                                            bool zsx, bool zsy, int lim) {
-    ((G * kBasisGroup < lim
-          ? basis3_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R, Ar, es, ati,
-                                   zsx, zsy)
-          : void()),
-     ...);
-}
-template <int M, bool TI, int... U>
-__device__ __forceinline__ void basis3_partial(std::integer_sequence<int, U...>, float2 (&R)[M],
-                                               const float* __restrict__ Ar,
-                                               const float* __restrict__ es,
-                                               const float (&ati)[M], bool zsx, bool zsy, int u0) {
-    ((U >= u0 ? basis3_step<M, TI, U>(R, Ar, es, ati, zsx, zsy) : void()), ...);
-}
-
-template <int M, bool TI>
-__global__ void __launch_bounds__(Basis3Cfg<M, TI>::W * 32, Basis3Cfg<M, TI>::MIN_CTAS)
-k_basis3(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
-         ScanArgs g) {
-    using C = Basis3Cfg<M, TI>;
-    constexpr int P = C::P, S = C::S, NSTB = C::NSTB;
-    static_assert(M + 1 <= 32, "order M must be <= 31");
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int tid = threadIdx.x;
-    const int q = tid % P;
-    const bool lane_used = tid / P < S;
-    const int sc = lane_used ? tid / P : S - 1;
-    const int64_t nsc = g.B * g.nsub;
-    const int64_t gid = (int64_t)blockIdx.x * S + sc;
-    const bool valid = lane_used && gid < nsc;  // idle lanes compute on garbage, never wait
-    const int64_t gg = gid < nsc ? gid : nsc - 1;
-    const int64_t b = gg / g.nsub;
-    const int j = (int)(gg % g.nsub);
-    const int len = g.Ls;  // all sub-chunks are full (T % Ls == 0)
-    const int u0 = (M - len % M) % M;  // first window covers ring positions u0..M-1
-    const int nwin = (len + u0) / M;
-    const int64_t row0 = b * g.T + (int64_t)j * g.Ls;
-    const float* eb = e + row0;
-    auto stage = [&](int st) { return smem + (sc * NSTB + st) * C::STAGE; };
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF) + sc * NSTB;
-    const bool leader = valid && q == 0;
-
-    auto issue = [&](int k) {
-        if (TI || !leader || k >= nwin) return;
-        const int st = k % NSTB;
-        const int first = k == 0 ? u0 : 0;
-        const int64_t tstart = (int64_t)k * M - u0 + first;
-        const int rows = M - first;
-        mbar_arrive_expect_tx(&bars[st], rows * M * 4);
-        tma_load_1d(stage(st) + first * M * 4, A + (row0 + tstart) * M, rows * M * 4, &bars[st]);
-    };
-    auto eload = [&](int w, int u) {
-        const int t = w * M + u - u0;
-        return (valid && u < M && t >= 0 && t < len) ? __ldg(eb + t) : 0.f;
-    };
-    auto estore = [&](int st, float v0, float v1) {
-        float* es = reinterpret_cast<float*>(stage(st) + C::E_OFF);
-        if (q < M) es[q] = v0;
-        if (q + P < M) es[q + P] = v1;
-    };
-    if (leader && !TI) {
-        for (int st = 0; st < NSTB; ++st) mbar_init(&bars[st], 1);
-        fence_mbar_init();
-    }
-    estore(0, eload(0, q), eload(0, q + P));
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < NSTB; ++k) issue(k);
-
-    float ati[M];
-    if (TI) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) ati[i] = A[b * M + i];
-    }
-    const int cx = 2 * q, cy = 2 * q + 1;
-    float2 R[M];
-#pragma unroll
-    for (int p = 0; p < M; ++p) {
-        const int c = ((u0 - 1 - p) % M + M) % M;  // state component held at ring position p
-        R[p] = make_float2(c == cx ? 1.f : 0.f, c == cy ? 1.f : 0.f);
-    }
-    const bool zsx = cx == M, zsy = cy == M;
-
-    for (int k = 0; k < nwin; ++k) {
-        const int st = k % NSTB;
-        const float en0 = eload(k + 1, q), en1 = eload(k + 1, q + P);
-        if (!TI && valid) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
-        const float* Ar = reinterpret_cast<const float*>(stage(st));
-        const float* es = reinterpret_cast<const float*>(stage(st) + C::E_OFF);
-        if (k == 0 && u0 != 0)
-            basis3_partial<M, TI>(std::make_integer_sequence<int, M>{}, R, Ar, es, ati, zsx, zsy,
-                                  u0);
-        else
-            basis3_full<M, TI>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
-                               R, Ar, es, ati, zsx, zsy, len);
-        estore((k + 1) % NSTB, en0, en1);
-        fence_proxy_async();
-        __syncthreads();  // every lane is done with stage st; window k+1's excitation is visible
-        issue(k + NSTB);
-    }
-
-    if (valid && cx <= M) {
-        float* tape = PhiZ + gid * Tape<M>::SIZE;
-        float* ox = tape + cx * Tape<M>::MP4;
-        float* oy = tape + cy * Tape<M>::MP4;
-        float* rr = tape + Tape<M>::R_ROW * Tape<M>::MP4;
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-            const float2 v = R[M - 1 - i];
-            ox[i] = v.x;
-            if (cx < M) rr[i * Tape<M>::MP4 + cx] = v.x;
-            if (cy <= M) oy[i] = v.y;
-            if (cy < M) rr[i * Tape<M>::MP4 + cy] = v.y;
-        }
-    }
-}
-
-// ============================================================================
 // fp32 basis, three chains per lane (scalar FFMA).  A sub-chunk takes
 // P = ceil((M+1)/3) lanes (M = 22: 8 lanes, 24 slots for the M unit chains and
 // the zero-state chain), a warp packs S = 32/P sub-chunks and is independent
@@ -626,6 +229,10 @@ k_basis3(const float* __restrict__ e, const float* __restrict__ A, float* __rest
 // loads (7 LDS per step for M = 22) are shared by its three chains, and the
 // three chains are independent FMA streams (ILP) within the step.
 // ============================================================================
+// steps per basic block in full windows: steps of a group interleave; the
+// group boundary bounds how far the scheduler runs ahead (register pressure)
+constexpr int kBasisGroup = TVLP_BASIS_GROUP;
+
 template <int M, bool TI>
 struct Basis4Cfg {
     static_assert(M % 2 == 0, "even orders only (odd orders are padded)");
@@ -704,6 +311,7 @@ template <int M, bool TI>
 __global__ void __launch_bounds__(Basis4Cfg<M, TI>::NW * 32)
 k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
          ScanArgs g) {
+    grid_dep_wait();
     using C = Basis4Cfg<M, TI>;
     constexpr int P = C::P, S = C::S, NSTB = C::NSTB;
     static_assert(M + 1 <= 32, "order M must be <= 31");
@@ -890,6 +498,7 @@ struct CarryArgs {
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_carry_fwd(const CarryArgs<CT> a) {
+    grid_dep_wait();
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
@@ -976,6 +585,7 @@ k_carry_fwd(const CarryArgs<CT> a) {
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_carry_bwd(const CarryArgs<CT> a) {
+    grid_dep_wait();
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
@@ -1062,6 +672,7 @@ template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_group_P(const CT* __restrict__ tape, CT* __restrict__ gtape, int64_t ngroups, int G, int nsub,
           const int* __restrict__ only) {
+    grid_dep_wait();
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT>;
     constexpr int MP4 = TP::MP4;
@@ -1174,6 +785,7 @@ __global__ void __launch_bounds__(32)
 k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
             const IO* __restrict__ Xin, int* __restrict__ flag, IO* __restrict__ Xend,
             unsigned* __restrict__ dstat, const int* __restrict__ only, ScanArgs g) {
+    grid_dep_wait();
     using S = LaneSmem<IO, M, TI>;
     constexpr int W = S::W;
     constexpr int MR = (M + W - 1) / W * W;
@@ -1324,6 +936,7 @@ __global__ void __launch_bounds__(32)
 k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
           const IO* __restrict__ Mu, IO* __restrict__ Nu, unsigned* __restrict__ dstat,
           const int* __restrict__ only, ScanArgs g) {
+    grid_dep_wait();
     using S = LaneSmem<IO, M, TI>;
     constexpr int W = S::W;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1463,6 +1076,7 @@ template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_refine_fwd(const CT* __restrict__ tape, CT* __restrict__ Xin, const CT* __restrict__ Xend,
              const unsigned* __restrict__ dstat, int* __restrict__ flags, int nsub, int64_t B) {
+    grid_dep_wait();
     using TP = Tape<M>;
     constexpr int MP4 = TP::MP4;
     __shared__ __align__(16) CT es[32];
@@ -1501,6 +1115,7 @@ __global__ void __launch_bounds__(32)
 k_refine_bwd(const CT* __restrict__ tape, CT* __restrict__ Mu, const CT* __restrict__ K,
              const unsigned* __restrict__ dstat, int* __restrict__ flags, int nsub, int64_t B,
              const int* __restrict__ fflags) {
+    grid_dep_wait();
     using TP = Tape<M>;
     constexpr int MP4 = TP::MP4;
     __shared__ __align__(16) CT es[32];
@@ -1540,6 +1155,7 @@ k_refine_bwd(const CT* __restrict__ tape, CT* __restrict__ Mu, const CT* __restr
 // short path decides inside k_refine_fwd/bwd).
 static __global__ void k_refine_decide(const unsigned* __restrict__ dstat, int* __restrict__ flags,
                                 const int* __restrict__ inherit, float tol, int64_t B) {
+    grid_dep_wait();
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     const float d = __uint_as_float(dstat[2 * b]), x = __uint_as_float(dstat[2 * b + 1]);
@@ -1554,6 +1170,7 @@ template <typename CT>
 __global__ void k_defects(const CT* __restrict__ P, const CT* __restrict__ Q, CT* __restrict__ D,
                           int nsub, int mp4, int M, bool fwd, const int* __restrict__ only,
                           int64_t B) {
+    grid_dep_wait();
     const int64_t n = B * (int64_t)nsub * mp4;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -1573,6 +1190,7 @@ __global__ void k_defects(const CT* __restrict__ P, const CT* __restrict__ Q, CT
 template <typename CT>
 __global__ void k_add_rows(CT* __restrict__ X, const CT* __restrict__ E, int nsub, int mp4,
                            const int* __restrict__ only, int64_t B) {
+    grid_dep_wait();
     const int64_t n = B * (int64_t)nsub * mp4;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -1589,6 +1207,7 @@ template <typename IO, int M>
 __global__ void __launch_bounds__(256)
 k_grad_A(const IO* __restrict__ ge, const IO* __restrict__ s, const IO* __restrict__ zi,
          IO* __restrict__ gA, int64_t T) {
+    grid_dep_wait();
     constexpr int RT = 256;
     __shared__ IO sh_s[RT + M];
     __shared__ IO sh_g[RT];
@@ -1623,6 +1242,7 @@ template <typename IO>
 __global__ void k_grad_a_partial(const IO* __restrict__ ge, const IO* __restrict__ s,
                                  const IO* __restrict__ zi, IO* __restrict__ part,
                                  int64_t T, int M, int nchunk) {
+    grid_dep_wait();
     const int64_t b = blockIdx.y;
     const int chunk = blockIdx.x;
     const int64_t len = (T + nchunk - 1) / nchunk;
@@ -1656,6 +1276,7 @@ __global__ void k_grad_a_partial(const IO* __restrict__ ge, const IO* __restrict
 template <typename IO>
 __global__ void k_grad_a_final(const IO* __restrict__ part, IO* __restrict__ ga, int64_t B, int M,
                                int nchunk) {
+    grid_dep_wait();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= B * M) return;
     const int64_t b = idx / M;

@@ -17,7 +17,7 @@ cudaError_t ensure_smem(K kernel, int bytes) {
 }
 
 #ifndef TVLP_BASIS_WARPS
-#define TVLP_BASIS_WARPS 2
+#define TVLP_BASIS_WARPS 4
 #endif
 constexpr int kBasisWarps = TVLP_BASIS_WARPS;
 
@@ -30,7 +30,7 @@ cudaError_t basis_impl(const IO* e, const IO* A, IO* PhiZ, const ScanArgs& g,
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
     const int64_t blocks = (nsc + kBasisWarps - 1) / kBasisWarps;
-    k<<<(unsigned)blocks, kBasisWarps * 32, S::BYTES, st>>>(e, A, PhiZ, g);
+    launch_pdl(k, (unsigned)blocks, kBasisWarps * 32, S::BYTES, st, e, A, PhiZ, g);
     return cudaGetLastError();
 }
 
@@ -78,32 +78,6 @@ cudaError_t lane_maps(LaneMaps& mp, const IO* A, const IO* X, const IO* O, const
 }
 
 template <int M, bool TI>
-cudaError_t basis2_impl(const float* e, const float* A, float* PhiZ, const ScanArgs& g,
-                        cudaStream_t st) {
-    using S = Basis2Smem<M, TI, kBasisWarps>;
-    auto k = k_basis2<M, TI, kBasisWarps>;
-    cudaError_t err = ensure_smem(k, S::BYTES);
-    if (err != cudaSuccess) return err;
-    const int64_t nsc = g.B * g.nsub;
-    const int64_t per_block = 2 * kBasisWarps;
-    k<<<(unsigned)((nsc + per_block - 1) / per_block), kBasisWarps * 32, S::BYTES, st>>>(e, A,
-                                                                                      PhiZ, g);
-    return cudaGetLastError();
-}
-
-template <int M, bool TI>
-cudaError_t basis3_impl(const float* e, const float* A, float* PhiZ, const ScanArgs& g,
-                        cudaStream_t st) {
-    using C = Basis3Cfg<M, TI>;
-    auto k = k_basis3<M, TI>;
-    cudaError_t err = ensure_smem(k, C::BYTES);
-    if (err != cudaSuccess) return err;
-    const int64_t nsc = g.B * g.nsub;
-    k<<<(unsigned)((nsc + C::S - 1) / C::S), C::W * 32, C::BYTES, st>>>(e, A, PhiZ, g);
-    return cudaGetLastError();
-}
-
-template <int M, bool TI>
 cudaError_t basis4_impl(const float* e, const float* A, float* PhiZ, const ScanArgs& g,
                         cudaStream_t st) {
     using C = Basis4Cfg<M, TI>;
@@ -112,7 +86,7 @@ cudaError_t basis4_impl(const float* e, const float* A, float* PhiZ, const ScanA
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
     const int64_t per = (int64_t)C::S * C::NW;
-    k<<<(unsigned)((nsc + per - 1) / per), C::NW * 32, C::BYTES, st>>>(e, A, PhiZ, g);
+    launch_pdl(k, (unsigned)((nsc + per - 1) / per), C::NW * 32, C::BYTES, st, e, A, PhiZ, g);
     return cudaGetLastError();
 }
 
@@ -127,7 +101,7 @@ cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag
     err = lane_maps<IO, M, TI>(mp, TI ? nullptr : A, e, s, g);
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
-    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Xin, flag, Xend,
+    launch_pdl(k, (unsigned)((nsc + 31) / 32), 32, S::BYTES, st, mp, TI ? A : nullptr, Xin, flag, Xend,
                                                         dstat, only, g);
     return cudaGetLastError();
 }
@@ -143,7 +117,7 @@ cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge
     err = lane_maps<IO, M, TI>(mp, TI ? nullptr : A, gs, MODE == 1 ? ge : nullptr, g);
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
-    k<<<(unsigned)((nsc + 31) / 32), 32, S::BYTES, st>>>(mp, TI ? A : nullptr, Mu, Nu, dstat,
+    launch_pdl(k, (unsigned)((nsc + 31) / 32), 32, S::BYTES, st, mp, TI ? A : nullptr, Mu, Nu, dstat,
                                                         only, g);
     return cudaGetLastError();
 }
@@ -195,7 +169,7 @@ cudaError_t carry_fwd_impl(const CarryArgs<IO>& a, cudaStream_t st) {
     auto k = k_carry_fwd<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
-    k<<<(unsigned)a.nseg, 32, SM::BYTES, st>>>(a);
+    launch_pdl(k, (unsigned)a.nseg, 32, SM::BYTES, st, a);
     return cudaGetLastError();
 }
 
@@ -205,7 +179,7 @@ cudaError_t carry_bwd_impl(const CarryArgs<IO>& a, cudaStream_t st) {
     auto k = k_carry_bwd<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
-    k<<<(unsigned)a.nseg, 32, SM::BYTES, st>>>(a);
+    launch_pdl(k, (unsigned)a.nseg, 32, SM::BYTES, st, a);
     return cudaGetLastError();
 }
 
@@ -216,7 +190,7 @@ cudaError_t group_P_impl(const IO* tape, IO* gtape, int64_t ngroups, int G, int 
     auto k = k_group_P<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
-    k<<<(unsigned)ngroups, 32, SM::BYTES, st>>>(tape, gtape, ngroups, G, nsub, only);
+    launch_pdl(k, (unsigned)ngroups, 32, SM::BYTES, st, tape, gtape, ngroups, G, nsub, only);
     return cudaGetLastError();
 }
 
@@ -253,11 +227,11 @@ cudaError_t launch_refine_helpers(int what, int Mp, const IO* P, const IO* Q, IO
     if (grid > 148 * 32) grid = 148 * 32;
     if (grid < 1) grid = 1;
     if (what == 0)
-        k_refine_decide<<<(unsigned)((B + 127) / 128), 128, 0, st>>>(dstat, flags, inherit, tol, B);
+        launch_pdl(k_refine_decide, (unsigned)((B + 127) / 128), 128, 0, st, dstat, flags, inherit, tol, B);
     else if (what == 1)
-        k_defects<IO><<<(unsigned)grid, 256, 0, st>>>(P, Q, D, nsub, mp4, Mp, fwd, only, B);
+        launch_pdl(k_defects<IO>, (unsigned)grid, 256, 0, st, P, Q, D, nsub, mp4, Mp, fwd, only, B);
     else
-        k_add_rows<IO><<<(unsigned)grid, 256, 0, st>>>(const_cast<IO*>(P), Q, nsub, mp4, only, B);
+        launch_pdl(k_add_rows<IO>, (unsigned)grid, 256, 0, st, const_cast<IO*>(P), Q, nsub, mp4, only, B);
     return cudaGetLastError();
 }
 
@@ -277,10 +251,10 @@ cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xen
                           cudaStream_t st) {
     TVLP_DISPATCH_M(Mp, {
         if (fwd)
-            k_refine_fwd<M_, IO><<<(unsigned)g.B, 32, 0, st>>>(tape, X, Xend, dstat, flags, g.nsub,
+            launch_pdl(k_refine_fwd<M_, IO>, (unsigned)g.B, 32, 0, st, tape, X, Xend, dstat, flags, g.nsub,
                                                                g.B);
         else
-            k_refine_bwd<M_, IO><<<(unsigned)g.B, 32, 0, st>>>(tape, X, Xend, dstat, flags, g.nsub,
+            launch_pdl(k_refine_bwd<M_, IO>, (unsigned)g.B, 32, 0, st, tape, X, Xend, dstat, flags, g.nsub,
                                                                g.B, fflags);
         return cudaGetLastError();
     })
@@ -304,7 +278,7 @@ cudaError_t launch_grad_A(int Mp, const IO* ge, const IO* s, const IO* zi, IO* g
                           int64_t T, cudaStream_t st) {
     dim3 grid((unsigned)((T + 255) / 256), (unsigned)B);
     TVLP_DISPATCH_M(Mp, {
-        k_grad_A<IO, M_><<<grid, 256, 0, st>>>(ge, s, zi, gA, T);
+        launch_pdl(k_grad_A<IO, M_>, grid, 256, 0, st, ge, s, zi, gA, T);
         return cudaGetLastError();
     })
 }
@@ -313,10 +287,10 @@ template <typename IO>
 cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* part, IO* ga,
                           int64_t B, int64_t T, int nchunk, cudaStream_t st) {
     dim3 grid((unsigned)nchunk, (unsigned)B);
-    k_grad_a_partial<IO><<<grid, 256, 0, st>>>(ge, s, zi, part, T, M, nchunk);
+    launch_pdl(k_grad_a_partial<IO>, grid, 256, 0, st, ge, s, zi, part, T, M, nchunk);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return err;
-    k_grad_a_final<IO><<<(unsigned)((B * M + 127) / 128), 128, 0, st>>>(part, ga, B, M, nchunk);
+    launch_pdl(k_grad_a_final<IO>, (unsigned)((B * M + 127) / 128), 128, 0, st, part, ga, B, M, nchunk);
     return cudaGetLastError();
 }
 
