@@ -122,8 +122,14 @@ inline int64_t mp4(const Plan& p) { return (p.Mp + 3) / 4 * 4; }
 // context"), recursively.  Level-l group tapes live in the carry tape after
 // the level-0 tapes and the per-sequence flag slots, so the backward reuses
 // the forward's group products.
-constexpr int kSerialMax = 256;
-constexpr int kGroup = 32;
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v != nullptr && v[0] != 0) ? std::atoi(v) : dflt;
+}
+// tuning knobs (read once per process): the longest serial carry chain and
+// the group length of the hierarchical scheme
+const int kSerialMax = env_int("TVLP_CARRY_SERIAL_MAX", 256);
+const int kGroup = env_int("TVLP_CARRY_GROUP", 32);
 struct Levels {
     int L = 1;
     int64_t n[8] = {};

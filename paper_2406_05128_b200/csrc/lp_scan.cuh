@@ -27,6 +27,9 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef TVLP_BASIS4_SPLIT
+#define TVLP_BASIS4_SPLIT 0
+#endif
 #ifndef TVLP_BASIS4_WARPS
 #define TVLP_BASIS4_WARPS 2
 #endif
@@ -262,6 +265,33 @@ __device__ __forceinline__ void basis4_step(float (&R0)[M], float (&R1)[M], floa
     }
     const float ev = es[U];
     float c0 = zs == 0 ? ev : 0.f, c1 = zs == 1 ? ev : 0.f, c2 = zs == 2 ? ev : 0.f;
+#if TVLP_BASIS4_SPLIT
+    // two accumulators per chain: six independent FMA streams per lane
+    float d0 = 0.f, d1 = 0.f, d2 = 0.f;
+#pragma unroll
+    for (int i = M; i >= 2; --i) {  // lags M..2, oldest first
+        const int r = (U - i + 2 * M) % M;
+        const float na = -a[i - 1];
+        if (((M - i) & 1) && M - i > 1) {
+            d0 = fmaf(na, R0[r], d0);
+            d1 = fmaf(na, R1[r], d1);
+            d2 = fmaf(na, R2[r], d2);
+        } else if ((M - i) & 1) {
+            d0 = na * R0[r];
+            d1 = na * R1[r];
+            d2 = na * R2[r];
+        } else {
+            c0 = fmaf(na, R0[r], c0);
+            c1 = fmaf(na, R1[r], c1);
+            c2 = fmaf(na, R2[r], c2);
+        }
+    }
+    if constexpr (M > 2) {
+        c0 += d0;
+        c1 += d1;
+        c2 += d2;
+    }
+#else
 #pragma unroll
     for (int i = M; i >= 2; --i) {  // lags M..2, oldest first
         const int r = (U - i + 2 * M) % M;
@@ -270,6 +300,7 @@ __device__ __forceinline__ void basis4_step(float (&R0)[M], float (&R1)[M], floa
         c1 = fmaf(na, R1[r], c1);
         c2 = fmaf(na, R2[r], c2);
     }
+#endif
     const int r1 = (U - 1 + M) % M;
     R0[U % M] = fmaf(-a[0], R0[r1], c0);
     R1[U % M] = fmaf(-a[0], R1[r1], c1);
