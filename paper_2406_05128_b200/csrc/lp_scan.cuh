@@ -30,6 +30,9 @@
 #ifndef TVLP_BASIS4_SPLIT
 #define TVLP_BASIS4_SPLIT 0
 #endif
+#ifndef TVLP_BASIS4_MINB
+#define TVLP_BASIS4_MINB 1
+#endif
 #ifndef TVLP_BASIS4_WARPS
 #define TVLP_BASIS4_WARPS 2
 #endif
@@ -339,7 +342,7 @@ __device__ __forceinline__ void basis4_partial(std::integer_sequence<int, U...>,
 }
 
 template <int M, bool TI>
-__global__ void __launch_bounds__(Basis4Cfg<M, TI>::NW * 32)
+__global__ void __launch_bounds__(Basis4Cfg<M, TI>::NW * 32, TVLP_BASIS4_MINB)
 k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
          ScanArgs g) {
     grid_dep_wait();
