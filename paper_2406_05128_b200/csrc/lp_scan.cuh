@@ -248,8 +248,12 @@ struct Basis4Cfg {
     static constexpr int NSTB = 2;
     static constexpr int ROWS_BYTES = TI ? 0 : (M * M * 4 + 15) / 16 * 16;
     static constexpr int E_OFF = ROWS_BYTES;
-    static constexpr int STAGE = ROWS_BYTES + 128;  // + the window's excitation (<= 32 floats)
-    static constexpr int WARP_BYTES = S * NSTB * STAGE;
+    static constexpr int STAGE = ROWS_BYTES + 128;  // + the window's excitation (<= 28 floats)
+    // after the scan a sub-chunk's region holds half of its tape at a time
+    // (W + z rows, then R rows) for the bulk store
+    static constexpr int OUT_BYTES = (M + 1) * Tape<M>::MP4 * 4;
+    static constexpr int SUB_BYTES = NSTB * STAGE > OUT_BYTES ? NSTB * STAGE : OUT_BYTES;
+    static constexpr int WARP_BYTES = S * SUB_BYTES;
     static constexpr int BAR_OFF = NW * WARP_BYTES;
     static constexpr int BYTES = BAR_OFF + NW * S * NSTB * 8;
 };
@@ -326,11 +330,18 @@ __device__ __forceinline__ void basis4_full(std::integer_sequence<int, G...>, fl
                                             const float* __restrict__ Ar,
                                             const float* __restrict__ es, const float (&ati)[M],
                                             int zs, int lim) {
-    ((G * kBasisGroup < lim
-          ? basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R0, R1, R2, Ar,
-                                   es, ati, zs)
-          : void()),
-     ...);
+    if constexpr (TI) {
+        // no row loads to keep in place: one straight-line window
+        (basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R0, R1, R2, Ar, es,
+                                ati, zs),
+         ...);
+    } else {
+        ((G * kBasisGroup < lim
+              ? basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R0, R1, R2,
+                                       Ar, es, ati, zs)
+              : void()),
+         ...);
+    }
 }
 template <int M, bool TI, int... U>
 __device__ __forceinline__ void basis4_partial(std::integer_sequence<int, U...>, float (&R0)[M],
@@ -366,34 +377,39 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
     const int64_t row0 = b * g.T + (int64_t)j * g.Ls;
     const float* eb = e + row0;
     unsigned char* wbase = smem + warp * C::WARP_BYTES;
-    auto stage = [&](int st) { return wbase + (sc * NSTB + st) * C::STAGE; };
+    unsigned char* sbase = wbase + sc * C::SUB_BYTES;
+    auto stage = [&](int st) { return sbase + st * C::STAGE; };
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF) + (warp * S + sc) * NSTB;
     const bool leader = valid && q == 0;
 
+    // Window k covers ring positions first..M-1 = times k*M - u0 + (first..M-1).
+    // Its coefficient rows and its excitation both arrive by bulk copy on the
+    // stage's mbarrier; the excitation copy starts at the 16-byte boundary at
+    // or below the window's first time (row0 is a multiple of 8 samples) and
+    // ends at the next boundary at or above its end (never past the sub-chunk,
+    // whose end is the end of the last window), so es = base + eoff.
+    auto e_lo = [&](int k) {
+        const int first = k == 0 ? u0 : 0;
+        return (k * M - u0 + first) & ~3;
+    };
     auto issue = [&](int k) {
-        if (TI || !leader || k >= nwin) return;
+        if (!leader || k >= nwin) return;
         const int st = k % NSTB;
         const int first = k == 0 ? u0 : 0;
         const int64_t tstart = (int64_t)k * M - u0 + first;
         const int rows = M - first;
-        mbar_arrive_expect_tx(&bars[st], rows * M * 4);
-        tma_load_1d(stage(st) + first * M * 4, A + (row0 + tstart) * M, rows * M * 4, &bars[st]);
+        const int elo = e_lo(k), ehi = (k * M - u0 + M + 3) & ~3;
+        const uint32_t ebytes = (uint32_t)(ehi - elo) * 4;
+        mbar_arrive_expect_tx(&bars[st], (TI ? 0 : rows * M * 4) + ebytes);
+        if (!TI)
+            tma_load_1d(stage(st) + first * M * 4, A + (row0 + tstart) * M, rows * M * 4,
+                        &bars[st]);
+        tma_load_1d(stage(st) + C::E_OFF, eb + elo, ebytes, &bars[st]);
     };
-    auto eload = [&](int w, int u) {
-        const int t = w * M + u - u0;
-        return (valid && u < M && t >= 0 && t < len) ? __ldg(eb + t) : 0.f;
-    };
-    auto estore = [&](int st, float v0, float v1, float v2) {
-        float* es = reinterpret_cast<float*>(stage(st) + C::E_OFF);
-        if (q < M) es[q] = v0;
-        if (q + P < M) es[q + P] = v1;
-        if (q + 2 * P < M) es[q + 2 * P] = v2;
-    };
-    if (leader && !TI) {
+    if (leader) {
         for (int st = 0; st < NSTB; ++st) mbar_init(&bars[st], 1);
         fence_mbar_init();
     }
-    estore(0, eload(0, q), eload(0, q + P), eload(0, q + 2 * P));
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < NSTB; ++k) issue(k);
@@ -416,35 +432,68 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
 
     for (int k = 0; k < nwin; ++k) {
         const int st = k % NSTB;
-        const float en0 = eload(k + 1, q), en1 = eload(k + 1, q + P), en2 = eload(k + 1, q + 2 * P);
-        if (!TI && valid) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
+        if (valid) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
         const float* Ar = reinterpret_cast<const float*>(stage(st));
-        const float* es = reinterpret_cast<const float*>(stage(st) + C::E_OFF);
+        const float* es =
+            reinterpret_cast<const float*>(stage(st) + C::E_OFF) + (k * M - u0 - e_lo(k));
         if (k == 0 && u0 != 0)
             basis4_partial<M, TI>(std::make_integer_sequence<int, M>{}, R0, R1, R2, Ar, es, ati, zs,
                                   u0);
         else
             basis4_full<M, TI>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
                                R0, R1, R2, Ar, es, ati, zs, len);
-        estore((k + 1) % NSTB, en0, en1, en2);
-        fence_proxy_async();
-        __syncwarp();  // the warp is done with stage st; window k+1's excitation is visible
+        __syncwarp();  // the warp is done with stage st (generic reads before the async refill
+                       // are ordered by this sync; no proxy fence is needed for WAR)
         issue(k + NSTB);
     }
 
-    if (valid) {
-        float* tape = PhiZ + gid * Tape<M>::SIZE;
-        float* rr = tape + Tape<M>::R_ROW * Tape<M>::MP4;
+    // Final states -> tape through shared memory: the tape rows of a sub-chunk
+    // are assembled in its (now idle) stage region and leave as two bulk
+    // stores (W + z rows, then the transposed R rows) instead of 132 scattered
+    // 4-byte stores per lane.
+    constexpr int MP4 = Tape<M>::MP4;
+    float* buf = reinterpret_cast<float*>(sbase);
+    float* tape = PhiZ + gg * Tape<M>::SIZE;
+    __syncwarp();
+    if (lane_used) {
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             const float v[3] = {R0[M - 1 - i], R1[M - 1 - i], R2[M - 1 - i]};
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int ch = c0 + c;
-                if (ch <= M) tape[ch * Tape<M>::MP4 + i] = v[c];  // W column ch / z row
-                if (ch < M) rr[i * Tape<M>::MP4 + ch] = v[c];    // R row i
-            }
+            for (int c = 0; c < 3; ++c)
+                if (c0 + c <= M) buf[(c0 + c) * MP4 + i] = v[c];  // W column c0+c / z row
         }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            if (c0 + c <= M)
+                for (int i = M; i < MP4; ++i) buf[(c0 + c) * MP4 + i] = 0.f;
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (leader) {
+        tma_store_1d(tape, buf, (M + 1) * MP4 * 4);
+        bulk_commit();
+        bulk_wait_read<0>();
+    }
+    __syncwarp();
+    if (lane_used) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const float v[3] = {R0[M - 1 - i], R1[M - 1 - i], R2[M - 1 - i]};
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if (c0 + c < M) buf[i * MP4 + c0 + c] = v[c];  // R row i
+        }
+        if (zs >= 0 && zs < 3)  // the zero-state lane pads the R rows
+            for (int i = 0; i < M; ++i)
+                for (int c = M; c < MP4; ++c) buf[i * MP4 + c] = 0.f;
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (leader) {
+        tma_store_1d(tape + Tape<M>::R_ROW * MP4, buf, M * MP4 * 4);
+        bulk_commit();
+        bulk_wait<0>();
     }
 }
 

@@ -37,9 +37,10 @@ int main() {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int iters = 20000;
-    for (int mode = 0; mode < 6; ++mode)
+    for (int wps : {64, 16, 12, 8})
+    for (int mode = 3; mode < 6; ++mode)
         for (int rep = 0; rep < 2; ++rep) {
-            const int blocks = 148 * 8, threads = 256;
+            const int blocks = 148 * wps / 2, threads = 64;
             cudaEventRecord(e0);
             if (mode == 0) k<0><<<blocks, threads>>>(out, 0.999f, iters);
             if (mode == 1) k<1><<<blocks, threads>>>(out, 0.999f, iters);
@@ -52,7 +53,7 @@ int main() {
             float ms;
             cudaEventElapsedTime(&ms, e0, e1);
             const double fma = 16.0 * iters * blocks * threads;
-            if (rep) printf("mode %d: %.2f TFMA/s\n", mode, fma / (ms * 1e-3) / 1e12);
+            if (rep) printf("warps/SM %d mode %d: %.2f TFMA/s\n", wps, mode, fma / (ms * 1e-3) / 1e12);
         }
     return 0;
 }
