@@ -279,9 +279,16 @@ def run_b200(args, cfg, rank, world, dist):
         cnt, tot = prof[dom]
         t_step = tot / nsteps * 1e-3  # seconds of this kernel per step (all its slices)
         ach = (bps * lp_rows * T / t_step / 1e9) if bps is not None else None
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "r1_traffic.json")
+        if os.path.exists(tf) and kind in ("tv", "hpn") and (lp_rows, T, M) == (64, 48000, 22):
+            # dram__bytes_read + dram__bytes_write of this kernel, one ncu --set
+            # full capture of the same config (profiles/r1_ncu_full_raw.csv)
+            with open(tf) as fh:
+                traffic = json.load(fh).get(dom, {}).get("dram_bytes")
         roof = {"bound": "hbm", "kernel": dom,
                 "achieved": None if ach is None else round(ach, 1), "peak": hbm, "unit": "GB/s",
-                "frac": None if ach is None else round(ach / hbm, 4), "traffic": None,
+                "frac": None if ach is None else round(ach / hbm, 4), "traffic": traffic,
                 "peak_source": peak_kind,
                 "bytes_per_step": None if bps is None else bps * lp_rows * T,
                 "us_per_step": round(t_step * 1e6, 2), "launches_per_step": cnt / nsteps}
