@@ -30,6 +30,9 @@
 #ifndef TVLP_BASIS4_SPLIT
 #define TVLP_BASIS4_SPLIT 0
 #endif
+#ifndef TVLP_BASIS4_PIPE
+#define TVLP_BASIS4_PIPE 0
+#endif
 #ifndef TVLP_BASIS4_MINB
 #define TVLP_BASIS4_MINB 1
 #endif
@@ -238,6 +241,7 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ Phi
 // steps per basic block in full windows: steps of a group interleave; the
 // group boundary bounds how far the scheduler runs ahead (register pressure)
 constexpr int kBasisGroup = TVLP_BASIS_GROUP;
+constexpr bool kBasisPipe = TVLP_BASIS4_PIPE;
 
 template <int M, bool TI>
 struct Basis4Cfg {
@@ -262,11 +266,17 @@ template <int M, bool TI, int U>
 __device__ __forceinline__ void basis4_step(float (&R0)[M], float (&R1)[M], float (&R2)[M],
                                             const float* __restrict__ Ar,
                                             const float* __restrict__ es, const float (&ati)[M],
-                                            int zs) {
+                                            float (&ac)[M], int zs) {
     float a[M];
     if constexpr (TI) {
 #pragma unroll
         for (int i = 0; i < M; ++i) a[i] = ati[i];
+    } else if constexpr (kBasisPipe) {
+        // row U was loaded one step ahead into ac; fetch row U+1 now so its
+        // shared-memory latency hides behind this step's FMAs
+#pragma unroll
+        for (int i = 0; i < M; ++i) a[i] = ac[i];
+        if constexpr (U + 1 < M) load_row_at<float, M>(Ar + (U + 1) * M, ac, (U + 1) * M * 4);
     } else {
         load_row_at<float, M>(Ar + U * M, a, U * M * 4);
     }
@@ -318,9 +328,9 @@ __device__ __forceinline__ void basis4_group(std::integer_sequence<int, V...>, f
                                              float (&R1)[M], float (&R2)[M],
                                              const float* __restrict__ Ar,
                                              const float* __restrict__ es, const float (&ati)[M],
-                                             int zs) {
+                                             float (&ac)[M], int zs) {
     ((G * kBasisGroup + V < M
-          ? basis4_step<M, TI, (G * kBasisGroup + V) % M>(R0, R1, R2, Ar, es, ati, zs)
+          ? basis4_step<M, TI, (G * kBasisGroup + V) % M>(R0, R1, R2, Ar, es, ati, ac, zs)
           : void()),
      ...);
 }
@@ -329,16 +339,16 @@ __device__ __forceinline__ void basis4_full(std::integer_sequence<int, G...>, fl
                                             float (&R1)[M], float (&R2)[M],
                                             const float* __restrict__ Ar,
                                             const float* __restrict__ es, const float (&ati)[M],
-                                            int zs, int lim) {
+                                            float (&ac)[M], int zs, int lim) {
     if constexpr (TI) {
         // no row loads to keep in place: one straight-line window
         (basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R0, R1, R2, Ar, es,
-                                ati, zs),
+                                ati, ac, zs),
          ...);
     } else {
         ((G * kBasisGroup < lim
               ? basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R0, R1, R2,
-                                       Ar, es, ati, zs)
+                                       Ar, es, ati, ac, zs)
               : void()),
          ...);
     }
@@ -348,8 +358,9 @@ __device__ __forceinline__ void basis4_partial(std::integer_sequence<int, U...>,
                                                float (&R1)[M], float (&R2)[M],
                                                const float* __restrict__ Ar,
                                                const float* __restrict__ es,
-                                               const float (&ati)[M], int zs, int u0) {
-    ((U >= u0 ? basis4_step<M, TI, U>(R0, R1, R2, Ar, es, ati, zs) : void()), ...);
+                                               const float (&ati)[M], float (&ac)[M], int zs,
+                                               int u0) {
+    ((U >= u0 ? basis4_step<M, TI, U>(R0, R1, R2, Ar, es, ati, ac, zs) : void()), ...);
 }
 
 template <int M, bool TI>
@@ -422,6 +433,7 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
     const int c0 = 3 * q;  // chains c0, c0+1, c0+2 (chain M is the zero-state chain)
     const int zs = M - c0;  // which of the three is the zero-state chain (0..2), if any
     float R0[M], R1[M], R2[M];
+    float ac[M];  // coefficient row of the next step (pipelined loads)
 #pragma unroll
     for (int p = 0; p < M; ++p) {
         const int c = ((u0 - 1 - p) % M + M) % M;  // state component held at ring position p
@@ -436,12 +448,16 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
         const float* Ar = reinterpret_cast<const float*>(stage(st));
         const float* es =
             reinterpret_cast<const float*>(stage(st) + C::E_OFF) + (k * M - u0 - e_lo(k));
+        if (!TI && kBasisPipe) {  // first row of the window (later rows are fetched a step ahead)
+            const int first = (k == 0) ? u0 : 0;
+            load_row_at<float, M>(Ar + first * M, ac, first * M * 4);
+        }
         if (k == 0 && u0 != 0)
-            basis4_partial<M, TI>(std::make_integer_sequence<int, M>{}, R0, R1, R2, Ar, es, ati, zs,
-                                  u0);
+            basis4_partial<M, TI>(std::make_integer_sequence<int, M>{}, R0, R1, R2, Ar, es, ati, ac,
+                                  zs, u0);
         else
             basis4_full<M, TI>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
-                               R0, R1, R2, Ar, es, ati, zs, len);
+                               R0, R1, R2, Ar, es, ati, ac, zs, len);
         __syncwarp();  // the warp is done with stage st (generic reads before the async refill
                        // are ordered by this sync; no proxy fence is needed for WAR)
         issue(k + NSTB);
