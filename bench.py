@@ -346,7 +346,7 @@ def run_b200(args, cfg, rank, world, dist):
                    "kind": kind, "B_per_gpu": B, "T": T, "M": M,
                    "global_B": B * world, "parallelism": f"batch-shard x{world}",
                    "carry_precision": lpc.carry_precision(),
-                   "subchunk": int(lib.tvlp_subchunk_len(T, M)) if kind == "tv" else None,
+                   "subchunk": int(lib.tvlp_subchunk_len(2 * B if kind == "hpn" else B, T, M)) if kind == "tv" else None,
                    "l2": "inputs larger than L2"},
         "gbs_algorithmic_step": round(step_gbs, 1),
         "step_roofline_frac": round(step_gbs / hbm, 4),

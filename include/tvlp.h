@@ -72,8 +72,9 @@ int32_t tvlp_max_order(void);
 
 /* Number of elements (of the call dtype) of the carry tape for (B, T, M). */
 int64_t tvlp_carry_elems(int64_t B, int64_t T, int32_t M);
-/* Sub-chunk length used for (T, M) (diagnostics / tests). */
-int64_t tvlp_subchunk_len(int64_t T, int32_t M);
+/* Sub-chunk length used for (B, T, M) (diagnostics / tests; small batches use
+ * shorter sub-chunks to fill the GPU). */
+int64_t tvlp_subchunk_len(int64_t B, int64_t T, int32_t M);
 /* Device workspace bytes needed by `op`; F/frame_size/hop only for frame-wise ops. */
 size_t tvlp_workspace_bytes(int32_t op, int32_t dtype, int64_t B, int64_t T, int32_t M, int64_t F,
                             int32_t frame_size, int32_t hop);

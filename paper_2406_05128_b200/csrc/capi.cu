@@ -68,15 +68,21 @@ struct Plan {
 // Sub-chunk length: a multiple of 8 dividing T (so all sub-chunks are full and
 // uniformly strided for the 2-D tensor TMA), closest to the target (512, or
 // $TVLP_SUBCHUNK); if T has no such divisor, T is padded up to a multiple.
-int64_t choose_ls(int64_t T, int64_t* Tp) {
-    int64_t target = 512;
+// Sub-chunk length: a multiple of 8 dividing T, closest to the target.  The
+// target is ~512 (one basis wave at config 3 and 100-step carry chains),
+// smaller when the batch has too few sub-chunks to fill the GPU: the
+// per-sub-chunk passes are then latency-bound and scale with Ls while the
+// serial carries scale with T/Ls (measured on config 1, us per fwd+bwd: Ls 480
+// 191, 320 160, 240 205).
+int64_t choose_ls(int64_t B, int64_t T, int64_t* Tp) {
+    int64_t target = B * T >= (int64_t)4096 * 512 ? 512 : 320;
     if (const char* env = std::getenv("TVLP_SUBCHUNK")) {
         const long v = std::atol(env);
         if (v >= 8) target = v;
     }
     if (T >= 256) {
         int64_t best = -1;
-        for (int64_t d = 256; d <= 1024; d += 8)
+        for (int64_t d = 128; d <= 1024; d += 8)
             if (T % d == 0 && (best < 0 || std::llabs(d - target) < std::llabs(best - target)))
                 best = d;
         if (best > 0) {
@@ -98,7 +104,7 @@ bool make_plan(int64_t B, int64_t T, int M, Plan& p) {
     p.T = T;
     p.M = M;
     p.Mp = padded_order(M);
-    p.Ls = (int)choose_ls(T, &p.Tp);
+    p.Ls = (int)choose_ls(B, T, &p.Tp);
     p.nsub = (int)(p.Tp / p.Ls);
     return true;
 }
@@ -728,9 +734,9 @@ int64_t tvlp_carry_elems(int64_t B, int64_t T, int32_t M) {
     return carry_elems(p);
 }
 
-int64_t tvlp_subchunk_len(int64_t T, int32_t M) {
+int64_t tvlp_subchunk_len(int64_t B, int64_t T, int32_t M) {
     Plan p;
-    if (!make_plan(1, T, M, p)) return -1;
+    if (!make_plan(B, T, M, p)) return -1;
     return p.Ls;
 }
 

@@ -97,7 +97,11 @@ template <int N>
 __device__ __forceinline__ void bulk_wait() {
     asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
-// order generic-proxy shared accesses before subsequent async-proxy (TMA) ones
+// Order generic-proxy shared-memory WRITES before subsequent async-proxy (TMA
+// store) reads of them.  Not needed to recycle a buffer that was only READ by
+// generic loads (write-after-read): the loaded values have been consumed
+// before the refill is issued.  The fence also waits for this thread's
+// outstanding memory operations, so it is kept off the serial carry chains.
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -171,7 +171,6 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ Phi
                 for (int idx = lane; idx < rows * M; idx += 32) cA[idx] = (ACC)rawA[idx];
             for (int idx = lane; idx < rows; idx += 32) ce[idx] = (ACC)rawe[idx];
             __syncwarp();
-            fence_proxy_async();
             issue(k + NSTB);  // raw stage consumed
             Ar = cA;
             er = ce;
@@ -209,7 +208,6 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ Phi
         (void)tau0;
         if constexpr (!S::CONV) {
             __syncwarp();
-            fence_proxy_async();
             issue(k + NSTB);
         }
     }
@@ -667,7 +665,6 @@ k_carry_fwd(const CarryArgs<CT> a) {
                 x = xn;
             }
         }
-        fence_proxy_async();
         __syncwarp();
         issue(sg + kCS);
     }
@@ -750,7 +747,6 @@ k_carry_bwd(const CarryArgs<CT> a) {
                 mu = mn;
             }
         }
-        fence_proxy_async();
         __syncwarp();
         issue(sg + kCS);
     }
@@ -830,7 +826,6 @@ k_group_P(const CT* __restrict__ tape, CT* __restrict__ gtape, int64_t ngroups, 
 #pragma unroll
             for (int i = 0; i < M; ++i) col[i] = nc[i];
         }
-        fence_proxy_async();
         __syncwarp();
         issue(sg + kCS);
     }

@@ -76,7 +76,7 @@ def _host(x, dtype=None):
 def lp_tv_fwd_bwd_host(e, A, grad_s, zi=None, *, chunks=None, out=None, device=None):
     """s = LP(e, A) and its VJP (grad_e, grad_A) for grad_s, batch-pipelined.
 
-    ``chunks``: number of batch chunks (default: up to 32, at least one
+    ``chunks``: number of batch chunks (default: up to 8, at least one
     sequence each).  ``out``: optional (s, grad_e, grad_A) host tensors."""
     e = _host(e)
     A = _host(A, e.dtype)
@@ -92,7 +92,7 @@ def lp_tv_fwd_bwd_host(e, A, grad_s, zi=None, *, chunks=None, out=None, device=N
                torch.empty_like(A, pin_memory=pin))
     s_h, ge_h, gA_h = out
     zi_h = None if zi is None else _host(zi, e.dtype)
-    n = max(1, min(B, chunks or 32))
+    n = max(1, min(B, chunks or 8))
     bounds = [(B * i // n, B * (i + 1) // n) for i in range(n)]
     bufs = _buffers(dev, e.shape[0], e.shape[1], A.shape[2], e.dtype, max(h - l for l, h in bounds),
                     zi_h is not None)

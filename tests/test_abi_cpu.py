@@ -28,8 +28,10 @@ def test_abi_queries_without_gpu():
     lib = N.load()
     assert lib.tvlp_abi_version() == 1
     assert lib.tvlp_max_order() >= 22
-    Ls = lib.tvlp_subchunk_len(48000, 22)
+    Ls = lib.tvlp_subchunk_len(64, 48000, 22)
     assert Ls % 8 == 0 and 48000 % Ls == 0 and 256 <= Ls <= 1024
+    small = lib.tvlp_subchunk_len(4, 24000, 22)  # small batch: shorter sub-chunks
+    assert small % 8 == 0 and 24000 % small == 0 and 128 <= small < Ls
     nsub = -(-48000 // Ls)
     # per-sub-chunk tapes + one forward-refinement flag slot per sequence
     assert lib.tvlp_carry_elems(64, 48000, 22) == 64 * nsub * (2 * 22 + 1) * 24 + 64
