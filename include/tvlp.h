@@ -64,6 +64,8 @@ extern "C" {
 #define TVLP_OP_BWD_TI 3
 #define TVLP_OP_FW_FWD 4
 #define TVLP_OP_FW_BWD 5
+#define TVLP_OP_FWD_TV_FRAMES 6
+#define TVLP_OP_BWD_TV_FRAMES 7
 
 int tvlp_abi_version(void);
 const char* tvlp_status_string(int status);
@@ -95,6 +97,24 @@ int tvlp_lp_backward_tv(int32_t dtype, const void* grad_s, const void* A, const 
                         const void* zi, void* grad_e, void* grad_A, int64_t B, int64_t T,
                         int32_t M, const void* carry, int32_t carry_prec, void* workspace,
                         size_t workspace_bytes, void* stream);
+
+/* Frame-rate coefficients: the TV filter with
+ * A = upsample_linear(frames, hop, T - 1) (params.py:107-132; the synthesiser's
+ * call site synth.py:268-273) without materialising A: frames [B, F, M],
+ * F = (T - 1) / hop + 1, rows interpolated inside the scan kernels (fp32; fp64
+ * I/O or fp64 carries materialise A in the workspace).  Replaces the pair of
+ * tape ops upsample_linear -> lp_tv (params.py:337-345, lpc.py:202-213). */
+int tvlp_lp_forward_tv_frames(int32_t dtype, const void* e, const void* frames, const void* zi,
+                              void* s, int64_t B, int64_t T, int32_t M, int64_t F, int32_t hop,
+                              void* carry, int32_t carry_prec, void* workspace,
+                              size_t workspace_bytes, int32_t* nonfinite, void* stream);
+/* (grad_e, grad_frames) of lp_forward_tv_frames: the VJP chain lpc.py:152-173
+ * then params.py:135-145, with grad_A never written (grad_frames [B, F, M]). */
+int tvlp_lp_backward_tv_frames(int32_t dtype, const void* grad_s, const void* frames,
+                               const void* s, const void* zi, void* grad_e, void* grad_frames,
+                               int64_t B, int64_t T, int32_t M, int64_t F, int32_t hop,
+                               const void* carry, int32_t carry_prec, void* workspace,
+                               size_t workspace_bytes, void* stream);
 
 /* Time-invariant special case: a [B, M] constant row per sequence. */
 int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,

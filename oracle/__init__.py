@@ -276,6 +276,59 @@ def framewise_backward(grad_out, frames, seg_outputs, hop, frame_size=None, wind
 # oracle.py:228-234
 # ---------------------------------------------------------------------------
 
+# ---------------------------------------------------------------------------
+# upsample_linear (params.py:102-145): restated for the frame-rate LP path
+# ---------------------------------------------------------------------------
+
+def expected_frame_count(T, hop):
+    """params.py:102-104."""
+    return T // hop + 1
+
+
+def _upsample_weights(F, hop, T):
+    """params.py:107-117: frame f anchored at sample f*hop, held after the last."""
+    if F != expected_frame_count(T, hop):
+        raise ValueError(
+            f"got {F} frames but T={T} at hop={hop} requires {expected_frame_count(T, hop)}")
+    t = np.arange(T + 1)
+    f0 = t // hop
+    w = (t - f0 * hop) / float(hop)
+    f1 = np.minimum(f0 + 1, F - 1)
+    w[f0 == F - 1] = 0.0
+    return f0, f1, w
+
+
+def upsample_linear(frames, hop, T):
+    """params.py:120-132: (F, D) frames -> (T+1, D) samples."""
+    frames = np.asarray(frames)
+    f0, f1, w = _upsample_weights(frames.shape[0], hop, T)
+    if frames.ndim == 1:
+        return (1.0 - w) * frames[f0] + w * frames[f1]
+    wcol = w[:, None]
+    return (1.0 - wcol) * frames[f0] + wcol * frames[f1]
+
+
+def upsample_linear_vjp(grad_out, F, hop, T):
+    """params.py:135-145 (np.add.at: f0 contributions, then f1, in t order)."""
+    f0, f1, w = _upsample_weights(F, hop, T)
+    grad_frames = np.zeros((F,) + grad_out.shape[1:], dtype=grad_out.dtype)
+    wcol = w if grad_out.ndim == 1 else w[:, None]
+    np.add.at(grad_frames, f0, (1.0 - wcol) * grad_out)
+    np.add.at(grad_frames, f1, wcol * grad_out)
+    return grad_frames
+
+
+def lp_tv_frames_fwd_bwd(e, frames, hop, grad_s, zi=None):
+    """The composed reference path the fused frame-rate kernels replace:
+    s = lp_forward_tv(e, upsample_linear(frames)); (grad_e, grad_frames) by
+    the VJP chain (lp_backward_tv, then the upsample VJP)."""
+    T = e.shape[-1] - 1
+    A = upsample_linear(frames, hop, T)
+    s = lp_forward_tv(e, A, zi)
+    ge, gA = lp_backward_tv(grad_s, A, s, zi)
+    return s, ge, upsample_linear_vjp(gA, frames.shape[0], hop, T)
+
+
 def gradcheck_error(analytic, numeric):
     """Max elementwise deviation normalised by the largest entry (oracle.py:228-234)."""
     analytic = np.asarray(analytic, dtype=np.float64)

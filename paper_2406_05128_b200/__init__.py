@@ -16,10 +16,12 @@ __version__ = "0.1.0"
 _LAZY = {
     "lp_forward_tv": "lpc", "lp_forward_ti": "lpc", "lp_backward_tv": "lpc",
     "lp_backward_ti": "lpc", "shift_coeffs": "lpc", "lagged_signal_matrix": "lpc",
+    "lp_forward_tv_frames": "lpc", "lp_backward_tv_frames": "lpc",
     "set_validation": "lpc", "check_nonfinite": "lpc", "set_carry_precision": "lpc",
     "FramePlan": "params", "framewise_lp": "params", "expected_frame_count": "params",
     "LPTV": "autograd", "LPTI": "autograd", "LPFramewise": "autograd", "lp_tv": "autograd",
-    "lp_ti": "autograd", "framewise": "autograd",
+    "lp_ti": "autograd", "framewise": "autograd", "LPTVFrames": "autograd",
+    "lp_tv_frames": "autograd", "lp_tv_fwd_bwd_host": "stream",
     "gradcheck_error": "metrics",
 }
 

@@ -16,7 +16,8 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libtvlp_b200.so")
 
 F32, F64 = 0, 1
 CARRY_F64, CARRY_F32, CARRY_AUTO = 0, 1, 2
-OP_FWD_TV, OP_BWD_TV, OP_FWD_TI, OP_BWD_TI, OP_FW_FWD, OP_FW_BWD = range(6)
+(OP_FWD_TV, OP_BWD_TV, OP_FWD_TI, OP_BWD_TI, OP_FW_FWD, OP_FW_BWD, OP_FWD_TV_FRAMES,
+ OP_BWD_TV_FRAMES) = range(8)
 
 _lib = None
 
@@ -39,6 +40,10 @@ _SIGS = [
      [_I32, _P, _P, _P, _P, _I64, _I64, _I32, _P, _I32, _P, _SZ, _P, _P]),
     ("tvlp_lp_backward_tv", ctypes.c_int,
      [_I32, _P, _P, _P, _P, _P, _P, _I64, _I64, _I32, _P, _I32, _P, _SZ, _P]),
+    ("tvlp_lp_forward_tv_frames", ctypes.c_int,
+     [_I32, _P, _P, _P, _P, _I64, _I64, _I32, _I64, _I32, _P, _I32, _P, _SZ, _P, _P]),
+    ("tvlp_lp_backward_tv_frames", ctypes.c_int,
+     [_I32, _P, _P, _P, _P, _P, _P, _I64, _I64, _I32, _I64, _I32, _P, _I32, _P, _SZ, _P]),
     ("tvlp_lp_forward_ti", ctypes.c_int,
      [_I32, _P, _P, _P, _P, _I64, _I64, _I32, _P, _I32, _P, _SZ, _P, _P]),
     ("tvlp_lp_backward_ti", ctypes.c_int,

@@ -37,6 +37,29 @@ class LPTV(torch.autograd.Function):
         return ge, gA, None
 
 
+class LPTVFrames(torch.autograd.Function):
+    """s = LP_{upsample(frames)}(e): the tape ops upsample_linear -> lp_tv
+    (params.py:337-345, lpc.py:202-209) as one fused op."""
+
+    @staticmethod
+    def forward(ctx, e, frames, hop, zi=None):
+        frames = frames.to(e.dtype)
+        s, carry = lpc.lp_forward_tv_frames(e.detach(), frames.detach(), hop,
+                                            None if zi is None else zi.detach(),
+                                            return_carry=True)
+        ctx.save_for_backward(frames, s, zi)
+        ctx.carry = carry
+        ctx.hop = hop
+        return s
+
+    @staticmethod
+    def backward(ctx, grad_s):
+        frames, s, zi = ctx.saved_tensors
+        ge, gF = lpc.lp_backward_tv_frames(grad_s.contiguous(), frames, ctx.hop, s, zi,
+                                           carry=ctx.carry)
+        return ge, gF, None, None
+
+
 class LPTI(torch.autograd.Function):
     """Time-invariant filter with the single-filter adjoint (lpc.py:212-219)."""
 
@@ -78,6 +101,10 @@ class LPFramewise(torch.autograd.Function):
 def lp_tv(e, A, zi=None):
     """Differentiable sample-wise LP filter."""
     return LPTV.apply(e, A, zi)
+
+
+def lp_tv_frames(e, frames, hop, zi=None):
+    return LPTVFrames.apply(e, frames, hop, zi)
 
 
 def lp_ti(e, a, zi=None):

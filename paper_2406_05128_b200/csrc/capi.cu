@@ -362,11 +362,15 @@ __global__ void k_lag(const IO* __restrict__ s, const IO* __restrict__ zi, IO* _
 template <typename IO>
 int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s, const Plan& p,
                  void* carry_v, int prec, void* ws, size_t ws_bytes, int32_t* nonfinite,
-                 cudaStream_t st, size_t* need) {
+                 cudaStream_t st, size_t* need, const FrameSrc<IO>* fr = nullptr) {
     const size_t sz = sizeof(IO);
     IO* carry = static_cast<IO*>(carry_v);
-    const bool packed = p.Tp != p.T || p.Mp != p.M || !aligned16(e) || !aligned16(A) ||
-                        !aligned16(s) || (zi && !aligned16(zi));
+    // frame-rate coefficients: rows interpolated inside the fp32 scan kernels,
+    // else (fp64 I/O or fp64 chains) materialised once into the workspace
+    const bool frames = fr != nullptr;
+    const bool native_fr = frames && std::is_same<IO, float>::value && prec != kPrecF64Chains;
+    const bool packed = p.Tp != p.T || (!frames && (p.Mp != p.M || !aligned16(A))) ||
+                        !aligned16(e) || !aligned16(s) || (zi && !aligned16(zi));
     const int64_t nsc = p.B * p.nsub;
     const int64_t mp = mp4(p);
     Hier<IO> h;
@@ -398,10 +402,12 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     void *pe = nullptr, *pA = nullptr, *ps = nullptr, *pz = nullptr;
     if (packed) {
         pe = c.take(p.B * p.Tp * sz);
-        pA = c.take((ti ? p.B : p.B * p.Tp) * p.Mp * sz);
+        if (!frames) pA = c.take((ti ? p.B : p.B * p.Tp) * p.Mp * sz);
         ps = c.take(p.B * p.Tp * sz);
         if (zi) pz = c.take(p.B * p.Mp * sz);
     }
+    // (the sizing pass reserves the materialised rows whatever the precision)
+    if (frames && (!native_fr || need)) pA = c.take(p.B * p.Tp * p.Mp * sz);
     if (need) {
         *need = c.used;
         return TVLP_OK;
@@ -410,23 +416,31 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     const ScanArgs g = scan_args(p);
     if (packed) {
         TVLP_CK(pack<IO>(e, pe, p.B, p.T, 1, p.Tp, 1, st));
-        if (ti)
-            TVLP_CK(pack<IO>(A, pA, p.B, 1, p.M, 1, p.Mp, st));
-        else
-            TVLP_CK(pack<IO>(A, pA, p.B, p.T, p.M, p.Tp, p.Mp, st));
+        if (!frames) {
+            if (ti)
+                TVLP_CK(pack<IO>(A, pA, p.B, 1, p.M, 1, p.Mp, st));
+            else
+                TVLP_CK(pack<IO>(A, pA, p.B, p.T, p.M, p.Tp, p.Mp, st));
+            A_p = static_cast<const IO*>(pA);
+        }
         if (zi) TVLP_CK(pack<IO>(zi, pz, p.B, 1, p.M, 1, p.Mp, st));
         e_p = static_cast<const IO*>(pe);
-        A_p = static_cast<const IO*>(pA);
         zi_p = static_cast<const IO*>(pz);
         s_p = static_cast<IO*>(ps);
     }
+    if (frames && !native_fr) {
+        TVLP_RUN("upsample", 1, st, (launch_upsample<IO>(p.Mp, *fr, static_cast<IO*>(pA), p.B,
+                                                          p.Tp, st)));
+        A_p = static_cast<const IO*>(pA);
+    }
+    const FrameSrc<IO>* frk = native_fr ? fr : nullptr;
     const int bprec = (prec == kPrecAuto || prec == kPrecF32Chains) ? prec : kPrecF64Chains;
-    TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, bprec, e_p, A_p, phiz, g, st)));
+    TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, bprec, e_p, A_p, phiz, g, st, frk)));
     if (hier) TVLP_RUN("compose", h.lv.L - 1, st, (h.compose()));
     TVLP_RUN("carry_fwd", 1, st, (h.fwd(0, nullptr, zi_p, p.Mp, xin, dstat, fflags)));
     TVLP_RUN("apply_fwd", 1, st,
              (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, xend, dstat, nullptr, g,
-                                   st)));
+                                   st, frk)));
     if (refine) {
         if (!hier) {
             TVLP_RUN("refine_fwd", 1, st,
@@ -452,7 +466,7 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
         }
         TVLP_RUN("apply_fwd_refined", 1, st,
                  (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nullptr, nullptr, nullptr, flags,
-                                       g, st)));
+                                       g, st, frk)));
     }
     if (packed) TVLP_CK(unpack<IO>(ps, s, p.B, p.T, 1, p.Tp, 1, st));
     return TVLP_OK;
@@ -468,11 +482,19 @@ inline int grad_a_chunks(const Plan& p) {
 template <typename IO>
 int backward_impl(bool ti, const void* gs, const void* A, const void* s, const void* zi, void* ge,
                   void* gA, const Plan& p, const void* carry_v, int prec, void* ws,
-                  size_t ws_bytes, cudaStream_t st, size_t* need) {
+                  size_t ws_bytes, cudaStream_t st, size_t* need,
+                  const FrameSrc<IO>* fr = nullptr) {
+    // frames mode: A is the frame-rate source fr, gA receives grad_frames [B][F][M]
     const size_t sz = sizeof(IO);
     const IO* carry = static_cast<const IO*>(carry_v);
-    const bool packed = p.Tp != p.T || p.Mp != p.M || !aligned16(gs) || !aligned16(A) ||
-                        !aligned16(s) || !aligned16(ge) || (!ti && !aligned16(gA)) ||
+    const bool frames = fr != nullptr;
+    // (without the forward's tape the basis is recomputed; the frame-rate
+    // basis has fp32 chains only)
+    const bool native_fr = frames && std::is_same<IO, float>::value &&
+                           (carry != nullptr || prec == kPrecF32Chains);
+    const bool packed = p.Tp != p.T ||
+                        (!frames && (p.Mp != p.M || !aligned16(A) || (!ti && !aligned16(gA)))) ||
+                        !aligned16(gs) || !aligned16(s) || !aligned16(ge) ||
                         (zi && !aligned16(zi));
     const int64_t nsc = p.B * p.nsub;
     const int64_t mp = mp4(p);
@@ -511,12 +533,14 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
          *pgA = nullptr;
     if (packed) {
         pgs = c.take(p.B * p.Tp * sz);
-        pA = c.take((ti ? p.B : p.B * p.Tp) * p.Mp * sz);
+        if (!frames) pA = c.take((ti ? p.B : p.B * p.Tp) * p.Mp * sz);
         ps = c.take(p.B * p.Tp * sz);
         if (zi) pz = c.take(p.B * p.Mp * sz);
         pge = c.take(p.B * p.Tp * sz);
-        if (!ti) pgA = c.take(p.B * p.Tp * p.Mp * sz);
+        if (!ti && !frames) pgA = c.take(p.B * p.Tp * p.Mp * sz);
     }
+    // (the sizing pass reserves the materialised rows whatever the precision)
+    if (frames && (!native_fr || need)) pA = c.take(p.B * p.Tp * p.Mp * sz);
     if (need) {
         *need = c.used;
         return TVLP_OK;
@@ -525,33 +549,43 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     const ScanArgs g = scan_args(p);
     if (packed) {
         TVLP_CK(pack<IO>(gs, pgs, p.B, p.T, 1, p.Tp, 1, st));
-        if (ti)
-            TVLP_CK(pack<IO>(A, pA, p.B, 1, p.M, 1, p.Mp, st));
-        else
-            TVLP_CK(pack<IO>(A, pA, p.B, p.T, p.M, p.Tp, p.Mp, st));
+        if (!frames) {
+            if (ti)
+                TVLP_CK(pack<IO>(A, pA, p.B, 1, p.M, 1, p.Mp, st));
+            else
+                TVLP_CK(pack<IO>(A, pA, p.B, p.T, p.M, p.Tp, p.Mp, st));
+            A_p = static_cast<const IO*>(pA);
+            gA_p = static_cast<IO*>(pgA);
+        }
         TVLP_CK(pack<IO>(s, ps, p.B, p.T, 1, p.Tp, 1, st));
         if (zi) TVLP_CK(pack<IO>(zi, pz, p.B, 1, p.M, 1, p.Mp, st));
         gs_p = static_cast<const IO*>(pgs);
-        A_p = static_cast<const IO*>(pA);
         s_p = static_cast<const IO*>(ps);
         zi_p = static_cast<const IO*>(pz);
         ge_p = static_cast<IO*>(pge);
-        gA_p = static_cast<IO*>(pgA);
     }
+    if (frames && !native_fr) {
+        TVLP_RUN("upsample", 1, st, (launch_upsample<IO>(p.Mp, *fr, static_cast<IO*>(pA), p.B,
+                                                          p.Tp, st)));
+        A_p = static_cast<const IO*>(pA);
+    }
+    const FrameSrc<IO>* frk = native_fr ? fr : nullptr;
     h.tape = carry ? const_cast<IO*>(carry) : phiz_own;
     if (!carry) {
         // transition matrices only (the zero-state row is unused here; s is a
         // valid stand-in for e of the same shape)
-        TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, prec, s_p, A_p, phiz_own, g, st)));
+        TVLP_RUN("basis", 1, st,
+                 (launch_basis<IO>(p.Mp, ti, prec, s_p, A_p, phiz_own, g, st, frk)));
         if (hier) TVLP_RUN("compose", h.lv.L - 1, st, (h.compose()));
     }
     TVLP_RUN("adjoint_zs", 1, st,
              (launch_adjoint<IO>(p.Mp, ti, 0, gs_p, A_p, nullptr, nu, nullptr, nullptr, nullptr, g,
-                                 st)));
+                                 st, frk)));
     if (dstat) TVLP_CK(cudaMemsetAsync(dstat, 0, p.B * 2 * sizeof(unsigned), st));
     TVLP_RUN("carry_bwd", 1, st, (h.bwd(0, nu, mu)));
     TVLP_RUN("adjoint_apply", 1, st,
-             (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, kout, ge_p, dstat, nullptr, g, st)));
+             (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, kout, ge_p, dstat, nullptr, g, st,
+                                 frk)));
     if (refine) {
         const int* inherit = carry ? reinterpret_cast<const int*>(carry + tape_body(p)) : nullptr;
         if (!hier) {
@@ -577,9 +611,13 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
         }
         TVLP_RUN("adjoint_apply_refined", 1, st,
                  (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, nullptr, flags, g,
-                                     st)));
+                                     st, frk)));
     }
-    if (ti) {
+    if (frames) {
+        TVLP_RUN("grad_frames", 1, st,
+                 (launch_grad_frames<IO>(*fr, ge_p, s_p, zi_p, zi_p == zi ? p.M : p.Mp,
+                                         static_cast<IO*>(gA), p.B, p.Tp, st)));
+    } else if (ti) {
         IO* ga_out = ga_p ? ga_p : static_cast<IO*>(gA);
         TVLP_RUN("grad_a", 2, st,
                  (launch_grad_a<IO>(p.Mp, ge_p, s_p, zi_p, part, ga_out, p.B, p.Tp, nchunk, st)));
@@ -589,7 +627,7 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     }
     if (packed) {
         TVLP_CK(unpack<IO>(pge, ge, p.B, p.T, 1, p.Tp, 1, st));
-        if (!ti) TVLP_CK(unpack<IO>(pgA, gA, p.B, p.T, p.M, p.Tp, p.Mp, st));
+        if (!ti && !frames) TVLP_CK(unpack<IO>(pgA, gA, p.B, p.T, p.M, p.Tp, p.Mp, st));
     }
     return TVLP_OK;
 }
@@ -665,6 +703,21 @@ int fw_backward_impl(const void* gout, const void* frames, const void* win, cons
 }  // namespace tvlp
 
 using namespace tvlp;
+
+bool frame_src_ok(int64_t T, int64_t F, int32_t hop) {
+    return hop >= 1 && T >= 1 && F == (T - 1) / hop + 1;  // params.py:102-117 (T = T1 - 1)
+}
+
+template <typename IO>
+FrameSrc<IO> frame_src(const void* frames, int64_t T, int32_t M, int64_t F, int32_t hop) {
+    FrameSrc<IO> fs;
+    fs.frames = static_cast<const IO*>(frames);
+    fs.nF = F;
+    fs.Tv = T;
+    fs.hop = hop;
+    fs.Mf = M;
+    return fs;
+}
 
 extern "C" {
 
@@ -780,6 +833,32 @@ size_t tvlp_workspace_bytes(int32_t op, int32_t dtype, int64_t B, int64_t T, int
         }
         return need;
     }
+    if (op == TVLP_OP_FWD_TV_FRAMES || op == TVLP_OP_BWD_TV_FRAMES) {
+        Plan p;
+        if (!make_plan(B, T, M, p) || !frame_src_ok(T, F, hop)) return 0;
+        if (op == TVLP_OP_FWD_TV_FRAMES) {
+            if (f64) {
+                const FrameSrc<double> fs = frame_src<double>(any, T, M, F, hop);
+                forward_impl<double>(false, any, any, any, (void*)any, p, nullptr, kPrecAuto,
+                                     nullptr, 0, nullptr, 0, &need, &fs);
+            } else {
+                const FrameSrc<float> fs = frame_src<float>(any, T, M, F, hop);
+                forward_impl<float>(false, any, any, any, (void*)any, p, nullptr, kPrecAuto,
+                                    nullptr, 0, nullptr, 0, &need, &fs);
+            }
+        } else {
+            if (f64) {
+                const FrameSrc<double> fs = frame_src<double>(any, T, M, F, hop);
+                backward_impl<double>(false, any, any, any, any, (void*)any, (void*)any, p,
+                                      nullptr, kPrecAuto, nullptr, 0, 0, &need, &fs);
+            } else {
+                const FrameSrc<float> fs = frame_src<float>(any, T, M, F, hop);
+                backward_impl<float>(false, any, any, any, any, (void*)any, (void*)any, p,
+                                     nullptr, kPrecAuto, nullptr, 0, 0, &need, &fs);
+            }
+        }
+        return need;
+    }
     FwArgs a;
     if (!fw_args(B, T, F, M, frame_size, hop, 1.0, a)) return 0;
     if (op == TVLP_OP_FW_FWD) {
@@ -845,6 +924,49 @@ int tvlp_lp_backward_tv(int32_t dtype, const void* grad_s, const void* A, const 
                         size_t workspace_bytes, void* stream) {
     return bwd_entry(false, dtype, grad_s, A, s, zi, grad_e, grad_A, B, T, M, carry, carry_prec,
                      workspace, workspace_bytes, stream);
+}
+
+int tvlp_lp_forward_tv_frames(int32_t dtype, const void* e, const void* frames, const void* zi,
+                              void* s, int64_t B, int64_t T, int32_t M, int64_t F, int32_t hop,
+                              void* carry, int32_t carry_prec, void* workspace,
+                              size_t workspace_bytes, int32_t* nonfinite, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!e || !frames || !s || !frame_src_ok(T, F, hop)) return TVLP_ERR_ARG;
+    Plan p;
+    if (!make_plan(B, T, M, p)) return TVLP_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64) {
+        const FrameSrc<double> fs = frame_src<double>(frames, T, M, F, hop);
+        return forward_impl<double>(false, e, frames, zi, s, p, carry, TVLP_CARRY_F64, workspace,
+                                    workspace_bytes, nonfinite, st, nullptr, &fs);
+    }
+    const FrameSrc<float> fs = frame_src<float>(frames, T, M, F, hop);
+    return forward_impl<float>(false, e, frames, zi, s, p, carry, carry_prec, workspace,
+                               workspace_bytes, nonfinite, st, nullptr, &fs);
+}
+
+int tvlp_lp_backward_tv_frames(int32_t dtype, const void* grad_s, const void* frames,
+                               const void* s, const void* zi, void* grad_e, void* grad_frames,
+                               int64_t B, int64_t T, int32_t M, int64_t F, int32_t hop,
+                               const void* carry, int32_t carry_prec, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!grad_s || !frames || !s || !grad_e || !grad_frames || !frame_src_ok(T, F, hop))
+        return TVLP_ERR_ARG;
+    Plan p;
+    if (!make_plan(B, T, M, p)) return TVLP_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64) {
+        const FrameSrc<double> fs = frame_src<double>(frames, T, M, F, hop);
+        return backward_impl<double>(false, grad_s, frames, s, zi, grad_e, grad_frames, p, carry,
+                                     TVLP_CARRY_F64, workspace, workspace_bytes, st, nullptr,
+                                     &fs);
+    }
+    const FrameSrc<float> fs = frame_src<float>(frames, T, M, F, hop);
+    return backward_impl<float>(false, grad_s, frames, s, zi, grad_e, grad_frames, p, carry,
+                                carry_prec, workspace, workspace_bytes, st, nullptr, &fs);
 }
 
 int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,

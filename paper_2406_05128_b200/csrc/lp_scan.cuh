@@ -26,6 +26,7 @@
 // T % Ls == 0 (all sub-chunks full), all pointers 16-byte aligned.
 #pragma once
 #include "common.cuh"
+#include "scan_launch.cuh"
 
 #ifndef TVLP_BASIS4_SPLIT
 #define TVLP_BASIS4_SPLIT 0
@@ -236,6 +237,66 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ Phi
 // loads (7 LDS per step for M = 22) are shared by its three chains, and the
 // three chains are independent FMA streams (ILP) within the step.
 // ============================================================================
+// ---------------------------------------------------------------- frame-rate rows
+// One formula for every kernel (the basis, apply and adjoint passes must see
+// bit-identical rows): w = r * (1/hop), a = w fb + (1 - w) fa.
+template <typename IO>
+__device__ __forceinline__ IO frame_mix(IO fa, IO fb, IO w, IO omw) {
+    return fma(w, fb, omw * fa);
+}
+// Row t of sequence b into dst[0..M) (generic stores); no caching.
+template <typename IO, int M>
+__device__ __forceinline__ void frame_row_store(const FrameSrc<IO>& fs, int64_t b, int64_t t,
+                                                IO inv_hop, IO* dst) {
+    if (t >= fs.Tv) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) dst[i] = (IO)0;
+        return;
+    }
+    const int tt = (int)t;
+    int f0 = tt / fs.hop;
+    IO w = (IO)(tt - f0 * fs.hop) * inv_hop;
+    if (f0 >= fs.nF - 1) {
+        f0 = (int)fs.nF - 1;
+        w = (IO)0;
+    }
+    const int f1 = min(f0 + 1, (int)fs.nF - 1);
+    const IO omw = (IO)1 - w;
+    const IO* pa = fs.frames + ((int64_t)b * fs.nF + f0) * fs.Mf;
+    const IO* pb = fs.frames + ((int64_t)b * fs.nF + f1) * fs.Mf;
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+        dst[i] = i < fs.Mf ? frame_mix<IO>(__ldg(pa + i), __ldg(pb + i), w, omw) : (IO)0;
+}
+// Row t into registers, caching the two frame rows of the current interval.
+template <typename IO, int M>
+__device__ __forceinline__ void frame_row_cached(const FrameSrc<IO>& fs, int64_t b, int64_t t,
+                                                 IO inv_hop, int& cf0, IO (&fa)[M], IO (&fb)[M],
+                                                 IO (&a)[M]) {
+    const int tt = (int)t;
+    int f0 = tt / fs.hop;
+    IO w = (IO)(tt - f0 * fs.hop) * inv_hop;
+    if (f0 >= fs.nF - 1) {
+        f0 = (int)fs.nF - 1;
+        w = (IO)0;
+    }
+    if (f0 != cf0) {
+        cf0 = f0;
+        const int f1 = min(f0 + 1, (int)fs.nF - 1);
+        const IO* pa = fs.frames + ((int64_t)b * fs.nF + f0) * fs.Mf;
+        const IO* pb = fs.frames + ((int64_t)b * fs.nF + f1) * fs.Mf;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            fa[i] = i < fs.Mf ? __ldg(pa + i) : (IO)0;
+            fb[i] = i < fs.Mf ? __ldg(pb + i) : (IO)0;
+        }
+    }
+    const IO omw = (IO)1 - w;
+    const bool valid = t < fs.Tv;
+#pragma unroll
+    for (int i = 0; i < M; ++i) a[i] = valid ? frame_mix<IO>(fa[i], fb[i], w, omw) : (IO)0;
+}
+
 // steps per basic block in full windows: steps of a group interleave; the
 // group boundary bounds how far the scheduler runs ahead (register pressure)
 constexpr int kBasisGroup = TVLP_BASIS_GROUP;
@@ -361,10 +422,10 @@ __device__ __forceinline__ void basis4_partial(std::integer_sequence<int, U...>,
     ((U >= u0 ? basis4_step<M, TI, U>(R0, R1, R2, Ar, es, ati, ac, zs) : void()), ...);
 }
 
-template <int M, bool TI>
+template <int M, bool TI, bool FR = false>
 __global__ void __launch_bounds__(Basis4Cfg<M, TI>::NW * 32, TVLP_BASIS4_MINB)
 k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
-         ScanArgs g) {
+         ScanArgs g, const FrameSrc<float> fs) {
     grid_dep_wait();
     using C = Basis4Cfg<M, TI>;
     constexpr int P = C::P, S = C::S, NSTB = C::NSTB;
@@ -409,8 +470,8 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
         const int rows = M - first;
         const int elo = e_lo(k), ehi = (k * M - u0 + M + 3) & ~3;
         const uint32_t ebytes = (uint32_t)(ehi - elo) * 4;
-        mbar_arrive_expect_tx(&bars[st], (TI ? 0 : rows * M * 4) + ebytes);
-        if (!TI)
+        mbar_arrive_expect_tx(&bars[st], ((TI || FR) ? 0 : rows * M * 4) + ebytes);
+        if (!TI && !FR)
             tma_load_1d(stage(st) + first * M * 4, A + (row0 + tstart) * M, rows * M * 4,
                         &bars[st]);
         tma_load_1d(stage(st) + C::E_OFF, eb + elo, ebytes, &bars[st]);
@@ -440,8 +501,21 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
         R2[p] = c == c0 + 2 ? 1.f : 0.f;
     }
 
+    const float inv_hop = FR ? 1.f / (float)fs.hop : 0.f;
     for (int k = 0; k < nwin; ++k) {
         const int st = k % NSTB;
+        if constexpr (FR) {
+            // the window's coefficient rows, interpolated from the frame rows by
+            // the sub-chunk's lanes into the stage (ring position U = row U)
+            if (lane_used) {
+                float* rows_out = reinterpret_cast<float*>(stage(st));
+                const int first = k == 0 ? u0 : 0;
+                for (int U = first + q; U < M; U += P)
+                    frame_row_store<float, M>(fs, b, (int64_t)j * g.Ls + k * M - u0 + U, inv_hop,
+                                              rows_out + U * M);
+            }
+            __syncwarp();
+        }
         if (valid) mbar_wait(&bars[st], (uint32_t)((k / NSTB) & 1));
         const float* Ar = reinterpret_cast<const float*>(stage(st));
         const float* es =
@@ -874,13 +948,14 @@ struct LaneMaps {
 // in a register ring of MR = round_up(M, W) slots (slot p holds s at local
 // step tau with tau mod MR == p); the unrolled body covers MR/W windows so
 // every ring index is a compile-time constant.
-template <typename IO, int M, bool TI>
+template <typename IO, int M, bool TI, bool FR = false>
 __global__ void __launch_bounds__(32)
 k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
             const IO* __restrict__ Xin, int* __restrict__ flag, IO* __restrict__ Xend,
-            unsigned* __restrict__ dstat, const int* __restrict__ only, ScanArgs g) {
+            unsigned* __restrict__ dstat, const int* __restrict__ only, ScanArgs g,
+            const FrameSrc<IO> fs) {
     grid_dep_wait();
-    using S = LaneSmem<IO, M, TI>;
+    using S = LaneSmem<IO, M, TI || FR>;
     constexpr int W = S::W;
     constexpr int MR = (M + W - 1) / W * W;
     constexpr int WPB = MR / W;
@@ -897,7 +972,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
     if (only != nullptr && !__any_sync(0xffffffffu, active && only[gid / g.nsub] != 0)) return;
 
     if (lane == 0) {
-        prefetch_tmap(&maps.A);
+        if (!TI && !FR) prefetch_tmap(&maps.A);
         prefetch_tmap(&maps.X);
         prefetch_tmap(&maps.O);
         for (int st = 0; st < kLaneStages; ++st) mbar_init(&bars[st], 1);
@@ -909,7 +984,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
             const int st = k % kLaneStages;
             unsigned char* base = smem + st * S::STAGE;
             mbar_arrive_expect_tx(&bars[st], S::TX);
-            if (!TI) tma_load_2d(base, &maps.A, k * W * M, g0, &bars[st]);
+            if (!TI && !FR) tma_load_2d(base, &maps.A, k * W * M, g0, &bars[st]);
             tma_load_2d(base + S::A_BYTES, &maps.X, k * W, g0, &bars[st]);
         }
     };
@@ -928,6 +1003,12 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 #pragma unroll
     for (int i = 0; i < M; ++i) R[MR - 1 - i] = active ? Xin[gid * Tape<M>::MP4 + i] : (IO)0;
     bool finite = true;
+    // frame-rate rows (FR): interval cache and the lane's sub-chunk start
+    const int64_t fb_b = active ? gid / g.nsub : 0;
+    const int64_t ft0 = active ? (gid % g.nsub) * (int64_t)g.Ls : 0;
+    const IO inv_hop = FR ? (IO)1 / (IO)fs.hop : (IO)0;
+    int cf0 = -1;
+    IO fra[FR ? M : 1], frb[FR ? M : 1];
 
     for (int kb = 0; kb < nwin; kb += WPB) {
 #pragma unroll
@@ -956,6 +1037,9 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
                     if constexpr (TI) {
 #pragma unroll
                         for (int i = 0; i < M; ++i) a[i] = ati[i];
+                    } else if constexpr (FR) {
+                        frame_row_cached<IO, M>(fs, fb_b, ft0 + (int64_t)k * W + u, inv_hop, cf0,
+                                                fra, frb, a);
                     } else {
                         load_row_at<IO, M>(Ar + u * M, a, (lane * S::AROW + u * M) * S::SZ);
                     }
@@ -1025,13 +1109,13 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 // write g_e.  Reverse time; row A[t] is used at step t:
 //   lambda += u0 g_s(t);  g_e(t) = lambda_0;  lambda = C(t)^T lambda.
 // The transposed-state update shifts lambda inside its FMAs (no moves).
-template <typename IO, int M, bool TI, int MODE>
+template <typename IO, int M, bool TI, int MODE, bool FR = false>
 __global__ void __launch_bounds__(32)
 k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
           const IO* __restrict__ Mu, IO* __restrict__ Nu, unsigned* __restrict__ dstat,
-          const int* __restrict__ only, ScanArgs g) {
+          const int* __restrict__ only, ScanArgs g, const FrameSrc<IO> fs) {
     grid_dep_wait();
-    using S = LaneSmem<IO, M, TI>;
+    using S = LaneSmem<IO, M, TI || FR>;
     constexpr int W = S::W;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x;
@@ -1044,7 +1128,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     if (only != nullptr && !__any_sync(0xffffffffu, active && only[gid / g.nsub] != 0)) return;
 
     if (lane == 0) {
-        prefetch_tmap(&maps.A);
+        if (!TI && !FR) prefetch_tmap(&maps.A);
         prefetch_tmap(&maps.X);
         if (MODE == 1) prefetch_tmap(&maps.O);
         for (int st = 0; st < kLaneStages; ++st) mbar_init(&bars[st], 1);
@@ -1058,7 +1142,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
             unsigned char* base = smem + st * S::STAGE;
             const int wr = nwin - 1 - k;
             mbar_arrive_expect_tx(&bars[st], S::TX);
-            if (!TI) tma_load_2d(base, &maps.A, wr * W * M, g0, &bars[st]);
+            if (!TI && !FR) tma_load_2d(base, &maps.A, wr * W * M, g0, &bars[st]);
             tma_load_2d(base + S::A_BYTES, &maps.X, wr * W, g0, &bars[st]);
         }
     };
@@ -1074,6 +1158,11 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     IO lam[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) lam[i] = (MODE == 1 && active) ? Mu[gid * Tape<M>::MP4 + i] : (IO)0;
+    const int64_t fb_b = active ? gid / g.nsub : 0;
+    const int64_t ft0 = active ? (gid % g.nsub) * (int64_t)g.Ls : 0;
+    const IO inv_hop = FR ? (IO)1 / (IO)fs.hop : (IO)0;
+    int cf0 = -1;
+    IO fra[FR ? M : 1], frb[FR ? M : 1];
 
     for (int k = 0; k < nwin; ++k) {
         const int st = k % kLaneStages;
@@ -1097,6 +1186,9 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
             if constexpr (TI) {
 #pragma unroll
                 for (int i = 0; i < M; ++i) a[i] = ati[i];
+            } else if constexpr (FR) {
+                frame_row_cached<IO, M>(fs, fb_b, ft0 + (int64_t)(nwin - 1 - k) * W + u, inv_hop,
+                                        cf0, fra, frb, a);
             } else {
                 load_row_at<IO, M>(Ar + u * M, a, (lane * S::AROW + u * M) * S::SZ);
             }
@@ -1378,6 +1470,64 @@ __global__ void k_grad_a_final(const IO* __restrict__ part, IO* __restrict__ ga,
     double tot = 0.0;
     for (int k = 0; k < nchunk; ++k) tot += (double)part[(b * nchunk + k) * M + c];
     ga[idx] = (IO)(-tot);
+}
+
+// ---------------------------------------------------------------- frame-rate helpers
+// A[b, t, :] for t < T (rows past Tv zero), padded to Mp columns.
+template <typename IO, int M>
+__global__ void __launch_bounds__(256)
+k_upsample(const FrameSrc<IO> fs, IO* __restrict__ A, int64_t B, int64_t T) {
+    grid_dep_wait();
+    const IO inv_hop = (IO)1 / (IO)fs.hop;
+    const int64_t n = B * T;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        frame_row_store<IO, M>(fs, r / T, r % T, inv_hop, A + r * M);
+}
+
+// grad_frames[b, f, c] = sum_{t: f0(t)=f} (1-w) gA(t,c) + sum_{t: f1(t)=f} w gA(t,c),
+// gA(t, c) = -grad_e(t) s(t-1-c), s(<0) = zi (params.py:135-145 over lpc.py:172).
+// One CTA per (frame, sequence); thread (c, part) sums a strided quarter of
+// the frame's support (<= 2 hop samples), then a fixed-order combine.
+template <typename IO>
+__global__ void __launch_bounds__(128)
+k_grad_frames(const FrameSrc<IO> fs, const IO* __restrict__ ge, const IO* __restrict__ s,
+              const IO* __restrict__ zi, int Mzi, IO* __restrict__ gF, int64_t T) {
+    grid_dep_wait();
+    __shared__ IO part[4][32];
+    const int64_t f = blockIdx.x, b = blockIdx.y;
+    const int c = threadIdx.x & 31, pq = threadIdx.x >> 5;
+    const IO inv_hop = (IO)1 / (IO)fs.hop;
+    const IO* gb = ge + b * T;
+    const IO* sb = s + b * T;
+    const int64_t Tv = fs.Tv;
+    auto lag = [&](int64_t t) -> IO {  // s(t - 1 - c)
+        const int64_t u = t - 1 - c;
+        if (u >= 0) return sb[u];
+        return zi != nullptr ? zi[b * Mzi + (-u - 1)] : (IO)0;
+    };
+    IO acc = (IO)0;
+    if (c < fs.Mf) {
+        // f0(t) = f: t in [f hop, (f+1) hop), weight 1 - w (w = 0 on the last anchor)
+        const int64_t lo0 = f * fs.hop;
+        const int64_t hi0 = (f == fs.nF - 1) ? Tv : min(Tv, (f + 1) * (int64_t)fs.hop);
+        for (int64_t t = lo0 + pq; t < hi0; t += 4) {
+            const IO w = (f == fs.nF - 1) ? (IO)0 : (IO)(t - lo0) * inv_hop;
+            acc = fma(((IO)1 - w) * (-gb[t]), lag(t), acc);
+        }
+        // f1(t) = f, i.e. f0(t) = f - 1 < nF - 1: weight w
+        if (f >= 1) {
+            const int64_t lo1 = (f - 1) * fs.hop, hi1 = min(Tv, f * (int64_t)fs.hop);
+            for (int64_t t = lo1 + pq; t < hi1; t += 4) {
+                const IO w = (IO)(t - lo1) * inv_hop;
+                acc = fma(w * (-gb[t]), lag(t), acc);
+            }
+        }
+    }
+    part[pq][c] = acc;
+    __syncthreads();
+    if (pq == 0 && c < fs.Mf)
+        gF[(b * fs.nF + f) * fs.Mf + c] = (part[0][c] + part[1][c]) + (part[2][c] + part[3][c]);
 }
 
 }  // namespace tvlp

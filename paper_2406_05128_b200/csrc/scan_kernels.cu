@@ -77,48 +77,54 @@ cudaError_t lane_maps(LaneMaps& mp, const IO* A, const IO* X, const IO* O, const
     return err;
 }
 
-template <int M, bool TI>
+template <int M, bool TI, bool FR = false>
 cudaError_t basis4_impl(const float* e, const float* A, float* PhiZ, const ScanArgs& g,
-                        cudaStream_t st) {
+                        cudaStream_t st, const FrameSrc<float>* fr = nullptr) {
     using C = Basis4Cfg<M, TI>;
-    auto k = k_basis4<M, TI>;
+    auto k = k_basis4<M, TI, FR>;
     cudaError_t err = ensure_smem(k, C::BYTES);
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
     const int64_t per = (int64_t)C::S * C::NW;
-    launch_pdl(k, (unsigned)((nsc + per - 1) / per), C::NW * 32, C::BYTES, st, e, A, PhiZ, g);
+    const FrameSrc<float> fs = fr ? *fr : FrameSrc<float>{};
+    launch_pdl(k, (unsigned)((nsc + per - 1) / per), C::NW * 32, C::BYTES, st, e, A, PhiZ, g, fs);
     return cudaGetLastError();
 }
 
-template <typename IO, int M, bool TI>
+template <typename IO, int M, bool TI, bool FR = false>
 cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag, IO* Xend,
-                       unsigned* dstat, const int* only, const ScanArgs& g, cudaStream_t st) {
-    using S = LaneSmem<IO, M, TI>;
-    auto k = k_apply_fwd<IO, M, TI>;
+                       unsigned* dstat, const int* only, const ScanArgs& g, cudaStream_t st,
+                       const FrameSrc<IO>* fr = nullptr) {
+    using S = LaneSmem<IO, M, TI || FR>;
+    auto k = k_apply_fwd<IO, M, TI, FR>;
     cudaError_t err = ensure_smem(k, S::BYTES);
     if (err != cudaSuccess) return err;
     LaneMaps mp;
-    err = lane_maps<IO, M, TI>(mp, TI ? nullptr : A, e, s, g);
+    err = lane_maps<IO, M, TI || FR>(mp, (TI || FR) ? nullptr : A, e, s, g);
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
-    launch_pdl(k, (unsigned)((nsc + 31) / 32), 32, S::BYTES, st, mp, TI ? A : nullptr, Xin, flag, Xend,
-                                                        dstat, only, g);
+    const FrameSrc<IO> fs = fr ? *fr : FrameSrc<IO>{};
+    launch_pdl(k, (unsigned)((nsc + 31) / 32), 32, S::BYTES, st, mp, TI ? A : nullptr, Xin, flag,
+               Xend, dstat, only, g, fs);
     return cudaGetLastError();
 }
 
-template <typename IO, int M, bool TI, int MODE>
+template <typename IO, int M, bool TI, int MODE, bool FR = false>
 cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge,
-                         unsigned* dstat, const int* only, const ScanArgs& g, cudaStream_t st) {
-    using S = LaneSmem<IO, M, TI>;
-    auto k = k_adjoint<IO, M, TI, MODE>;
+                         unsigned* dstat, const int* only, const ScanArgs& g, cudaStream_t st,
+                         const FrameSrc<IO>* fr = nullptr) {
+    using S = LaneSmem<IO, M, TI || FR>;
+    auto k = k_adjoint<IO, M, TI, MODE, FR>;
     cudaError_t err = ensure_smem(k, S::BYTES);
     if (err != cudaSuccess) return err;
     LaneMaps mp;
-    err = lane_maps<IO, M, TI>(mp, TI ? nullptr : A, gs, MODE == 1 ? ge : nullptr, g);
+    err = lane_maps<IO, M, TI || FR>(mp, (TI || FR) ? nullptr : A, gs, MODE == 1 ? ge : nullptr,
+                                     g);
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
-    launch_pdl(k, (unsigned)((nsc + 31) / 32), 32, S::BYTES, st, mp, TI ? A : nullptr, Mu, Nu, dstat,
-                                                        only, g);
+    const FrameSrc<IO> fs = fr ? *fr : FrameSrc<IO>{};
+    launch_pdl(k, (unsigned)((nsc + 31) / 32), 32, S::BYTES, st, mp, TI ? A : nullptr, Mu, Nu,
+               dstat, only, g, fs);
     return cudaGetLastError();
 }
 
@@ -140,9 +146,11 @@ cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge
 
 template <typename IO>
 cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO* PhiZ,
-                         const ScanArgs& g, cudaStream_t st) {
+                         const ScanArgs& g, cudaStream_t st, const FrameSrc<IO>* fr) {
     TVLP_DISPATCH_M(Mp, {
         if constexpr (std::is_same<IO, float>::value) {
+            if (fr != nullptr)  // frame-rate rows: fp32 chains, TV only (the caller checks)
+                return basis4_impl<M_, false, true>(e, A, PhiZ, g, st, fr);
             if (prec == kPrecF32Chains || prec == kPrecAuto)
                 return ti ? basis4_impl<M_, true>(e, A, PhiZ, g, st)
                           : basis4_impl<M_, false>(e, A, PhiZ, g, st);
@@ -238,8 +246,13 @@ cudaError_t launch_refine_helpers(int what, int Mp, const IO* P, const IO* Q, IO
 template <typename IO>
 cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO* Xin, IO* s,
                              int* flag, IO* Xend, unsigned* dstat, const int* only,
-                             const ScanArgs& g, cudaStream_t st) {
+                             const ScanArgs& g, cudaStream_t st, const FrameSrc<IO>* fr) {
     TVLP_DISPATCH_M(Mp, {
+        if constexpr (std::is_same<IO, float>::value) {
+            if (fr != nullptr)
+                return apply_impl<IO, M_, false, true>(e, A, Xin, s, flag, Xend, dstat, only, g,
+                                                       st, fr);
+        }
         return ti ? apply_impl<IO, M_, true>(e, A, Xin, s, flag, Xend, dstat, only, g, st)
                   : apply_impl<IO, M_, false>(e, A, Xin, s, flag, Xend, dstat, only, g, st);
     })
@@ -263,14 +276,41 @@ cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xen
 template <typename IO>
 cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const IO* Mu,
                            IO* Nu, IO* ge, unsigned* dstat, const int* only, const ScanArgs& g,
-                           cudaStream_t st) {
+                           cudaStream_t st, const FrameSrc<IO>* fr) {
     TVLP_DISPATCH_M(Mp, {
+        if constexpr (std::is_same<IO, float>::value) {
+            if (fr != nullptr)
+                return mode == 0 ? adjoint_impl<IO, M_, false, 0, true>(gs, A, Mu, Nu, ge, dstat,
+                                                                        only, g, st, fr)
+                                 : adjoint_impl<IO, M_, false, 1, true>(gs, A, Mu, Nu, ge, dstat,
+                                                                        only, g, st, fr);
+        }
         if (mode == 0)
             return ti ? adjoint_impl<IO, M_, true, 0>(gs, A, Mu, Nu, ge, dstat, only, g, st)
                       : adjoint_impl<IO, M_, false, 0>(gs, A, Mu, Nu, ge, dstat, only, g, st);
         return ti ? adjoint_impl<IO, M_, true, 1>(gs, A, Mu, Nu, ge, dstat, only, g, st)
                   : adjoint_impl<IO, M_, false, 1>(gs, A, Mu, Nu, ge, dstat, only, g, st);
     })
+}
+
+template <typename IO>
+cudaError_t launch_upsample(int Mp, const FrameSrc<IO>& fr, IO* A, int64_t B, int64_t T,
+                            cudaStream_t st) {
+    int64_t blocks = (B * T + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    TVLP_DISPATCH_M(Mp, {
+        launch_pdl(k_upsample<IO, M_>, (unsigned)blocks, 256, 0, st, fr, A, B, T);
+        return cudaGetLastError();
+    })
+}
+
+template <typename IO>
+cudaError_t launch_grad_frames(const FrameSrc<IO>& fr, const IO* ge, const IO* s, const IO* zi,
+                               int Mzi, IO* gF, int64_t B, int64_t T, cudaStream_t st) {
+    if (fr.Mf > 32) return cudaErrorInvalidValue;
+    launch_pdl(k_grad_frames<IO>, dim3((unsigned)fr.nF, (unsigned)B), 128, 0, st, fr, ge, s, zi,
+               Mzi, gF, T);
+    return cudaGetLastError();
 }
 
 template <typename IO>
@@ -296,7 +336,7 @@ cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* pa
 
 #define TVLP_INST(IO)                                                                            \
     template cudaError_t launch_basis<IO>(int, bool, int, const IO*, const IO*, IO*,             \
-                                          const ScanArgs&, cudaStream_t);                        \
+                                          const ScanArgs&, cudaStream_t, const FrameSrc<IO>*);   \
     template cudaError_t launch_carry_fwd<IO>(int, const CarryArgs<IO>&, cudaStream_t);          \
     template cudaError_t launch_carry_bwd<IO>(int, const CarryArgs<IO>&, cudaStream_t);          \
     template cudaError_t launch_group_P<IO>(int, const IO*, IO*, int64_t, int, int, const int*,  \
@@ -306,13 +346,18 @@ cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* pa
                                                    const int*, float, int64_t, cudaStream_t);    \
     template cudaError_t launch_apply_fwd<IO>(int, bool, const IO*, const IO*, const IO*, IO*,   \
                                               int*, IO*, unsigned*, const int*, const ScanArgs&, \
-                                              cudaStream_t);                                     \
+                                              cudaStream_t, const FrameSrc<IO>*);                \
     template cudaError_t launch_adjoint<IO>(int, bool, int, const IO*, const IO*, const IO*,     \
                                             IO*, IO*, unsigned*, const int*, const ScanArgs&,    \
-                                            cudaStream_t);                                       \
+                                            cudaStream_t, const FrameSrc<IO>*);                  \
     template cudaError_t launch_refine<IO>(int, bool, const IO*, IO*, const IO*,                 \
                                            const unsigned*, int*, const int*, const ScanArgs&,   \
                                            cudaStream_t);                                        \
+    template cudaError_t launch_upsample<IO>(int, const FrameSrc<IO>&, IO*, int64_t, int64_t,      \
+                                             cudaStream_t);                                       \
+    template cudaError_t launch_grad_frames<IO>(const FrameSrc<IO>&, const IO*, const IO*,         \
+                                                const IO*, int, IO*, int64_t, int64_t,            \
+                                                cudaStream_t);                                    \
     template cudaError_t launch_grad_A<IO>(int, const IO*, const IO*, const IO*, IO*, int64_t,   \
                                            int64_t, cudaStream_t);                               \
     template cudaError_t launch_grad_a<IO>(int, const IO*, const IO*, const IO*, IO*, IO*,       \

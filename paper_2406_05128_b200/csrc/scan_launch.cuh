@@ -7,6 +7,20 @@ namespace tvlp {
 
 struct ScanArgs;
 
+// Frame-rate coefficient source (upsample_linear,
+// params.py:107-132, fused into the scan kernels).  Row t of A is
+// (1-w) F[f0] + w F[f1] with f0 = t/hop, w = (t - f0*hop)/hop, f1 = f0+1,
+// held (w = 0) on the last anchor; rows at or past Tv (padding) are zero and
+// columns at or past Mf (padded orders) are zero.
+template <typename IO>
+struct FrameSrc {
+    const IO* frames;  // [B][nF][Mf]
+    int64_t nF;        // frames per sequence: (T - 1) / hop + 1 (params.py:102-104)
+    int64_t Tv;        // valid samples per sequence
+    int hop;
+    int Mf;
+};
+
 // Orders with compiled kernels; other orders are zero-padded up to the next
 // one by the C ABI (exact: padded coefficients are 0).
 constexpr int kNumOrders = 9;
@@ -21,7 +35,7 @@ enum Prec : int { kPrecF64Chains = 0, kPrecF32Chains = 1 };
 
 template <typename IO>
 cudaError_t launch_basis(int Mp, bool ti, int prec, const IO* e, const IO* A, IO* PhiZ,
-                         const ScanArgs& g, cudaStream_t st);
+                         const ScanArgs& g, cudaStream_t st, const FrameSrc<IO>* fr = nullptr);
 int tape_elems(int Mp);  // carry-tape elements per sub-chunk
 template <typename CT>
 struct CarryArgs;
@@ -44,11 +58,21 @@ enum Prec2 : int { kPrecAuto = 2 };
 template <typename IO>
 cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO* Xin, IO* s,
                              int* flag, IO* Xend, unsigned* dstat, const int* only,
-                             const ScanArgs& g, cudaStream_t st);
+                             const ScanArgs& g, cudaStream_t st,
+                             const FrameSrc<IO>* fr = nullptr);
 template <typename IO>
 cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const IO* Mu,
                            IO* Nu, IO* ge, unsigned* dstat, const int* only, const ScanArgs& g,
-                           cudaStream_t st);
+                           cudaStream_t st, const FrameSrc<IO>* fr = nullptr);
+// A[b, t, :] = the frame-rate rows upsampled (params.py:120-132), [B][T][Mp]
+template <typename IO>
+cudaError_t launch_upsample(int Mp, const FrameSrc<IO>& fr, IO* A, int64_t B, int64_t T,
+                            cudaStream_t st);
+// grad_frames[b, f, c] = sum_t dA[t, c]/dF[f, c] * (-grad_e(t) s(t-1-c))
+// (params.py:135-145 composed with lpc.py:172), without materialising grad_A
+template <typename IO>
+cudaError_t launch_grad_frames(const FrameSrc<IO>& fr, const IO* ge, const IO* s, const IO* zi,
+                               int Mzi, IO* gF, int64_t B, int64_t T, cudaStream_t st);
 template <typename IO>
 cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xend,
                           const unsigned* dstat, int* flags, const int* fflags, const ScanArgs& g,

@@ -31,6 +31,8 @@ __all__ = [
     "lp_forward_tv",
     "lp_backward_ti",
     "lp_backward_tv",
+    "lp_forward_tv_frames",
+    "lp_backward_tv_frames",
     "shift_coeffs",
     "lagged_signal_matrix",
     "set_validation",
@@ -292,6 +294,86 @@ def lp_backward_ti(grad_s, a, s, zi=None, *, carry=None, carry_precision=None):
     """Adjoints of :func:`lp_forward_ti` (lpc.py:176-195):
     ``grad_a[i-1] = -sum_t grad_e(t) s(t-i)``."""
     return _backward(True, grad_s, a, s, zi, carry, carry_precision)
+
+
+# ---------------------------------------------------------------------------
+# frame-rate coefficients: upsample_linear fused into the filter
+# ---------------------------------------------------------------------------
+
+def _frames_args(e_or_g, frames, hop, conv):
+    batched = e_or_g.dim() == 2
+    B = e_or_g.shape[0] if batched else 1
+    T = e_or_g.shape[-1]
+    if frames.dim() != e_or_g.dim() + 1 or (batched and frames.shape[0] != B):
+        raise ValueError("frames must be a (F, M) track ((B, F, M) with a batch axis)")
+    F, M = frames.shape[-2], frames.shape[-1]
+    hop = int(hop)
+    if hop < 1 or F != (T - 1) // hop + 1:
+        raise ValueError(
+            f"got {F} frames but T={T - 1} at hop={hop} requires {(T - 1) // max(hop, 1) + 1}")
+    if M > N.load().tvlp_max_order():
+        raise ValueError(f"order M={M} exceeds the kernels' maximum {N.load().tvlp_max_order()}")
+    return B, T, F, M, hop, batched
+
+
+def lp_forward_tv_frames(e, frames, hop, zi=None, *, carry_precision=None, return_carry=False):
+    """``lp_forward_tv(e, upsample_linear(frames, hop, T - 1))`` without
+    materialising the (T, M) track (params.py:120-132 + lpc.py:101-117; the
+    synthesiser's H(z) call site synth.py:268-273).  ``frames`` [F, M] or
+    [B, F, M] with F = (T - 1) // hop + 1; rows are interpolated inside the
+    scan kernels."""
+    conv = _Conv(e, frames, zi)
+    e = _signal(conv.t(e), "e").contiguous()
+    frames = conv.t(frames, e.dtype)
+    B, T, F, M, hop, batched = _frames_args(e, frames, hop, conv)
+    if _VALIDATION == "eager" and not bool(torch.isfinite(frames).all()):
+        raise ValueError("frames contains non-finite values")
+    zi = _zi(zi, M, B, batched, e.dtype, conv)
+    dt = N.dtype_code(e.dtype)
+    lib = N.load()
+    s = torch.empty_like(e)
+    carry = torch.empty(lib.tvlp_carry_elems(B, T, M), dtype=e.dtype, device=conv.device)
+    ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FWD_TV_FRAMES, dt, B, T, M, F, 0, hop),
+                          conv.device)
+    flag = _flag(conv.device)
+    with torch.cuda.device(conv.device):
+        N.check(lib.tvlp_lp_forward_tv_frames(
+            dt, N.ptr(e), N.ptr(frames), N.ptr(zi), N.ptr(s), B, T, M, F, hop, N.ptr(carry),
+            _carry_code(carry_precision), N.ptr(ws), nws, N.ptr(flag), N.stream_ptr(conv.device)))
+    _raise_nonfinite(flag, e, frames, "frames")
+    out = conv.out(s)
+    return (out, carry) if return_carry else out
+
+
+def lp_backward_tv_frames(grad_s, frames, hop, s, zi=None, *, carry=None, carry_precision=None):
+    """(grad_e, grad_frames) of :func:`lp_forward_tv_frames`: the reference's
+    VJP chain lpc.py:152-173 -> params.py:135-145, with grad_A never
+    written."""
+    conv = _Conv(grad_s, frames, s, zi)
+    grad_s = conv.t(grad_s)
+    if grad_s.dtype not in (torch.float32, torch.float64):
+        grad_s = grad_s.to(torch.float32)
+    dtype = grad_s.dtype
+    frames = conv.t(frames, dtype)
+    s = conv.t(s, dtype)
+    B, T, F, M, hop, batched = _frames_args(grad_s, frames, hop, conv)
+    if s.shape != grad_s.shape:
+        raise ValueError("grad_s and s must share the same length")
+    zi = _zi(zi, M, B, batched, dtype, conv)
+    dt = N.dtype_code(dtype)
+    lib = N.load()
+    ge = torch.empty_like(grad_s)
+    gF = torch.empty(frames.shape, dtype=dtype, device=conv.device)
+    if carry is not None and carry.numel() != lib.tvlp_carry_elems(B, T, M):
+        carry = None
+    ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_BWD_TV_FRAMES, dt, B, T, M, F, 0, hop),
+                          conv.device)
+    with torch.cuda.device(conv.device):
+        N.check(lib.tvlp_lp_backward_tv_frames(
+            dt, N.ptr(grad_s), N.ptr(frames), N.ptr(s), N.ptr(zi), N.ptr(ge), N.ptr(gF), B, T, M,
+            F, hop, N.ptr(carry), _carry_code(carry_precision), N.ptr(ws), nws,
+            N.stream_ptr(conv.device)))
+    return conv.out(ge), conv.out(gF)
 
 
 # ---------------------------------------------------------------------------

@@ -116,10 +116,35 @@ def d1_cases():
     return out
 
 
+def upsample_cases():
+    """upsample_linear + its VJP (params.py:107-145) and the composed TV LP
+    through it (the path the fused frame-rate kernels replace, SURVEY.md
+    §8(f) rank 1): lp_forward_tv(e, upsample_linear(frames)) and the VJP
+    chain back to the frame rows."""
+    rng = np.random.default_rng(7070)
+    out = {}
+    for i, (T, hop, M) in enumerate([(9, 4, 3), (47, 8, 5), (960, 240, 22), (1200, 80, 22)]):
+        F = params.expected_frame_count(T, hop)
+        raw = np.clip(rng.normal(0, 0.25, size=(F, M)), -0.9, 0.9)
+        frames = params.reflection_to_lpc(params.squash_reflection(raw))
+        A = params.upsample_linear(frames, hop, T)
+        e = rng.normal(size=T + 1)
+        g = rng.normal(size=T + 1)
+        s = lpc.lp_forward_tv(e, A)
+        ge, gA = lpc.lp_backward_tv(g, A, s)
+        gf = params._upsample_linear_vjp(gA, F, hop, T)
+        out.update({f"c{i}_frames": frames, f"c{i}_hop": np.array(hop), f"c{i}_A": A,
+                    f"c{i}_e": e, f"c{i}_g": g, f"c{i}_s": s, f"c{i}_ge": ge, f"c{i}_gA": gA,
+                    f"c{i}_gf": gf})
+    out["n"] = np.array(4)
+    return out
+
+
 def main():
     np.savez_compressed(os.path.join(HERE, "golden_lpc.npz"), **lpc_cases())
     np.savez_compressed(os.path.join(HERE, "golden_framewise.npz"), **framewise_cases())
     np.savez_compressed(os.path.join(HERE, "golden_d1.npz"), **d1_cases())
+    np.savez_compressed(os.path.join(HERE, "golden_upsample.npz"), **upsample_cases())
     for f in ("golden_lpc.npz", "golden_framewise.npz", "golden_d1.npz"):
         print(f, os.path.getsize(os.path.join(HERE, f)))
 

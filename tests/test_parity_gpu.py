@@ -393,3 +393,56 @@ def test_host_pipeline_matches_device_path():
     np.testing.assert_array_equal(gA_h.numpy(), _np(gA))
     rs = oracle.lp_forward_tv(e[0], A[0])
     assert oracle.gradcheck_error(s_h.numpy()[0], rs) < 1e-4
+
+
+# ---------------------------------------------------------------- frame-rate coefficients
+def _frames_case(seed, B, T1, hop, M=22, dtype=np.float32):
+    """D1 frame rows (reflection walk -> step-up), F = (T1-1)//hop + 1."""
+    return data.d1_frames_batch(seed, B, T1, M, hop, dtype)
+
+
+@pytest.mark.parametrize("T1,hop,dtype,prec", [
+    (48001, 240, np.float32, "auto"), (24001, 240, np.float32, "fp32"),
+    (1000, 80, np.float32, "auto"), (961, 240, np.float64, "fp64"),
+    (48001, 240, np.float32, "fp64")])
+def test_tv_frames_parity(T1, hop, dtype, prec):
+    """lp_forward_tv_frames / lp_backward_tv_frames == the reference's
+    upsample_linear -> lp_tv chain (oracle.lp_tv_frames_fwd_bwd, pinned by
+    tests/golden/golden_upsample.npz), fp64 oracle on the same inputs."""
+    e, fr, g = _frames_case(T1 + hop, 3, T1, hop, dtype=dtype)
+    et, ft, gt = _cuda(e), _cuda(fr), _cuda(g)
+    s, carry = lpc.lp_forward_tv_frames(et, ft, hop, carry_precision=prec, return_carry=True)
+    ge, gf = lpc.lp_backward_tv_frames(gt, ft, hop, s, carry=carry, carry_precision=prec)
+    tol = 1e-9 if dtype == np.float64 else 1e-4
+    for b in range(e.shape[0]):
+        rs, rge, rgf = oracle.lp_tv_frames_fwd_bwd(e[b].astype(np.float64), fr[b].astype(np.float64),
+                                                   hop, g[b].astype(np.float64))
+        assert oracle.gradcheck_error(_np(s)[b], rs) < tol
+        assert oracle.gradcheck_error(_np(ge)[b], rge) < tol
+        assert oracle.gradcheck_error(_np(gf)[b], rgf) < tol
+
+
+def test_tv_frames_matches_materialised_track():
+    """The fused path equals lp_forward_tv on the explicitly upsampled track
+    (same fp32 rows up to the interpolation's rounding) and the no-carry
+    backward equals the carried one."""
+    e, fr, g = _frames_case(5, 2, 24001, 240)
+    et, ft, gt = _cuda(e), _cuda(fr), _cuda(g)
+    s = lpc.lp_forward_tv_frames(et, ft, 240)
+    A = np.stack([oracle.upsample_linear(fr[b].astype(np.float64), 240, 24000) for b in range(2)])
+    s_ref = lpc.lp_forward_tv(et, _cuda(A.astype(np.float32)))
+    assert oracle.gradcheck_error(_np(s), _np(s_ref)) < 1e-5
+    ge1, gf1 = lpc.lp_backward_tv_frames(gt, ft, 240, s)
+    ge2, gf2 = lpc.lp_backward_tv_frames(gt, ft, 240, s, carry_precision="fp32")
+    assert oracle.gradcheck_error(_np(ge1), _np(ge2)) < 1e-5
+    assert oracle.gradcheck_error(_np(gf1), _np(gf2)) < 1e-5
+
+
+def test_tv_frames_autograd_gradcheck():
+    from paper_2406_05128_b200.autograd import lp_tv_frames
+
+    e, fr, g = _frames_case(9, 1, 41, 8, M=4, dtype=np.float64)
+    et = torch.from_numpy(e[0]).cuda().requires_grad_(True)
+    ft = torch.from_numpy(fr[0]).cuda().requires_grad_(True)
+    assert torch.autograd.gradcheck(lambda x, f: lp_tv_frames(x, f, 8), (et, ft), eps=1e-6,
+                                    atol=1e-6)
