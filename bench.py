@@ -51,6 +51,9 @@ CONFIGS = {
     # noise) grouped into one launch; 256 items over 8 GPUs = 32 items per GPU
     "hpn_b32_t48000": dict(kind="hpn", B=32, T=48000, M=22, baseline_cfg=5,
                            encoder_params=6_100_000),
+    # config 3 with frame-rate coefficients (hop 240)
+    # upsampled inside the kernels (the synthesiser's upsample_linear -> lp_tv)
+    "tv_frames_b64_t48000": dict(kind="tvf", B=64, T=48000, M=22, hop=240, baseline_cfg=3),
 }
 DEFAULT = "tv_b64_t48000"
 
@@ -63,6 +66,10 @@ def algorithmic_bytes_per_sample(cfg):
         return 4 * (3 * M + 5)
     if cfg["kind"] == "hpn":
         return 2 * 4 * (3 * M + 5)
+    if cfg["kind"] == "tvf":
+        # e, s (fwd); g_s, s, g_e (bwd); frames in twice and grad_frames out
+        # at 1/hop of the sample rate
+        return 4 * 5 + 3 * 4 * M / cfg["hop"]
     return 21.1
 
 
@@ -75,6 +82,12 @@ def kernel_bytes_per_sample(name, M):
         "adjoint_apply": 4 * (M + 2),  # A, g_s in; g_e out
         "grad_A": 4 * (M + 2),         # g_e, s in; g_A out
     }.get(name)
+
+
+def kernel_bytes_per_sample_frames(name, M):
+    """frame-rate path (rows interpolated in the kernels)"""
+    return {"basis": 4, "apply_fwd": 8, "adjoint_zs": 4, "adjoint_apply": 8,
+            "grad_frames": 8}.get(name)
 
 
 def peaks():
@@ -149,6 +162,30 @@ def cpu_baseline(cfg, seconds=10.0):
     nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     T, M = cfg["T"], cfg["M"]
     lps_per_sample = 2 if cfg["kind"] == "hpn" else 1
+    if cfg["kind"] == "tvf":
+        # the reference chain upsample_linear -> lp_tv fwd+bwd -> upsample VJP
+        # (params.py:120-145 in numpy, the LP in the threaded C port)
+        hop = cfg["hop"]
+        B_s = max(1, min(cfg["B"], nthreads))
+        e, fr, g = data.d1_frames_batch(1000, B_s, T, M, hop)
+
+        def run_once():
+            A = np.stack([oracle.upsample_linear(fr[b], hop, T - 1) for b in range(B_s)])
+            s, ge, gA = oracle.batch_fwd_bwd("tv", e, A.astype(np.float32), g, nthreads=nthreads)
+            return [oracle.upsample_linear_vjp(gA[b], fr.shape[1], hop, T - 1) for b in range(B_s)]
+
+        run_once()
+        times = []
+        t_end = time.perf_counter() + seconds
+        while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 50):
+            t0 = time.perf_counter()
+            run_once()
+            times.append(time.perf_counter() - t0)
+        med = float(np.median(times))
+        return {"value": B_s * T / med, "unit": UNIT, "cores": nthreads, "kind": "port",
+                "sample": f"{B_s} x {T} samples (M={M}, hop={hop}, D1 frames): upsample_linear "
+                          f"(numpy) + LP fwd+bwd (oracle/tvlp_oracle.c, {nthreads} threads) + "
+                          f"upsample VJP (numpy) per repeat, median of {len(times)} repeats"}
     if cfg["kind"] in ("tv", "hpn"):
         T_s = min(T, 480_000)
         B_s = max(1, min(cfg["B"] * lps_per_sample, 4 * nthreads)) if T <= 480_000 else nthreads
@@ -217,6 +254,17 @@ def run_b200(args, cfg, rank, world, dist):
             if work is not None:
                 work.wait()
             return s, ge, gA
+    elif kind == "tvf":
+        ev, fr, gv = data.d1_frames_batch(lo, B, T, M, cfg["hop"])
+        e = torch.from_numpy(ev).to(dev)
+        A = torch.from_numpy(fr).to(dev)  # frame rows [B, F, M]
+        g = torch.from_numpy(gv).to(dev)
+        hop = cfg["hop"]
+
+        def step(e=e, A=A, g=g):
+            s, carry = lpc.lp_forward_tv_frames(e, A, hop, return_carry=True)
+            ge, gf = lpc.lp_backward_tv_frames(g, A, hop, s, carry=carry)
+            return s, ge, gf
     else:
         ev, fr, gv = data.d1_frames_batch(lo, B, T, M, cfg["hop"])
         e = torch.from_numpy(ev).to(dev)
@@ -274,7 +322,7 @@ def run_b200(args, cfg, rank, world, dist):
     dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
     roof = None
     if dom is not None:
-        bps = kernel_bytes_per_sample(dom, M)
+        bps = (kernel_bytes_per_sample_frames if kind == "tvf" else kernel_bytes_per_sample)(dom, M)
         lp_rows = 2 * B if kind == "hpn" else B  # LP sequences per GPU
         cnt, tot = prof[dom]
         t_step = tot / nsteps * 1e-3  # seconds of this kernel per step (all its slices)
@@ -292,7 +340,7 @@ def run_b200(args, cfg, rank, world, dist):
                 "peak_source": peak_kind,
                 "bytes_per_step": None if bps is None else bps * lp_rows * T,
                 "us_per_step": round(t_step * 1e6, 2), "launches_per_step": cnt / nsteps}
-        if dom in ("basis",) and kind in ("tv", "hpn"):
+        if dom in ("basis",) and kind in ("tv", "hpn", "tvf"):
             # the basis is FP32-FMA bound: 23 chains x 22 FMA per sample
             fl = 2.0 * (M + 1) * M * lp_rows * T / t_step / 1e12
             fp32_peak = 148 * 128 * 2 * 1.965e-3  # TFLOP/s at the max SM clock (derived)
@@ -346,7 +394,7 @@ def run_b200(args, cfg, rank, world, dist):
                    "kind": kind, "B_per_gpu": B, "T": T, "M": M,
                    "global_B": B * world, "parallelism": f"batch-shard x{world}",
                    "carry_precision": lpc.carry_precision(),
-                   "subchunk": int(lib.tvlp_subchunk_len(2 * B if kind == "hpn" else B, T, M)) if kind == "tv" else None,
+                   "subchunk": int(lib.tvlp_subchunk_len(2 * B if kind == "hpn" else B, T, M)) if kind in ("tv", "hpn", "tvf") else None,
                    "l2": "inputs larger than L2"},
         "gbs_algorithmic_step": round(step_gbs, 1),
         "step_roofline_frac": round(step_gbs / hbm, 4),
