@@ -74,6 +74,8 @@ int32_t tvlp_max_order(void);
 
 /* Number of elements (of the call dtype) of the carry tape for (B, T, M). */
 int64_t tvlp_carry_elems(int64_t B, int64_t T, int32_t M);
+/* Same for tvlp_lp_forward_tv_frames (its plan uses shorter sub-chunks). */
+int64_t tvlp_carry_elems_frames(int64_t B, int64_t T, int32_t M);
 /* Sub-chunk length used for (B, T, M) (diagnostics / tests; small batches use
  * shorter sub-chunks to fill the GPU). */
 int64_t tvlp_subchunk_len(int64_t B, int64_t T, int32_t M);

@@ -33,6 +33,7 @@ _SIGS = [
     ("tvlp_last_cuda_error", ctypes.c_int, []),
     ("tvlp_max_order", _I32, []),
     ("tvlp_carry_elems", _I64, [_I64, _I64, _I32]),
+    ("tvlp_carry_elems_frames", _I64, [_I64, _I64, _I32]),
     ("tvlp_subchunk_len", _I64, [_I64, _I64, _I32]),
     ("tvlp_workspace_bytes", _SZ, [_I32, _I32, _I64, _I64, _I32, _I64, _I32, _I32]),
     ("tvlp_framewise_nframes", _I64, [_I64, _I64, _I32, _I32]),

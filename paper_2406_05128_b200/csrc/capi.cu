@@ -74,15 +74,19 @@ struct Plan {
 // per-sub-chunk passes are then latency-bound and scale with Ls while the
 // serial carries scale with T/Ls (measured on config 1, us per fwd+bwd: Ls 480
 // 191, 320 160, 240 205).
-int64_t choose_ls(int64_t B, int64_t T, int64_t* Tp) {
+int64_t choose_ls(int64_t B, int64_t T, int64_t* Tp, bool frames) {
     int64_t target = B * T >= (int64_t)4096 * 512 ? 512 : 320;
+    // frame-rate rows: the lane passes interpolate rows instead of streaming
+    // them and are latency-bound, so more (shorter) sub-chunks pay for the
+    // longer carry chains (config 3 measured: Ls 480 396 us, 240 354 us)
+    if (frames) target = B * T >= (int64_t)4096 * 512 ? 240 : 160;
     if (const char* env = std::getenv("TVLP_SUBCHUNK")) {
         const long v = std::atol(env);
         if (v >= 8) target = v;
     }
     if (T >= 256) {
         int64_t best = -1;
-        for (int64_t d = 128; d <= 1024; d += 8)
+        for (int64_t d = 96; d <= 1024; d += 8)
             if (T % d == 0 && (best < 0 || std::llabs(d - target) < std::llabs(best - target)))
                 best = d;
         if (best > 0) {
@@ -98,13 +102,13 @@ int64_t choose_ls(int64_t B, int64_t T, int64_t* Tp) {
     return Ls;
 }
 
-bool make_plan(int64_t B, int64_t T, int M, Plan& p) {
+bool make_plan(int64_t B, int64_t T, int M, Plan& p, bool frames = false) {
     if (B < 1 || T < 1 || M < 1 || M > kMaxOrder) return false;
     p.B = B;
     p.T = T;
     p.M = M;
     p.Mp = padded_order(M);
-    p.Ls = (int)choose_ls(B, T, &p.Tp);
+    p.Ls = (int)choose_ls(B, T, &p.Tp, frames);
     p.nsub = (int)(p.Tp / p.Ls);
     return true;
 }
@@ -368,7 +372,9 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     // frame-rate coefficients: rows interpolated inside the fp32 scan kernels,
     // else (fp64 I/O or fp64 chains) materialised once into the workspace
     const bool frames = fr != nullptr;
-    const bool native_fr = frames && std::is_same<IO, float>::value && prec != kPrecF64Chains;
+    // (frame intervals must fall on the lane kernels' 8-row windows)
+    const bool native_fr = frames && std::is_same<IO, float>::value && prec != kPrecF64Chains &&
+                           fr->hop % kLaneWin == 0;
     const bool packed = p.Tp != p.T || (!frames && (p.Mp != p.M || !aligned16(A))) ||
                         !aligned16(e) || !aligned16(s) || (zi && !aligned16(zi));
     const int64_t nsc = p.B * p.nsub;
@@ -491,7 +497,8 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     // (without the forward's tape the basis is recomputed; the frame-rate
     // basis has fp32 chains only)
     const bool native_fr = frames && std::is_same<IO, float>::value &&
-                           (carry != nullptr || prec == kPrecF32Chains);
+                           (carry != nullptr || prec == kPrecF32Chains) &&
+                           fr->hop % kLaneWin == 0;
     const bool packed = p.Tp != p.T ||
                         (!frames && (p.Mp != p.M || !aligned16(A) || (!ti && !aligned16(gA)))) ||
                         !aligned16(gs) || !aligned16(s) || !aligned16(ge) ||
@@ -787,6 +794,12 @@ int64_t tvlp_carry_elems(int64_t B, int64_t T, int32_t M) {
     return carry_elems(p);
 }
 
+int64_t tvlp_carry_elems_frames(int64_t B, int64_t T, int32_t M) {
+    Plan p;
+    if (!make_plan(B, T, M, p, true)) return -1;
+    return carry_elems(p);
+}
+
 int64_t tvlp_subchunk_len(int64_t B, int64_t T, int32_t M) {
     Plan p;
     if (!make_plan(B, T, M, p)) return -1;
@@ -835,7 +848,7 @@ size_t tvlp_workspace_bytes(int32_t op, int32_t dtype, int64_t B, int64_t T, int
     }
     if (op == TVLP_OP_FWD_TV_FRAMES || op == TVLP_OP_BWD_TV_FRAMES) {
         Plan p;
-        if (!make_plan(B, T, M, p) || !frame_src_ok(T, F, hop)) return 0;
+        if (!make_plan(B, T, M, p, true) || !frame_src_ok(T, F, hop)) return 0;
         if (op == TVLP_OP_FWD_TV_FRAMES) {
             if (f64) {
                 const FrameSrc<double> fs = frame_src<double>(any, T, M, F, hop);
@@ -934,7 +947,7 @@ int tvlp_lp_forward_tv_frames(int32_t dtype, const void* e, const void* frames, 
     if (rc != TVLP_OK) return rc;
     if (!e || !frames || !s || !frame_src_ok(T, F, hop)) return TVLP_ERR_ARG;
     Plan p;
-    if (!make_plan(B, T, M, p)) return TVLP_ERR_ARG;
+    if (!make_plan(B, T, M, p, true)) return TVLP_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (dtype == TVLP_F64) {
         const FrameSrc<double> fs = frame_src<double>(frames, T, M, F, hop);
@@ -956,7 +969,7 @@ int tvlp_lp_backward_tv_frames(int32_t dtype, const void* grad_s, const void* fr
     if (!grad_s || !frames || !s || !grad_e || !grad_frames || !frame_src_ok(T, F, hop))
         return TVLP_ERR_ARG;
     Plan p;
-    if (!make_plan(B, T, M, p)) return TVLP_ERR_ARG;
+    if (!make_plan(B, T, M, p, true)) return TVLP_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (dtype == TVLP_F64) {
         const FrameSrc<double> fs = frame_src<double>(frames, T, M, F, hop);

@@ -239,12 +239,8 @@ k_basis(const IO* __restrict__ e, const IO* __restrict__ A, IO* __restrict__ Phi
 // ============================================================================
 // ---------------------------------------------------------------- frame-rate rows
 // One formula for every kernel (the basis, apply and adjoint passes must see
-// bit-identical rows): w = r * (1/hop), a = w fb + (1 - w) fa.
-template <typename IO>
-__device__ __forceinline__ IO frame_mix(IO fa, IO fb, IO w, IO omw) {
-    return fma(w, fb, omw * fa);
-}
-// Row t of sequence b into dst[0..M) (generic stores); no caching.
+// bit-identical rows): w = r * (1/hop), row = fa + w (fb - fa) (one FMA per
+// coefficient; the last anchor has fb = fa, i.e. w = 0 as in params.py:116).
 template <typename IO, int M>
 __device__ __forceinline__ void frame_row_store(const FrameSrc<IO>& fs, int64_t b, int64_t t,
                                                 IO inv_hop, IO* dst) {
@@ -255,47 +251,57 @@ __device__ __forceinline__ void frame_row_store(const FrameSrc<IO>& fs, int64_t 
     }
     const int tt = (int)t;
     int f0 = tt / fs.hop;
-    IO w = (IO)(tt - f0 * fs.hop) * inv_hop;
-    if (f0 >= fs.nF - 1) {
-        f0 = (int)fs.nF - 1;
-        w = (IO)0;
-    }
+    const int r = tt - f0 * fs.hop;
+    if (f0 > fs.nF - 1) f0 = (int)fs.nF - 1;
     const int f1 = min(f0 + 1, (int)fs.nF - 1);
-    const IO omw = (IO)1 - w;
+    const IO w = (IO)r * inv_hop;
     const IO* pa = fs.frames + ((int64_t)b * fs.nF + f0) * fs.Mf;
     const IO* pb = fs.frames + ((int64_t)b * fs.nF + f1) * fs.Mf;
 #pragma unroll
-    for (int i = 0; i < M; ++i)
-        dst[i] = i < fs.Mf ? frame_mix<IO>(__ldg(pa + i), __ldg(pb + i), w, omw) : (IO)0;
-}
-// Row t into registers, caching the two frame rows of the current interval.
-template <typename IO, int M>
-__device__ __forceinline__ void frame_row_cached(const FrameSrc<IO>& fs, int64_t b, int64_t t,
-                                                 IO inv_hop, int& cf0, IO (&fa)[M], IO (&fb)[M],
-                                                 IO (&a)[M]) {
-    const int tt = (int)t;
-    int f0 = tt / fs.hop;
-    IO w = (IO)(tt - f0 * fs.hop) * inv_hop;
-    if (f0 >= fs.nF - 1) {
-        f0 = (int)fs.nF - 1;
-        w = (IO)0;
+    for (int i = 0; i < M; ++i) {
+        const IO fa = i < fs.Mf ? __ldg(pa + i) : (IO)0;
+        const IO fb = i < fs.Mf ? __ldg(pb + i) : (IO)0;
+        dst[i] = fma(w, fb - fa, fa);
     }
-    if (f0 != cf0) {
-        cf0 = f0;
-        const int f1 = min(f0 + 1, (int)fs.nF - 1);
-        const IO* pa = fs.frames + ((int64_t)b * fs.nF + f0) * fs.Mf;
-        const IO* pb = fs.frames + ((int64_t)b * fs.nF + f1) * fs.Mf;
+}
+// Rows of one window of W consecutive times for one lane.  Interval changes
+// (multiples of hop) fall on window boundaries because hop % W == 0 (the C
+// ABI materialises A otherwise), so the frame rows are (re)loaded once per
+// window at most and kept as (fa, fb - fa) in registers; per step one FMA per
+// coefficient.  Keeping the reload out of the unrolled steps keeps the
+// kernel's code small (a per-step reload thrashed the instruction cache).
+template <typename IO, int M>
+struct FrameCursor {
+    int f0 = -1, r0 = 0;
+    int64_t t = 0;
+    IO fa[M], d[M];
+    __device__ __forceinline__ void window(const FrameSrc<IO>& fs, int64_t b, int64_t t_first) {
+        t = t_first;
+        const int tt = (int)min(t_first, fs.Tv - 1);
+        const int f = tt / fs.hop;
+        r0 = (int)(t_first - (int64_t)f * fs.hop);
+        if (f != f0 && t_first < fs.Tv) {
+            f0 = f;
+            const int g1 = min(f + 1, (int)fs.nF - 1);
+            const IO* pa = fs.frames + ((int64_t)b * fs.nF + f) * fs.Mf;
+            const IO* pb = fs.frames + ((int64_t)b * fs.nF + g1) * fs.Mf;
 #pragma unroll
-        for (int i = 0; i < M; ++i) {
-            fa[i] = i < fs.Mf ? __ldg(pa + i) : (IO)0;
-            fb[i] = i < fs.Mf ? __ldg(pb + i) : (IO)0;
+            for (int i = 0; i < M; ++i) {
+                const IO x = i < fs.Mf ? __ldg(pa + i) : (IO)0;
+                const IO y = i < fs.Mf ? __ldg(pb + i) : (IO)0;
+                fa[i] = x;
+                d[i] = y - x;
+            }
         }
     }
-    const IO omw = (IO)1 - w;
-    const bool valid = t < fs.Tv;
+    __device__ __forceinline__ void row(const FrameSrc<IO>& fs, IO inv_hop, int u,
+                                        IO (&a)[M]) const {
+        const IO w = (IO)(r0 + u) * inv_hop;
+        const bool valid = t + u < fs.Tv;
 #pragma unroll
-    for (int i = 0; i < M; ++i) a[i] = valid ? frame_mix<IO>(fa[i], fb[i], w, omw) : (IO)0;
-}
+        for (int i = 0; i < M; ++i) a[i] = valid ? fma(w, d[i], fa[i]) : (IO)0;
+    }
+};
 
 // steps per basic block in full windows: steps of a group interleave; the
 // group boundary bounds how far the scheduler runs ahead (register pressure)
@@ -1003,12 +1009,11 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 #pragma unroll
     for (int i = 0; i < M; ++i) R[MR - 1 - i] = active ? Xin[gid * Tape<M>::MP4 + i] : (IO)0;
     bool finite = true;
-    // frame-rate rows (FR): interval cache and the lane's sub-chunk start
+    // frame-rate rows (FR): the lane walks its sub-chunk forward in time
     const int64_t fb_b = active ? gid / g.nsub : 0;
-    const int64_t ft0 = active ? (gid % g.nsub) * (int64_t)g.Ls : 0;
     const IO inv_hop = FR ? (IO)1 / (IO)fs.hop : (IO)0;
-    int cf0 = -1;
-    IO fra[FR ? M : 1], frb[FR ? M : 1];
+    FrameCursor<IO, FR ? M : 1> cur;
+    const int64_t ft0 = active ? (gid % g.nsub) * (int64_t)g.Ls : 0;
 
     for (int kb = 0; kb < nwin; kb += WPB) {
 #pragma unroll
@@ -1030,6 +1035,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
                 IO ev[W];
 #pragma unroll
                 for (int u = 0; u < W; ++u) ev[u] = er[u];
+                if constexpr (FR) cur.window(fs, fb_b, ft0 + (int64_t)k * W);
 #pragma unroll
                 for (int u = 0; u < W; ++u) {
                     const int pos = w * W + u;  // compile-time after unrolling
@@ -1038,8 +1044,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 #pragma unroll
                         for (int i = 0; i < M; ++i) a[i] = ati[i];
                     } else if constexpr (FR) {
-                        frame_row_cached<IO, M>(fs, fb_b, ft0 + (int64_t)k * W + u, inv_hop, cf0,
-                                                fra, frb, a);
+                        cur.row(fs, inv_hop, u, a);
                     } else {
                         load_row_at<IO, M>(Ar + u * M, a, (lane * S::AROW + u * M) * S::SZ);
                     }
@@ -1158,11 +1163,11 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     IO lam[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) lam[i] = (MODE == 1 && active) ? Mu[gid * Tape<M>::MP4 + i] : (IO)0;
+    // frame-rate rows (FR): the lane walks its sub-chunk backward in time
     const int64_t fb_b = active ? gid / g.nsub : 0;
-    const int64_t ft0 = active ? (gid % g.nsub) * (int64_t)g.Ls : 0;
     const IO inv_hop = FR ? (IO)1 / (IO)fs.hop : (IO)0;
-    int cf0 = -1;
-    IO fra[FR ? M : 1], frb[FR ? M : 1];
+    FrameCursor<IO, FR ? M : 1> cur;
+    const int64_t ft0 = active ? (gid % g.nsub) * (int64_t)g.Ls : 0;
 
     for (int k = 0; k < nwin; ++k) {
         const int st = k % kLaneStages;
@@ -1180,6 +1185,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
         IO gv[W];
 #pragma unroll
         for (int u = 0; u < W; ++u) gv[u] = xr[u];
+        if constexpr (FR) cur.window(fs, fb_b, ft0 + (int64_t)(nwin - 1 - k) * W);
 #pragma unroll
         for (int u = W - 1; u >= 0; --u) {
             IO a[M];
@@ -1187,8 +1193,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
 #pragma unroll
                 for (int i = 0; i < M; ++i) a[i] = ati[i];
             } else if constexpr (FR) {
-                frame_row_cached<IO, M>(fs, fb_b, ft0 + (int64_t)(nwin - 1 - k) * W + u, inv_hop,
-                                        cf0, fra, frb, a);
+                cur.row(fs, inv_hop, u, a);
             } else {
                 load_row_at<IO, M>(Ar + u * M, a, (lane * S::AROW + u * M) * S::SZ);
             }
@@ -1487,47 +1492,108 @@ k_upsample(const FrameSrc<IO> fs, IO* __restrict__ A, int64_t B, int64_t T) {
 
 // grad_frames[b, f, c] = sum_{t: f0(t)=f} (1-w) gA(t,c) + sum_{t: f1(t)=f} w gA(t,c),
 // gA(t, c) = -grad_e(t) s(t-1-c), s(<0) = zi (params.py:135-145 over lpc.py:172).
-// One CTA per (frame, sequence); thread (c, part) sums a strided quarter of
-// the frame's support (<= 2 hop samples), then a fixed-order combine.
+// One CTA per (sequence, kFramesPerCta consecutive frames).  The weighted
+// adjoints p0(t) = (1-w)(-grad_e), p1(t) = w(-grad_e) and s over the frames'
+// support (plus lags) are staged in shared memory; thread (frame, 4 lags,
+// part) runs one interval with a sliding register window over s (one shared
+// load of p and one of s per 4 FMAs), the two parts are added at the end.
+constexpr int kFramesPerCta = 8;
 template <typename IO>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kFramesPerCta * 16)
 k_grad_frames(const FrameSrc<IO> fs, const IO* __restrict__ ge, const IO* __restrict__ s,
               const IO* __restrict__ zi, int Mzi, IO* __restrict__ gF, int64_t T) {
     grid_dep_wait();
-    __shared__ IO part[4][32];
-    const int64_t f = blockIdx.x, b = blockIdx.y;
-    const int c = threadIdx.x & 31, pq = threadIdx.x >> 5;
-    const IO inv_hop = (IO)1 / (IO)fs.hop;
+    extern __shared__ __align__(16) unsigned char gf_smem[];
+    __shared__ IO red[kFramesPerCta][32];
+    const int64_t b = blockIdx.y;
+    const int64_t fbase = (int64_t)blockIdx.x * kFramesPerCta;
+    const int hop = fs.hop;
+    constexpr int LAG = 32;  // staged lags (>= Mf)
+    // support of frames fbase..fbase+K-1: t in [(fbase-1) hop, (fbase+K) hop)
+    const int64_t tlo = (fbase - 1) * hop;
+    const int span = (kFramesPerCta + 1) * hop;
+    IO* p0 = reinterpret_cast<IO*>(gf_smem);  // (1-w(t)) (-grad_e(t)), t = tlo + i
+    IO* p1 = p0 + span;                        // w(t) (-grad_e(t))
+    IO* ss = p1 + span;                        // s(tlo - LAG + i)
     const IO* gb = ge + b * T;
     const IO* sb = s + b * T;
-    const int64_t Tv = fs.Tv;
-    auto lag = [&](int64_t t) -> IO {  // s(t - 1 - c)
-        const int64_t u = t - 1 - c;
-        if (u >= 0) return sb[u];
-        return zi != nullptr ? zi[b * Mzi + (-u - 1)] : (IO)0;
-    };
-    IO acc = (IO)0;
-    if (c < fs.Mf) {
-        // f0(t) = f: t in [f hop, (f+1) hop), weight 1 - w (w = 0 on the last anchor)
-        const int64_t lo0 = f * fs.hop;
-        const int64_t hi0 = (f == fs.nF - 1) ? Tv : min(Tv, (f + 1) * (int64_t)fs.hop);
-        for (int64_t t = lo0 + pq; t < hi0; t += 4) {
-            const IO w = (f == fs.nF - 1) ? (IO)0 : (IO)(t - lo0) * inv_hop;
-            acc = fma(((IO)1 - w) * (-gb[t]), lag(t), acc);
+    const IO inv_hop = (IO)1 / (IO)hop;
+    // staging: 8 independent global loads in flight per thread and pass
+    constexpr int U = 8;
+    for (int i0 = threadIdx.x; i0 < span + LAG; i0 += U * blockDim.x) {
+        IO v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int i = i0 + j * blockDim.x;
+            const int64_t u = tlo - LAG + i;  // s index
+            v[j] = (IO)0;
+            if (i < span + LAG) {
+                if (u >= 0)
+                    v[j] = u < fs.Tv ? sb[u] : (IO)0;
+                else if (zi != nullptr && -u - 1 < fs.Mf)
+                    v[j] = zi[b * Mzi + (-u - 1)];
+            }
         }
-        // f1(t) = f, i.e. f0(t) = f - 1 < nF - 1: weight w
-        if (f >= 1) {
-            const int64_t lo1 = (f - 1) * fs.hop, hi1 = min(Tv, f * (int64_t)fs.hop);
-            for (int64_t t = lo1 + pq; t < hi1; t += 4) {
-                const IO w = (IO)(t - lo1) * inv_hop;
-                acc = fma(w * (-gb[t]), lag(t), acc);
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+            if (i0 + j * (int)blockDim.x < span + LAG) ss[i0 + j * blockDim.x] = v[j];
+    }
+    for (int i0 = threadIdx.x; i0 < span; i0 += U * blockDim.x) {
+        IO v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int i = i0 + j * blockDim.x;
+            const int64_t t = tlo + i;
+            v[j] = (i < span && t >= 0 && t < fs.Tv) ? -gb[t] : (IO)0;
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int i = i0 + j * blockDim.x;
+            if (i < span) {
+                const int q = i / hop;  // frame fbase - 1 + q, offset i - q hop
+                const IO w = (fbase - 1 + q < fs.nF - 1) ? (IO)(i - q * hop) * inv_hop : (IO)0;
+                p0[i] = ((IO)1 - w) * v[j];
+                p1[i] = w * v[j];
             }
         }
     }
-    part[pq][c] = acc;
     __syncthreads();
-    if (pq == 0 && c < fs.Mf)
-        gF[(b * fs.nF + f) * fs.Mf + c] = (part[0][c] + part[1][c]) + (part[2][c] + part[3][c]);
+    const int k = threadIdx.x >> 4;          // frame in the CTA
+    const int c0 = ((threadIdx.x >> 1) & 7) * 4;  // first of 4 lags
+    const int part = threadIdx.x & 1;        // 0: f0(t) = f, 1: f1(t) = f
+    const int64_t f = fbase + k;
+    // part 0: t in [f hop, (f+1) hop) -> local i = (k+1) hop + r, weight p0
+    // part 1: t in [(f-1) hop, f hop) -> local i = k hop + r, weight p1 (f >= 1)
+    const int i0 = (k + 1 - part) * hop;
+    const IO* pw = part == 0 ? p0 : p1;
+    IO acc[4] = {(IO)0, (IO)0, (IO)0, (IO)0};
+    if (f < fs.nF && (part == 0 || f >= 1)) {
+        // x[j] = s(t - 1 - c0 - j) at the current t (ss index LAG + i - 1 - c0 - j)
+        const IO* sp = ss + LAG + i0 - 1 - c0;
+        IO x0 = sp[0], x1 = sp[-1], x2 = sp[-2], x3 = sp[-3];
+#pragma unroll 4
+        for (int r = 0; r < hop; ++r) {
+            const IO pv = pw[i0 + r];
+            acc[0] = fma(pv, x0, acc[0]);
+            acc[1] = fma(pv, x1, acc[1]);
+            acc[2] = fma(pv, x2, acc[2]);
+            acc[3] = fma(pv, x3, acc[3]);
+            x3 = x2;
+            x2 = x1;
+            x1 = x0;
+            x0 = sp[r + 1];
+        }
+    }
+    if (part == 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) red[k][c0 + j] = acc[j];
+    }
+    __syncthreads();
+    if (part == 0 && f < fs.nF) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (c0 + j < fs.Mf) gF[(b * fs.nF + f) * fs.Mf + c0 + j] = acc[j] + red[k][c0 + j];
+    }
 }
 
 }  // namespace tvlp

@@ -332,7 +332,7 @@ def lp_forward_tv_frames(e, frames, hop, zi=None, *, carry_precision=None, retur
     dt = N.dtype_code(e.dtype)
     lib = N.load()
     s = torch.empty_like(e)
-    carry = torch.empty(lib.tvlp_carry_elems(B, T, M), dtype=e.dtype, device=conv.device)
+    carry = torch.empty(lib.tvlp_carry_elems_frames(B, T, M), dtype=e.dtype, device=conv.device)
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FWD_TV_FRAMES, dt, B, T, M, F, 0, hop),
                           conv.device)
     flag = _flag(conv.device)
@@ -364,7 +364,7 @@ def lp_backward_tv_frames(grad_s, frames, hop, s, zi=None, *, carry=None, carry_
     lib = N.load()
     ge = torch.empty_like(grad_s)
     gF = torch.empty(frames.shape, dtype=dtype, device=conv.device)
-    if carry is not None and carry.numel() != lib.tvlp_carry_elems(B, T, M):
+    if carry is not None and carry.numel() != lib.tvlp_carry_elems_frames(B, T, M):
         carry = None
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_BWD_TV_FRAMES, dt, B, T, M, F, 0, hop),
                           conv.device)

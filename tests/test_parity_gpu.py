@@ -403,7 +403,7 @@ def _frames_case(seed, B, T1, hop, M=22, dtype=np.float32):
 
 @pytest.mark.parametrize("T1,hop,dtype,prec", [
     (48001, 240, np.float32, "auto"), (24001, 240, np.float32, "fp32"),
-    (1000, 80, np.float32, "auto"), (961, 240, np.float64, "fp64"),
+    (1000, 80, np.float32, "auto"), (961, 240, np.float64, "fp64"), (1000, 37, np.float32, "auto"),
     (48001, 240, np.float32, "fp64")])
 def test_tv_frames_parity(T1, hop, dtype, prec):
     """lp_forward_tv_frames / lp_backward_tv_frames == the reference's
