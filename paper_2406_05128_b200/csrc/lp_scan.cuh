@@ -653,8 +653,10 @@ template <int M, typename CT>
 struct CarrySmem {
     static constexpr int MP4 = Tape<M>::MP4;
     static constexpr int SUB = Tape<M>::SIZE * (int)sizeof(CT);  // one sub-chunk's tape
-    static constexpr int STAGE = kCB * SUB;
-    static constexpr int NU = kCB * MP4 * (int)sizeof(CT);        // bwd: nu of the stage
+    // fp64 tapes are twice as large: 4 per stage keeps the ring under 227 KB
+    static constexpr int CB = sizeof(CT) == 4 ? kCB : 4;
+    static constexpr int STAGE = CB * SUB;
+    static constexpr int NU = CB * MP4 * (int)sizeof(CT);        // bwd: nu of the stage
     static constexpr int BYTES = kCS * (STAGE + NU) + 64 * (int)sizeof(CT) + kCS * 8;
 };
 
@@ -679,7 +681,7 @@ struct CarryArgs {
 };
 
 // Forward carry: x(k0) = x0 (or zero), x(k+1) = Phi_k x(k) + z_k.  One warp per
-// segment (one CTA); whole tapes of kCB consecutive sub-chunks per bulk copy.
+// segment (one CTA); whole tapes of SM::CB consecutive sub-chunks per bulk copy.
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)
 k_carry_fwd(const CarryArgs<CT> a) {
@@ -701,21 +703,21 @@ k_carry_fwd(const CarryArgs<CT> a) {
     const int64_t base = b * a.nsub + k0;
     const int r = lane < M ? lane : 0;
     const int nsteps = a.tail != nullptr ? n : n - 1;  // mat-vecs needed
-    const int nst = (nsteps + kCB - 1) / kCB;
+    const int nst = (nsteps + SM::CB - 1) / SM::CB;
     if (lane == 0) {
         for (int i = 0; i < kCS; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     __syncwarp();
-    auto issue = [&](int sg) {  // stage sg: sub-chunks sg*kCB .. +kCB-1
+    auto issue = [&](int sg) {  // stage sg: sub-chunks sg*SM::CB .. +SM::CB-1
         if (lane == 0 && sg < nst) {
             const int st = sg % kCS;
-            const int cnt = min(kCB, nsteps - sg * kCB);
+            const int cnt = min(SM::CB, nsteps - sg * SM::CB);
             unsigned char* dst = smem + st * (SM::STAGE + SM::NU);
             mbar_arrive_expect_tx(&bars[st], cnt * (SM::SUB + (a.force ? MP4 * (int)sizeof(CT) : 0)));
-            tma_load_1d(dst, a.tape + (base + sg * kCB) * TP::SIZE, cnt * SM::SUB, &bars[st]);
+            tma_load_1d(dst, a.tape + (base + sg * SM::CB) * TP::SIZE, cnt * SM::SUB, &bars[st]);
             if (a.force)
-                tma_load_1d(dst + SM::STAGE, a.force + (base + sg * kCB) * MP4,
+                tma_load_1d(dst + SM::STAGE, a.force + (base + sg * SM::CB) * MP4,
                             cnt * MP4 * sizeof(CT), &bars[st]);
         }
     };
@@ -735,8 +737,8 @@ k_carry_fwd(const CarryArgs<CT> a) {
         const CT* sgb = reinterpret_cast<const CT*>(dst);
         const CT* fgb = reinterpret_cast<const CT*>(dst + SM::STAGE);
 #pragma unroll
-        for (int u = 0; u < kCB; ++u) {
-            const int i = sg * kCB + u;
+        for (int u = 0; u < SM::CB; ++u) {
+            const int i = sg * SM::CB + u;
             if (i < nsteps) {
                 // the matrix row does not depend on x: load it before the
                 // broadcast so only STS -> LDS -> FMA chain is serial
@@ -788,10 +790,10 @@ k_carry_bwd(const CarryArgs<CT> a) {
     const int64_t base = b * a.nsub + k0;
     const int r = lane < M ? lane : 0;
     // mat-vec i uses sub-chunk kk = n-1-i (kk >= 1, or >= 0 with a tail);
-    // stage sg holds sub-chunks kk = n-1-sg*kCB-u (descending), i.e. the
-    // contiguous range [hi-cnt+1, hi] with hi = n-1-sg*kCB.
+    // stage sg holds sub-chunks kk = n-1-sg*SM::CB-u (descending), i.e. the
+    // contiguous range [hi-cnt+1, hi] with hi = n-1-sg*SM::CB.
     const int nsteps = a.tail != nullptr ? n : n - 1;
-    const int nst = (nsteps + kCB - 1) / kCB;
+    const int nst = (nsteps + SM::CB - 1) / SM::CB;
     if (lane == 0) {
         for (int i = 0; i < kCS; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
@@ -800,8 +802,8 @@ k_carry_bwd(const CarryArgs<CT> a) {
     auto issue = [&](int sg) {
         if (lane == 0 && sg < nst) {
             const int st = sg % kCS;
-            const int cnt = min(kCB, nsteps - sg * kCB);
-            const int lo = n - sg * kCB - cnt;  // lowest sub-chunk of the stage
+            const int cnt = min(SM::CB, nsteps - sg * SM::CB);
+            const int lo = n - sg * SM::CB - cnt;  // lowest sub-chunk of the stage
             unsigned char* dst = smem + st * (SM::STAGE + SM::NU);
             mbar_arrive_expect_tx(&bars[st], cnt * (SM::SUB + MP4 * (int)sizeof(CT)));
             tma_load_1d(dst, a.tape + (base + lo) * TP::SIZE, cnt * SM::SUB, &bars[st]);
@@ -815,10 +817,10 @@ k_carry_bwd(const CarryArgs<CT> a) {
         const int st = sg % kCS;
         mbar_wait(&bars[st], (uint32_t)((sg / kCS) & 1));
         const unsigned char* dst = smem + st * (SM::STAGE + SM::NU);
-        const int cnt = min(kCB, nsteps - sg * kCB);
+        const int cnt = min(SM::CB, nsteps - sg * SM::CB);
 #pragma unroll
-        for (int u = 0; u < kCB; ++u) {
-            const int i = sg * kCB + u;
+        for (int u = 0; u < SM::CB; ++u) {
+            const int i = sg * SM::CB + u;
             if (i < nsteps) {
                 const int kk = n - 1 - i;
                 const int slot = cnt - 1 - u;  // position of kk inside the stage
@@ -870,7 +872,7 @@ k_group_P(const CT* __restrict__ tape, CT* __restrict__ gtape, int64_t ngroups, 
     const int k0 = (int)(gi % ng) * G;
     const int n = min(G, nsub - k0);
     const int64_t base = b * nsub + k0;
-    const int nst = (n + kCB - 1) / kCB;
+    const int nst = (n + SM::CB - 1) / SM::CB;
     if (lane == 0) {
         for (int i = 0; i < kCS; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
@@ -879,9 +881,9 @@ k_group_P(const CT* __restrict__ tape, CT* __restrict__ gtape, int64_t ngroups, 
     auto issue = [&](int sg) {
         if (lane == 0 && sg < nst) {
             const int st = sg % kCS;
-            const int cnt = min(kCB, n - sg * kCB);
+            const int cnt = min(SM::CB, n - sg * SM::CB);
             mbar_arrive_expect_tx(&bars[st], cnt * SM::SUB);
-            tma_load_1d(smem + st * (SM::STAGE + SM::NU), tape + (base + sg * kCB) * TP::SIZE,
+            tma_load_1d(smem + st * (SM::STAGE + SM::NU), tape + (base + sg * SM::CB) * TP::SIZE,
                         cnt * SM::SUB, &bars[st]);
         }
     };
@@ -893,7 +895,7 @@ k_group_P(const CT* __restrict__ tape, CT* __restrict__ gtape, int64_t ngroups, 
         const int st = sg % kCS;
         mbar_wait(&bars[st], (uint32_t)((sg / kCS) & 1));
         const CT* sgb = reinterpret_cast<const CT*>(smem + st * (SM::STAGE + SM::NU));
-        const int cnt = min(kCB, n - sg * kCB);
+        const int cnt = min(SM::CB, n - sg * SM::CB);
         for (int u = 0; u < cnt; ++u) {
             const CT* R = sgb + u * TP::SIZE + TP::R_ROW * MP4;
             CT nc[M];
