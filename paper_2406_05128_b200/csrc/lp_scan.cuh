@@ -47,7 +47,10 @@
 namespace tvlp {
 
 constexpr int kLaneWin = 8;     // rows per TMA window in the lane-per-sub-chunk kernels
-constexpr int kLaneStages = 3;  // input stages (per warp)
+#ifndef TVLP_LANE_STAGES
+#define TVLP_LANE_STAGES 3
+#endif
+constexpr int kLaneStages = TVLP_LANE_STAGES;  // input stages (per warp)
 constexpr int kOutStages = 2;   // output staging slots
 
 template <int M>
