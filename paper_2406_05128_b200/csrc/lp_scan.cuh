@@ -652,12 +652,12 @@ __device__ __forceinline__ CT dot_rows(const CT (&w)[Tape<M>::MP4], const CT (&x
     return (q0 + q1) + (q2 + q3);
 }
 
-template <int M, typename CT>
+template <int M, typename CT, int CBW = kCB>
 struct CarrySmem {
     static constexpr int MP4 = Tape<M>::MP4;
     static constexpr int SUB = Tape<M>::SIZE * (int)sizeof(CT);  // one sub-chunk's tape
     // fp64 tapes are twice as large: 4 per stage keeps the ring under 227 KB
-    static constexpr int CB = sizeof(CT) == 4 ? kCB : 4;
+    static constexpr int CB = sizeof(CT) == 4 ? CBW : (CBW < 4 ? CBW : 4);
     static constexpr int STAGE = CB * SUB;
     static constexpr int NU = CB * MP4 * (int)sizeof(CT);        // bwd: nu of the stage
     static constexpr int BYTES = kCS * (STAGE + NU) + 64 * (int)sizeof(CT) + kCS * 8;
@@ -685,12 +685,12 @@ struct CarryArgs {
 
 // Forward carry: x(k0) = x0 (or zero), x(k+1) = Phi_k x(k) + z_k.  One warp per
 // segment (one CTA); whole tapes of SM::CB consecutive sub-chunks per bulk copy.
-template <int M, typename CT>
+template <int M, typename CT, int CBW = kCB>
 __global__ void __launch_bounds__(32)
 k_carry_fwd(const CarryArgs<CT> a) {
     grid_dep_wait();
     using TP = Tape<M>;
-    using SM = CarrySmem<M, CT>;
+    using SM = CarrySmem<M, CT, CBW>;
     constexpr int MP4 = TP::MP4;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x;
@@ -772,12 +772,12 @@ k_carry_fwd(const CarryArgs<CT> a) {
 
 // Adjoint carry (right to left): mu(k_last) = x0 (or zero),
 // mu(k-1) = Phi_k^T mu(k) + nu_k.  X[k] = carry into sub-chunk k from the right.
-template <int M, typename CT>
+template <int M, typename CT, int CBW = kCB>
 __global__ void __launch_bounds__(32)
 k_carry_bwd(const CarryArgs<CT> a) {
     grid_dep_wait();
     using TP = Tape<M>;
-    using SM = CarrySmem<M, CT>;
+    using SM = CarrySmem<M, CT, CBW>;
     constexpr int MP4 = TP::MP4;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x;
@@ -862,7 +862,7 @@ k_group_P(const CT* __restrict__ tape, CT* __restrict__ gtape, int64_t ngroups, 
           const int* __restrict__ only) {
     grid_dep_wait();
     using TP = Tape<M>;
-    using SM = CarrySmem<M, CT>;
+    using SM = CarrySmem<M, CT, 4>;
     constexpr int MP4 = TP::MP4;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x;

@@ -171,30 +171,41 @@ int tape_elems(int Mp) {
     }
 }
 
-template <int M, typename IO>
-cudaError_t carry_fwd_impl(const CarryArgs<IO>& a, cudaStream_t st) {
-    using SM = CarrySmem<M, IO>;
-    auto k = k_carry_fwd<M, IO>;
+// Few long chains (one per sequence) want deep bulk copies (8 tapes per
+// stage); many short segments (the hierarchy's groups) want small rings so
+// several segments share an SM.
+template <int M, typename IO, int CBW>
+cudaError_t carry_fwd_cb(const CarryArgs<IO>& a, cudaStream_t st) {
+    using SM = CarrySmem<M, IO, CBW>;
+    auto k = k_carry_fwd<M, IO, CBW>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
     launch_pdl(k, (unsigned)a.nseg, 32, SM::BYTES, st, a);
     return cudaGetLastError();
 }
-
 template <int M, typename IO>
-cudaError_t carry_bwd_impl(const CarryArgs<IO>& a, cudaStream_t st) {
-    using SM = CarrySmem<M, IO>;
-    auto k = k_carry_bwd<M, IO>;
+cudaError_t carry_fwd_impl(const CarryArgs<IO>& a, cudaStream_t st) {
+    return a.nseg <= 296 ? carry_fwd_cb<M, IO, kCB>(a, st) : carry_fwd_cb<M, IO, 2>(a, st);
+}
+
+template <int M, typename IO, int CBW>
+cudaError_t carry_bwd_cb(const CarryArgs<IO>& a, cudaStream_t st) {
+    using SM = CarrySmem<M, IO, CBW>;
+    auto k = k_carry_bwd<M, IO, CBW>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
     launch_pdl(k, (unsigned)a.nseg, 32, SM::BYTES, st, a);
     return cudaGetLastError();
+}
+template <int M, typename IO>
+cudaError_t carry_bwd_impl(const CarryArgs<IO>& a, cudaStream_t st) {
+    return a.nseg <= 296 ? carry_bwd_cb<M, IO, kCB>(a, st) : carry_bwd_cb<M, IO, 2>(a, st);
 }
 
 template <int M, typename IO>
 cudaError_t group_P_impl(const IO* tape, IO* gtape, int64_t ngroups, int G, int nsub,
                          const int* only, cudaStream_t st) {
-    using SM = CarrySmem<M, IO>;
+    using SM = CarrySmem<M, IO, 4>;
     auto k = k_group_P<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
