@@ -118,6 +118,16 @@ int tvlp_lp_backward_tv_frames(int32_t dtype, const void* grad_s, const void* fr
                                const void* carry, int32_t carry_prec, void* workspace,
                                size_t workspace_bytes, void* stream);
 
+/* Reflection rows -> direct-form rows by the step-up recursion (params.py:43-71,
+ * reflection_to_lpc): k, a [rows, M]; float64
+ * arithmetic in the reference's order (bit-identical in fp64).  bad (nullable,
+ * device int32) is OR-ed with 1 when some |k| >= 1 (params.py:67-68 raise). */
+int tvlp_reflection_to_lpc(int32_t dtype, const void* k, void* a, int64_t rows, int32_t M,
+                           int32_t* bad, void* stream);
+/* grad_k of reflection_to_lpc (params.py:74-84, _reflection_to_lpc_vjp). */
+int tvlp_reflection_to_lpc_vjp(int32_t dtype, const void* grad_a, const void* k, void* grad_k,
+                               int64_t rows, int32_t M, void* stream);
+
 /* Time-invariant special case: a [B, M] constant row per sequence. */
 int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,
                        int64_t B, int64_t T, int32_t M, void* carry, int32_t carry_prec,

@@ -329,6 +329,49 @@ def lp_tv_frames_fwd_bwd(e, frames, hop, grad_s, zi=None):
     return s, ge, upsample_linear_vjp(gA, frames.shape[0], hop, T)
 
 
+# ---------------------------------------------------------------------------
+# step-up recursion (params.py:43-84), restated for the frame-rate path
+# ---------------------------------------------------------------------------
+
+def step_up(k):
+    """params.py:43-53: rows plus the per-stage intermediates."""
+    k = np.asarray(k, dtype=np.float64)
+    M = k.shape[-1]
+    stages = []
+    a = k[..., :1].copy()
+    for m in range(2, M + 1):
+        stages.append(a)
+        km = k[..., m - 1: m]
+        a = np.concatenate([a + km * a[..., ::-1], km], axis=-1)
+    return a, stages
+
+
+def reflection_to_lpc(k):
+    """params.py:56-71."""
+    k = np.asarray(k, dtype=np.float64)
+    if k.shape[-1] < 1:
+        raise ValueError("reflection rows need order >= 1")
+    if np.any(np.abs(k) >= 1.0):
+        raise ValueError("reflection coefficients must satisfy |k| < 1")
+    return step_up(k)[0]
+
+
+def reflection_to_lpc_vjp(grad_a, k):
+    """params.py:74-84."""
+    k = np.asarray(k, dtype=np.float64)
+    _, stages = step_up(k)
+    g = np.array(grad_a, dtype=np.float64, copy=True)
+    grad_k = np.zeros_like(k)
+    M = k.shape[-1]
+    for m in range(M, 1, -1):
+        prev = stages[m - 2]
+        g_new = g[..., : m - 1]
+        grad_k[..., m - 1] = g[..., m - 1] + np.sum(g_new * prev[..., ::-1], axis=-1)
+        g = g_new + k[..., m - 1: m] * g_new[..., ::-1]
+    grad_k[..., 0] = g[..., 0]
+    return grad_k
+
+
 def gradcheck_error(analytic, numeric):
     """Max elementwise deviation normalised by the largest entry (oracle.py:228-234)."""
     analytic = np.asarray(analytic, dtype=np.float64)

@@ -22,6 +22,8 @@ _LAZY = {
     "LPTV": "autograd", "LPTI": "autograd", "LPFramewise": "autograd", "lp_tv": "autograd",
     "lp_ti": "autograd", "framewise": "autograd", "LPTVFrames": "autograd",
     "lp_tv_frames": "autograd", "lp_tv_fwd_bwd_host": "stream",
+    "reflection_to_lpc": "params", "squash_reflection": "params",
+    "ReflectionToLPC": "autograd",
     "gradcheck_error": "metrics",
 }
 

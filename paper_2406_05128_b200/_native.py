@@ -45,6 +45,8 @@ _SIGS = [
      [_I32, _P, _P, _P, _P, _I64, _I64, _I32, _I64, _I32, _P, _I32, _P, _SZ, _P, _P]),
     ("tvlp_lp_backward_tv_frames", ctypes.c_int,
      [_I32, _P, _P, _P, _P, _P, _P, _I64, _I64, _I32, _I64, _I32, _P, _I32, _P, _SZ, _P]),
+    ("tvlp_reflection_to_lpc", ctypes.c_int, [_I32, _P, _P, _I64, _I32, _P, _P]),
+    ("tvlp_reflection_to_lpc_vjp", ctypes.c_int, [_I32, _P, _P, _P, _I64, _I32, _P]),
     ("tvlp_lp_forward_ti", ctypes.c_int,
      [_I32, _P, _P, _P, _P, _I64, _I64, _I32, _P, _I32, _P, _SZ, _P, _P]),
     ("tvlp_lp_backward_ti", ctypes.c_int,

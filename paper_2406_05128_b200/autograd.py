@@ -60,6 +60,21 @@ class LPTVFrames(torch.autograd.Function):
         return ge, gF, None, None
 
 
+class ReflectionToLPC(torch.autograd.Function):
+    """a = step_up(k) with the analytic VJP (params.py:56-84, 320-334)."""
+
+    @staticmethod
+    def forward(ctx, k):
+        a = _params.reflection_to_lpc(k.detach())
+        ctx.save_for_backward(k)
+        return a
+
+    @staticmethod
+    def backward(ctx, grad_a):
+        (k,) = ctx.saved_tensors
+        return _params.reflection_to_lpc_vjp(grad_a.contiguous(), k)
+
+
 class LPTI(torch.autograd.Function):
     """Time-invariant filter with the single-filter adjoint (lpc.py:212-219)."""
 
@@ -105,6 +120,10 @@ def lp_tv(e, A, zi=None):
 
 def lp_tv_frames(e, frames, hop, zi=None):
     return LPTVFrames.apply(e, frames, hop, zi)
+
+
+def reflection_to_lpc(k):
+    return ReflectionToLPC.apply(k)
 
 
 def lp_ti(e, a, zi=None):

@@ -12,6 +12,14 @@
 #include "../../include/tvlp.h"
 #include "framewise_launch.cuh"
 #include "lp_scan.cuh"
+
+namespace tvlp {
+template <typename IO>
+cudaError_t launch_step_up(const IO* k, IO* a, int64_t rows, int M, int* bad, cudaStream_t st);
+template <typename IO>
+cudaError_t launch_step_up_vjp(const IO* ga, const IO* k, IO* gk, int64_t rows, int M,
+                               cudaStream_t st);
+}  // namespace tvlp
 #include "scan_launch.cuh"
 
 namespace tvlp {
@@ -980,6 +988,41 @@ int tvlp_lp_backward_tv_frames(int32_t dtype, const void* grad_s, const void* fr
     const FrameSrc<float> fs = frame_src<float>(frames, T, M, F, hop);
     return backward_impl<float>(false, grad_s, frames, s, zi, grad_e, grad_frames, p, carry,
                                 carry_prec, workspace, workspace_bytes, st, nullptr, &fs);
+}
+
+int tvlp_reflection_to_lpc(int32_t dtype, const void* k, void* a, int64_t rows, int32_t M,
+                           int32_t* bad, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!k || !a || rows < 0) return TVLP_ERR_ARG;
+    if (rows == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    g_launches += 1;
+    cudaError_t err = dtype == TVLP_F64
+                          ? launch_step_up<double>(static_cast<const double*>(k),
+                                                   static_cast<double*>(a), rows, M, bad, st)
+                          : launch_step_up<float>(static_cast<const float*>(k),
+                                                  static_cast<float*>(a), rows, M, bad, st);
+    return err == cudaSuccess ? TVLP_OK : TVLP_ERR_CUDA;
+}
+
+int tvlp_reflection_to_lpc_vjp(int32_t dtype, const void* grad_a, const void* k, void* grad_k,
+                               int64_t rows, int32_t M, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!grad_a || !k || !grad_k || rows < 0) return TVLP_ERR_ARG;
+    if (rows == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    g_launches += 1;
+    cudaError_t err =
+        dtype == TVLP_F64
+            ? launch_step_up_vjp<double>(static_cast<const double*>(grad_a),
+                                         static_cast<const double*>(k),
+                                         static_cast<double*>(grad_k), rows, M, st)
+            : launch_step_up_vjp<float>(static_cast<const float*>(grad_a),
+                                        static_cast<const float*>(k),
+                                        static_cast<float*>(grad_k), rows, M, st);
+    return err == cudaSuccess ? TVLP_OK : TVLP_ERR_CUDA;
 }
 
 int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,

@@ -23,7 +23,63 @@ __all__ = [
     "framewise_lp",
     "framewise_forward",
     "framewise_backward",
+    "squash_reflection",
+    "reflection_to_lpc",
+    "reflection_to_lpc_vjp",
 ]
+
+SQUASH_LIMIT = 0.999  # params.py:31
+
+
+def squash_reflection(raw):
+    """params.py:34-36 (elementwise; torch or numpy)."""
+    if isinstance(raw, torch.Tensor):
+        return SQUASH_LIMIT * torch.tanh(raw)
+    return SQUASH_LIMIT * np.tanh(np.asarray(raw))
+
+
+def reflection_to_lpc(k):
+    """Direct-form rows from reflection rows, ``|k_i| < 1`` (params.py:56-71):
+    the step-up recursion on the device, float64 arithmetic in the
+    reference's order.  ``k`` [..., M]; numpy in -> numpy out."""
+    conv = _Conv(k)
+    kt = conv.t(k)
+    if kt.dtype not in (torch.float32, torch.float64):
+        kt = kt.to(torch.float64)
+    kt = kt.contiguous()
+    if kt.dim() < 1 or kt.shape[-1] < 1:
+        raise ValueError("reflection rows need order >= 1")
+    M = kt.shape[-1]
+    rows = kt.numel() // M
+    lib = N.load()
+    a = torch.empty_like(kt)
+    bad = torch.zeros(1, dtype=torch.int32, device=conv.device)
+    with torch.cuda.device(conv.device):
+        N.check(lib.tvlp_reflection_to_lpc(N.dtype_code(kt.dtype), N.ptr(kt), N.ptr(a), rows, M,
+                                           N.ptr(bad), N.stream_ptr(conv.device)))
+    if int(bad.item()) != 0:
+        raise ValueError("reflection coefficients must satisfy |k| < 1")
+    return conv.out(a)
+
+
+def reflection_to_lpc_vjp(grad_a, k):
+    """grad_k of :func:`reflection_to_lpc` (params.py:74-84)."""
+    conv = _Conv(grad_a, k)
+    kt = conv.t(k)
+    if kt.dtype not in (torch.float32, torch.float64):
+        kt = kt.to(torch.float64)
+    kt = kt.contiguous()
+    ga = conv.t(grad_a, kt.dtype).contiguous()
+    if ga.shape != kt.shape:
+        raise ValueError("grad_a and k must share the same shape")
+    M = kt.shape[-1]
+    rows = kt.numel() // M
+    lib = N.load()
+    gk = torch.empty_like(kt)
+    with torch.cuda.device(conv.device):
+        N.check(lib.tvlp_reflection_to_lpc_vjp(N.dtype_code(kt.dtype), N.ptr(ga), N.ptr(kt),
+                                               N.ptr(gk), rows, M, N.stream_ptr(conv.device)))
+    return conv.out(gk)
 
 
 def expected_frame_count(T, hop):

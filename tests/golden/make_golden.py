@@ -140,11 +140,27 @@ def upsample_cases():
     return out
 
 
+def stepup_cases():
+    """reflection_to_lpc + its VJP (params.py:43-84) on random rows."""
+    rng = np.random.default_rng(4343)
+    out = {}
+    for i, (F, M) in enumerate([(1, 1), (3, 2), (17, 9), (201, 22), (5, 30)]):
+        k = params.squash_reflection(rng.normal(0, 0.6, size=(F, M)))
+        a, stages = params._step_up(k)
+        ga = rng.normal(size=(F, M))
+        gk = params._reflection_to_lpc_vjp(ga, k, stages)
+        out.update({f"c{i}_k": k, f"c{i}_a": params.reflection_to_lpc(k), f"c{i}_ga": ga,
+                    f"c{i}_gk": gk})
+    out["n"] = np.array(5)
+    return out
+
+
 def main():
     np.savez_compressed(os.path.join(HERE, "golden_lpc.npz"), **lpc_cases())
     np.savez_compressed(os.path.join(HERE, "golden_framewise.npz"), **framewise_cases())
     np.savez_compressed(os.path.join(HERE, "golden_d1.npz"), **d1_cases())
     np.savez_compressed(os.path.join(HERE, "golden_upsample.npz"), **upsample_cases())
+    np.savez_compressed(os.path.join(HERE, "golden_stepup.npz"), **stepup_cases())
     for f in ("golden_lpc.npz", "golden_framewise.npz", "golden_d1.npz"):
         print(f, os.path.getsize(os.path.join(HERE, f)))
 

@@ -446,3 +446,35 @@ def test_tv_frames_autograd_gradcheck():
     ft = torch.from_numpy(fr[0]).cuda().requires_grad_(True)
     assert torch.autograd.gradcheck(lambda x, f: lp_tv_frames(x, f, 8), (et, ft), eps=1e-6,
                                     atol=1e-6)
+
+
+# ---------------------------------------------------------------- step-up (§8(f) rank 2)
+def test_reflection_to_lpc_bitexact_vs_reference(golden_dir=None):
+    """The device step-up and its VJP reproduce the reference's fp64 outputs
+    bit for bit (params.py:43-84; tests/golden/golden_stepup.npz)."""
+    import os
+
+    from paper_2406_05128_b200 import params
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_stepup.npz"))
+    for i in range(int(z["n"])):
+        k = z[f"c{i}_k"]
+        np.testing.assert_array_equal(params.reflection_to_lpc(k), z[f"c{i}_a"])
+        np.testing.assert_array_equal(params.reflection_to_lpc_vjp(z[f"c{i}_ga"], k),
+                                      z[f"c{i}_gk"])
+    with pytest.raises(ValueError, match="reflection"):
+        params.reflection_to_lpc(np.array([[0.5, 1.0]]))
+
+
+def test_reflection_frames_lp_chain_autograd():
+    """k (frame-rate reflection) -> step-up -> fused upsample+LP, end to end
+    through autograd, against the oracle chain (fp64, gradcheck)."""
+    from paper_2406_05128_b200.autograd import lp_tv_frames, reflection_to_lpc
+
+    rng = np.random.default_rng(3)
+    hop, T1, M = 8, 41, 4
+    F = (T1 - 1) // hop + 1
+    k = torch.from_numpy(0.999 * np.tanh(rng.normal(0, 0.4, (F, M)))).cuda().requires_grad_(True)
+    e = torch.from_numpy(rng.normal(size=T1)).cuda().requires_grad_(True)
+    assert torch.autograd.gradcheck(lambda kk, ee: lp_tv_frames(ee, reflection_to_lpc(kk), hop),
+                                    (k, e), eps=1e-6, atol=1e-6)
