@@ -656,8 +656,10 @@ template <int M, typename CT, int CBW = kCB>
 struct CarrySmem {
     static constexpr int MP4 = Tape<M>::MP4;
     static constexpr int SUB = Tape<M>::SIZE * (int)sizeof(CT);  // one sub-chunk's tape
-    // fp64 tapes are twice as large: 4 per stage keeps the ring under 227 KB
-    static constexpr int CB = sizeof(CT) == 4 ? CBW : (CBW < 4 ? CBW : 4);
+    // as many tapes per stage as requested while the ring stays under ~200 KB
+    // (fp64 tapes and high orders are larger)
+    static constexpr int CB_FIT = (200 * 1024) / (kCS * (SUB + MP4 * (int)sizeof(CT)));
+    static constexpr int CB = CBW < CB_FIT ? CBW : (CB_FIT > 0 ? CB_FIT : 1);
     static constexpr int STAGE = CB * SUB;
     static constexpr int NU = CB * MP4 * (int)sizeof(CT);        // bwd: nu of the stage
     static constexpr int BYTES = kCS * (STAGE + NU) + 64 * (int)sizeof(CT) + kCS * 8;

@@ -478,3 +478,38 @@ def test_reflection_frames_lp_chain_autograd():
     e = torch.from_numpy(rng.normal(size=T1)).cuda().requires_grad_(True)
     assert torch.autograd.gradcheck(lambda kk, ee: lp_tv_frames(ee, reflection_to_lpc(kk), hop),
                                     (k, e), eps=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("M", list(range(1, 31)))
+def test_every_order_tv_ti(M, rng):
+    """Every order 1..30 (compiled orders 2..30, odd ones zero-padded), ragged
+    lengths (no 8-aligned divisor -> padded plan), zi: TV and TI against the
+    oracle."""
+    T1 = 1999 + 37 * M
+    e, A, g = data.d1_batch(100 + M, 2, T1, M, hop=61)
+    zi = (0.1 * rng.standard_normal((2, M))).astype(np.float32)
+    _tv_parity(e, A, g, zi=zi)
+    a = np.ascontiguousarray(A[:, T1 // 2, :])
+    et, at, gt, zt = _cuda(e), _cuda(a), _cuda(g), _cuda(zi)
+    s = lpc.lp_forward_ti(et, at, zt)
+    ge, ga = lpc.lp_backward_ti(gt, at, s, zt)
+    for b in range(2):
+        rs = oracle.lp_forward_ti(e[b].astype(np.float64), a[b].astype(np.float64),
+                                  zi[b].astype(np.float64))
+        rge, rga = oracle.lp_backward_ti(g[b].astype(np.float64), a[b].astype(np.float64), rs,
+                                         zi[b].astype(np.float64))
+        errs = (_err(_np(s)[b], rs), _err(_np(ge)[b], rge), _err(_np(ga)[b], rga))
+        assert max(errs) < TOL32, (M, b, errs)
+
+
+@pytest.mark.parametrize("B,T1", [(1, 24000), (3, 48000), (5, 9600), (17, 4800)])
+def test_small_batch_plans(B, T1):
+    """Small batches take shorter sub-chunks (plan depends on B*T): parity and
+    the carry tape size agree with the plan."""
+    from paper_2406_05128_b200 import _native as N
+
+    lib = N.load()
+    Ls = lib.tvlp_subchunk_len(B, T1, 22)
+    assert T1 % Ls == 0
+    e, A, g = data.d1_batch(200 + B, B, T1)
+    _tv_parity(e, A, g)
