@@ -66,6 +66,8 @@ extern "C" {
 #define TVLP_OP_FW_BWD 5
 #define TVLP_OP_FWD_TV_FRAMES 6
 #define TVLP_OP_BWD_TV_FRAMES 7
+#define TVLP_OP_BWD_TV_EX 8
+#define TVLP_OP_SEGMENT_TRANSITION 9
 
 int tvlp_abi_version(void);
 const char* tvlp_status_string(int status);
@@ -127,6 +129,21 @@ int tvlp_reflection_to_lpc(int32_t dtype, const void* k, void* a, int64_t rows, 
 /* grad_k of reflection_to_lpc (params.py:74-84, _reflection_to_lpc_vjp). */
 int tvlp_reflection_to_lpc_vjp(int32_t dtype, const void* grad_a, const void* k, void* grad_k,
                                int64_t rows, int32_t M, void* stream);
+
+/* Time segments of one long sequence on several GPUs (the
+ * exchange step; host side paper_2406_05128_b200/longseq.py):
+ * tvlp_lp_backward_tv_ex = tvlp_lp_backward_tv with mu_in (nullable, [B, M]):
+ * the adjoint of the state at the segment's end contributed by later segments,
+ * and grad_zi (nullable, [B, M]): dL/dzi, the adjoint leaving through the
+ * segment's initial state.  tvlp_segment_transition: Phi [B, M, M] (row-major)
+ * = the product of all sub-chunk transitions of each sequence, from the carry
+ * tape a tvlp_lp_forward_tv call filled; x_end = Phi zi + (zero-state end). */
+int tvlp_lp_backward_tv_ex(int32_t dtype, const void* grad_s, const void* A, const void* s,
+                           const void* zi, void* grad_e, void* grad_A, int64_t B, int64_t T,
+                           int32_t M, const void* carry, int32_t carry_prec, const void* mu_in,
+                           void* grad_zi, void* workspace, size_t workspace_bytes, void* stream);
+int tvlp_segment_transition(int32_t dtype, const void* carry, int64_t B, int64_t T, int32_t M,
+                            void* Phi, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Time-invariant special case: a [B, M] constant row per sequence. */
 int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,

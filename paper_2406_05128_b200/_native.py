@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libtvlp_b200.so")
 F32, F64 = 0, 1
 CARRY_F64, CARRY_F32, CARRY_AUTO = 0, 1, 2
 (OP_FWD_TV, OP_BWD_TV, OP_FWD_TI, OP_BWD_TI, OP_FW_FWD, OP_FW_BWD, OP_FWD_TV_FRAMES,
- OP_BWD_TV_FRAMES) = range(8)
+ OP_BWD_TV_FRAMES, OP_BWD_TV_EX, OP_SEGMENT_TRANSITION) = range(10)
 
 _lib = None
 
@@ -47,6 +47,9 @@ _SIGS = [
      [_I32, _P, _P, _P, _P, _P, _P, _I64, _I64, _I32, _I64, _I32, _P, _I32, _P, _SZ, _P]),
     ("tvlp_reflection_to_lpc", ctypes.c_int, [_I32, _P, _P, _I64, _I32, _P, _P]),
     ("tvlp_reflection_to_lpc_vjp", ctypes.c_int, [_I32, _P, _P, _P, _I64, _I32, _P]),
+    ("tvlp_lp_backward_tv_ex", ctypes.c_int,
+     [_I32, _P, _P, _P, _P, _P, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _P, _SZ, _P]),
+    ("tvlp_segment_transition", ctypes.c_int, [_I32, _P, _I64, _I64, _I32, _P, _P, _SZ, _P]),
     ("tvlp_lp_forward_ti", ctypes.c_int,
      [_I32, _P, _P, _P, _P, _I64, _I64, _I32, _P, _I32, _P, _SZ, _P, _P]),
     ("tvlp_lp_backward_ti", ctypes.c_int,

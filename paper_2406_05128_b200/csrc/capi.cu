@@ -234,7 +234,9 @@ struct Hier {
         return launch_carry_fwd<IO>(p->Mp, e, st);
     }
     // mu(k-1) = Phi_k^T mu(k) + nu_k on level l
-    cudaError_t bwd(int l, const IO* nu, IO* X) const {
+    // x0 (nullable, [B][mp4]): adjoint state entering each sequence from the
+    // right (a later time segment held elsewhere, longseq.py)
+    cudaError_t bwd(int l, const IO* nu, IO* X, const IO* x0 = nullptr) const {
         const int64_t B = p->B;
         if (l == lv.L - 1) {
             CarryArgs<IO> a = args(l);
@@ -242,6 +244,8 @@ struct Hier {
             a.X = X;
             a.nseg = B;
             a.seglen = a.nsub;
+            a.x0 = x0;
+            a.x0_stride = mp4(*p);
             return launch_carry_bwd<IO>(p->Mp, a, st);
         }
         CarryArgs<IO> t = args(l);
@@ -252,7 +256,7 @@ struct Hier {
         t.seglen = kGroup;
         cudaError_t err = launch_carry_bwd<IO>(p->Mp, t, st);
         if (err != cudaSuccess) return err;
-        err = bwd(l + 1, U[l + 1], V[l + 1]);
+        err = bwd(l + 1, U[l + 1], V[l + 1], x0);
         if (err != cudaSuccess) return err;
         CarryArgs<IO> e = args(l);
         e.force = nu;
@@ -368,6 +372,47 @@ __global__ void k_lag(const IO* __restrict__ s, const IO* __restrict__ zi, IO* _
         const int64_t src = t - c - 1;
         out[i] = src >= 0 ? s[b * T + src] : (zi ? zi[b * M + (c - t)] : (IO)0);
     }
+}
+
+// Phi[b][i][c] = R rows of a product tape (Tape layout: rows R_ROW + i).
+template <typename IO>
+__global__ void k_extract_phi(const IO* __restrict__ tape, IO* __restrict__ Phi, int64_t B, int M,
+                              int mp4, int tsize, int rrow) {
+    grid_dep_wait();
+    const int64_t n = B * M * M;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(x % M);
+        const int i = (int)((x / M) % M);
+        const int64_t b = x / ((int64_t)M * M);
+        Phi[x] = tape[b * tsize + (int64_t)(rrow + i) * mp4 + c];
+    }
+}
+
+// Transition of a whole sequence (segment): the product of its sub-chunk
+// transitions Phi_{n-1} ... Phi_0, from the top level of the carry tape.
+template <typename IO>
+int segment_transition_impl(const void* carry_v, const Plan& p, void* Phi, void* ws,
+                            size_t ws_bytes, cudaStream_t st, size_t* need) {
+    const size_t sz = sizeof(IO);
+    const int TS = tape_elems(p.Mp);
+    Carver c(ws);
+    IO* out = static_cast<IO*>(c.take(p.B * (int64_t)TS * sz));
+    if (need) {
+        *need = c.used;
+        return TVLP_OK;
+    }
+    if (ws_bytes < c.used) return TVLP_ERR_WORKSPACE;
+    const Levels lv = make_levels(p);
+    const IO* top = static_cast<const IO*>(carry_v) + lv.off[lv.L - 1];
+    const int n = (int)lv.n[lv.L - 1];
+    TVLP_CK(launch_group_P<IO>(p.Mp, top, out, p.B, n, n, nullptr, st));
+    g_launches += 1;
+    const int64_t tot = p.B * (int64_t)p.M * p.M;
+    launch_pdl(k_extract_phi<IO>, grid_for(tot), 256, 0, st, out, static_cast<IO*>(Phi), p.B, p.M,
+               (int)mp4(p), TS, p.Mp + 1);
+    TVLP_CK(cudaGetLastError());
+    return TVLP_OK;
 }
 
 // ---------------------------------------------------------------- TV / TI
@@ -497,7 +542,8 @@ template <typename IO>
 int backward_impl(bool ti, const void* gs, const void* A, const void* s, const void* zi, void* ge,
                   void* gA, const Plan& p, const void* carry_v, int prec, void* ws,
                   size_t ws_bytes, cudaStream_t st, size_t* need,
-                  const FrameSrc<IO>* fr = nullptr) {
+                  const FrameSrc<IO>* fr = nullptr, const void* mu_in = nullptr,
+                  void* grad_zi = nullptr) {
     // frames mode: A is the frame-rate source fr, gA receives grad_frames [B][F][M]
     const size_t sz = sizeof(IO);
     const IO* carry = static_cast<const IO*>(carry_v);
@@ -530,7 +576,8 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     // backward recomputes the transition matrices with fp64 chains
     if (carry == nullptr && prec == kPrecAuto) prec = kPrecF64Chains;
     const bool refine = sizeof(IO) == 4 && (prec == kPrecAuto || hier);
-    IO* kout = refine ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
+    IO* kout = (refine || grad_zi || need) ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
+    IO* mu_in_p = (mu_in || need) ? static_cast<IO*>(c.take(p.B * mp * sz)) : nullptr;
     int* flags = refine ? static_cast<int*>(c.take(p.B * sizeof(int))) : nullptr;
     unsigned* dstat = refine ? static_cast<unsigned*>(c.take(p.B * 2 * sizeof(unsigned))) : nullptr;
     IO* D0 = (refine && hier) ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
@@ -597,7 +644,12 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
              (launch_adjoint<IO>(p.Mp, ti, 0, gs_p, A_p, nullptr, nu, nullptr, nullptr, nullptr, g,
                                  st, frk)));
     if (dstat) TVLP_CK(cudaMemsetAsync(dstat, 0, p.B * 2 * sizeof(unsigned), st));
-    TVLP_RUN("carry_bwd", 1, st, (h.bwd(0, nu, mu)));
+    if (mu_in) {  // [B][M] -> [B][mp4] (zero padded)
+        TVLP_CK(cudaMemsetAsync(mu_in_p, 0, p.B * mp * sz, st));
+        TVLP_CK(cudaMemcpy2DAsync(mu_in_p, mp * sz, mu_in, p.M * sz, p.M * sz, p.B,
+                                  cudaMemcpyDeviceToDevice, st));
+    }
+    TVLP_RUN("carry_bwd", 1, st, (h.bwd(0, nu, mu, mu_in ? mu_in_p : nullptr)));
     TVLP_RUN("adjoint_apply", 1, st,
              (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, kout, ge_p, dstat, nullptr, g, st,
                                  frk)));
@@ -625,8 +677,12 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
             }()));
         }
         TVLP_RUN("adjoint_apply_refined", 1, st,
-                 (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, nullptr, flags, g,
-                                     st, frk)));
+                 (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, grad_zi ? kout : nullptr, ge_p,
+                                     nullptr, flags, g, st, frk)));
+    }
+    if (grad_zi) {  // adjoint at the segment's left boundary: carry-out of sub-chunk 0
+        TVLP_CK(cudaMemcpy2DAsync(grad_zi, p.M * sz, kout, p.nsub * mp * sz, p.M * sz, p.B,
+                                  cudaMemcpyDeviceToDevice, st));
     }
     if (frames) {
         TVLP_RUN("grad_frames", 1, st,
@@ -854,6 +910,23 @@ size_t tvlp_workspace_bytes(int32_t op, int32_t dtype, int64_t B, int64_t T, int
         }
         return need;
     }
+    if (op == TVLP_OP_BWD_TV_EX || op == TVLP_OP_SEGMENT_TRANSITION) {
+        Plan p;
+        if (!make_plan(B, T, M, p)) return 0;
+        if (op == TVLP_OP_SEGMENT_TRANSITION) {
+            if (f64)
+                segment_transition_impl<double>(any, p, (void*)any, nullptr, 0, 0, &need);
+            else
+                segment_transition_impl<float>(any, p, (void*)any, nullptr, 0, 0, &need);
+        } else if (f64) {
+            backward_impl<double>(false, any, any, any, any, (void*)any, (void*)any, p, nullptr,
+                                  kPrecAuto, nullptr, 0, 0, &need, nullptr, any, (void*)any);
+        } else {
+            backward_impl<float>(false, any, any, any, any, (void*)any, (void*)any, p, nullptr,
+                                 kPrecAuto, nullptr, 0, 0, &need, nullptr, any, (void*)any);
+        }
+        return need;
+    }
     if (op == TVLP_OP_FWD_TV_FRAMES || op == TVLP_OP_BWD_TV_FRAMES) {
         Plan p;
         if (!make_plan(B, T, M, p, true) || !frame_src_ok(T, F, hop)) return 0;
@@ -1023,6 +1096,38 @@ int tvlp_reflection_to_lpc_vjp(int32_t dtype, const void* grad_a, const void* k,
                                         static_cast<const float*>(k),
                                         static_cast<float*>(grad_k), rows, M, st);
     return err == cudaSuccess ? TVLP_OK : TVLP_ERR_CUDA;
+}
+
+int tvlp_lp_backward_tv_ex(int32_t dtype, const void* grad_s, const void* A, const void* s,
+                           const void* zi, void* grad_e, void* grad_A, int64_t B, int64_t T,
+                           int32_t M, const void* carry, int32_t carry_prec, const void* mu_in,
+                           void* grad_zi, void* workspace, size_t workspace_bytes, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!grad_s || !A || !s || !grad_e || !grad_A) return TVLP_ERR_ARG;
+    Plan p;
+    if (!make_plan(B, T, M, p)) return TVLP_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64)
+        return backward_impl<double>(false, grad_s, A, s, zi, grad_e, grad_A, p, carry,
+                                     TVLP_CARRY_F64, workspace, workspace_bytes, st, nullptr,
+                                     nullptr, mu_in, grad_zi);
+    return backward_impl<float>(false, grad_s, A, s, zi, grad_e, grad_A, p, carry, carry_prec,
+                                workspace, workspace_bytes, st, nullptr, nullptr, mu_in, grad_zi);
+}
+
+int tvlp_segment_transition(int32_t dtype, const void* carry, int64_t B, int64_t T, int32_t M,
+                            void* Phi, void* workspace, size_t workspace_bytes, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!carry || !Phi) return TVLP_ERR_ARG;
+    Plan p;
+    if (!make_plan(B, T, M, p)) return TVLP_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64)
+        return segment_transition_impl<double>(carry, p, Phi, workspace, workspace_bytes, st,
+                                               nullptr);
+    return segment_transition_impl<float>(carry, p, Phi, workspace, workspace_bytes, st, nullptr);
 }
 
 int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,

@@ -67,3 +67,93 @@ def test_strong_shard_partition():
             parts = [pdist.strong_shard(B, r, world) for r in range(world)]
             assert parts[0][0] == 0 and parts[-1][1] == B
             assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+
+
+# ---------------------------------------------------------------- one sequence split in time
+class _NumpySegments:
+    """Segment primitives of longseq.py restated in numpy on the oracle (CPU),
+    so the exchange and its fold can run on a gloo world without a GPU."""
+
+    def forward(self, e, A, zi):
+        s = np.stack([oracle.lp_forward_tv(e[b].numpy(), A[b].numpy(),
+                                           None if zi is None else zi[b].numpy())
+                      for b in range(e.shape[0])])
+        return torch.from_numpy(s), (A, e)
+
+    def transition(self, tape, B, T, M, dtype, device):
+        A, _ = tape
+        Phi = np.zeros((B, M, M))
+        for b in range(B):
+            for k in range(M):
+                zi = np.zeros(M)
+                zi[k] = 1.0
+                s = oracle.lp_forward_tv(np.zeros(T), A[b].numpy(), zi)
+                Phi[b, :, k] = s[::-1][:M]
+        return torch.from_numpy(Phi)
+
+    def backward(self, g, A, s, zi, tape, mu_in):
+        B, T = g.shape
+        M = A.shape[-1]
+        ge = np.zeros((B, T))
+        gA = np.zeros((B, T, M))
+        nu = np.zeros((B, M))
+        for b in range(B):
+            a = A[b].numpy()
+            lam = np.zeros(M) if mu_in is None else mu_in[b].numpy().copy()
+            for t in range(T - 1, -1, -1):  # transposed-state adjoint (k_adjoint)
+                l0 = lam[0] + g[b, t].item()
+                ge[b, t] = l0
+                new = np.empty(M)
+                new[:-1] = -a[t, :-1] * l0 + lam[1:]
+                new[-1] = -a[t, -1] * l0
+                lam = new
+            nu[b] = lam
+            sb = s[b].numpy()
+            z = np.zeros(M) if zi is None else zi[b].numpy()
+            for t in range(T):
+                for c in range(M):
+                    u = t - 1 - c
+                    gA[b, t, c] = -ge[b, t] * (sb[u] if u >= 0 else z[-u - 1])
+        return torch.from_numpy(ge), torch.from_numpy(gA), torch.from_numpy(nu)
+
+
+def _split_worker(rank, world, port, outdir):
+    from paper_2406_05128_b200 import longseq
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo")
+    e, A, g = data.d1_batch(77, 2, 3 * 40, 3, hop=17, dtype=np.float64)
+    zi = np.array([[0.3, -0.2, 0.1], [0.0, 0.5, -0.4]])
+    seg = slice(rank * 40, (rank + 1) * 40)
+    eng = _NumpySegments()
+    s, ctx = longseq.lp_tv_forward_split(torch.from_numpy(e[:, seg].copy()),
+                                         torch.from_numpy(A[:, seg].copy()),
+                                         torch.from_numpy(zi), engine=eng)
+    ge, gA = longseq.lp_tv_backward_split(torch.from_numpy(g[:, seg].copy()),
+                                          torch.from_numpy(A[:, seg].copy()), s, ctx, engine=eng)
+    np.savez(os.path.join(outdir, f"split{rank}.npz"), s=s.numpy(), ge=ge.numpy(), gA=gA.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_world3_time_split_exchange(tmp_path):
+    """SURVEY.md §8(e) exchange step on a gloo world of 3: one all_gather of
+    (Phi, end state) forward and of the boundary adjoints backward gives every
+    rank its exact segment of the whole-sequence result."""
+    world = 3
+    port = _free_port()
+    mp.start_processes(_split_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    e, A, g = data.d1_batch(77, 2, 3 * 40, 3, hop=17, dtype=np.float64)
+    zi = np.array([[0.3, -0.2, 0.1], [0.0, 0.5, -0.4]])
+    parts = [np.load(tmp_path / f"split{r}.npz") for r in range(world)]
+    s = np.concatenate([p["s"] for p in parts], 1)
+    ge = np.concatenate([p["ge"] for p in parts], 1)
+    gA = np.concatenate([p["gA"] for p in parts], 1)
+    for b in range(2):
+        rs = oracle.lp_forward_tv(e[b], A[b], zi[b])
+        rge, rgA = oracle.lp_backward_tv(g[b], A[b], rs, zi[b])
+        np.testing.assert_allclose(s[b], rs, rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(ge[b], rge, rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(gA[b], rgA, rtol=1e-10, atol=1e-12)

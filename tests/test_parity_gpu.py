@@ -513,3 +513,83 @@ def test_small_batch_plans(B, T1):
     assert T1 % Ls == 0
     e, A, g = data.d1_batch(200 + B, B, T1)
     _tv_parity(e, A, g)
+
+
+# ---------------------------------------------------------------- one sequence split in time
+@pytest.mark.parametrize("R,T_seg,precision", [(3, 48000, "auto"), (4, 480 * 300, "auto"),
+                                               (2, 24000, "fp64")])
+def test_time_split_segments_match_whole_sequence(R, T_seg, precision):
+    """longseq.py's exchange (segment transitions + end states forward,
+    boundary adjoints backward), all R 'ranks' played in one process: equals
+    the oracle on the concatenated sequence."""
+    from paper_2406_05128_b200 import longseq
+
+    lpc.set_carry_precision(precision)
+    try:
+        e, A, g = data.d1_batch(61, 2, R * T_seg)
+        zi = (0.1 * np.random.default_rng(1).standard_normal((2, 22))).astype(np.float32)
+        eng = longseq.GpuSegmentEngine()
+        seg = [slice(r * T_seg, (r + 1) * T_seg) for r in range(R)]
+        et, At, gt, zt = _cuda(e), _cuda(A), _cuda(g), _cuda(zi)
+        loc = [longseq.forward_local(eng, r, et[:, seg[r]].contiguous(), At[:, seg[r]].contiguous(),
+                                     zt) for r in range(R)]
+        Phis, zs = [x[2] for x in loc], [x[3] for x in loc]
+        s_parts, ctxs = [], []
+        for r in range(R):
+            x_in = longseq.forward_combine(r, Phis, zs)
+            if x_in is None:
+                s, tape, zr = loc[r][0], loc[r][1], zt
+            else:
+                s, tape = eng.forward(et[:, seg[r]].contiguous(), At[:, seg[r]].contiguous(), x_in)
+                zr = x_in
+            s_parts.append(s)
+            ctxs.append((tape, zr))
+        bl = [longseq.backward_local(eng, gt[:, seg[r]].contiguous(), At[:, seg[r]].contiguous(),
+                                     s_parts[r], ctxs[r][1], ctxs[r][0]) for r in range(R)]
+        nus = [x[2] for x in bl]
+        ge_parts, gA_parts = [], []
+        for r in range(R):
+            mu = longseq.backward_combine(r, Phis, nus)
+            if mu is None:
+                ge, gA = bl[r][0], bl[r][1]
+            else:
+                ge, gA, _ = eng.backward(gt[:, seg[r]].contiguous(), At[:, seg[r]].contiguous(),
+                                         s_parts[r], ctxs[r][1], ctxs[r][0], mu)
+            ge_parts.append(ge)
+            gA_parts.append(gA)
+        s = _np(torch.cat(s_parts, 1))
+        ge = _np(torch.cat(ge_parts, 1))
+        gA = _np(torch.cat(gA_parts, 1))
+        for b in range(2):
+            z64 = zi[b].astype(np.float64)
+            rs = oracle.lp_forward_tv(e[b].astype(np.float64), A[b].astype(np.float64), z64)
+            rge, rgA = oracle.lp_backward_tv(g[b].astype(np.float64), A[b].astype(np.float64), rs,
+                                             z64)
+            errs = (_err(s[b], rs), _err(ge[b], rge), _err(gA[b], rgA))
+            assert max(errs) < TOL32, (b, errs)
+    finally:
+        lpc.set_carry_precision("auto")
+
+
+def test_backward_ex_grad_zi_matches_gradcheck():
+    """tvlp_lp_backward_tv_ex's grad_zi is dL/dzi (checked by finite
+    differences in fp64)."""
+    from paper_2406_05128_b200 import longseq
+
+    rng = np.random.default_rng(2)
+    e, A, g = data.d1_batch(9, 1, 600, 6, hop=50, dtype=np.float64)
+    zi = rng.standard_normal((1, 6))
+    eng = longseq.GpuSegmentEngine()
+    et, At, gt, zt = _cuda(e), _cuda(A), _cuda(g), _cuda(zi)
+    s, tape = eng.forward(et, At, zt)
+    _, _, nu = eng.backward(gt, At, s, zt, tape, None)
+    h = 1e-6
+    fd = np.zeros(6)
+    for i in range(6):
+        zp, zm = zi.copy(), zi.copy()
+        zp[0, i] += h
+        zm[0, i] -= h
+        sp = _np(lpc.lp_forward_tv(et, At, _cuda(zp)))
+        sm = _np(lpc.lp_forward_tv(et, At, _cuda(zm)))
+        fd[i] = np.sum(g * (sp - sm)) / (2 * h)
+    np.testing.assert_allclose(_np(nu)[0], fd, rtol=1e-6, atol=1e-8)
