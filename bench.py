@@ -54,6 +54,9 @@ CONFIGS = {
     # config 3 with frame-rate coefficients (hop 240)
     # upsampled inside the kernels (the synthesiser's upsample_linear -> lp_tv)
     "tv_frames_b64_t48000": dict(kind="tvf", B=64, T=48000, M=22, hop=240, baseline_cfg=3),
+    # config 4 as ONE sequence split in time across the ranks (strong scaling;
+    # longseq.py: one all_gather of segment summaries per direction)
+    "tv_b1_t14400000_split": dict(kind="tvsplit", B=1, T=14_400_000, M=22, baseline_cfg=4),
 }
 DEFAULT = "tv_b64_t48000"
 
@@ -62,7 +65,7 @@ def algorithmic_bytes_per_sample(cfg):
     """SURVEY.md §8(d): TV fwd 4(M+2) + bwd 4(2M+3) = 4(3M+5); frame-wise ~21.1;
     HpN: two TV LPs per audio sample (568 B)."""
     M = cfg["M"]
-    if cfg["kind"] == "tv":
+    if cfg["kind"] in ("tv", "tvsplit"):
         return 4 * (3 * M + 5)
     if cfg["kind"] == "hpn":
         return 2 * 4 * (3 * M + 5)
@@ -186,7 +189,7 @@ def cpu_baseline(cfg, seconds=10.0):
                 "sample": f"{B_s} x {T} samples (M={M}, hop={hop}, D1 frames): upsample_linear "
                           f"(numpy) + LP fwd+bwd (oracle/tvlp_oracle.c, {nthreads} threads) + "
                           f"upsample VJP (numpy) per repeat, median of {len(times)} repeats"}
-    if cfg["kind"] in ("tv", "hpn"):
+    if cfg["kind"] in ("tv", "hpn", "tvsplit"):
         T_s = min(T, 480_000)
         B_s = max(1, min(cfg["B"] * lps_per_sample, 4 * nthreads)) if T <= 480_000 else nthreads
         e, A, g = data.d1_batch(1000, B_s, T_s, M)
@@ -254,6 +257,24 @@ def run_b200(args, cfg, rank, world, dist):
             if work is not None:
                 work.wait()
             return s, ge, gA
+    elif kind == "tvsplit":
+        from paper_2406_05128_b200 import longseq
+
+        Tr = T // world  # this rank's time segment of the one sequence
+        e_all, A_all, g_all = data.d1_batch_torch(0, 1, T, M, device=dev)
+        e = e_all[:, rank * Tr:(rank + 1) * Tr].contiguous()
+        A = A_all[:, rank * Tr:(rank + 1) * Tr].contiguous()
+        g = g_all[:, rank * Tr:(rank + 1) * Tr].contiguous()
+        del e_all, A_all, g_all
+
+        def step(e=e, A=A, g=g):
+            if dist is None:
+                s, carry = lpc._forward(False, e, A, None, return_carry=True)
+                ge, gA = lpc._backward(False, g, A, s, None, carry)
+                return s, ge, gA
+            s, ctx = longseq.lp_tv_forward_split(e, A)
+            ge, gA = longseq.lp_tv_backward_split(g, A, s, ctx)
+            return s, ge, gA
     elif kind == "tvf":
         ev, fr, gv = data.d1_frames_batch(lo, B, T, M, cfg["hop"])
         e = torch.from_numpy(ev).to(dev)
@@ -300,7 +321,7 @@ def run_b200(args, cfg, rank, world, dist):
     refined = lib.tvlp_refined_sequences() - r0
     ms = pdist.max_over_ranks(ev0.elapsed_time(ev1) / args.steps, dist, dev)
     nonfinite_seen = lpc.check_nonfinite(dev)
-    samples = B * T * world
+    samples = B * T * (1 if kind == "tvsplit" else world)
     value = samples / (ms * 1e-3)
 
     # profiling pass: per-kernel CUDA-event durations over K steps
@@ -324,9 +345,10 @@ def run_b200(args, cfg, rank, world, dist):
     if dom is not None:
         bps = (kernel_bytes_per_sample_frames if kind == "tvf" else kernel_bytes_per_sample)(dom, M)
         lp_rows = 2 * B if kind == "hpn" else B  # LP sequences per GPU
+        T_k = T // world if kind == "tvsplit" else T  # samples per sequence on this GPU
         cnt, tot = prof[dom]
         t_step = tot / nsteps * 1e-3  # seconds of this kernel per step (all its slices)
-        ach = (bps * lp_rows * T / t_step / 1e9) if bps is not None else None
+        ach = (bps * lp_rows * T_k / t_step / 1e9) if bps is not None else None
         traffic = None
         tf = os.path.join(ROOT, "profiles", "r1_traffic.json")
         if os.path.exists(tf) and kind in ("tv", "hpn") and (lp_rows, T, M) == (64, 48000, 22):
@@ -338,11 +360,11 @@ def run_b200(args, cfg, rank, world, dist):
                 "achieved": None if ach is None else round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": None if ach is None else round(ach / hbm, 4), "traffic": traffic,
                 "peak_source": peak_kind,
-                "bytes_per_step": None if bps is None else bps * lp_rows * T,
+                "bytes_per_step": None if bps is None else bps * lp_rows * T_k,
                 "us_per_step": round(t_step * 1e6, 2), "launches_per_step": cnt / nsteps}
-        if dom in ("basis",) and kind in ("tv", "hpn", "tvf"):
+        if dom in ("basis",) and kind in ("tv", "hpn", "tvf", "tvsplit"):
             # the basis is FP32-FMA bound: 23 chains x 22 FMA per sample
-            fl = 2.0 * (M + 1) * M * lp_rows * T / t_step / 1e12
+            fl = 2.0 * (M + 1) * M * lp_rows * T_k / t_step / 1e12
             fp32_peak = 148 * 128 * 2 * 1.965e-3  # TFLOP/s at the max SM clock (derived)
             roof["fp32_tflops"] = round(fl, 2)
             roof["fp32_frac_of_derived_peak"] = round(fl / fp32_peak, 4)
@@ -386,7 +408,8 @@ def run_b200(args, cfg, rank, world, dist):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if kind == "tvsplit" else "weak",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic D1 (SURVEY.md §8(d)); inputs resident in HBM; working set "
                 f"{round(algorithmic_bytes_per_sample(cfg) * B * T / 1e6)} MB > 126 MB L2 "
                 "(no flush needed)",
