@@ -52,10 +52,15 @@ extern "C" {
 #define TVLP_ERR_CUDA 4      /* a CUDA launch failed */
 
 /* precision of the sub-chunk transition matrices ("carries") */
-#define TVLP_CARRY_F64 0 /* fp64 chains, default: matches the fp64 oracle to 1e-4 on resonant tracks */
+#define TVLP_CARRY_F64 0 /* fp64 chains: matches the fp64 oracle to 1e-4 on resonant tracks */
 #define TVLP_CARRY_F32 1 /* fp32 chains: faster, ~1e-3 relative on near-unit-circle poles */
 #define TVLP_CARRY_AUTO 2 /* fp32 chains + boundary-defect check + device-side refinement of the
                              sequences whose carries fail it (fp32 I/O; fp64 I/O uses fp64) */
+/* OR-ed into carry_prec of a forward: `carry` already holds the tape of a
+ * forward over the same (e, A, B, T, M) -- the tape does not depend on zi --
+ * so the transition pass is skipped and only the carry and apply passes run
+ * (a new initial state, longseq.py). */
+#define TVLP_CARRY_REUSE 16
 
 /* workspace op codes */
 #define TVLP_OP_FWD_TV 0

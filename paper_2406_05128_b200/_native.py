@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libtvlp_b200.so")
 
 F32, F64 = 0, 1
 CARRY_F64, CARRY_F32, CARRY_AUTO = 0, 1, 2
+CARRY_REUSE = 16  # OR-ed: the carry tape is already filled for the same (e, A)
 (OP_FWD_TV, OP_BWD_TV, OP_FWD_TI, OP_BWD_TI, OP_FW_FWD, OP_FW_BWD, OP_FWD_TV_FRAMES,
  OP_BWD_TV_FRAMES, OP_BWD_TV_EX, OP_SEGMENT_TRANSITION) = range(10)
 

@@ -422,6 +422,10 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
                  cudaStream_t st, size_t* need, const FrameSrc<IO>* fr = nullptr) {
     const size_t sz = sizeof(IO);
     IO* carry = static_cast<IO*>(carry_v);
+    // TVLP_CARRY_REUSE: the caller's tape already holds Phi_j and z_j for the
+    // same (e, A); only zi is new, so the basis (and compose) passes are skipped
+    const bool reuse_tape = (prec & TVLP_CARRY_REUSE) && carry != nullptr;
+    prec &= ~TVLP_CARRY_REUSE;
     // frame-rate coefficients: rows interpolated inside the fp32 scan kernels,
     // else (fp64 I/O or fp64 chains) materialised once into the workspace
     const bool frames = fr != nullptr;
@@ -494,8 +498,10 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     }
     const FrameSrc<IO>* frk = native_fr ? fr : nullptr;
     const int bprec = (prec == kPrecAuto || prec == kPrecF32Chains) ? prec : kPrecF64Chains;
-    TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, bprec, e_p, A_p, phiz, g, st, frk)));
-    if (hier) TVLP_RUN("compose", h.lv.L - 1, st, (h.compose()));
+    if (!reuse_tape) {
+        TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, bprec, e_p, A_p, phiz, g, st, frk)));
+        if (hier) TVLP_RUN("compose", h.lv.L - 1, st, (h.compose()));
+    }
     TVLP_RUN("carry_fwd", 1, st, (h.fwd(0, nullptr, zi_p, p.Mp, xin, dstat, fflags)));
     TVLP_RUN("apply_fwd", 1, st,
              (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, xend, dstat, nullptr, g,
@@ -983,7 +989,8 @@ static int fwd_entry(bool ti, int32_t dtype, const void* e, const void* A, const
     if (!make_plan(B, T, M, p)) return TVLP_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (dtype == TVLP_F64)
-        return forward_impl<double>(ti, e, A, zi, s, p, carry, TVLP_CARRY_F64, ws, ws_bytes,
+        return forward_impl<double>(ti, e, A, zi, s, p, carry,
+                                    TVLP_CARRY_F64 | (prec & TVLP_CARRY_REUSE), ws, ws_bytes,
                                     nonfinite, st, nullptr);
     return forward_impl<float>(ti, e, A, zi, s, p, carry, prec, ws, ws_bytes, nonfinite, st,
                                nullptr);

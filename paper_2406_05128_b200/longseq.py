@@ -11,8 +11,9 @@ forward
      segment's sub-chunk transitions (tvlp_segment_transition), z_r = the end
      state of s0_r.
   2. all_gather (Phi_r, z_r)  -- M*M + M values per sequence per rank.
-  3. x_1 = z_0, x_{q+1} = Phi_q x_q + z_q: rank r re-runs its segment with
-     zi = x_r (r > 0).
+  3. x_1 = z_0, x_{q+1} = Phi_q x_q + z_q: rank r re-runs the carry and apply
+     passes of its segment with zi = x_r (r > 0), reusing its carry tape
+     (TVLP_CARRY_REUSE: the tape does not depend on zi).
 
 backward (adjoint flows right to left)
   1. ge0_r, nu_r = VJP of segment r with nothing entering from the right;
@@ -23,7 +24,7 @@ backward (adjoint flows right to left)
 
 The summaries are tiny, so the collective is one all_gather per direction
 (NCCL on GPUs, gloo in the CPU tests); the per-rank work is one extra
-forward/VJP pass over the rank's own segment.  The phases are exposed
+carry+apply pass and one extra VJP pass over the rank's own segment.  The phases are exposed
 separately (``*_local`` / ``*_combine``) so one process can play every rank
 (tests) and the CPU tests can swap in a numpy segment engine.
 """
@@ -41,8 +42,25 @@ __all__ = ["GpuSegmentEngine", "forward_local", "forward_combine", "backward_loc
 class GpuSegmentEngine:
     """Segment primitives on the B200 kernels (the C ABI)."""
 
-    def forward(self, e, A, zi):
-        return lpc._forward(False, e, A, zi, return_carry=True)
+    def forward(self, e, A, zi, tape=None):
+        """(s, tape); with ``tape`` from a forward over the same (e, A) only the
+        carry and apply passes run (the tape does not depend on zi)."""
+        if tape is None:
+            return lpc._forward(False, e, A, zi, return_carry=True)
+        lib = N.load()
+        B, T = e.shape
+        M = A.shape[-1]
+        dt = N.dtype_code(e.dtype)
+        s = torch.empty_like(e)
+        ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FWD_TV, dt, B, T, M, 0, 0, 0),
+                              e.device)
+        flag = lpc._flag(e.device)
+        with torch.cuda.device(e.device):
+            N.check(lib.tvlp_lp_forward_tv(dt, N.ptr(e), N.ptr(A), N.ptr(zi.contiguous()),
+                                           N.ptr(s), B, T, M, N.ptr(tape),
+                                           lpc._carry_code() | N.CARRY_REUSE, N.ptr(ws), nws,
+                                           N.ptr(flag), N.stream_ptr(e.device)))
+        return s, tape
 
     def transition(self, tape, B, T, M, dtype, device):
         lib = N.load()
@@ -139,7 +157,7 @@ def lp_tv_forward_split(e, A, zi=None, group=None, engine=None):
     if x_in is None:
         s, zi_r = s0, zi
     else:
-        s, tape = engine.forward(e, A, x_in)
+        s, tape = engine.forward(e, A, x_in, tape)  # same (e, A): reuse the tape
         zi_r = x_in
     return s, {"tape": tape, "Phis": Phis, "zi": zi_r, "rank": rank}
 

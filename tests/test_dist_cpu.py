@@ -74,7 +74,7 @@ class _NumpySegments:
     """Segment primitives of longseq.py restated in numpy on the oracle (CPU),
     so the exchange and its fold can run on a gloo world without a GPU."""
 
-    def forward(self, e, A, zi):
+    def forward(self, e, A, zi, tape=None):
         s = np.stack([oracle.lp_forward_tv(e[b].numpy(), A[b].numpy(),
                                            None if zi is None else zi[b].numpy())
                       for b in range(e.shape[0])])

@@ -540,7 +540,8 @@ def test_time_split_segments_match_whole_sequence(R, T_seg, precision):
             if x_in is None:
                 s, tape, zr = loc[r][0], loc[r][1], zt
             else:
-                s, tape = eng.forward(et[:, seg[r]].contiguous(), At[:, seg[r]].contiguous(), x_in)
+                s, tape = eng.forward(et[:, seg[r]].contiguous(), At[:, seg[r]].contiguous(), x_in,
+                                      loc[r][1])
                 zr = x_in
             s_parts.append(s)
             ctxs.append((tape, zr))
