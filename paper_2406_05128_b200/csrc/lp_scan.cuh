@@ -46,7 +46,10 @@
 
 namespace tvlp {
 
-constexpr int kLaneWin = 8;     // rows per TMA window in the lane-per-sub-chunk kernels
+#ifndef TVLP_LANE_WIN
+#define TVLP_LANE_WIN 8
+#endif
+constexpr int kLaneWin = TVLP_LANE_WIN;  // rows per TMA window in the lane-per-sub-chunk kernels
 #ifndef TVLP_LANE_STAGES
 #define TVLP_LANE_STAGES 3
 #endif
