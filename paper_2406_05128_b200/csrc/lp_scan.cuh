@@ -673,6 +673,12 @@ struct CarrySmem {
 // scheme, one group in the expansion step of the hierarchical scheme.
 template <typename CT>
 struct CarryArgs {
+    // 3-D view [tapes][2M+1 rows][MP4] of `tape` (use_tmap): each ring stage
+    // is ONE tensor copy of just the rows the chain reads (z + R rows forward,
+    // W rows backward) -- a single CTA's bulk copies stream at ~24 GB/s, so
+    // the carry chains were bound by the tape bytes they moved (measured)
+    alignas(64) CUtensorMap tmap;
+    int use_tmap;
     const CT* tape;      // [B*nsub][Tape<M>::SIZE]
     const CT* force;     // fwd: nullable override of the tape's z rows; bwd: nu. [B*nsub][MP4]
     const CT* x0;        // nullable initial state per segment (fwd: left end, bwd: right end)
@@ -690,9 +696,9 @@ struct CarryArgs {
 
 // Forward carry: x(k0) = x0 (or zero), x(k+1) = Phi_k x(k) + z_k.  One warp per
 // segment (one CTA); whole tapes of SM::CB consecutive sub-chunks per bulk copy.
-template <int M, typename CT, int CBW = kCB>
+template <int M, typename CT, int CBW = kCB, bool TM = false>
 __global__ void __launch_bounds__(32)
-k_carry_fwd(const CarryArgs<CT> a) {
+k_carry_fwd(const __grid_constant__ CarryArgs<CT> a) {
     grid_dep_wait();
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT, CBW>;
@@ -722,8 +728,16 @@ k_carry_fwd(const CarryArgs<CT> a) {
             const int st = sg % kCS;
             const int cnt = min(SM::CB, nsteps - sg * SM::CB);
             unsigned char* dst = smem + st * (SM::STAGE + SM::NU);
-            mbar_arrive_expect_tx(&bars[st], cnt * (SM::SUB + (a.force ? MP4 * (int)sizeof(CT) : 0)));
-            tma_load_1d(dst, a.tape + (base + sg * SM::CB) * TP::SIZE, cnt * SM::SUB, &bars[st]);
+            if (TM) {  // z + R rows of SM::CB tapes: box [CB][M+1][MP4]
+                mbar_arrive_expect_tx(&bars[st], SM::CB * (M + 1) * MP4 * (int)sizeof(CT) +
+                                                     (a.force ? cnt * MP4 * (int)sizeof(CT) : 0));
+                tma_load_3d(dst, &a.tmap, 0, TP::Z_ROW, (int)(base + sg * SM::CB), &bars[st]);
+            } else {
+                mbar_arrive_expect_tx(&bars[st],
+                                      cnt * (SM::SUB + (a.force ? MP4 * (int)sizeof(CT) : 0)));
+                tma_load_1d(dst, a.tape + (base + sg * SM::CB) * TP::SIZE, cnt * SM::SUB,
+                            &bars[st]);
+            }
             if (a.force)
                 tma_load_1d(dst + SM::STAGE, a.force + (base + sg * SM::CB) * MP4,
                             cnt * MP4 * sizeof(CT), &bars[st]);
@@ -750,7 +764,9 @@ k_carry_fwd(const CarryArgs<CT> a) {
             if (i < nsteps) {
                 // the matrix row does not depend on x: load it before the
                 // broadcast so only STS -> LDS -> FMA chain is serial
-                const CT* tp = sgb + u * TP::SIZE;
+                // tensor-copied stage: tape u is [z row, R rows] at stride (M+1) MP4
+                const CT* tp = TM ? sgb + u * (M + 1) * MP4 - TP::Z_ROW * MP4
+                                  : sgb + u * TP::SIZE;
                 CT w[MP4], xv[MP4];
                 load_vec<CT, MP4>(tp + (TP::R_ROW + r) * MP4, w);
                 const CT zr = a.force ? fgb[u * MP4 + r] : tp[TP::Z_ROW * MP4 + r];
@@ -777,9 +793,9 @@ k_carry_fwd(const CarryArgs<CT> a) {
 
 // Adjoint carry (right to left): mu(k_last) = x0 (or zero),
 // mu(k-1) = Phi_k^T mu(k) + nu_k.  X[k] = carry into sub-chunk k from the right.
-template <int M, typename CT, int CBW = kCB>
+template <int M, typename CT, int CBW = kCB, bool TM = false>
 __global__ void __launch_bounds__(32)
-k_carry_bwd(const CarryArgs<CT> a) {
+k_carry_bwd(const __grid_constant__ CarryArgs<CT> a) {
     grid_dep_wait();
     using TP = Tape<M>;
     using SM = CarrySmem<M, CT, CBW>;
@@ -813,8 +829,14 @@ k_carry_bwd(const CarryArgs<CT> a) {
             const int cnt = min(SM::CB, nsteps - sg * SM::CB);
             const int lo = n - sg * SM::CB - cnt;  // lowest sub-chunk of the stage
             unsigned char* dst = smem + st * (SM::STAGE + SM::NU);
-            mbar_arrive_expect_tx(&bars[st], cnt * (SM::SUB + MP4 * (int)sizeof(CT)));
-            tma_load_1d(dst, a.tape + (base + lo) * TP::SIZE, cnt * SM::SUB, &bars[st]);
+            if (TM) {  // W rows of SM::CB tapes from the stage's lowest: box [CB][M][MP4]
+                mbar_arrive_expect_tx(&bars[st], SM::CB * M * MP4 * (int)sizeof(CT) +
+                                                     cnt * MP4 * (int)sizeof(CT));
+                tma_load_3d(dst, &a.tmap, 0, 0, (int)(base + lo), &bars[st]);
+            } else {
+                mbar_arrive_expect_tx(&bars[st], cnt * (SM::SUB + MP4 * (int)sizeof(CT)));
+                tma_load_1d(dst, a.tape + (base + lo) * TP::SIZE, cnt * SM::SUB, &bars[st]);
+            }
             tma_load_1d(dst + SM::STAGE, a.force + (base + lo) * MP4, cnt * MP4 * sizeof(CT),
                         &bars[st]);
         }
@@ -832,7 +854,7 @@ k_carry_bwd(const CarryArgs<CT> a) {
             if (i < nsteps) {
                 const int kk = n - 1 - i;
                 const int slot = cnt - 1 - u;  // position of kk inside the stage
-                const CT* tp = reinterpret_cast<const CT*>(dst) + slot * TP::SIZE;
+                const CT* tp = reinterpret_cast<const CT*>(dst) + slot * (TM ? M * MP4 : TP::SIZE);
                 const CT* nu = reinterpret_cast<const CT*>(dst + SM::STAGE) + slot * MP4;
                 CT w[MP4], mv[MP4];
                 load_vec<CT, MP4>(tp + r * MP4, w);

@@ -65,6 +65,23 @@ cudaError_t map2d(CUtensorMap* m, const void* base, int sz, uint64_t dim0, uint6
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 3-D view [ntapes][rows][MP4] of a carry tape array, box [cb][box_rows][MP4]
+cudaError_t map_tapes(CUtensorMap* m, const void* base, int sz, int mp4, int rows,
+                      uint64_t ntapes, int tape_elems_, uint32_t box_rows, uint32_t cb) {
+    std::memset(m, 0, sizeof(*m));
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    cuuint64_t gdim[3] = {(cuuint64_t)mp4, (cuuint64_t)rows, ntapes};
+    cuuint64_t gstr[2] = {(cuuint64_t)mp4 * sz, (cuuint64_t)tape_elems_ * sz};
+    cuuint32_t box[3] = {(cuuint32_t)mp4, box_rows, cb};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, sz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                    3, const_cast<void*>(base), gdim, gstr, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <typename IO, int M, bool TI>
 cudaError_t lane_maps(LaneMaps& mp, const IO* A, const IO* X, const IO* O, const ScanArgs& g) {
     using S = LaneSmem<IO, M, TI>;
@@ -175,11 +192,27 @@ int tape_elems(int Mp) {
 // stage); many short segments (the hierarchy's groups) want small rings so
 // several segments share an SM.
 template <int M, typename IO, int CBW>
-cudaError_t carry_fwd_cb(const CarryArgs<IO>& a, cudaStream_t st) {
+cudaError_t carry_tmap(CarryArgs<IO>& a, bool fwd) {
     using SM = CarrySmem<M, IO, CBW>;
-    auto k = k_carry_fwd<M, IO, CBW>;
+    const int64_t nper = (a.nsub + a.seglen - 1) / a.seglen;
+    const uint64_t ntapes = (uint64_t)(a.nseg / nper) * a.nsub;
+    a.use_tmap = 1;
+    return map_tapes(&a.tmap, a.tape, (int)sizeof(IO), Tape<M>::MP4, 2 * M + 1, ntapes,
+                     Tape<M>::SIZE, fwd ? M + 1 : M, SM::CB);
+}
+
+template <int M, typename IO, int CBW>
+cudaError_t carry_fwd_cb(const CarryArgs<IO>& a0, cudaStream_t st) {
+    using SM = CarrySmem<M, IO, CBW>;
+    auto k = k_carry_fwd<M, IO, CBW, (CBW < kCB)>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
+    CarryArgs<IO> a = a0;
+    if (CBW < kCB) {  // many short segments: tensor copies of the needed rows (measured
+                      // faster there; one 1-D copy of whole tapes is faster for long chains)
+        err = carry_tmap<M, IO, CBW>(a, true);
+        if (err != cudaSuccess) return err;
+    }
     launch_pdl(k, (unsigned)a.nseg, 32, SM::BYTES, st, a);
     return cudaGetLastError();
 }
@@ -189,11 +222,16 @@ cudaError_t carry_fwd_impl(const CarryArgs<IO>& a, cudaStream_t st) {
 }
 
 template <int M, typename IO, int CBW>
-cudaError_t carry_bwd_cb(const CarryArgs<IO>& a, cudaStream_t st) {
+cudaError_t carry_bwd_cb(const CarryArgs<IO>& a0, cudaStream_t st) {
     using SM = CarrySmem<M, IO, CBW>;
-    auto k = k_carry_bwd<M, IO, CBW>;
+    auto k = k_carry_bwd<M, IO, CBW, (CBW < kCB)>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
+    CarryArgs<IO> a = a0;
+    if (CBW < kCB) {
+        err = carry_tmap<M, IO, CBW>(a, false);
+        if (err != cudaSuccess) return err;
+    }
     launch_pdl(k, (unsigned)a.nseg, 32, SM::BYTES, st, a);
     return cudaGetLastError();
 }
