@@ -28,8 +28,8 @@
 #include "common.cuh"
 #include "scan_launch.cuh"
 
-#ifndef TVLP_BASIS4_SPLIT
-#define TVLP_BASIS4_SPLIT 0
+#ifndef TVLP_BASIS_CHAINS
+#define TVLP_BASIS_CHAINS 3
 #endif
 #ifndef TVLP_BASIS4_PIPE
 #define TVLP_BASIS4_PIPE 0
@@ -312,12 +312,14 @@ struct FrameCursor {
 // steps per basic block in full windows: steps of a group interleave; the
 // group boundary bounds how far the scheduler runs ahead (register pressure)
 constexpr int kBasisGroup = TVLP_BASIS_GROUP;
+// independent scalar chains per lane (3: M = 22 -> 8 lanes per sub-chunk)
+constexpr int kChains = TVLP_BASIS_CHAINS;
 constexpr bool kBasisPipe = TVLP_BASIS4_PIPE;
 
 template <int M, bool TI>
 struct Basis4Cfg {
     static_assert(M % 2 == 0, "even orders only (odd orders are padded)");
-    static constexpr int P = (M + 1 + 2) / 3;
+    static constexpr int P = (M + kChains) / kChains;  // ceil((M + 1) / kChains)
     static constexpr int S = 32 / P;
     static constexpr int NW = TVLP_BASIS4_WARPS;  // independent warps per CTA
     static constexpr int NSTB = 2;
@@ -334,8 +336,7 @@ struct Basis4Cfg {
 };
 
 template <int M, bool TI, int U>
-__device__ __forceinline__ void basis4_step(float (&R0)[M], float (&R1)[M], float (&R2)[M],
-                                            const float* __restrict__ Ar,
+__device__ __forceinline__ void basis4_step(float (&R)[kChains][M], const float* __restrict__ Ar,
                                             const float* __restrict__ es, const float (&ati)[M],
                                             float (&ac)[M], int zs) {
     float a[M];
@@ -352,86 +353,58 @@ __device__ __forceinline__ void basis4_step(float (&R0)[M], float (&R1)[M], floa
         load_row_at<float, M>(Ar + U * M, a, U * M * 4);
     }
     const float ev = es[U];
-    float c0 = zs == 0 ? ev : 0.f, c1 = zs == 1 ? ev : 0.f, c2 = zs == 2 ? ev : 0.f;
-#if TVLP_BASIS4_SPLIT
-    // two accumulators per chain: six independent FMA streams per lane
-    float d0 = 0.f, d1 = 0.f, d2 = 0.f;
+    float c[kChains];
+#pragma unroll
+    for (int j = 0; j < kChains; ++j) c[j] = zs == j ? ev : 0.f;
 #pragma unroll
     for (int i = M; i >= 2; --i) {  // lags M..2, oldest first
         const int r = (U - i + 2 * M) % M;
         const float na = -a[i - 1];
-        if (((M - i) & 1) && M - i > 1) {
-            d0 = fmaf(na, R0[r], d0);
-            d1 = fmaf(na, R1[r], d1);
-            d2 = fmaf(na, R2[r], d2);
-        } else if ((M - i) & 1) {
-            d0 = na * R0[r];
-            d1 = na * R1[r];
-            d2 = na * R2[r];
-        } else {
-            c0 = fmaf(na, R0[r], c0);
-            c1 = fmaf(na, R1[r], c1);
-            c2 = fmaf(na, R2[r], c2);
-        }
-    }
-    if constexpr (M > 2) {
-        c0 += d0;
-        c1 += d1;
-        c2 += d2;
-    }
-#else
 #pragma unroll
-    for (int i = M; i >= 2; --i) {  // lags M..2, oldest first
-        const int r = (U - i + 2 * M) % M;
-        const float na = -a[i - 1];
-        c0 = fmaf(na, R0[r], c0);
-        c1 = fmaf(na, R1[r], c1);
-        c2 = fmaf(na, R2[r], c2);
+        for (int j = 0; j < kChains; ++j) c[j] = fmaf(na, R[j][r], c[j]);
     }
-#endif
     const int r1 = (U - 1 + M) % M;
-    R0[U % M] = fmaf(-a[0], R0[r1], c0);
-    R1[U % M] = fmaf(-a[0], R1[r1], c1);
-    R2[U % M] = fmaf(-a[0], R2[r1], c2);
+#pragma unroll
+    for (int j = 0; j < kChains; ++j) R[j][U % M] = fmaf(-a[0], R[j][r1], c[j]);
 }
 template <int M, bool TI, int G, int... V>
-__device__ __forceinline__ void basis4_group(std::integer_sequence<int, V...>, float (&R0)[M],
-                                             float (&R1)[M], float (&R2)[M],
+__device__ __forceinline__ void basis4_group(std::integer_sequence<int, V...>,
+                                             float (&R)[kChains][M],
                                              const float* __restrict__ Ar,
                                              const float* __restrict__ es, const float (&ati)[M],
                                              float (&ac)[M], int zs) {
     ((G * kBasisGroup + V < M
-          ? basis4_step<M, TI, (G * kBasisGroup + V) % M>(R0, R1, R2, Ar, es, ati, ac, zs)
+          ? basis4_step<M, TI, (G * kBasisGroup + V) % M>(R, Ar, es, ati, ac, zs)
           : void()),
      ...);
 }
 template <int M, bool TI, int... G>
-__device__ __forceinline__ void basis4_full(std::integer_sequence<int, G...>, float (&R0)[M],
-                                            float (&R1)[M], float (&R2)[M],
+__device__ __forceinline__ void basis4_full(std::integer_sequence<int, G...>,
+                                            float (&R)[kChains][M],
                                             const float* __restrict__ Ar,
                                             const float* __restrict__ es, const float (&ati)[M],
                                             float (&ac)[M], int zs, int lim) {
     if constexpr (TI) {
         // no row loads to keep in place: one straight-line window
-        (basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R0, R1, R2, Ar, es,
-                                ati, ac, zs),
+        (basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R, Ar, es, ati, ac,
+                                zs),
          ...);
     } else {
         ((G * kBasisGroup < lim
-              ? basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R0, R1, R2,
-                                       Ar, es, ati, ac, zs)
+              ? basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R, Ar, es,
+                                       ati, ac, zs)
               : void()),
          ...);
     }
 }
 template <int M, bool TI, int... U>
-__device__ __forceinline__ void basis4_partial(std::integer_sequence<int, U...>, float (&R0)[M],
-                                               float (&R1)[M], float (&R2)[M],
+__device__ __forceinline__ void basis4_partial(std::integer_sequence<int, U...>,
+                                               float (&R)[kChains][M],
                                                const float* __restrict__ Ar,
                                                const float* __restrict__ es,
                                                const float (&ati)[M], float (&ac)[M], int zs,
                                                int u0) {
-    ((U >= u0 ? basis4_step<M, TI, U>(R0, R1, R2, Ar, es, ati, ac, zs) : void()), ...);
+    ((U >= u0 ? basis4_step<M, TI, U>(R, Ar, es, ati, ac, zs) : void()), ...);
 }
 
 template <int M, bool TI, bool FR = false>
@@ -501,16 +474,15 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
 #pragma unroll
         for (int i = 0; i < M; ++i) ati[i] = A[b * M + i];
     }
-    const int c0 = 3 * q;  // chains c0, c0+1, c0+2 (chain M is the zero-state chain)
-    const int zs = M - c0;  // which of the three is the zero-state chain (0..2), if any
-    float R0[M], R1[M], R2[M];
+    const int c0 = kChains * q;  // chains c0 .. c0+kChains-1 (chain M: the zero-state chain)
+    const int zs = M - c0;       // which of the lane's chains is the zero-state one, if any
+    float R[kChains][M];
     float ac[M];  // coefficient row of the next step (pipelined loads)
 #pragma unroll
     for (int p = 0; p < M; ++p) {
         const int c = ((u0 - 1 - p) % M + M) % M;  // state component held at ring position p
-        R0[p] = c == c0 ? 1.f : 0.f;
-        R1[p] = c == c0 + 1 ? 1.f : 0.f;
-        R2[p] = c == c0 + 2 ? 1.f : 0.f;
+#pragma unroll
+        for (int j = 0; j < kChains; ++j) R[j][p] = c == c0 + j ? 1.f : 0.f;
     }
 
     const float inv_hop = FR ? 1.f / (float)fs.hop : 0.f;
@@ -537,11 +509,10 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
             load_row_at<float, M>(Ar + first * M, ac, first * M * 4);
         }
         if (k == 0 && u0 != 0)
-            basis4_partial<M, TI>(std::make_integer_sequence<int, M>{}, R0, R1, R2, Ar, es, ati, ac,
-                                  zs, u0);
+            basis4_partial<M, TI>(std::make_integer_sequence<int, M>{}, R, Ar, es, ati, ac, zs, u0);
         else
             basis4_full<M, TI>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
-                               R0, R1, R2, Ar, es, ati, ac, zs, len);
+                               R, Ar, es, ati, ac, zs, len);
         __syncwarp();  // the warp is done with stage st (generic reads before the async refill
                        // are ordered by this sync; no proxy fence is needed for WAR)
         issue(k + NSTB);
@@ -558,13 +529,12 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
     if (lane_used) {
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            const float v[3] = {R0[M - 1 - i], R1[M - 1 - i], R2[M - 1 - i]};
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-                if (c0 + c <= M) buf[(c0 + c) * MP4 + i] = v[c];  // W column c0+c / z row
+            for (int c = 0; c < kChains; ++c)
+                if (c0 + c <= M) buf[(c0 + c) * MP4 + i] = R[c][M - 1 - i];  // W column / z row
         }
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
+        for (int c = 0; c < kChains; ++c)
             if (c0 + c <= M)
                 for (int i = M; i < MP4; ++i) buf[(c0 + c) * MP4 + i] = 0.f;
     }
@@ -579,12 +549,11 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
     if (lane_used) {
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            const float v[3] = {R0[M - 1 - i], R1[M - 1 - i], R2[M - 1 - i]};
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-                if (c0 + c < M) buf[i * MP4 + c0 + c] = v[c];  // R row i
+            for (int c = 0; c < kChains; ++c)
+                if (c0 + c < M) buf[i * MP4 + c0 + c] = R[c][M - 1 - i];  // R row i
         }
-        if (zs >= 0 && zs < 3)  // the zero-state lane pads the R rows
+        if (zs >= 0 && zs < kChains)  // the zero-state lane pads the R rows
             for (int i = 0; i < M; ++i)
                 for (int c = M; c < MP4; ++c) buf[i * MP4 + c] = 0.f;
     }
