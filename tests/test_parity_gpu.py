@@ -594,3 +594,25 @@ def test_backward_ex_grad_zi_matches_gradcheck():
         sm = _np(lpc.lp_forward_tv(et, At, _cuda(zm)))
         fd[i] = np.sum(g * (sp - sm)) / (2 * h)
     np.testing.assert_allclose(_np(nu)[0], fd, rtol=1e-6, atol=1e-8)
+
+
+def test_long_sequence_frames_and_ti():
+    """Long single sequences through the frame-rate path (hierarchical carries
+    on the frames plan) and the TI path."""
+    T1 = 1_440_001
+    e, fr, g = data.d1_frames_batch(5, 1, T1, 22, 240)
+    et, ft, gt = _cuda(e), _cuda(fr), _cuda(g)
+    s, carry = lpc.lp_forward_tv_frames(et, ft, 240, return_carry=True)
+    ge, gf = lpc.lp_backward_tv_frames(gt, ft, 240, s, carry=carry)
+    rs, rge, rgf = oracle.lp_tv_frames_fwd_bwd(e[0].astype(np.float64), fr[0].astype(np.float64),
+                                               240, g[0].astype(np.float64))
+    errs = (_err(_np(s)[0], rs), _err(_np(ge)[0], rge), _err(_np(gf)[0], rgf))
+    assert max(errs) < 1e-5, errs
+    a = np.ascontiguousarray(fr[:, 100, :])
+    at = _cuda(a)
+    s = lpc.lp_forward_ti(et, at)
+    ge, ga = lpc.lp_backward_ti(gt, at, s)
+    rs = oracle.lp_forward_ti(e[0].astype(np.float64), a[0].astype(np.float64))
+    rge, rga = oracle.lp_backward_ti(g[0].astype(np.float64), a[0].astype(np.float64), rs)
+    errs = (_err(_np(s)[0], rs), _err(_np(ge)[0], rge), _err(_np(ga)[0], rga))
+    assert max(errs) < 1e-5, errs
