@@ -40,7 +40,7 @@ constexpr size_t kFwStageMax = 200 * 1024;
 template <typename IO, bool DIV>
 __device__ __forceinline__ void stage_span(IO* __restrict__ dst, const IO* __restrict__ src,
                                            int64_t t0, int64_t n, int64_t n_src, IO div) {
-    constexpr int U = 16;
+    constexpr int U = 64;  // loads in flight per lane (staging is latency-bound)
     const int lane = threadIdx.x & 31;
     for (int64_t i0 = lane; i0 < n; i0 += 32 * U) {
         IO v[U];
