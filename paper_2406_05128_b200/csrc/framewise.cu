@@ -13,12 +13,16 @@
 #include "common.cuh"
 #include "framewise_launch.cuh"
 
+#ifndef TVLP_FW_PREFETCH
+#define TVLP_FW_PREFETCH 16
+#endif
+
 namespace tvlp {
 
 template <int M>
 struct FwGeo {
     static constexpr int L = clcm(M, 4);  // unrolled body; ring positions static
-    static constexpr int RS = (M + 16 + 3) / 4 * 4;  // backward ring: M live + prefetch slots
+    static constexpr int RS = (M + TVLP_FW_PREFETCH + 3) / 4 * 4;  // backward ring: M live + prefetch slots
 };
 
 // One warp = 32 consecutive frames of one sequence (grid: B x ceil(nfr/32),
