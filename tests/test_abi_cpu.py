@@ -68,3 +68,47 @@ def test_frameplan_host_logic():
         bad.validate_cola()
     with pytest.raises(ValueError, match="non-integer"):
         FramePlan.raised_cosine(7, overlap=0.7)
+
+
+def test_abi_queries_frames_and_split():
+    """Workspace/carry queries of the frame-rate pair and the time-split
+    helpers (no kernel launches)."""
+    lib = N.load()
+    B, T, M, hop = 64, 48000, 22, 240
+    F = (T - 1) // hop + 1
+    assert lib.tvlp_workspace_bytes(N.OP_FWD_TV_FRAMES, 0, B, T, M, F, 0, hop) > 0
+    assert lib.tvlp_workspace_bytes(N.OP_BWD_TV_FRAMES, 0, B, T, M, F, 0, hop) > 0
+    assert lib.tvlp_workspace_bytes(N.OP_FWD_TV_FRAMES, 0, B, T, M, F + 1, 0, hop) == 0  # bad F
+    # the frames plan uses shorter sub-chunks: more tapes than the A-track plan
+    assert lib.tvlp_carry_elems_frames(B, T, M) > lib.tvlp_carry_elems(B, T, M)
+    assert lib.tvlp_workspace_bytes(N.OP_BWD_TV_EX, 0, B, T, M, 0, 0, 0) >= \
+        lib.tvlp_workspace_bytes(N.OP_BWD_TV, 0, B, T, M, 0, 0, 0)
+    assert lib.tvlp_workspace_bytes(N.OP_SEGMENT_TRANSITION, 0, 1, 14_400_000, M, 0, 0, 0) > 0
+    # null pointers are rejected before any launch
+    assert lib.tvlp_reflection_to_lpc(0, None, None, 4, 3, None, None) == 1
+    assert lib.tvlp_segment_transition(0, None, 1, 100, 3, None, None, 0, None) == 1
+
+
+def test_longseq_combine_algebra():
+    """The fold of the time split on small matrices (CPU torch): forward
+    states and backward adjoints against a direct composition."""
+    import torch
+
+    from paper_2406_05128_b200 import longseq
+
+    g = torch.Generator().manual_seed(0)
+    R, B, M = 4, 2, 3
+    Phis = [torch.randn(B, M, M, generator=g, dtype=torch.float64) * 0.5 for _ in range(R)]
+    zs = [torch.randn(B, M, generator=g, dtype=torch.float64) for _ in range(R)]
+    nus = [torch.randn(B, M, generator=g, dtype=torch.float64) for _ in range(R)]
+    assert longseq.forward_combine(0, Phis, zs) is None
+    x = zs[0]
+    for r in range(1, R):
+        got = longseq.forward_combine(r, Phis, zs)
+        assert torch.allclose(got, x)
+        x = torch.bmm(Phis[r], x.unsqueeze(-1)).squeeze(-1) + zs[r]
+    assert longseq.backward_combine(R - 1, Phis, nus) is None
+    mu = nus[R - 1]
+    for r in range(R - 2, -1, -1):
+        assert torch.allclose(longseq.backward_combine(r, Phis, nus), mu)
+        mu = nus[r] + torch.bmm(Phis[r].transpose(1, 2), mu.unsqueeze(-1)).squeeze(-1)
