@@ -73,11 +73,30 @@ def _host(x, dtype=None):
     return x.contiguous() if dtype is None else x.to(dtype).contiguous()
 
 
+def schedule(B, n=8):
+    """Default chunk sizes: n equal chunks (at least one sequence each)."""
+    n = max(1, min(B, n))
+    return [B * (i + 1) // n - B * i // n for i in range(n)]
+
+
+def _bounds(B, chunks):
+    sizes = schedule(B) if chunks is None else \
+        schedule(B, chunks) if isinstance(chunks, int) else [int(c) for c in chunks]
+    if sum(sizes) != B or min(sizes) < 1:
+        raise ValueError(f"chunk sizes {sizes} must be positive and sum to B={B}")
+    out, lo = [], 0
+    for c in sizes:
+        out.append((lo, lo + c))
+        lo += c
+    return out
+
+
 def lp_tv_fwd_bwd_host(e, A, grad_s, zi=None, *, chunks=None, out=None, device=None):
     """s = LP(e, A) and its VJP (grad_e, grad_A) for grad_s, batch-pipelined.
 
-    ``chunks``: number of batch chunks (default: up to 8, at least one
-    sequence each).  ``out``: optional (s, grad_e, grad_A) host tensors."""
+    ``chunks``: number of equal batch chunks, or a sequence of chunk sizes
+    (sequences per chunk, summing to B); default :func:`schedule`.
+    ``out``: optional (s, grad_e, grad_A) host tensors."""
     e = _host(e)
     A = _host(A, e.dtype)
     grad_s = _host(grad_s, e.dtype)
@@ -92,8 +111,7 @@ def lp_tv_fwd_bwd_host(e, A, grad_s, zi=None, *, chunks=None, out=None, device=N
                torch.empty_like(A, pin_memory=pin))
     s_h, ge_h, gA_h = out
     zi_h = None if zi is None else _host(zi, e.dtype)
-    n = max(1, min(B, chunks or 8))
-    bounds = [(B * i // n, B * (i + 1) // n) for i in range(n)]
+    bounds = _bounds(B, chunks)
     bufs = _buffers(dev, e.shape[0], e.shape[1], A.shape[2], e.dtype, max(h - l for l, h in bounds),
                     zi_h is not None)
     lib = N.load()

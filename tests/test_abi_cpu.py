@@ -112,3 +112,14 @@ def test_longseq_combine_algebra():
     for r in range(R - 2, -1, -1):
         assert torch.allclose(longseq.backward_combine(r, Phis, nus), mu)
         mu = nus[r] + torch.bmm(Phis[r].transpose(1, 2), mu.unsqueeze(-1)).squeeze(-1)
+
+
+def test_host_pipeline_chunk_schedule():
+    from paper_2406_05128_b200 import stream
+
+    assert stream._bounds(64, None) == [(8 * i, 8 * i + 8) for i in range(8)]
+    assert stream._bounds(5, 8) == [(i, i + 1) for i in range(5)]  # at least one sequence each
+    assert stream._bounds(10, [2, 8]) == [(0, 2), (2, 10)]
+    for bad in ([3, 3], [0, 10], [11, -1]):
+        with pytest.raises(ValueError):
+            stream._bounds(10, bad)
