@@ -54,7 +54,10 @@ constexpr int kLaneWin = TVLP_LANE_WIN;  // rows per TMA window in the lane-per-
 #define TVLP_LANE_STAGES 3
 #endif
 constexpr int kLaneStages = TVLP_LANE_STAGES;  // input stages (per warp)
-constexpr int kOutStages = 2;   // output staging slots
+constexpr int kOutStages = 2;
+#ifndef TVLP_GRAD_A_VEC
+#define TVLP_GRAD_A_VEC 1
+#endif   // output staging slots
 
 template <int M>
 struct Geo {
@@ -1429,10 +1432,26 @@ k_grad_A(const IO* __restrict__ ge, const IO* __restrict__ s, const IO* __restri
     __syncthreads();
     IO* out = gA + (b * T + tlo) * M;
     const int n = rows * M;
-    for (int idx = threadIdx.x; idx < n; idx += 256) {
-        const int r = idx / M;
-        const int c = idx - r * M;
-        out[idx] = (-sh_g[r]) * sh_s[M + r - c - 1];
+    if constexpr (sizeof(IO) == 4 && TVLP_GRAD_A_VEC) {
+        // 16-byte stores: the block's output span starts 16B-aligned
+        // (T % 4 == 0 and RT * M * 4 % 16 == 0); rows*M % 4 == 0 as rows % 4 == 0
+        for (int q = threadIdx.x * 4; q < n; q += 256 * 4) {
+            float r4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int idx = q + e;
+                const int r = idx / M;
+                const int c = idx - r * M;
+                r4[e] = (-sh_g[r]) * sh_s[M + r - c - 1];
+            }
+            *reinterpret_cast<float4*>(out + q) = make_float4(r4[0], r4[1], r4[2], r4[3]);
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < n; idx += 256) {
+            const int r = idx / M;
+            const int c = idx - r * M;
+            out[idx] = (-sh_g[r]) * sh_s[M + r - c - 1];
+        }
     }
 }
 
