@@ -376,22 +376,28 @@ def test_framewise_single_rect_frame_equals_ti(rng):  # test_params.py:123-128
     np.testing.assert_array_equal(out, lpc.lp_forward_ti(e, a[0]))
 
 
-def test_host_pipeline_matches_device_path():
+@pytest.mark.parametrize("chunks,with_zi", [(4, False), ([1, 2, 3], True), (1, False),
+                                            ([5, 1], True)])
+def test_host_pipeline_matches_device_path(chunks, with_zi):
     """stream.lp_tv_fwd_bwd_host (chunked, multi-stream, host buffers) gives
     bit-identical results to the one-shot device path: sequences are
-    independent, so chunking the batch changes nothing."""
+    independent, so chunking the batch changes nothing (whatever the copy
+    grouping of the per-sequence signals)."""
     from paper_2406_05128_b200 import stream
 
     e, A, g = data.d1_batch(40, 6, 24000)
+    zi = np.random.default_rng(3).standard_normal((6, A.shape[-1])).astype(np.float32) * 0.1 \
+        if with_zi else None
     eh, Ah, gh = (torch.from_numpy(x).pin_memory() for x in (e, A, g))
-    s_h, ge_h, gA_h = stream.lp_tv_fwd_bwd_host(eh, Ah, gh, chunks=4)
-    torch.cuda.synchronize()
-    s, carry = lpc._forward(False, _cuda(e), _cuda(A), None, return_carry=True)
-    ge, gA = lpc._backward(False, _cuda(g), _cuda(A), s, None, carry)
+    s_h, ge_h, gA_h = stream.lp_tv_fwd_bwd_host(
+        eh, Ah, gh, None if zi is None else torch.from_numpy(zi), chunks=chunks)
+    zd = None if zi is None else _cuda(zi)
+    s, carry = lpc._forward(False, _cuda(e), _cuda(A), zd, return_carry=True)
+    ge, gA = lpc._backward(False, _cuda(g), _cuda(A), s, zd, carry)
     np.testing.assert_array_equal(s_h.numpy(), _np(s))
     np.testing.assert_array_equal(ge_h.numpy(), _np(ge))
     np.testing.assert_array_equal(gA_h.numpy(), _np(gA))
-    rs = oracle.lp_forward_tv(e[0], A[0])
+    rs = oracle.lp_forward_tv(e[0], A[0], None if zi is None else zi[0])
     assert oracle.gradcheck_error(s_h.numpy()[0], rs) < 1e-4
 
 
