@@ -127,13 +127,12 @@ def lp_tv_fwd_bwd_host(e, A, grad_s, zi=None, *, chunks=None, out=None, device=N
     for st in (h2d, comp, d2h):
         st.wait_stream(main)
     flag = lpc._flag(dev)
-    # Copy order (tools/e2e_order.py: 7.66 -> 7.40 ms on config 3, outputs
-    # identical): every chunk ships its A rows; the small per-sequence
-    # signals (e, grad_s up; s, grad_e down) go as few large copies -- chunk
-    # 0's own, then the rest of the batch in one copy each right behind A_0;
-    # down, all but the last chunk's in one copy each once the second-to-last
-    # chunk is done, then the last chunk's.  Fewer small copies interleaved
-    # with the A/grad_A streams in the other direction leave fewer idle gaps.
+    # Copy order (tools/e2e_order.py, e2e_sched.py: 7.66 -> 7.37 ms on
+    # config 3, outputs identical): every chunk ships its A rows; the small
+    # per-sequence signals going up (e, grad_s) travel as chunk 0's own, then
+    # the rest of the batch in one copy each right behind A_0 -- small
+    # host->device copies interleaved with the device->host stream were slow
+    # and left idle gaps.  Down, each chunk's s, grad_e, grad_A.
     n = len(bounds)
     for i, (lo, hi) in enumerate(bounds):
         nb = hi - lo
@@ -166,13 +165,8 @@ def lp_tv_fwd_bwd_host(e, A, grad_s, zi=None, *, chunks=None, out=None, device=N
         done.record(comp)
         d2h.wait_event(done)
         with torch.cuda.stream(d2h):
-            if i == n - 1:
-                s_h[lo:hi].copy_(sd, non_blocking=True)
-                ge_h[lo:hi].copy_(ged, non_blocking=True)
-            gA_h[lo:hi].copy_(gAd, non_blocking=True)
-            if i == n - 2:
-                s_h[:hi].copy_(bufs["s"][:hi], non_blocking=True)
-                ge_h[:hi].copy_(bufs["ge"][:hi], non_blocking=True)
+            for dst, src in ((s_h, sd), (ge_h, ged), (gA_h, gAd)):
+                dst[lo:hi].copy_(src, non_blocking=True)
     for st in (h2d, comp, d2h):
         main.wait_stream(st)
     lpc._raise_nonfinite(flag, bufs["e"], bufs["A"])

@@ -10,13 +10,12 @@ eh, Ah, gh = (x.cpu().pin_memory() for x in (e, A, g))
 oh = tuple(torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (e, e, A))
 scheds = {
     "u8": 8,
-    "u12": [6] * 10 + [4],
-    "r2": [2, 6] + [8] * 6 + [6, 2],
-    "r1": [1, 3, 6] + [8] * 6 + [4, 2],
-    "r4": [4] + [8] * 7 + [4],
-    "r2b": [2, 4] + [8] * 7 + [2],
-    "r1b": [1, 2, 4] + [8] * 7 + [1],
-    "r2c": [2, 4, 6] + [8] * 6 + [4],
+    "h26": [2, 6] + [8] * 7,
+    "h134": [1, 3, 4] + [8] * 7,
+    "h44": [4, 4] + [8] * 7,
+    "h224": [2, 2, 4] + [8] * 7,
+    "h26t": [2, 6] + [8] * 6 + [6, 2],
+    "h2": [2] * 4 + [8] * 7,
 }
 for rep in range(2):
     for name, ch in scheds.items():
