@@ -206,7 +206,20 @@ __device__ __forceinline__ bool is_finite_val(T x) {
 // kernel in the stream; griddepcontrol.wait then blocks until that kernel has
 // completed and its writes are visible.  Kernels call it before touching
 // global memory.  Without the launch attribute the wait is a no-op.
-__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// TVLP_PDL_TRIGGER=1 also triggers the dependent right after the wait
+// (griddepcontrol.launch_dependents), so the next kernel's CTAs park in their
+// own wait on the SMs this grid's finished CTAs free.  Measured slower on
+// every config (config 3: 340 -> 352 us, config 1: 138 -> 166 us): the parked
+// CTAs hold SM slots through this grid's tail.  Off by default.
+#ifndef TVLP_PDL_TRIGGER
+#define TVLP_PDL_TRIGGER 0
+#endif
+__device__ __forceinline__ void grid_dep_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#if TVLP_PDL_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+#endif
+}
 
 inline bool pdl_enabled() {
     static const bool on = [] {
