@@ -148,6 +148,9 @@ int env_int(const char* name, int dflt) {
 // the group length of the hierarchical scheme
 const int kSerialMax = env_int("TVLP_CARRY_SERIAL_MAX", 256);
 const int kGroup = env_int("TVLP_CARRY_GROUP", 32);
+// single-level "auto" refinement folded into the re-apply launch (1) or as a
+// separate per-sequence refine kernel before it (0)
+const int kFusedRefine = env_int("TVLP_FUSED_REFINE", 1);
 struct Levels {
     int L = 1;
     int64_t n[8] = {};
@@ -506,7 +509,17 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     TVLP_RUN("apply_fwd", 1, st,
              (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nonfinite, xend, dstat, nullptr, g,
                                    st, frk)));
-    if (refine) {
+    if (refine && !hier && kFusedRefine) {
+        // flagged sequences: correction recurrence + re-apply in one launch
+        RefineSrc<IO> rf;
+        rf.tape = phiz;
+        rf.K = xend;
+        rf.dstat = dstat;
+        rf.flags = flags;
+        TVLP_RUN("apply_fwd_refined", 1, st,
+                 (launch_apply_fwd<IO>(p.Mp, ti, e_p, A_p, xin, s_p, nullptr, nullptr, nullptr,
+                                       nullptr, g, st, frk, &rf)));
+    } else if (refine) {
         if (!hier) {
             TVLP_RUN("refine_fwd", 1, st,
                      (launch_refine<IO>(p.Mp, true, phiz, xin, xend, dstat, flags, nullptr, g, st)));
@@ -659,7 +672,17 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     TVLP_RUN("adjoint_apply", 1, st,
              (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, kout, ge_p, dstat, nullptr, g, st,
                                  frk)));
-    if (refine) {
+    if (refine && !hier && kFusedRefine && !grad_zi) {
+        // (grad_zi re-writes the carry-outs the recurrence reads: separate kernels)
+        RefineSrc<IO> rf;
+        rf.tape = h.tape;
+        rf.K = kout;
+        rf.dstat = dstat;
+        rf.inherit = carry ? reinterpret_cast<const int*>(carry + tape_body(p)) : nullptr;
+        TVLP_RUN("adjoint_apply_refined", 1, st,
+                 (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, nullptr, ge_p, nullptr, nullptr,
+                                     g, st, frk, &rf)));
+    } else if (refine) {
         const int* inherit = carry ? reinterpret_cast<const int*>(carry + tape_body(p)) : nullptr;
         if (!hier) {
             TVLP_RUN("refine_bwd", 1, st,

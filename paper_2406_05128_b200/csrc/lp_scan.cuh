@@ -961,6 +961,91 @@ struct LaneMaps {
     CUtensorMap O;  // [B*nsub, Ls]   box {W, 32}      (s or g_e)
 };
 
+// ---------------------------------------------------------------- fused refinement
+constexpr float kDefectTol = 2e-5f;     // forward: relative to max |x| (samples of s)
+constexpr float kDefectTolBwd = 2e-5f;  // adjoint: relative to max |lambda_0| (= |grad_e|)
+
+static __device__ unsigned long long g_refined_sequences = 0;  // launched from scan_kernels.cu only
+
+
+// Prologue of the fused re-apply: for every flagged sequence among the warp's
+// 32 sub-chunks the warp runs the correction recurrence of k_refine_fwd/bwd
+// (same arithmetic, same order) up to its own sub-chunks and hands each lane
+// the correction of its carry-in state.  Returns false when no sequence of the
+// warp is flagged (the warp then exits: its first-pass outputs stand).  sm:
+// 32 + 32 M scratch values (the idle stage memory).
+template <int M, typename CT>
+__device__ bool refine_prologue(const RefineSrc<CT>& rf, bool fwd, const CT* __restrict__ X,
+                                const ScanArgs& g, int64_t g0, CT* sm, CT (&corr)[M]) {
+    using TP = Tape<M>;
+    constexpr int MP4 = TP::MP4;
+    const int lane = threadIdx.x & 31;
+    const int64_t nsc = g.B * g.nsub;
+    const int64_t glast = (g0 + 31 < nsc ? g0 + 31 : nsc - 1);
+    const int64_t b0 = g0 / g.nsub, b1 = glast / g.nsub;
+    CT* es = sm;
+    CT* E = sm + 32;  // E[lane][i]: correction of the lane's carry-in state
+#pragma unroll
+    for (int i = 0; i < M; ++i) E[lane * M + i] = (CT)0;
+    __syncwarp();
+    bool any = false;
+    const int r = lane < M ? lane : 0;
+    for (int64_t b = b0; b <= b1; ++b) {
+        const float dmax = __uint_as_float(rf.dstat[2 * b]);
+        const float xmax = __uint_as_float(rf.dstat[2 * b + 1]);
+        const bool bad = fwd ? dmax > kDefectTol * xmax
+                             : (dmax > kDefectTolBwd * xmax ||
+                                (rf.inherit != nullptr && rf.inherit[b] != 0));
+        if (!bad) continue;
+        any = true;
+        const int64_t base = b * g.nsub;
+        if (lane == 0) {
+            if (fwd && rf.flags != nullptr) rf.flags[b] = 1;
+            if (base >= g0) atomicAdd(&g_refined_sequences, 1ull);  // one warp per sequence
+        }
+        const int jlo = (int)(g0 > base ? g0 - base : 0);
+        const int jhi = (int)(glast - base < g.nsub - 1 ? glast - base : g.nsub - 1);
+        CT e = (CT)0;
+        if (fwd) {
+            for (int j = 0; j < jhi; ++j) {  // e_{j+1} = Phi_j e_j + d_j
+                const CT* t = rf.tape + (base + j) * TP::SIZE;
+                es[lane] = lane < M ? e : (CT)0;
+                __syncwarp();
+                CT w[MP4], ev[MP4];
+                load_vec<CT, MP4>(t + (TP::R_ROW + r) * MP4, w);
+                load_vec<CT, MP4>(es, ev);
+                const CT d = lane < M ? rf.K[(base + j) * MP4 + r] - X[(base + j + 1) * MP4 + r]
+                                      : (CT)0;
+                const CT en = dot_rows<M, CT>(w, ev, d);
+                __syncwarp();
+                e = en;
+                if (j + 1 >= jlo && lane < M) E[(base + j + 1 - g0) * M + lane] = e;
+            }
+        } else {
+            for (int j = g.nsub - 1; j > jlo; --j) {  // e_{j-1} = Phi_j^T e_j + d_j
+                const CT* t = rf.tape + (base + j) * TP::SIZE;
+                es[lane] = lane < M ? e : (CT)0;
+                __syncwarp();
+                CT w[MP4], ev[MP4];
+                load_vec<CT, MP4>(t + r * MP4, w);
+                load_vec<CT, MP4>(es, ev);
+                const CT d = lane < M ? rf.K[(base + j) * MP4 + r] - X[(base + j - 1) * MP4 + r]
+                                      : (CT)0;
+                const CT en = dot_rows<M, CT>(w, ev, d);
+                __syncwarp();
+                e = en;
+                if (j - 1 <= jhi && lane < M) E[(base + j - 1 - g0) * M + lane] = e;
+            }
+        }
+    }
+    if (!any) return false;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < M; ++i) corr[i] = E[lane * M + i];
+    __syncwarp();  // the scratch is stage memory: read out before the first bulk copy
+    return true;
+}
+
 // ---------------------------------------------------------------- apply fwd
 // One lane re-runs the recursion of its sub-chunk from x_in.  The state lives
 // in a register ring of MR = round_up(M, W) slots (slot p holds s at local
@@ -971,9 +1056,12 @@ __global__ void __launch_bounds__(32)
 k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
             const IO* __restrict__ Xin, int* __restrict__ flag, IO* __restrict__ Xend,
             unsigned* __restrict__ dstat, const int* __restrict__ only, ScanArgs g,
-            const FrameSrc<IO> fs) {
+            const FrameSrc<IO> fs, const RefineSrc<IO> rf) {
     grid_dep_wait();
     using S = LaneSmem<IO, M, TI || FR>;
+    // the refinement ("auto") exists for fp32 I/O only
+    static_assert(S::SZ != 4 || (32 + 32 * M) * S::SZ <= kLaneStages * S::STAGE,
+                  "refinement scratch");
     constexpr int W = S::W;
     constexpr int MR = (M + W - 1) / W * W;
     constexpr int WPB = MR / W;
@@ -988,6 +1076,14 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
     // refinement pass: only warps holding a flagged sequence recompute (the
     // others would reproduce their first-pass outputs bit-for-bit)
     if (only != nullptr && !__any_sync(0xffffffffu, active && only[gid / g.nsub] != 0)) return;
+    IO corr[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) corr[i] = (IO)0;
+    if constexpr (sizeof(IO) == 4) {
+        if (rf.tape != nullptr &&
+            !refine_prologue<M, IO>(rf, true, Xin, g, g0, reinterpret_cast<IO*>(smem), corr))
+            return;
+    }
 
     if (lane == 0) {
         if (!TI && !FR) prefetch_tmap(&maps.A);
@@ -1019,7 +1115,8 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 #pragma unroll
     for (int p = 0; p < MR; ++p) R[p] = (IO)0;
 #pragma unroll
-    for (int i = 0; i < M; ++i) R[MR - 1 - i] = active ? Xin[gid * Tape<M>::MP4 + i] : (IO)0;
+    for (int i = 0; i < M; ++i)
+        R[MR - 1 - i] = active ? Xin[gid * Tape<M>::MP4 + i] + corr[i] : (IO)0;
     bool finite = true;
     // frame-rate rows (FR): the lane walks its sub-chunk forward in time
     const int64_t fb_b = active ? gid / g.nsub : 0;
@@ -1094,7 +1191,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
         const unsigned bad = __ballot_sync(0xffffffffu, active && !finite);
         if (bad && lane == 0) atomicOr(flag, 1);
     }
-    if (Xend != nullptr && active) {
+    if (Xend != nullptr && active && rf.tape == nullptr) {
         // end state x[i] = s(t1 - i): the defect check compares it with the
         // carry's x_in of the next sub-chunk
         IO tmp[MR];
@@ -1130,9 +1227,13 @@ template <typename IO, int M, bool TI, int MODE, bool FR = false>
 __global__ void __launch_bounds__(32)
 k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
           const IO* __restrict__ Mu, IO* __restrict__ Nu, unsigned* __restrict__ dstat,
-          const int* __restrict__ only, ScanArgs g, const FrameSrc<IO> fs) {
+          const int* __restrict__ only, ScanArgs g, const FrameSrc<IO> fs,
+          const RefineSrc<IO> rf) {
     grid_dep_wait();
     using S = LaneSmem<IO, M, TI || FR>;
+    // the refinement ("auto") exists for fp32 I/O only
+    static_assert(S::SZ != 4 || (32 + 32 * M) * S::SZ <= kLaneStages * S::STAGE,
+                  "refinement scratch");
     constexpr int W = S::W;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x;
@@ -1143,6 +1244,14 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     const bool active = gid < nsc;
     const int nwin = g.Ls / W;
     if (only != nullptr && !__any_sync(0xffffffffu, active && only[gid / g.nsub] != 0)) return;
+    IO corr[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) corr[i] = (IO)0;
+    if constexpr (MODE == 1 && sizeof(IO) == 4) {
+        if (rf.tape != nullptr &&
+            !refine_prologue<M, IO>(rf, false, Mu, g, g0, reinterpret_cast<IO*>(smem), corr))
+            return;
+    }
 
     if (lane == 0) {
         if (!TI && !FR) prefetch_tmap(&maps.A);
@@ -1174,7 +1283,8 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     }
     IO lam[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) lam[i] = (MODE == 1 && active) ? Mu[gid * Tape<M>::MP4 + i] : (IO)0;
+    for (int i = 0; i < M; ++i)
+        lam[i] = (MODE == 1 && active) ? Mu[gid * Tape<M>::MP4 + i] + corr[i] : (IO)0;
     // frame-rate rows (FR): the lane walks its sub-chunk backward in time
     const int64_t fb_b = active ? gid / g.nsub : 0;
     const IO inv_hop = FR ? (IO)1 / (IO)fs.hop : (IO)0;
@@ -1263,8 +1373,8 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
 // carries are corrected by e_{j+1} = Phi_j e_j + d_j (e_0 = 0, Xin += e): the
 // correction is linear and small, so the fp32 Phi_j (relative error ~1e-5
 // after cancellation) contracts the error by ~1e-4 per pass.
-constexpr float kDefectTol = 2e-5f;     // forward: relative to max |x| (samples of s)
-constexpr float kDefectTolBwd = 2e-5f;  // adjoint: relative to max |lambda_0| (= |grad_e|)
+// (kDefectTol / kDefectTolBwd are defined with the fused refinement prologue
+// above the apply kernels)
 
 template <typename CT>
 __device__ __forceinline__ CT warp_max(CT v) {
@@ -1273,7 +1383,6 @@ __device__ __forceinline__ CT warp_max(CT v) {
     return v;
 }
 
-static __device__ unsigned long long g_refined_sequences = 0;  // launched from scan_kernels.cu only
 
 template <int M, typename CT>
 __global__ void __launch_bounds__(32)

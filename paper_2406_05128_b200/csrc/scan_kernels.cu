@@ -111,7 +111,7 @@ cudaError_t basis4_impl(const float* e, const float* A, float* PhiZ, const ScanA
 template <typename IO, int M, bool TI, bool FR = false>
 cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag, IO* Xend,
                        unsigned* dstat, const int* only, const ScanArgs& g, cudaStream_t st,
-                       const FrameSrc<IO>* fr = nullptr) {
+                       const FrameSrc<IO>* fr = nullptr, const RefineSrc<IO>* rf = nullptr) {
     using S = LaneSmem<IO, M, TI || FR>;
     auto k = k_apply_fwd<IO, M, TI, FR>;
     cudaError_t err = ensure_smem(k, S::BYTES);
@@ -121,15 +121,16 @@ cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
     const FrameSrc<IO> fs = fr ? *fr : FrameSrc<IO>{};
+    const RefineSrc<IO> rs = rf ? *rf : RefineSrc<IO>{};
     launch_pdl(k, (unsigned)((nsc + 31) / 32), 32, S::BYTES, st, mp, TI ? A : nullptr, Xin, flag,
-               Xend, dstat, only, g, fs);
+               Xend, dstat, only, g, fs, rs);
     return cudaGetLastError();
 }
 
 template <typename IO, int M, bool TI, int MODE, bool FR = false>
 cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge,
                          unsigned* dstat, const int* only, const ScanArgs& g, cudaStream_t st,
-                         const FrameSrc<IO>* fr = nullptr) {
+                         const FrameSrc<IO>* fr = nullptr, const RefineSrc<IO>* rf = nullptr) {
     using S = LaneSmem<IO, M, TI || FR>;
     auto k = k_adjoint<IO, M, TI, MODE, FR>;
     cudaError_t err = ensure_smem(k, S::BYTES);
@@ -140,8 +141,9 @@ cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge
     if (err != cudaSuccess) return err;
     const int64_t nsc = g.B * g.nsub;
     const FrameSrc<IO> fs = fr ? *fr : FrameSrc<IO>{};
+    const RefineSrc<IO> rs = rf ? *rf : RefineSrc<IO>{};
     launch_pdl(k, (unsigned)((nsc + 31) / 32), 32, S::BYTES, st, mp, TI ? A : nullptr, Mu, Nu,
-               dstat, only, g, fs);
+               dstat, only, g, fs, rs);
     return cudaGetLastError();
 }
 
@@ -295,15 +297,18 @@ cudaError_t launch_refine_helpers(int what, int Mp, const IO* P, const IO* Q, IO
 template <typename IO>
 cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO* Xin, IO* s,
                              int* flag, IO* Xend, unsigned* dstat, const int* only,
-                             const ScanArgs& g, cudaStream_t st, const FrameSrc<IO>* fr) {
+                             const ScanArgs& g, cudaStream_t st, const FrameSrc<IO>* fr,
+                             const RefineSrc<IO>* rf) {
     TVLP_DISPATCH_M(Mp, {
         if constexpr (std::is_same<IO, float>::value) {
             if (fr != nullptr)
                 return apply_impl<IO, M_, false, true>(e, A, Xin, s, flag, Xend, dstat, only, g,
-                                                       st, fr);
+                                                       st, fr, rf);
         }
-        return ti ? apply_impl<IO, M_, true>(e, A, Xin, s, flag, Xend, dstat, only, g, st)
-                  : apply_impl<IO, M_, false>(e, A, Xin, s, flag, Xend, dstat, only, g, st);
+        return ti ? apply_impl<IO, M_, true>(e, A, Xin, s, flag, Xend, dstat, only, g, st,
+                                             nullptr, rf)
+                  : apply_impl<IO, M_, false>(e, A, Xin, s, flag, Xend, dstat, only, g, st,
+                                              nullptr, rf);
     })
 }
 
@@ -325,20 +330,24 @@ cudaError_t launch_refine(int Mp, bool fwd, const IO* tape, IO* X, const IO* Xen
 template <typename IO>
 cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const IO* Mu,
                            IO* Nu, IO* ge, unsigned* dstat, const int* only, const ScanArgs& g,
-                           cudaStream_t st, const FrameSrc<IO>* fr) {
+                           cudaStream_t st, const FrameSrc<IO>* fr, const RefineSrc<IO>* rf) {
     TVLP_DISPATCH_M(Mp, {
         if constexpr (std::is_same<IO, float>::value) {
             if (fr != nullptr)
                 return mode == 0 ? adjoint_impl<IO, M_, false, 0, true>(gs, A, Mu, Nu, ge, dstat,
-                                                                        only, g, st, fr)
+                                                                        only, g, st, fr, rf)
                                  : adjoint_impl<IO, M_, false, 1, true>(gs, A, Mu, Nu, ge, dstat,
-                                                                        only, g, st, fr);
+                                                                        only, g, st, fr, rf);
         }
         if (mode == 0)
-            return ti ? adjoint_impl<IO, M_, true, 0>(gs, A, Mu, Nu, ge, dstat, only, g, st)
-                      : adjoint_impl<IO, M_, false, 0>(gs, A, Mu, Nu, ge, dstat, only, g, st);
-        return ti ? adjoint_impl<IO, M_, true, 1>(gs, A, Mu, Nu, ge, dstat, only, g, st)
-                  : adjoint_impl<IO, M_, false, 1>(gs, A, Mu, Nu, ge, dstat, only, g, st);
+            return ti ? adjoint_impl<IO, M_, true, 0>(gs, A, Mu, Nu, ge, dstat, only, g, st,
+                                                      nullptr, rf)
+                      : adjoint_impl<IO, M_, false, 0>(gs, A, Mu, Nu, ge, dstat, only, g, st,
+                                                       nullptr, rf);
+        return ti ? adjoint_impl<IO, M_, true, 1>(gs, A, Mu, Nu, ge, dstat, only, g, st, nullptr,
+                                                  rf)
+                  : adjoint_impl<IO, M_, false, 1>(gs, A, Mu, Nu, ge, dstat, only, g, st, nullptr,
+                                                   rf);
     })
 }
 
@@ -400,10 +409,12 @@ cudaError_t launch_grad_a(int M, const IO* ge, const IO* s, const IO* zi, IO* pa
                                                    const int*, float, int64_t, cudaStream_t);    \
     template cudaError_t launch_apply_fwd<IO>(int, bool, const IO*, const IO*, const IO*, IO*,   \
                                               int*, IO*, unsigned*, const int*, const ScanArgs&, \
-                                              cudaStream_t, const FrameSrc<IO>*);                \
+                                              cudaStream_t, const FrameSrc<IO>*,                 \
+                                              const RefineSrc<IO>*);                             \
     template cudaError_t launch_adjoint<IO>(int, bool, int, const IO*, const IO*, const IO*,     \
                                             IO*, IO*, unsigned*, const int*, const ScanArgs&,    \
-                                            cudaStream_t, const FrameSrc<IO>*);                  \
+                                            cudaStream_t, const FrameSrc<IO>*,                   \
+                                            const RefineSrc<IO>*);                               \
     template cudaError_t launch_refine<IO>(int, bool, const IO*, IO*, const IO*,                 \
                                            const unsigned*, int*, const int*, const ScanArgs&,   \
                                            cudaStream_t);                                        \

@@ -21,6 +21,18 @@ struct FrameSrc {
     int Mf;
 };
 
+// Inputs of the refinement folded into the re-apply launch (precision "auto",
+// single-level carries; see k_refine_fwd/bwd below for the recurrence).  With
+// tape == nullptr the lane kernels run unchanged.
+template <typename CT>
+struct RefineSrc {
+    const CT* tape = nullptr;        // carry tape (Phi_j rows/columns)
+    const CT* K = nullptr;           // fwd: Xend (apply's end states); bwd: the carry-outs
+    const unsigned* dstat = nullptr; // per-sequence defect statistics of the first pass
+    int* flags = nullptr;            // fwd: forward refinement flags (set to 1 when refined)
+    const int* inherit = nullptr;    // bwd: the forward's flags (refine those sequences too)
+};
+
 // Orders with compiled kernels; other orders are zero-padded up to the next
 // one by the C ABI (exact: padded coefficients are 0).
 constexpr int kNumOrders = 9;
@@ -59,11 +71,13 @@ template <typename IO>
 cudaError_t launch_apply_fwd(int Mp, bool ti, const IO* e, const IO* A, const IO* Xin, IO* s,
                              int* flag, IO* Xend, unsigned* dstat, const int* only,
                              const ScanArgs& g, cudaStream_t st,
-                             const FrameSrc<IO>* fr = nullptr);
+                             const FrameSrc<IO>* fr = nullptr,
+                             const RefineSrc<IO>* rf = nullptr);
 template <typename IO>
 cudaError_t launch_adjoint(int Mp, bool ti, int mode, const IO* gs, const IO* A, const IO* Mu,
                            IO* Nu, IO* ge, unsigned* dstat, const int* only, const ScanArgs& g,
-                           cudaStream_t st, const FrameSrc<IO>* fr = nullptr);
+                           cudaStream_t st, const FrameSrc<IO>* fr = nullptr,
+                           const RefineSrc<IO>* rf = nullptr);
 // A[b, t, :] = the frame-rate rows upsampled (params.py:120-132), [B][T][Mp]
 template <typename IO>
 cudaError_t launch_upsample(int Mp, const FrameSrc<IO>& fr, IO* A, int64_t B, int64_t T,

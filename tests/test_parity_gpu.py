@@ -21,6 +21,7 @@ TOL32 = 1e-4   # float32 kernels vs float64 oracle on identical inputs
 TOL64 = 1e-9   # float64 kernels vs float64 reference golden vectors
 
 lpc = pytest.importorskip("paper_2406_05128_b200.lpc")
+from paper_2406_05128_b200 import _native as N  # noqa: E402
 
 
 def _cuda(x):
@@ -240,7 +241,15 @@ def test_config1_d1_and_stress(precision):
     e = np.stack([x[0] for x in items])
     A = np.stack([x[1] for x in items])
     g = np.stack([x[2] for x in items])
+    lib = N.load()
+    r0 = lib.tvlp_refined_sequences()
     _tv_parity(e, A, g, precision=precision)
+    # under 'auto' every resonant item takes the forward refinement pass (fp32
+    # chains alone miss 1e-4 on them; the backward, recomputing its basis
+    # without the forward's tape, refines only what its own check flags); the
+    # fp64 chains never refine
+    n = lib.tvlp_refined_sequences() - r0
+    assert (n >= 4) if precision == "auto" else (n == 0), n
 
 
 def test_stress_mixed_batch_auto():
