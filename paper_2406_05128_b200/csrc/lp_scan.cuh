@@ -1051,7 +1051,7 @@ __device__ bool refine_prologue(const RefineSrc<CT>& rf, bool fwd, const CT* __r
 // in a register ring of MR = round_up(M, W) slots (slot p holds s at local
 // step tau with tau mod MR == p); the unrolled body covers MR/W windows so
 // every ring index is a compile-time constant.
-template <typename IO, int M, bool TI, bool FR = false>
+template <typename IO, int M, bool TI, bool FR = false, bool RF = false>
 __global__ void __launch_bounds__(32)
 k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
             const IO* __restrict__ Xin, int* __restrict__ flag, IO* __restrict__ Xend,
@@ -1060,8 +1060,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
     grid_dep_wait();
     using S = LaneSmem<IO, M, TI || FR>;
     // the refinement ("auto") exists for fp32 I/O only
-    static_assert(S::SZ != 4 || (32 + 32 * M) * S::SZ <= kLaneStages * S::STAGE,
-                  "refinement scratch");
+    static_assert(!RF || (32 + 32 * M) * S::SZ <= kLaneStages * S::STAGE, "refinement scratch");
     constexpr int W = S::W;
     constexpr int MR = (M + W - 1) / W * W;
     constexpr int WPB = MR / W;
@@ -1076,12 +1075,10 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
     // refinement pass: only warps holding a flagged sequence recompute (the
     // others would reproduce their first-pass outputs bit-for-bit)
     if (only != nullptr && !__any_sync(0xffffffffu, active && only[gid / g.nsub] != 0)) return;
+    // RF: the re-apply launch of precision "auto" with the refine step folded in
     IO corr[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) corr[i] = (IO)0;
-    if constexpr (sizeof(IO) == 4) {
-        if (rf.tape != nullptr &&
-            !refine_prologue<M, IO>(rf, true, Xin, g, g0, reinterpret_cast<IO*>(smem), corr))
+    if constexpr (RF) {
+        if (!refine_prologue<M, IO>(rf, true, Xin, g, g0, reinterpret_cast<IO*>(smem), corr))
             return;
     }
 
@@ -1115,8 +1112,12 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 #pragma unroll
     for (int p = 0; p < MR; ++p) R[p] = (IO)0;
 #pragma unroll
-    for (int i = 0; i < M; ++i)
-        R[MR - 1 - i] = active ? Xin[gid * Tape<M>::MP4 + i] + corr[i] : (IO)0;
+    for (int i = 0; i < M; ++i) {
+        if constexpr (RF)
+            R[MR - 1 - i] = active ? Xin[gid * Tape<M>::MP4 + i] + corr[i] : (IO)0;
+        else
+            R[MR - 1 - i] = active ? Xin[gid * Tape<M>::MP4 + i] : (IO)0;
+    }
     bool finite = true;
     // frame-rate rows (FR): the lane walks its sub-chunk forward in time
     const int64_t fb_b = active ? gid / g.nsub : 0;
@@ -1191,7 +1192,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
         const unsigned bad = __ballot_sync(0xffffffffu, active && !finite);
         if (bad && lane == 0) atomicOr(flag, 1);
     }
-    if (Xend != nullptr && active && rf.tape == nullptr) {
+    if (!RF && Xend != nullptr && active) {
         // end state x[i] = s(t1 - i): the defect check compares it with the
         // carry's x_in of the next sub-chunk
         IO tmp[MR];
@@ -1223,7 +1224,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
 // write g_e.  Reverse time; row A[t] is used at step t:
 //   lambda += u0 g_s(t);  g_e(t) = lambda_0;  lambda = C(t)^T lambda.
 // The transposed-state update shifts lambda inside its FMAs (no moves).
-template <typename IO, int M, bool TI, int MODE, bool FR = false>
+template <typename IO, int M, bool TI, int MODE, bool FR = false, bool RF = false>
 __global__ void __launch_bounds__(32)
 k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
           const IO* __restrict__ Mu, IO* __restrict__ Nu, unsigned* __restrict__ dstat,
@@ -1232,8 +1233,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     grid_dep_wait();
     using S = LaneSmem<IO, M, TI || FR>;
     // the refinement ("auto") exists for fp32 I/O only
-    static_assert(S::SZ != 4 || (32 + 32 * M) * S::SZ <= kLaneStages * S::STAGE,
-                  "refinement scratch");
+    static_assert(!RF || (32 + 32 * M) * S::SZ <= kLaneStages * S::STAGE, "refinement scratch");
     constexpr int W = S::W;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x;
@@ -1245,11 +1245,9 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     const int nwin = g.Ls / W;
     if (only != nullptr && !__any_sync(0xffffffffu, active && only[gid / g.nsub] != 0)) return;
     IO corr[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) corr[i] = (IO)0;
-    if constexpr (MODE == 1 && sizeof(IO) == 4) {
-        if (rf.tape != nullptr &&
-            !refine_prologue<M, IO>(rf, false, Mu, g, g0, reinterpret_cast<IO*>(smem), corr))
+    if constexpr (RF) {
+        static_assert(MODE == 1, "the refinement re-applies the adjoint from Mu");
+        if (!refine_prologue<M, IO>(rf, false, Mu, g, g0, reinterpret_cast<IO*>(smem), corr))
             return;
     }
 
@@ -1283,8 +1281,12 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     }
     IO lam[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i)
-        lam[i] = (MODE == 1 && active) ? Mu[gid * Tape<M>::MP4 + i] + corr[i] : (IO)0;
+    for (int i = 0; i < M; ++i) {
+        if constexpr (RF)
+            lam[i] = active ? Mu[gid * Tape<M>::MP4 + i] + corr[i] : (IO)0;
+        else
+            lam[i] = (MODE == 1 && active) ? Mu[gid * Tape<M>::MP4 + i] : (IO)0;
+    }
     // frame-rate rows (FR): the lane walks its sub-chunk backward in time
     const int64_t fb_b = active ? gid / g.nsub : 0;
     const IO inv_hop = FR ? (IO)1 / (IO)fs.hop : (IO)0;

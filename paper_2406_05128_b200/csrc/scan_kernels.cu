@@ -114,6 +114,8 @@ cudaError_t apply_impl(const IO* e, const IO* A, const IO* Xin, IO* s, int* flag
                        const FrameSrc<IO>* fr = nullptr, const RefineSrc<IO>* rf = nullptr) {
     using S = LaneSmem<IO, M, TI || FR>;
     auto k = k_apply_fwd<IO, M, TI, FR>;
+    if constexpr (sizeof(IO) == 4)  // precision "auto" (fp32 I/O only)
+        if (rf != nullptr && rf->tape != nullptr) k = k_apply_fwd<IO, M, TI, FR, true>;
     cudaError_t err = ensure_smem(k, S::BYTES);
     if (err != cudaSuccess) return err;
     LaneMaps mp;
@@ -133,6 +135,8 @@ cudaError_t adjoint_impl(const IO* gs, const IO* A, const IO* Mu, IO* Nu, IO* ge
                          const FrameSrc<IO>* fr = nullptr, const RefineSrc<IO>* rf = nullptr) {
     using S = LaneSmem<IO, M, TI || FR>;
     auto k = k_adjoint<IO, M, TI, MODE, FR>;
+    if constexpr (sizeof(IO) == 4 && MODE == 1)
+        if (rf != nullptr && rf->tape != nullptr) k = k_adjoint<IO, M, TI, MODE, FR, true>;
     cudaError_t err = ensure_smem(k, S::BYTES);
     if (err != cudaSuccess) return err;
     LaneMaps mp;
