@@ -115,9 +115,48 @@ class Clocks:
         self.index = index
         self.rows = []
         self._stop = threading.Event()
+        self.go = threading.Event()  # set by the caller when its timed region starts
         self._t = None
+        self._nvml = self._nvml_handle(index)
+
+    @staticmethod
+    def _nvml_handle(index):
+        """In-process NVML sampling: an nvidia-smi child forked from this
+        process during the timed region can stall the launching thread long
+        enough to drain the GPU queue (step times 345-361 us on one box)."""
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            p = torch.cuda.get_device_properties(index)
+            bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            try:
+                return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                return pynvml, pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            return None
+
+    def _sample_nvml(self):
+        nv, h = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        flags = ["Active" if r & b else "Not Active" for b in bits]
+        self.rows.append([str(self.index), str(sm), str(mx), "", hex(r)] + flags)
 
     def _run(self):
+        self.go.wait(30)
+        if self._nvml is not None:
+            while not self._stop.is_set():
+                try:
+                    self._sample_nvml()
+                except Exception:
+                    self._nvml = None
+                    break
+                self._stop.wait(0.001)
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
@@ -136,6 +175,7 @@ class Clocks:
 
     def __exit__(self, *a):
         self._stop.set()
+        self.go.set()
         self._t.join(timeout=10)
 
     def summary(self):
@@ -313,6 +353,7 @@ def run_b200(args, cfg, rank, world, dist):
     with Clocks(dev.index) as clk:
         barrier()
         ev0.record(stream)
+        clk.go.set()  # the sampler starts with the timed region
         for _ in range(args.steps):
             step()
         ev1.record(stream)
