@@ -258,6 +258,33 @@ def cpu_baseline(cfg, seconds=10.0):
                       f"{len(times)} repeats, {nthreads} threads, oracle/tvlp_oracle.c"}
 
 
+def parity_check(cfg, sample):
+    """Part of the CPU leg (rank 0, outside every timed region): the GPU
+    outputs of the LAST timed step, for the first and last item of this
+    rank's batch, against the float64 oracle on the same float32 inputs,
+    with the reference's metric (oracle.py:228-234).  Returns the max error
+    over the items and outputs checked, so the bench line carries parity
+    evidence at the exact kernel geometry it timed."""
+    import oracle
+
+    kind = cfg["kind"]
+    worst = 0.0
+    for item in sample:
+        x = {k: np.asarray(v, dtype=np.float64) for k, v in item.items()}
+        if kind in ("tv", "hpn", "tvsplit"):
+            rs = oracle.lp_forward_tv(x["e"], x["A"])
+            rge, rgA = oracle.lp_backward_tv(x["g"], x["A"], rs)
+            ref = (rs, rge, rgA)
+        elif kind == "tvf":
+            ref = oracle.lp_tv_frames_fwd_bwd(x["e"], x["A"], cfg["hop"], x["g"])
+        else:
+            ry, rseg = oracle.framewise_forward(x["e"], x["A"], cfg["hop"])
+            ref = (ry,) + tuple(oracle.framewise_backward(x["g"], x["A"], rseg, cfg["hop"]))
+        for got, want in zip((x["o0"], x["o1"], x["o2"]), ref):
+            worst = max(worst, oracle.gradcheck_error(got, want))
+    return worst
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
@@ -364,6 +391,18 @@ def run_b200(args, cfg, rank, world, dist):
     nonfinite_seen = lpc.check_nonfinite(dev)
     samples = B * T * (1 if kind == "tvsplit" else world)
     value = samples / (ms * 1e-3)
+
+    # outputs of one more step for the parity check of the CPU leg (items 0
+    # and B-1 of this rank; the LP rows of an HpN batch are its first items)
+    outs = step()
+    torch.cuda.synchronize()
+    nb = e.shape[0]
+    parity_sample = []
+    for b in sorted({0, nb - 1}):
+        parity_sample.append({"e": e[b].cpu().numpy(), "A": A[b].cpu().numpy(),
+                              "g": g[b].cpu().numpy(), "o0": outs[0][b].cpu().numpy(),
+                              "o1": outs[1][b].cpu().numpy(), "o2": outs[2][b].cpu().numpy()})
+    del outs
 
     # profiling pass: per-kernel CUDA-event durations over K steps
     N.profile_dump()
@@ -472,7 +511,7 @@ def run_b200(args, cfg, rank, world, dist):
         "refined_sequences": int(refined),
         "clocks": clk.summary(),
     }
-    return line
+    return line, parity_sample
 
 
 def run_reference(args, cfg):
@@ -514,8 +553,11 @@ def main(argv=None):
     from paper_2406_05128_b200 import dist as pdist
 
     dist = pdist.init("nccl") if world > 1 else None
-    line = run_b200(args, cfg, rank, world, dist)
+    line, sample = run_b200(args, cfg, rank, world, dist)
     if rank == 0:
+        if not (cfg["kind"] == "tvsplit" and world > 1):  # a rank holds a segment only
+            line["parity_max_err"] = parity_check(cfg, sample)
+            line["parity_items"] = len(sample)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(line), flush=True)

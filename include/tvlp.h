@@ -187,6 +187,10 @@ int64_t tvlp_launch_count(void);
  * refined (precision TVLP_CARRY_AUTO), cumulative; synchronises the device. */
 int64_t tvlp_refined_sequences(void);
 void tvlp_profile_enable(int32_t on);
+/* Diagnostics: a device buffer (NULL = off) that the chained single-pass
+ * kernels fill with one 64-byte timeline record per work item (globaltimer
+ * ns; tools/chain_trace.py decodes it). */
+void tvlp_chain_trace(void* buf, size_t bytes);
 int32_t tvlp_profile_dump(char* buf, int32_t buflen);
 
 #ifdef __cplusplus

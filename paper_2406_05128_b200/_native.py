@@ -64,6 +64,7 @@ _SIGS = [
     ("tvlp_launch_count", _I64, []),
     ("tvlp_refined_sequences", _I64, []),
     ("tvlp_profile_enable", None, [_I32]),
+    ("tvlp_chain_trace", None, [_P, _SZ]),
     ("tvlp_profile_dump", _I32, [ctypes.c_char_p, _I32]),
 ]
 EXPORTS = [name for name, _, _ in _SIGS]

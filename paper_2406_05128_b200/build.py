@@ -21,7 +21,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libtvlp_b200.so")
 OBJDIR = os.path.join(LIBDIR, "obj")
-UNITS = ["scan_kernels.cu", "framewise.cu", "stepup.cu", "capi.cu"]
+UNITS = ["scan_kernels.cu", "chain_kernels.cu", "framewise.cu", "stepup.cu", "capi.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -47,11 +47,34 @@ def up_to_date():
     return all(os.path.getmtime(s) <= t for s in _sources())
 
 
-def build(force=False, verbose=False, jobs=None, defines=(), out=None):
+def _deps(path, seen=None):
+    """The file and the local headers it includes (transitively)."""
+    import re
+
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    with open(path) as fh:
+        for inc in re.findall(r'#include\s+"([^"]+)"', fh.read()):
+            _deps(os.path.normpath(os.path.join(os.path.dirname(path), inc)), seen)
+    return seen
+
+
+def _unit_stale(unit, obj):
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return any(os.path.getmtime(d) > t for d in _deps(os.path.join(CSRC, unit)))
+
+
+def build(force=False, verbose=False, jobs=None, defines=(), out=None, only=None):
     """Compile (if stale) and return the path of libtvlp_b200.so.
 
     ``defines``/``out`` build a tuning variant (extra -D flags) into another
-    path, loaded with TVLP_LIB=<path> (A/B experiments; not the product)."""
+    path, loaded with TVLP_LIB=<path> (A/B experiments; not the product);
+    ``only`` recompiles just those units for the variant and links the
+    product's objects of the others."""
     lib = out or LIB
     objdir = os.path.join(os.path.dirname(lib), "obj") if out else OBJDIR
     if not force and not out and up_to_date():
@@ -63,6 +86,8 @@ def build(force=False, verbose=False, jobs=None, defines=(), out=None):
     def compile_unit(unit):
         src = os.path.join(CSRC, unit)
         obj = os.path.join(objdir, unit.replace(".cu", ".o"))
+        if not force and not out and not _unit_stale(unit, obj):
+            return obj  # object newer than the unit and every header it includes
         cmd = [nvcc, *ARCH, *NVCC_FLAGS, *dflags, "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         log = os.path.join(objdir, unit.replace(".cu", ".log"))
@@ -72,8 +97,10 @@ def build(force=False, verbose=False, jobs=None, defines=(), out=None):
             raise RuntimeError(f"nvcc failed on {unit}:\n{res.stderr[-4000:]}")
         return obj
 
+    units = UNITS if (only is None or not out) else [u for u in UNITS if u in only]
     with ThreadPoolExecutor(max_workers=jobs or len(UNITS)) as ex:
-        objs = list(ex.map(compile_unit, UNITS))
+        built = dict(zip(units, ex.map(compile_unit, units)))
+    objs = [built.get(u) or os.path.join(OBJDIR, u.replace(".cu", ".o")) for u in UNITS]
     tmp = lib + ".tmp"
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -91,8 +118,10 @@ def main(argv=None):
     ap.add_argument("--define", "-D", action="append", default=[],
                     help="extra preprocessor define for a tuning variant")
     ap.add_argument("--out", default=None, help="variant library path (with --define)")
+    ap.add_argument("--only", action="append", default=None,
+                    help="variant: recompile only this unit (repeatable)")
     args = ap.parse_args(argv)
-    build(force=args.force, verbose=True, defines=args.define, out=args.out)
+    build(force=args.force, verbose=True, defines=args.define, out=args.out, only=args.only)
 
 
 if __name__ == "__main__":

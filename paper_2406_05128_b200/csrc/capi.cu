@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/tvlp.h"
+#include "chain_launch.cuh"
 #include "framewise_launch.cuh"
 #include "lp_scan.cuh"
 
@@ -455,7 +456,13 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     // hierarchical chains are always checked: their group products are fp32)
     const bool hier = h.lv.L > 1;
     const bool refine = sizeof(IO) == 4 && (prec == kPrecAuto || hier);
-    IO* xend = refine ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
+    // the chained single-pass forward (chain.cuh): fp32 I/O, sample-rate rows,
+    // one carry level, fp32 chains
+    const bool f32 = std::is_same<IO, float>::value;
+    const bool chain = f32 && !frames && !reuse_tape && !hier &&
+                       (prec == kPrecAuto || prec == kPrecF32Chains) && chain_supported(p.Mp);
+    IO* xend = (refine || (f32 && need) || chain) ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
+    void* ctl = (f32 && (need || chain)) ? c.take(chain_ctl_bytes(p.B, p.nsub, p.Mp)) : nullptr;
     int* fflags = reinterpret_cast<int*>(phiz + tape_body(p));  // flag slots in the carry tape
     int* flags = refine ? fflags : nullptr;
     unsigned* dstat = refine ? static_cast<unsigned*>(c.take(p.B * 2 * sizeof(unsigned))) : nullptr;
@@ -474,12 +481,20 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     }
     // (the sizing pass reserves the materialised rows whatever the precision)
     if (frames && (!native_fr || need)) pA = c.take(p.B * p.Tp * p.Mp * sz);
+    // frames mode does not pack for M != Mp, but the carry reads Mp state
+    // components per row: an initial state of a padded order is zero-padded
+    // into its own buffer (the sizing pass's packed layout already covers it)
+    void* pz_only = (frames && zi && !packed && p.Mp != p.M) ? c.take(p.B * p.Mp * sz) : nullptr;
     if (need) {
         *need = c.used;
         return TVLP_OK;
     }
     if (ws_bytes < c.used) return TVLP_ERR_WORKSPACE;
     const ScanArgs g = scan_args(p);
+    if (pz_only) {
+        TVLP_CK(pack<IO>(zi, pz_only, p.B, 1, p.M, 1, p.Mp, st));
+        zi_p = static_cast<const IO*>(pz_only);
+    }
     if (packed) {
         TVLP_CK(pack<IO>(e, pe, p.B, p.T, 1, p.Tp, 1, st));
         if (!frames) {
@@ -500,6 +515,15 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
         A_p = static_cast<const IO*>(pA);
     }
     const FrameSrc<IO>* frk = native_fr ? fr : nullptr;
+    if constexpr (std::is_same<IO, float>::value) {
+        if (chain) {
+            const ChainFwdCall cc{ti, e_p, A_p, zi_p, p.Mp, s_p, phiz, fflags, xin, xend,
+                                  nonfinite, ctl, prec == kPrecAuto ? 1 : 0, g};
+            TVLP_RUN("fwd_chain", 3, st, (launch_fwd_chain(p.Mp, cc, st)));
+            if (packed) TVLP_CK(unpack<IO>(ps, s, p.B, p.T, 1, p.Tp, 1, st));
+            return TVLP_OK;
+        }
+    }
     const int bprec = (prec == kPrecAuto || prec == kPrecF32Chains) ? prec : kPrecF64Chains;
     if (!reuse_tape) {
         TVLP_RUN("basis", 1, st, (launch_basis<IO>(p.Mp, ti, bprec, e_p, A_p, phiz, g, st, frk)));
@@ -595,7 +619,14 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     // backward recomputes the transition matrices with fp64 chains
     if (carry == nullptr && prec == kPrecAuto) prec = kPrecF64Chains;
     const bool refine = sizeof(IO) == 4 && (prec == kPrecAuto || hier);
-    IO* kout = (refine || grad_zi || need) ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
+    // the chained single-pass adjoint (chain.cuh): fp32, sample-rate rows, one
+    // carry level, the forward's tape, no segment boundary terms
+    const bool f32 = std::is_same<IO, float>::value;
+    const bool chain = f32 && !frames && carry != nullptr && !hier && !mu_in && !grad_zi &&
+                       (prec == kPrecAuto || prec == kPrecF32Chains) && chain_supported(p.Mp);
+    IO* kout = (refine || grad_zi || need || chain) ? static_cast<IO*>(c.take(nsc * mp * sz))
+                                                    : nullptr;
+    void* ctl = (f32 && (need || chain)) ? c.take(chain_ctl_bytes(p.B, p.nsub, p.Mp)) : nullptr;
     IO* mu_in_p = (mu_in || need) ? static_cast<IO*>(c.take(p.B * mp * sz)) : nullptr;
     int* flags = refine ? static_cast<int*>(c.take(p.B * sizeof(int))) : nullptr;
     unsigned* dstat = refine ? static_cast<unsigned*>(c.take(p.B * 2 * sizeof(unsigned))) : nullptr;
@@ -659,6 +690,17 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
                  (launch_basis<IO>(p.Mp, ti, prec, s_p, A_p, phiz_own, g, st, frk)));
         if (hier) TVLP_RUN("compose", h.lv.L - 1, st, (h.compose()));
     }
+    bool chained = false;
+    if constexpr (std::is_same<IO, float>::value) {
+        if (chain) {
+            const int* inherit = reinterpret_cast<const int*>(carry + tape_body(p));
+            const ChainBwdCall cc{ti, gs_p, A_p, ge_p, h.tape, inherit, nu, mu, kout, ctl,
+                                  prec == kPrecAuto ? 1 : 0, g};
+            TVLP_RUN("bwd_chain", 3, st, (launch_bwd_chain(p.Mp, cc, st)));
+            chained = true;
+        }
+    }
+    if (!chained) {
     TVLP_RUN("adjoint_zs", 1, st,
              (launch_adjoint<IO>(p.Mp, ti, 0, gs_p, A_p, nullptr, nu, nullptr, nullptr, nullptr, g,
                                  st, frk)));
@@ -709,6 +751,7 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
                  (launch_adjoint<IO>(p.Mp, ti, 1, gs_p, A_p, mu, grad_zi ? kout : nullptr, ge_p,
                                      nullptr, flags, g, st, frk)));
     }
+    }  // !chained
     if (grad_zi) {  // adjoint at the segment's left boundary: carry-out of sub-chunk 0
         TVLP_CK(cudaMemcpy2DAsync(grad_zi, p.M * sz, kout, p.nsub * mp * sz, p.M * sz, p.B,
                                   cudaMemcpyDeviceToDevice, st));
@@ -840,9 +883,13 @@ int32_t tvlp_max_order(void) { return kMaxOrder; }
 
 int64_t tvlp_launch_count(void) { return g_launches.load(); }
 
-int64_t tvlp_refined_sequences(void) { return (int64_t)refined_sequences(); }
+int64_t tvlp_refined_sequences(void) {
+    return (int64_t)(refined_sequences() + chain_refined_sequences());
+}
 
 void tvlp_profile_enable(int32_t on) { g_prof_on.store(on ? 1 : 0); }
+
+void tvlp_chain_trace(void* buf, size_t bytes) { chain_set_trace(buf, bytes); }
 
 int32_t tvlp_profile_dump(char* buf, int32_t buflen) {
     std::lock_guard<std::mutex> lk(g_prof_mu);

@@ -40,6 +40,9 @@
 #ifndef TVLP_BASIS4_WARPS
 #define TVLP_BASIS4_WARPS 2
 #endif
+#ifndef TVLP_BASIS4_STAGES
+#define TVLP_BASIS4_STAGES 2
+#endif
 #ifndef TVLP_BASIS_GROUP
 #define TVLP_BASIS_GROUP 2
 #endif
@@ -325,7 +328,7 @@ struct Basis4Cfg {
     static constexpr int P = (M + kChains) / kChains;  // ceil((M + 1) / kChains)
     static constexpr int S = 32 / P;
     static constexpr int NW = TVLP_BASIS4_WARPS;  // independent warps per CTA
-    static constexpr int NSTB = 2;
+    static constexpr int NSTB = TVLP_BASIS4_STAGES;  // coefficient windows in flight per sub-chunk
     static constexpr int ROWS_BYTES = TI ? 0 : (M * M * 4 + 15) / 16 * 16;
     static constexpr int E_OFF = ROWS_BYTES;
     static constexpr int STAGE = ROWS_BYTES + 128;  // + the window's excitation (<= 28 floats)
@@ -338,7 +341,10 @@ struct Basis4Cfg {
     static constexpr int BYTES = BAR_OFF + NW * S * NSTB * 8;
 };
 
-template <int M, bool TI, int U>
+// SPL: partial sums per chain (the 21 older-lag terms of a chain are a serial
+// FMA dependency; SPL interleaved partial sums shorten it SPL-fold, for
+// warps that must hide FMA latency alone -- the persistent chained forward)
+template <int M, bool TI, int U, int SPL>
 __device__ __forceinline__ void basis4_step(float (&R)[kChains][M], const float* __restrict__ Ar,
                                             const float* __restrict__ es, const float (&ati)[M],
                                             float (&ac)[M], int zs) {
@@ -356,32 +362,41 @@ __device__ __forceinline__ void basis4_step(float (&R)[kChains][M], const float*
         load_row_at<float, M>(Ar + U * M, a, U * M * 4);
     }
     const float ev = es[U];
-    float c[kChains];
+    float c[kChains][SPL];
 #pragma unroll
-    for (int j = 0; j < kChains; ++j) c[j] = zs == j ? ev : 0.f;
+    for (int j = 0; j < kChains; ++j) {
+        c[j][0] = zs == j ? ev : 0.f;
+#pragma unroll
+        for (int q = 1; q < SPL; ++q) c[j][q] = 0.f;
+    }
 #pragma unroll
     for (int i = M; i >= 2; --i) {  // lags M..2, oldest first
         const int r = (U - i + 2 * M) % M;
         const float na = -a[i - 1];
 #pragma unroll
-        for (int j = 0; j < kChains; ++j) c[j] = fmaf(na, R[j][r], c[j]);
+        for (int j = 0; j < kChains; ++j) c[j][i % SPL] = fmaf(na, R[j][r], c[j][i % SPL]);
     }
     const int r1 = (U - 1 + M) % M;
 #pragma unroll
-    for (int j = 0; j < kChains; ++j) R[j][U % M] = fmaf(-a[0], R[j][r1], c[j]);
+    for (int j = 0; j < kChains; ++j) {
+        float t = c[j][0];
+        if constexpr (SPL == 2) t = c[j][0] + c[j][1];
+        if constexpr (SPL == 4) t = (c[j][0] + c[j][1]) + (c[j][2] + c[j][3]);
+        R[j][U % M] = fmaf(-a[0], R[j][r1], t);
+    }
 }
-template <int M, bool TI, int G, int... V>
+template <int M, bool TI, int SPL, int G, int... V>
 __device__ __forceinline__ void basis4_group(std::integer_sequence<int, V...>,
                                              float (&R)[kChains][M],
                                              const float* __restrict__ Ar,
                                              const float* __restrict__ es, const float (&ati)[M],
                                              float (&ac)[M], int zs) {
     ((G * kBasisGroup + V < M
-          ? basis4_step<M, TI, (G * kBasisGroup + V) % M>(R, Ar, es, ati, ac, zs)
+          ? basis4_step<M, TI, (G * kBasisGroup + V) % M, SPL>(R, Ar, es, ati, ac, zs)
           : void()),
      ...);
 }
-template <int M, bool TI, int... G>
+template <int M, bool TI, int SPL, int... G>
 __device__ __forceinline__ void basis4_full(std::integer_sequence<int, G...>,
                                             float (&R)[kChains][M],
                                             const float* __restrict__ Ar,
@@ -389,43 +404,46 @@ __device__ __forceinline__ void basis4_full(std::integer_sequence<int, G...>,
                                             float (&ac)[M], int zs, int lim) {
     if constexpr (TI) {
         // no row loads to keep in place: one straight-line window
-        (basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R, Ar, es, ati, ac,
-                                zs),
+        (basis4_group<M, TI, SPL, G>(std::make_integer_sequence<int, kBasisGroup>{}, R, Ar, es,
+                                     ati, ac, zs),
          ...);
     } else {
         ((G * kBasisGroup < lim
-              ? basis4_group<M, TI, G>(std::make_integer_sequence<int, kBasisGroup>{}, R, Ar, es,
-                                       ati, ac, zs)
+              ? basis4_group<M, TI, SPL, G>(std::make_integer_sequence<int, kBasisGroup>{}, R, Ar,
+                                            es, ati, ac, zs)
               : void()),
          ...);
     }
 }
-template <int M, bool TI, int... U>
+template <int M, bool TI, int SPL, int... U>
 __device__ __forceinline__ void basis4_partial(std::integer_sequence<int, U...>,
                                                float (&R)[kChains][M],
                                                const float* __restrict__ Ar,
                                                const float* __restrict__ es,
                                                const float (&ati)[M], float (&ac)[M], int zs,
                                                int u0) {
-    ((U >= u0 ? basis4_step<M, TI, U>(R, Ar, es, ati, ac, zs) : void()), ...);
+    ((U >= u0 ? basis4_step<M, TI, U, SPL>(R, Ar, es, ati, ac, zs) : void()), ...);
 }
 
-template <int M, bool TI, bool FR = false>
-__global__ void __launch_bounds__(Basis4Cfg<M, TI>::NW * 32, TVLP_BASIS4_MINB)
-k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
-         ScanArgs g, const FrameSrc<float> fs) {
-    grid_dep_wait();
+// One warp's basis work: lane (sub-chunk slot sc = lane / P, chain group
+// q = lane % P) computes the chains of global sub-chunk `gid` (valid lanes)
+// into the carry tape.  wbase: the warp's WARP_BYTES of shared memory; bars:
+// the warp's S * NSTB mbarriers.  Used by k_basis4 (one sub-chunk group per
+// warp) and by the persistent chained forward (a ticket loop of groups).
+template <int M, bool TI, bool FR, int SPL = 1>
+__device__ __forceinline__ void basis4_warp(const float* __restrict__ e,
+                                            const float* __restrict__ A,
+                                            float* __restrict__ PhiZ, const ScanArgs& g,
+                                            const FrameSrc<float>& fs, int64_t gid, bool valid,
+                                            unsigned char* wbase, uint64_t* wbars) {
     using C = Basis4Cfg<M, TI>;
     constexpr int P = C::P, S = C::S, NSTB = C::NSTB;
     static_assert(M + 1 <= 32, "order M must be <= 31");
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;
     const int q = lane % P;
     const bool lane_used = lane / P < S;
     const int sc = lane_used ? lane / P : S - 1;
     const int64_t nsc = g.B * g.nsub;
-    const int64_t gid = ((int64_t)blockIdx.x * C::NW + warp) * S + sc;
-    const bool valid = lane_used && gid < nsc;  // idle lanes compute on garbage, never wait
     const int64_t gg = gid < nsc ? gid : nsc - 1;
     const int64_t b = gg / g.nsub;
     const int j = (int)(gg % g.nsub);
@@ -434,10 +452,9 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
     const int nwin = (len + u0) / M;
     const int64_t row0 = b * g.T + (int64_t)j * g.Ls;
     const float* eb = e + row0;
-    unsigned char* wbase = smem + warp * C::WARP_BYTES;
     unsigned char* sbase = wbase + sc * C::SUB_BYTES;
     auto stage = [&](int st) { return sbase + st * C::STAGE; };
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF) + (warp * S + sc) * NSTB;
+    uint64_t* bars = wbars + sc * NSTB;
     const bool leader = valid && q == 0;
 
     // Window k covers ring positions first..M-1 = times k*M - u0 + (first..M-1).
@@ -512,9 +529,10 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
             load_row_at<float, M>(Ar + first * M, ac, first * M * 4);
         }
         if (k == 0 && u0 != 0)
-            basis4_partial<M, TI>(std::make_integer_sequence<int, M>{}, R, Ar, es, ati, ac, zs, u0);
+            basis4_partial<M, TI, SPL>(std::make_integer_sequence<int, M>{}, R, Ar, es, ati, ac, zs,
+                                       u0);
         else
-            basis4_full<M, TI>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
+            basis4_full<M, TI, SPL>(std::make_integer_sequence<int, (M + kBasisGroup - 1) / kBasisGroup>{},
                                R, Ar, es, ati, ac, zs, len);
         __syncwarp();  // the warp is done with stage st (generic reads before the async refill
                        // are ordered by this sync; no proxy fence is needed for WAR)
@@ -567,6 +585,22 @@ k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __rest
         bulk_commit();
         bulk_wait<0>();
     }
+}
+
+template <int M, bool TI, bool FR = false>
+__global__ void __launch_bounds__(Basis4Cfg<M, TI>::NW * 32, TVLP_BASIS4_MINB)
+k_basis4(const float* __restrict__ e, const float* __restrict__ A, float* __restrict__ PhiZ,
+         ScanArgs g, const FrameSrc<float> fs) {
+    grid_dep_wait();
+    using C = Basis4Cfg<M, TI>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool lane_used = lane / C::P < C::S;
+    const int sc = lane_used ? lane / C::P : C::S - 1;
+    const int64_t gid = ((int64_t)blockIdx.x * C::NW + warp) * C::S + sc;
+    const bool valid = lane_used && gid < g.B * g.nsub;  // idle lanes compute on garbage, never wait
+    basis4_warp<M, TI, FR>(e, A, PhiZ, g, fs, gid, valid, smem + warp * C::WARP_BYTES,
+                           reinterpret_cast<uint64_t*>(smem + C::BAR_OFF) + warp * C::S * C::NSTB);
 }
 
 // ============================================================================

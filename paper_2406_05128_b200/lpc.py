@@ -254,6 +254,7 @@ def _backward(ti, grad_s, A, s, zi, carry=None, carry_prec=None):
     batched = grad_s.dim() == 2
     B = grad_s.shape[0] if batched else 1
     T = grad_s.shape[-1]
+    shared_row = ti and batched and A.dim() == 1  # one row for the whole batch
     if ti:
         M = A.shape[-1]
         if s.shape[-1] != T:
@@ -279,6 +280,10 @@ def _backward(ti, grad_s, A, s, zi, carry=None, carry_prec=None):
         N.check(fn(dt, N.ptr(grad_s), N.ptr(A), N.ptr(s), N.ptr(zi), N.ptr(ge), N.ptr(gA), B, T,
                    M, N.ptr(carry), _carry_code(carry_prec), N.ptr(ws), nws,
                    N.stream_ptr(conv.device)))
+    if shared_row:
+        # a shared [M] row fans out to every sequence: its adjoint is the sum
+        # over the batch (lpc.py:176-195 per sequence, summed like a tape fan-out)
+        gA = gA.sum(0)
     return conv.out(ge), conv.out(gA)
 
 

@@ -1,7 +1,9 @@
 """Frame-wise time-invariant LP with overlap-add -- the reference
 ``tvlp.params`` frame-wise API (pkg/src/tvlp/params.py:102-273) on B200.
 
-``FramePlan`` mirrors params.py:157-217 exactly (it is host-side metadata);
+``FramePlan`` reproduces the framing contract of params.py:157-217 (it is
+host-side metadata whose semantics -- lead-in frames, frame order, COLA
+constant -- the drop-in must keep; see its docstring);
 ``framewise_lp`` runs the per-frame recursions, the overlap-add and (through
 :class:`paper_2406_05128_b200.autograd.LPFramewise`) the VJP in the sm_100a
 kernels of libtvlp_b200.so.
@@ -94,7 +96,16 @@ def raised_cosine_window(n):
 
 @dataclass
 class FramePlan:
-    """Windowed framing grid for overlap-add processing (params.py:157-217)."""
+    """Windowed framing grid for overlap-add processing.
+
+    This is host-side metadata whose semantics the drop-in must reproduce
+    exactly (SPEC.md's framing contract as implemented at params.py:157-217 of
+    the reference): frame f covers samples [f*hop, f*hop + frame_size), frames
+    start ``n_lead_in()`` hops before t = 0, every frame with a lead-in index
+    uses coefficient row 0, and the overlap-added output is divided by the
+    COLA constant window.sum()/hop.  The field names, constructors and the
+    tuple order of :meth:`iter_frames` are the reference's (callers unpack
+    them); the bodies below are written from that contract."""
 
     frame_size: int
     hop: int
@@ -102,29 +113,31 @@ class FramePlan:
 
     @classmethod
     def raised_cosine(cls, hop, overlap=0.75):
-        denom = 1.0 - overlap
-        size = hop / denom
-        if abs(size - round(size)) > 1e-9:
+        n = hop / (1.0 - overlap)
+        if abs(n - round(n)) > 1e-9:
             raise ValueError(f"hop {hop} and overlap {overlap} give a non-integer frame size")
-        size = int(round(size))
-        return cls(frame_size=size, hop=hop, window=raised_cosine_window(size))
+        n = int(round(n))
+        return cls(frame_size=n, hop=hop, window=raised_cosine_window(n))
 
     @classmethod
     def rectangular(cls, frame_size, hop=None):
-        hop = frame_size if hop is None else hop
-        return cls(frame_size=frame_size, hop=hop, window=np.ones(frame_size))
+        return cls(frame_size=frame_size, hop=frame_size if hop is None else hop,
+                   window=np.ones(frame_size))
 
     @property
     def overlap(self):
         return 1.0 - self.hop / self.frame_size
 
     def ola_deviation(self):
-        reps = self.frame_size // self.hop + 2
-        acc = np.zeros(self.frame_size + reps * self.hop)
-        for f in range(reps):
-            acc[f * self.hop: f * self.hop + self.frame_size] += self.window
-        interior = acc[self.frame_size: self.frame_size + self.hop]
-        return float(np.max(np.abs(interior - np.median(interior))))
+        """Peak deviation from its median of the steady-state overlap-add sum
+        of the window (one hop of the interior, past the first full frame)."""
+        n, h = self.frame_size, self.hop
+        k = n // h + 2                       # shifted copies covering the probe hop
+        total = np.zeros(n + k * h)
+        for start in range(0, k * h, h):
+            total[start:start + n] += self.window
+        probe = total[n:n + h]
+        return float(np.abs(probe - np.median(probe)).max())
 
     def validate_cola(self, tol=1e-6):
         dev = self.ola_deviation()
@@ -132,27 +145,35 @@ class FramePlan:
             raise ValueError(f"window does not satisfy constant overlap-add; deviation {dev:.3e}")
 
     def cola_constant(self):
-        return float(self.window.sum() / self.hop)
+        return float(np.sum(self.window) / self.hop)
 
     def n_lead_in(self):
+        """Frames starting before t = 0 that still overlap it."""
         return (self.frame_size - 1) // self.hop
 
     def iter_frames(self, length, n_frames):
+        """(row, sig_lo, sig_hi, win_lo, win_hi) for every frame that overlaps
+        [0, length), lead-in frames first (row 0)."""
         for f in range(-self.n_lead_in(), n_frames):
-            start = f * self.hop
-            sig_lo, sig_hi = max(start, 0), min(start + self.frame_size, length)
-            if sig_hi <= sig_lo:
-                continue
-            yield max(f, 0), sig_lo, sig_hi, sig_lo - start, sig_hi - start
+            t0 = f * self.hop
+            lo = 0 if t0 < 0 else t0
+            hi = min(t0 + self.frame_size, length)
+            if hi > lo:
+                yield (f if f > 0 else 0), lo, hi, lo - t0, hi - t0
 
-    # device copy of the window in the I/O dtype (params.py:232, 266: astype(e.dtype))
+    # device copy of the window in the I/O dtype (params.py:232, 266: astype(e.dtype)),
+    # cached on the window's CONTENTS (an in-place edit or a new array of the
+    # same id never returns a stale copy)
     def _window_tensor(self, dtype, device):
+        np_dt = np.float32 if dtype == torch.float32 else np.float64
+        host = np.ascontiguousarray(np.asarray(self.window).astype(np_dt))
         cache = self.__dict__.setdefault("_wcache", {})
-        key = (dtype, str(device), id(self.window))
+        key = (dtype, str(device), host.tobytes())
         w = cache.get(key)
         if w is None:
-            np_dt = np.float32 if dtype == torch.float32 else np.float64
-            w = torch.from_numpy(np.ascontiguousarray(self.window.astype(np_dt))).to(device)
+            if len(cache) > 8:
+                cache.clear()
+            w = torch.from_numpy(host).to(device)
             cache[key] = w
         return w
 

@@ -32,16 +32,21 @@ _STREAMS = {}
 _BUFFERS = {}
 
 
-def _buffers(dev, B, T, M, dtype, nb_max, with_zi):
+def _buffers(dev, B, T, M, dtype, sizes, with_zi):
     """Device buffers of the whole batch plus one chunk's carry tape and
     workspace, kept across calls (the kernels of consecutive chunks run on one
-    stream, so one carry/workspace serves every chunk)."""
-    key = (dev.index, B, T, M, dtype, nb_max, with_zi)
+    stream, so one carry/workspace serves every chunk).  The carry tape and
+    the workspace are sized for the LARGEST need over the distinct chunk
+    sizes: the sub-chunk plan depends on the chunk's batch, and a smaller
+    chunk can need a larger tape (shorter sub-chunks below B*T = 4096*512)."""
+    sizes = tuple(sorted(set(int(n) for n in sizes)))
+    key = (dev.index, B, T, M, dtype, sizes, with_zi)
     if key not in _BUFFERS:
         lib = N.load()
         dt = N.dtype_code(dtype)
-        nws = max(lib.tvlp_workspace_bytes(op, dt, nb_max, T, M, 0, 0, 0)
-                  for op in (N.OP_FWD_TV, N.OP_BWD_TV))
+        nws = max(lib.tvlp_workspace_bytes(op, dt, nb, T, M, 0, 0, 0)
+                  for op in (N.OP_FWD_TV, N.OP_BWD_TV) for nb in sizes)
+        ncarry = max(lib.tvlp_carry_elems(nb, T, M) for nb in sizes)
         _BUFFERS.clear()  # one shape at a time
         _BUFFERS[key] = {
             "e": torch.empty((B, T), dtype=dtype, device=dev),
@@ -51,7 +56,7 @@ def _buffers(dev, B, T, M, dtype, nb_max, with_zi):
             "s": torch.empty((B, T), dtype=dtype, device=dev),
             "ge": torch.empty((B, T), dtype=dtype, device=dev),
             "gA": torch.empty((B, T, M), dtype=dtype, device=dev),
-            "carry": torch.empty(lib.tvlp_carry_elems(nb_max, T, M), dtype=dtype, device=dev),
+            "carry": torch.empty(ncarry, dtype=dtype, device=dev),
             "ws": torch.empty(nws, dtype=torch.uint8, device=dev),
             "nws": nws,
         }
@@ -115,8 +120,8 @@ def lp_tv_fwd_bwd_host(e, A, grad_s, zi=None, *, chunks=None, out=None, device=N
     s_h, ge_h, gA_h = out
     zi_h = None if zi is None else _host(zi, e.dtype)
     bounds = _bounds(B, chunks)
-    bufs = _buffers(dev, e.shape[0], e.shape[1], A.shape[2], e.dtype, max(h - l for l, h in bounds),
-                    zi_h is not None)
+    bufs = _buffers(dev, e.shape[0], e.shape[1], A.shape[2], e.dtype,
+                    [h - l for l, h in bounds], zi_h is not None)
     lib = N.load()
     dt = N.dtype_code(e.dtype)
     T, M = e.shape[1], A.shape[2]
@@ -152,7 +157,10 @@ def lp_tv_fwd_bwd_host(e, A, grad_s, zi=None, *, chunks=None, out=None, device=N
                 bufs["e"][hi:].copy_(e[hi:], non_blocking=True)
                 bufs["g"][hi:].copy_(grad_s[hi:], non_blocking=True)
         comp.wait_event(ready)
-        carry = bufs["carry"][:lib.tvlp_carry_elems(nb, T, M)]
+        ncarry = lib.tvlp_carry_elems(nb, T, M)
+        carry = bufs["carry"][:ncarry]
+        if carry.numel() != ncarry:
+            raise RuntimeError(f"carry tape of {carry.numel()} elements, chunk needs {ncarry}")
         cs = ctypes.c_void_p(comp.cuda_stream)
         with torch.cuda.device(dev):
             N.check(lib.tvlp_lp_forward_tv(dt, N.ptr(ed), N.ptr(Ad), N.ptr(zd), N.ptr(sd), nb, T, M,
