@@ -81,8 +81,10 @@ def kernel_bytes_per_sample(name, M):
     return {
         "basis": 4 * (M + 1),          # A, e in
         "apply_fwd": 4 * (M + 2),      # A, e in; s out
+        "fwd_chain": 4 * (M + 2),      # carries + re-application: A, e in; s out
         "adjoint_zs": 4 * (M + 1),     # A, g_s in
         "adjoint_apply": 4 * (M + 2),  # A, g_s in; g_e out
+        "bwd_chain": 4 * (M + 2),      # adjoint carries + re-application: A, g_s in; g_e out
         "grad_A": 4 * (M + 2),         # g_e, s in; g_A out
     }.get(name)
 
@@ -307,23 +309,33 @@ def run_b200(args, cfg, rank, world, dist):
     if kind in ("tv", "hpn"):
         if kind == "tv":
             e, A, g = data.d1_batch_torch(lo, B, T, M, device=dev)
+
+            def step(e=e, A=A, g=g):
+                s, carry = lpc._forward(False, e, A, None, return_carry=True)
+                ge, gA = lpc._backward(False, g, A, s, None, carry)
+                return s, ge, gA
         else:
-            # grouped launch: rows [0, B) are H(z) on the glottal source, rows
-            # [B, 2B) C(z) on the noise (both D1 tracks, distinct seeds)
-            e, A, g = data.d1_batch_torch(2 * lo, 2 * B, T, M, device=dev)
+            # the HpN decoder's two LPs on their OWN buffers -- H(z) on the
+            # glottal source, C(z) on the noise (D1 tracks, distinct seeds) --
+            # through the grouped launch (tvlp_lp_*_tv_grouped)
+            eh, Ah, gh = data.d1_batch_torch(2 * lo, B, T, M, device=dev)
+            ec, Ac, gc = data.d1_batch_torch(2 * lo + B, B, T, M, device=dev)
+            e, A, g = [eh, ec], [Ah, Ac], [gh, gc]
             if dist is not None:
                 grad = torch.randn(cfg["encoder_params"], device=dev)
 
                 def allreduce():
                     return dist.all_reduce(grad, async_op=True)
 
-        def step(e=e, A=A, g=g):
-            s, carry = lpc._forward(False, e, A, None, return_carry=True)
-            work = allreduce() if allreduce is not None else None
-            ge, gA = lpc._backward(False, g, A, s, None, carry)
-            if work is not None:
-                work.wait()
-            return s, ge, gA
+            def step(e=e, A=A, g=g):
+                (sh, sc), carry = lpc.lp_forward_tv_grouped([(e[0], A[0]), (e[1], A[1])],
+                                                            return_carry=True)
+                work = allreduce() if allreduce is not None else None
+                (geh, gAh), (gec, gAc) = lpc.lp_backward_tv_grouped(
+                    [(g[0], A[0], sh), (g[1], A[1], sc)], carry=carry)
+                if work is not None:
+                    work.wait()
+                return [sh, sc], [geh, gec], [gAh, gAc]
     elif kind == "tvsplit":
         from paper_2406_05128_b200 import longseq
 
@@ -396,12 +408,15 @@ def run_b200(args, cfg, rank, world, dist):
     # and B-1 of this rank; the LP rows of an HpN batch are its first items)
     outs = step()
     torch.cuda.synchronize()
-    nb = e.shape[0]
     parity_sample = []
-    for b in sorted({0, nb - 1}):
-        parity_sample.append({"e": e[b].cpu().numpy(), "A": A[b].cpu().numpy(),
-                              "g": g[b].cpu().numpy(), "o0": outs[0][b].cpu().numpy(),
-                              "o1": outs[1][b].cpu().numpy(), "o2": outs[2][b].cpu().numpy()})
+    # (HpN: item 0 of the H(z) group and the last item of the C(z) group)
+    picks = ([(0, 0), (1, B - 1)] if kind == "hpn" else
+             [(None, b) for b in sorted({0, e.shape[0] - 1})])
+    for grp, b in picks:
+        sel = (lambda x: x[b]) if grp is None else (lambda x, grp=grp: x[grp][b])
+        parity_sample.append({"e": sel(e).cpu().numpy(), "A": sel(A).cpu().numpy(),
+                              "g": sel(g).cpu().numpy(), "o0": sel(outs[0]).cpu().numpy(),
+                              "o1": sel(outs[1]).cpu().numpy(), "o2": sel(outs[2]).cpu().numpy()})
     del outs
 
     # profiling pass: per-kernel CUDA-event durations over K steps
@@ -450,10 +465,15 @@ def run_b200(args, cfg, rank, world, dist):
             roof["fp32_frac_of_derived_peak"] = round(fl / fp32_peak, 4)
     step_gbs = algorithmic_bytes_per_sample(cfg) * B * T / (ms * 1e-3) / 1e9
 
-    # e2e: pinned host buffers through the public API
-    eh, Ah, gh = (x.cpu().pin_memory() for x in (e, A, g))
-    outs = step()
-    oh = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+    # e2e: pinned host buffers through the public API (HpN: the host batch of
+    # both filters' rows, H(z) then C(z), through the pipelined host API)
+    if kind == "hpn":
+        eh, Ah, gh = (torch.cat([y.cpu() for y in x]).pin_memory() for x in (e, A, g))
+        oh = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (eh, eh, Ah)]
+    else:
+        eh, Ah, gh = (x.cpu().pin_memory() for x in (e, A, g))
+        outs = step()
+        oh = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
     h2d = sum(x.numel() * x.element_size() for x in (eh, Ah, gh))
     d2h = sum(x.numel() * x.element_size() for x in oh)
 

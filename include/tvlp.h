@@ -150,6 +150,43 @@ int tvlp_lp_backward_tv_ex(int32_t dtype, const void* grad_s, const void* A, con
 int tvlp_segment_transition(int32_t dtype, const void* carry, int64_t B, int64_t T, int32_t M,
                             void* Phi, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Grouped launch (north star (3); SURVEY.md §8(b) "grouped variant"): n
+ * independent batches with their OWN buffers and the same (T, M) -- the
+ * GOLF HpN synthesiser's H(z) filter on the glottal source and its C(z) filter
+ * on the noise (synth.py:264-273 records them as separate lp_tv tape ops) --
+ * filtered by ONE launch sequence, without concatenating the inputs.  Each
+ * group is exactly tvlp_lp_forward_tv / tvlp_lp_backward_tv on its own
+ * arrays.  carry: tvlp_carry_elems(sum of B, T, M) values shared by the
+ * groups (the backward reads the forward's).  Workspace:
+ * tvlp_workspace_bytes_grouped().  n <= 4. */
+typedef struct tvlp_lp_fwd_group {
+    const void* e;  /* [B, T] */
+    const void* A;  /* [B, T, M] */
+    const void* zi; /* [B, M] or NULL */
+    void* s;        /* [B, T] out */
+    int64_t B;
+} tvlp_lp_fwd_group;
+typedef struct tvlp_lp_bwd_group {
+    const void* grad_s; /* [B, T] */
+    const void* A;      /* [B, T, M] */
+    const void* s;      /* [B, T] the forward's output */
+    const void* zi;     /* [B, M] or NULL */
+    void* grad_e;       /* [B, T] out */
+    void* grad_A;       /* [B, T, M] out */
+    int64_t B;
+} tvlp_lp_bwd_group;
+#define TVLP_MAX_GROUPS 4
+int tvlp_lp_forward_tv_grouped(int32_t dtype, int32_t n, const tvlp_lp_fwd_group* groups,
+                               int64_t T, int32_t M, void* carry, int32_t carry_prec,
+                               void* workspace, size_t workspace_bytes, int32_t* nonfinite,
+                               void* stream);
+int tvlp_lp_backward_tv_grouped(int32_t dtype, int32_t n, const tvlp_lp_bwd_group* groups,
+                                int64_t T, int32_t M, const void* carry, int32_t carry_prec,
+                                void* workspace, size_t workspace_bytes, void* stream);
+/* op: TVLP_OP_FWD_TV or TVLP_OP_BWD_TV; B: the n batch sizes (host array). */
+size_t tvlp_workspace_bytes_grouped(int32_t op, int32_t dtype, int32_t n, const int64_t* B,
+                                    int64_t T, int32_t M);
+
 /* Time-invariant special case: a [B, M] constant row per sequence. */
 int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,
                        int64_t B, int64_t T, int32_t M, void* carry, int32_t carry_prec,

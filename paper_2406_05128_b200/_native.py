@@ -22,6 +22,22 @@ CARRY_REUSE = 16  # OR-ed: the carry tape is already filled for the same (e, A)
 
 _lib = None
 
+
+class FwdGroup(ctypes.Structure):
+    """tvlp_lp_fwd_group (include/tvlp.h)."""
+    _fields_ = [("e", ctypes.c_void_p), ("A", ctypes.c_void_p), ("zi", ctypes.c_void_p),
+                ("s", ctypes.c_void_p), ("B", ctypes.c_int64)]
+
+
+class BwdGroup(ctypes.Structure):
+    """tvlp_lp_bwd_group (include/tvlp.h)."""
+    _fields_ = [("grad_s", ctypes.c_void_p), ("A", ctypes.c_void_p), ("s", ctypes.c_void_p),
+                ("zi", ctypes.c_void_p), ("grad_e", ctypes.c_void_p), ("grad_A", ctypes.c_void_p),
+                ("B", ctypes.c_int64)]
+
+
+MAX_GROUPS = 4
+
 # (name, restype, argtypes)
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
@@ -51,6 +67,11 @@ _SIGS = [
     ("tvlp_lp_backward_tv_ex", ctypes.c_int,
      [_I32, _P, _P, _P, _P, _P, _P, _I64, _I64, _I32, _P, _I32, _P, _P, _P, _SZ, _P]),
     ("tvlp_segment_transition", ctypes.c_int, [_I32, _P, _I64, _I64, _I32, _P, _P, _SZ, _P]),
+    ("tvlp_lp_forward_tv_grouped", ctypes.c_int,
+     [_I32, _I32, ctypes.POINTER(FwdGroup), _I64, _I32, _P, _I32, _P, _SZ, _P, _P]),
+    ("tvlp_lp_backward_tv_grouped", ctypes.c_int,
+     [_I32, _I32, ctypes.POINTER(BwdGroup), _I64, _I32, _P, _I32, _P, _SZ, _P]),
+    ("tvlp_workspace_bytes_grouped", _SZ, [_I32, _I32, _I32, ctypes.POINTER(_I64), _I64, _I32]),
     ("tvlp_lp_forward_ti", ctypes.c_int,
      [_I32, _P, _P, _P, _P, _I64, _I64, _I32, _P, _I32, _P, _SZ, _P, _P]),
     ("tvlp_lp_backward_ti", ctypes.c_int,

@@ -15,7 +15,8 @@ import torch
 from . import lpc
 from . import params as _params
 
-__all__ = ["LPTV", "LPTI", "LPFramewise", "lp_tv", "lp_ti", "framewise"]
+__all__ = ["LPTV", "LPTI", "LPFramewise", "LPTVGrouped", "lp_tv", "lp_ti", "framewise",
+           "lp_tv_grouped"]
 
 
 class LPTV(torch.autograd.Function):
@@ -35,6 +36,32 @@ class LPTV(torch.autograd.Function):
         A, s, zi = ctx.saved_tensors
         ge, gA = lpc._backward(False, grad_s.contiguous(), A, s, zi, ctx.carry)
         return ge, gA, None
+
+
+class LPTVGrouped(torch.autograd.Function):
+    """Several independent lp_tv ops (e.g. the HpN decoder's H(z) on the
+    glottal source and C(z) on the noise, synth.py:264-273) in one grouped
+    launch: apply(e_1, A_1, e_2, A_2, ...) -> (s_1, s_2, ...), each pair with
+    the contract of LPTV (saves A and s, no grad for zi)."""
+
+    @staticmethod
+    def forward(ctx, *args):
+        pairs = [(args[2 * i].detach(), args[2 * i + 1].detach().to(args[2 * i].dtype))
+                 for i in range(len(args) // 2)]
+        outs, carry = lpc.lp_forward_tv_grouped(pairs, return_carry=True)
+        ctx.save_for_backward(*[p[1] for p in pairs], *outs)
+        ctx.n = len(pairs)
+        ctx.carry = carry
+        return tuple(outs)
+
+    @staticmethod
+    def backward(ctx, *grads):
+        n = ctx.n
+        saved = ctx.saved_tensors
+        As, ss = saved[:n], saved[n:]
+        gs = [torch.zeros_like(s) if g is None else g.contiguous() for g, s in zip(grads, ss)]
+        res = lpc.lp_backward_tv_grouped(list(zip(gs, As, ss)), carry=ctx.carry)
+        return tuple(x for ge_gA in res for x in ge_gA)
 
 
 class LPTVFrames(torch.autograd.Function):
@@ -116,6 +143,12 @@ class LPFramewise(torch.autograd.Function):
 def lp_tv(e, A, zi=None):
     """Differentiable sample-wise LP filter."""
     return LPTV.apply(e, A, zi)
+
+
+def lp_tv_grouped(*pairs):
+    """Differentiable grouped filter: lp_tv_grouped((e1, A1), (e2, A2)) -> (s1, s2)."""
+    flat = [x for p in pairs for x in p]
+    return LPTVGrouped.apply(*flat)
 
 
 def lp_tv_frames(e, frames, hop, zi=None):

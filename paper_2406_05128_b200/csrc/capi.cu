@@ -517,9 +517,11 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     const FrameSrc<IO>* frk = native_fr ? fr : nullptr;
     if constexpr (std::is_same<IO, float>::value) {
         if (chain) {
-            const ChainFwdCall cc{ti, e_p, A_p, zi_p, p.Mp, s_p, phiz, fflags, xin, xend,
-                                  nonfinite, ctl, prec == kPrecAuto ? 1 : 0, g};
-            TVLP_RUN("fwd_chain", 3, st, (launch_fwd_chain(p.Mp, cc, st)));
+            ChainFwdCall cc{ti, 1, {}, p.Mp, phiz, fflags, xin, xend,
+                            nonfinite, ctl, prec == kPrecAuto ? 1 : 0, g};
+            cc.grp[0] = ChainGroup{e_p, A_p, zi_p, s_p, p.B};
+            TVLP_RUN("basis", 2, st, (launch_fwd_chain(p.Mp, cc, st, 0)));
+            TVLP_RUN("fwd_chain", 1, st, (launch_fwd_chain(p.Mp, cc, st, 1)));
             if (packed) TVLP_CK(unpack<IO>(ps, s, p.B, p.T, 1, p.Tp, 1, st));
             return TVLP_OK;
         }
@@ -694,9 +696,11 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     if constexpr (std::is_same<IO, float>::value) {
         if (chain) {
             const int* inherit = reinterpret_cast<const int*>(carry + tape_body(p));
-            const ChainBwdCall cc{ti, gs_p, A_p, ge_p, h.tape, inherit, nu, mu, kout, ctl,
-                                  prec == kPrecAuto ? 1 : 0, g};
-            TVLP_RUN("bwd_chain", 3, st, (launch_bwd_chain(p.Mp, cc, st)));
+            ChainBwdCall cc{ti, 1, {}, h.tape, inherit, nu, mu, kout, ctl,
+                            prec == kPrecAuto ? 1 : 0, g};
+            cc.grp[0] = ChainGroup{gs_p, A_p, nullptr, ge_p, p.B};
+            TVLP_RUN("adjoint_zs", 2, st, (launch_bwd_chain(p.Mp, cc, st, 0)));
+            TVLP_RUN("bwd_chain", 1, st, (launch_bwd_chain(p.Mp, cc, st, 1)));
             chained = true;
         }
     }
@@ -839,6 +843,179 @@ int fw_backward_impl(const void* gout, const void* frames, const void* win, cons
                                      static_cast<const IO*>(win), static_cast<const IO*>(seg), gew,
                                      gap, static_cast<IO*>(ge), gf_out, a, st)));
     if (gfp) TVLP_CK(unpack<IO>(gfp, gf, a.B, a.F, M, a.F, Mp, st));
+    return TVLP_OK;
+}
+
+// ---------------------------------------------------------------- grouped
+// The chained kernels take the groups' own buffers (per-group tensor maps):
+// fp32, one carry level, a compiled order equal to M, T a multiple of the
+// sub-chunk length and 16-byte aligned arrays.  Otherwise the groups are
+// concatenated into workspace, filtered as one batch and split back.
+template <typename IO>
+bool grouped_direct(const Plan& p, int prec, bool aligned) {
+    return std::is_same<IO, float>::value && make_levels(p).L == 1 &&
+           (prec == kPrecAuto || prec == kPrecF32Chains) && chain_supported(p.Mp) &&
+           p.Tp == p.T && p.Mp == p.M && aligned;
+}
+
+template <typename IO>
+int grouped_forward_impl(int n, const tvlp_lp_fwd_group* gr, const Plan& p, void* carry_v,
+                         int prec, void* ws, size_t ws_bytes, int32_t* nonfinite,
+                         cudaStream_t st, size_t* need) {
+    const size_t sz = sizeof(IO);
+    bool al = true, any_zi = false;
+    for (int i = 0; i < n && !need; ++i) {
+        al = al && aligned16(gr[i].e) && aligned16(gr[i].A) && aligned16(gr[i].s) &&
+             (!gr[i].zi || aligned16(gr[i].zi));
+        any_zi = any_zi || gr[i].zi != nullptr;
+    }
+    const bool direct = !need && grouped_direct<IO>(p, prec, al);
+    const int64_t nsc = p.B * p.nsub, mp = mp4(p);
+    Carver c(ws);
+    IO* carry = carry_v ? static_cast<IO*>(carry_v) : static_cast<IO*>(c.take(carry_elems(p) * sz));
+    if (direct) {
+        IO* xin = static_cast<IO*>(c.take(nsc * mp * sz));
+        IO* xend = static_cast<IO*>(c.take(nsc * mp * sz));
+        void* ctl = c.take(chain_ctl_bytes(p.B, p.nsub, p.Mp));
+        if (ws_bytes < c.used) return TVLP_ERR_WORKSPACE;
+        if constexpr (std::is_same<IO, float>::value) {
+            const ScanArgs g = scan_args(p);
+            ChainFwdCall cc{false, n, {}, p.Mp, carry,
+                            reinterpret_cast<int*>(carry + tape_body(p)), xin, xend, nonfinite,
+                            ctl, prec == kPrecAuto ? 1 : 0, g};
+            for (int i = 0; i < n; ++i)
+                cc.grp[i] = ChainGroup{static_cast<const float*>(gr[i].e),
+                                       static_cast<const float*>(gr[i].A),
+                                       static_cast<const float*>(gr[i].zi),
+                                       static_cast<float*>(gr[i].s), gr[i].B};
+            TVLP_RUN("basis", 1 + n, st, (launch_fwd_chain(p.Mp, cc, st, 0)));
+            TVLP_RUN("fwd_chain", 1, st, (launch_fwd_chain(p.Mp, cc, st, 1)));
+        }
+        return TVLP_OK;
+    }
+    // concatenation fallback
+    IO* ce = static_cast<IO*>(c.take(p.B * p.T * sz));
+    IO* cA = static_cast<IO*>(c.take(p.B * p.T * p.M * sz));
+    IO* cz = static_cast<IO*>(c.take(p.B * p.M * sz));
+    IO* cs = static_cast<IO*>(c.take(p.B * p.T * sz));
+    size_t inner = 0;
+    const void* any16 = reinterpret_cast<const void*>(uintptr_t(256));  // sizing: aligned, non-null
+    forward_impl<IO>(false, any16, any16, any16, (void*)any16, p, nullptr, prec, nullptr, 0, nullptr,
+                     st, &inner);
+    void* iws = c.take(inner);
+    if (need) {
+        *need = c.used;
+        return TVLP_OK;
+    }
+    if (ws_bytes < c.used) return TVLP_ERR_WORKSPACE;
+    int64_t off = 0;
+    if (any_zi) TVLP_CK(cudaMemsetAsync(cz, 0, p.B * p.M * sz, st));
+    for (int i = 0; i < n; ++i) {
+        const int64_t B = gr[i].B;
+        TVLP_CK(cudaMemcpyAsync(ce + off * p.T, gr[i].e, B * p.T * sz, cudaMemcpyDeviceToDevice, st));
+        TVLP_CK(cudaMemcpyAsync(cA + off * p.T * p.M, gr[i].A, B * p.T * p.M * sz,
+                                cudaMemcpyDeviceToDevice, st));
+        if (gr[i].zi)
+            TVLP_CK(cudaMemcpyAsync(cz + off * p.M, gr[i].zi, B * p.M * sz,
+                                    cudaMemcpyDeviceToDevice, st));
+        off += B;
+    }
+    const int rc = forward_impl<IO>(false, ce, cA, any_zi ? cz : nullptr, cs, p, carry, prec, iws,
+                                    inner, nonfinite, st, nullptr);
+    if (rc != TVLP_OK) return rc;
+    off = 0;
+    for (int i = 0; i < n; ++i) {
+        TVLP_CK(cudaMemcpyAsync(gr[i].s, cs + off * p.T, gr[i].B * p.T * sz,
+                                cudaMemcpyDeviceToDevice, st));
+        off += gr[i].B;
+    }
+    return TVLP_OK;
+}
+
+template <typename IO>
+int grouped_backward_impl(int n, const tvlp_lp_bwd_group* gr, const Plan& p, const void* carry_v,
+                          int prec, void* ws, size_t ws_bytes, cudaStream_t st, size_t* need) {
+    const size_t sz = sizeof(IO);
+    bool al = true, any_zi = false;
+    for (int i = 0; i < n && !need; ++i) {
+        al = al && aligned16(gr[i].grad_s) && aligned16(gr[i].A) && aligned16(gr[i].s) &&
+             aligned16(gr[i].grad_e) && aligned16(gr[i].grad_A) &&
+             (!gr[i].zi || aligned16(gr[i].zi));
+        any_zi = any_zi || gr[i].zi != nullptr;
+    }
+    const bool direct = !need && carry_v != nullptr && grouped_direct<IO>(p, prec, al);
+    const int64_t nsc = p.B * p.nsub, mp = mp4(p);
+    Carver c(ws);
+    if (direct) {
+        IO* nu = static_cast<IO*>(c.take(nsc * mp * sz));
+        IO* mu = static_cast<IO*>(c.take(nsc * mp * sz));
+        IO* kout = static_cast<IO*>(c.take(nsc * mp * sz));
+        void* ctl = c.take(chain_ctl_bytes(p.B, p.nsub, p.Mp));
+        if (ws_bytes < c.used) return TVLP_ERR_WORKSPACE;
+        if constexpr (std::is_same<IO, float>::value) {
+            const float* carry = static_cast<const float*>(carry_v);
+            const ScanArgs g = scan_args(p);
+            ChainBwdCall cc{false, n, {}, carry,
+                            reinterpret_cast<const int*>(carry + tape_body(p)), nu, mu, kout, ctl,
+                            prec == kPrecAuto ? 1 : 0, g};
+            for (int i = 0; i < n; ++i)
+                cc.grp[i] = ChainGroup{static_cast<const float*>(gr[i].grad_s),
+                                       static_cast<const float*>(gr[i].A), nullptr,
+                                       static_cast<float*>(gr[i].grad_e), gr[i].B};
+            TVLP_RUN("adjoint_zs", 1 + n, st, (launch_bwd_chain(p.Mp, cc, st, 0)));
+            TVLP_RUN("bwd_chain", 1, st, (launch_bwd_chain(p.Mp, cc, st, 1)));
+            for (int i = 0; i < n; ++i)
+                TVLP_RUN("grad_A", 1, st,
+                         (launch_grad_A<IO>(p.Mp, static_cast<const IO*>(gr[i].grad_e),
+                                            static_cast<const IO*>(gr[i].s),
+                                            static_cast<const IO*>(gr[i].zi),
+                                            static_cast<IO*>(gr[i].grad_A), gr[i].B, p.T, st)));
+        }
+        return TVLP_OK;
+    }
+    IO* cg = static_cast<IO*>(c.take(p.B * p.T * sz));
+    IO* cA = static_cast<IO*>(c.take(p.B * p.T * p.M * sz));
+    IO* cs = static_cast<IO*>(c.take(p.B * p.T * sz));
+    IO* cz = static_cast<IO*>(c.take(p.B * p.M * sz));
+    IO* cge = static_cast<IO*>(c.take(p.B * p.T * sz));
+    IO* cgA = static_cast<IO*>(c.take(p.B * p.T * p.M * sz));
+    size_t inner = 0;
+    const void* any16 = reinterpret_cast<const void*>(uintptr_t(256));  // sizing: aligned, non-null
+    backward_impl<IO>(false, any16, any16, any16, any16, (void*)any16, (void*)any16, p, nullptr,
+                      prec, nullptr, 0, st, &inner);
+    void* iws = c.take(inner);
+    if (need) {
+        *need = c.used;
+        return TVLP_OK;
+    }
+    if (ws_bytes < c.used) return TVLP_ERR_WORKSPACE;
+    if (any_zi) TVLP_CK(cudaMemsetAsync(cz, 0, p.B * p.M * sz, st));
+    int64_t off = 0;
+    for (int i = 0; i < n; ++i) {
+        const int64_t B = gr[i].B;
+        TVLP_CK(cudaMemcpyAsync(cg + off * p.T, gr[i].grad_s, B * p.T * sz,
+                                cudaMemcpyDeviceToDevice, st));
+        TVLP_CK(cudaMemcpyAsync(cA + off * p.T * p.M, gr[i].A, B * p.T * p.M * sz,
+                                cudaMemcpyDeviceToDevice, st));
+        TVLP_CK(cudaMemcpyAsync(cs + off * p.T, gr[i].s, B * p.T * sz, cudaMemcpyDeviceToDevice,
+                                st));
+        if (gr[i].zi)
+            TVLP_CK(cudaMemcpyAsync(cz + off * p.M, gr[i].zi, B * p.M * sz,
+                                    cudaMemcpyDeviceToDevice, st));
+        off += B;
+    }
+    const int rc = backward_impl<IO>(false, cg, cA, cs, any_zi ? cz : nullptr, cge, cgA, p,
+                                     carry_v, prec, iws, inner, st, nullptr);
+    if (rc != TVLP_OK) return rc;
+    off = 0;
+    for (int i = 0; i < n; ++i) {
+        const int64_t B = gr[i].B;
+        TVLP_CK(cudaMemcpyAsync(gr[i].grad_e, cge + off * p.T, B * p.T * sz,
+                                cudaMemcpyDeviceToDevice, st));
+        TVLP_CK(cudaMemcpyAsync(gr[i].grad_A, cgA + off * p.T * p.M, B * p.T * p.M * sz,
+                                cudaMemcpyDeviceToDevice, st));
+        off += B;
+    }
     return TVLP_OK;
 }
 
@@ -1205,6 +1382,89 @@ int tvlp_segment_transition(int32_t dtype, const void* carry, int64_t B, int64_t
         return segment_transition_impl<double>(carry, p, Phi, workspace, workspace_bytes, st,
                                                nullptr);
     return segment_transition_impl<float>(carry, p, Phi, workspace, workspace_bytes, st, nullptr);
+}
+
+static int grouped_plan(int32_t dtype, int32_t n, const int64_t* Bs, int64_t T, int32_t M,
+                        Plan& p) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (n < 1 || n > TVLP_MAX_GROUPS || n > kMaxGroups || T < 1) return TVLP_ERR_ARG;
+    int64_t Bt = 0;
+    for (int i = 0; i < n; ++i) {
+        if (Bs[i] < 1) return TVLP_ERR_ARG;
+        Bt += Bs[i];
+    }
+    return make_plan(Bt, T, M, p) ? TVLP_OK : TVLP_ERR_ARG;
+}
+
+int tvlp_lp_forward_tv_grouped(int32_t dtype, int32_t n, const tvlp_lp_fwd_group* groups,
+                               int64_t T, int32_t M, void* carry, int32_t carry_prec,
+                               void* workspace, size_t workspace_bytes, int32_t* nonfinite,
+                               void* stream) {
+    if (!groups || n < 1 || n > TVLP_MAX_GROUPS) return TVLP_ERR_ARG;
+    int64_t Bs[TVLP_MAX_GROUPS];
+    for (int i = 0; i < n; ++i) {
+        if (!groups[i].e || !groups[i].A || !groups[i].s) return TVLP_ERR_ARG;
+        Bs[i] = groups[i].B;
+    }
+    Plan p;
+    int rc = grouped_plan(dtype, n, Bs, T, M, p);
+    if (rc != TVLP_OK) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64)
+        return grouped_forward_impl<double>(n, groups, p, carry, TVLP_CARRY_F64, workspace,
+                                            workspace_bytes, nonfinite, st, nullptr);
+    return grouped_forward_impl<float>(n, groups, p, carry, carry_prec, workspace,
+                                       workspace_bytes, nonfinite, st, nullptr);
+}
+
+int tvlp_lp_backward_tv_grouped(int32_t dtype, int32_t n, const tvlp_lp_bwd_group* groups,
+                                int64_t T, int32_t M, const void* carry, int32_t carry_prec,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+    if (!groups || n < 1 || n > TVLP_MAX_GROUPS) return TVLP_ERR_ARG;
+    int64_t Bs[TVLP_MAX_GROUPS];
+    for (int i = 0; i < n; ++i) {
+        const tvlp_lp_bwd_group& g = groups[i];
+        if (!g.grad_s || !g.A || !g.s || !g.grad_e || !g.grad_A) return TVLP_ERR_ARG;
+        Bs[i] = g.B;
+    }
+    Plan p;
+    int rc = grouped_plan(dtype, n, Bs, T, M, p);
+    if (rc != TVLP_OK) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64)
+        return grouped_backward_impl<double>(n, groups, p, carry, TVLP_CARRY_F64, workspace,
+                                             workspace_bytes, st, nullptr);
+    return grouped_backward_impl<float>(n, groups, p, carry, carry_prec, workspace,
+                                        workspace_bytes, st, nullptr);
+}
+
+size_t tvlp_workspace_bytes_grouped(int32_t op, int32_t dtype, int32_t n, const int64_t* B,
+                                    int64_t T, int32_t M) {
+    if (!B || n < 1 || n > TVLP_MAX_GROUPS) return 0;
+    Plan p;
+    if (grouped_plan(dtype, n, B, T, M, p) != TVLP_OK) return 0;
+    size_t need = 0;
+    // the sizing pass covers the concatenation fallback (a superset of the
+    // direct path's buffers)
+    if (op == TVLP_OP_FWD_TV) {
+        if (dtype == TVLP_F64)
+            grouped_forward_impl<double>(n, nullptr, p, nullptr, TVLP_CARRY_F64, nullptr, 0,
+                                         nullptr, 0, &need);
+        else
+            grouped_forward_impl<float>(n, nullptr, p, nullptr, TVLP_CARRY_AUTO, nullptr, 0,
+                                        nullptr, 0, &need);
+    } else if (op == TVLP_OP_BWD_TV) {
+        if (dtype == TVLP_F64)
+            grouped_backward_impl<double>(n, nullptr, p, nullptr, TVLP_CARRY_F64, nullptr, 0, 0,
+                                          &need);
+        else
+            grouped_backward_impl<float>(n, nullptr, p, nullptr, TVLP_CARRY_AUTO, nullptr, 0, 0,
+                                         &need);
+    }
+    const size_t direct = 3 * (size_t)p.B * p.nsub * mp4(p) * 8 +
+                          chain_ctl_bytes(p.B, p.nsub, p.Mp) + 4096;
+    return need > direct ? need : direct;
 }
 
 int tvlp_lp_forward_ti(int32_t dtype, const void* e, const void* a, const void* zi, void* s,

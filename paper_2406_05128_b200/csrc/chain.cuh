@@ -460,12 +460,29 @@ __device__ __forceinline__ float warp_fmax(float v) {
 }
 
 // ---------------------------------------------------------------- arguments
+// Grouped launches (tvlp_lp_*_tv_grouped): up to kMaxGroups independent
+// batches with their own buffers and the same (T, M) share one launch;
+// sequence b of the launch is sequence b - gB0[g] of group g.
+struct GroupIdx {
+    int64_t gB0[kMaxGroups + 1];  // first sequence of each group (gB0[ng] = total B)
+    int ng;
+    __device__ __forceinline__ int of(int64_t b) const {
+        int g = 0;
+#pragma unroll
+        for (int i = 1; i < kMaxGroups; ++i)
+            if (i < ng && b >= gB0[i]) g = i;
+        return g;
+    }
+};
+
 struct ChainFwdArgs {
-    UnitMaps mp;           // A, e, s lane views
+    UnitMaps mp[kMaxGroups];  // A, e, s lane views of each group
+    GroupIdx gi;
+    const float* Ag[kMaxGroups];  // TI: the constant rows [B_g][Mp] of each group
+    const float* zig[kMaxGroups]; // nullable initial states [B_g][zs]
     CUtensorMap Tz;        // carry tape, 3-D [ntapes][2M+1][MP4], box [8][M+1][MP4] from row M
-    const float* e;
+    const float* e;        // (basis role: one group)
     const float* A;
-    const float* zi;       // nullable, row stride zs
     int zs;
     float* tape;           // carry tape [B*nsub][Tape::SIZE] + per-sequence flags after it
     int* fflags;           // per-sequence refinement flags (the backward inherits them)
@@ -485,9 +502,10 @@ struct ChainFwdArgs {
 };
 
 struct ChainBwdArgs {
-    UnitMaps mp;           // A, g_s, g_e lane views
+    UnitMaps mp[kMaxGroups];  // A, g_s, g_e lane views of each group
+    GroupIdx gi;
+    const float* Ag[kMaxGroups];  // TI: the constant rows [B_g][Mp]
     CUtensorMap Tw;        // carry tape, box [8][M][MP4] from row 0 (W rows)
-    const float* A;        // TI: the constant rows [B][Mp]
     const float* Nu;       // [B*nsub][MP4] zero-state adjoints (kernels without the pass)
     const float* tape;
     const int* inherit;    // nullable: the forward's refinement flags
@@ -565,6 +583,9 @@ __device__ bool refine_sequence_fwd(const ChainFwdArgs& a, int64_t b, unsigned c
     const int nsub = a.g.nsub;
     const int64_t base = b * nsub;
     const int nwin = a.g.Ls / kLaneWin;
+    const int grp = a.gi.of(b);
+    const int64_t vbase = (b - a.gi.gB0[grp]) * nsub;  // the group's lane-view rows
+    const float* arow = TI ? a.Ag[grp] + (b - a.gi.gB0[grp]) * M : nullptr;
     for (int it = 0; it < kRefineIters; ++it) {
         float e = 0.f, emax = 0.f;
         for (int j = 0; j + 1 < nsub; ++j) {
@@ -596,8 +617,8 @@ __device__ bool refine_sequence_fwd(const ChainFwdArgs& a, int64_t b, unsigned c
             __syncwarp();
             float xe[M];
             bool fin = true;
-            unit_fwd_pass<M, U, NST, TI>(a.mp, L == U ? 0 : 1, g0, L, nwin, sm, bars, xs, xe, fin,
-                                         a.A + b * M);
+            unit_fwd_pass<M, U, NST, TI>(a.mp[grp], L == U ? 0 : 1, vbase + (int64_t)ru * U, L, nwin,
+                                         sm, bars, xs, xe, fin, arow);
             if (lane < L) {
                 const bool has_next = ru * U + lane + 1 < nsub;
 #pragma unroll
@@ -633,6 +654,9 @@ __device__ bool refine_sequence_bwd(const ChainBwdArgs& a, int64_t b, unsigned c
     const int nsub = a.g.nsub;
     const int64_t base = b * nsub;
     const int nwin = a.g.Ls / kLaneWin;
+    const int grp = a.gi.of(b);
+    const int64_t vbase = (b - a.gi.gB0[grp]) * nsub;
+    const float* arow = TI ? a.Ag[grp] + (b - a.gi.gB0[grp]) * M : nullptr;
     for (int it = 0; it < kRefineIters; ++it) {
         float e = 0.f, emax = 0.f;
         for (int j = nsub - 1; j >= 1; --j) {
@@ -662,8 +686,8 @@ __device__ bool refine_sequence_bwd(const ChainBwdArgs& a, int64_t b, unsigned c
             float lam[M];
 #pragma unroll
             for (int i = 0; i < M; ++i) lam[i] = lane < L ? a.Mu[(g0 + lane) * MP4 + i] : 0.f;
-            unit_adj_pass<M, U, NST, 1, TI>(a.mp, L == U ? 0 : 1, g0, L, nwin, sm, bars, lam,
-                                            a.A + b * M);
+            unit_adj_pass<M, U, NST, 1, TI>(a.mp[grp], L == U ? 0 : 1, vbase + (int64_t)ru * U, L,
+                                            nwin, sm, bars, lam, arow);
             if (lane < L) {
                 const bool has_prev = ru * U + lane > 0;
                 const float* prev = a.Mu + (g0 + lane - 1) * MP4;
@@ -681,6 +705,74 @@ __device__ bool refine_sequence_bwd(const ChainBwdArgs& a, int64_t b, unsigned c
         if (dm <= kRefineTarget * xm) break;
     }
     return true;
+}
+
+// ---------------------------------------------------------------- grouped streaming passes
+// The transition tapes of every group's sequences in ONE k_basis4-shaped
+// launch: a lane's global sub-chunk selects its group's e and A (a warp may
+// straddle two groups; the tape is indexed by the global sub-chunk).
+struct GroupSrc {
+    const float* x[kMaxGroups];  // e (fwd) or g_s (bwd)
+    const float* A[kMaxGroups];
+    GroupIdx gi;
+};
+template <int M, bool TI>
+__global__ void __launch_bounds__(Basis4Cfg<M, TI>::NW * 32, TVLP_BASIS4_MINB)
+k_basis4_groups(const __grid_constant__ GroupSrc gs, float* __restrict__ PhiZ, ScanArgs g) {
+    grid_dep_wait();
+    using C = Basis4Cfg<M, TI>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool lane_used = lane / C::P < C::S;
+    const int sc = lane_used ? lane / C::P : C::S - 1;
+    const int64_t gid = ((int64_t)blockIdx.x * C::NW + warp) * C::S + sc;
+    const int64_t nsc = g.B * g.nsub;
+    const int64_t gq = gid < nsc ? gid : nsc - 1;
+    const int64_t b = gq / g.nsub;
+    const int grp = gs.gi.of(b);
+    const int64_t b0 = gs.gi.gB0[grp];
+    ScanArgs gl = g;
+    gl.B = gs.gi.gB0[grp + 1] - b0;
+    const FrameSrc<float> fs{};
+    basis4_warp<M, TI, false>(gs.x[grp], gs.A[grp], PhiZ, gl, fs, gq - b0 * g.nsub,
+                              lane_used && gid < nsc, smem + warp * C::WARP_BYTES,
+                              reinterpret_cast<uint64_t*>(smem + C::BAR_OFF) +
+                                  warp * C::S * C::NSTB,
+                              gq);
+}
+
+// Zero-state adjoints of every group's sub-chunks in one launch: one warp per
+// unit (units never straddle sequences, so a unit is in one group's lane
+// views); nu of sub-chunk g0 + l goes to Nu[global sub-chunk].
+template <int M, int U, int NST, bool TI>
+__global__ void __launch_bounds__(32)
+k_adj_zs_units(const __grid_constant__ ChainBwdArgs a) {
+    grid_dep_wait();
+    constexpr int MP4 = Tape<M>::MP4;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int64_t t = blockIdx.x;
+    const int nu = a.u.nu, nsub = a.g.nsub;
+    if (t >= a.g.B * nu) return;
+    const int64_t b = t / nu;
+    const int ru = (int)(t % nu);
+    const int L = a.u.len(ru);
+    const int grp = a.gi.of(b);
+    const int64_t bl = b - a.gi.gB0[grp];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + UnitLane<M, U, NST>::BYTES);
+    float lam[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) lam[i] = 0.f;
+    unit_adj_pass<M, U, NST, 0, TI>(a.mp[grp], L == U ? 0 : 1, bl * nsub + (int64_t)ru * U, L,
+                                    a.g.Ls / kLaneWin, smem, bars, lam,
+                                    TI ? a.Ag[grp] + bl * M : nullptr);
+    if (lane < L) {
+        float* out = const_cast<float*>(a.Nu) + (b * nsub + (int64_t)ru * U + lane) * MP4;
+#pragma unroll
+        for (int i = 0; i < M; ++i) out[i] = lam[i];
+#pragma unroll
+        for (int i = M; i < MP4; ++i) out[i] = 0.f;
+    }
 }
 
 // ---------------------------------------------------------------- forward kernel
@@ -744,6 +836,9 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
         const int64_t b = t % B;
         const int L = a.u.len(ru);
         const int64_t g0 = b * nsub + (int64_t)ru * U;
+        const int grp = a.gi.of(b);
+        const int64_t bl = b - a.gi.gB0[grp];              // sequence within its group
+        const int64_t r0 = bl * nsub + (int64_t)ru * U;    // row of the group's lane views
         unsigned long long tt[5] = {gtime(), 0, 0, 0, 0};
         // 1. tapes of the unit complete? (NWB == 0: a previous launch wrote them)
         if constexpr (NWB > 0) wait_count(&a.cnt[b * nu + ru], (unsigned)L);
@@ -762,7 +857,7 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
         // 3. state entering the unit
         float x = 0.f;
         if (ru == 0) {
-            if (a.zi != nullptr && lane < M) x = a.zi[b * a.zs + lane];
+            if (a.zig[grp] != nullptr && lane < M) x = a.zig[grp][bl * a.zs + lane];
             __syncwarp();
         } else {
             x = wait_state<M>(a.pub + (b * nu + ru - 1) * MP4);
@@ -780,8 +875,8 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
         tt[3] = gtime();
         // 5. re-run the unit's sub-chunks from their carried-in states
         float xe[M];
-        unit_fwd_pass<M, U, NST, TI>(a.mp, L == U ? 0 : 1, g0, L, nwin, sa, abars, xs, xe, finite,
-                                     a.A + b * M);
+        unit_fwd_pass<M, U, NST, TI>(a.mp[grp], L == U ? 0 : 1, r0, L, nwin, sa, abars, xs, xe,
+                                     finite, TI ? a.Ag[grp] + bl * M : nullptr);
         tt[4] = gtime();
         trace_rec(a.tr, (NWB > 0 ? (unsigned)(B * ((nsub + BC::S - 1) / BC::S)) : 0u) + t, 2, t, tt);
         // 6. boundary defects (precision "auto")
@@ -870,6 +965,10 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
         const int L = a.u.len(ru);
         const int which = L == U ? 0 : 1;
         const int64_t g0 = b * nsub + (int64_t)ru * U;
+        const int grp = a.gi.of(b);
+        const int64_t bl = b - a.gi.gB0[grp];
+        const int64_t r0 = bl * nsub + (int64_t)ru * U;
+        const float* arow = TI ? a.Ag[grp] + bl * M : nullptr;
         // W rows of the unit's tapes (read by the carry), staged during the
         // zero-state pass
         uint64_t* tb = bars + NST;
@@ -888,7 +987,7 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
             // 1. zero-state adjoint -> nu
 #pragma unroll
             for (int i = 0; i < M; ++i) lam[i] = 0.f;
-            unit_adj_pass<M, U, NST, 0, TI>(a.mp, which, g0, L, nwin, sl, bars, lam, a.A + b * M);
+            unit_adj_pass<M, U, NST, 0, TI>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow);
             if (lane < L) {
 #pragma unroll
                 for (int i = 0; i < M; ++i) nus[lane * MP4 + i] = lam[i];
@@ -912,7 +1011,7 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
         // keep the unit's left carry for lane 0's defect check (nus is free now)
         if (lane < M) nus[lane] = mu;
         __syncwarp();
-        unit_adj_pass<M, U, NST, 1, TI>(a.mp, which, g0, L, nwin, sl, bars, lam, a.A + b * M);
+        unit_adj_pass<M, U, NST, 1, TI>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow);
         tt[4] = gtime();
         trace_rec(a.tr, t, 3, t, tt);
         if (a.refine) {

@@ -10,6 +10,7 @@
 #include "scan_launch.cuh"
 
 namespace tvlp {
+UnitGeo chain_units_n(int nsub, int U);
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 encode() {
@@ -166,28 +167,78 @@ CtlLayout ctl_layout(int64_t B, const UnitGeo& u, int mp4) {
     return c;
 }
 
+GroupIdx group_index(int ng, const ChainGroup* grp) {
+    GroupIdx gi;
+    std::memset(&gi, 0, sizeof(gi));
+    gi.ng = ng;
+    int64_t acc = 0;
+    for (int i = 0; i < ng; ++i) {
+        gi.gB0[i] = acc;
+        acc += grp[i].B;
+    }
+    for (int i = ng; i <= kMaxGroups; ++i) gi.gB0[i] = acc;
+    return gi;
+}
+
+// a group's own ScanArgs (its B) for the per-group streaming launches
+ScanArgs group_args(const ScanArgs& g, int64_t B) {
+    ScanArgs s = g;
+    s.B = B;
+    return s;
+}
+
 template <int M, bool TI>
-cudaError_t fwd_chain_impl(const ChainFwdCall& c, cudaStream_t st) {
+cudaError_t fwd_chain_impl(const ChainFwdCall& c, cudaStream_t st, int phase) {
     constexpr int NWB = TVLP_CHAIN_BASIS_WARPS, NST = TVLP_CHAIN_FWD_STAGES;
     using SM = FwdChainSmem<M, NWB, NST>;
     constexpr int MP4 = Tape<M>::MP4;
     auto k = k_fwd_chain<M, NWB, NST, TI && NWB == 0>;
     cudaError_t err = set_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
+    if (c.ng < 1 || c.ng > kMaxGroups || (NWB > 0 && c.ng != 1)) return cudaErrorInvalidValue;
     const UnitGeo u = chain_units(c.g.nsub, true);
     const CtlLayout L = ctl_layout(c.g.B, u, MP4);
     unsigned char* ctl = static_cast<unsigned char*>(c.ctl);
-    err = zero_ctl(ctl, L.bytes, st);
-    if (err != cudaSuccess) return err;
+    if (phase == 0) {
+        // the control words, then the transition tapes (k_basis4, one launch
+        // per group: each fills its own sequences' tapes)
+        err = zero_ctl(ctl, L.bytes, st);
+        if (err != cudaSuccess || NWB > 0) return err;
+        if (c.ng == 1)
+            return launch_basis<float>(M, TI, kPrecF32Chains, c.grp[0].x, c.grp[0].A, c.tape, c.g,
+                                       st);
+        // groups: one launch over all of them (each lane picks its group)
+        using BC = Basis4Cfg<M, TI>;
+        auto kb = k_basis4_groups<M, TI>;
+        err = set_smem(kb, BC::BYTES);
+        if (err != cudaSuccess) return err;
+        GroupSrc gs;
+        std::memset(&gs, 0, sizeof(gs));
+        gs.gi = group_index(c.ng, c.grp);
+        for (int i = 0; i < c.ng; ++i) {
+            gs.x[i] = c.grp[i].x;
+            gs.A[i] = c.grp[i].A;
+        }
+        const int64_t per = (int64_t)BC::S * BC::NW;
+        launch_pdl(kb, (unsigned)((c.g.B * c.g.nsub + per - 1) / per), BC::NW * 32, BC::BYTES, st,
+                   gs, c.tape, c.g);
+        return cudaGetLastError();
+    }
     ChainFwdArgs a;
     std::memset(&a, 0, sizeof(a));
-    err = unit_maps<M, SM::U, NST>(a.mp, TI ? nullptr : c.A, c.e, c.s, c.g, u);
-    if (err != cudaSuccess) return err;
+    a.gi = group_index(c.ng, c.grp);
+    for (int i = 0; i < c.ng; ++i) {
+        const ScanArgs gg = group_args(c.g, c.grp[i].B);
+        err = unit_maps<M, SM::U, NST>(a.mp[i], TI ? nullptr : c.grp[i].A, c.grp[i].x, c.grp[i].y,
+                                       gg, u);
+        if (err != cudaSuccess) return err;
+        a.Ag[i] = c.grp[i].A;
+        a.zig[i] = c.grp[i].zi;
+    }
     err = view_tapes(&a.Tz, c.tape, M, MP4, Tape<M>::SIZE, (uint64_t)c.g.B * c.g.nsub, M + 1);
     if (err != cudaSuccess) return err;
-    a.e = c.e;
-    a.A = c.A;
-    a.zi = c.zi;
+    a.e = c.grp[0].x;
+    a.A = c.grp[0].A;
     a.zs = c.zs;
     a.tape = c.tape;
     a.fflags = c.fflags;
@@ -212,10 +263,7 @@ cudaError_t fwd_chain_impl(const ChainFwdCall& c, cudaStream_t st) {
         const int64_t need = (groups + NWB - 1) / NWB;
         if (grid > need) grid = need;
     } else {
-        // the transition tapes first (k_basis4), then the chained carries and
-        // re-application over units
-        err = launch_basis<float>(M, TI, kPrecF32Chains, c.e, c.A, c.tape, c.g, st);
-        if (err != cudaSuccess) return err;
+        // the chained carries and re-application over the units of every group
         grid = balanced_grid(c.g.B * u.nu, k, (NWB + 1) * 32, SM::BYTES, "TVLP_CHAIN_FWD_CTAS");
     }
     if (grid < 1) grid = 1;
@@ -224,7 +272,7 @@ cudaError_t fwd_chain_impl(const ChainFwdCall& c, cudaStream_t st) {
 }
 
 template <int M, bool TI>
-cudaError_t bwd_chain_impl(const ChainBwdCall& c, cudaStream_t st) {
+cudaError_t bwd_chain_impl(const ChainBwdCall& c, cudaStream_t st, int phase) {
     constexpr int NST = TVLP_CHAIN_BWD_STAGES;
     constexpr bool ZS = TVLP_CHAIN_BWD_ZS != 0;
     using SM = BwdChainSmem<M, NST, ZS>;
@@ -232,25 +280,54 @@ cudaError_t bwd_chain_impl(const ChainBwdCall& c, cudaStream_t st) {
     auto k = k_bwd_chain<M, NST, ZS, TI>;
     cudaError_t err = set_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
+    if (c.ng < 1 || c.ng > kMaxGroups) return cudaErrorInvalidValue;
     const UnitGeo u = chain_units(c.g.nsub, false);
     const CtlLayout L = ctl_layout(c.g.B, u, MP4);
     unsigned char* ctl = static_cast<unsigned char*>(c.ctl);
-    err = zero_ctl(ctl, L.bytes, st);
-    if (err != cudaSuccess) return err;
-    if constexpr (!ZS) {
-        // the zero-state adjoints first (the streaming k_adjoint<MODE 0>)
-        err = launch_adjoint<float>(M, TI, 0, c.gs, c.A, nullptr, c.Nu, nullptr, nullptr,
-                                    nullptr, c.g, st);
+    if (phase == 0) {
+        err = zero_ctl(ctl, L.bytes, st);
         if (err != cudaSuccess) return err;
+        if constexpr (!ZS) {
+            // the zero-state adjoints: the streaming k_adjoint<MODE 0> for one
+            // group; for several, one launch of unit warps over all of them
+            if (c.ng == 1)
+                return launch_adjoint<float>(M, TI, 0, c.grp[0].x, c.grp[0].A, nullptr, c.Nu,
+                                             nullptr, nullptr, nullptr, c.g, st);
+            constexpr int UZ = 32, NZ = 3;
+            const UnitGeo uz = chain_units_n(c.g.nsub, UZ);
+            ChainBwdArgs z;
+            std::memset(&z, 0, sizeof(z));
+            z.gi = group_index(c.ng, c.grp);
+            for (int i = 0; i < c.ng; ++i) {
+                err = unit_maps<M, UZ, NZ>(z.mp[i], TI ? nullptr : c.grp[i].A, c.grp[i].x,
+                                           c.grp[i].y, group_args(c.g, c.grp[i].B), uz);
+                if (err != cudaSuccess) return err;
+                z.Ag[i] = c.grp[i].A;
+            }
+            z.Nu = c.Nu;
+            z.g = c.g;
+            z.u = uz;
+            auto kz = k_adj_zs_units<M, UZ, NZ, TI>;
+            const int smz = UnitLane<M, UZ, NZ>::BYTES + NZ * 8;
+            err = set_smem(kz, smz);
+            if (err != cudaSuccess) return err;
+            launch_pdl(kz, (unsigned)(c.g.B * uz.nu), 32, smz, st, z);
+            return cudaGetLastError();
+        }
+        return cudaSuccess;
     }
     ChainBwdArgs a;
     std::memset(&a, 0, sizeof(a));
-    err = unit_maps<M, SM::U, NST>(a.mp, TI ? nullptr : c.A, c.gs, c.ge, c.g, u);
-    if (err != cudaSuccess) return err;
+    a.gi = group_index(c.ng, c.grp);
+    for (int i = 0; i < c.ng; ++i) {
+        err = unit_maps<M, SM::U, NST>(a.mp[i], TI ? nullptr : c.grp[i].A, c.grp[i].x, c.grp[i].y,
+                                       group_args(c.g, c.grp[i].B), u);
+        if (err != cudaSuccess) return err;
+        a.Ag[i] = c.grp[i].A;
+    }
     err = view_tapes(&a.Tw, c.tape, M, MP4, Tape<M>::SIZE, (uint64_t)c.g.B * c.g.nsub, M);
     if (err != cudaSuccess) return err;
     a.Nu = c.Nu;
-    a.A = c.A;
     a.tape = c.tape;
     a.inherit = c.inherit;
     a.Mu = c.Mu;
@@ -271,12 +348,16 @@ cudaError_t bwd_chain_impl(const ChainBwdCall& c, cudaStream_t st) {
 
 }  // namespace
 
-UnitGeo chain_units(int nsub, bool fwd) {
+UnitGeo chain_units_n(int nsub, int U) {
     UnitGeo u;
-    u.U = fwd ? TVLP_CHAIN_FWD_UNIT : TVLP_CHAIN_BWD_UNIT;
+    u.U = U;
     u.nu = (nsub + u.U - 1) / u.U;
     u.rem = nsub - (u.nu - 1) * u.U;
     return u;
+}
+
+UnitGeo chain_units(int nsub, bool fwd) {
+    return chain_units_n(nsub, fwd ? TVLP_CHAIN_FWD_UNIT : TVLP_CHAIN_BWD_UNIT);
 }
 
 bool chain_supported(int Mp) {
@@ -291,16 +372,20 @@ size_t chain_ctl_bytes(int64_t B, int nsub, int Mp) {
     return f > b ? f : b;
 }
 
-cudaError_t launch_fwd_chain(int Mp, const ChainFwdCall& c, cudaStream_t st) {
+cudaError_t launch_fwd_chain(int Mp, const ChainFwdCall& c, cudaStream_t st, int phase) {
     switch (Mp) {
-        case 22: return c.ti ? fwd_chain_impl<22, true>(c, st) : fwd_chain_impl<22, false>(c, st);
+        case 22:
+            return c.ti ? fwd_chain_impl<22, true>(c, st, phase)
+                        : fwd_chain_impl<22, false>(c, st, phase);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_bwd_chain(int Mp, const ChainBwdCall& c, cudaStream_t st) {
+cudaError_t launch_bwd_chain(int Mp, const ChainBwdCall& c, cudaStream_t st, int phase) {
     switch (Mp) {
-        case 22: return c.ti ? bwd_chain_impl<22, true>(c, st) : bwd_chain_impl<22, false>(c, st);
+        case 22:
+            return c.ti ? bwd_chain_impl<22, true>(c, st, phase)
+                        : bwd_chain_impl<22, false>(c, st, phase);
         default: return cudaErrorInvalidValue;
     }
 }

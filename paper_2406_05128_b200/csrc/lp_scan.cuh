@@ -435,7 +435,8 @@ __device__ __forceinline__ void basis4_warp(const float* __restrict__ e,
                                             const float* __restrict__ A,
                                             float* __restrict__ PhiZ, const ScanArgs& g,
                                             const FrameSrc<float>& fs, int64_t gid, bool valid,
-                                            unsigned char* wbase, uint64_t* wbars) {
+                                            unsigned char* wbase, uint64_t* wbars,
+                                            int64_t tgid = -1) {
     using C = Basis4Cfg<M, TI>;
     constexpr int P = C::P, S = C::S, NSTB = C::NSTB;
     static_assert(M + 1 <= 32, "order M must be <= 31");
@@ -545,7 +546,8 @@ __device__ __forceinline__ void basis4_warp(const float* __restrict__ e,
     // 4-byte stores per lane.
     constexpr int MP4 = Tape<M>::MP4;
     float* buf = reinterpret_cast<float*>(sbase);
-    float* tape = PhiZ + gg * Tape<M>::SIZE;
+    // (grouped launches: e/A index the lane's group, the tape the whole launch)
+    float* tape = PhiZ + (tgid >= 0 ? tgid : gg) * Tape<M>::SIZE;
     __syncwarp();
     if (lane_used) {
 #pragma unroll

@@ -19,6 +19,7 @@ fused into the forward kernel (a device flag); ``set_validation("eager")``
 """
 from __future__ import annotations
 
+import ctypes
 import os
 
 import numpy as np
@@ -33,6 +34,8 @@ __all__ = [
     "lp_backward_tv",
     "lp_forward_tv_frames",
     "lp_backward_tv_frames",
+    "lp_forward_tv_grouped",
+    "lp_backward_tv_grouped",
     "shift_coeffs",
     "lagged_signal_matrix",
     "set_validation",
@@ -379,6 +382,104 @@ def lp_backward_tv_frames(grad_s, frames, hop, s, zi=None, *, carry=None, carry_
             F, hop, N.ptr(carry), _carry_code(carry_precision), N.ptr(ws), nws,
             N.stream_ptr(conv.device)))
     return conv.out(ge), conv.out(gF)
+
+
+# ---------------------------------------------------------------------------
+# grouped: several independent batches (own buffers, same T and M) per launch
+# ---------------------------------------------------------------------------
+
+def _group_args(pairs, what):
+    if not 1 <= len(pairs) <= N.MAX_GROUPS:
+        raise ValueError(f"1..{N.MAX_GROUPS} groups, got {len(pairs)}")
+    conv = _Conv(*[x for p in pairs for x in p])
+    return conv
+
+
+def lp_forward_tv_grouped(groups, *, carry_precision=None, return_carry=False):
+    """``[lp_forward_tv(e, A, zi) for (e, A[, zi]) in groups]`` in ONE launch
+    sequence, each group on its own buffers: the HpN synthesiser's H(z) on the
+    glottal source and C(z) on the noise (synth.py:264-273 records them as two
+    lp_tv tape ops).  Every group is [B_g, T] / [B_g, T, M] with the same T
+    and M; returns the list of outputs (and the shared carry tape)."""
+    conv = _group_args(groups, "groups")
+    es, As, zis = [], [], []
+    for gspec in groups:
+        e, A = gspec[0], gspec[1]
+        zi = gspec[2] if len(gspec) > 2 else None
+        e = _signal(conv.t(e), "e").contiguous()
+        if e.dim() == 1:
+            raise ValueError("grouped calls take batched signals [B, T]")
+        A = conv.t(A, e.dtype)
+        if A.dim() != 3 or A.shape[:2] != e.shape:
+            raise ValueError("A must be a (B, T, M) coefficient track per group")
+        es.append(e)
+        As.append(A.contiguous())
+        zis.append(_zi(zi, A.shape[-1], e.shape[0], True, e.dtype, conv))
+    T, M, dtype = es[0].shape[-1], As[0].shape[-1], es[0].dtype
+    if any(e.shape[-1] != T or A.shape[-1] != M or e.dtype != dtype for e, A in zip(es, As)):
+        raise ValueError("grouped batches must share T, M and dtype")
+    lib = N.load()
+    dt = N.dtype_code(dtype)
+    Bs = (ctypes.c_int64 * len(es))(*[e.shape[0] for e in es])
+    outs = [torch.empty_like(e) for e in es]
+    carry = torch.empty(lib.tvlp_carry_elems(sum(Bs), T, M), dtype=dtype, device=conv.device)
+    ws, nws = N.workspace(lib.tvlp_workspace_bytes_grouped(N.OP_FWD_TV, dt, len(es), Bs, T, M),
+                          conv.device)
+    arr = (N.FwdGroup * len(es))(*[N.FwdGroup(e.data_ptr(), A.data_ptr(),
+                                              0 if z is None else z.data_ptr(), s.data_ptr(),
+                                              e.shape[0])
+                                   for e, A, z, s in zip(es, As, zis, outs)])
+    flag = _flag(conv.device)
+    with torch.cuda.device(conv.device):
+        N.check(lib.tvlp_lp_forward_tv_grouped(dt, len(es), arr, T, M, N.ptr(carry),
+                                               _carry_code(carry_precision), N.ptr(ws), nws,
+                                               N.ptr(flag), N.stream_ptr(conv.device)))
+    if flag is not None and _VALIDATION == "eager" and int(flag.item()) != 0:
+        for e, A in zip(es, As):
+            _raise_nonfinite(flag, e, A)
+    res = [conv.out(s) for s in outs]
+    return (res, carry) if return_carry else res
+
+
+def lp_backward_tv_grouped(groups, *, carry=None, carry_precision=None):
+    """Adjoints of :func:`lp_forward_tv_grouped`: ``groups`` holds
+    (grad_s, A, s[, zi]) per group; returns [(grad_e, grad_A), ...]."""
+    conv = _group_args(groups, "groups")
+    gs_, As, ss, zis = [], [], [], []
+    for gspec in groups:
+        g = conv.t(gspec[0]).contiguous()
+        if g.dtype not in (torch.float32, torch.float64):
+            g = g.to(torch.float32)
+        A = conv.t(gspec[1], g.dtype).contiguous()
+        s = conv.t(gspec[2], g.dtype).contiguous()
+        zi = gspec[3] if len(gspec) > 3 else None
+        if g.dim() != 2 or A.dim() != 3 or A.shape[:2] != g.shape or s.shape != g.shape:
+            raise ValueError("grad_s, A and s must share the same length")
+        gs_.append(g)
+        As.append(A)
+        ss.append(s)
+        zis.append(_zi(zi, A.shape[-1], g.shape[0], True, g.dtype, conv))
+    T, M, dtype = gs_[0].shape[-1], As[0].shape[-1], gs_[0].dtype
+    if any(g.shape[-1] != T or A.shape[-1] != M or g.dtype != dtype for g, A in zip(gs_, As)):
+        raise ValueError("grouped batches must share T, M and dtype")
+    lib = N.load()
+    dt = N.dtype_code(dtype)
+    Bs = (ctypes.c_int64 * len(gs_))(*[g.shape[0] for g in gs_])
+    if carry is not None and carry.numel() != lib.tvlp_carry_elems(sum(Bs), T, M):
+        carry = None
+    ges = [torch.empty_like(g) for g in gs_]
+    gAs = [torch.empty_like(A) for A in As]
+    ws, nws = N.workspace(lib.tvlp_workspace_bytes_grouped(N.OP_BWD_TV, dt, len(gs_), Bs, T, M),
+                          conv.device)
+    arr = (N.BwdGroup * len(gs_))(*[N.BwdGroup(g.data_ptr(), A.data_ptr(), s.data_ptr(),
+                                               0 if z is None else z.data_ptr(), ge.data_ptr(),
+                                               gA.data_ptr(), g.shape[0])
+                                    for g, A, s, z, ge, gA in zip(gs_, As, ss, zis, ges, gAs)])
+    with torch.cuda.device(conv.device):
+        N.check(lib.tvlp_lp_backward_tv_grouped(dt, len(gs_), arr, T, M, N.ptr(carry),
+                                                _carry_code(carry_precision), N.ptr(ws), nws,
+                                                N.stream_ptr(conv.device)))
+    return [(conv.out(ge), conv.out(gA)) for ge, gA in zip(ges, gAs)]
 
 
 # ---------------------------------------------------------------------------
