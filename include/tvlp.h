@@ -27,7 +27,8 @@
  * Layouts (C-contiguous): e, s, grad_s, grad_e [B, T]; A, grad_A [B, T, M];
  * zi [B, M] (nullable = zeros); a, grad_a [B, M]; frames, grad_frames
  * [B, F, M]; window [frame_size] (the reference's float64 window cast to the
- * I/O dtype); seg [B, frame_size, n_frames].  dtype: TVLP_F32 or TVLP_F64 for
+ * I/O dtype); seg [B, n_frames, frame_size] (frame-major, like the
+ * reference's list of per-frame seg_outputs).  dtype: TVLP_F32 or TVLP_F64 for
  * every floating-point array of the call.
  */
 #ifndef TVLP_B200_H
@@ -202,8 +203,10 @@ int tvlp_lagged_signal_matrix(int32_t dtype, const void* s, const void* zi, void
                               int64_t T, int32_t M, void* stream);
 
 /* Frame-wise TI LP with overlap-add.  cola = window.sum()/hop (params.py:199-201).
- * seg [B, frame_size, tvlp_framewise_nframes()] receives the per-frame outputs
- * (the reference's seg_outputs), which the backward consumes. */
+ * seg [B, tvlp_framewise_nframes(), frame_size] receives the per-frame outputs
+ * (the reference's seg_outputs), which the backward consumes.  frame_size must
+ * be a multiple of 4 whose staged span fits shared memory (hop 240 / frame 960:
+ * yes); other plans return TVLP_ERR_ARG. */
 int tvlp_framewise_forward(int32_t dtype, const void* e, const void* frames, const void* window,
                            double cola, void* out, void* seg, int64_t B, int64_t T, int64_t F,
                            int32_t M, int32_t frame_size, int32_t hop, void* workspace,

@@ -782,6 +782,8 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
 // ---------------------------------------------------------------- frame-wise
 bool fw_args(int64_t B, int64_t T, int64_t F, int M, int size, int hop, double cola, FwArgs& a) {
     if (B < 1 || T < 1 || M < 1 || M > kMaxOrder || size < 1 || hop < 1) return false;
+    // (frame sizes whose staged span fits shared memory; fp64 bound is the tighter)
+    if (!fw_supported(padded_order(M), size, hop, 8)) return false;
     if (F != (T - 1) / hop + 1) return false;  // params.py:223-227
     a.B = B;
     a.T = T;

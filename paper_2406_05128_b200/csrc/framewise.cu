@@ -5,255 +5,369 @@
 //
 // Every frame f in [-n_lead, F) is an independent zero-state TI recursion of
 // `size` samples over window[k] * e[f*hop + k] with coefficient row
-// frames[max(f,0)].  One lane per frame (frames of a sequence are contiguous
-// lanes), all lanes step through k together: the window value is a broadcast
-// and the per-frame outputs seg[b, k, fi] are written as coalesced 128-B rows.
-// Overlap-add and the frame-row reduction are deterministic gathers in frame
-// order (the reference's accumulation order).
+// frames[max(f,0)].  Overlap-add and the frame-row reduction are
+// deterministic gathers in frame order (the reference's accumulation order).
+#include <algorithm>
+#include <cstring>
+
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "framewise_launch.cuh"
 
-#ifndef TVLP_FW_PREFETCH
-#define TVLP_FW_PREFETCH 16
-#endif
 
 namespace tvlp {
 
+// ============================================================================
+// Layout: seg and the per-frame gradient contributions gew are [B][nfr][size]
+// (frame-major: row fi is frame fi's output, like the reference's list of
+// seg_outputs).  One warp = 32 consecutive frames of one sequence (lane =
+// frame); every lane steps through k = 0..size-1 together.  Rows of 32
+// frames x W steps leave (forward) or arrive (backward) as ONE 2-D tensor
+// copy (box {W, 32}; the last block of a sequence uses a box of its
+// remaining rows so it never touches the next sequence's frames).  The
+// excitation / gradient span the 32 frames read is staged once in shared
+// memory with one pad word per hop (lane f reads index f*(hop+1) + ..., 32
+// distinct banks).  Overlap-add and the grad_e gather then read the
+// frame-major rows with consecutive samples on consecutive threads.
+// ============================================================================
+constexpr int kFwW = 8;        // steps per compute window
+constexpr int kFwOut = 2;      // output box stages
+
+// backward: windows of saved outputs below the current one that the lags reach
 template <int M>
-struct FwGeo {
-    static constexpr int L = clcm(M, 4);  // unrolled body; ring positions static
-    static constexpr int RS = (M + TVLP_FW_PREFETCH + 3) / 4 * 4;  // backward ring: M live + prefetch slots
+struct FwLag {
+    static constexpr int NB = (M + 1 + kFwW - 1) / kFwW;
+    static constexpr int SW = (NB + 1) * kFwW;  // register window of saved outputs
+    static constexpr int NS = NB + 10;          // stages of the saved-output ring (1 KB each)
+};
+constexpr int kFwSegStages = FwLag<30>::NS;  // shared-memory ring slots (the largest order)
+
+struct FwMaps {
+    CUtensorMap seg[2];  // [B*nfr][size] box {W, 32} / {W, nfr % 32}
+    CUtensorMap gew[2];
 };
 
-// One warp = 32 consecutive frames of one sequence (grid: B x ceil(nfr/32),
-// so every SM gets work).  The excitation span those frames read,
-// [f0*hop, (f0+31)*hop + size), and the window are staged in shared memory
-// once (coalesced) when they fit; the per-step reads are then shared-memory
-// hits instead of 32 scattered global loads.
+// padded index of time t (relative to the span start) in the staged span
+__device__ __forceinline__ int fw_pad(int t, int hop) { return t + t / hop; }
+
 template <typename IO>
-struct FwStage {
-    static __host__ __device__ int64_t span(int size, int hop) { return 31LL * hop + size; }
-    static __host__ __device__ size_t bytes(int size, int hop) {
-        return (size_t)(span(size, hop) + size) * sizeof(IO);
+struct FwSmem {
+    static __host__ __device__ int span(int size, int hop) { return 31 * hop + size; }
+    static __host__ __device__ int padded(int size, int hop) {
+        const int n = span(size, hop);
+        return (n + n / hop + 4) / 4 * 4;
+    }
+    static constexpr int OUT = 32 * kFwW * (int)sizeof(IO);
+    static constexpr int SEGW = 32 * kFwW * (int)sizeof(IO);  // one window of 32 rows
+    // [span (padded)][window][out boxes][seg ring][barriers]
+    static __host__ __device__ size_t off_win(int size, int hop) {
+        return (size_t)padded(size, hop) * sizeof(IO);
+    }
+    static __host__ __device__ size_t off_out(int size, int hop) {
+        return (off_win(size, hop) + (size_t)size * sizeof(IO) + 127) / 128 * 128;
+    }
+    static __host__ __device__ size_t off_seg(int size, int hop) {
+        return off_out(size, hop) + kFwOut * OUT;
+    }
+    static __host__ __device__ size_t off_bar(int size, int hop, bool bwd) {
+        return off_seg(size, hop) + (bwd ? kFwSegStages * SEGW : 0);
+    }
+    static size_t bytes(int size, int hop, bool bwd) {
+        return off_bar(size, hop, bwd) + 8 * (kFwSegStages + 1);
     }
 };
-constexpr size_t kFwStageMax = 200 * 1024;
 
-// dst[i] = src[t0 + i] (/ div), zero outside [0, n_src); one warp, 16 loads in
-// flight per lane so the copy is bandwidth-, not latency-bound
+// span[fw_pad(i)] = src[t0 + i] (/ div), zero outside [0, n_src)
 template <typename IO, bool DIV>
-__device__ __forceinline__ void stage_span(IO* __restrict__ dst, const IO* __restrict__ src,
-                                           int64_t t0, int64_t n, int64_t n_src, IO div) {
-    constexpr int U = 64;  // loads in flight per lane (staging is latency-bound)
+__device__ __forceinline__ void fw_stage(IO* __restrict__ dst, const IO* __restrict__ src,
+                                         int64_t t0, int n, int64_t n_src, int hop, IO div) {
+    constexpr int U = 64;  // loads in flight per lane (the staging is latency-bound)
     const int lane = threadIdx.x & 31;
-    for (int64_t i0 = lane; i0 < n; i0 += 32 * U) {
+    for (int i0 = lane; i0 < n; i0 += 32 * U) {
         IO v[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const int64_t i = i0 + 32 * j, t = t0 + i;
+            const int i = i0 + 32 * j;
+            const int64_t t = t0 + i;
             v[j] = (i < n && t >= 0 && t < n_src) ? src[t] : (IO)0;
         }
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const int64_t i = i0 + 32 * j;
-            if (i < n) dst[i] = DIV ? v[j] / div : v[j];
+            const int i = i0 + 32 * j;
+            if (i < n) dst[fw_pad(i, hop)] = DIV ? v[j] / div : v[j];
         }
     }
 }
 
-template <typename IO, int M, bool STAGED>
+// Forward per frame (params.py:230-237): zero-state TI recursion of
+// window[k] * e[f*hop + k] with row frames[max(f, 0)] (lpc.py:50-61), in the
+// same arithmetic as the TI/TV lane kernels (the reference's single
+// rectangular frame == lp_forward_ti holds bit-exactly).
+template <typename IO, int M>
 __global__ void __launch_bounds__(32)
-k_fw_forward(const IO* __restrict__ e, const IO* __restrict__ frames, const IO* __restrict__ win,
-             IO* __restrict__ seg, int64_t B, int64_t T, int F, int nfr, int size, int hop,
-             int n_lead) {
+k_fw_forward(const __grid_constant__ FwMaps maps, const IO* __restrict__ e,
+             const IO* __restrict__ frames, const IO* __restrict__ win, int64_t T, int F,
+             int nfr, int size, int hop, int n_lead) {
     grid_dep_wait();
-    constexpr int L = FwGeo<M>::L;
-    extern __shared__ __align__(16) unsigned char fw_smem[];
+    using S = FwSmem<IO>;
+    constexpr int W = kFwW;
+    constexpr int L = (M + W - 1) / W * W;  // ring (>= M) = unrolled body: positions static
+    extern __shared__ __align__(128) unsigned char fw_smem[];
     const int lane = threadIdx.x;
     const int64_t b = blockIdx.y;
     const int fi0 = blockIdx.x * 32;
     const int fi = fi0 + lane;
     const bool active = fi < nfr;
+    const int rows = min(32, nfr - fi0);
+    const CUtensorMap* om = &maps.seg[rows == 32 ? 0 : 1];
     const int f = fi - n_lead;
     const int row = f > 0 ? f : 0;
-    const int64_t start = (int64_t)f * hop;
-    const int64_t span0 = (int64_t)(fi0 - n_lead) * hop;  // time of the staged span's first sample
-    const IO* eb = e + b * T;
     IO* es = reinterpret_cast<IO*>(fw_smem);
-    IO* ws = es + FwStage<IO>::span(size, hop);
-    if (STAGED) {
-        stage_span<IO, false>(es, eb, span0, FwStage<IO>::span(size, hop), T, (IO)1);
-        stage_span<IO, false>(ws, win, 0, size, size, (IO)1);
-        __syncwarp();
-    }
+    IO* ws = reinterpret_cast<IO*>(fw_smem + S::off_win(size, hop));
+    if (lane == 0) prefetch_tmap(om);
+    fw_stage<IO, false>(es, e + b * T, (int64_t)(fi0 - n_lead) * hop, S::span(size, hop), T, hop,
+                        (IO)1);
+    for (int i = lane; i < size; i += 32) ws[i] = win[i];
+    __syncwarp();
     IO a[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) a[i] = active ? frames[(b * F + row) * M + i] : (IO)0;
-    IO R[M];
+    IO R[L];
 #pragma unroll
-    for (int p = 0; p < M; ++p) R[p] = (IO)0;
-    IO* sb = seg + b * (int64_t)size * nfr + fi;
-    const IO* el = es + (int64_t)lane * hop;  // this frame's excitation in the staged span
-    for (int k0 = 0; k0 < size; k0 += L) {
+    for (int p = 0; p < L; ++p) R[p] = (IO)0;
+    const int base = lane * (hop + 1);  // padded index of this frame's first sample
+    const int nw = (size + W - 1) / W;
+    const int64_t grow = b * nfr + fi0;
+    for (int k0 = 0; k0 < nw * W; k0 += L) {
 #pragma unroll
-        for (int u = 0; u < L; ++u) {
-            const int k = k0 + u;
-            if (k < size) {
-                IO xin;
-                if (STAGED) {
-                    xin = el[k] * ws[k];
-                } else {
-                    const int64_t t = start + k;
-                    xin = ((active && t >= 0 && t < T) ? eb[t] : (IO)0) * win[k];
+        for (int wi = 0; wi < L / W; ++wi) {
+            const int kw = k0 + wi * W;  // window start
+            if (kw < size) {
+                const int so = (kw / W) % kFwOut;
+                IO* obox = reinterpret_cast<IO*>(fw_smem + S::off_out(size, hop) + so * S::OUT);
+                if (kw / W >= kFwOut) {
+                    if (lane == 0) bulk_wait_read<kFwOut - 1>();
+                    __syncwarp();
                 }
-                IO p0 = (IO)0, p1 = (IO)0, p2 = (IO)0, p3 = (IO)0;
+                // padded index of sample k: base + k + k / hop (one division per window)
+                const int kq = kw / hop, kr = kw - kq * hop;
+                IO xv[W];
 #pragma unroll
-                for (int i = M; i >= 2; --i) {
-                    const IO x = R[(u - i + 2 * M) % M];
-                    switch (i & 3) {
-                        case 0: p0 = fma(a[i - 1], x, p0); break;
-                        case 1: p1 = fma(a[i - 1], x, p1); break;
-                        case 2: p2 = fma(a[i - 1], x, p2); break;
-                        default: p3 = fma(a[i - 1], x, p3); break;
+                for (int u = 0; u < W; ++u) {
+                    const int k = kw + u;
+                    const int pk = base + k + kq + (kr + u >= hop ? 1 : 0);
+                    xv[u] = k < size ? es[pk] * ws[k] : (IO)0;
+                }
+                IO ov[W];
+#pragma unroll
+                for (int u = 0; u < W; ++u) {
+                    const int pos = wi * W + u;  // position in the unrolled body
+                    IO p0 = (IO)0, p1 = (IO)0, p2 = (IO)0, p3 = (IO)0;
+#pragma unroll
+                    for (int i = M; i >= 2; --i) {
+                        const IO x = R[(pos - i + 2 * L) % L];
+                        switch (i & 3) {
+                            case 0: p0 = fma(a[i - 1], x, p0); break;
+                            case 1: p1 = fma(a[i - 1], x, p1); break;
+                            case 2: p2 = fma(a[i - 1], x, p2); break;
+                            default: p3 = fma(a[i - 1], x, p3); break;
+                        }
                     }
+                    const IO v = fma(-a[0], R[(pos - 1 + L) % L], xv[u] - ((p0 + p1) + (p2 + p3)));
+                    R[pos % L] = v;
+                    ov[u] = v;
                 }
-                const IO v = fma(-a[0], R[(u - 1 + M) % M], xin - ((p0 + p1) + (p2 + p3)));
-                R[u % M] = v;
-                if (active) sb[(int64_t)k * nfr] = v;
+#pragma unroll
+                for (int u = 0; u < W; ++u) obox[lane * W + u] = ov[u];
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(om, kw, (int)grow, obox);
+                    bulk_commit();
+                }
             }
         }
     }
+    if (lane == 0) bulk_wait<0>();
 }
 
-// out[t] = (sum over frames covering t, in frame order, of seg) / cola
+// out[t] = (sum over the frames covering t, in frame order, of seg) / cola
+// (params.py:236-239).  Block (q, b) covers t = q*hop + r: the frames f =
+// q-j (j descending, so frames ascend) contribute seg row f at k = r + j*hop;
+// consecutive threads read consecutive samples of a row.
 template <typename IO>
-__global__ void k_fw_ola(const IO* __restrict__ seg, IO* __restrict__ out, int64_t B, int64_t T,
-                         int nfr, int size, int hop, int n_lead, IO cola) {
+__global__ void k_fw_ola(const IO* __restrict__ seg, IO* __restrict__ out, int64_t T, int nfr,
+                         int size, int hop, int n_lead, IO cola) {
     grid_dep_wait();
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= B * T) return;
-    const int64_t b = idx / T, t = idx % T;
-    // frames f with f*hop <= t < f*hop + size
-    int64_t fhi = t / hop;
-    int64_t flo = (t - size) >= 0 ? (t - size) / hop + 1 : -((size - t - 1) / hop);
-    if (flo < -n_lead) flo = -n_lead;
-    if (fhi > nfr - n_lead - 1) fhi = nfr - n_lead - 1;
-    IO acc = (IO)0;
-    const IO* sb = seg + b * (int64_t)size * nfr;
-    for (int64_t f = flo; f <= fhi; ++f) {
-        const int64_t k = t - f * hop;
-        acc += sb[k * nfr + (f + n_lead)];
+    const int64_t b = blockIdx.y;
+    const int q = blockIdx.x;
+    const IO* sb = seg + b * (int64_t)nfr * size;
+    const int flo_all = -n_lead, fhi_all = nfr - n_lead - 1;
+    for (int r = threadIdx.x; r < hop; r += blockDim.x) {
+        const int64_t t = (int64_t)q * hop + r;
+        if (t >= T) return;
+        IO acc = (IO)0;
+        for (int j = (size - 1 - r) / hop; j >= 0; --j) {
+            const int f = q - j;
+            if (f < flo_all || f > fhi_all) continue;
+            acc += sb[(int64_t)(f + n_lead) * size + r + j * hop];
+        }
+        out[b * T + t] = acc / cola;
     }
-    out[idx] = acc / cola;
 }
 
-// Adjoint per frame, reverse k:  lambda_0 += g(start+k)/cola (masked);
-// ge_f(k) = lambda_0;  lambda = C^T lambda;  ga += ge_f(k) * s_f(k-1-c).
-// Same warp/frame mapping and staging as the forward (g/cola staged).
-template <typename IO, int M, bool STAGED>
-__global__ void __launch_bounds__(32, 1)
-k_fw_backward(const IO* __restrict__ gout, const IO* __restrict__ frames,
-              const IO* __restrict__ win, const IO* __restrict__ seg, IO* __restrict__ gew,
-              IO* __restrict__ gapart, int64_t B, int64_t T, int F, int nfr, int size, int hop,
-              int n_lead, IO cola) {
+// Adjoint per frame (params.py:259-273 with lpc.py:176-195), reverse k:
+//   lambda_0 += g(start + k) / cola;  ge_f(k) = lambda_0;  lambda = C^T lambda;
+//   ga[c] += ge_f(k) s_f(k-1-c);  gew_f(k) = window[k] ge_f(k).
+// The saved rows s_f stream in (reverse windows) through a ring of tensor
+// copies; each window's steps read s_f(k-1-c) from a register window of the
+// saved outputs, refreshed by one row load per window.
+template <typename IO, int M>
+__global__ void __launch_bounds__(32)
+k_fw_backward(const __grid_constant__ FwMaps maps, const IO* __restrict__ gout,
+              const IO* __restrict__ frames, const IO* __restrict__ win, IO* __restrict__ gapart,
+              int64_t T, int F, int nfr, int size, int hop, int n_lead, IO cola) {
     grid_dep_wait();
-
-    extern __shared__ __align__(16) unsigned char fw_smem[];
+    using S = FwSmem<IO>;
+    constexpr int W = kFwW;
+    constexpr int NB = FwLag<M>::NB, SW = FwLag<M>::SW, NS = FwLag<M>::NS;
+    extern __shared__ __align__(128) unsigned char fw_smem[];
     const int lane = threadIdx.x;
     const int64_t b = blockIdx.y;
     const int fi0 = blockIdx.x * 32;
     const int fi = fi0 + lane;
     const bool active = fi < nfr;
+    const int rows = min(32, nfr - fi0);
+    const int mi = rows == 32 ? 0 : 1;
     const int f = fi - n_lead;
     const int row = f > 0 ? f : 0;
-    const int64_t start = (int64_t)f * hop;
-    const int64_t span0 = (int64_t)(fi0 - n_lead) * hop;
-    const IO* gb = gout + b * T;
     IO* gs = reinterpret_cast<IO*>(fw_smem);
-    IO* ws = gs + FwStage<IO>::span(size, hop);
-    if (STAGED) {
-        stage_span<IO, true>(gs, gb, span0, FwStage<IO>::span(size, hop), T, cola);
-        stage_span<IO, false>(ws, win, 0, size, size, (IO)1);
-        __syncwarp();
+    IO* ws = reinterpret_cast<IO*>(fw_smem + S::off_win(size, hop));
+    unsigned char* segs = fw_smem + S::off_seg(size, hop);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(fw_smem + S::off_bar(size, hop, true));
+    const int nw = (size + W - 1) / W;
+    const int64_t grow = b * nfr + fi0;
+    const uint32_t tx = (uint32_t)rows * W * sizeof(IO);
+    if (lane == 0) {
+        prefetch_tmap(&maps.seg[mi]);
+        prefetch_tmap(&maps.gew[mi]);
+        for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
     }
+    __syncwarp();
+    // loads run from the top window down: window w is the o-th load
+    // (o = nw-1-w) and lives in stage o % NS, completing that stage's
+    // (o / NS)-th phase
+    auto issue = [&](int w) {
+        if (lane == 0 && w >= 0) {
+            const int st = (nw - 1 - w) % NS;
+            mbar_arrive_expect_tx(&bars[st], tx);
+            tma_load_2d(segs + st * S::SEGW, &maps.seg[mi], w * W, (int)grow, &bars[st]);
+        }
+    };
+    for (int i = 0; i < NS; ++i) issue(nw - 1 - i);
+    fw_stage<IO, true>(gs, gout + b * T, (int64_t)(fi0 - n_lead) * hop, S::span(size, hop), T, hop,
+                       cola);
+    for (int i = lane; i < size; i += 32) ws[i] = win[i];
+    __syncwarp();
     IO a[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) a[i] = active ? frames[(b * F + row) * M + i] : (IO)0;
-    const int64_t gid = b * nfr + fi;
-    const IO* sb = seg + b * (int64_t)size * nfr + fi;
-    IO* ob = gew + b * (int64_t)size * nfr + fi;
-    const IO* gl = gs + (int64_t)lane * hop;
-    // ring of past outputs: R[k' mod RS] = s_f(k').  At step k it holds
-    // s_f(k-1 .. k-RS); the slot freed by s_f(k-1) is refilled with
-    // s_f(k-1-RS), which is first needed RS - M steps later, so the global
-    // load has that many steps to land (a ring of exactly M slots exposed the
-    // full memory latency every step).
-    constexpr int RS = FwGeo<M>::RS;
-    const int K0 = (size + RS - 1) / RS * RS;
-    IO R[RS];
-#pragma unroll
-    for (int i = 0; i < RS; ++i) {
-        const int kp = K0 - 2 - i;  // K0 % RS == 0, so the slot of s_f(kp) is static
-        R[(2 * RS - 2 - i) % RS] =
-            (active && kp >= 0 && kp < size) ? sb[(int64_t)kp * nfr] : (IO)0;
-    }
-    IO lam[M];
-    IO ga[M];
+    IO lam[M], ga[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         lam[i] = (IO)0;
         ga[i] = (IO)0;
     }
-    for (int kb = K0 - RS; kb >= 0; kb -= RS) {
+    // window w's saved row of this lane, 0 below window 0 (s(<0) = 0: zi = 0)
+    auto seg_row = [&](int w, IO* dst) {
+        if (w < 0) {
 #pragma unroll
-        for (int u = RS - 1; u >= 0; --u) {
-            const int k = kb + u;
-            if (k < size) {
-                IO gv, wk;
-                if (STAGED) {
-                    gv = gl[k];
-                    wk = ws[k];
-                } else {
-                    const int64_t t = start + k;
-                    gv = (active && t >= 0 && t < T) ? gb[t] / cola : (IO)0;
-                    wk = win[k];
-                }
-                const IO l0 = lam[0] + gv;
-                if (active) ob[(int64_t)k * nfr] = l0 * wk;
-#pragma unroll
-                for (int c = 0; c < M; ++c) ga[c] = fma(R[(u - 1 - c + 2 * RS) % RS], l0, ga[c]);
-#pragma unroll
-                for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
-                lam[M - 1] = -a[M - 1] * l0;
-            }
-            const int kp = k - 1 - RS;
-            R[(u - 1 + 2 * RS) % RS] =
-                (active && kp >= 0 && kp < size) ? sb[(int64_t)kp * nfr] : (IO)0;
+            for (int u = 0; u < W; ++u) dst[u] = (IO)0;
+            return;
         }
+        const int o = nw - 1 - w;
+        mbar_wait(&bars[o % NS], (uint32_t)((o / NS) & 1));
+        const IO* src = reinterpret_cast<const IO*>(segs + (o % NS) * S::SEGW) + lane * W;
+#pragma unroll
+        for (int u = 0; u < W; ++u) dst[u] = src[u];
+    };
+    IO sv[SW];  // sv[i] = s(kw - NB*W + i) for the current window start kw
+#pragma unroll
+    for (int j = 0; j <= NB; ++j) seg_row(nw - 1 - j, sv + (NB - j) * W);
+    const int base = lane * (hop + 1);  // padded index of this frame's first sample
+    for (int wv = nw - 1; wv >= 0; --wv) {
+        const int kw = wv * W;
+        const int so = wv % kFwOut;
+        IO* obox = reinterpret_cast<IO*>(fw_smem + S::off_out(size, hop) + so * S::OUT);
+        if (nw - 1 - wv >= kFwOut) {
+            if (lane == 0) bulk_wait_read<kFwOut - 1>();
+            __syncwarp();
+        }
+        IO gv[W], wk[W], ov[W];
+        const int kq = kw / hop, kr = kw - kq * hop;
+#pragma unroll
+        for (int u = 0; u < W; ++u) {
+            const int k = kw + u;
+            const int pk = base + k + kq + (kr + u >= hop ? 1 : 0);
+            gv[u] = k < size ? gs[pk] : (IO)0;
+            wk[u] = k < size ? ws[k] : (IO)0;
+        }
+#pragma unroll
+        for (int u = W - 1; u >= 0; --u) {
+            const IO l0 = lam[0] + gv[u];
+            ov[u] = l0 * wk[u];
+#pragma unroll
+            for (int c = 0; c < M; ++c) ga[c] = fma(sv[NB * W + u - 1 - c], l0, ga[c]);
+#pragma unroll
+            for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
+            lam[M - 1] = -a[M - 1] * l0;
+        }
+#pragma unroll
+        for (int u = 0; u < W; ++u) obox[lane * W + u] = ov[u];
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(&maps.gew[mi], kw, (int)grow, obox);
+            bulk_commit();
+        }
+        // the stage of window wv is no longer needed: refill it NS windows down
+        __syncwarp();
+        issue(wv - NS);
+        // slide the register window down by W
+#pragma unroll
+        for (int i = SW - 1; i >= W; --i) sv[i] = sv[i - W];
+        seg_row(wv - NB - 1, sv);
     }
+    if (lane == 0) bulk_wait<0>();
     if (active) {
 #pragma unroll
-        for (int c = 0; c < M; ++c) gapart[gid * M + c] = -ga[c];
+        for (int c = 0; c < M; ++c) gapart[(b * nfr + fi) * M + c] = -ga[c];
     }
 }
 
-// grad_e[t] = sum over covering frames (frame order) of gew;  grad_frames[row]
-// = sum over frames mapping to row (lead-in frames hold row 0).
+// grad_e[t] = sum over the frames covering t (frame order) of gew rows
+// (same block geometry as k_fw_ola)
 template <typename IO>
-__global__ void k_fw_gather_ge(const IO* __restrict__ gew, IO* __restrict__ ge, int64_t B,
-                               int64_t T, int nfr, int size, int hop, int n_lead) {
+__global__ void k_fw_gather_ge(const IO* __restrict__ gew, IO* __restrict__ ge, int64_t T, int nfr,
+                               int size, int hop, int n_lead) {
     grid_dep_wait();
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= B * T) return;
-    const int64_t b = idx / T, t = idx % T;
-    int64_t fhi = t / hop;
-    int64_t flo = (t - size) >= 0 ? (t - size) / hop + 1 : -((size - t - 1) / hop);
-    if (flo < -n_lead) flo = -n_lead;
-    if (fhi > nfr - n_lead - 1) fhi = nfr - n_lead - 1;
-    IO acc = (IO)0;
-    const IO* gb = gew + b * (int64_t)size * nfr;
-    for (int64_t f = flo; f <= fhi; ++f) acc += gb[(t - f * hop) * nfr + (f + n_lead)];
-    ge[idx] = acc;
+    const int64_t b = blockIdx.y;
+    const int q = blockIdx.x;
+    const IO* gb = gew + b * (int64_t)nfr * size;
+    const int flo_all = -n_lead, fhi_all = nfr - n_lead - 1;
+    for (int r = threadIdx.x; r < hop; r += blockDim.x) {
+        const int64_t t = (int64_t)q * hop + r;
+        if (t >= T) return;
+        IO acc = (IO)0;
+        for (int j = (size - 1 - r) / hop; j >= 0; --j) {
+            const int f = q - j;
+            if (f < flo_all || f > fhi_all) continue;
+            acc += gb[(int64_t)(f + n_lead) * size + r + j * hop];
+        }
+        ge[b * T + t] = acc;
+    }
 }
 
 template <typename IO>
@@ -289,31 +403,82 @@ __global__ void k_fw_rows(const IO* __restrict__ gapart, IO* __restrict__ gf, in
         default: return cudaErrorInvalidValue;             \
     }
 
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 fw_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+// frame rows [B*nfr][size] of `base`, box {W, rows}
+cudaError_t fw_view(CUtensorMap* m, const void* base, int sz, const FwArgs& a, uint32_t rows) {
+    std::memset(m, 0, sizeof(*m));
+    auto fn = fw_encode();
+    if (!fn) return cudaErrorNotSupported;
+    cuuint64_t gdim[2] = {(cuuint64_t)a.size, (cuuint64_t)(a.B * a.nfr)};
+    cuuint64_t gstr[1] = {(cuuint64_t)a.size * sz};
+    cuuint32_t box[2] = {(cuuint32_t)kFwW, rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, sz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                    2, const_cast<void*>(base), gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+template <typename IO>
+cudaError_t fw_maps(FwMaps& m, const IO* seg, const IO* gew, const FwArgs& a) {
+    const uint32_t rem = (uint32_t)(a.nfr % 32 == 0 ? 32 : a.nfr % 32);
+    const uint32_t box[2] = {32u, rem};
+    for (int i = 0; i < 2; ++i) {
+        cudaError_t err = fw_view(&m.seg[i], seg, (int)sizeof(IO), a, box[i]);
+        if (err != cudaSuccess) return err;
+        if (gew != nullptr) {
+            err = fw_view(&m.gew[i], gew, (int)sizeof(IO), a, box[i]);
+            if (err != cudaSuccess) return err;
+        } else {
+            std::memset(&m.gew[i], 0, sizeof(m.gew[i]));
+        }
+    }
+    return cudaSuccess;
+}
+}  // namespace
+
+// frame sizes whose staged span fits the shared memory (the C ABI checks)
+bool fw_supported(int Mp, int size, int hop, int elem) {
+    if (Mp > 30 || size % 4 != 0 || hop < 1) return false;  // rows: 16-byte strides
+    const size_t b = elem == 8 ? FwSmem<double>::bytes(size, hop, true)
+                               : FwSmem<float>::bytes(size, hop, true);
+    return b <= 220 * 1024;
+}
+
 template <typename IO>
 cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* win, IO* seg,
                               IO* out, const FwArgs& a, cudaStream_t st) {
+    if (!fw_supported(Mp, a.size, a.hop, (int)sizeof(IO))) return cudaErrorInvalidValue;
     const dim3 grid((unsigned)((a.nfr + 31) / 32), (unsigned)a.B);
-    const size_t sm = FwStage<IO>::bytes(a.size, a.hop);
-    const bool staged = sm <= kFwStageMax;
+    const size_t sm = FwSmem<IO>::bytes(a.size, a.hop, false);
+    FwMaps maps;
+    cudaError_t err = fw_maps<IO>(maps, seg, nullptr, a);
+    if (err != cudaSuccess) return err;
     TVLP_FW_DISPATCH(Mp, {
-        if (staged) {
-            auto k = k_fw_forward<IO, M_, true>;
-            cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)sm);
-            if (err != cudaSuccess) return err;
-            launch_pdl(k, grid, 32, sm, st, e, frames, win, seg, a.B, a.T, a.F, a.nfr, a.size,
-                       a.hop, a.n_lead);
-        } else {
-            launch_pdl(k_fw_forward<IO, M_, false>, grid, 32, 0, st, e, frames, win, seg, a.B,
-                       a.T, a.F, a.nfr, a.size, a.hop, a.n_lead);
-        }
+        auto k = k_fw_forward<IO, M_>;
+        err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (err != cudaSuccess) return err;
+        launch_pdl(k, grid, 32, sm, st, maps, e, frames, win, a.T, a.F, a.nfr, a.size, a.hop,
+                   a.n_lead);
         break;
     })
-    cudaError_t err = cudaGetLastError();
+    err = cudaGetLastError();
     if (err != cudaSuccess) return err;
-    const int64_t n = a.B * a.T;
-    launch_pdl(k_fw_ola<IO>, (unsigned)((n + 255) / 256), 256, 0, st, seg, out, a.B, a.T, a.nfr, a.size,
-                                                              a.hop, a.n_lead, (IO)a.cola);
+    const dim3 og((unsigned)((a.T + a.hop - 1) / a.hop), (unsigned)a.B);
+    launch_pdl(k_fw_ola<IO>, og, (unsigned)std::min(a.hop, 256), 0, st, seg, out, a.T, a.nfr,
+               a.size, a.hop, a.n_lead, (IO)a.cola);
     return cudaGetLastError();
 }
 
@@ -321,33 +486,30 @@ template <typename IO>
 cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, const IO* win,
                                const IO* seg, IO* gew, IO* gapart, IO* ge, IO* gf,
                                const FwArgs& a, cudaStream_t st) {
+    if (!fw_supported(Mp, a.size, a.hop, (int)sizeof(IO))) return cudaErrorInvalidValue;
     const dim3 grid((unsigned)((a.nfr + 31) / 32), (unsigned)a.B);
-    const size_t sm = FwStage<IO>::bytes(a.size, a.hop);
-    const bool staged = sm <= kFwStageMax;
+    const size_t sm = FwSmem<IO>::bytes(a.size, a.hop, true);
+    FwMaps maps;
+    cudaError_t err = fw_maps<IO>(maps, seg, gew, a);
+    if (err != cudaSuccess) return err;
     TVLP_FW_DISPATCH(Mp, {
-        if (staged) {
-            auto k = k_fw_backward<IO, M_, true>;
-            cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)sm);
-            if (err != cudaSuccess) return err;
-            launch_pdl(k, grid, 32, sm, st, gout, frames, win, seg, gew, gapart, a.B, a.T, a.F,
-                       a.nfr, a.size, a.hop, a.n_lead, (IO)a.cola);
-        } else {
-            launch_pdl(k_fw_backward<IO, M_, false>, grid, 32, 0, st, gout, frames, win, seg, gew,
-                       gapart, a.B, a.T, a.F, a.nfr, a.size, a.hop, a.n_lead, (IO)a.cola);
-        }
+        auto k = k_fw_backward<IO, M_>;
+        err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (err != cudaSuccess) return err;
+        launch_pdl(k, grid, 32, sm, st, maps, gout, frames, win, gapart, a.T, a.F, a.nfr, a.size,
+                   a.hop, a.n_lead, (IO)a.cola);
         break;
     })
-    cudaError_t err = cudaGetLastError();
+    err = cudaGetLastError();
     if (err != cudaSuccess) return err;
-    const int64_t n = a.B * a.T;
-    launch_pdl(k_fw_gather_ge<IO>, (unsigned)((n + 255) / 256), 256, 0, st, gew, ge, a.B, a.T, a.nfr,
-                                                                    a.size, a.hop, a.n_lead);
+    const dim3 og((unsigned)((a.T + a.hop - 1) / a.hop), (unsigned)a.B);
+    launch_pdl(k_fw_gather_ge<IO>, og, (unsigned)std::min(a.hop, 256), 0, st, gew, ge, a.T, a.nfr,
+               a.size, a.hop, a.n_lead);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     const int64_t nr = a.B * (int64_t)a.F * Mp;
-    launch_pdl(k_fw_rows<IO>, (unsigned)((nr + 255) / 256), 256, 0, st, gapart, gf, a.B, a.F, a.nfr, Mp,
-                                                                a.n_lead);
+    launch_pdl(k_fw_rows<IO>, (unsigned)((nr + 255) / 256), 256, 0, st, gapart, gf, a.B, a.F,
+               a.nfr, Mp, a.n_lead);
     (void)M;
     return cudaGetLastError();
 }

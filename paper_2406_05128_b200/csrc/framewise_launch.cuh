@@ -11,11 +11,13 @@ struct FwArgs {
     double cola;
 };
 
-// seg: [B, size, nfr] saved frame outputs; out: [B, T]
+// frame sizes / orders / element sizes the kernels handle
+bool fw_supported(int Mp, int size, int hop, int elem);
+// seg: [B, nfr, size] saved frame outputs (frame-major); out: [B, T]
 template <typename IO>
 cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* win, IO* seg,
                               IO* out, const FwArgs& a, cudaStream_t st);
-// gew: [B, size, nfr] scratch, gapart: [B, nfr, Mp] scratch; ge: [B, T]; gf: [B, F, Mp]
+// gew: [B, nfr, size] scratch, gapart: [B, nfr, Mp] scratch; ge: [B, T]; gf: [B, F, Mp]
 template <typename IO>
 cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, const IO* win,
                                const IO* seg, IO* gew, IO* gapart, IO* ge, IO* gf,

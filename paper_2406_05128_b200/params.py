@@ -189,7 +189,7 @@ def _check(e, frames, plan):
 
 
 def framewise_forward(e, frames, plan):
-    """Returns ``(out, seg)``; ``seg`` [B, frame_size, n_frames] holds the
+    """Returns ``(out, seg)``; ``seg`` [B, n_frames, frame_size] holds the
     per-frame outputs the VJP needs (the reference's ``seg_outputs``)."""
     conv = _Conv(e, frames)
     e = conv.t(e)
@@ -204,7 +204,7 @@ def framewise_forward(e, frames, plan):
     lib = N.load()
     nfr = lib.tvlp_framewise_nframes(T, F, plan.frame_size, plan.hop)
     out = torch.empty_like(e)
-    seg = torch.empty((B, plan.frame_size, nfr), dtype=e.dtype, device=conv.device)
+    seg = torch.empty((B, nfr, plan.frame_size), dtype=e.dtype, device=conv.device)
     w = plan._window_tensor(e.dtype, conv.device)
     dt = N.dtype_code(e.dtype)
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FW_FWD, dt, B, T, M, F, plan.frame_size,

@@ -117,7 +117,11 @@ def test_golden_framewise(golden_framewise):
             ry, rsegs = oracle.framewise_forward(e.astype(np.float64), fr.astype(np.float64), hop)
             rge, rgf = oracle.framewise_backward(g.astype(np.float64), fr.astype(np.float64),
                                                  rsegs, hop)
-            tol = TOL32
+            # case 3 holds a near-resonant row: the reference's own float32
+            # kernel is at 1.0e-4 there; float32 may not add to that
+            y32, s32 = oracle.framewise_forward(e, fr, hop)
+            ge32, gf32 = oracle.framewise_backward(g, fr, s32, hop)
+            tol = max(TOL32, 1.5 * max(_err(y32, ry), _err(ge32, rge), _err(gf32, rgf)))
         assert _err(_np(y), ry) < tol, (i, "y")
         assert _err(_np(ge), rge) < tol, (i, "ge")
         assert _err(_np(gf), rgf) < tol, (i, "gf")
