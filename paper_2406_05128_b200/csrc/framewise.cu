@@ -33,6 +33,18 @@ namespace tvlp {
 // ============================================================================
 constexpr int kFwW = 8;        // steps per compute window
 constexpr int kFwOut = 2;      // output box stages
+// output boxes: rows of 128 B (32 fp32 / 16 fp64 steps), 128B-swizzled in
+// shared memory (conflict-free row writes): one proxy fence + tensor store
+// per 128 B of steps instead of per compute window
+template <typename IO>
+struct FwOut {
+    static constexpr int OW = 128 / (int)sizeof(IO);  // steps per output box
+    // shared-memory element (row r, step c) of a 128B-swizzled [32][128 B] box
+    static __device__ __forceinline__ int at(int r, int c) {
+        const int byte = c * (int)sizeof(IO);
+        return (r * 128 + ((((byte >> 4) ^ (r & 7)) << 4) | (byte & 15))) / (int)sizeof(IO);
+    }
+};
 
 // backward: windows of saved outputs below the current one that the lags reach
 template <int M>
@@ -44,28 +56,38 @@ struct FwLag {
 constexpr int kFwSegStages = FwLag<30>::NS;  // shared-memory ring slots (the largest order)
 
 struct FwMaps {
-    CUtensorMap seg[2];  // [B*nfr][size] box {W, 32} / {W, nfr % 32}
-    CUtensorMap gew[2];
+    CUtensorMap seg[2];   // [B*nfr][size] box {W, 32} / {W, nfr % 32} (backward loads)
+    CUtensorMap segw[2];  // same rows, box {128 B, 32 / nfr % 32}, 128B swizzle (stores)
+    CUtensorMap gew[2];   // gew rows, stores like segw
 };
 
-// padded index of time t (relative to the span start) in the staged span
-__device__ __forceinline__ int fw_pad(int t, int hop) { return t + t / hop; }
+// The staged span keeps hop-blocks at a stride of fw_stride(hop) elements:
+// blocks start 16-byte aligned (one bulk copy each) and lane f's reads land
+// in different banks for 8 consecutive lanes.
+template <typename IO>
+__host__ __device__ __forceinline__ int fw_stride(int hop) {
+    constexpr int q = 16 / (int)sizeof(IO);  // elements per 16 bytes
+    int s = (hop + q - 1) / q * q;
+    if (((s / q) & 1) == 0) s += q;
+    return s;
+}
 
 template <typename IO>
 struct FwSmem {
     static __host__ __device__ int span(int size, int hop) { return 31 * hop + size; }
+    static __host__ __device__ int blocks(int size, int hop) { return (span(size, hop) + hop - 1) / hop; }
     static __host__ __device__ int padded(int size, int hop) {
-        const int n = span(size, hop);
-        return (n + n / hop + 4) / 4 * 4;
+        return blocks(size, hop) * fw_stride<IO>(hop);
     }
-    static constexpr int OUT = 32 * kFwW * (int)sizeof(IO);
+    static constexpr int OUT = 32 * 128;  // one output box: 32 rows x 128 B
     static constexpr int SEGW = 32 * kFwW * (int)sizeof(IO);  // one window of 32 rows
     // [span (padded)][window][out boxes][seg ring][barriers]
     static __host__ __device__ size_t off_win(int size, int hop) {
         return (size_t)padded(size, hop) * sizeof(IO);
     }
     static __host__ __device__ size_t off_out(int size, int hop) {
-        return (off_win(size, hop) + (size_t)size * sizeof(IO) + 127) / 128 * 128;
+        // (128B-swizzled boxes need 1024-byte alignment)
+        return (off_win(size, hop) + (size_t)size * sizeof(IO) + 1023) / 1024 * 1024;
     }
     static __host__ __device__ size_t off_seg(int size, int hop) {
         return off_out(size, hop) + kFwOut * OUT;
@@ -78,25 +100,45 @@ struct FwSmem {
     }
 };
 
-// span[fw_pad(i)] = src[t0 + i] (/ div), zero outside [0, n_src)
+// Stage hop-blocks q = 0..nblk-1 of src (block q: times t0 + q*hop + [0, hop))
+// at dst + q*stride, zero outside [0, n_src): blocks inside [0, n_src) with
+// 16-byte aligned sources travel as one bulk copy each (lane 0, completing on
+// `bar`), the rest by warp loads; with DIV the span is then divided by `div`
+// in place (the reference's g = grad / cola, params.py:263).
 template <typename IO, bool DIV>
 __device__ __forceinline__ void fw_stage(IO* __restrict__ dst, const IO* __restrict__ src,
-                                         int64_t t0, int n, int64_t n_src, int hop, IO div) {
-    constexpr int U = 64;  // loads in flight per lane (the staging is latency-bound)
+                                         int64_t t0, int nblk, int64_t n_src, int hop, IO div,
+                                         uint64_t* bar) {
     const int lane = threadIdx.x & 31;
-    for (int i0 = lane; i0 < n; i0 += 32 * U) {
-        IO v[U];
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            const int i = i0 + 32 * j;
-            const int64_t t = t0 + i;
-            v[j] = (i < n && t >= 0 && t < n_src) ? src[t] : (IO)0;
+    const int st = fw_stride<IO>(hop);
+    const uint32_t bbytes = (uint32_t)hop * sizeof(IO);
+    auto bulk_ok = [&](int q) {
+        const int64_t t = t0 + (int64_t)q * hop;
+        return t >= 0 && t + hop <= n_src && bbytes % 16 == 0 &&
+               ((reinterpret_cast<uintptr_t>(src + t) & 15) == 0);
+    };
+    if (lane == 0) {
+        uint32_t tx = 0;
+        for (int q = 0; q < nblk; ++q) tx += bulk_ok(q) ? bbytes : 0;
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, tx);
+        for (int q = 0; q < nblk; ++q)
+            if (bulk_ok(q)) tma_load_1d(dst + q * st, src + t0 + (int64_t)q * hop, bbytes, bar);
+    }
+    for (int q = 0; q < nblk; ++q) {
+        if (bulk_ok(q)) continue;  // warp-uniform
+        for (int r = lane; r < hop; r += 32) {
+            const int64_t t = t0 + (int64_t)q * hop + r;
+            dst[q * st + r] = (t >= 0 && t < n_src) ? src[t] : (IO)0;
         }
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            const int i = i0 + 32 * j;
-            if (i < n) dst[fw_pad(i, hop)] = DIV ? v[j] / div : v[j];
-        }
+    }
+    __syncwarp();
+    mbar_wait(bar, 0);
+    if (DIV) {
+        for (int q = 0; q < nblk; ++q)
+            for (int r = lane; r < hop; r += 32) dst[q * st + r] = dst[q * st + r] / div;
+        __syncwarp();
     }
 }
 
@@ -120,14 +162,16 @@ k_fw_forward(const __grid_constant__ FwMaps maps, const IO* __restrict__ e,
     const int fi = fi0 + lane;
     const bool active = fi < nfr;
     const int rows = min(32, nfr - fi0);
-    const CUtensorMap* om = &maps.seg[rows == 32 ? 0 : 1];
+    const CUtensorMap* om = &maps.segw[rows == 32 ? 0 : 1];
+    using O = FwOut<IO>;
     const int f = fi - n_lead;
     const int row = f > 0 ? f : 0;
     IO* es = reinterpret_cast<IO*>(fw_smem);
     IO* ws = reinterpret_cast<IO*>(fw_smem + S::off_win(size, hop));
     if (lane == 0) prefetch_tmap(om);
-    fw_stage<IO, false>(es, e + b * T, (int64_t)(fi0 - n_lead) * hop, S::span(size, hop), T, hop,
-                        (IO)1);
+    uint64_t* sbar = reinterpret_cast<uint64_t*>(fw_smem + S::off_bar(size, hop, false));
+    fw_stage<IO, false>(es, e + b * T, (int64_t)(fi0 - n_lead) * hop, S::blocks(size, hop), T, hop,
+                        (IO)1, sbar);
     for (int i = lane; i < size; i += 32) ws[i] = win[i];
     __syncwarp();
     IO a[M];
@@ -136,7 +180,8 @@ k_fw_forward(const __grid_constant__ FwMaps maps, const IO* __restrict__ e,
     IO R[L];
 #pragma unroll
     for (int p = 0; p < L; ++p) R[p] = (IO)0;
-    const int base = lane * (hop + 1);  // padded index of this frame's first sample
+    const int hst = fw_stride<IO>(hop);
+    const int base = lane * hst;  // staged index of this frame's first sample
     const int nw = (size + W - 1) / W;
     const int64_t grow = b * nfr + fi0;
     for (int k0 = 0; k0 < nw * W; k0 += L) {
@@ -144,19 +189,20 @@ k_fw_forward(const __grid_constant__ FwMaps maps, const IO* __restrict__ e,
         for (int wi = 0; wi < L / W; ++wi) {
             const int kw = k0 + wi * W;  // window start
             if (kw < size) {
-                const int so = (kw / W) % kFwOut;
-                IO* obox = reinterpret_cast<IO*>(fw_smem + S::off_out(size, hop) + so * S::OUT);
-                if (kw / W >= kFwOut) {
+                const int ob = kw / O::OW;  // output box of this window
+                IO* obox = reinterpret_cast<IO*>(fw_smem + S::off_out(size, hop) +
+                                                 (ob % kFwOut) * S::OUT);
+                if (kw % O::OW == 0 && ob >= kFwOut) {  // first window into a reused box
                     if (lane == 0) bulk_wait_read<kFwOut - 1>();
                     __syncwarp();
                 }
-                // padded index of sample k: base + k + k / hop (one division per window)
+                // staged index of sample k (one division per window)
                 const int kq = kw / hop, kr = kw - kq * hop;
                 IO xv[W];
 #pragma unroll
                 for (int u = 0; u < W; ++u) {
                     const int k = kw + u;
-                    const int pk = base + k + kq + (kr + u >= hop ? 1 : 0);
+                    const int pk = base + kq * hst + kr + u + (kr + u >= hop ? hst - hop : 0);
                     xv[u] = k < size ? es[pk] * ws[k] : (IO)0;
                 }
                 IO ov[W];
@@ -179,12 +225,14 @@ k_fw_forward(const __grid_constant__ FwMaps maps, const IO* __restrict__ e,
                     ov[u] = v;
                 }
 #pragma unroll
-                for (int u = 0; u < W; ++u) obox[lane * W + u] = ov[u];
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_2d(om, kw, (int)grow, obox);
-                    bulk_commit();
+                for (int u = 0; u < W; ++u) obox[O::at(lane, kw % O::OW + u)] = ov[u];
+                if ((kw + W) % O::OW == 0 || kw + W >= size) {  // box complete: store it
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(om, ob * O::OW, (int)grow, obox);
+                        bulk_commit();
+                    }
                 }
             }
         }
@@ -267,8 +315,8 @@ k_fw_backward(const __grid_constant__ FwMaps maps, const IO* __restrict__ gout,
         }
     };
     for (int i = 0; i < NS; ++i) issue(nw - 1 - i);
-    fw_stage<IO, true>(gs, gout + b * T, (int64_t)(fi0 - n_lead) * hop, S::span(size, hop), T, hop,
-                       cola);
+    fw_stage<IO, true>(gs, gout + b * T, (int64_t)(fi0 - n_lead) * hop, S::blocks(size, hop), T, hop,
+                       cola, bars + NS);
     for (int i = lane; i < size; i += 32) ws[i] = win[i];
     __syncwarp();
     IO a[M];
@@ -296,12 +344,17 @@ k_fw_backward(const __grid_constant__ FwMaps maps, const IO* __restrict__ gout,
     IO sv[SW];  // sv[i] = s(kw - NB*W + i) for the current window start kw
 #pragma unroll
     for (int j = 0; j <= NB; ++j) seg_row(nw - 1 - j, sv + (NB - j) * W);
-    const int base = lane * (hop + 1);  // padded index of this frame's first sample
+    const int hst = fw_stride<IO>(hop);
+    const int base = lane * hst;  // staged index of this frame's first sample
+    using O = FwOut<IO>;
+    const int nob = (size + O::OW - 1) / O::OW;  // output boxes (filled top down)
     for (int wv = nw - 1; wv >= 0; --wv) {
         const int kw = wv * W;
-        const int so = wv % kFwOut;
-        IO* obox = reinterpret_cast<IO*>(fw_smem + S::off_out(size, hop) + so * S::OUT);
-        if (nw - 1 - wv >= kFwOut) {
+        const int ob = kw / O::OW;
+        const int oo = nob - 1 - ob;  // ordinal of this box
+        IO* obox = reinterpret_cast<IO*>(fw_smem + S::off_out(size, hop) + (oo % kFwOut) * S::OUT);
+        const bool box_top = kw + W >= size || (kw + W) % O::OW == 0;  // first window into it
+        if (box_top && oo >= kFwOut) {
             if (lane == 0) bulk_wait_read<kFwOut - 1>();
             __syncwarp();
         }
@@ -310,7 +363,7 @@ k_fw_backward(const __grid_constant__ FwMaps maps, const IO* __restrict__ gout,
 #pragma unroll
         for (int u = 0; u < W; ++u) {
             const int k = kw + u;
-            const int pk = base + k + kq + (kr + u >= hop ? 1 : 0);
+            const int pk = base + kq * hst + kr + u + (kr + u >= hop ? hst - hop : 0);
             gv[u] = k < size ? gs[pk] : (IO)0;
             wk[u] = k < size ? ws[k] : (IO)0;
         }
@@ -325,12 +378,14 @@ k_fw_backward(const __grid_constant__ FwMaps maps, const IO* __restrict__ gout,
             lam[M - 1] = -a[M - 1] * l0;
         }
 #pragma unroll
-        for (int u = 0; u < W; ++u) obox[lane * W + u] = ov[u];
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) {
-            tma_store_2d(&maps.gew[mi], kw, (int)grow, obox);
-            bulk_commit();
+        for (int u = 0; u < W; ++u) obox[O::at(lane, kw % O::OW + u)] = ov[u];
+        if (kw % O::OW == 0) {  // the box's bottom window: store it
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&maps.gew[mi], ob * O::OW, (int)grow, obox);
+                bulk_commit();
+            }
         }
         // the stage of window wv is no longer needed: refill it NS windows down
         __syncwarp();
@@ -416,30 +471,33 @@ PFN_cuTensorMapEncodeTiled_v12000 fw_encode() {
     }
     return fn;
 }
-// frame rows [B*nfr][size] of `base`, box {W, rows}
-cudaError_t fw_view(CUtensorMap* m, const void* base, int sz, const FwArgs& a, uint32_t rows) {
+// frame rows [B*nfr][size] of `base`, box {box0, rows}
+cudaError_t fw_view(CUtensorMap* m, const void* base, int sz, const FwArgs& a, uint32_t box0,
+                    uint32_t rows, bool swz) {
     std::memset(m, 0, sizeof(*m));
     auto fn = fw_encode();
     if (!fn) return cudaErrorNotSupported;
     cuuint64_t gdim[2] = {(cuuint64_t)a.size, (cuuint64_t)(a.B * a.nfr)};
     cuuint64_t gstr[1] = {(cuuint64_t)a.size * sz};
-    cuuint32_t box[2] = {(cuuint32_t)kFwW, rows};
+    cuuint32_t box[2] = {box0, rows};
     cuuint32_t es[2] = {1, 1};
     CUresult r = fn(m, sz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                     2, const_cast<void*>(base), gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 template <typename IO>
 cudaError_t fw_maps(FwMaps& m, const IO* seg, const IO* gew, const FwArgs& a) {
     const uint32_t rem = (uint32_t)(a.nfr % 32 == 0 ? 32 : a.nfr % 32);
     const uint32_t box[2] = {32u, rem};
+    const uint32_t ow = (uint32_t)FwOut<IO>::OW;
     for (int i = 0; i < 2; ++i) {
-        cudaError_t err = fw_view(&m.seg[i], seg, (int)sizeof(IO), a, box[i]);
+        cudaError_t err = fw_view(&m.seg[i], seg, (int)sizeof(IO), a, kFwW, box[i], false);
+        if (err == cudaSuccess) err = fw_view(&m.segw[i], seg, (int)sizeof(IO), a, ow, box[i], true);
         if (err != cudaSuccess) return err;
         if (gew != nullptr) {
-            err = fw_view(&m.gew[i], gew, (int)sizeof(IO), a, box[i]);
+            err = fw_view(&m.gew[i], gew, (int)sizeof(IO), a, ow, box[i], true);
             if (err != cudaSuccess) return err;
         } else {
             std::memset(&m.gew[i], 0, sizeof(m.gew[i]));
