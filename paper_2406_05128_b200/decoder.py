@@ -1,0 +1,310 @@
+"""The rest of the GOLF decoder on the GPU.
+
+The reference renders its source-filter (SF) and harmonic-plus-noise (HpN)
+decoders on a numpy tape (pkg/src/tvlp/synth.py:217-275) from these pieces:
+
+* wavetable oscillator at ``oversample`` x the output rate, read with
+  bilinear interpolation (source.py:224-268) and decimated by a 127-tap
+  windowed-sinc lowpass (source.py:215-222, 271-291);
+* frame-wise shaped Gaussian noise: linear-phase FIRs from 256 log-magnitude
+  bins per frame, overlap-added with the raised-cosine plan (source.py:349-428);
+* the trainable 128-tap global FIR at the output (source.py:445-459);
+* the multi-resolution spectral loss at prime FFT sizes 509/1021/2053
+  (loss.py:25-132; no zero-padding: the transforms run at the native sizes).
+
+Here they are batched torch operations on CUDA tensors (cuFFT/cuDNN
+library kernels -- SURVEY.md §8(f): "torch/cuFFT first, fuse only if
+profiled hot"), differentiated by torch autograd; the LP filters are this
+package's sm_100a kernels (the fused upsample+LP ``autograd.lp_tv_frames``
+and the grouped pair ``autograd.lp_tv_grouped`` for a C(z) LP).
+Every op follows the reference's arithmetic order closely enough that the
+float64 decoder matches the reference tape to ~1e-12 (tests/test_decoder_gpu.py).
+Inputs of shape [B, ...] render B items at once.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.nn.functional as TF
+
+from . import autograd as ag
+
+__all__ = [
+    "NOISE_BINS", "FIR_TAPS", "design_lowpass", "oscillator_phase", "upsample_linear",
+    "wavetable_read", "decimate_fir", "fir_from_logmag", "shape_noise", "generate_noise",
+    "global_fir", "stft_mag", "mss_loss", "Decoder",
+]
+
+NOISE_BINS = 256          # source.py:52
+FIR_TAPS = 128            # synth.py FIR_TAPS
+SQUASH_LIMIT = 0.999      # params.py:31
+DEFAULT_FFT_SIZES = (509, 1021, 2053)  # loss.py:22
+LOG_EPS = 1e-8            # loss.py:23
+
+
+def design_lowpass(num_taps=127, cutoff=0.45, oversample=4):
+    """Windowed-sinc decimation lowpass (source.py:215-222), float64 numpy."""
+    fc = cutoff / (2.0 * oversample)
+    n = np.arange(num_taps) - (num_taps - 1) / 2.0
+    h = 2.0 * fc * np.sinc(2.0 * fc * n) * np.blackman(num_taps)
+    return h / h.sum()
+
+
+def _weights(F, hop, T1, device, dtype):
+    """params.py:107-117 on the device: anchors f0, f1 and weights for T1 samples."""
+    t = torch.arange(T1, device=device)
+    f0 = torch.div(t, hop, rounding_mode="floor")
+    w = (t - f0 * hop).to(dtype) / float(hop)
+    f1 = torch.clamp(f0 + 1, max=F - 1)
+    w = torch.where(f0 == F - 1, torch.zeros_like(w), w)
+    return f0, f1, w
+
+
+def upsample_linear(frames, hop, T1):
+    """params.py:120-132 for [B, F] or [B, F, D] frame controls -> [B, T1(, D)]
+    (T1 = T + 1 samples).  Differentiable (the VJP is the scatter of
+    params.py:135-145, by autograd)."""
+    F = frames.shape[1]
+    if F != (T1 - 1) // hop + 1:
+        raise ValueError(f"got {F} frames but T={T1 - 1} at hop={hop} requires "
+                         f"{(T1 - 1) // hop + 1}")
+    f0, f1, w = _weights(F, hop, T1, frames.device, frames.dtype)
+    if frames.dim() == 3:
+        w = w[:, None]
+    return (1.0 - w) * frames[:, f0] + w * frames[:, f1]
+
+
+def oscillator_phase(f0_frames, hop, n_out, fs, oversample):
+    """Per-sample table phase (periods, mod 1) at the oversampled rate
+    (source.py:224-238): float64 cumulative sum on the device."""
+    f0_frames = torch.as_tensor(f0_frames, dtype=torch.float64)
+    if f0_frames.dim() == 1:
+        f0_frames = f0_frames[None]
+    if bool((f0_frames >= fs / 2.0).any()):
+        raise ValueError("f0 at or above the output Nyquist frequency")
+    if bool((f0_frames < 0).any()):
+        raise ValueError("f0 must be nonnegative")
+    n_os = n_out * oversample
+    f0 = upsample_linear(f0_frames, hop * oversample, n_os)
+    return torch.remainder(torch.cumsum(f0 / (fs * oversample), dim=-1), 1.0)
+
+
+class _WavetableRead(torch.autograd.Function):
+    """source.py:241-268: bilinear read; d(out)/d(pos) = the row difference
+    (the reference keeps it through the position clip)."""
+
+    @staticmethod
+    def forward(ctx, pos, tables, phase):
+        K, L = tables.shape
+        p = torch.clamp(pos, 0.0, K - 1.0)
+        r0 = torch.clamp(torch.floor(p).long(), max=K - 1)
+        r1 = torch.clamp(r0 + 1, max=K - 1)
+        wr = p - r0.to(p.dtype)
+        x = phase * L
+        fx = torch.floor(x)
+        i0 = torch.remainder(fx.long(), L)
+        i1 = torch.remainder(i0 + 1, L)
+        wi = x - fx
+        low = (1.0 - wi) * tables[r0, i0] + wi * tables[r0, i1]
+        high = (1.0 - wi) * tables[r1, i0] + wi * tables[r1, i1]
+        ctx.save_for_backward(high - low)
+        return (1.0 - wr) * low + wr * high
+
+    @staticmethod
+    def backward(ctx, grad):
+        (delta,) = ctx.saved_tensors
+        return grad * delta, None, None
+
+
+def wavetable_read(pos, tables, phase):
+    return _WavetableRead.apply(pos, tables, phase)
+
+
+def decimate_fir(x, taps, factor, n_out):
+    """source.py:271-291: full convolution with ``taps`` (odd length, group
+    delay gd), every ``factor``-th sample from gd.  x [B, N] -> [B, n_out]."""
+    nt = taps.shape[0]
+    gd = (nt - 1) // 2
+    xp = TF.pad(x[:, None], (nt - 1, nt - 1))[:, :, gd:]
+    y = TF.conv1d(xp, taps.flip(0)[None, None], stride=factor)
+    return y[:, 0, :n_out]
+
+
+def generate_noise(n, seed):
+    """source.py:349-352: unit Gaussian noise from numpy's Philox keyed by the
+    seed (a host-side generator: the bits of the reference's noise)."""
+    gen = np.random.Generator(np.random.Philox(key=seed))
+    return gen.standard_normal(n)
+
+
+def fir_from_logmag(logmag):
+    """source.py:355-364: linear-phase FIR bank [.., 2(B-1)] from log-magnitude
+    rows [.., B]: irfft of exp(logmag), centred, Hann-windowed."""
+    B = logmag.shape[-1]
+    n_fir = 2 * (B - 1)
+    zero_phase = torch.fft.irfft(torch.exp(logmag).to(torch.complex128
+                                                       if logmag.dtype == torch.float64
+                                                       else torch.complex64),
+                                 n=n_fir, dim=-1)
+    centered = torch.roll(zero_phase, B - 1, dims=-1)
+    window = torch.as_tensor(np.hanning(n_fir), dtype=logmag.dtype, device=logmag.device)
+    return centered * window
+
+
+def _frame_index(plan, n_out, F, device):
+    """Per-frame (row, sample index into [0, n_out) or -1) of plan.iter_frames."""
+    size = plan.frame_size
+    rows, idx = [], []
+    for row, sig_lo, sig_hi, win_lo, win_hi in plan.iter_frames(n_out, F):
+        ix = np.full(size, -1, dtype=np.int64)
+        ix[win_lo:win_hi] = np.arange(sig_lo, sig_hi)
+        rows.append(row)
+        idx.append(ix)
+    return (torch.as_tensor(np.array(rows), device=device),
+            torch.as_tensor(np.stack(idx), device=device))
+
+
+def shape_noise(logmag, noise, plan):
+    """source.py:367-428 for [B, F, 256] log-magnitudes and [B, n_out] unit
+    noise: each windowed noise frame convolved with its frame's FIR (the
+    centred part, delay 255), overlap-added, / COLA constant."""
+    Bn, F, nb = logmag.shape
+    if nb != NOISE_BINS:
+        raise ValueError(f"noise filter frames must be (F, {NOISE_BINS})")
+    n_out = noise.shape[-1]
+    if F != (n_out - 1) // plan.hop + 1:
+        raise ValueError(f"got {F} noise filter frames but length {n_out} at hop {plan.hop}")
+    size = plan.frame_size
+    delay = NOISE_BINS - 1
+    dev, dt = logmag.device, logmag.dtype
+    rows, idx = _frame_index(plan, n_out, F, dev)
+    fir = fir_from_logmag(logmag)                                 # [B, F, 510]
+    win = torch.as_tensor(np.asarray(plan.window), dtype=dt, device=dev)
+    valid = idx >= 0
+    segs = torch.where(valid, noise[:, idx.clamp(min=0)], torch.zeros((), dtype=dt, device=dev))
+    segs = segs * win                                            # [B, nfr, size]
+    n_fir = fir.shape[-1]
+    nfft = 1 << (size + n_fir - 2).bit_length()
+    spec = torch.fft.rfft(segs, n=nfft) * torch.fft.rfft(fir[:, rows], n=nfft)
+    y = torch.fft.irfft(spec, n=nfft)[..., delay:delay + size]   # [B, nfr, size]
+    out = torch.zeros((Bn, n_out + 1), dtype=dt, device=dev)     # (slot n_out: padding)
+    tgt = torch.where(valid, idx, torch.full_like(idx, n_out))
+    # frames f, f + nc, f + 2nc, ... never overlap: nc collision-free (hence
+    # deterministic) scatter-adds
+    nc = -(-size // plan.hop)
+    for j in range(nc):
+        out = out.index_add(1, tgt[j::nc].reshape(-1), y[:, j::nc].reshape(Bn, -1))
+    return out[:, :n_out] / plan.cola_constant()
+
+
+def global_fir(x, taps):
+    """source.py:445-459: causal same-length convolution, x [B, n], taps [B, m]."""
+    Bn, n = x.shape
+    m = taps.shape[-1]
+    xp = TF.pad(x, (m - 1, 0))
+    # grouped conv: one filter per item (the taps are per-item parameters)
+    y = TF.conv1d(xp[None], taps.flip(-1)[:, None], groups=Bn)
+    return y[0, :, :n]
+
+
+def stft_mag(x, size, hop=None, window=None):
+    """loss.py:53-65: reflect-padded centred frames, raised-cosine window,
+    |rfft| at the native size (cuFFT handles the prime sizes).  x [B, n]."""
+    if hop is None:
+        hop = -(-size // 4)
+    if x.shape[-1] < size:
+        raise ValueError(f"signal of length {x.shape[-1]} is shorter than one {size}-sample frame")
+    if window is None:
+        window = 0.5 - 0.5 * torch.cos(2.0 * math.pi * torch.arange(size, dtype=x.dtype,
+                                                                  device=x.device) / size)
+    xp = TF.pad(x[:, None], (size // 2, size // 2), mode="reflect")[:, 0]
+    frames = xp.unfold(-1, size, hop) * window
+    return torch.abs(torch.fft.rfft(frames, dim=-1))
+
+
+def mss_loss(x, y, fft_sizes=DEFAULT_FFT_SIZES, eps=LOG_EPS):
+    """loss.py:105-126, per item: mean over sizes of spectral convergence +
+    mean |log-magnitude difference|; returns [B] losses."""
+    total = 0.0
+    for size in fft_sizes:
+        hop = -(-size // 4)
+        xm = stft_mag(x, size, hop)
+        ym = stft_mag(y, size, hop).detach()
+        ynorm = torch.clamp(torch.sqrt(torch.sum(ym * ym, dim=(-2, -1))), min=1e-12)
+        sc = torch.sqrt(torch.sum((xm - ym) ** 2, dim=(-2, -1))) / ynorm
+        la = torch.mean(torch.abs(torch.log(xm + eps) - torch.log(ym + eps)), dim=(-2, -1))
+        total = total + sc + la
+    return total / len(fft_sizes)
+
+
+@dataclass
+class Decoder:
+    """The reference decoder graph (synth.py:217-275) in torch on the GPU.
+
+    ``tables`` [K, L] wavetable rows (source.py:57-208 builds them; data here),
+    ``mode`` "sf" or "hpn"; ``c_lp=True`` (HpN only) filters the shaped noise
+    with an all-pole C(z) too -- the paper's GOLF-v1 form the
+    reference does not implement -- with the H(z) and C(z)
+    filters in ONE grouped launch."""
+
+    tables: torch.Tensor
+    hop: int = 240
+    fs: float = 24000.0
+    mode: str = "sf"
+    oversample: int = 4
+    c_lp: bool = False
+    framewise: bool = False   # SF with the frame-wise TI LP (synth.render_framewise)
+
+    def __post_init__(self):
+        self.plan = None
+
+    def _plan(self):
+        from .params import FramePlan
+
+        if self.plan is None:
+            self.plan = FramePlan.raised_cosine(self.hop)
+        return self.plan
+
+    def render(self, p, n_out, noise, f0_frames, c_frames=None):
+        """p: dict of [B, ...] parameter tensors (reflection_raw, table_pos_raw,
+        voiced_gain_raw, noise_gain_raw, h_gain_raw, noise_logmag, fir_taps);
+        noise [B, n_out] unit noise; f0_frames [B, F] (no unvoiced zeros).
+        Returns the output signal [B, n_out]."""
+        hop, T1 = self.hop, n_out
+        K = self.tables.shape[0]
+        k = SQUASH_LIMIT * torch.tanh(p["reflection_raw"])
+        a_frames = ag.reflection_to_lpc(k)
+        pos = torch.sigmoid(p["table_pos_raw"]) * (K - 1)
+        vgain = torch.exp(p["voiced_gain_raw"])
+        # oscillator (source.py:294-314)
+        phase = oscillator_phase(f0_frames, hop, n_out, self.fs, self.oversample).to(
+            device=pos.device, dtype=pos.dtype)
+        pos_track = upsample_linear(pos, hop * self.oversample, n_out * self.oversample)
+        raw = wavetable_read(pos_track, self.tables.to(pos.dtype), phase)
+        if self.oversample > 1:
+            taps = torch.as_tensor(design_lowpass(oversample=self.oversample), dtype=pos.dtype,
+                                   device=pos.device)
+            sig = decimate_fir(raw, taps, self.oversample, n_out)
+        else:
+            sig = raw
+        osc = sig * upsample_linear(vgain, hop, T1)
+        noise_unit = shape_noise(p["noise_logmag"], noise.to(pos.dtype), self._plan())
+        noise_s = noise_unit * upsample_linear(torch.exp(p["noise_gain_raw"]), hop, T1)
+        hgain = upsample_linear(torch.exp(p["h_gain_raw"]), hop, T1)
+        if self.mode == "sf":
+            if self.framewise:
+                s = ag.framewise(hgain * (osc + noise_s), a_frames, self._plan())
+            else:
+                s = ag.lp_tv_frames(hgain * (osc + noise_s), a_frames, hop)
+            return global_fir(s, p["fir_taps"])
+        if self.c_lp:
+            # H(z) on the glottal source and C(z) on the noise, one grouped launch
+            A_h = upsample_linear(a_frames, hop, T1)
+            A_c = upsample_linear(c_frames, hop, T1)
+            s, c = ag.lp_tv_grouped((hgain * osc, A_h), (noise_s, A_c))
+            return global_fir(s + c, p["fir_taps"])
+        s = ag.lp_tv_frames(hgain * osc, a_frames, hop)
+        return global_fir(s + noise_s, p["fir_taps"])
