@@ -6,9 +6,10 @@
 A step is one LP forward + backward (lp_forward_tv then lp_backward_tv with
 the forward's carry tape, i.e. what ``LPTV`` autograd runs) over one batch of
 synthetic D1 input already resident in HBM.  The default
-workload is config 3 of BASELINE.json (B=64, T=48000, M=22, fp32) per GPU;
-with N GPUs (torchrun, one process per GPU) every rank filters its own 64
-sequences with no collective in the filter (batch sharding, weak scaling);
+workload is config 3 of BASELINE.json (B=64, T=48000, M=22, fp32); with N
+GPUs (torchrun, one process per GPU) the fixed global batch of 64 is split
+64/N per rank with no collective in the filter (batch sharding, strong
+scaling as the config defines it; ``--scaling weak`` keeps 64 per rank);
 the timed region is bracketed by a barrier and synchronisation and the
 reported time is the max over ranks.
 
@@ -43,7 +44,7 @@ UNIT = "samples/s"
 
 CONFIGS = {
     # name: kind, B (per GPU), T, M[, hop]
-    "tv_b64_t48000": dict(kind="tv", B=64, T=48000, M=22, baseline_cfg=3),
+    "tv_b64_t48000": dict(kind="tv", B=64, T=48000, M=22, baseline_cfg=3, scaling="strong"),
     "tv_b4_t24000": dict(kind="tv", B=4, T=24000, M=22, baseline_cfg=1),
     "framewise_b32_t48000": dict(kind="framewise", B=32, T=48000, M=22, hop=240, baseline_cfg=2),
     "tv_b1_t14400000": dict(kind="tv", B=1, T=14_400_000, M=22, baseline_cfg=4),
@@ -93,6 +94,21 @@ def kernel_bytes_per_sample_frames(name, M):
     """frame-rate path (rows interpolated in the kernels)"""
     return {"basis": 4, "apply_fwd": 8, "adjoint_zs": 4, "adjoint_apply": 8,
             "grad_frames": 8}.get(name)
+
+
+def kernel_flops_per_sample_framewise(name, M, overlap=4):
+    """frame-wise TI (SURVEY.md §8(d), 536 flop per audio sample at M=22):
+    every sample lies in ``overlap`` frames; per frame-sample the forward runs
+    M FMAs (+ the window), the backward M FMAs of the adjoint filter and M of
+    the coefficient reduction (+ the window); OLA / gather add one each."""
+    return {"fw_forward": overlap * (2 * M + 1),
+            "fw_backward": overlap * (4 * M + 1)}.get(name)
+
+
+def fp32_peak_tflops(sm_mhz=1965.0):
+    """148 SMs x 128 FP32 lanes x 2 flop per FMA at the SM clock (derived;
+    MEASURED_PEAKS.json carries HBM and bf16 only)."""
+    return 148 * 128 * 2 * sm_mhz * 1e-6
 
 
 def peaks():
@@ -200,11 +216,39 @@ class Clocks:
 # CPU baseline: the oracle (C port of the reference path), threaded
 # ---------------------------------------------------------------------------
 
-def cpu_baseline(cfg, seconds=10.0):
+def cpu_baseline(cfg, seconds=10.0, reference=True):
+    """The oracle's threaded C port on all host threads (the headline
+    ``cpu_baseline``, kind "port"), the same port on one thread, and -- when
+    baseline/_ref holds the reference install -- the unmodified reference
+    ``tvlp`` itself on 1 and N processes (baseline/tvlp_cpu.py), with the CPU
+    model string."""
+    nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    # the reference filters each sequence serially: a step's work spreads over
+    # at most one core per independent sequence (config 4's one 14.4 M-sample
+    # sequence is one core's work whatever the host)
+    nthreads = max(1, min(nthreads, cfg["B"] * (2 if cfg["kind"] == "hpn" else 1)))
+    out = _port_baseline(cfg, nthreads, seconds)
+    one = _port_baseline(cfg, 1, max(3.0, seconds / 3), one_core=True)
+    out["one_core"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
+    sys.path.insert(0, os.path.join(ROOT, "baseline"))
+    import tvlp_cpu
+
+    out["cpu_model"] = tvlp_cpu.cpu_model()
+    if reference and tvlp_cpu.available():
+        T_ref = min(cfg["T"], 480_000)  # a bounded slice of config 4's one sequence
+        try:
+            out["reference_tvlp"] = tvlp_cpu.measure(
+                cfg["kind"], T_ref, cfg["M"], cfg.get("hop", 240), procs=nthreads,
+                seconds=max(3.0, seconds / 2), lps_per_sample=2 if cfg["kind"] == "hpn" else 1)
+        except Exception as ex:  # reported, never fatal to the GPU line
+            out["reference_tvlp"] = {"unavailable": f"{type(ex).__name__}: {ex}"[:200]}
+    return out
+
+
+def _port_baseline(cfg, nthreads, seconds, one_core=False):
     import oracle
     from paper_2406_05128_b200 import data
 
-    nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     T, M = cfg["T"], cfg["M"]
     lps_per_sample = 2 if cfg["kind"] == "hpn" else 1
     if cfg["kind"] == "tvf":
@@ -227,18 +271,22 @@ def cpu_baseline(cfg, seconds=10.0):
             run_once()
             times.append(time.perf_counter() - t0)
         med = float(np.median(times))
-        return {"value": B_s * T / med, "unit": UNIT, "cores": nthreads, "kind": "port",
+        return {"value": round(B_s * T / med, 1), "unit": UNIT, "cores": nthreads, "kind": "port",
                 "sample": f"{B_s} x {T} samples (M={M}, hop={hop}, D1 frames): upsample_linear "
                           f"(numpy) + LP fwd+bwd (oracle/tvlp_oracle.c, {nthreads} threads) + "
                           f"upsample VJP (numpy) per repeat, median of {len(times)} repeats"}
     if cfg["kind"] in ("tv", "hpn", "tvsplit"):
         T_s = min(T, 480_000)
         B_s = max(1, min(cfg["B"] * lps_per_sample, 4 * nthreads)) if T <= 480_000 else nthreads
+        if one_core:
+            B_s = min(B_s, 2)
         e, A, g = data.d1_batch(1000, B_s, T_s, M)
         kind = "tv"
     else:
         T_s = T
         B_s = max(1, min(cfg["B"], 4 * nthreads))
+        if one_core:
+            B_s = min(B_s, 2)
         e, A, g = data.d1_frames_batch(1000, B_s, T_s, M, cfg["hop"])
         kind = "framewise"
     oracle.batch_fwd_bwd(kind, e[:1], A[:1], g[:1], nthreads=1)  # warm (page-in)
@@ -253,7 +301,7 @@ def cpu_baseline(cfg, seconds=10.0):
         if len(times) >= 50:
             break
     med = float(np.median(times))
-    return {"value": B_s * T_s / med / lps_per_sample, "unit": UNIT, "cores": nthreads,
+    return {"value": round(B_s * T_s / med / lps_per_sample, 1), "unit": UNIT, "cores": nthreads,
             "kind": "port",
             "sample": f"{B_s} x {T_s} samples (M={M}, D1) LP fwd+bwd per repeat"
                       f"{' (2 LPs per audio sample)' if lps_per_sample == 2 else ''}, median of "
@@ -304,7 +352,19 @@ def run_b200(args, cfg, rank, world, dist):
     lib = N.load()
     B, T, M = cfg["B"], cfg["T"], cfg["M"]
     kind = cfg["kind"]
-    lo, hi = pdist.shard(B, rank)
+    strong = args.scaling == "strong" and kind != "tvsplit"
+    if strong:
+        # a fixed global batch of cfg["B"] split over the ranks (config 3 as
+        # BASELINE.json defines it: 64 items over 1/2/4/8 GPUs); --shard-of S
+        # runs rank 0's share of an S-way split on one GPU (a probe of the
+        # per-GPU regime, reported as such)
+        parts = args.shard_of if (world == 1 and args.shard_of > 1) else world
+        lo, hi = pdist.strong_shard(B, rank, parts)
+        B_glob = B if parts == world else hi - lo
+        B = hi - lo
+    else:
+        lo, hi = pdist.shard(B, rank)
+        B_glob = B * world
     allreduce = None
     if kind in ("tv", "hpn"):
         if kind == "tv":
@@ -401,7 +461,7 @@ def run_b200(args, cfg, rank, world, dist):
     refined = lib.tvlp_refined_sequences() - r0
     ms = pdist.max_over_ranks(ev0.elapsed_time(ev1) / args.steps, dist, dev)
     nonfinite_seen = lpc.check_nonfinite(dev)
-    samples = B * T * (1 if kind == "tvsplit" else world)
+    samples = T * (B if kind == "tvsplit" else B_glob)
     value = samples / (ms * 1e-3)
 
     # outputs of one more step for the parity check of the CPU leg (items 0
@@ -437,7 +497,21 @@ def run_b200(args, cfg, rank, world, dist):
                             "share": round(tot / tot_all, 4)}
     dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
     roof = None
-    if dom is not None:
+    if dom is not None and kind == "framewise":
+        cnt, tot = prof[dom]
+        t_step = tot / nsteps * 1e-3
+        fps = kernel_flops_per_sample_framewise(dom, M, cfg.get("frame_size", 4 * cfg["hop"]) // cfg["hop"])
+        ach = fps * B * T / t_step / 1e12
+        pk = fp32_peak_tflops()
+        roof = {"bound": "fp32", "kernel": dom, "achieved": round(ach, 2), "peak": round(pk, 1),
+                "unit": "TFLOP/s", "frac": round(ach / pk, 4), "traffic": None,
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 flop x 1965 MHz (max SM "
+                               "clock); the path has no tensor-core contraction",
+                "flops_per_sample": fps, "us_per_step": round(t_step * 1e6, 2),
+                "launches_per_step": cnt / nsteps,
+                "step_flops_per_sample": sum(kernel_flops_per_sample_framewise(k, M)
+                                             for k in ("fw_forward", "fw_backward"))}
+    elif dom is not None:
         bps = (kernel_bytes_per_sample_frames if kind == "tvf" else kernel_bytes_per_sample)(dom, M)
         lp_rows = 2 * B if kind == "hpn" else B  # LP sequences per GPU
         T_k = T // world if kind == "tvsplit" else T  # samples per sequence on this GPU
@@ -508,19 +582,24 @@ def run_b200(args, cfg, rank, world, dist):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": True, "scaling": "strong" if kind == "tvsplit" else "weak",
+        "higher_is_better": True, "scaling": "strong" if (kind == "tvsplit" or strong) else "weak",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic D1 (SURVEY.md §8(d)); inputs resident in HBM; working set "
                 f"{round(algorithmic_bytes_per_sample(cfg) * B * T / 1e6)} MB > 126 MB L2 "
                 "(no flush needed)",
         "config": {"workload": args.config, "baseline_config": cfg["baseline_cfg"],
                    "kind": kind, "B_per_gpu": B, "T": T, "M": M,
-                   "global_B": B * world, "parallelism": f"batch-shard x{world}",
+                   "global_B": B_glob, "parallelism": f"batch-shard x{world}",
+                   "shard_of": args.shard_of if (strong and world == 1 and args.shard_of > 1) else None,
                    "carry_precision": lpc.carry_precision(),
                    "subchunk": int(lib.tvlp_subchunk_len(2 * B if kind == "hpn" else B, T, M)) if kind in ("tv", "hpn", "tvf") else None,
                    "l2": "inputs larger than L2"},
         "gbs_algorithmic_step": round(step_gbs, 1),
         "step_roofline_frac": round(step_gbs / hbm, 4),
+        **({"step_fp32_tflops": round(roof["step_flops_per_sample"] * B * T / (ms * 1e-3) / 1e12, 2),
+            "step_fp32_frac": round(roof["step_flops_per_sample"] * B * T / (ms * 1e-3) / 1e12
+                                    / fp32_peak_tflops(), 4)}
+           if kind == "framewise" and roof else {}),
         "roofline": roof,
         "kernels": per_kernel,
         "e2e": {"value": round(samples / (e2e_ms * 1e-3), 1), "unit": UNIT,
@@ -558,10 +637,16 @@ def main(argv=None):
     ap.add_argument("--config", default=DEFAULT, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="default: the config's own (config 3: strong, global B=64)")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="1-GPU probe: run rank 0's share of an S-way strong split")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    if args.scaling is None:
+        args.scaling = cfg.get("scaling", "weak")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
 
