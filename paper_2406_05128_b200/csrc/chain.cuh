@@ -398,19 +398,19 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
 // as [l][M+1][MP4] (z row, then the M rows of Phi); records x(l) in xs[l].
 template <int M>
 __device__ __forceinline__ float unit_carry_fwd(const float* tz, int L, float x, float* xs,
-                                                float* xg, float* xb, float& nrm) {
+                                                float* xg, float* xb) {
     constexpr int MP4 = Tape<M>::MP4;
     const int lane = threadIdx.x & 31;
     const int r = lane < M ? lane : 0;
+    // row r of Phi_l and z_l are independent of the state: loaded one hop
+    // ahead, so a hop's critical path is the state broadcast + one dot
+    float w[MP4], wn[MP4];
+    load_vec<float, MP4>(tz + (1 + r) * MP4, w);
+    float zr = tz[r];
     for (int l = 0; l < L; ++l) {
-        const float* tp = tz + l * (M + 1) * MP4;
-        float w[MP4], xv[MP4];
-        load_vec<float, MP4>(tp + (1 + r) * MP4, w);
-        const float zr = tp[r];
-        float rs = 0.f;  // |row r of Phi_l|_1: the max over rows is ||Phi_l||_inf
-#pragma unroll
-        for (int c = 0; c < M; ++c) rs += fabsf(w[c]);
-        if (lane < M) nrm = fmaxf(nrm, rs);
+        const float* tn = tz + (l + 1 < L ? l + 1 : l) * (M + 1) * MP4;
+        load_vec<float, MP4>(tn + (1 + r) * MP4, wn);
+        const float zn = tn[r];
         if (lane < M) {
             xs[l * MP4 + lane] = x;
             xg[l * MP4 + lane] = x;
@@ -418,8 +418,12 @@ __device__ __forceinline__ float unit_carry_fwd(const float* tz, int L, float x,
         float* b = xb + (l & 1) * 32;
         b[lane] = lane < M ? x : 0.f;
         __syncwarp();
+        float xv[MP4];
         load_vec<float, MP4>(b, xv);
         x = dot_rows<M, float>(w, xv, zr);
+#pragma unroll
+        for (int c = 0; c < MP4; ++c) w[c] = wn[c];
+        zr = zn;
     }
     return x;
 }
@@ -427,18 +431,17 @@ __device__ __forceinline__ float unit_carry_fwd(const float* tz, int L, float x,
 // [l][M][MP4] (row c = column c of Phi_l); records mu(l) in xs[l].
 template <int M>
 __device__ __forceinline__ float unit_carry_bwd(const float* tw, const float* nu, int L, float mu,
-                                                float* xs, float* xg, float* xb, float& nrm) {
+                                                float* xs, float* xg, float* xb) {
     constexpr int MP4 = Tape<M>::MP4;
     const int lane = threadIdx.x & 31;
     const int r = lane < M ? lane : 0;
+    float w[MP4], wn[MP4];
+    load_vec<float, MP4>(tw + ((L - 1) * M + r) * MP4, w);
+    float nr = nu[(L - 1) * MP4 + r];
     for (int l = L - 1; l >= 0; --l) {
-        float w[MP4], mv[MP4];
-        load_vec<float, MP4>(tw + (l * M + r) * MP4, w);
-        const float nr = nu[l * MP4 + r];
-        float rs = 0.f;  // |column r of Phi_l|_1: the max is ||Phi_l^T||_inf
-#pragma unroll
-        for (int c = 0; c < M; ++c) rs += fabsf(w[c]);
-        if (lane < M) nrm = fmaxf(nrm, rs);
+        const int ln = l > 0 ? l - 1 : 0;
+        load_vec<float, MP4>(tw + (ln * M + r) * MP4, wn);
+        const float nn = nu[ln * MP4 + r];
         if (lane < M) {
             xs[l * MP4 + lane] = mu;
             xg[l * MP4 + lane] = mu;
@@ -446,8 +449,12 @@ __device__ __forceinline__ float unit_carry_bwd(const float* tw, const float* nu
         float* b = xb + (l & 1) * 32;
         b[lane] = lane < M ? mu : 0.f;
         __syncwarp();
+        float mv[MP4];
         load_vec<float, MP4>(b, mv);
         mu = dot_rows<M, float>(w, mv, nr);
+#pragma unroll
+        for (int c = 0; c < MP4; ++c) w[c] = wn[c];
+        nr = nn;
     }
     return mu;
 }
@@ -558,7 +565,8 @@ struct BwdChainSmem {
     static constexpr int OFF_XB = OFF_XS + XS;
     static constexpr int OFF_BAR = OFF_XB + 64 * 4;
     static constexpr int BYTES = OFF_BAR + (NST + 1) * 8;
-    static_assert(ZS || TW <= NST * UnitLane<M, U, NST>::STAGE, "W rows stay clear of the out boxes");
+    // (ZS == false: the W rows may also cover the out boxes -- the previous
+    // unit's pass drained its bulk stores (bulk_wait<0>) before they land)
 };
 
 // ---------------------------------------------------------------- refinement of one sequence
@@ -866,9 +874,7 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
         mbar_wait(tb, 0);
         tt[2] = gtime();
         // 4. carries through the unit, publish the state past it
-        float nrm = 0.f;
-        x = unit_carry_fwd<M>(reinterpret_cast<const float*>(sa), L, x, xs, a.Xin + g0 * MP4, xb,
-                              nrm);
+        x = unit_carry_fwd<M>(reinterpret_cast<const float*>(sa), L, x, xs, a.Xin + g0 * MP4, xb);
         if (ru + 1 < nu && lane < M) st_state(a.pub + (b * nu + ru) * MP4 + lane, x);
         if (lane < M) xs[L * MP4 + lane] = x;
         __syncwarp();
@@ -898,11 +904,9 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
             }
             dm = warp_fmax(dm);
             xm = warp_fmax(xm);
-            nrm = warp_fmax(nrm);
             if (lane == 0) {
                 atomicMax(&a.dstat[3 * b], __float_as_uint(dm));
                 atomicMax(&a.dstat[3 * b + 1], __float_as_uint(xm));
-                atomicMax(&a.dstat[3 * b + 2], __float_as_uint(nrm));
             }
             // 7. the unit completing a sequence refines it when the check failed
             unsigned old = 0;
@@ -915,9 +919,7 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
                 __threadfence();
                 const float dmax = __uint_as_float(ld_acquire_u32(&a.dstat[3 * b]));
                 const float xmax = __uint_as_float(ld_acquire_u32(&a.dstat[3 * b + 1]));
-                const float pmax = __uint_as_float(ld_acquire_u32(&a.dstat[3 * b + 2]));
                 // defects above tol are refined (the boundary-defect check)
-                (void)pmax;
                 if (dmax > a.tol * xmax) {
                     const bool done = refine_sequence_fwd<M, NST, TI>(
                         a, b, sa, abars, xs, xb, dmax > a.tol * xmax, xmax);
@@ -1000,8 +1002,7 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
         mbar_wait(tb, 0);
         __syncwarp();
         tt[2] = gtime();
-        float nrm = 0.f;
-        mu = unit_carry_bwd<M>(tw, nus, L, mu, xs, a.Mu + g0 * MP4, xb, nrm);
+        mu = unit_carry_bwd<M>(tw, nus, L, mu, xs, a.Mu + g0 * MP4, xb);
         if (ru > 0 && lane < M) st_state(a.pub + (b * nu + ru) * MP4 + lane, mu);
         tt[3] = gtime();
         __syncwarp();
@@ -1030,11 +1031,9 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
             }
             dm = warp_fmax(dm);
             xm = warp_fmax(xm);
-            nrm = warp_fmax(nrm);
             if (lane == 0) {
                 atomicMax(&a.dstat[3 * b], __float_as_uint(dm));
                 atomicMax(&a.dstat[3 * b + 1], __float_as_uint(xm));
-                atomicMax(&a.dstat[3 * b + 2], __float_as_uint(nrm));
             }
             unsigned old = 0;
             if (lane == 0) {
@@ -1046,10 +1045,8 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
                 __threadfence();
                 const float dmax = __uint_as_float(ld_acquire_u32(&a.dstat[3 * b]));
                 const float xmax = __uint_as_float(ld_acquire_u32(&a.dstat[3 * b + 1]));
-                const float pmax = __uint_as_float(ld_acquire_u32(&a.dstat[3 * b + 2]));
                 const bool bad = dmax > a.tol * xmax ||
                                  (a.inherit != nullptr && a.inherit[b] != 0);
-                (void)pmax;
                 if (bad) {
                     const bool done =
                         refine_sequence_bwd<M, NST, TI>(a, b, sl, bars, xb, bad, xmax);
