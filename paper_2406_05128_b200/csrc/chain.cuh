@@ -176,7 +176,22 @@ struct UnitMaps {
     CUtensorMap A[2];
     CUtensorMap X[2];
     CUtensorMap O[2];
+    float* o;  // the output rows ([B*nsub][Ls]): lanes store their windows directly
 };
+
+// A lane's W outputs of one window, stored straight from registers: W
+// consecutive floats of its own sub-chunk row are whole 32-byte sectors, and
+// no output box means no async-proxy fence, warp syncs or bulk-store waits
+// per window (tools/micro/apply_lane.cu: the fence + syncs of a boxed TMA
+// store cost ~50 cycles per sample, more than the recursion's own ~39).
+template <int W>
+__device__ __forceinline__ void store_window(float* dst, const float (&v)[W]) {
+    static_assert(W % 4 == 0, "windows are whole float4s");
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q)
+        __stcs(reinterpret_cast<float4*>(dst) + q,
+               make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+}
 
 template <int M, int U, int NST>
 struct UnitLane {
@@ -186,8 +201,7 @@ struct UnitLane {
     static constexpr int A_BYTES = (U * AROW * 4 + 127) / 128 * 128;
     static constexpr int X_BYTES = (U * XROW * 4 + 127) / 128 * 128;
     static constexpr int STAGE = A_BYTES + X_BYTES;
-    static constexpr int OUT = (U * W * 4 + 127) / 128 * 128;
-    static constexpr int BYTES = NST * STAGE + 2 * OUT;  // + the caller's barriers
+    static constexpr int BYTES = NST * STAGE;  // + the caller's barriers
     __device__ static uint32_t tx(int L) { return (uint32_t)L * (AROW + XROW) * 4u; }
 };
 
@@ -246,14 +260,7 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
                 const unsigned char* base = sm + st * S::STAGE;
                 const float* Ar = reinterpret_cast<const float*>(base) + ln * S::AROW;
                 const float* er = reinterpret_cast<const float*>(base + S::A_BYTES) + ln * S::XROW;
-                const int so = k & 1;
-                float* obox = reinterpret_cast<float*>(sm + NST * S::STAGE + so * S::OUT);
-                float* ob = obox + ln * W;
-                if (k >= 2) {
-                    if (lane == 0) bulk_wait_read<1>();
-                    __syncwarp();
-                }
-                float ev[W];
+                float ev[W], ov[W];
 #pragma unroll
                 for (int u = 0; u < W; ++u) ev[u] = er[u];
                 // rows are loaded one step ahead (issued before this step's
@@ -281,22 +288,15 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
                     }
                     const float v = fmaf(-a[0], R[(pos - 1 + MR) % MR], ev[u] - ((p0 + p1) + (p2 + p3)));
                     R[pos % MR] = v;
-                    if (lane < U) ob[u] = v;
+                    ov[u] = v;
                     finite &= !active || isfinite(v);
                 }
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_2d(&mp.O[which], k * W, (int)g0, obox);
-                    bulk_commit();
-                }
-                __syncwarp();
+                if (active) store_window<W>(mp.o + (g0 + lane) * (int64_t)(nwin * W) + k * W, ov);
+                __syncwarp();  // every lane is done with the stage: refill it
                 issue(k + NST);
             }
         }
     }
-    if (lane == 0) bulk_wait<0>();
-    __syncwarp();
     const int last = (nwin * W - 1) % MR;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -350,14 +350,7 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
         const unsigned char* base = sm + st * S::STAGE;
         const float* Ar = reinterpret_cast<const float*>(base) + ln * S::AROW;
         const float* xr = reinterpret_cast<const float*>(base + S::A_BYTES) + ln * S::XROW;
-        const int so = k & 1;
-        float* obox = reinterpret_cast<float*>(sm + NST * S::STAGE + so * S::OUT);
-        float* ob = obox + ln * W;
-        if (MODE == 1 && k >= 2) {
-            if (lane == 0) bulk_wait_read<1>();
-            __syncwarp();
-        }
-        float gv[W];
+        float gv[W], ov[W];
 #pragma unroll
         for (int u = 0; u < W; ++u) gv[u] = xr[u];
         // rows are loaded one step ahead (issued before this step's output
@@ -373,24 +366,16 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
             if (!TI && u > 0)
                 load_row_at<float, M>(Ar + (u - 1) * M, an, (ln * S::AROW + (u - 1) * M) * 4);
             const float l0 = lam[0] + gv[u];
-            if (MODE == 1 && lane < U) ob[u] = l0;
+            ov[u] = l0;
 #pragma unroll
             for (int i = 0; i < M - 1; ++i) lam[i] = fmaf(-a[i], l0, lam[i + 1]);
             lam[M - 1] = -a[M - 1] * l0;
         }
-        if (MODE == 1) {
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                tma_store_2d(&mp.O[which], (nwin - 1 - k) * W, (int)g0, obox);
-                bulk_commit();
-            }
-        }
-        __syncwarp();
+        if (MODE == 1 && lane < L)
+            store_window<W>(mp.o + (g0 + lane) * (int64_t)(nwin * W) + (nwin - 1 - k) * W, ov);
+        __syncwarp();  // every lane is done with the stage: refill it
         issue(k + NST);
     }
-    if (MODE == 1 && lane == 0) bulk_wait<0>();
-    __syncwarp();
 }
 
 // ---------------------------------------------------------------- carries of a unit
@@ -565,8 +550,6 @@ struct BwdChainSmem {
     static constexpr int OFF_XB = OFF_XS + XS;
     static constexpr int OFF_BAR = OFF_XB + 64 * 4;
     static constexpr int BYTES = OFF_BAR + (NST + 1) * 8;
-    // (ZS == false: the W rows may also cover the out boxes -- the previous
-    // unit's pass drained its bulk stores (bulk_wait<0>) before they land)
 };
 
 // ---------------------------------------------------------------- refinement of one sequence

@@ -71,6 +71,7 @@ cudaError_t unit_maps(UnitMaps& mp, const float* A, const float* X, const float*
         if (err == cudaSuccess) err = view2d(&mp.O[i], O, (uint64_t)g.Ls, rows, S::W, box[i]);
         if (err != cudaSuccess) return err;
     }
+    mp.o = const_cast<float*>(O);
     return cudaSuccess;
 }
 

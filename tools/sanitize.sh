@@ -13,8 +13,7 @@ for tool in $tools; do
     extra=""
     [ "$fam" = hier ] && extra="TVLP_CARRY_SERIAL_MAX=16 TVLP_CARRY_GROUP=8"
     echo "=== $tool $fam" >> $log
-    env $extra PYTORCH_NO_CUDA_MEMORY_CACHING=1 timeout 900 $CS --tool $tool --error-exitcode 9
-      python tools/sanitize_driver.py $fam >> $log 2>&1
+    env $extra PYTORCH_NO_CUDA_MEMORY_CACHING=1 timeout 900 $CS --tool $tool --error-exitcode 9 python tools/sanitize_driver.py $fam >> $log 2>&1
     rc=$?
     echo "$tool $fam rc=$rc $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $log | tail -1)" >> $sum
   done
