@@ -179,20 +179,6 @@ struct UnitMaps {
     float* o;  // the output rows ([B*nsub][Ls]): lanes store their windows directly
 };
 
-// A lane's W outputs of one window, stored straight from registers: W
-// consecutive floats of its own sub-chunk row are whole 32-byte sectors, and
-// no output box means no async-proxy fence, warp syncs or bulk-store waits
-// per window (tools/micro/apply_lane.cu: the fence + syncs of a boxed TMA
-// store cost ~50 cycles per sample, more than the recursion's own ~39).
-template <int W>
-__device__ __forceinline__ void store_window(float* dst, const float (&v)[W]) {
-    static_assert(W % 4 == 0, "windows are whole float4s");
-#pragma unroll
-    for (int q = 0; q < W / 4; ++q)
-        __stcs(reinterpret_cast<float4*>(dst) + q,
-               make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-}
-
 template <int M, int U, int NST>
 struct UnitLane {
     static constexpr int W = kLaneWin;
@@ -291,7 +277,7 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
                     ov[u] = v;
                     finite &= !active || isfinite(v);
                 }
-                if (active) store_window<W>(mp.o + (g0 + lane) * (int64_t)(nwin * W) + k * W, ov);
+                if (active) store_window<float, W>(mp.o + (g0 + lane) * (int64_t)(nwin * W) + k * W, ov);
                 __syncwarp();  // every lane is done with the stage: refill it
                 issue(k + NST);
             }
@@ -372,7 +358,7 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
             lam[M - 1] = -a[M - 1] * l0;
         }
         if (MODE == 1 && lane < L)
-            store_window<W>(mp.o + (g0 + lane) * (int64_t)(nwin * W) + (nwin - 1 - k) * W, ov);
+            store_window<float, W>(mp.o + (g0 + lane) * (int64_t)(nwin * W) + (nwin - 1 - k) * W, ov);
         __syncwarp();  // every lane is done with the stage: refill it
         issue(k + NST);
     }

@@ -59,7 +59,27 @@ struct FwMaps {
     CUtensorMap seg[2];   // [B*nfr][size] box {W, 32} / {W, nfr % 32} (backward loads)
     CUtensorMap segw[2];  // same rows, box {128 B, 32 / nfr % 32}, 128B swizzle (stores)
     CUtensorMap gew[2];   // gew rows, stores like segw
+    void* segp;           // the seg / gew rows themselves: lanes store their windows directly
+    void* gewp;
 };
+
+// W outputs of a lane's frame row from registers as 16-byte vectors (n valid:
+// a multiple of the vector width, frame sizes are multiples of 4); see
+// store_window in lp_scan.cuh for why there is no output box.
+template <typename IO, int W>
+__device__ __forceinline__ void fw_store_window(IO* dst, const IO (&v)[W], int n) {
+    constexpr int V = 16 / (int)sizeof(IO);
+#pragma unroll
+    for (int q = 0; q < W / V; ++q) {
+        if (q * V < n) {
+            if constexpr (sizeof(IO) == 4)
+                __stcs(reinterpret_cast<float4*>(dst) + q,
+                       make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+            else
+                __stcs(reinterpret_cast<double2*>(dst) + q, make_double2(v[2 * q], v[2 * q + 1]));
+        }
+    }
+}
 
 // The staged span keeps hop-blocks at a stride of fw_stride(hop) elements:
 // blocks start 16-byte aligned (one bulk copy each) and lane f's reads land
@@ -162,13 +182,10 @@ k_fw_forward(const __grid_constant__ FwMaps maps, const IO* __restrict__ e,
     const int fi = fi0 + lane;
     const bool active = fi < nfr;
     const int rows = min(32, nfr - fi0);
-    const CUtensorMap* om = &maps.segw[rows == 32 ? 0 : 1];
-    using O = FwOut<IO>;
     const int f = fi - n_lead;
     const int row = f > 0 ? f : 0;
     IO* es = reinterpret_cast<IO*>(fw_smem);
     IO* ws = reinterpret_cast<IO*>(fw_smem + S::off_win(size, hop));
-    if (lane == 0) prefetch_tmap(om);
     uint64_t* sbar = reinterpret_cast<uint64_t*>(fw_smem + S::off_bar(size, hop, false));
     fw_stage<IO, false>(es, e + b * T, (int64_t)(fi0 - n_lead) * hop, S::blocks(size, hop), T, hop,
                         (IO)1, sbar);
@@ -189,13 +206,6 @@ k_fw_forward(const __grid_constant__ FwMaps maps, const IO* __restrict__ e,
         for (int wi = 0; wi < L / W; ++wi) {
             const int kw = k0 + wi * W;  // window start
             if (kw < size) {
-                const int ob = kw / O::OW;  // output box of this window
-                IO* obox = reinterpret_cast<IO*>(fw_smem + S::off_out(size, hop) +
-                                                 (ob % kFwOut) * S::OUT);
-                if (kw % O::OW == 0 && ob >= kFwOut) {  // first window into a reused box
-                    if (lane == 0) bulk_wait_read<kFwOut - 1>();
-                    __syncwarp();
-                }
                 // staged index of sample k (one division per window)
                 const int kq = kw / hop, kr = kw - kq * hop;
                 IO xv[W];
@@ -224,20 +234,12 @@ k_fw_forward(const __grid_constant__ FwMaps maps, const IO* __restrict__ e,
                     R[pos % L] = v;
                     ov[u] = v;
                 }
-#pragma unroll
-                for (int u = 0; u < W; ++u) obox[O::at(lane, kw % O::OW + u)] = ov[u];
-                if ((kw + W) % O::OW == 0 || kw + W >= size) {  // box complete: store it
-                    fence_proxy_async();
-                    __syncwarp();
-                    if (lane == 0) {
-                        tma_store_2d(om, ob * O::OW, (int)grow, obox);
-                        bulk_commit();
-                    }
-                }
+                if (active)
+                    fw_store_window<IO, W>(static_cast<IO*>(maps.segp) + (grow + lane) * size + kw,
+                                           ov, size - kw);
             }
         }
     }
-    if (lane == 0) bulk_wait<0>();
 }
 
 // out[t] = (sum over the frames covering t, in frame order, of seg) / cola
@@ -299,7 +301,6 @@ k_fw_backward(const __grid_constant__ FwMaps maps, const IO* __restrict__ gout,
     const uint32_t tx = (uint32_t)rows * W * sizeof(IO);
     if (lane == 0) {
         prefetch_tmap(&maps.seg[mi]);
-        prefetch_tmap(&maps.gew[mi]);
         for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
@@ -346,18 +347,8 @@ k_fw_backward(const __grid_constant__ FwMaps maps, const IO* __restrict__ gout,
     for (int j = 0; j <= NB; ++j) seg_row(nw - 1 - j, sv + (NB - j) * W);
     const int hst = fw_stride<IO>(hop);
     const int base = lane * hst;  // staged index of this frame's first sample
-    using O = FwOut<IO>;
-    const int nob = (size + O::OW - 1) / O::OW;  // output boxes (filled top down)
     for (int wv = nw - 1; wv >= 0; --wv) {
         const int kw = wv * W;
-        const int ob = kw / O::OW;
-        const int oo = nob - 1 - ob;  // ordinal of this box
-        IO* obox = reinterpret_cast<IO*>(fw_smem + S::off_out(size, hop) + (oo % kFwOut) * S::OUT);
-        const bool box_top = kw + W >= size || (kw + W) % O::OW == 0;  // first window into it
-        if (box_top && oo >= kFwOut) {
-            if (lane == 0) bulk_wait_read<kFwOut - 1>();
-            __syncwarp();
-        }
         IO gv[W], wk[W], ov[W];
         const int kq = kw / hop, kr = kw - kq * hop;
 #pragma unroll
@@ -377,16 +368,9 @@ k_fw_backward(const __grid_constant__ FwMaps maps, const IO* __restrict__ gout,
             for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
             lam[M - 1] = -a[M - 1] * l0;
         }
-#pragma unroll
-        for (int u = 0; u < W; ++u) obox[O::at(lane, kw % O::OW + u)] = ov[u];
-        if (kw % O::OW == 0) {  // the box's bottom window: store it
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                tma_store_2d(&maps.gew[mi], ob * O::OW, (int)grow, obox);
-                bulk_commit();
-            }
-        }
+        if (active)
+            fw_store_window<IO, W>(static_cast<IO*>(maps.gewp) + (grow + lane) * size + kw, ov,
+                                   size - kw);
         // the stage of window wv is no longer needed: refill it NS windows down
         __syncwarp();
         issue(wv - NS);
@@ -395,7 +379,6 @@ k_fw_backward(const __grid_constant__ FwMaps maps, const IO* __restrict__ gout,
         for (int i = SW - 1; i >= W; --i) sv[i] = sv[i - W];
         seg_row(wv - NB - 1, sv);
     }
-    if (lane == 0) bulk_wait<0>();
     if (active) {
 #pragma unroll
         for (int c = 0; c < M; ++c) gapart[(b * nfr + fi) * M + c] = -ga[c];
@@ -503,6 +486,8 @@ cudaError_t fw_maps(FwMaps& m, const IO* seg, const IO* gew, const FwArgs& a) {
             std::memset(&m.gew[i], 0, sizeof(m.gew[i]));
         }
     }
+    m.segp = const_cast<IO*>(seg);
+    m.gewp = const_cast<IO*>(gew);
     return cudaSuccess;
 }
 }  // namespace

@@ -994,8 +994,29 @@ struct LaneSmem {
 struct LaneMaps {
     CUtensorMap A;  // [B*nsub, Ls*M] box {AROW, 32}   (unused for TI)
     CUtensorMap X;  // [B*nsub, Ls]   box {XROW, 32}   (e or g_s)
-    CUtensorMap O;  // [B*nsub, Ls]   box {W, 32}      (s or g_e)
+    CUtensorMap O;  // [B*nsub, Ls]   box {W, 32}      (s or g_e; unused by the lane passes)
+    void* o;        // the same rows: lanes store their output windows directly
 };
+
+// A lane's W outputs of one window, stored straight from registers as 16-byte
+// vectors: W consecutive values of the lane's own sub-chunk row are whole
+// 32-byte sectors, and without an output box there is no async-proxy fence,
+// warp sync or bulk-store wait per window (tools/micro/apply_lane.cu: the
+// fence + syncs of a boxed TMA store cost ~50 cycles per sample at one warp
+// per SM, more than the recursion itself at ~39).
+template <typename IO, int W>
+__device__ __forceinline__ void store_window(IO* dst, const IO (&v)[W]) {
+    constexpr int V = 16 / (int)sizeof(IO);
+    static_assert(W % V == 0, "windows are whole 16-byte vectors");
+#pragma unroll
+    for (int q = 0; q < W / V; ++q) {
+        if constexpr (sizeof(IO) == 4)
+            __stcs(reinterpret_cast<float4*>(dst) + q,
+                   make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        else
+            __stcs(reinterpret_cast<double2*>(dst) + q, make_double2(v[2 * q], v[2 * q + 1]));
+    }
+}
 
 // ---------------------------------------------------------------- fused refinement
 constexpr float kDefectTol = 2e-5f;     // forward: relative to max |x| (samples of s)
@@ -1121,7 +1142,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
     if (lane == 0) {
         if (!TI && !FR) prefetch_tmap(&maps.A);
         prefetch_tmap(&maps.X);
-        prefetch_tmap(&maps.O);
+
         for (int st = 0; st < kLaneStages; ++st) mbar_init(&bars[st], 1);
         fence_mbar_init();
     }
@@ -1171,14 +1192,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
                 const unsigned char* base = smem + st * S::STAGE;
                 const IO* Ar = reinterpret_cast<const IO*>(base) + lane * S::AROW;
                 const IO* er = reinterpret_cast<const IO*>(base + S::A_BYTES) + lane * S::XROW;
-                const int so = k % kOutStages;
-                IO* obox = reinterpret_cast<IO*>(smem + kLaneStages * S::STAGE + so * S::OUT);
-                IO* ob = obox + lane * W;
-                if (k >= kOutStages) {
-                    if (lane == 0) bulk_wait_read<kOutStages - 1>();
-                    __syncwarp();
-                }
-                IO ev[W];
+                IO ev[W], ov[W];
 #pragma unroll
                 for (int u = 0; u < W; ++u) ev[u] = er[u];
                 if constexpr (FR) cur.window(fs, fb_b, ft0 + (int64_t)k * W);
@@ -1208,20 +1222,16 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
                     const IO v =
                         fma(-a[0], R[(pos - 1 + MR) % MR], ev[u] - ((p0 + p1) + (p2 + p3)));
                     R[pos % MR] = v;
-                    ob[u] = v;
+                    ov[u] = v;
                     finite &= is_finite_val(v);
                 }
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_2d(&maps.O, k * W, g0, obox);
-                    bulk_commit();
-                }
+                if (active)
+                    store_window<IO, W>(static_cast<IO*>(maps.o) + gid * (int64_t)g.Ls + k * W, ov);
+                __syncwarp();  // every lane is done with the stage: refill it
                 issue(k + kLaneStages);
             }
         }
     }
-    if (lane == 0) bulk_wait<0>();
     if (flag != nullptr) {
         // a non-finite output means non-finite input or overflow; the host
         // tells them apart (overflow of an unstable filter is legitimate).
@@ -1290,7 +1300,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     if (lane == 0) {
         if (!TI && !FR) prefetch_tmap(&maps.A);
         prefetch_tmap(&maps.X);
-        if (MODE == 1) prefetch_tmap(&maps.O);
+
         for (int st = 0; st < kLaneStages; ++st) mbar_init(&bars[st], 1);
         fence_mbar_init();
     }
@@ -1335,14 +1345,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
         const unsigned char* base = smem + st * S::STAGE;
         const IO* Ar = reinterpret_cast<const IO*>(base) + lane * S::AROW;
         const IO* xr = reinterpret_cast<const IO*>(base + S::A_BYTES) + lane * S::XROW;
-        const int so = k % kOutStages;
-        IO* obox = reinterpret_cast<IO*>(smem + kLaneStages * S::STAGE + so * S::OUT);
-        IO* ob = obox + lane * W;
-        if (MODE == 1 && k >= kOutStages) {
-            if (lane == 0) bulk_wait_read<kOutStages - 1>();
-            __syncwarp();
-        }
-        IO gv[W];
+        IO gv[W], ov[W];
 #pragma unroll
         for (int u = 0; u < W; ++u) gv[u] = xr[u];
         if constexpr (FR) cur.window(fs, fb_b, ft0 + (int64_t)(nwin - 1 - k) * W);
@@ -1358,23 +1361,17 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
                 load_row_at<IO, M>(Ar + u * M, a, (lane * S::AROW + u * M) * S::SZ);
             }
             const IO l0 = lam[0] + gv[u];
-            if (MODE == 1) ob[u] = l0;
+            ov[u] = l0;
 #pragma unroll
             for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
             lam[M - 1] = -a[M - 1] * l0;
         }
-        if (MODE == 1) {
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                tma_store_2d(&maps.O, (nwin - 1 - k) * W, g0, obox);
-                bulk_commit();
-            }
-        }
-        __syncwarp();
+        if (MODE == 1 && active)
+            store_window<IO, W>(static_cast<IO*>(maps.o) + gid * (int64_t)g.Ls + (nwin - 1 - k) * W,
+                                ov);
+        __syncwarp();  // every lane is done with the stage: refill it
         issue(k + kLaneStages);
     }
-    if (MODE == 1 && lane == 0) bulk_wait<0>();
     // MODE 0: Nu = zero-state carry-out.  MODE 1: Nu (if given) = the carry-out
     // C(t0)^T lambda(t0) obtained from Mu, which the defect check compares with
     // the carry chain's Mu of the previous sub-chunk.

@@ -91,6 +91,7 @@ cudaError_t lane_maps(LaneMaps& mp, const IO* A, const IO* X, const IO* O, const
     else std::memset(&mp.A, 0, sizeof(mp.A));
     if (err == cudaSuccess) err = map2d(&mp.X, X, S::SZ, (uint64_t)g.Ls, rows, S::XROW, 32);
     if (err == cudaSuccess) err = map2d(&mp.O, O, S::SZ, (uint64_t)g.Ls, rows, S::W, 32);
+    mp.o = const_cast<IO*>(O);
     return err;
 }
 
