@@ -8,6 +8,7 @@
 // frames[max(f,0)].  Overlap-add and the frame-row reduction are
 // deterministic gathers in frame order (the reference's accumulation order).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include <cudaTypedefs.h>
@@ -427,6 +428,19 @@ __global__ void k_fw_rows(const IO* __restrict__ gapart, IO* __restrict__ gf, in
     gf[idx] = acc;
 }
 
+#include "framewise_pieces.cuh"
+
+namespace {
+// piece kernels for the plans they serve ($TVLP_FW_PIECES=0: one lane per frame)
+bool fw_pieces(const FwArgs& a) {
+    static const int on = [] {
+        const char* v = std::getenv("TVLP_FW_PIECES");
+        return (v != nullptr && v[0] != 0) ? std::atoi(v) : 1;
+    }();
+    return on != 0 && fwp_supported(a.size, a.hop);
+}
+}  // namespace
+
 #define TVLP_FW_DISPATCH(Mp, ...)                          \
     switch (Mp) {                                          \
         case 2: { constexpr int M_ = 2; __VA_ARGS__ }      \
@@ -505,9 +519,21 @@ cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* w
                               IO* out, const FwArgs& a, cudaStream_t st) {
     if (!fw_supported(Mp, a.size, a.hop, (int)sizeof(IO))) return cudaErrorInvalidValue;
     const dim3 grid((unsigned)((a.nfr + 31) / 32), (unsigned)a.B);
+    cudaError_t err = cudaSuccess;
+    if (fw_pieces(a)) {
+        const size_t sm = FwpSmem<IO>::bytes(a.size, a.hop);
+        TVLP_FW_DISPATCH(Mp, {
+            auto k = k_fwp_forward<IO, M_>;
+            err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (err != cudaSuccess) return err;
+            launch_pdl(k, grid, 128, sm, st, seg, e, frames, win, a.T, a.F, a.nfr, a.size, a.hop,
+                       a.n_lead);
+            break;
+        })
+    } else {
     const size_t sm = FwSmem<IO>::bytes(a.size, a.hop, false);
     FwMaps maps;
-    cudaError_t err = fw_maps<IO>(maps, seg, nullptr, a);
+    err = fw_maps<IO>(maps, seg, nullptr, a);
     if (err != cudaSuccess) return err;
     TVLP_FW_DISPATCH(Mp, {
         auto k = k_fw_forward<IO, M_>;
@@ -517,6 +543,7 @@ cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* w
                    a.n_lead);
         break;
     })
+    }
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     const dim3 og((unsigned)((a.T + a.hop - 1) / a.hop), (unsigned)a.B);
@@ -531,9 +558,21 @@ cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, 
                                const FwArgs& a, cudaStream_t st) {
     if (!fw_supported(Mp, a.size, a.hop, (int)sizeof(IO))) return cudaErrorInvalidValue;
     const dim3 grid((unsigned)((a.nfr + 31) / 32), (unsigned)a.B);
+    cudaError_t err = cudaSuccess;
+    if (fw_pieces(a)) {
+        const size_t sm = FwpSmem<IO>::bytes(a.size, a.hop);
+        TVLP_FW_DISPATCH(Mp, {
+            auto k = k_fwp_backward<IO, M_>;
+            err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (err != cudaSuccess) return err;
+            launch_pdl(k, grid, 128, sm, st, gew, gapart, seg, gout, frames, win, a.T, a.F, a.nfr,
+                       a.size, a.hop, a.n_lead, (IO)a.cola);
+            break;
+        })
+    } else {
     const size_t sm = FwSmem<IO>::bytes(a.size, a.hop, true);
     FwMaps maps;
-    cudaError_t err = fw_maps<IO>(maps, seg, gew, a);
+    err = fw_maps<IO>(maps, seg, gew, a);
     if (err != cudaSuccess) return err;
     TVLP_FW_DISPATCH(Mp, {
         auto k = k_fw_backward<IO, M_>;
@@ -543,6 +582,7 @@ cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, 
                    a.hop, a.n_lead, (IO)a.cola);
         break;
     })
+    }
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     const dim3 og((unsigned)((a.T + a.hop - 1) / a.hop), (unsigned)a.B);
