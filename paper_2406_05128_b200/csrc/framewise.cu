@@ -243,6 +243,76 @@ k_fw_forward(const __grid_constant__ FwMaps maps, const IO* __restrict__ e,
     }
 }
 
+// sum over the frames f = q - j covering sample r of hop-block q, in frame
+// order (j descending), of row (f + n_lead) at k = r + j*hop; the loads of a
+// group of four are issued before the adds (a serial load-add chain was
+// latency-bound: 4 dependent L2 trips per sample)
+template <typename IO>
+__device__ __forceinline__ IO fw_gather_sum(const IO* __restrict__ sb, int q, int r, int size,
+                                            int hop, int n_lead, int flo, int fhi) {
+    IO acc = (IO)0;
+    for (int j0 = (size - 1 - r) / hop; j0 >= 0; j0 -= 4) {
+        IO v[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const int j = j0 - d, f = q - j;
+            v[d] = (j >= 0 && f >= flo && f <= fhi) ? sb[(int64_t)(f + n_lead) * size + r + j * hop]
+                                                     : (IO)0;
+        }
+#pragma unroll
+        for (int d = 0; d < 4; ++d)
+            if (j0 - d >= 0 && q - (j0 - d) >= flo && q - (j0 - d) <= fhi) acc += v[d];
+    }
+    return acc;
+}
+
+// Vector form of k_fw_ola / k_fw_gather_ge (fp32, hop % 4 == 0, T % 4 == 0):
+// one thread per 4 consecutive samples, one 16-byte load per covering frame
+// (the four samples share their frame range: r % 4 == 0 and hop % 4 == 0),
+// summed per element in the same frame order.  DIV: / cola (the OLA).
+template <bool DIV>
+__global__ void k_fw_gather4(const float* __restrict__ rows, float* __restrict__ out, int64_t B,
+                             int64_t T, int nfr, int size, int hop, int n_lead, float cola) {
+    grid_dep_wait();
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t T4 = T / 4;
+    if (idx >= B * T4) return;
+    const int64_t b = idx / T4;
+    const int t = (int)(idx - b * T4) * 4;
+    const int q = t / hop, r = t - q * hop;
+    const float* sb = rows + b * (int64_t)nfr * size;
+    const int flo = -n_lead, fhi = nfr - n_lead - 1;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j0 = (size - 1 - r) / hop; j0 >= 0; j0 -= 4) {
+        float4 v[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const int j = j0 - d, f = q - j;
+            v[d] = (j >= 0 && f >= flo && f <= fhi)
+                       ? __ldcs(reinterpret_cast<const float4*>(sb + (f + n_lead) * size + r +
+                                                                j * hop))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const int j = j0 - d, f = q - j;
+            if (j >= 0 && f >= flo && f <= fhi) {
+                acc.x += v[d].x;
+                acc.y += v[d].y;
+                acc.z += v[d].z;
+                acc.w += v[d].w;
+            }
+        }
+    }
+    if (DIV) {
+        acc.x = acc.x / cola;
+        acc.y = acc.y / cola;
+        acc.z = acc.z / cola;
+        acc.w = acc.w / cola;
+    }
+    reinterpret_cast<float4*>(out + b * T)[t / 4] = acc;
+}
+
 // out[t] = (sum over the frames covering t, in frame order, of seg) / cola
 // (params.py:236-239).  Block (q, b) covers t = q*hop + r: the frames f =
 // q-j (j descending, so frames ascend) contribute seg row f at k = r + j*hop;
@@ -258,13 +328,7 @@ __global__ void k_fw_ola(const IO* __restrict__ seg, IO* __restrict__ out, int64
     for (int r = threadIdx.x; r < hop; r += blockDim.x) {
         const int64_t t = (int64_t)q * hop + r;
         if (t >= T) return;
-        IO acc = (IO)0;
-        for (int j = (size - 1 - r) / hop; j >= 0; --j) {
-            const int f = q - j;
-            if (f < flo_all || f > fhi_all) continue;
-            acc += sb[(int64_t)(f + n_lead) * size + r + j * hop];
-        }
-        out[b * T + t] = acc / cola;
+        out[b * T + t] = fw_gather_sum<IO>(sb, q, r, size, hop, n_lead, flo_all, fhi_all) / cola;
     }
 }
 
@@ -399,13 +463,7 @@ __global__ void k_fw_gather_ge(const IO* __restrict__ gew, IO* __restrict__ ge, 
     for (int r = threadIdx.x; r < hop; r += blockDim.x) {
         const int64_t t = (int64_t)q * hop + r;
         if (t >= T) return;
-        IO acc = (IO)0;
-        for (int j = (size - 1 - r) / hop; j >= 0; --j) {
-            const int f = q - j;
-            if (f < flo_all || f > fhi_all) continue;
-            acc += gb[(int64_t)(f + n_lead) * size + r + j * hop];
-        }
-        ge[b * T + t] = acc;
+        ge[b * T + t] = fw_gather_sum<IO>(gb, q, r, size, hop, n_lead, flo_all, fhi_all);
     }
 }
 
@@ -438,6 +496,13 @@ bool fw_pieces(const FwArgs& a) {
         return (v != nullptr && v[0] != 0) ? std::atoi(v) : 1;
     }();
     return on != 0 && fwp_supported(a.size, a.hop);
+}
+// the vector OLA / grad_e gather applies (fp32, 16-byte aligned rows and outputs)
+template <typename IO>
+bool fw_gather4(const FwArgs& a, const void* rows, const void* out) {
+    return sizeof(IO) == 4 && a.hop % 4 == 0 && a.T % 4 == 0 && a.size % 4 == 0 &&
+           (reinterpret_cast<uintptr_t>(rows) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(out) & 15) == 0;
 }
 }  // namespace
 
@@ -526,7 +591,8 @@ cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* w
             auto k = k_fwp_forward<IO, M_>;
             err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             if (err != cudaSuccess) return err;
-            launch_pdl(k, grid, 128, sm, st, seg, e, frames, win, a.T, a.F, a.nfr, a.size, a.hop,
+            launch_pdl(k, dim3((unsigned)((a.nfr + kFwpFrames - 1) / kFwpFrames), (unsigned)a.B),
+                       kFwpThreads, sm, st, seg, e, frames, win, a.T, a.F, a.nfr, a.size, a.hop,
                        a.n_lead);
             break;
         })
@@ -546,6 +612,13 @@ cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* w
     }
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
+    if (fw_gather4<IO>(a, seg, out)) {
+        const int64_t n = a.B * (a.T / 4);
+        launch_pdl(k_fw_gather4<true>, (unsigned)((n + 255) / 256), 256, 0, st,
+                   reinterpret_cast<const float*>(seg), reinterpret_cast<float*>(out), a.B, a.T,
+                   a.nfr, a.size, a.hop, a.n_lead, (float)a.cola);
+        return cudaGetLastError();
+    }
     const dim3 og((unsigned)((a.T + a.hop - 1) / a.hop), (unsigned)a.B);
     launch_pdl(k_fw_ola<IO>, og, (unsigned)std::min(a.hop, 256), 0, st, seg, out, a.T, a.nfr,
                a.size, a.hop, a.n_lead, (IO)a.cola);
@@ -565,7 +638,8 @@ cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, 
             auto k = k_fwp_backward<IO, M_>;
             err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             if (err != cudaSuccess) return err;
-            launch_pdl(k, grid, 128, sm, st, gew, gapart, seg, gout, frames, win, a.T, a.F, a.nfr,
+            launch_pdl(k, dim3((unsigned)((a.nfr + kFwpFrames - 1) / kFwpFrames), (unsigned)a.B),
+                       kFwpThreads, sm, st, gew, gapart, seg, gout, frames, win, a.T, a.F, a.nfr,
                        a.size, a.hop, a.n_lead, (IO)a.cola);
             break;
         })
@@ -585,9 +659,16 @@ cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, 
     }
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
-    const dim3 og((unsigned)((a.T + a.hop - 1) / a.hop), (unsigned)a.B);
-    launch_pdl(k_fw_gather_ge<IO>, og, (unsigned)std::min(a.hop, 256), 0, st, gew, ge, a.T, a.nfr,
-               a.size, a.hop, a.n_lead);
+    if (fw_gather4<IO>(a, gew, ge)) {
+        const int64_t n = a.B * (a.T / 4);
+        launch_pdl(k_fw_gather4<false>, (unsigned)((n + 255) / 256), 256, 0, st,
+                   reinterpret_cast<const float*>(gew), reinterpret_cast<float*>(ge), a.B, a.T,
+                   a.nfr, a.size, a.hop, a.n_lead, 1.f);
+    } else {
+        const dim3 og((unsigned)((a.T + a.hop - 1) / a.hop), (unsigned)a.B);
+        launch_pdl(k_fw_gather_ge<IO>, og, (unsigned)std::min(a.hop, 256), 0, st, gew, ge, a.T,
+                   a.nfr, a.size, a.hop, a.n_lead);
+    }
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     const int64_t nr = a.B * (int64_t)a.F * Mp;

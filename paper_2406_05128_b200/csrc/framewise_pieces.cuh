@@ -30,13 +30,24 @@
 // which also accumulates ga[c] = sum_k ge(k) s(k-1-c) against the saved
 // frame outputs and writes gew = window * ge.
 //
-// Lanes: lane = 4 * (frame within the warp) + piece, 8 frames per warp, a CTA
-// of 4 warps covers 32 consecutive frames of one sequence (the staged span of
+// Lanes: lane = kFwP * (frame within the warp) + piece, a CTA of 128
+// threads covers 128 / kFwP consecutive frames of one sequence (the staged span of
 // k_fw_forward).  Arithmetic differs from the one-lane-per-frame kernels (the
 // carry adds one rounding level), so the plans that must stay bit-identical
 // to lp_forward_ti (one rectangular frame) keep those kernels.
 
-constexpr int kFwP = 4;  // pieces per frame
+#ifndef TVLP_FW_P
+#define TVLP_FW_P 4
+#endif
+constexpr int kFwP = TVLP_FW_P;  // pieces per frame (lanes per frame)
+static_assert(kFwP == 2 || kFwP == 4 || kFwP == 8, "a frame's lanes share a warp");
+constexpr int kFwpThreads = 128;                 // CTA
+constexpr int kFwpFrames = kFwpThreads / kFwP;   // consecutive frames per CTA
+
+// hop-blocks of the span the CTA's frames read
+__host__ __device__ __forceinline__ int fwp_blocks(int size, int hop) {
+    return ((kFwpFrames - 1) * hop + size + hop - 1) / hop;
+}
 
 template <typename IO>
 __host__ __device__ __forceinline__ int fwp_lpad(int L) {
@@ -50,7 +61,7 @@ __host__ __device__ __forceinline__ int fwp_lpad(int L) {
 template <typename IO>
 struct FwpSmem {
     static __host__ __device__ size_t off_win(int size, int hop) {
-        return ((size_t)FwSmem<IO>::blocks(size, hop) * fw_stride<IO>(hop) * sizeof(IO) + 15) / 16 *
+        return ((size_t)fwp_blocks(size, hop) * fw_stride<IO>(hop) * sizeof(IO) + 15) / 16 *
                16;
     }
     static __host__ __device__ size_t off_bar(int size, int hop) {
@@ -109,10 +120,8 @@ __device__ __forceinline__ void fwp_stage(IO* __restrict__ es, const IO* __restr
     __syncthreads();  // the barrier's init and the thread-filled blocks
     mbar_wait(bar, 0);
     if (DIV) {
-        for (int i = tid; i < nblk * hop; i += nt) {
-            const int q = i / hop, r = i - q * hop;
-            es[q * st + r] = es[q * st + r] / div;
-        }
+        for (int q = 0; q < nblk; ++q)
+            for (int r = tid; r < hop; r += nt) es[q * st + r] = es[q * st + r] / div;
         __syncthreads();
     }
 }
@@ -236,7 +245,7 @@ __device__ __forceinline__ void fwp_carry(const IO (&a)[M], const IO (&ht)[2 * M
 }
 
 template <typename IO, int M>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kFwpThreads)
 k_fwp_forward(IO* __restrict__ seg, const IO* __restrict__ e, const IO* __restrict__ frames,
               const IO* __restrict__ win, int64_t T, int F, int nfr, int size, int hop,
               int n_lead) {
@@ -248,9 +257,9 @@ k_fwp_forward(IO* __restrict__ seg, const IO* __restrict__ e, const IO* __restri
     extern __shared__ __align__(128) unsigned char fw_smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int p = lane & (kFwP - 1);
-    const int fc = warp * (32 / kFwP) + lane / kFwP;  // frame within the CTA
+    const int fc = tid / kFwP;  // frame within the CTA (kFwP lanes each)
     const int64_t b = blockIdx.y;
-    const int fi0 = blockIdx.x * 32;
+    const int fi0 = blockIdx.x * kFwpFrames;
     const int fi = fi0 + fc;
     const bool active = fi < nfr;
     const int L = size / kFwP;
@@ -264,7 +273,7 @@ k_fwp_forward(IO* __restrict__ seg, const IO* __restrict__ e, const IO* __restri
 #pragma unroll
     for (int i = 0; i < M; ++i) a[i] = active ? frames[(b * F + row) * M + i] : (IO)0;
     fwp_stage<IO, false>(es, e + b * T, (int64_t)(fi0 - n_lead) * hop,
-                         FwSmem<IO>::blocks(size, hop), T, hop, (IO)1, ws, win, L, lp, sbar);
+                         fwp_blocks(size, hop), T, hop, (IO)1, ws, win, L, lp, sbar);
     (void)warp;
     // input of window kw of this piece: window * e over the staged span
     const IO* wsp = ws + p * lp;
@@ -321,7 +330,7 @@ k_fwp_forward(IO* __restrict__ seg, const IO* __restrict__ e, const IO* __restri
 }
 
 template <typename IO, int M>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kFwpThreads)
 k_fwp_backward(IO* __restrict__ gew, IO* __restrict__ gapart, const IO* __restrict__ seg,
                const IO* __restrict__ gout, const IO* __restrict__ frames,
                const IO* __restrict__ win, int64_t T, int F, int nfr, int size, int hop,
@@ -330,14 +339,14 @@ k_fwp_backward(IO* __restrict__ gew, IO* __restrict__ gapart, const IO* __restri
     using S = FwpSmem<IO>;
     constexpr int W = kFwW;
     constexpr int NBK = (M + 1 + W - 1) / W;  // blocks below the window that the lags reach
-    constexpr int NRB = NBK + 1;              // ring blocks: those and the window's own
+    constexpr int NRB = NBK + 1;              // those and the window's own
     constexpr int SR = NRB * W;
     extern __shared__ __align__(128) unsigned char fw_smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int p = lane & (kFwP - 1);
-    const int fc = warp * (32 / kFwP) + lane / kFwP;
+    const int fc = tid / kFwP;
     const int64_t b = blockIdx.y;
-    const int fi0 = blockIdx.x * 32;
+    const int fi0 = blockIdx.x * kFwpFrames;
     const int fi = fi0 + fc;
     const bool active = fi < nfr;
     const int L = size / kFwP;
@@ -351,7 +360,7 @@ k_fwp_backward(IO* __restrict__ gew, IO* __restrict__ gapart, const IO* __restri
 #pragma unroll
     for (int i = 0; i < M; ++i) a[i] = active ? frames[(b * F + row) * M + i] : (IO)0;
     fwp_stage<IO, true>(gs, gout + b * T, (int64_t)(fi0 - n_lead) * hop,
-                        FwSmem<IO>::blocks(size, hop), T, hop, cola, ws, win, L, lp, sbar);
+                        fwp_blocks(size, hop), T, hop, cola, ws, win, L, lp, sbar);
     (void)warp;
     const int kend = (p + 1) * L;  // the piece covers k in [kend - L, kend), walked downward
     // pass 1 input, reversed time m: g(kend - 1 - m)
@@ -405,6 +414,10 @@ k_fwp_backward(IO* __restrict__ gew, IO* __restrict__ gapart, const IO* __restri
     // lives in ring block (NBK - j) mod NRB, so with NRB windows unrolled
     // every index is static.  The block that replaces a finished window is
     // prefetched one window ahead.
+    // sv[i] = s(kw - NBK*W + i): the current window's saved outputs and the
+    // NBK blocks below (the lags reach M samples down), a shift register
+    // moved down one block per window (one window of code: it stays in the
+    // instruction cache); the next two blocks below are prefetched
     IO sv[SR];
     const int nwin = L / W;
     const int kw0 = kend - W;  // top window
@@ -417,58 +430,50 @@ k_fwp_backward(IO* __restrict__ gew, IO* __restrict__ gapart, const IO* __restri
             for (int u = 0; u < W; ++u) sv[(NBK - j) * W + u] = t[u];
         }
     }
-    IO pf[W];
-    sload(kw0 - NRB * W, pf);
-    for (int wb = 0; wb < nwin; wb += NRB) {
+    IO pf0[W], pf1[W];
+    sload(kw0 - NRB * W, pf0);
+    sload(kw0 - (NRB + 1) * W, pf1);
+#pragma unroll 1
+    for (int wi = 0; wi < nwin; ++wi) {
+        const int kw = kw0 - wi * W;
+        IO gv[W], wk[W], ov[W];
+        {
+            const int o0 = fc * hop + kw;
+            const int q0 = o0 / hop, r0 = o0 - q0 * hop;
 #pragma unroll
-        for (int w4 = 0; w4 < NRB; ++w4) {
-            const int wi = wb + w4;  // window index from the top
-            if (wi < nwin) {
-                const int kw = kw0 - wi * W;
-                // ring block of the current window: the top window's is NBK,
-                // each window down one less (mod NRB) -- compile-time here
-                const int cb = (NBK - w4 + NRB) % NRB;
-                IO gv[W], wk[W], ov[W];
-                {
-                    const int o0 = fc * hop + kw;
-                    const int q0 = o0 / hop, r0 = o0 - q0 * hop;
-#pragma unroll
-                    for (int u = 0; u < W; ++u) {
-                        const int r = r0 + u;
-                        gv[u] = gs[q0 * hst + r + (r >= hop ? hst - hop : 0)];
-                        wk[u] = wsp[kw - p * L + u];
-                    }
-                }
-#pragma unroll
-                for (int u = W - 1; u >= 0; --u) {
-                    const IO l0 = lam[0] + gv[u];
-                    ov[u] = l0 * wk[u];
-#pragma unroll
-                    for (int c = 0; c < M; ++c) {
-                        // s(kw + u - 1 - c): ring slot (cb * W + u - 1 - c) mod SR
-                        ga[c] = fma(sv[(cb * W + u - 1 - c + 2 * SR) % SR], l0, ga[c]);
-                    }
-#pragma unroll
-                    for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
-                    lam[M - 1] = -a[M - 1] * l0;
-                }
-                if (active) fw_store_window<IO, W>(grow + kw, ov, W);
-                // the window just finished (block cb) becomes the block NRB
-                // below it, prefetched during this window
-#pragma unroll
-                for (int u = 0; u < W; ++u) sv[cb * W + u] = pf[u];
-                sload(kw - (NRB + 1) * W, pf);
+            for (int u = 0; u < W; ++u) {
+                const int r = r0 + u;
+                gv[u] = gs[q0 * hst + r + (r >= hop ? hst - hop : 0)];
+                wk[u] = wsp[kw - p * L + u];
             }
         }
+#pragma unroll
+        for (int u = W - 1; u >= 0; --u) {
+            const IO l0 = lam[0] + gv[u];
+            ov[u] = l0 * wk[u];
+#pragma unroll
+            for (int c = 0; c < M; ++c) ga[c] = fma(sv[NBK * W + u - 1 - c], l0, ga[c]);
+#pragma unroll
+            for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
+            lam[M - 1] = -a[M - 1] * l0;
+        }
+        if (active) fw_store_window<IO, W>(grow + kw, ov, W);
+#pragma unroll
+        for (int i = SR - 1; i >= W; --i) sv[i] = sv[i - W];
+#pragma unroll
+        for (int u = 0; u < W; ++u) {
+            sv[u] = pf0[u];
+            pf0[u] = pf1[u];
+        }
+        sload(kw - (NRB + 2) * W, pf1);
     }
-    // the frame's four partial correlations, summed in piece order
+    // the frame's partial correlations, summed in piece order
 #pragma unroll
     for (int c = 0; c < M; ++c) {
         IO v = ga[c];
-        const IO v1 = __shfl_down_sync(0xffffffffu, v, 1);
-        const IO v2 = __shfl_down_sync(0xffffffffu, v, 2);
-        const IO v3 = __shfl_down_sync(0xffffffffu, v, 3);
-        ga[c] = ((v + v1) + v2) + v3;
+#pragma unroll
+        for (int d = 1; d < kFwP; ++d) v += __shfl_down_sync(0xffffffffu, ga[c], d);
+        ga[c] = v;
     }
     if (active && p == 0) {
 #pragma unroll
