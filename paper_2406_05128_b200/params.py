@@ -161,20 +161,39 @@ class FramePlan:
             if hi > lo:
                 yield (f if f > 0 else 0), lo, hi, lo - t0, hi - t0
 
-    # device copy of the window in the I/O dtype (params.py:232, 266: astype(e.dtype)),
-    # cached on the window's CONTENTS (an in-place edit or a new array of the
-    # same id never returns a stale copy)
+    # Per-call derived state of the kernel path: the COLA deviation, the COLA
+    # constant and the device copies of the window in each I/O dtype
+    # (params.py:232, 266: astype(e.dtype)).  All are functions of
+    # (frame_size, hop, window contents), so they are cached on exactly that
+    # key: an in-place edit of the window or a new array is seen (the key
+    # holds the window's bytes), while a repeated call costs one comparison
+    # instead of re-validating the window (~50 us of numpy per call).
+    def _derived(self):
+        w = np.asarray(self.window)
+        key = (self.frame_size, self.hop, w.dtype.str, w.shape, w.tobytes())
+        st = self.__dict__.get("_derived_cache")
+        if st is None or st[0] != key:
+            st = (key, self.ola_deviation(), self.cola_constant(), {})
+            self.__dict__["_derived_cache"] = st
+        return st
+
+    def _validate_cola_cached(self, tol=1e-6):
+        dev = self._derived()[1]
+        if dev > tol:
+            raise ValueError(f"window does not satisfy constant overlap-add; deviation {dev:.3e}")
+
+    def _cola_cached(self):
+        return self._derived()[2]
+
     def _window_tensor(self, dtype, device):
-        np_dt = np.float32 if dtype == torch.float32 else np.float64
-        host = np.ascontiguousarray(np.asarray(self.window).astype(np_dt))
-        cache = self.__dict__.setdefault("_wcache", {})
-        key = (dtype, str(device), host.tobytes())
-        w = cache.get(key)
+        tens = self._derived()[3]
+        key = (dtype, str(device))
+        w = tens.get(key)
         if w is None:
-            if len(cache) > 8:
-                cache.clear()
+            np_dt = np.float32 if dtype == torch.float32 else np.float64
+            host = np.ascontiguousarray(np.asarray(self.window).astype(np_dt))
             w = torch.from_numpy(host).to(device)
-            cache[key] = w
+            tens[key] = w
         return w
 
 
@@ -185,7 +204,7 @@ def _check(e, frames, plan):
         raise ValueError(
             f"got {F} coefficient frames but length {T1} at hop {plan.hop} "
             f"requires {expected_frame_count(T1 - 1, plan.hop)}")
-    plan.validate_cola()
+    plan._validate_cola_cached()
 
 
 def framewise_forward(e, frames, plan):
@@ -211,7 +230,7 @@ def framewise_forward(e, frames, plan):
                                                    plan.hop), conv.device)
     with torch.cuda.device(conv.device):
         N.check(lib.tvlp_framewise_forward(dt, N.ptr(e), N.ptr(frames), N.ptr(w),
-                                           plan.cola_constant(), N.ptr(out), N.ptr(seg), B, T, F,
+                                           plan._cola_cached(), N.ptr(out), N.ptr(seg), B, T, F,
                                            M, plan.frame_size, plan.hop, N.ptr(ws), nws,
                                            N.stream_ptr(conv.device)))
     return conv.out(out), seg
@@ -239,7 +258,7 @@ def framewise_backward(grad_out, frames, seg, plan):
                                                    plan.hop), conv.device)
     with torch.cuda.device(conv.device):
         N.check(lib.tvlp_framewise_backward(dt, N.ptr(g), N.ptr(frames), N.ptr(w),
-                                            plan.cola_constant(), N.ptr(seg), N.ptr(ge),
+                                            plan._cola_cached(), N.ptr(seg), N.ptr(ge),
                                             N.ptr(gf), B, T, F, M, plan.frame_size, plan.hop,
                                             N.ptr(ws), nws, N.stream_ptr(conv.device)))
     return conv.out(ge), conv.out(gf)

@@ -166,14 +166,25 @@ def test_frameplan_semantics_match_reference_contract():
 
 
 def test_window_cache_follows_contents():
-    """The device window cache is keyed by the window's contents: editing the
-    window in place yields the new values (no stale copy)."""
+    """The kernel path's cached window state (COLA check, COLA constant, the
+    device copy of the window) is keyed by the window's contents: editing the
+    window in place is seen on the next call (no stale copy), and a repeated
+    call reuses the cached copy."""
     import numpy as np
+    import pytest
+    import torch
 
     from paper_2406_05128_b200 import params
 
-    p = params.FramePlan.rectangular(8)
-    k1 = (np.float32, np.asarray(p.window).astype(np.float32).tobytes())
-    p.window[3] = 0.5
-    k2 = (np.float32, np.asarray(p.window).astype(np.float32).tobytes())
-    assert k1 != k2
+    p = params.FramePlan.raised_cosine(8)
+    w1 = p._window_tensor(torch.float32, "cpu")
+    assert p._window_tensor(torch.float32, "cpu") is w1  # cached
+    np.testing.assert_array_equal(w1.numpy(), p.window.astype(np.float32))
+    p._validate_cola_cached()
+    assert p._cola_cached() == p.cola_constant()
+    p.window[3] = 0.5  # in place: no longer COLA
+    w2 = p._window_tensor(torch.float32, "cpu")
+    assert float(w2[3]) == 0.5
+    with pytest.raises(ValueError, match="constant overlap-add"):
+        p._validate_cola_cached()
+    assert p._cola_cached() == p.cola_constant()
