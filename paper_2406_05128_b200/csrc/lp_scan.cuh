@@ -966,6 +966,85 @@ k_group_P(const CT* __restrict__ tape, CT* __restrict__ gtape, int64_t ngroups, 
     }
 }
 
+// Group products as a tree: one CTA per group loads the G transition
+// matrices (R rows) with bulk copies and multiplies neighbours level by level
+// in shared memory (slot i <- slot i+s x slot i; later sub-chunks on the
+// left), so a group costs log2(G) dependent mat-mats instead of G (k_group_P:
+// one warp, 32 serial mat-mats per group, 83 us at config 4).  Lane j of a
+// warp forms column j of a product from its own column of the right factor
+// (registers) and broadcast rows of the left one; the result overwrites the
+// right factor in place (column j is only read by lane j).
+constexpr int kTreeWarps = 8;
+template <int M, typename CT>
+__global__ void __launch_bounds__(kTreeWarps * 32)
+k_group_P_tree(const CT* __restrict__ tape, CT* __restrict__ gtape, int64_t ngroups, int G,
+               int nsub, const int* __restrict__ only) {
+    grid_dep_wait();
+    using TP = Tape<M>;
+    constexpr int MP4 = TP::MP4;
+    constexpr int MAT = M * MP4;  // one matrix: M rows of MP4
+    extern __shared__ __align__(128) unsigned char smem[];
+    CT* slots = reinterpret_cast<CT*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)G * MAT * sizeof(CT));
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t gi = blockIdx.x;
+    if (gi >= ngroups) return;
+    const int ng = (nsub + G - 1) / G;
+    const int64_t b = gi / ng;
+    if (only != nullptr && only[b] == 0) return;
+    const int k0 = (int)(gi % ng) * G;
+    const int n = min(G, nsub - k0);
+    const int64_t base = b * nsub + k0;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, (uint32_t)(n * MAT * sizeof(CT)));
+        for (int t = 0; t < n; ++t)
+            tma_load_1d(slots + t * MAT, tape + (base + t) * TP::SIZE + TP::R_ROW * MP4,
+                        (uint32_t)(MAT * sizeof(CT)), bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    for (int st = 1; st < n; st *= 2) {
+        const int npair = (n - st + 2 * st - 1) / (2 * st);  // pairs (i, i+st), i = 2*st*q
+        for (int q = warp; q < npair; q += kTreeWarps) {
+            CT* R = slots + (2 * st * q) * MAT;   // right factor, overwritten
+            const CT* L = R + st * MAT;           // left factor
+            if (lane < M) {
+                CT col[MP4];
+#pragma unroll
+                for (int k = 0; k < MP4; ++k) col[k] = k < M ? R[k * MP4 + lane] : (CT)0;
+                // outer-product order: one accumulator per row, a 4-wide slice
+                // of every row of L per step -- 22 independent FMA chains
+                CT out[M];
+#pragma unroll
+                for (int r = 0; r < M; ++r) out[r] = (CT)0;
+#pragma unroll
+                for (int kb = 0; kb < MP4; kb += 4) {
+#pragma unroll
+                    for (int r = 0; r < M; ++r) {
+                        CT v[4];
+                        load_vec<CT, 4>(L + r * MP4 + kb, v);
+#pragma unroll
+                        for (int d = 0; d < 4; ++d)
+                            if (kb + d < M) out[r] = fma(v[d], col[kb + d], out[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < M; ++r) R[r * MP4 + lane] = out[r];
+            }
+        }
+        __syncthreads();
+    }
+    CT* gt = gtape + gi * TP::SIZE;
+    for (int idx = tid; idx < M * M; idx += blockDim.x) {
+        const int r = idx / M, c = idx - r * M;
+        const CT v = slots[r * MP4 + c];
+        gt[(TP::R_ROW + r) * MP4 + c] = v;  // R[r][c] = P[r][c]
+        gt[c * MP4 + r] = v;                // W[c] = column c
+    }
+}
+
 // ============================================================================
 // Lane-per-sub-chunk streaming kernels (apply fwd, adjoint zero-state, apply
 // bwd).  One warp = 32 consecutive sub-chunks; lane l runs the recursion of

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // scan_kernels.cu -- instantiations and launchers of the chunked-scan kernels.
 #include <cstring>
 
@@ -250,6 +251,20 @@ cudaError_t carry_bwd_impl(const CarryArgs<IO>& a, cudaStream_t st) {
 template <int M, typename IO>
 cudaError_t group_P_impl(const IO* tape, IO* gtape, int64_t ngroups, int G, int nsub,
                          const int* only, cudaStream_t st) {
+    // product tree (default) or one warp of serial mat-mats ($TVLP_COMPOSE_TREE=0)
+    static const int tree = [] {
+        const char* v = std::getenv("TVLP_COMPOSE_TREE");
+        return (v != nullptr && v[0] != 0) ? std::atoi(v) : 1;
+    }();
+    const size_t tb = (size_t)G * M * Tape<M>::MP4 * sizeof(IO) + 16;
+    if (tree && tb <= 220 * 1024) {
+        auto kt = k_group_P_tree<M, IO>;
+        cudaError_t err = ensure_smem(kt, (int)tb);
+        if (err != cudaSuccess) return err;
+        launch_pdl(kt, (unsigned)ngroups, kTreeWarps * 32, tb, st, tape, gtape, ngroups, G, nsub,
+                   only);
+        return cudaGetLastError();
+    }
     using SM = CarrySmem<M, IO, 4>;
     auto k = k_group_P<M, IO>;
     cudaError_t err = ensure_smem(k, SM::BYTES);
