@@ -20,9 +20,12 @@ Besides the device-resident ``value`` the line carries:
   roofline     the dominant kernel's algorithmic bytes / its CUDA-event
                duration (profiling pass over the same K steps) vs the measured
                HBM copy bandwidth in MEASURED_PEAKS.json, plus the whole step;
-  cpu_baseline the oracle (C port of the reference LP path, oracle/) timed on
-               this host's cores on a bounded sample (rank 0, N=1 only).
-``--impl reference`` times that CPU port alone (the reference arm).
+  cpu_baseline the reference's own CPU implementation -- the unmodified tvlp
+               (numba) installed in baseline/_ref -- on N worker processes
+               (N = host threads, capped at the step's sequences) and on one,
+               with the oracle's threaded C port (oracle/) beside it, on a
+               bounded sample (rank 0, N=1 only; baseline/tvlp_cpu.py).
+``--impl reference`` times the same CPU leg alone (the reference arm).
 """
 from __future__ import annotations
 
@@ -216,33 +219,40 @@ class Clocks:
 # CPU baseline: the oracle (C port of the reference path), threaded
 # ---------------------------------------------------------------------------
 
-def cpu_baseline(cfg, seconds=10.0, reference=True):
-    """The oracle's threaded C port on all host threads (the headline
-    ``cpu_baseline``, kind "port"), the same port on one thread, and -- when
-    baseline/_ref holds the reference install -- the unmodified reference
-    ``tvlp`` itself on 1 and N processes (baseline/tvlp_cpu.py), with the CPU
-    model string."""
+def cpu_baseline(cfg, seconds=10.0):
+    """The reference's own CPU implementation on this host: the unmodified
+    ``tvlp`` (numba, baseline/_ref) on N worker processes is the headline
+    (kind "reference"), with its 1-process figure; the oracle's threaded C
+    port (oracle/tvlp_oracle.c) on N threads and on 1 thread is reported
+    beside it (kind "port", the headline only when baseline/_ref is absent).
+    N = host threads, capped at the step's independent sequences (the
+    reference filters each sequence serially).  Includes the CPU model."""
     nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     # the reference filters each sequence serially: a step's work spreads over
     # at most one core per independent sequence (config 4's one 14.4 M-sample
     # sequence is one core's work whatever the host)
     nthreads = max(1, min(nthreads, cfg["B"] * (2 if cfg["kind"] == "hpn" else 1)))
-    out = _port_baseline(cfg, nthreads, seconds)
+    port = _port_baseline(cfg, nthreads, seconds)
     one = _port_baseline(cfg, 1, max(3.0, seconds / 3), one_core=True)
-    out["one_core"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
+    port["one_core"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
     sys.path.insert(0, os.path.join(ROOT, "baseline"))
     import tvlp_cpu
 
-    out["cpu_model"] = tvlp_cpu.cpu_model()
-    if reference and tvlp_cpu.available():
+    ref = None
+    if tvlp_cpu.available():
         T_ref = min(cfg["T"], 480_000)  # a bounded slice of config 4's one sequence
         try:
-            out["reference_tvlp"] = tvlp_cpu.measure(
-                cfg["kind"], T_ref, cfg["M"], cfg.get("hop", 240), procs=nthreads,
-                seconds=max(3.0, seconds / 2), lps_per_sample=2 if cfg["kind"] == "hpn" else 1)
-        except Exception as ex:  # reported, never fatal to the GPU line
-            out["reference_tvlp"] = {"unavailable": f"{type(ex).__name__}: {ex}"[:200]}
-    return out
+            ref = tvlp_cpu.measure(cfg["kind"], T_ref, cfg["M"], cfg.get("hop", 240),
+                                   procs=nthreads, seconds=max(3.0, seconds / 2),
+                                   lps_per_sample=2 if cfg["kind"] == "hpn" else 1)
+        except Exception as ex:  # reported; the port stands in
+            port["reference_error"] = f"{type(ex).__name__}: {ex}"[:200]
+    if ref is None:
+        port["cpu_model"] = tvlp_cpu.cpu_model()
+        return port
+    return {"value": ref["n_core"]["value"], "unit": UNIT, "cores": ref["n_core"]["cores"],
+            "kind": "reference", "impl": ref["impl"], "cpu_model": ref["cpu_model"],
+            "sample": ref["sample"], "one_core": ref["one_core"], "port": port}
 
 
 def _port_baseline(cfg, nthreads, seconds, one_core=False):
@@ -519,12 +529,14 @@ def run_b200(args, cfg, rank, world, dist):
         t_step = tot / nsteps * 1e-3  # seconds of this kernel per step (all its slices)
         ach = (bps * lp_rows * T_k / t_step / 1e9) if bps is not None else None
         traffic = None
-        tf = os.path.join(ROOT, "profiles", "r1_traffic.json")
-        if os.path.exists(tf) and kind in ("tv", "hpn") and (lp_rows, T, M) == (64, 48000, 22):
-            # dram__bytes_read + dram__bytes_write of this kernel, one ncu --set
-            # full capture of the same config (profiles/r1_ncu_full_raw.csv)
+        tf = os.path.join(ROOT, "profiles", "r2_traffic.json")
+        if (os.path.exists(tf) and kind in ("tv", "hpn") and (lp_rows, T, M) == (64, 48000, 22)
+                and world == 1):
+            # dram__bytes_read + dram__bytes_write of this phase's kernels in one
+            # step, from the ncu capture of the same config
+            # (profiles/r2_ncu_tv_b64_t48000.csv via tools/traffic_from_ncu.py)
             with open(tf) as fh:
-                traffic = json.load(fh).get(dom, {}).get("dram_bytes")
+                traffic = json.load(fh).get("per_step", {}).get(dom, {}).get("dram_bytes")
         roof = {"bound": "hbm", "kernel": dom,
                 "achieved": None if ach is None else round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": None if ach is None else round(ach / hbm, 4), "traffic": traffic,
