@@ -23,6 +23,7 @@ Inputs of shape [B, ...] render B items at once.
 """
 from __future__ import annotations
 
+import functools
 import math
 from dataclasses import dataclass
 
@@ -45,12 +46,36 @@ DEFAULT_FFT_SIZES = (509, 1021, 2053)  # loss.py:22
 LOG_EPS = 1e-8            # loss.py:23
 
 
-def design_lowpass(num_taps=127, cutoff=0.45, oversample=4):
-    """Windowed-sinc decimation lowpass (source.py:215-222), float64 numpy."""
+@functools.lru_cache(maxsize=16)
+def _lowpass_np(num_taps, cutoff, oversample):
     fc = cutoff / (2.0 * oversample)
     n = np.arange(num_taps) - (num_taps - 1) / 2.0
     h = 2.0 * fc * np.sinc(2.0 * fc * n) * np.blackman(num_taps)
-    return h / h.sum()
+    h = h / h.sum()
+    h.setflags(write=False)
+    return h
+
+
+_DEV_CACHE = {}
+
+
+def _on_device(key, build, device, dtype):
+    """Host-built constants (taps, windows, frame indices) uploaded once per
+    (key, device, dtype): a decoder step makes no host->device copies."""
+    k = (key, str(device), dtype)
+    t = _DEV_CACHE.get(k)
+    if t is None:
+        if len(_DEV_CACHE) > 64:
+            _DEV_CACHE.clear()
+        t = build()
+        t = t.to(device=device, dtype=dtype) if dtype is not None else t.to(device=device)
+        _DEV_CACHE[k] = t
+    return t
+
+
+def design_lowpass(num_taps=127, cutoff=0.45, oversample=4):
+    """Windowed-sinc decimation lowpass (source.py:215-222), float64 numpy."""
+    return _lowpass_np(num_taps, cutoff, oversample).copy()
 
 
 def _weights(F, hop, T1, device, dtype):
@@ -63,29 +88,75 @@ def _weights(F, hop, T1, device, dtype):
     return f0, f1, w
 
 
+def _block_weights(F, hop, device, dtype):
+    """The same weights as [F, hop] blocks (block f covers t = f*hop + j):
+    j / hop, and 0 in the last block (params.py:113-115)."""
+    w = (torch.arange(hop, device=device).to(dtype) / float(hop))[None].repeat(F, 1)
+    w[F - 1] = 0
+    return w
+
+
+class _Upsample(torch.autograd.Function):
+    """params.py:120-145 as dense block arithmetic: forward
+    (1 - w) frames[f] + w frames[f + 1] over [F, hop] blocks (bit-identical to
+    the gather form), backward the two weighted block sums (the scatter of
+    params.py:135-145 without a sorting index_put)."""
+
+    @staticmethod
+    def forward(ctx, frames, hop, T1):
+        Bn, F = frames.shape[:2]
+        w = _block_weights(F, hop, frames.device, frames.dtype)
+        nxt = torch.cat([frames[:, 1:], frames[:, -1:]], dim=1)
+        if frames.dim() == 3:
+            w = w[..., None]
+            out = (1.0 - w) * frames[:, :, None] + w * nxt[:, :, None]   # [B, F, hop, D]
+            out = out.reshape(Bn, F * hop, frames.shape[2])[:, :T1]
+        else:
+            out = (1.0 - w) * frames[:, :, None] + w * nxt[:, :, None]   # [B, F, hop]
+            out = out.reshape(Bn, F * hop)[:, :T1]
+        ctx.shape = (F, hop, T1, frames.dim())
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        F, hop, T1, nd = ctx.shape
+        Bn = g.shape[0]
+        w = _block_weights(F, hop, g.device, g.dtype)
+        pad = F * hop - T1
+        if nd == 3:
+            gp = TF.pad(g, (0, 0, 0, pad)).reshape(Bn, F, hop, g.shape[-1])
+            w = w[..., None]
+        else:
+            gp = TF.pad(g, (0, pad)).reshape(Bn, F, hop)
+        ga = ((1.0 - w) * gp).sum(dim=2)        # to frame f
+        gb = (w * gp).sum(dim=2)                # to frame f + 1 (zero in the last block)
+        gf = ga.clone()
+        gf[:, 1:] += gb[:, :-1]
+        return gf, None, None
+
+
 def upsample_linear(frames, hop, T1):
     """params.py:120-132 for [B, F] or [B, F, D] frame controls -> [B, T1(, D)]
     (T1 = T + 1 samples).  Differentiable (the VJP is the scatter of
-    params.py:135-145, by autograd)."""
+    params.py:135-145)."""
     F = frames.shape[1]
     if F != (T1 - 1) // hop + 1:
         raise ValueError(f"got {F} frames but T={T1 - 1} at hop={hop} requires "
                          f"{(T1 - 1) // hop + 1}")
-    f0, f1, w = _weights(F, hop, T1, frames.device, frames.dtype)
-    if frames.dim() == 3:
-        w = w[:, None]
-    return (1.0 - w) * frames[:, f0] + w * frames[:, f1]
+    return _Upsample.apply(frames, hop, T1)
 
 
-def oscillator_phase(f0_frames, hop, n_out, fs, oversample):
+def oscillator_phase(f0_frames, hop, n_out, fs, oversample, device=None):
     """Per-sample table phase (periods, mod 1) at the oversampled rate
-    (source.py:224-238): float64 cumulative sum on the device."""
-    f0_frames = torch.as_tensor(f0_frames, dtype=torch.float64)
+    (source.py:224-238): float64 cumulative sum, on ``device`` (default: the
+    device of ``f0_frames``; host arrays -> CPU)."""
+    f0_frames = torch.as_tensor(f0_frames, dtype=torch.float64, device=device)
     if f0_frames.dim() == 1:
         f0_frames = f0_frames[None]
-    if bool((f0_frames >= fs / 2.0).any()):
-        raise ValueError("f0 at or above the output Nyquist frequency")
-    if bool((f0_frames < 0).any()):
+    bad = ((f0_frames >= fs / 2.0) | (f0_frames < 0)).any()
+    if bool(bad):  # one host sync; the message as the reference's
+        if bool((f0_frames >= fs / 2.0).any()):
+            raise ValueError("f0 at or above the output Nyquist frequency")
         raise ValueError("f0 must be nonnegative")
     n_os = n_out * oversample
     f0 = upsample_linear(f0_frames, hop * oversample, n_os)
@@ -150,12 +221,21 @@ def fir_from_logmag(logmag):
                                                        else torch.complex64),
                                  n=n_fir, dim=-1)
     centered = torch.roll(zero_phase, B - 1, dims=-1)
-    window = torch.as_tensor(np.hanning(n_fir), dtype=logmag.dtype, device=logmag.device)
+    window = _on_device(("hann", n_fir), lambda: torch.as_tensor(np.hanning(n_fir)),
+                        logmag.device, logmag.dtype)
     return centered * window
 
 
 def _frame_index(plan, n_out, F, device):
-    """Per-frame (row, sample index into [0, n_out) or -1) of plan.iter_frames."""
+    """Per-frame (row, sample index into [0, n_out) or -1) of plan.iter_frames
+    (cached per grid and device)."""
+    key = ("frames", plan.frame_size, plan.hop, n_out, F)
+    rows = _on_device(key + ("rows",), lambda: _frame_index_host(plan, n_out, F)[0], device, None)
+    idx = _on_device(key + ("idx",), lambda: _frame_index_host(plan, n_out, F)[1], device, None)
+    return rows, idx
+
+
+def _frame_index_host(plan, n_out, F):
     size = plan.frame_size
     rows, idx = [], []
     for row, sig_lo, sig_hi, win_lo, win_hi in plan.iter_frames(n_out, F):
@@ -163,8 +243,7 @@ def _frame_index(plan, n_out, F, device):
         ix[win_lo:win_hi] = np.arange(sig_lo, sig_hi)
         rows.append(row)
         idx.append(ix)
-    return (torch.as_tensor(np.array(rows), device=device),
-            torch.as_tensor(np.stack(idx), device=device))
+    return torch.as_tensor(np.array(rows)), torch.as_tensor(np.stack(idx))
 
 
 def shape_noise(logmag, noise, plan):
@@ -182,7 +261,7 @@ def shape_noise(logmag, noise, plan):
     dev, dt = logmag.device, logmag.dtype
     rows, idx = _frame_index(plan, n_out, F, dev)
     fir = fir_from_logmag(logmag)                                 # [B, F, 510]
-    win = torch.as_tensor(np.asarray(plan.window), dtype=dt, device=dev)
+    win = plan._window_tensor(dt, dev)
     valid = idx >= 0
     segs = torch.where(valid, noise[:, idx.clamp(min=0)], torch.zeros((), dtype=dt, device=dev))
     segs = segs * win                                            # [B, nfr, size]
@@ -197,7 +276,7 @@ def shape_noise(logmag, noise, plan):
     nc = -(-size // plan.hop)
     for j in range(nc):
         out = out.index_add(1, tgt[j::nc].reshape(-1), y[:, j::nc].reshape(Bn, -1))
-    return out[:, :n_out] / plan.cola_constant()
+    return out[:, :n_out] / plan._cola_cached()
 
 
 def global_fir(x, taps):
@@ -280,13 +359,14 @@ class Decoder:
         pos = torch.sigmoid(p["table_pos_raw"]) * (K - 1)
         vgain = torch.exp(p["voiced_gain_raw"])
         # oscillator (source.py:294-314)
-        phase = oscillator_phase(f0_frames, hop, n_out, self.fs, self.oversample).to(
-            device=pos.device, dtype=pos.dtype)
+        phase = oscillator_phase(f0_frames, hop, n_out, self.fs, self.oversample,
+                                 device=pos.device).to(pos.dtype)
         pos_track = upsample_linear(pos, hop * self.oversample, n_out * self.oversample)
         raw = wavetable_read(pos_track, self.tables.to(pos.dtype), phase)
         if self.oversample > 1:
-            taps = torch.as_tensor(design_lowpass(oversample=self.oversample), dtype=pos.dtype,
-                                   device=pos.device)
+            taps = _on_device(("lowpass", self.oversample),
+                              lambda: torch.as_tensor(_lowpass_np(127, 0.45, self.oversample).copy()),
+                              pos.device, pos.dtype)
             sig = decimate_fir(raw, taps, self.oversample, n_out)
         else:
             sig = raw
