@@ -44,15 +44,20 @@ __all__ = [
     "carry_precision",
 ]
 
-_VALIDATION = os.environ.get("TVLP_VALIDATION", "eager")
+_VALIDATION = os.environ.get("TVLP_VALIDATION", "auto")
 _CARRY = os.environ.get("TVLP_CARRY", "auto")
 _pending_flags = {}
 
 
 def set_validation(mode):
-    """'eager' (reference semantics), 'lazy' (check_nonfinite()) or 'off'."""
+    """Non-finite input checks: 'eager' (the reference's semantics: the call
+    raises ValueError, one host sync per forward), 'lazy' (a device flag,
+    reported by check_nonfinite()), 'off', or 'auto' (default): eager for
+    numpy callers -- the reference API, whose result returns to the host
+    anyway -- and lazy for CUDA-tensor callers, so a training step's
+    forwards never stall the host."""
     global _VALIDATION
-    if mode not in ("eager", "lazy", "off"):
+    if mode not in ("eager", "lazy", "off", "auto"):
         raise ValueError(f"unknown validation mode {mode!r}")
     _VALIDATION = mode
 
@@ -151,10 +156,18 @@ def _zi(zi, M, B, batched, dtype, conv):
     return zi.reshape(B, M).contiguous()
 
 
-def _flag(device):
-    if _VALIDATION == "off":
+def _mode(numpy_io=True):
+    """The effective validation mode of a call (numpy_io: host arrays in/out)."""
+    if _VALIDATION == "auto":
+        return "eager" if numpy_io else "lazy"
+    return _VALIDATION
+
+
+def _flag(device, mode=None):
+    mode = mode or _mode()
+    if mode == "off":
         return None
-    if _VALIDATION == "lazy":
+    if mode == "lazy":
         f = _pending_flags.get(device)
         if f is None:
             f = torch.zeros(1, dtype=torch.int32, device=device)
@@ -163,11 +176,11 @@ def _flag(device):
     return torch.zeros(1, dtype=torch.int32, device=device)
 
 
-def _raise_nonfinite(flag, e, A, a_name="A"):
+def _raise_nonfinite(flag, e, A, a_name="A", mode=None):
     """The kernel flags a non-finite OUTPUT: either non-finite input (an error,
     lpc.py:68-69/111-112) or overflow of an unstable filter (legitimate,
     lpc.py:86-87).  Only then are the inputs scanned to tell them apart."""
-    if flag is None or _VALIDATION != "eager":
+    if flag is None or (mode or _mode()) != "eager":
         return
     if int(flag.item()) != 0:
         if not bool(torch.isfinite(e).all()):
@@ -196,7 +209,7 @@ def _forward(ti, e, A, zi, carry_prec=None, return_carry=False):
         A = A.to(e.dtype).expand(B, M).contiguous() if A.dim() == 1 else A.to(e.dtype)
         if batched and A.shape[0] != B:
             raise ValueError(f"a has {A.shape[0]} rows but the batch has {B} signals")
-        if _VALIDATION == "eager" and not bool(torch.isfinite(A).all()):  # lpc.py:92-93
+        if _mode(conv.numpy) == "eager" and not bool(torch.isfinite(A).all()):  # lpc.py:92-93
             raise ValueError("a contains non-finite values")
     else:
         if A.dim() != e.dim() + 1:
@@ -217,13 +230,14 @@ def _forward(ti, e, A, zi, carry_prec=None, return_carry=False):
     carry = torch.empty(ncarry, dtype=e.dtype, device=conv.device)
     op = N.OP_FWD_TI if ti else N.OP_FWD_TV
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(op, dt, B, T, M, 0, 0, 0), conv.device)
-    flag = _flag(conv.device)
+    vmode = _mode(conv.numpy)
+    flag = _flag(conv.device, vmode)
     fn = lib.tvlp_lp_forward_ti if ti else lib.tvlp_lp_forward_tv
     cp = _carry_code(carry_prec)
     with torch.cuda.device(conv.device):
         N.check(fn(dt, N.ptr(e), N.ptr(A), N.ptr(zi), N.ptr(s), B, T, M, N.ptr(carry), cp,
                    N.ptr(ws), nws, N.ptr(flag), N.stream_ptr(conv.device)))
-    _raise_nonfinite(flag, e, A, "a" if ti else "A")
+    _raise_nonfinite(flag, e, A, "a" if ti else "A", vmode)
     out = conv.out(s)
     if return_carry:
         return out, carry
@@ -334,7 +348,7 @@ def lp_forward_tv_frames(e, frames, hop, zi=None, *, carry_precision=None, retur
     e = _signal(conv.t(e), "e").contiguous()
     frames = conv.t(frames, e.dtype)
     B, T, F, M, hop, batched = _frames_args(e, frames, hop, conv)
-    if _VALIDATION == "eager" and not bool(torch.isfinite(frames).all()):
+    if _mode(conv.numpy) == "eager" and not bool(torch.isfinite(frames).all()):
         raise ValueError("frames contains non-finite values")
     zi = _zi(zi, M, B, batched, e.dtype, conv)
     dt = N.dtype_code(e.dtype)
@@ -343,12 +357,13 @@ def lp_forward_tv_frames(e, frames, hop, zi=None, *, carry_precision=None, retur
     carry = torch.empty(lib.tvlp_carry_elems_frames(B, T, M), dtype=e.dtype, device=conv.device)
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FWD_TV_FRAMES, dt, B, T, M, F, 0, hop),
                           conv.device)
-    flag = _flag(conv.device)
+    vmode = _mode(conv.numpy)
+    flag = _flag(conv.device, vmode)
     with torch.cuda.device(conv.device):
         N.check(lib.tvlp_lp_forward_tv_frames(
             dt, N.ptr(e), N.ptr(frames), N.ptr(zi), N.ptr(s), B, T, M, F, hop, N.ptr(carry),
             _carry_code(carry_precision), N.ptr(ws), nws, N.ptr(flag), N.stream_ptr(conv.device)))
-    _raise_nonfinite(flag, e, frames, "frames")
+    _raise_nonfinite(flag, e, frames, "frames", vmode)
     out = conv.out(s)
     return (out, carry) if return_carry else out
 
@@ -429,14 +444,15 @@ def lp_forward_tv_grouped(groups, *, carry_precision=None, return_carry=False):
                                               0 if z is None else z.data_ptr(), s.data_ptr(),
                                               e.shape[0])
                                    for e, A, z, s in zip(es, As, zis, outs)])
-    flag = _flag(conv.device)
+    vmode = _mode(conv.numpy)
+    flag = _flag(conv.device, vmode)
     with torch.cuda.device(conv.device):
         N.check(lib.tvlp_lp_forward_tv_grouped(dt, len(es), arr, T, M, N.ptr(carry),
                                                _carry_code(carry_precision), N.ptr(ws), nws,
                                                N.ptr(flag), N.stream_ptr(conv.device)))
-    if flag is not None and _VALIDATION == "eager" and int(flag.item()) != 0:
+    if flag is not None and vmode == "eager" and int(flag.item()) != 0:
         for e, A in zip(es, As):
-            _raise_nonfinite(flag, e, A)
+            _raise_nonfinite(flag, e, A, "A", vmode)
     res = [conv.out(s) for s in outs]
     return (res, carry) if return_carry else res
 

@@ -199,6 +199,27 @@ def test_nonfinite_and_shape_errors():  # test_lpc.py:27-29, 59-61, 117-119
         lpc.lp_backward_tv(np.ones(4), np.zeros((5, 1)), np.ones(5))
 
 
+def test_validation_auto_modes():
+    """Default 'auto': numpy callers get the reference's immediate ValueError;
+    CUDA-tensor callers are not synchronised -- the device flag reports the
+    non-finite input at the next check_nonfinite()."""
+    assert lpc._mode(True) == "eager" and lpc._mode(False) == "lazy"
+    lpc.check_nonfinite()  # clear
+    e = torch.ones(2, 64, device="cuda")
+    A = torch.zeros(2, 64, 3, device="cuda")
+    A[1, 7, 2] = float("nan")
+    s = lpc.lp_forward_tv(e, A)  # no raise, no sync
+    assert lpc.check_nonfinite() is True
+    assert lpc.check_nonfinite() is False  # cleared
+    lpc.set_validation("eager")
+    try:
+        with pytest.raises(ValueError, match="A contains non-finite"):
+            lpc.lp_forward_tv(e, A)
+    finally:
+        lpc.set_validation("auto")
+    del s
+
+
 def test_no_cpu_fallback():
     with pytest.raises(RuntimeError, match="CUDA"):
         lpc.lp_forward_tv(torch.ones(8), torch.zeros(8, 2))
