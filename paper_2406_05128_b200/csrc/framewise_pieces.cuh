@@ -39,6 +39,9 @@
 #ifndef TVLP_FW_P
 #define TVLP_FW_P 4
 #endif
+#ifndef TVLP_FW_CARRY64
+#define TVLP_FW_CARRY64 0
+#endif
 constexpr int kFwP = TVLP_FW_P;  // pieces per frame (lanes per frame)
 static_assert(kFwP == 2 || kFwP == 4 || kFwP == 8, "a frame's lanes share a warp");
 constexpr int kFwpThreads = 128;                 // CTA
@@ -202,20 +205,25 @@ __device__ __forceinline__ void fwp_pass1(const IO (&a)[M], int L, In in, IO (&z
 template <typename IO, int M>
 __device__ __forceinline__ void fwp_exit(const IO (&a)[M], const IO (&ht)[2 * M], const IO (&z)[M],
                                          const IO (&x)[M], IO (&out)[M]) {
-    IO q[M];
+#if TVLP_FW_CARRY64
+    using AC = double;  // the carry's dot products in fp64 (one rounding per exit)
+#else
+    using AC = IO;
+#endif
+    AC q[M];
 #pragma unroll
     for (int k = 1; k <= M; ++k) {
-        IO v = x[k - 1];
+        AC v = (AC)x[k - 1];
 #pragma unroll
-        for (int i = 1; i <= M - k; ++i) v = fma(a[i - 1], x[k - 1 + i], v);
+        for (int i = 1; i <= M - k; ++i) v = fma((AC)a[i - 1], (AC)x[k - 1 + i], v);
         q[k - 1] = v;
     }
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-        IO v = z[j];
+        AC v = (AC)z[j];
 #pragma unroll
-        for (int k = 1; k <= M; ++k) v = fma(q[k - 1], ht[M - 1 - j + k], v);
-        out[j] = v;
+        for (int k = 1; k <= M; ++k) v = fma(q[k - 1], (AC)ht[M - 1 - j + k], v);
+        out[j] = (IO)v;
     }
 }
 
