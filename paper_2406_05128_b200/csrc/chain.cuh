@@ -300,15 +300,20 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
 // right), writes grad_e through the unit's output box; returns the carry-out.
 // grad_A fused into the adjoint re-application (north star (2)): the lanes
 // that produce grad_e(t) also write grad_A[t, c] = -grad_e(t) s(t-1-c)
-// (lpc.py:172), reading s once, with s(<0) from zi.  Measured slower than the
-// separate coalesced k_grad_A (config 3: bwd_chain 210 us against 66 + 52):
-// a lane's 704-byte window of grad_A rows is its own, so every 16-byte store
-// of a warp touches 32 different lines.  Off by default ($TVLP_FUSE_GRAD_A=1).
+// (lpc.py:172), reading s once, with s(<0) from zi.  Each lane's window of
+// rows is staged in shared memory and the warp writes the blocks
+// cooperatively (whole lines).  Measured slower than the separate k_grad_A
+// (config 3: bwd_chain 158 us against 66 + 52; 210 us with per-lane 16-byte
+// stores): grad_A is 88 B per sample and the 1.7 warps per SM of the chained
+// kernel cannot issue its stores fast enough (the separate kernel spreads
+// them over 56 k CTAs).  Off by default ($TVLP_FUSE_GRAD_A=1).
 struct GaOut {
     const float* s;   // the sequence's forward output [T]
     const float* zi;  // its initial state [M] (s(-i) = zi[i-1]) or null
     float* gA;        // its grad_A rows [T][M]
     int j0;           // sub-chunk (within the sequence) of the unit's lane 0
+    float* gst;       // shared staging, lane l at gst + l * gstride floats
+    int gstride;
 };
 
 template <int M, int U, int NST, int MODE, bool TI, bool GA = false>
@@ -414,8 +419,9 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
                     float glo[M];
 #pragma unroll
                     for (int c = 0; c < M; ++c) glo[c] = -l0 * sv[NBK * W + u - 1 - c];
-                    if (act) {
-                        float4* dst = reinterpret_cast<float4*>(go.gA + (tb + u) * M);
+                    {   // rows u, u+1 into the lane's staging block
+                        float4* dst =
+                            reinterpret_cast<float4*>(go.gst + lane * go.gstride + u * M);
 #pragma unroll
                         for (int q = 0; q < (2 * M) / 4; ++q) {
                             float v4[4];
@@ -424,7 +430,7 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
                                 const int i = 4 * q + d;
                                 v4[d] = i < M ? glo[i < M ? i : 0] : ghi[i >= M ? i - M : 0];
                             }
-                            __stcs(dst + q, make_float4(v4[0], v4[1], v4[2], v4[3]));
+                            dst[q] = make_float4(v4[0], v4[1], v4[2], v4[3]);
                         }
                     }
                 }
@@ -436,6 +442,20 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
         if (MODE == 1 && lane < L)
             store_window<float, W>(mp.o + (g0 + lane) * (int64_t)(nwin * W) + (nwin - 1 - k) * W, ov);
         if constexpr (GA) {
+            // the unit's windows of grad_A rows, one lane's block (W*M floats,
+            // contiguous in memory) per step: whole lines per store
+            __syncwarp();
+            constexpr int NQ = W * M / 4;  // float4 per block
+            const int64_t wofs = (int64_t)(nwin - 1 - k) * W;
+            for (int l = 0; l < L; ++l) {
+                const float4* src = reinterpret_cast<const float4*>(go.gst + l * go.gstride);
+                float4* dst = reinterpret_cast<float4*>(
+                    go.gA + ((int64_t)(go.j0 + l) * (nwin * W) + wofs) * M);
+#pragma unroll
+                for (int q0 = 0; q0 < NQ; q0 += 32)
+                    if (q0 + lane < NQ) __stcs(dst + q0 + lane, src[q0 + lane]);
+            }
+            __syncwarp();
 #pragma unroll
             for (int i = SV - 1; i >= W; --i) sv[i] = sv[i - W];
 #pragma unroll
@@ -625,7 +645,11 @@ struct BwdChainSmem {
     static constexpr int OFF_XS = OFF_NU + NU;
     static constexpr int OFF_XB = OFF_XS + XS;
     static constexpr int OFF_BAR = OFF_XB + 64 * 4;
-    static constexpr int BYTES = OFF_BAR + (NST + 1) * 8;
+    // fused grad_A: each lane's window of rows ([W][M] floats) is staged at a
+    // 16-byte-odd stride, then written warp-cooperatively (whole lines)
+    static constexpr int GST_LANE = ((kLaneWin * M * 4 + 15) / 16 | 1) * 16;
+    static constexpr int OFF_GST = (OFF_BAR + (NST + 1) * 8 + 15) / 16 * 16;
+    static constexpr int BYTES = OFF_GST + 32 * GST_LANE;
 };
 
 // ---------------------------------------------------------------- refinement of one sequence
@@ -712,7 +736,8 @@ __device__ bool refine_sequence_fwd(const ChainFwdArgs& a, int64_t b, unsigned c
 // repeated like the forward.
 template <int M, int NST, bool TI, bool GA>
 __device__ bool refine_sequence_bwd(const ChainBwdArgs& a, int64_t b, unsigned char* sm,
-                                    uint64_t* bars, float* xb, bool force, float xmax) {
+                                    uint64_t* bars, float* xb, bool force, float xmax,
+                                    float* gst, int gstride) {
     using TP = Tape<M>;
     constexpr int MP4 = TP::MP4;
     constexpr int U = TVLP_CHAIN_BWD_UNIT;
@@ -756,7 +781,7 @@ __device__ bool refine_sequence_bwd(const ChainBwdArgs& a, int64_t b, unsigned c
             const int64_t blr = b - a.gi.gB0[grp];
             const GaOut go{GA ? a.sg[grp] + blr * a.g.T : nullptr,
                            (GA && a.zig[grp] != nullptr) ? a.zig[grp] + blr * a.zs : nullptr,
-                           GA ? a.gAg[grp] + blr * a.g.T * M : nullptr, ru * U};
+                           GA ? a.gAg[grp] + blr * a.g.T * M : nullptr, ru * U, gst, gstride};
             unit_adj_pass<M, U, NST, 1, TI, GA>(a.mp[grp], L == U ? 0 : 1, vbase + (int64_t)ru * U,
                                                 L, nwin, sm, bars, lam, arow, go);
             if (lane < L) {
@@ -1077,7 +1102,8 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
         __syncwarp();
         const GaOut go{GA ? a.sg[grp] + bl * a.g.T : nullptr,
                        (GA && a.zig[grp] != nullptr) ? a.zig[grp] + bl * a.zs : nullptr,
-                       GA ? a.gAg[grp] + bl * a.g.T * M : nullptr, ru * U};
+                       GA ? a.gAg[grp] + bl * a.g.T * M : nullptr, ru * U,
+                       reinterpret_cast<float*>(smem + SM::OFF_GST), SM::GST_LANE / 4};
         unit_adj_pass<M, U, NST, 1, TI, GA>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow,
                                             go);
         tt[4] = gtime();
@@ -1116,7 +1142,9 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
                                  (a.inherit != nullptr && a.inherit[b] != 0);
                 if (bad) {
                     const bool done =
-                        refine_sequence_bwd<M, NST, TI, GA>(a, b, sl, bars, xb, bad, xmax);
+                        refine_sequence_bwd<M, NST, TI, GA>(
+                            a, b, sl, bars, xb, bad, xmax,
+                            reinterpret_cast<float*>(smem + SM::OFF_GST), SM::GST_LANE / 4);
                     if (done && lane == 0) atomicAdd(&g_chain_refined, 1ull);
                 }
             }
