@@ -81,10 +81,12 @@ struct Plan {
 // target is ~512 (one basis wave at config 3 and 100-step carry chains),
 // smaller when the batch has too few sub-chunks to fill the GPU: the
 // per-sub-chunk passes are then latency-bound and scale with Ls while the
-// serial carries scale with T/Ls (measured on config 1, us per fwd+bwd: Ls 480
-// 191, 320 160, 240 205).
+// serial carries scale with T/Ls.  Measured with the chained kernels (us per
+// fwd+bwd, tools/r2_ls_small.sh): config 1 (96 k samples) Ls 480 151, 320
+// 125, 240 115, 200 114, 160 113, 120 121; config 3's 8- and 4-way shares
+// (384 k / 768 k samples) flat within 2% over 240-320.
 int64_t choose_ls(int64_t B, int64_t T, int64_t* Tp, bool frames) {
-    int64_t target = B * T >= (int64_t)4096 * 512 ? 512 : 320;
+    int64_t target = B * T >= (int64_t)4096 * 512 ? 512 : (B * T >= 200000 ? 320 : 200);
     // frame-rate rows: the lane passes interpolate rows instead of streaming
     // them and are latency-bound, so more (shorter) sub-chunks pay for the
     // longer carry chains (config 3 measured: Ls 480 396 us, 240 354 us)
