@@ -694,18 +694,13 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
                  (launch_basis<IO>(p.Mp, ti, prec, s_p, A_p, phiz_own, g, st, frk)));
         if (hier) TVLP_RUN("compose", h.lv.L - 1, st, (h.compose()));
     }
-    bool chained = false, fused_gA = false;
+    bool chained = false;
     if constexpr (std::is_same<IO, float>::value) {
         if (chain) {
             const int* inherit = reinterpret_cast<const int*>(carry + tape_body(p));
             ChainBwdCall cc{ti, 1, {}, h.tape, inherit, nu, mu, kout, ctl,
                             prec == kPrecAuto ? 1 : 0, g};
-            cc.grp[0] = ChainGroup{gs_p, A_p, ti ? nullptr : zi_p, ge_p, p.B};
-            fused_gA = !ti && chain_fuse_grad_A();
-            if (fused_gA) {  // grad_A inside the adjoint re-application (measured slower)
-                cc.grp[0].s = s_p;
-                cc.grp[0].gA = gA_p;
-            }
+            cc.grp[0] = ChainGroup{gs_p, A_p, nullptr, ge_p, p.B};
             TVLP_RUN("adjoint_zs", 2, st, (launch_bwd_chain(p.Mp, cc, st, 0)));
             TVLP_RUN("bwd_chain", 1, st, (launch_bwd_chain(p.Mp, cc, st, 1)));
             chained = true;
@@ -776,7 +771,7 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
         TVLP_RUN("grad_a", 2, st,
                  (launch_grad_a<IO>(p.Mp, ge_p, s_p, zi_p, part, ga_out, p.B, p.Tp, nchunk, st)));
         if (ga_p) TVLP_CK(unpack<IO>(ga_p, gA, p.B, 1, p.M, 1, p.Mp, st));
-    } else if (!fused_gA) {
+    } else {
         TVLP_RUN("grad_A", 1, st, (launch_grad_A<IO>(p.Mp, ge_p, s_p, zi_p, gA_p, p.B, p.Tp, st)));
     }
     if (packed) {
@@ -967,25 +962,18 @@ int grouped_backward_impl(int n, const tvlp_lp_bwd_group* gr, const Plan& p, con
             ChainBwdCall cc{false, n, {}, carry,
                             reinterpret_cast<const int*>(carry + tape_body(p)), nu, mu, kout, ctl,
                             prec == kPrecAuto ? 1 : 0, g};
-            for (int i = 0; i < n; ++i) {
+            for (int i = 0; i < n; ++i)
                 cc.grp[i] = ChainGroup{static_cast<const float*>(gr[i].grad_s),
-                                       static_cast<const float*>(gr[i].A),
-                                       static_cast<const float*>(gr[i].zi),
+                                       static_cast<const float*>(gr[i].A), nullptr,
                                        static_cast<float*>(gr[i].grad_e), gr[i].B};
-                if (chain_fuse_grad_A()) {
-                    cc.grp[i].s = static_cast<const float*>(gr[i].s);
-                    cc.grp[i].gA = static_cast<float*>(gr[i].grad_A);
-                }
-            }
             TVLP_RUN("adjoint_zs", 1 + n, st, (launch_bwd_chain(p.Mp, cc, st, 0)));
             TVLP_RUN("bwd_chain", 1, st, (launch_bwd_chain(p.Mp, cc, st, 1)));
-            if (!chain_fuse_grad_A())
-                for (int i = 0; i < n; ++i)
-                    TVLP_RUN("grad_A", 1, st,
-                             (launch_grad_A<IO>(p.Mp, static_cast<const IO*>(gr[i].grad_e),
-                                                static_cast<const IO*>(gr[i].s),
-                                                static_cast<const IO*>(gr[i].zi),
-                                                static_cast<IO*>(gr[i].grad_A), gr[i].B, p.T, st)));
+            for (int i = 0; i < n; ++i)
+                TVLP_RUN("grad_A", 1, st,
+                         (launch_grad_A<IO>(p.Mp, static_cast<const IO*>(gr[i].grad_e),
+                                            static_cast<const IO*>(gr[i].s),
+                                            static_cast<const IO*>(gr[i].zi),
+                                            static_cast<IO*>(gr[i].grad_A), gr[i].B, p.T, st)));
         }
         return TVLP_OK;
     }

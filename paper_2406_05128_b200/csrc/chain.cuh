@@ -298,29 +298,10 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
 // MODE 0: zero-state adjoint of sub-chunk g0 + l (lam starts at 0), returns
 // nu_l in lam.  MODE 1: from lam (the carry into the sub-chunk from the
 // right), writes grad_e through the unit's output box; returns the carry-out.
-// grad_A fused into the adjoint re-application (north star (2)): the lanes
-// that produce grad_e(t) also write grad_A[t, c] = -grad_e(t) s(t-1-c)
-// (lpc.py:172), reading s once, with s(<0) from zi.  Each lane's window of
-// rows is staged in shared memory and the warp writes the blocks
-// cooperatively (whole lines).  Measured slower than the separate k_grad_A
-// (config 3: bwd_chain 158 us against 66 + 52; 210 us with per-lane 16-byte
-// stores): grad_A is 88 B per sample and the 1.7 warps per SM of the chained
-// kernel cannot issue its stores fast enough (the separate kernel spreads
-// them over 56 k CTAs).  Off by default ($TVLP_FUSE_GRAD_A=1).
-struct GaOut {
-    const float* s;   // the sequence's forward output [T]
-    const float* zi;  // its initial state [M] (s(-i) = zi[i-1]) or null
-    float* gA;        // its grad_A rows [T][M]
-    int j0;           // sub-chunk (within the sequence) of the unit's lane 0
-    float* gst;       // shared staging, lane l at gst + l * gstride floats
-    int gstride;
-};
-
-template <int M, int U, int NST, int MODE, bool TI, bool GA = false>
+template <int M, int U, int NST, int MODE, bool TI>
 __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int64_t g0, int L,
                                               int nwin, unsigned char* sm, uint64_t* bars,
-                                              float (&lam)[M], const float* ati,
-                                              const GaOut& go = GaOut{}) {
+                                              float (&lam)[M], const float* ati) {
     using S = UnitLane<M, U, NST>;
     constexpr int W = S::W;
     const int lane = threadIdx.x & 31;
@@ -349,51 +330,13 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
     };
 #pragma unroll
     for (int k = 0; k < NST; ++k) issue(k);
-    // GA: sv[i] = s(tb - NBK*W + i) for the current window's first time tb
-    // (the window and the NBK blocks below it that the lags reach), moved
-    // down one block per window; the next two blocks below are prefetched
-    constexpr int NBK = (M + 1 + W - 1) / W;
-    constexpr int SV = GA ? (NBK + 1) * W : 1;
-    float sv[SV], pf0[GA ? W : 1], pf1[GA ? W : 1];
-    const bool act = lane < L;
-    const int64_t tseq = GA ? (int64_t)(go.j0 + lane) * (nwin * W) : 0;  // lane's sub-chunk start
-    auto sblk = [&](int64_t t0, float* v) {  // s(t0 .. t0 + W - 1), t0 % W == 0
-        if (!act) {
-#pragma unroll
-            for (int e = 0; e < W; ++e) v[e] = 0.f;
-        } else if (t0 >= 0) {
-#pragma unroll
-            for (int q = 0; q < W / 4; ++q) {
-                const float4 f = __ldg(reinterpret_cast<const float4*>(go.s + t0) + q);
-                v[4 * q] = f.x;
-                v[4 * q + 1] = f.y;
-                v[4 * q + 2] = f.z;
-                v[4 * q + 3] = f.w;
-            }
-        } else {
-#pragma unroll
-            for (int e = 0; e < W; ++e) {
-                const int64_t t = t0 + e;
-                v[e] = t >= 0 ? go.s[t] : ((go.zi != nullptr && -t - 1 < M) ? go.zi[-t - 1] : 0.f);
-            }
-        }
-    };
-    if constexpr (GA) {
-        const int64_t tb0 = tseq + (int64_t)(nwin - 1) * W;
-#pragma unroll
-        for (int j = 0; j <= NBK; ++j) sblk(tb0 - j * W, sv + (NBK - j) * W);
-        sblk(tb0 - (NBK + 1) * W, pf0);
-        sblk(tb0 - (NBK + 2) * W, pf1);
-    }
     for (int k = 0; k < nwin; ++k) {
         const int st = k % NST;
         mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
         const unsigned char* base = sm + st * S::STAGE;
         const float* Ar = reinterpret_cast<const float*>(base) + ln * S::AROW;
         const float* xr = reinterpret_cast<const float*>(base + S::A_BYTES) + ln * S::XROW;
-        const int64_t tb = tseq + (int64_t)(nwin - 1 - k) * W;
         float gv[W], ov[W];
-        float ghi[GA ? M : 1];  // grad_A row of the odd sample of a pair
 #pragma unroll
         for (int u = 0; u < W; ++u) gv[u] = xr[u];
         // rows are loaded one step ahead (issued before this step's output
@@ -410,61 +353,12 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
                 load_row_at<float, M>(Ar + (u - 1) * M, an, (ln * S::AROW + (u - 1) * M) * 4);
             const float l0 = lam[0] + gv[u];
             ov[u] = l0;
-            if constexpr (GA) {
-                // rows u (even) and u+1 are 176 contiguous, 16-byte aligned bytes
-                if (u & 1) {
-#pragma unroll
-                    for (int c = 0; c < M; ++c) ghi[c] = -l0 * sv[NBK * W + u - 1 - c];
-                } else {
-                    float glo[M];
-#pragma unroll
-                    for (int c = 0; c < M; ++c) glo[c] = -l0 * sv[NBK * W + u - 1 - c];
-                    {   // rows u, u+1 into the lane's staging block
-                        float4* dst =
-                            reinterpret_cast<float4*>(go.gst + lane * go.gstride + u * M);
-#pragma unroll
-                        for (int q = 0; q < (2 * M) / 4; ++q) {
-                            float v4[4];
-#pragma unroll
-                            for (int d = 0; d < 4; ++d) {
-                                const int i = 4 * q + d;
-                                v4[d] = i < M ? glo[i < M ? i : 0] : ghi[i >= M ? i - M : 0];
-                            }
-                            dst[q] = make_float4(v4[0], v4[1], v4[2], v4[3]);
-                        }
-                    }
-                }
-            }
 #pragma unroll
             for (int i = 0; i < M - 1; ++i) lam[i] = fmaf(-a[i], l0, lam[i + 1]);
             lam[M - 1] = -a[M - 1] * l0;
         }
         if (MODE == 1 && lane < L)
             store_window<float, W>(mp.o + (g0 + lane) * (int64_t)(nwin * W) + (nwin - 1 - k) * W, ov);
-        if constexpr (GA) {
-            // the unit's windows of grad_A rows, one lane's block (W*M floats,
-            // contiguous in memory) per step: whole lines per store
-            __syncwarp();
-            constexpr int NQ = W * M / 4;  // float4 per block
-            const int64_t wofs = (int64_t)(nwin - 1 - k) * W;
-            for (int l = 0; l < L; ++l) {
-                const float4* src = reinterpret_cast<const float4*>(go.gst + l * go.gstride);
-                float4* dst = reinterpret_cast<float4*>(
-                    go.gA + ((int64_t)(go.j0 + l) * (nwin * W) + wofs) * M);
-#pragma unroll
-                for (int q0 = 0; q0 < NQ; q0 += 32)
-                    if (q0 + lane < NQ) __stcs(dst + q0 + lane, src[q0 + lane]);
-            }
-            __syncwarp();
-#pragma unroll
-            for (int i = SV - 1; i >= W; --i) sv[i] = sv[i - W];
-#pragma unroll
-            for (int e = 0; e < W; ++e) {
-                sv[e] = pf0[e];
-                pf0[e] = pf1[e];
-            }
-            sblk(tb - (NBK + 3) * W, pf1);
-        }
         __syncwarp();  // every lane is done with the stage: refill it
         issue(k + NST);
     }
@@ -589,10 +483,6 @@ struct ChainBwdArgs {
     UnitMaps mp[kMaxGroups];  // A, g_s, g_e lane views of each group
     GroupIdx gi;
     const float* Ag[kMaxGroups];  // TI: the constant rows [B_g][Mp]
-    const float* sg[kMaxGroups];  // TV, fused grad_A: the forward outputs [B_g][T]
-    const float* zig[kMaxGroups]; // and the initial states [B_g][zs] (nullable)
-    float* gAg[kMaxGroups];       // grad_A out [B_g][T][M]
-    int zs;
     CUtensorMap Tw;        // carry tape, box [8][M][MP4] from row 0 (W rows)
     const float* Nu;       // [B*nsub][MP4] zero-state adjoints (kernels without the pass)
     const float* tape;
@@ -645,11 +535,7 @@ struct BwdChainSmem {
     static constexpr int OFF_XS = OFF_NU + NU;
     static constexpr int OFF_XB = OFF_XS + XS;
     static constexpr int OFF_BAR = OFF_XB + 64 * 4;
-    // fused grad_A: each lane's window of rows ([W][M] floats) is staged at a
-    // 16-byte-odd stride, then written warp-cooperatively (whole lines)
-    static constexpr int GST_LANE = ((kLaneWin * M * 4 + 15) / 16 | 1) * 16;
-    static constexpr int OFF_GST = (OFF_BAR + (NST + 1) * 8 + 15) / 16 * 16;
-    static constexpr int BYTES = OFF_GST + 32 * GST_LANE;
+    static constexpr int BYTES = OFF_BAR + (NST + 1) * 8;
 };
 
 // ---------------------------------------------------------------- refinement of one sequence
@@ -734,10 +620,9 @@ __device__ bool refine_sequence_fwd(const ChainFwdArgs& a, int64_t b, unsigned c
 // Backward: e_{j-1} = Phi_j^T e_j + d_j, d_j = K_j - Mu_{j-1} (k_refine_bwd),
 // Mu += e; then the adjoint re-application of every unit of the sequence,
 // repeated like the forward.
-template <int M, int NST, bool TI, bool GA>
+template <int M, int NST, bool TI>
 __device__ bool refine_sequence_bwd(const ChainBwdArgs& a, int64_t b, unsigned char* sm,
-                                    uint64_t* bars, float* xb, bool force, float xmax,
-                                    float* gst, int gstride) {
+                                    uint64_t* bars, float* xb, bool force, float xmax) {
     using TP = Tape<M>;
     constexpr int MP4 = TP::MP4;
     constexpr int U = TVLP_CHAIN_BWD_UNIT;
@@ -778,12 +663,8 @@ __device__ bool refine_sequence_bwd(const ChainBwdArgs& a, int64_t b, unsigned c
             float lam[M];
 #pragma unroll
             for (int i = 0; i < M; ++i) lam[i] = lane < L ? a.Mu[(g0 + lane) * MP4 + i] : 0.f;
-            const int64_t blr = b - a.gi.gB0[grp];
-            const GaOut go{GA ? a.sg[grp] + blr * a.g.T : nullptr,
-                           (GA && a.zig[grp] != nullptr) ? a.zig[grp] + blr * a.zs : nullptr,
-                           GA ? a.gAg[grp] + blr * a.g.T * M : nullptr, ru * U, gst, gstride};
-            unit_adj_pass<M, U, NST, 1, TI, GA>(a.mp[grp], L == U ? 0 : 1, vbase + (int64_t)ru * U,
-                                                L, nwin, sm, bars, lam, arow, go);
+            unit_adj_pass<M, U, NST, 1, TI>(a.mp[grp], L == U ? 0 : 1, vbase + (int64_t)ru * U, L,
+                                            nwin, sm, bars, lam, arow);
             if (lane < L) {
                 const bool has_prev = ru * U + lane > 0;
                 const float* prev = a.Mu + (g0 + lane - 1) * MP4;
@@ -1027,7 +908,7 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
 }
 
 // ---------------------------------------------------------------- backward kernel
-template <int M, int NST, bool ZS, bool TI, bool GA = false>
+template <int M, int NST, bool ZS, bool TI>
 __global__ void __launch_bounds__(32)
 k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
     grid_dep_wait();
@@ -1100,12 +981,7 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
         // keep the unit's left carry for lane 0's defect check (nus is free now)
         if (lane < M) nus[lane] = mu;
         __syncwarp();
-        const GaOut go{GA ? a.sg[grp] + bl * a.g.T : nullptr,
-                       (GA && a.zig[grp] != nullptr) ? a.zig[grp] + bl * a.zs : nullptr,
-                       GA ? a.gAg[grp] + bl * a.g.T * M : nullptr, ru * U,
-                       reinterpret_cast<float*>(smem + SM::OFF_GST), SM::GST_LANE / 4};
-        unit_adj_pass<M, U, NST, 1, TI, GA>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow,
-                                            go);
+        unit_adj_pass<M, U, NST, 1, TI>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow);
         tt[4] = gtime();
         trace_rec(a.tr, t, 3, t, tt);
         if (a.refine) {
@@ -1142,9 +1018,7 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
                                  (a.inherit != nullptr && a.inherit[b] != 0);
                 if (bad) {
                     const bool done =
-                        refine_sequence_bwd<M, NST, TI, GA>(
-                            a, b, sl, bars, xb, bad, xmax,
-                            reinterpret_cast<float*>(smem + SM::OFF_GST), SM::GST_LANE / 4);
+                        refine_sequence_bwd<M, NST, TI>(a, b, sl, bars, xb, bad, xmax);
                     if (done && lane == 0) atomicAdd(&g_chain_refined, 1ull);
                 }
             }

@@ -278,9 +278,7 @@ cudaError_t bwd_chain_impl(const ChainBwdCall& c, cudaStream_t st, int phase) {
     constexpr bool ZS = TVLP_CHAIN_BWD_ZS != 0;
     using SM = BwdChainSmem<M, NST, ZS>;
     constexpr int MP4 = Tape<M>::MP4;
-    // grad_A fused in when the call carries s / gA (TV, $TVLP_FUSE_GRAD_A=1)
-    const bool ga = !TI && c.grp[0].gA != nullptr;
-    auto k = ga ? k_bwd_chain<M, NST, ZS, TI, !TI> : k_bwd_chain<M, NST, ZS, TI, false>;
+    auto k = k_bwd_chain<M, NST, ZS, TI>;
     cudaError_t err = set_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
     if (c.ng < 1 || c.ng > kMaxGroups) return cudaErrorInvalidValue;
@@ -327,12 +325,7 @@ cudaError_t bwd_chain_impl(const ChainBwdCall& c, cudaStream_t st, int phase) {
                                        group_args(c.g, c.grp[i].B), u);
         if (err != cudaSuccess) return err;
         a.Ag[i] = c.grp[i].A;
-        a.sg[i] = c.grp[i].s;
-        a.zig[i] = c.grp[i].zi;
-        a.gAg[i] = c.grp[i].gA;
-        if (ga && (c.grp[i].s == nullptr || c.grp[i].gA == nullptr)) return cudaErrorInvalidValue;
     }
-    a.zs = M;  // initial states in the padded order's stride
     err = view_tapes(&a.Tw, c.tape, M, MP4, Tape<M>::SIZE, (uint64_t)c.g.B * c.g.nsub, M);
     if (err != cudaSuccess) return err;
     a.Nu = c.Nu;
@@ -366,11 +359,6 @@ UnitGeo chain_units_n(int nsub, int U) {
 
 UnitGeo chain_units(int nsub, bool fwd) {
     return chain_units_n(nsub, fwd ? TVLP_CHAIN_FWD_UNIT : TVLP_CHAIN_BWD_UNIT);
-}
-
-bool chain_fuse_grad_A() {
-    static const int on = env_int("TVLP_FUSE_GRAD_A", 0);
-    return on != 0;
 }
 
 bool chain_supported(int Mp) {

@@ -23,11 +23,9 @@ constexpr int kMaxGroups = 4;
 struct ChainGroup {
     const float* x;    // fwd: e [B,T]; bwd: grad_s [B,T]
     const float* A;    // [B,T,Mp] (TI: [B,Mp])
-    const float* zi;   // nullable: [B][zs] (padded components zero); bwd: s(<0) for grad_A
+    const float* zi;   // fwd, nullable: [B][zs] (padded components zero)
     float* y;          // fwd: s [B,T]; bwd: grad_e [B,T]
     int64_t B;
-    const float* s = nullptr;  // bwd, TV: the forward output [B,T] (grad_A fused in)
-    float* gA = nullptr;       // bwd, TV: grad_A out [B,T,Mp]
 };
 
 struct ChainFwdCall {
@@ -48,7 +46,7 @@ struct ChainFwdCall {
 struct ChainBwdCall {
     bool ti;
     int ng;
-    ChainGroup grp[kMaxGroups];  // TV: s and gA set -- the launch writes grad_A too
+    ChainGroup grp[kMaxGroups];
     const float* tape;
     const int* inherit;  // nullable
     float* Nu;           // zero-state adjoints (written by the launch when the chained
@@ -62,7 +60,6 @@ struct ChainBwdCall {
 
 UnitGeo chain_units(int nsub, bool fwd);
 bool chain_supported(int Mp);
-bool chain_fuse_grad_A();  // $TVLP_FUSE_GRAD_A: grad_A inside the chained adjoint
 size_t chain_ctl_bytes(int64_t B, int nsub, int Mp);
 // phase 0: zero the control words and run the streaming pass the chained
 // kernel consumes (fwd: k_basis4 tapes; bwd: k_adjoint<MODE 0> nu);

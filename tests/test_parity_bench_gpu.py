@@ -272,39 +272,3 @@ def test_lp_ti_shared_row_batched_backward():
               for b in range(3))
     np.testing.assert_allclose(_np(ga), ref, rtol=1e-10, atol=1e-12)
 
-
-_FUSED_SCRIPT = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, sys.argv[1])
-from paper_2406_05128_b200 import data, lpc
-lpc.set_validation("lazy")
-e, A, g = data.d1_batch(11, 3, 4800)
-se, sA, sg = data.stress_item(4, 4800)
-e[2], A[2], g[2] = se, sA, sg                     # one resonant row: refined in kernel
-zi = (0.2 * np.random.default_rng(3).standard_normal((3, 22))).astype(np.float32)
-t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
-s, c = lpc._forward(False, t(e), t(A), t(zi), return_carry=True)
-ge, gA = lpc._backward(False, t(g), t(A), s, t(zi), c)
-np.savez(sys.argv[2], ge=ge.cpu().numpy(), gA=gA.cpu().numpy())
-"""
-
-
-def test_fused_grad_A_matches_separate(tmp_path):
-    """$TVLP_FUSE_GRAD_A=1 (grad_A written by the chained adjoint itself) gives
-    the same grad_e and grad_A bit for bit as the separate k_grad_A, with zi
-    and a sequence the in-kernel refinement re-applies."""
-    import subprocess
-    import sys
-
-    script = tmp_path / "fused.py"
-    script.write_text(_FUSED_SCRIPT)
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    outs = {}
-    for flag in ("0", "1"):
-        env = dict(os.environ, TVLP_FUSE_GRAD_A=flag)
-        dst = tmp_path / f"out{flag}.npz"
-        subprocess.run([sys.executable, str(script), root, str(dst)], check=True, env=env,
-                       timeout=300)
-        outs[flag] = np.load(dst)
-    np.testing.assert_array_equal(outs["0"]["ge"], outs["1"]["ge"])
-    np.testing.assert_array_equal(outs["0"]["gA"], outs["1"]["gA"])
