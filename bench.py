@@ -363,19 +363,12 @@ def run_b200(args, cfg, rank, world, dist):
     B, T, M = cfg["B"], cfg["T"], cfg["M"]
     kind = cfg["kind"]
     strong = args.scaling == "strong" and kind != "tvsplit"
-    if strong:
-        # a fixed global batch of cfg["B"] split over the ranks (config 3 as
-        # BASELINE.json defines it: 64 items over 1/2/4/8 GPUs); --shard-of S
-        # runs rank 0's share of an S-way split on one GPU (a probe of the
-        # per-GPU regime, reported as such)
-        parts = args.shard_of if (world == 1 and args.shard_of > 1) else world
-        lo, hi = pdist.strong_shard(B, rank, parts)
-        B_glob = B if parts == world else hi - lo
-        B = hi - lo
-    else:
-        lo, hi = pdist.shard(B, rank)
-        B_glob = B * world
+    # (strong: a fixed global batch split over the ranks; --shard-of S runs
+    # rank 0's share of an S-way split on one GPU, reported as such)
+    lo, B, B_glob = pdist.bench_shard(B, "strong" if strong else "weak", rank, world,
+                                      args.shard_of)
     allreduce = None
+    grad = None
     if kind in ("tv", "hpn"):
         if kind == "tv":
             e, A, g = data.d1_batch_torch(lo, B, T, M, device=dev)
@@ -400,11 +393,10 @@ def run_b200(args, cfg, rank, world, dist):
             def step(e=e, A=A, g=g):
                 (sh, sc), carry = lpc.lp_forward_tv_grouped([(e[0], A[0]), (e[1], A[1])],
                                                             return_carry=True)
-                work = allreduce() if allreduce is not None else None
-                (geh, gAh), (gec, gAc) = lpc.lp_backward_tv_grouped(
-                    [(g[0], A[0], sh), (g[1], A[1], sc)], carry=carry)
-                if work is not None:
-                    work.wait()
+                # the encoder all-reduce in flight during the LP backward
+                (geh, gAh), (gec, gAc) = pdist.overlapped_allreduce(
+                    grad, dist, lambda: lpc.lp_backward_tv_grouped(
+                        [(g[0], A[0], sh), (g[1], A[1], sc)], carry=carry))
                 return [sh, sc], [geh, gec], [gAh, gAc]
     elif kind == "tvsplit":
         from paper_2406_05128_b200 import longseq

@@ -46,6 +46,32 @@ def strong_shard(B_total, rank, world):
     return lo, hi
 
 
+def bench_shard(B_cfg, scaling, rank, world, shard_of=0):
+    """The bench's batch split (bench.py): returns (lo, B_local, B_global).
+    strong -- a fixed global batch B_cfg over the ranks (BASELINE.json config 3:
+    64 items over 1/2/4/8 GPUs); with world == 1 and shard_of > 1, rank 0's
+    share of a shard_of-way split (a one-GPU probe of the per-GPU regime:
+    B_global is then that share).  weak -- B_cfg items per rank."""
+    if scaling == "strong":
+        parts = shard_of if (world == 1 and shard_of > 1) else world
+        lo, hi = strong_shard(B_cfg, rank, parts)
+        return lo, hi - lo, (B_cfg if parts == world else hi - lo)
+    lo, hi = shard(B_cfg, rank)
+    return lo, B_cfg, B_cfg * world
+
+
+def overlapped_allreduce(grad, dist, work):
+    """The HpN step's encoder-gradient all-reduce issued
+    asynchronously, ``work()`` (the LP backward) run while it is in flight,
+    then joined; returns work()'s result.  dist None: just work()."""
+    if dist is None:
+        return work()
+    handle = dist.all_reduce(grad, async_op=True)
+    out = work()
+    handle.wait()
+    return out
+
+
 def max_over_ranks(value, dist, device=None):
     """The timed value of a multi-rank run is the slowest rank's."""
     if dist is None:

@@ -69,6 +69,56 @@ def test_strong_shard_partition():
             assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
 
 
+def test_bench_shard_plans():
+    """bench.py's split: config 3 strong (global 64 over 1/2/4/8 ranks, disjoint
+    and covering, B_global = 64 on every rank), the one-GPU --shard-of probe
+    (rank 0's share, reported as its own global batch), weak (64 per rank)."""
+    for world in (1, 2, 4, 8):
+        got = [pdist.bench_shard(64, "strong", r, world) for r in range(world)]
+        assert [lo for lo, _, _ in got] == [64 * r // world for r in range(world)]
+        assert sum(n for _, n, _ in got) == 64 and all(g == 64 for _, _, g in got)
+        weak = [pdist.bench_shard(64, "weak", r, world) for r in range(world)]
+        assert [(lo, n, g) for lo, n, g in weak] == [(64 * r, 64, 64 * world)
+                                                      for r in range(world)]
+    for s in (2, 4, 8):
+        assert pdist.bench_shard(64, "strong", 0, 1, shard_of=s) == (0, 64 // s, 64 // s)
+
+
+def _allreduce_worker(rank, world, port, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    d = pdist.init("gloo")
+    grad = torch.full((1 << 20,), float(rank + 1))
+    e, A, g = data.d1_batch(10 + rank, 1, 2000, 22)
+
+    def work():  # the rank's LP backward stands in as the overlapped work
+        s = oracle.lp_forward_tv(e[0].astype(np.float64), A[0].astype(np.float64))
+        return oracle.lp_backward_tv(g[0].astype(np.float64), A[0].astype(np.float64), s)
+
+    ge, gA = pdist.overlapped_allreduce(grad, d, work)
+    s = oracle.lp_forward_tv(e[0].astype(np.float64), A[0].astype(np.float64))
+    ge2, gA2 = oracle.lp_backward_tv(g[0].astype(np.float64), A[0].astype(np.float64), s)
+    np.savez(os.path.join(outdir, f"a{rank}.npz"), grad=grad[:8].numpy(),
+             same=np.array_equal(ge, ge2) and np.array_equal(gA, gA2))
+    d.barrier()
+    d.destroy_process_group()
+
+
+def test_world2_hpn_allreduce_overlap(tmp_path):
+    """The HpN step's encoder all-reduce (bench hpn config) runs asynchronously
+    around the rank's backward: the reduced gradient is the sum over ranks and
+    the overlapped work's result is unchanged."""
+    world = 2
+    port = _free_port()
+    mp.start_processes(_allreduce_worker, args=(world, port, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    for r in range(world):
+        z = np.load(tmp_path / f"a{r}.npz")
+        assert np.all(z["grad"] == 3.0)  # 1 + 2
+        assert bool(z["same"])
+    assert pdist.overlapped_allreduce(None, None, lambda: 7) == 7
+
+
 # ---------------------------------------------------------------- one sequence split in time
 class _NumpySegments:
     """Segment primitives of longseq.py restated in numpy on the oracle (CPU),
