@@ -435,8 +435,8 @@ def run_b200(args, cfg, rank, world, dist):
         plan = params.FramePlan.raised_cosine(cfg["hop"])
 
         def step(e=e, A=A, g=g):
-            y, seg = params.framewise_forward(e, A, plan)
-            ge, gf = params.framewise_backward(g, A, seg, plan)
+            y, seg, aux = params.framewise_forward(e, A, plan, return_aux=True)
+            ge, gf = params.framewise_backward(g, A, seg, plan, aux=aux)
             return y, ge, gf
 
     def barrier():

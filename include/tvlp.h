@@ -216,6 +216,23 @@ int tvlp_framewise_backward(int32_t dtype, const void* grad_out, const void* fra
                             void* grad_frames, int64_t B, int64_t T, int64_t F, int32_t M,
                             int32_t frame_size, int32_t hop, void* workspace,
                             size_t workspace_bytes, void* stream);
+/* The same pair with an auxiliary buffer the forward fills and the backward
+ * reads: [B, n_frames, 2 * padded M] values of the I/O dtype, each frame's
+ * impulse-response tail (the frames-in-pieces kernels' carry needs it in both
+ * directions; the backward then skips recomputing it).
+ * tvlp_framewise_aux_elems() gives its size, 0 for plans that do not use it
+ * (aux is then ignored).  aux NULL == the plain entry points. */
+int64_t tvlp_framewise_aux_elems(int64_t B, int64_t T, int64_t F, int32_t M, int32_t frame_size,
+                                 int32_t hop);
+int tvlp_framewise_forward_ex(int32_t dtype, const void* e, const void* frames,
+                              const void* window, double cola, void* out, void* seg, void* aux,
+                              int64_t B, int64_t T, int64_t F, int32_t M, int32_t frame_size,
+                              int32_t hop, void* workspace, size_t workspace_bytes, void* stream);
+int tvlp_framewise_backward_ex(int32_t dtype, const void* grad_out, const void* frames,
+                               const void* window, double cola, const void* seg, const void* aux,
+                               void* grad_e, void* grad_frames, int64_t B, int64_t T, int64_t F,
+                               int32_t M, int32_t frame_size, int32_t hop, void* workspace,
+                               size_t workspace_bytes, void* stream);
 
 /* Instrumentation (bench.py): number of kernels this library has launched,
  * and optional CUDA-event timing of every launch (off by default; when on,

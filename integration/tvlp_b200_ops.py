@@ -89,13 +89,13 @@ def make_ops(device=None):
         # (params.py:157-217); the B200 plan restates the same grid
         bplan = params.FramePlan(frame_size=plan.frame_size, hop=plan.hop,
                                  window=np.asarray(plan.window))
-        out, seg = params.framewise_forward(et, ft, bplan)
-        ctx[_STASH] = (ft, seg, bplan)
+        out, seg, aux = params.framewise_forward(et, ft, bplan, return_aux=True)
+        ctx[_STASH] = (ft, seg, bplan, aux)
         return out.cpu().numpy()
 
     def vjp_framewise(grad, values, out, ctx):
-        ft, seg, bplan = ctx[_STASH]
-        ge, gf = params.framewise_backward(_dev(grad, dev, ft.dtype), ft, seg, bplan)
+        ft, seg, bplan, aux = ctx[_STASH]
+        ge, gf = params.framewise_backward(_dev(grad, dev, ft.dtype), ft, seg, bplan, aux=aux)
         return ge.cpu().numpy(), gf.cpu().numpy()
 
     def fw_lp_tv_frames(values, ctx, dtype):

@@ -82,6 +82,11 @@ _SIGS = [
      [_I32, _P, _P, _P, _D, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _P, _SZ, _P]),
     ("tvlp_framewise_backward", ctypes.c_int,
      [_I32, _P, _P, _P, _D, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _P, _SZ, _P]),
+    ("tvlp_framewise_aux_elems", _I64, [_I64, _I64, _I64, _I32, _I32, _I32]),
+    ("tvlp_framewise_forward_ex", ctypes.c_int,
+     [_I32, _P, _P, _P, _D, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _P, _SZ, _P]),
+    ("tvlp_framewise_backward_ex", ctypes.c_int,
+     [_I32, _P, _P, _P, _D, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _P, _SZ, _P]),
     ("tvlp_launch_count", _I64, []),
     ("tvlp_refined_sequences", _I64, []),
     ("tvlp_profile_enable", None, [_I32]),

@@ -128,15 +128,18 @@ class LPFramewise(torch.autograd.Function):
     @staticmethod
     def forward(ctx, e, frames, plan):
         frames = frames.to(e.dtype)
-        out, seg = _params.framewise_forward(e.detach(), frames.detach(), plan)
+        out, seg, aux = _params.framewise_forward(e.detach(), frames.detach(), plan,
+                                                  return_aux=True)
         ctx.save_for_backward(frames, seg)
+        ctx.aux = aux  # the frames' impulse-response tails (or None)
         ctx.plan = plan
         return out
 
     @staticmethod
     def backward(ctx, grad_out):
         frames, seg = ctx.saved_tensors
-        ge, gf = _params.framewise_backward(grad_out.contiguous(), frames, seg, ctx.plan)
+        ge, gf = _params.framewise_backward(grad_out.contiguous(), frames, seg, ctx.plan,
+                                            aux=ctx.aux)
         return ge, gf, None
 
 

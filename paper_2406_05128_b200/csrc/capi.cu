@@ -801,7 +801,7 @@ bool fw_args(int64_t B, int64_t T, int64_t F, int M, int size, int hop, double c
 template <typename IO>
 int fw_forward_impl(const void* e, const void* frames, const void* win, void* out, void* seg,
                     const FwArgs& a, int M, void* ws, size_t ws_bytes, cudaStream_t st,
-                    size_t* need) {
+                    size_t* need, void* aux = nullptr) {
     const int Mp = padded_order(M);
     Carver c(ws);
     void* fp = (Mp != M) ? c.take(a.B * (int64_t)a.F * Mp * sizeof(IO)) : nullptr;
@@ -817,14 +817,15 @@ int fw_forward_impl(const void* e, const void* frames, const void* win, void* ou
     }
     TVLP_RUN("fw_forward", 2, st,
              (launch_fw_forward<IO>(Mp, static_cast<const IO*>(e), fr, static_cast<const IO*>(win),
-                                    static_cast<IO*>(seg), static_cast<IO*>(out), a, st)));
+                                    static_cast<IO*>(seg), static_cast<IO*>(out), a, st,
+                                    static_cast<IO*>(aux))));
     return TVLP_OK;
 }
 
 template <typename IO>
 int fw_backward_impl(const void* gout, const void* frames, const void* win, const void* seg,
                      void* ge, void* gf, const FwArgs& a, int M, void* ws, size_t ws_bytes,
-                     cudaStream_t st, size_t* need) {
+                     cudaStream_t st, size_t* need, const void* aux = nullptr) {
     const int Mp = padded_order(M);
     Carver c(ws);
     void* fp = (Mp != M) ? c.take(a.B * (int64_t)a.F * Mp * sizeof(IO)) : nullptr;
@@ -845,7 +846,8 @@ int fw_backward_impl(const void* gout, const void* frames, const void* win, cons
     TVLP_RUN("fw_backward", 3, st,
              (launch_fw_backward<IO>(Mp, M, static_cast<const IO*>(gout), fr,
                                      static_cast<const IO*>(win), static_cast<const IO*>(seg), gew,
-                                     gap, static_cast<IO*>(ge), gf_out, a, st)));
+                                     gap, static_cast<IO*>(ge), gf_out, a, st,
+                                     static_cast<const IO*>(aux))));
     if (gfp) TVLP_CK(unpack<IO>(gfp, gf, a.B, a.F, M, a.F, Mp, st));
     return TVLP_OK;
 }
@@ -1520,21 +1522,50 @@ int tvlp_lagged_signal_matrix(int32_t dtype, const void* s, const void* zi, void
     return TVLP_OK;
 }
 
-int tvlp_framewise_forward(int32_t dtype, const void* e, const void* frames, const void* window,
-                           double cola, void* out, void* seg, int64_t B, int64_t T, int64_t F,
-                           int32_t M, int32_t frame_size, int32_t hop, void* workspace,
-                           size_t workspace_bytes, void* stream) {
+int tvlp_framewise_forward_ex(int32_t dtype, const void* e, const void* frames,
+                              const void* window, double cola, void* out, void* seg, void* aux,
+                              int64_t B, int64_t T, int64_t F, int32_t M, int32_t frame_size,
+                              int32_t hop, void* workspace, size_t workspace_bytes,
+                              void* stream) {
     int rc = check_common(dtype, M);
     if (rc != TVLP_OK) return rc;
     if (!e || !frames || !window || !out || !seg) return TVLP_ERR_ARG;
     FwArgs a;
     if (!fw_args(B, T, F, M, frame_size, hop, cola, a)) return TVLP_ERR_ARG;
+    if (fw_aux_elems(a, padded_order(M)) == 0) aux = nullptr;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (dtype == TVLP_F64)
         return fw_forward_impl<double>(e, frames, window, out, seg, a, M, workspace,
-                                       workspace_bytes, st, nullptr);
+                                       workspace_bytes, st, nullptr, aux);
     return fw_forward_impl<float>(e, frames, window, out, seg, a, M, workspace, workspace_bytes,
-                                  st, nullptr);
+                                  st, nullptr, aux);
+}
+
+int tvlp_framewise_forward(int32_t dtype, const void* e, const void* frames, const void* window,
+                           double cola, void* out, void* seg, int64_t B, int64_t T, int64_t F,
+                           int32_t M, int32_t frame_size, int32_t hop, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+    return tvlp_framewise_forward_ex(dtype, e, frames, window, cola, out, seg, nullptr, B, T, F,
+                                     M, frame_size, hop, workspace, workspace_bytes, stream);
+}
+
+int tvlp_framewise_backward_ex(int32_t dtype, const void* grad_out, const void* frames,
+                               const void* window, double cola, const void* seg,
+                               const void* aux, void* grad_e, void* grad_frames, int64_t B,
+                               int64_t T, int64_t F, int32_t M, int32_t frame_size, int32_t hop,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+    int rc = check_common(dtype, M);
+    if (rc != TVLP_OK) return rc;
+    if (!grad_out || !frames || !window || !seg || !grad_e || !grad_frames) return TVLP_ERR_ARG;
+    FwArgs a;
+    if (!fw_args(B, T, F, M, frame_size, hop, cola, a)) return TVLP_ERR_ARG;
+    if (fw_aux_elems(a, padded_order(M)) == 0) aux = nullptr;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == TVLP_F64)
+        return fw_backward_impl<double>(grad_out, frames, window, seg, grad_e, grad_frames, a, M,
+                                        workspace, workspace_bytes, st, nullptr, aux);
+    return fw_backward_impl<float>(grad_out, frames, window, seg, grad_e, grad_frames, a, M,
+                                   workspace, workspace_bytes, st, nullptr, aux);
 }
 
 int tvlp_framewise_backward(int32_t dtype, const void* grad_out, const void* frames,
@@ -1542,17 +1573,16 @@ int tvlp_framewise_backward(int32_t dtype, const void* grad_out, const void* fra
                             void* grad_frames, int64_t B, int64_t T, int64_t F, int32_t M,
                             int32_t frame_size, int32_t hop, void* workspace,
                             size_t workspace_bytes, void* stream) {
-    int rc = check_common(dtype, M);
-    if (rc != TVLP_OK) return rc;
-    if (!grad_out || !frames || !window || !seg || !grad_e || !grad_frames) return TVLP_ERR_ARG;
+    return tvlp_framewise_backward_ex(dtype, grad_out, frames, window, cola, seg, nullptr, grad_e,
+                                      grad_frames, B, T, F, M, frame_size, hop, workspace,
+                                      workspace_bytes, stream);
+}
+
+int64_t tvlp_framewise_aux_elems(int64_t B, int64_t T, int64_t F, int32_t M, int32_t frame_size,
+                                 int32_t hop) {
     FwArgs a;
-    if (!fw_args(B, T, F, M, frame_size, hop, cola, a)) return TVLP_ERR_ARG;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (dtype == TVLP_F64)
-        return fw_backward_impl<double>(grad_out, frames, window, seg, grad_e, grad_frames, a, M,
-                                        workspace, workspace_bytes, st, nullptr);
-    return fw_backward_impl<float>(grad_out, frames, window, seg, grad_e, grad_frames, a, M,
-                                   workspace, workspace_bytes, st, nullptr);
+    if (M < 1 || M > kMaxOrder || !fw_args(B, T, F, M, frame_size, hop, 1.0, a)) return 0;
+    return fw_aux_elems(a, padded_order(M));
 }
 
 }  // extern "C"

@@ -506,6 +506,12 @@ bool fw_gather4(const FwArgs& a, const void* rows, const void* out) {
 }
 }  // namespace
 
+// impulse-response tails the piece kernels exchange between forward and
+// backward: [B][nfr][2 Mp] (0: the plan does not use the piece kernels)
+int64_t fw_aux_elems(const FwArgs& a, int Mp) {
+    return fw_pieces(a) ? a.B * (int64_t)a.nfr * 2 * Mp : 0;
+}
+
 #define TVLP_FW_DISPATCH(Mp, ...)                          \
     switch (Mp) {                                          \
         case 2: { constexpr int M_ = 2; __VA_ARGS__ }      \
@@ -581,7 +587,7 @@ bool fw_supported(int Mp, int size, int hop, int elem) {
 
 template <typename IO>
 cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* win, IO* seg,
-                              IO* out, const FwArgs& a, cudaStream_t st) {
+                              IO* out, const FwArgs& a, cudaStream_t st, IO* aux) {
     if (!fw_supported(Mp, a.size, a.hop, (int)sizeof(IO))) return cudaErrorInvalidValue;
     const dim3 grid((unsigned)((a.nfr + 31) / 32), (unsigned)a.B);
     cudaError_t err = cudaSuccess;
@@ -593,7 +599,7 @@ cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* w
             if (err != cudaSuccess) return err;
             launch_pdl(k, dim3((unsigned)((a.nfr + kFwpFrames - 1) / kFwpFrames), (unsigned)a.B),
                        kFwpThreads, sm, st, seg, e, frames, win, a.T, a.F, a.nfr, a.size, a.hop,
-                       a.n_lead);
+                       a.n_lead, aux);
             break;
         })
     } else {
@@ -628,19 +634,19 @@ cudaError_t launch_fw_forward(int Mp, const IO* e, const IO* frames, const IO* w
 template <typename IO>
 cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, const IO* win,
                                const IO* seg, IO* gew, IO* gapart, IO* ge, IO* gf,
-                               const FwArgs& a, cudaStream_t st) {
+                               const FwArgs& a, cudaStream_t st, const IO* aux) {
     if (!fw_supported(Mp, a.size, a.hop, (int)sizeof(IO))) return cudaErrorInvalidValue;
     const dim3 grid((unsigned)((a.nfr + 31) / 32), (unsigned)a.B);
     cudaError_t err = cudaSuccess;
     if (fw_pieces(a)) {
         const size_t sm = FwpSmem<IO>::bytes(a.size, a.hop);
         TVLP_FW_DISPATCH(Mp, {
-            auto k = k_fwp_backward<IO, M_>;
+            auto k = aux != nullptr ? k_fwp_backward<IO, M_, true> : k_fwp_backward<IO, M_, false>;
             err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             if (err != cudaSuccess) return err;
             launch_pdl(k, dim3((unsigned)((a.nfr + kFwpFrames - 1) / kFwpFrames), (unsigned)a.B),
                        kFwpThreads, sm, st, gew, gapart, seg, gout, frames, win, a.T, a.F, a.nfr,
-                       a.size, a.hop, a.n_lead, (IO)a.cola);
+                       a.size, a.hop, a.n_lead, (IO)a.cola, aux);
             break;
         })
     } else {
@@ -679,14 +685,16 @@ cudaError_t launch_fw_backward(int Mp, int M, const IO* gout, const IO* frames, 
 }
 
 template cudaError_t launch_fw_forward<float>(int, const float*, const float*, const float*,
-                                              float*, float*, const FwArgs&, cudaStream_t);
+                                              float*, float*, const FwArgs&, cudaStream_t, float*);
 template cudaError_t launch_fw_forward<double>(int, const double*, const double*, const double*,
-                                               double*, double*, const FwArgs&, cudaStream_t);
+                                               double*, double*, const FwArgs&, cudaStream_t,
+                                               double*);
 template cudaError_t launch_fw_backward<float>(int, int, const float*, const float*, const float*,
                                                const float*, float*, float*, float*, float*,
-                                               const FwArgs&, cudaStream_t);
+                                               const FwArgs&, cudaStream_t, const float*);
 template cudaError_t launch_fw_backward<double>(int, int, const double*, const double*,
                                                 const double*, const double*, double*, double*,
-                                                double*, double*, const FwArgs&, cudaStream_t);
+                                                double*, double*, const FwArgs&, cudaStream_t,
+                                                const double*);
 
 }  // namespace tvlp

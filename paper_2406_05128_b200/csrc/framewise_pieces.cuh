@@ -133,7 +133,7 @@ __device__ __forceinline__ void fwp_stage(IO* __restrict__ es, const IO* __restr
 // x(n) = in(n) (in(kw, xv) fills window kw, in processing order) and of the
 // impulse response, then M more impulse-response steps.  Returns the exit
 // state z[i] = y(L-1-i) and ht[t] = h(L-M+t), t = 0..2M-1.
-template <typename IO, int M, typename In>
+template <typename IO, int M, typename In, bool WITH_H = true>
 __device__ __forceinline__ void fwp_pass1(const IO (&a)[M], int L, In in, IO (&z)[M],
                                           IO (&ht)[2 * M]) {
     constexpr int W = kFwW;
@@ -171,8 +171,11 @@ __device__ __forceinline__ void fwp_pass1(const IO (&a)[M], int L, In in, IO (&z
                     }
                     R[pos % MR] =
                         fma(-a[0], R[(pos - 1 + MR) % MR], xv[u] - ((p0 + p1) + (p2 + p3)));
-                    const IO d = (kb == 0 && pos == 0) ? (IO)1 : (IO)0;
-                    H[pos % MR] = fma(-a[0], H[(pos - 1 + MR) % MR], d - ((h0 + h1) + (h2 + h3)));
+                    if constexpr (WITH_H) {
+                        const IO d = (kb == 0 && pos == 0) ? (IO)1 : (IO)0;
+                        H[pos % MR] =
+                            fma(-a[0], H[(pos - 1 + MR) % MR], d - ((h0 + h1) + (h2 + h3)));
+                    }
                 }
             }
         }
@@ -188,9 +191,10 @@ __device__ __forceinline__ void fwp_pass1(const IO (&a)[M], int L, In in, IO (&z
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             z[i] = Rl[(L - 1 - i) % MR];
-            ht[i] = Hl[(L - M + i) % MR];
+            if (WITH_H) ht[i] = Hl[(L - M + i) % MR];
         }
     }
+    if constexpr (!WITH_H) return;
     // h(L .. L+M-1): zero input
 #pragma unroll
     for (int n = 0; n < M; ++n) {
@@ -256,7 +260,7 @@ template <typename IO, int M>
 __global__ void __launch_bounds__(kFwpThreads)
 k_fwp_forward(IO* __restrict__ seg, const IO* __restrict__ e, const IO* __restrict__ frames,
               const IO* __restrict__ win, int64_t T, int F, int nfr, int size, int hop,
-              int n_lead) {
+              int n_lead, IO* __restrict__ aux) {
     grid_dep_wait();
     using S = FwpSmem<IO>;
     constexpr int W = kFwW;
@@ -296,6 +300,12 @@ k_fwp_forward(IO* __restrict__ seg, const IO* __restrict__ e, const IO* __restri
     };
     IO z[M], ht[2 * M], xe[M];
     fwp_pass1<IO, M>(a, L, in, z, ht);
+    // the frame's impulse-response tail, for the backward (same row, same L)
+    if (aux != nullptr && active && p == 0) {
+        IO* dst = aux + (b * nfr + fi) * (int64_t)(2 * M);
+#pragma unroll
+        for (int i = 0; i < 2 * M; ++i) dst[i] = ht[i];
+    }
     fwp_carry<IO, M, false>(a, ht, z, p, xe);
     // pass 2: from the carried-in state, outputs to the frame's row
     IO R[MR];
@@ -337,12 +347,12 @@ k_fwp_forward(IO* __restrict__ seg, const IO* __restrict__ e, const IO* __restri
     }
 }
 
-template <typename IO, int M>
+template <typename IO, int M, bool HT = false>
 __global__ void __launch_bounds__(kFwpThreads)
 k_fwp_backward(IO* __restrict__ gew, IO* __restrict__ gapart, const IO* __restrict__ seg,
                const IO* __restrict__ gout, const IO* __restrict__ frames,
                const IO* __restrict__ win, int64_t T, int F, int nfr, int size, int hop,
-               int n_lead, IO cola) {
+               int n_lead, IO cola, const IO* __restrict__ aux) {
     grid_dep_wait();
     using S = FwpSmem<IO>;
     constexpr int W = kFwW;
@@ -382,7 +392,15 @@ k_fwp_backward(IO* __restrict__ gew, IO* __restrict__ gapart, const IO* __restri
         }
     };
     IO z[M], ht[2 * M], xe[M];
-    fwp_pass1<IO, M>(a, L, in, z, ht);
+    if constexpr (HT) {
+        // the forward saved this frame's impulse-response tail: one chain here
+#pragma unroll
+        for (int i = 0; i < 2 * M; ++i)
+            ht[i] = active ? aux[(b * nfr + fi) * (int64_t)(2 * M) + i] : (IO)0;
+        fwp_pass1<IO, M, decltype(in), false>(a, L, in, z, ht);
+    } else {
+        fwp_pass1<IO, M>(a, L, in, z, ht);
+    }
     fwp_carry<IO, M, true>(a, ht, z, p, xe);
     // pass 2 (push form): lam[i] = -sum_{j > i} a_j ge(k + j - i) entering
     // step k, from the entry state xe[i] = ge(kend + i)

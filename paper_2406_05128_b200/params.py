@@ -207,9 +207,11 @@ def _check(e, frames, plan):
     plan._validate_cola_cached()
 
 
-def framewise_forward(e, frames, plan):
+def framewise_forward(e, frames, plan, return_aux=False):
     """Returns ``(out, seg)``; ``seg`` [B, n_frames, frame_size] holds the
-    per-frame outputs the VJP needs (the reference's ``seg_outputs``)."""
+    per-frame outputs the VJP needs (the reference's ``seg_outputs``).
+    ``return_aux``: also the frames' impulse-response tails (or None) that
+    framewise_backward(..., aux=) can reuse instead of recomputing."""
     conv = _Conv(e, frames)
     e = conv.t(e)
     if e.dtype not in (torch.float32, torch.float64):
@@ -224,21 +226,26 @@ def framewise_forward(e, frames, plan):
     nfr = lib.tvlp_framewise_nframes(T, F, plan.frame_size, plan.hop)
     out = torch.empty_like(e)
     seg = torch.empty((B, nfr, plan.frame_size), dtype=e.dtype, device=conv.device)
+    na = lib.tvlp_framewise_aux_elems(B, T, F, M, plan.frame_size, plan.hop) if return_aux else 0
+    aux = torch.empty(na, dtype=e.dtype, device=conv.device) if na > 0 else None
     w = plan._window_tensor(e.dtype, conv.device)
     dt = N.dtype_code(e.dtype)
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FW_FWD, dt, B, T, M, F, plan.frame_size,
                                                    plan.hop), conv.device)
     with torch.cuda.device(conv.device):
-        N.check(lib.tvlp_framewise_forward(dt, N.ptr(e), N.ptr(frames), N.ptr(w),
-                                           plan._cola_cached(), N.ptr(out), N.ptr(seg), B, T, F,
-                                           M, plan.frame_size, plan.hop, N.ptr(ws), nws,
-                                           N.stream_ptr(conv.device)))
+        N.check(lib.tvlp_framewise_forward_ex(dt, N.ptr(e), N.ptr(frames), N.ptr(w),
+                                              plan._cola_cached(), N.ptr(out), N.ptr(seg),
+                                              N.ptr(aux), B, T, F, M, plan.frame_size, plan.hop,
+                                              N.ptr(ws), nws, N.stream_ptr(conv.device)))
+    if return_aux:
+        return conv.out(out), seg, aux
     return conv.out(out), seg
 
 
-def framewise_backward(grad_out, frames, seg, plan):
+def framewise_backward(grad_out, frames, seg, plan, aux=None):
     """VJP of :func:`framewise_forward` (params.py:259-273):
-    returns ``(grad_e, grad_frames)``."""
+    returns ``(grad_e, grad_frames)``; ``aux`` from the same forward
+    (return_aux=True) saves recomputing the frames' impulse responses."""
     conv = _Conv(grad_out, frames, seg)
     g = conv.t(grad_out)
     if g.dtype not in (torch.float32, torch.float64):
@@ -250,6 +257,9 @@ def framewise_backward(grad_out, frames, seg, plan):
     T = g.shape[-1]
     F, M = frames.shape[-2], frames.shape[-1]
     lib = N.load()
+    if aux is not None and (aux.dtype != g.dtype or aux.numel() != lib.tvlp_framewise_aux_elems(
+            B, T, F, M, plan.frame_size, plan.hop)):
+        aux = None  # not this plan's
     ge = torch.empty_like(g)
     gf = torch.empty(frames.shape, dtype=g.dtype, device=conv.device)
     w = plan._window_tensor(g.dtype, conv.device)
@@ -257,10 +267,11 @@ def framewise_backward(grad_out, frames, seg, plan):
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FW_BWD, dt, B, T, M, F, plan.frame_size,
                                                    plan.hop), conv.device)
     with torch.cuda.device(conv.device):
-        N.check(lib.tvlp_framewise_backward(dt, N.ptr(g), N.ptr(frames), N.ptr(w),
-                                            plan._cola_cached(), N.ptr(seg), N.ptr(ge),
-                                            N.ptr(gf), B, T, F, M, plan.frame_size, plan.hop,
-                                            N.ptr(ws), nws, N.stream_ptr(conv.device)))
+        N.check(lib.tvlp_framewise_backward_ex(dt, N.ptr(g), N.ptr(frames), N.ptr(w),
+                                               plan._cola_cached(), N.ptr(seg), N.ptr(aux),
+                                               N.ptr(ge), N.ptr(gf), B, T, F, M, plan.frame_size,
+                                               plan.hop, N.ptr(ws), nws,
+                                               N.stream_ptr(conv.device)))
     return conv.out(ge), conv.out(gf)
 
 

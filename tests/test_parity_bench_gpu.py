@@ -194,8 +194,12 @@ def test_framewise_exact_all_items():
     ev, fr, gv = data.d1_frames_batch(0, B, T, 22, hop)
     plan = params.FramePlan.raised_cosine(hop)
     e, f, g = (torch.from_numpy(x).cuda() for x in (ev, fr, gv))
-    y, seg = params.framewise_forward(e, f, plan)
-    ge, gf = params.framewise_backward(g, f, seg, plan)
+    # the bench's step: the forward's impulse-response tails reused (aux)
+    y, seg, aux = params.framewise_forward(e, f, plan, return_aux=True)
+    assert aux is not None
+    ge, gf = params.framewise_backward(g, f, seg, plan, aux=aux)
+    ge0, gf0 = params.framewise_backward(g, f, seg, plan)  # tails recomputed: same bits
+    assert torch.equal(ge, ge0) and torch.equal(gf, gf0)
     y, ge, gf = _np(y), _np(ge), _np(gf)
 
     def one(b):

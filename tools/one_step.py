@@ -49,8 +49,8 @@ def make_step(cfg, shard_of=0):
         plan = params.FramePlan.raised_cosine(cfg["hop"])
 
         def step():
-            y, seg = params.framewise_forward(e, f, plan)
-            params.framewise_backward(g, f, seg, plan)
+            y, seg, aux = params.framewise_forward(e, f, plan, return_aux=True)
+            params.framewise_backward(g, f, seg, plan, aux=aux)
     return step
 
 
