@@ -242,6 +242,7 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
             const int k = kb + w;
             if (k < nwin) {
                 const int st = k % NST;
+                TVLP_ASSERT(k < nwin && ln < U && L <= U);
                 mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
                 const unsigned char* base = sm + st * S::STAGE;
                 const float* Ar = reinterpret_cast<const float*>(base) + ln * S::AROW;
@@ -332,6 +333,7 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
     for (int k = 0; k < NST; ++k) issue(k);
     for (int k = 0; k < nwin; ++k) {
         const int st = k % NST;
+        TVLP_ASSERT(k < nwin && ln < U && L <= U);
         mbar_wait(&bars[st], (uint32_t)((k / NST) & 1));
         const unsigned char* base = sm + st * S::STAGE;
         const float* Ar = reinterpret_cast<const float*>(base) + ln * S::AROW;
@@ -816,6 +818,8 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
         const int grp = a.gi.of(b);
         const int64_t bl = b - a.gi.gB0[grp];              // sequence within its group
         const int64_t r0 = bl * nsub + (int64_t)ru * U;    // row of the group's lane views
+        TVLP_ASSERT(ru < nu && b < B && L >= 1 && L <= U && g0 + L <= B * nsub);
+        TVLP_ASSERT(grp < a.gi.ng && bl >= 0 && bl < a.gi.gB0[grp + 1] - a.gi.gB0[grp]);
         unsigned long long tt[5] = {gtime(), 0, 0, 0, 0};
         // 1. tapes of the unit complete? (NWB == 0: a previous launch wrote them)
         if constexpr (NWB > 0) wait_count(&a.cnt[b * nu + ru], (unsigned)L);
@@ -837,6 +841,7 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
             if (a.zig[grp] != nullptr && lane < M) x = a.zig[grp][bl * a.zs + lane];
             __syncwarp();
         } else {
+            TVLP_ASSERT(b * nu + ru - 1 < B * nu);
             x = wait_state<M>(a.pub + (b * nu + ru - 1) * MP4);
         }
         if (ru == 0 && lane == 0) a.fflags[b] = 0;
@@ -939,6 +944,8 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
         const int grp = a.gi.of(b);
         const int64_t bl = b - a.gi.gB0[grp];
         const int64_t r0 = bl * nsub + (int64_t)ru * U;
+        TVLP_ASSERT(ru >= 0 && ru < nu && b < B && L >= 1 && L <= U && g0 + L <= B * nsub);
+        TVLP_ASSERT(grp < a.gi.ng && bl >= 0 && bl < a.gi.gB0[grp + 1] - a.gi.gB0[grp]);
         const float* arow = TI ? a.Ag[grp] + bl * M : nullptr;
         // W rows of the unit's tapes (read by the carry), staged during the
         // zero-state pass

@@ -9,6 +9,30 @@
 #include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cstdio>
+
+// Checked build (-D TVLP_CHECKED=1, `python -m paper_2406_05128_b200.build
+// --define TVLP_CHECKED=1 --out variants/checked/libtvlp_b200.so`): device-side
+// bounds and protocol assertions on the index arithmetic of the hand-written
+// kernels (staged spans, stage slots, unit/sub-chunk/row ranges, output
+// offsets).  A failed assertion prints its site and traps the kernel.  The
+// stand-in for compute-sanitizer on GPU pools where it is unavailable
+// (tools/checked_tests.sh runs the GPU suite against this build).
+#ifndef TVLP_CHECKED
+#define TVLP_CHECKED 0
+#endif
+#if TVLP_CHECKED
+#define TVLP_ASSERT(c)                                                                        \
+    do {                                                                                      \
+        if (!(c)) {                                                                           \
+            printf("TVLP_ASSERT %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c,   \
+                   (int)blockIdx.x, (int)threadIdx.x);                                        \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define TVLP_ASSERT(c) ((void)0)
+#endif
 
 namespace tvlp {
 

@@ -289,13 +289,16 @@ k_fwp_forward(IO* __restrict__ seg, const IO* __restrict__ e, const IO* __restri
     (void)warp;
     // input of window kw of this piece: window * e over the staged span
     const IO* wsp = ws + p * lp;
+    const int nspan = fwp_blocks(size, hop) * hst;  // staged elements
     auto in = [&](int kw, IO (&xv)[W]) {
         const int o0 = fc * hop + p * L + kw;  // span offset of the window's first sample
         const int q0 = o0 / hop, r0 = o0 - q0 * hop;
 #pragma unroll
         for (int u = 0; u < W; ++u) {
             const int r = r0 + u;
-            xv[u] = es[q0 * hst + r + (r >= hop ? hst - hop : 0)] * wsp[kw + u];
+            const int ix = q0 * hst + r + (r >= hop ? hst - hop : 0);
+            TVLP_ASSERT(ix >= 0 && ix < nspan && kw + u < L);
+            xv[u] = es[ix] * wsp[kw + u];
         }
     };
     IO z[M], ht[2 * M], xe[M];
@@ -341,6 +344,7 @@ k_fwp_forward(IO* __restrict__ seg, const IO* __restrict__ e, const IO* __restri
                     R[pos % MR] = v;
                     ov[u] = v;
                 }
+                TVLP_ASSERT(!active || p * L + k * W + W <= size);
                 if (active) fw_store_window<IO, W>(out + k * W, ov, W);
             }
         }
@@ -382,13 +386,16 @@ k_fwp_backward(IO* __restrict__ gew, IO* __restrict__ gapart, const IO* __restri
     (void)warp;
     const int kend = (p + 1) * L;  // the piece covers k in [kend - L, kend), walked downward
     // pass 1 input, reversed time m: g(kend - 1 - m)
+    const int nspan = fwp_blocks(size, hop) * hst;  // staged elements
     auto in = [&](int mw, IO (&xv)[W]) {
         const int o0 = fc * hop + kend - 1 - mw;  // span offset of the window's first (top) sample
         const int q0 = o0 / hop, r0 = o0 - q0 * hop;
 #pragma unroll
         for (int u = 0; u < W; ++u) {
             const int r = r0 - u;
-            xv[u] = gs[q0 * hst + r - (r < 0 ? hst - hop : 0)];
+            const int ix = q0 * hst + r - (r < 0 ? hst - hop : 0);
+            TVLP_ASSERT(ix >= 0 && ix < nspan);
+            xv[u] = gs[ix];
         }
     };
     IO z[M], ht[2 * M], xe[M];
@@ -418,6 +425,7 @@ k_fwp_backward(IO* __restrict__ gew, IO* __restrict__ gapart, const IO* __restri
     const IO* wsp = ws + p * lp;
     // saved outputs s(k) for 0 <= k < size (zero below: frames start at rest)
     auto sload = [&](int k0, IO (&v)[W]) {
+        TVLP_ASSERT(k0 + W <= size);
         if (k0 >= 0 && active) {
             constexpr int V = 16 / (int)sizeof(IO);
 #pragma unroll
@@ -483,6 +491,7 @@ k_fwp_backward(IO* __restrict__ gew, IO* __restrict__ gapart, const IO* __restri
             for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
             lam[M - 1] = -a[M - 1] * l0;
         }
+        TVLP_ASSERT(kw >= 0 && kw + W <= size && kw - p * L >= 0 && kw - p * L + W <= L);
         if (active) fw_store_window<IO, W>(grow + kw, ov, W);
 #pragma unroll
         for (int i = SR - 1; i >= W; --i) sv[i] = sv[i - W];

@@ -1304,6 +1304,7 @@ k_apply_fwd(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_pt
                     ov[u] = v;
                     finite &= is_finite_val(v);
                 }
+                TVLP_ASSERT(!active || (gid < nsc && k * W + W <= g.Ls));
                 if (active)
                     store_window<IO, W>(static_cast<IO*>(maps.o) + gid * (int64_t)g.Ls + k * W, ov);
                 __syncwarp();  // every lane is done with the stage: refill it
@@ -1445,6 +1446,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
             for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
             lam[M - 1] = -a[M - 1] * l0;
         }
+        TVLP_ASSERT(!(MODE == 1 && active) || (gid < nsc && (nwin - k) * W <= g.Ls));
         if (MODE == 1 && active)
             store_window<IO, W>(static_cast<IO*>(maps.o) + gid * (int64_t)g.Ls + (nwin - 1 - k) * W,
                                 ov);
