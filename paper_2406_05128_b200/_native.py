@@ -6,7 +6,9 @@ missing, every call raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import functools
 import os
 
 import torch
@@ -116,8 +118,24 @@ def load(path=None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        # size queries are pure functions of their arguments (the plan is
+        # deterministic): memoised, so a training step's calls skip the
+        # ctypes round trips
+        for name in _PURE:
+            setattr(lib, name, functools.lru_cache(maxsize=256)(getattr(lib, name)))
         _lib = lib
     return _lib
+
+
+_PURE = ("tvlp_workspace_bytes", "tvlp_carry_elems", "tvlp_max_order",
+         "tvlp_framewise_aux_elems", "tvlp_framewise_nframes", "tvlp_subchunk_len")
+
+
+def on_device(device):
+    """``torch.cuda.device(device)`` only when it is not already current."""
+    if device.index is None or device.index == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(device)
 
 
 def profile_dump():

@@ -209,10 +209,15 @@ __device__ __forceinline__ void fwp_pass1(const IO (&a)[M], int L, In in, IO (&z
 template <typename IO, int M>
 __device__ __forceinline__ void fwp_exit(const IO (&a)[M], const IO (&ht)[2 * M], const IO (&z)[M],
                                          const IO (&x)[M], IO (&out)[M]) {
-#if TVLP_FW_CARRY64
+#if TVLP_FW_CARRY64 == 1
     using AC = double;  // the carry's dot products in fp64 (one rounding per exit)
 #else
     using AC = IO;
+#endif
+#if TVLP_FW_CARRY64 == 2
+    using AS = double;  // only the exit sums in fp64
+#else
+    using AS = AC;
 #endif
     AC q[M];
 #pragma unroll
@@ -224,9 +229,9 @@ __device__ __forceinline__ void fwp_exit(const IO (&a)[M], const IO (&ht)[2 * M]
     }
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-        AC v = (AC)z[j];
+        AS v = (AS)z[j];
 #pragma unroll
-        for (int k = 1; k <= M; ++k) v = fma(q[k - 1], (AC)ht[M - 1 - j + k], v);
+        for (int k = 1; k <= M; ++k) v = fma((AS)q[k - 1], (AS)ht[M - 1 - j + k], v);
         out[j] = (IO)v;
     }
 }

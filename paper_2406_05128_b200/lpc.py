@@ -234,7 +234,7 @@ def _forward(ti, e, A, zi, carry_prec=None, return_carry=False):
     flag = _flag(conv.device, vmode)
     fn = lib.tvlp_lp_forward_ti if ti else lib.tvlp_lp_forward_tv
     cp = _carry_code(carry_prec)
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(fn(dt, N.ptr(e), N.ptr(A), N.ptr(zi), N.ptr(s), B, T, M, N.ptr(carry), cp,
                    N.ptr(ws), nws, N.ptr(flag), N.stream_ptr(conv.device)))
     _raise_nonfinite(flag, e, A, "a" if ti else "A", vmode)
@@ -293,7 +293,7 @@ def _backward(ti, grad_s, A, s, zi, carry=None, carry_prec=None):
     if carry is not None and carry.numel() != lib.tvlp_carry_elems(B, T, M):
         carry = None
     fn = lib.tvlp_lp_backward_ti if ti else lib.tvlp_lp_backward_tv
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(fn(dt, N.ptr(grad_s), N.ptr(A), N.ptr(s), N.ptr(zi), N.ptr(ge), N.ptr(gA), B, T,
                    M, N.ptr(carry), _carry_code(carry_prec), N.ptr(ws), nws,
                    N.stream_ptr(conv.device)))
@@ -359,7 +359,7 @@ def lp_forward_tv_frames(e, frames, hop, zi=None, *, carry_precision=None, retur
                           conv.device)
     vmode = _mode(conv.numpy)
     flag = _flag(conv.device, vmode)
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(lib.tvlp_lp_forward_tv_frames(
             dt, N.ptr(e), N.ptr(frames), N.ptr(zi), N.ptr(s), B, T, M, F, hop, N.ptr(carry),
             _carry_code(carry_precision), N.ptr(ws), nws, N.ptr(flag), N.stream_ptr(conv.device)))
@@ -391,7 +391,7 @@ def lp_backward_tv_frames(grad_s, frames, hop, s, zi=None, *, carry=None, carry_
         carry = None
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_BWD_TV_FRAMES, dt, B, T, M, F, 0, hop),
                           conv.device)
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(lib.tvlp_lp_backward_tv_frames(
             dt, N.ptr(grad_s), N.ptr(frames), N.ptr(s), N.ptr(zi), N.ptr(ge), N.ptr(gF), B, T, M,
             F, hop, N.ptr(carry), _carry_code(carry_precision), N.ptr(ws), nws,
@@ -446,7 +446,7 @@ def lp_forward_tv_grouped(groups, *, carry_precision=None, return_carry=False):
                                    for e, A, z, s in zip(es, As, zis, outs)])
     vmode = _mode(conv.numpy)
     flag = _flag(conv.device, vmode)
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(lib.tvlp_lp_forward_tv_grouped(dt, len(es), arr, T, M, N.ptr(carry),
                                                _carry_code(carry_precision), N.ptr(ws), nws,
                                                N.ptr(flag), N.stream_ptr(conv.device)))
@@ -491,7 +491,7 @@ def lp_backward_tv_grouped(groups, *, carry=None, carry_precision=None):
                                                0 if z is None else z.data_ptr(), ge.data_ptr(),
                                                gA.data_ptr(), g.shape[0])
                                     for g, A, s, z, ge, gA in zip(gs_, As, ss, zis, ges, gAs)])
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(lib.tvlp_lp_backward_tv_grouped(dt, len(gs_), arr, T, M, N.ptr(carry),
                                                 _carry_code(carry_precision), N.ptr(ws), nws,
                                                 N.stream_ptr(conv.device)))
@@ -513,7 +513,7 @@ def shift_coeffs(A):
     B = A.shape[0] if A.dim() == 3 else 1
     T, M = A.shape[-2], A.shape[-1]
     out = torch.empty_like(A)
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(N.load().tvlp_shift_coeffs(N.dtype_code(A.dtype), N.ptr(A), N.ptr(out), B, T, M,
                                            N.stream_ptr(conv.device)))
     return conv.out(out)
@@ -530,7 +530,7 @@ def lagged_signal_matrix(s, M, zi=None):
     T = s.shape[-1]
     zi = None if zi is None else conv.t(zi, s.dtype).expand(B, M).contiguous()
     out = torch.empty(s.shape + (M,), dtype=s.dtype, device=conv.device)
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(N.load().tvlp_lagged_signal_matrix(N.dtype_code(s.dtype), N.ptr(s), N.ptr(zi),
                                                    N.ptr(out), B, T, M,
                                                    N.stream_ptr(conv.device)))

@@ -56,7 +56,7 @@ def reflection_to_lpc(k):
     lib = N.load()
     a = torch.empty_like(kt)
     bad = torch.zeros(1, dtype=torch.int32, device=conv.device)
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(lib.tvlp_reflection_to_lpc(N.dtype_code(kt.dtype), N.ptr(kt), N.ptr(a), rows, M,
                                            N.ptr(bad), N.stream_ptr(conv.device)))
     if int(bad.item()) != 0:
@@ -78,7 +78,7 @@ def reflection_to_lpc_vjp(grad_a, k):
     rows = kt.numel() // M
     lib = N.load()
     gk = torch.empty_like(kt)
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(lib.tvlp_reflection_to_lpc_vjp(N.dtype_code(kt.dtype), N.ptr(ga), N.ptr(kt),
                                                N.ptr(gk), rows, M, N.stream_ptr(conv.device)))
     return conv.out(gk)
@@ -232,7 +232,7 @@ def framewise_forward(e, frames, plan, return_aux=False):
     dt = N.dtype_code(e.dtype)
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FW_FWD, dt, B, T, M, F, plan.frame_size,
                                                    plan.hop), conv.device)
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(lib.tvlp_framewise_forward_ex(dt, N.ptr(e), N.ptr(frames), N.ptr(w),
                                               plan._cola_cached(), N.ptr(out), N.ptr(seg),
                                               N.ptr(aux), B, T, F, M, plan.frame_size, plan.hop,
@@ -266,7 +266,7 @@ def framewise_backward(grad_out, frames, seg, plan, aux=None):
     dt = N.dtype_code(g.dtype)
     ws, nws = N.workspace(lib.tvlp_workspace_bytes(N.OP_FW_BWD, dt, B, T, M, F, plan.frame_size,
                                                    plan.hop), conv.device)
-    with torch.cuda.device(conv.device):
+    with N.on_device(conv.device):
         N.check(lib.tvlp_framewise_backward_ex(dt, N.ptr(g), N.ptr(frames), N.ptr(w),
                                                plan._cola_cached(), N.ptr(seg), N.ptr(aux),
                                                N.ptr(ge), N.ptr(gf), B, T, F, M, plan.frame_size,

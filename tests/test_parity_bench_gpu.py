@@ -276,3 +276,43 @@ def test_lp_ti_shared_row_batched_backward():
               for b in range(3))
     np.testing.assert_allclose(_np(ga), ref, rtol=1e-10, atol=1e-12)
 
+
+
+@pytest.mark.parametrize("M,dt,tol", [(20, np.float32, TOL32), (22, np.float64, 1e-9),
+                                      (12, np.float32, TOL32)])
+def test_framewise_pieces_padded_order_and_fp64(M, dt, tol):
+    """The frames-in-pieces kernels at a padded order (M=20 -> 22) and in
+    float64, with the forward's saved impulse-response tails (aux) reused by
+    the backward, against the fp64 oracle."""
+    from paper_2406_05128_b200 import params
+
+    B, T, hop = 3, 4800, 240
+    ev, fr, gv = data.d1_frames_batch(40 + M, B, T, M, hop)
+    ev, fr, gv = ev.astype(dt), fr.astype(dt), gv.astype(dt)
+    plan = params.FramePlan.raised_cosine(hop)
+    e, f, g = (torch.from_numpy(x).cuda() for x in (ev, fr, gv))
+    y, seg, aux = params.framewise_forward(e, f, plan, return_aux=True)
+    assert aux is not None and aux.numel() % (B * seg.shape[1] * 2) == 0  # [B, nfr, 2 Mp]
+    ge, gf = params.framewise_backward(g, f, seg, plan, aux=aux)
+    for b in range(B):
+        ry, rseg = oracle.framewise_forward(ev[b].astype(np.float64), fr[b].astype(np.float64), hop)
+        rge, rgf = oracle.framewise_backward(gv[b].astype(np.float64), fr[b].astype(np.float64),
+                                             rseg, hop)
+        errs = (oracle.gradcheck_error(_np(y)[b], ry), oracle.gradcheck_error(_np(ge)[b], rge),
+                oracle.gradcheck_error(_np(gf)[b], rgf))
+        assert max(errs) < tol, (b, errs)
+
+
+def test_grouped_three_groups():
+    """Three independent batches (sizes 2, 1, 3) in one grouped launch."""
+    sizes = (2, 1, 3)
+    batches = [data.d1_batch(70 + 10 * i, n, 4800) for i, n in enumerate(sizes)]
+    t = lambda x: torch.from_numpy(x).cuda()  # noqa: E731
+    outs, carry = lpc.lp_forward_tv_grouped([(t(e), t(A)) for e, A, _ in batches],
+                                            return_carry=True)
+    grads = lpc.lp_backward_tv_grouped([(t(g), t(A), s) for (e, A, g), s in zip(batches, outs)],
+                                       carry=carry)
+    for (e, A, g), s, (ge, gA) in zip(batches, outs, grads):
+        for b in range(e.shape[0]):
+            errs = _tv_item_errs(e[b], A[b], g[b], _np(s)[b], _np(ge)[b], _np(gA)[b])
+            assert max(errs) < TOL32, errs
