@@ -79,7 +79,38 @@ def _items(kind, seeds, T, M, hop):
     return out
 
 
+def _decoder_items(seeds, T, hop):
+    from paper_2406_05128_b200 import decoder as dmod
+
+    out = []
+    for sd in seeds:
+        fields, f0, noise, target = dmod.synthetic_inputs(1, T + 1, hop, seed=sd)
+        out.append(({k: v[0] for k, v in fields.items()}, f0[0], sd, target[0]))
+    return out, dmod.synthetic_tables()
+
+
+def _one_decoder(item, tables, hop):
+    """The reference HpN decoder step on its Tape (float32 tape): synthesis,
+    MSS loss, backward (synth.py:217-275, loss.py:105-126)."""
+    from tvlp import loss, source, synth
+    from tvlp.tape import Tape
+    import numpy as np
+
+    fields, f0, seed, target = item
+    n_out = target.shape[0]
+    F = (n_out - 1) // hop + 1
+    p = synth.init_params(F, 22, hop, mode="hpn", seed=0, f0_frames=f0)
+    for k, v in fields.items():
+        setattr(p, k, v)
+    wt = source.Wavetable(tables=tables, rd_grid=np.linspace(0.3, 2.7, tables.shape[0]))
+    tape = Tape(np.float32)
+    y, _ = synth.build_synth_graph(tape, p, n_out, 24000.0, seed, wavetable=wt)
+    tape.backward(loss.mss_loss(tape, y, target))
+
+
 def _one(lpc, params, kind, item, hop, plan):
+    if kind == "decoder":
+        return _one_decoder(item[0], item[1], hop)
     e, A, g = item
     if kind == "tvf":
         T1 = e.shape[0]
@@ -99,7 +130,11 @@ def _worker(kind, seeds, T, M, hop, seconds, barrier, q):
     _single_thread_env()
     lpc, params = _import()
     plan = params.FramePlan.raised_cosine(hop) if kind == "framewise" else None
-    items = _items(kind, seeds, T, M, hop)
+    if kind == "decoder":
+        its, tables = _decoder_items(seeds, T, hop)
+        items = [(it, tables) for it in its]
+    else:
+        items = _items(kind, seeds, T, M, hop)
     _one(lpc, params, kind, items[0], hop, plan)  # jit compile / cache load
     barrier.wait()
     n = 0
@@ -145,7 +180,10 @@ def measure(kind, T, M, hop=240, procs=None, seconds=6.0, lps_per_sample=1):
             "hpn": "lp_forward_tv + lp_backward_tv per LP, 2 LPs per audio sample",
             "tvsplit": "lp_forward_tv + lp_backward_tv (lpc.py:101-173)",
             "tvf": "upsample_linear + lp_forward_tv + lp_backward_tv + upsample VJP",
-            "framewise": "_framewise_forward + _framewise_vjp (params.py:220-273)"}[kind]
+            "framewise": "_framewise_forward + _framewise_vjp (params.py:220-273)",
+            "decoder": "the reference's HpN decoder step on its Tape: build_synth_graph + "
+                       "mss_loss + backward (synth.py:217-275, loss.py:105-126; no C(z) LP: "
+                       "the reference has none)"}[kind]
     return {
         "kind": "reference", "impl": "tvlp (numba, baseline/_ref, unmodified)",
         "unit": "samples/s", "cpu_model": cpu_model(),

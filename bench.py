@@ -55,6 +55,13 @@ CONFIGS = {
     # noise) grouped into one launch; 256 items over 8 GPUs = 32 items per GPU
     "hpn_b32_t48000": dict(kind="hpn", B=32, T=48000, M=22, baseline_cfg=5,
                            encoder_params=6_100_000),
+    # config 5 as BASELINE.json states it: the FULL GOLF HpN synthesiser step
+    # on the GPU -- oscillator x4 + decimator, shaped noise, H(z) and the
+    # paper's C(z) LP in one grouped launch, global FIR, the prime-size MSS
+    # loss and the backward to every frame parameter (decoder.py, §8(f)
+    # ranks 3-4) -- 32 items per GPU, encoder all-reduce stand-in overlapped
+    "hpn_full_b32_t48000": dict(kind="decoder", B=32, T=48000, M=22, hop=240, baseline_cfg=5,
+                                encoder_params=6_100_000, mode="hpn", c_lp=True),
     # config 3 with frame-rate coefficients (hop 240)
     # upsampled inside the kernels (the synthesiser's upsample_linear -> lp_tv)
     "tv_frames_b64_t48000": dict(kind="tvf", B=64, T=48000, M=22, hop=240, baseline_cfg=3),
@@ -71,7 +78,7 @@ def algorithmic_bytes_per_sample(cfg):
     M = cfg["M"]
     if cfg["kind"] in ("tv", "tvsplit"):
         return 4 * (3 * M + 5)
-    if cfg["kind"] == "hpn":
+    if cfg["kind"] in ("hpn", "decoder"):
         return 2 * 4 * (3 * M + 5)
     if cfg["kind"] == "tvf":
         # e, s (fwd); g_s, s, g_e (bwd); frames in twice and grad_frames out
@@ -232,9 +239,12 @@ def cpu_baseline(cfg, seconds=10.0):
     # at most one core per independent sequence (config 4's one 14.4 M-sample
     # sequence is one core's work whatever the host)
     nthreads = max(1, min(nthreads, cfg["B"] * (2 if cfg["kind"] == "hpn" else 1)))
-    port = _port_baseline(cfg, nthreads, seconds)
-    one = _port_baseline(cfg, 1, max(3.0, seconds / 3), one_core=True)
-    port["one_core"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
+    if cfg["kind"] == "decoder":
+        port = None  # the C port covers the LP path only
+    else:
+        port = _port_baseline(cfg, nthreads, seconds)
+        one = _port_baseline(cfg, 1, max(3.0, seconds / 3), one_core=True)
+        port["one_core"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
     sys.path.insert(0, os.path.join(ROOT, "baseline"))
     import tvlp_cpu
 
@@ -246,8 +256,13 @@ def cpu_baseline(cfg, seconds=10.0):
                                    procs=nthreads, seconds=max(3.0, seconds / 2),
                                    lps_per_sample=2 if cfg["kind"] == "hpn" else 1)
         except Exception as ex:  # reported; the port stands in
-            port["reference_error"] = f"{type(ex).__name__}: {ex}"[:200]
+            if port is not None:
+                port["reference_error"] = f"{type(ex).__name__}: {ex}"[:200]
     if ref is None:
+        if port is None:
+            return {"value": None, "unit": UNIT, "cores": nthreads, "kind": "reference",
+                    "unavailable": "baseline/_ref absent",
+                    "cpu_model": tvlp_cpu.cpu_model()}
         port["cpu_model"] = tvlp_cpu.cpu_model()
         return port
     return {"value": ref["n_core"]["value"], "unit": UNIT, "cores": ref["n_core"]["cores"],
@@ -318,6 +333,52 @@ def _port_baseline(cfg, nthreads, seconds, one_core=False):
                       f"{len(times)} repeats, {nthreads} threads, oracle/tvlp_oracle.c"}
 
 
+def _reference_decoder(item, dtype, fields, f0, noise_seed, target, tables):
+    """The reference's own decoder step (synth.build_synth_graph +
+    loss.mss_loss + Tape.backward) for one item: (y, loss, grads)."""
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    from tvlp import loss, source, synth
+    from tvlp.tape import Tape
+
+    n_out, hop, mode = item["n_out"], item["hop"], item["mode"]
+    F = (n_out - 1) // hop + 1
+    p = synth.init_params(F, 22, hop, mode=mode, seed=0, f0_frames=f0)
+    for k, v in fields.items():
+        setattr(p, k, np.asarray(v, dtype=np.float64))
+    wt = source.Wavetable(tables=tables, rd_grid=np.linspace(0.3, 2.7, tables.shape[0]))
+    tape = Tape(dtype)
+    y, leaves = synth.build_synth_graph(tape, p, n_out, 24000.0, noise_seed, wavetable=wt)
+    L = loss.mss_loss(tape, y, target)
+    tape.backward(L)
+    return y.value, float(L.value), {k: tape.grad(v) for k, v in leaves.items()}
+
+
+def parity_decoder(item):
+    """The GPU decoder (float64, c_lp off: the reference has no C(z) LP)
+    against the reference's own graph on one item of the bench's generator:
+    max gradcheck_error over the output, the loss and every gradient."""
+    import torch
+
+    import oracle
+    from paper_2406_05128_b200 import decoder as dmod
+
+    n_out, hop = item["n_out"], item["hop"]
+    fields, f0, noise, target = dmod.synthetic_inputs(1, n_out, hop, seed=item["seed"])
+    tables = dmod.synthetic_tables()
+    ry, rL, rg = _reference_decoder(item, np.float64, {k: v[0] for k, v in fields.items()}, f0[0],
+                                    item["seed"], target[0], tables)
+    dev = torch.device("cuda", 0)
+    dec = dmod.Decoder(torch.tensor(tables, device=dev), hop=hop, mode=item["mode"])
+    p = {k: torch.tensor(v, device=dev, requires_grad=True) for k, v in fields.items()}
+    y = dec.render(p, n_out, torch.tensor(noise, device=dev), f0)
+    L = dmod.mss_loss(y, torch.tensor(target, device=dev))
+    L.sum().backward()
+    errs = [oracle.gradcheck_error(y.detach().cpu().numpy()[0], ry),
+            abs(float(L[0]) - rL) / max(abs(rL), 1e-12)]
+    errs += [oracle.gradcheck_error(p[k].grad.cpu().numpy()[0], rg[k]) for k in rg]
+    return max(errs)
+
+
 def parity_check(cfg, sample):
     """Part of the CPU leg (rank 0, outside every timed region): the GPU
     outputs of the LAST timed step, for the first and last item of this
@@ -328,6 +389,11 @@ def parity_check(cfg, sample):
     import oracle
 
     kind = cfg["kind"]
+    if kind == "decoder":
+        try:
+            return parity_decoder(sample[0])
+        except ImportError:  # the reference install (baseline/_ref) is absent
+            return None
     worst = 0.0
     for item in sample:
         x = {k: np.asarray(v, dtype=np.float64) for k, v in item.items()}
@@ -398,6 +464,31 @@ def run_b200(args, cfg, rank, world, dist):
                     grad, dist, lambda: lpc.lp_backward_tv_grouped(
                         [(g[0], A[0], sh), (g[1], A[1], sc)], carry=carry))
                 return [sh, sc], [geh, gec], [gAh, gAc]
+    elif kind == "decoder":
+        from paper_2406_05128_b200 import decoder as dmod
+
+        n_out = T + 1
+        F = (n_out - 1) // cfg["hop"] + 1
+        fields, f0, noise, target = dmod.synthetic_inputs(B, n_out, cfg["hop"], seed=lo)
+        dec = dmod.Decoder(torch.tensor(dmod.synthetic_tables(), dtype=torch.float32, device=dev),
+                           hop=cfg["hop"], mode=cfg["mode"], c_lp=cfg["c_lp"])
+        params_d = {k: torch.tensor(v, dtype=torch.float32, device=dev, requires_grad=True)
+                    for k, v in fields.items()}
+        noise_d = torch.tensor(noise, dtype=torch.float32, device=dev)
+        target_d = torch.tensor(target, dtype=torch.float32, device=dev)
+        c_frames = torch.tensor(dmod.stable_c_frames(B, F, seed=lo), dtype=torch.float32,
+                                device=dev) if cfg["c_lp"] else None
+        if dist is not None:
+            grad = torch.randn(cfg["encoder_params"], device=dev)
+        e, A, g = noise_d, params_d, target_d  # (host copies for e2e: see below)
+
+        def step(e=noise_d, A=params_d, g=target_d):
+            for t_ in A.values():
+                t_.grad = None
+            y = dec.render(A, n_out, e, f0, c_frames)
+            L = dmod.mss_loss(y, g)
+            pdist.overlapped_allreduce(grad, dist, lambda: L.sum().backward())
+            return y, L, A["reflection_raw"].grad
     elif kind == "tvsplit":
         from paper_2406_05128_b200 import longseq
 
@@ -471,8 +562,13 @@ def run_b200(args, cfg, rank, world, dist):
     outs = step()
     torch.cuda.synchronize()
     parity_sample = []
+    if kind == "decoder":
+        # the CPU leg compares the decoder in float64 (c_lp off: the
+        # reference has no C(z) LP) with the reference's own graph, item 0
+        parity_sample.append({"seed": lo, "n_out": T + 1, "hop": cfg["hop"], "mode": cfg["mode"]})
+        outs = None
     # (HpN: item 0 of the H(z) group and the last item of the C(z) group)
-    picks = ([(0, 0), (1, B - 1)] if kind == "hpn" else
+    picks = ([] if kind == "decoder" else [(0, 0), (1, B - 1)] if kind == "hpn" else
              [(None, b) for b in sorted({0, e.shape[0] - 1})])
     for grp, b in picks:
         sel = (lambda x: x[b]) if grp is None else (lambda x, grp=grp: x[grp][b])
@@ -515,7 +611,7 @@ def run_b200(args, cfg, rank, world, dist):
                                              for k in ("fw_forward", "fw_backward"))}
     elif dom is not None:
         bps = (kernel_bytes_per_sample_frames if kind == "tvf" else kernel_bytes_per_sample)(dom, M)
-        lp_rows = 2 * B if kind == "hpn" else B  # LP sequences per GPU
+        lp_rows = 2 * B if kind in ("hpn", "decoder") else B  # LP sequences per GPU
         T_k = T // world if kind == "tvsplit" else T  # samples per sequence on this GPU
         cnt, tot = prof[dom]
         t_step = tot / nsteps * 1e-3  # seconds of this kernel per step (all its slices)
@@ -545,17 +641,42 @@ def run_b200(args, cfg, rank, world, dist):
 
     # e2e: pinned host buffers through the public API (HpN: the host batch of
     # both filters' rows, H(z) then C(z), through the pipelined host API)
-    if kind == "hpn":
+    if kind == "decoder":
+        # host: the frame parameters, noise and target in; the output signal,
+        # the per-item losses and every parameter gradient out
+        ph = {k: v.detach().cpu().pin_memory() for k, v in A.items()}
+        nh, th = e.cpu().pin_memory(), g.cpu().pin_memory()
+        yh = torch.empty((B, T + 1), dtype=torch.float32, pin_memory=True)
+        lh = torch.empty(B, dtype=torch.float32, pin_memory=True)
+        gh_ = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in ph.items()}
+        h2d = sum(x.numel() * x.element_size() for x in list(ph.values()) + [nh, th])
+        d2h = sum(x.numel() * x.element_size() for x in list(gh_.values()) + [yh, lh])
+
+        def e2e_step():
+            with torch.no_grad():
+                for k, v in ph.items():
+                    A[k].copy_(v, non_blocking=True)
+                e.copy_(nh, non_blocking=True)
+                g.copy_(th, non_blocking=True)
+            y, L, _ = step()
+            yh.copy_(y.detach(), non_blocking=True)
+            lh.copy_(L.detach(), non_blocking=True)
+            for k in ph:
+                gh_[k].copy_(A[k].grad, non_blocking=True)
+    elif kind == "hpn":
         eh, Ah, gh = (torch.cat([y.cpu() for y in x]).pin_memory() for x in (e, A, g))
         oh = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (eh, eh, Ah)]
     else:
         eh, Ah, gh = (x.cpu().pin_memory() for x in (e, A, g))
         outs = step()
         oh = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
-    h2d = sum(x.numel() * x.element_size() for x in (eh, Ah, gh))
-    d2h = sum(x.numel() * x.element_size() for x in oh)
+    if kind != "decoder":
+        h2d = sum(x.numel() * x.element_size() for x in (eh, Ah, gh))
+        d2h = sum(x.numel() * x.element_size() for x in oh)
 
-    if kind in ("tv", "hpn"):
+    if kind == "decoder":
+        pass  # e2e_step defined above
+    elif kind in ("tv", "hpn"):
         from paper_2406_05128_b200 import stream as pstream
 
         def e2e_step():

@@ -302,7 +302,8 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
 template <int M, int U, int NST, int MODE, bool TI>
 __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int64_t g0, int L,
                                               int nwin, unsigned char* sm, uint64_t* bars,
-                                              float (&lam)[M], const float* ati) {
+                                              float (&lam)[M], const float* ati,
+                                              float* gmax = nullptr) {
     using S = UnitLane<M, U, NST>;
     constexpr int W = S::W;
     const int lane = threadIdx.x & 31;
@@ -331,6 +332,7 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
     };
 #pragma unroll
     for (int k = 0; k < NST; ++k) issue(k);
+    float gm = 0.f;  // MODE 1: max |grad_e| over the lane's samples
     for (int k = 0; k < nwin; ++k) {
         const int st = k % NST;
         TVLP_ASSERT(k < nwin && ln < U && L <= U);
@@ -355,6 +357,7 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
                 load_row_at<float, M>(Ar + (u - 1) * M, an, (ln * S::AROW + (u - 1) * M) * 4);
             const float l0 = lam[0] + gv[u];
             ov[u] = l0;
+            if (MODE == 1) gm = fmaxf(gm, fabsf(l0));
 #pragma unroll
             for (int i = 0; i < M - 1; ++i) lam[i] = fmaf(-a[i], l0, lam[i + 1]);
             lam[M - 1] = -a[M - 1] * l0;
@@ -364,6 +367,7 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
         __syncwarp();  // every lane is done with the stage: refill it
         issue(k + NST);
     }
+    if (gmax != nullptr) *gmax = lane < L ? gm : 0.f;
 }
 
 // ---------------------------------------------------------------- carries of a unit
@@ -988,7 +992,8 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
         // keep the unit's left carry for lane 0's defect check (nus is free now)
         if (lane < M) nus[lane] = mu;
         __syncwarp();
-        unit_adj_pass<M, U, NST, 1, TI>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow);
+        float gmx = 0.f;
+        unit_adj_pass<M, U, NST, 1, TI>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow, &gmx);
         tt[4] = gtime();
         trace_rec(a.tr, t, 3, t, tt);
         if (a.refine) {
@@ -998,9 +1003,13 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
                 for (int i = 0; i < M; ++i) a.Kout[(g0 + lane) * MP4 + i] = lam[i];
             }
             const bool chk = lane < L && (lane > 0 || ru > 0);
+            // scale: max |grad_e| over the unit's samples (the parity metric is
+            // relative to the sequence's max |grad_e|; the boundary values of
+            // lambda_0 alone can be far smaller and flag rounding-level defects)
+            xm = gmx;
             if (chk) {
                 const float* prev = lane > 0 ? xs + (lane - 1) * MP4 : nus;
-                xm = fmaxf(fabsf(lam[0]), fabsf(prev[0]));
+                xm = fmaxf(xm, fmaxf(fabsf(lam[0]), fabsf(prev[0])));
 #pragma unroll
                 for (int i = 0; i < M; ++i) dm = fmaxf(dm, fabsf(lam[i] - prev[i]));
                 if (!(dm == dm)) dm = __int_as_float(0x7f800000);

@@ -388,3 +388,61 @@ class Decoder:
             return global_fir(s + c, p["fir_taps"])
         s = ag.lp_tv_frames(hgain * osc, a_frames, hop)
         return global_fir(s + noise_s, p["fir_taps"])
+
+
+# ---------------------------------------------------------------- synthetic inputs
+FIELDS = ("reflection_raw", "table_pos_raw", "voiced_gain_raw", "noise_gain_raw", "h_gain_raw",
+          "noise_logmag", "fir_taps")
+
+
+def synthetic_tables(K=9, L=512):
+    """K smooth one-period waveforms of L samples (harmonic series with a
+    spectral tilt growing with the row: a stand-in for the LF wavetable rows
+    source.py:57-208 builds; the tables are data here), float64 [K, L]."""
+    n = np.arange(L) / L
+    rows = []
+    for k in range(K):
+        tilt = 0.3 + 0.25 * k
+        h = np.arange(1, 40)
+        amp = h ** (-1.0 - tilt)
+        w = (amp[:, None] * np.sin(2 * np.pi * h[:, None] * n[None, :] + 0.1 * h[:, None])).sum(0)
+        rows.append(w / np.abs(w).max())
+    return np.stack(rows)
+
+
+def synthetic_inputs(B, n_out, hop=240, seed=0, order=22):
+    """Decoder inputs for B items of n_out samples (numpy float64): the
+    trainable fields [B, ...] in the ranges of a fitted voice (the golden
+    fixtures' generator, tests/golden/make_golden_decoder.py) with the
+    reflection frames of distribution D1 (a smooth AR(1)
+    walk, as the LP benchmarks use), f0 frames [B, F], the reference's noise
+    stream per item [B, n_out] and a target."""
+    from .data import d1_reflection_raw
+
+    F = (n_out - 1) // hop + 1
+    rng = np.random.default_rng(seed)
+    f = {
+        "reflection_raw": np.stack([d1_reflection_raw(1000 * seed + b, n_out, order, hop)
+                                    for b in range(B)]),
+        "table_pos_raw": rng.normal(0.0, 1.0, size=(B, F)),
+        "voiced_gain_raw": rng.normal(-1.0, 0.3, size=(B, F)),
+        "noise_gain_raw": rng.normal(-2.5, 0.3, size=(B, F)),
+        "h_gain_raw": rng.normal(-0.5, 0.2, size=(B, F)),
+        "noise_logmag": rng.normal(0.0, 0.5, size=(B, F, NOISE_BINS)),
+        "fir_taps": np.concatenate([np.ones((B, 1)), 0.05 * rng.standard_normal((B, FIR_TAPS - 1))],
+                                   axis=1),
+    }
+    f0 = np.linspace(110.0, 190.0, F)[None] * (1 + 0.05 * rng.standard_normal((B, F)))
+    noise = np.stack([generate_noise(n_out, seed + b) for b in range(B)])
+    target = 0.3 * rng.standard_normal((B, n_out))
+    return f, f0, noise, target
+
+
+def stable_c_frames(B, F, seed=0, order=22):
+    """A C(z) all-pole track for the GOLF-v1 noise filter (c_lp=True): step-up
+    of squashed small reflection rows (stable), float64 [B, F, order]."""
+    from .data import reflection_to_lpc
+
+    rng = np.random.default_rng(seed + 7)
+    k = 0.999 * np.tanh(rng.normal(0.0, 0.2, size=(B * F, order)))
+    return reflection_to_lpc(k).reshape(B, F, order)

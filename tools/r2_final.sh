@@ -2,8 +2,8 @@
 # End-of-round measurement set (outputs in gpurun_out/, summarised into profiles/)
 mkdir -p gpurun_out
 p=${1:-r2_final}
-for c in tv_b64_t48000 tv_b4_t24000 framewise_b32_t48000 tv_b1_t14400000 hpn_b32_t48000 tv_frames_b64_t48000; do
-  timeout 600 python bench.py --config $c > gpurun_out/${p}_$c.json 2> gpurun_out/${p}_$c.err
+for c in tv_b64_t48000 tv_b4_t24000 framewise_b32_t48000 tv_b1_t14400000 hpn_b32_t48000 hpn_full_b32_t48000 tv_frames_b64_t48000; do
+  timeout 900 python bench.py --config $c > gpurun_out/${p}_$c.json 2> gpurun_out/${p}_$c.err
 done
 for s in 2 4 8; do
   timeout 300 python bench.py --shard-of $s --no-cpu-baseline > gpurun_out/${p}_shard$s.json 2> gpurun_out/${p}_shard$s.err
