@@ -1419,6 +1419,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
     FrameCursor<IO, FR ? M : 1> cur;
     const int64_t ft0 = active ? (gid % g.nsub) * (int64_t)g.Ls : 0;
 
+    float gmx = 0.f;  // MODE 1: max |grad_e| over the lane's samples (defect scale)
     for (int k = 0; k < nwin; ++k) {
         const int st = k % kLaneStages;
         mbar_wait(&bars[st], (uint32_t)((k / kLaneStages) & 1));
@@ -1442,6 +1443,7 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
             }
             const IO l0 = lam[0] + gv[u];
             ov[u] = l0;
+            if (MODE == 1) gmx = fmaxf(gmx, (float)fabs(l0));
 #pragma unroll
             for (int i = 0; i < M - 1; ++i) lam[i] = fma(-a[i], l0, lam[i + 1]);
             lam[M - 1] = -a[M - 1] * l0;
@@ -1460,13 +1462,16 @@ k_adjoint(const __grid_constant__ LaneMaps maps, const IO* __restrict__ ati_ptr,
 #pragma unroll
         for (int i = 0; i < M; ++i) Nu[gid * Tape<M>::MP4 + i] = lam[i];
         if (MODE == 1 && dstat != nullptr && (gid % g.nsub) > 0) {
-            // scale: |lambda_0| = |grad_e| at the boundary.  The other adjoint
-            // components are coefficient-weighted sums of future grad_e and can
-            // be orders larger on resonant rows, while a defect in component i
-            // reaches grad_e unamplified i steps later (it shifts into lambda_0).
+            // scale: |grad_e| = |lambda_0|, over the sub-chunk's samples and the
+            // boundary.  The other adjoint components are coefficient-weighted
+            // sums of future grad_e and can be orders larger on resonant rows,
+            // while a defect in component i reaches grad_e unamplified i steps
+            // later (it shifts into lambda_0); the parity metric is relative to
+            // the sequence's max |grad_e|, which the boundary value alone can
+            // understate by orders (false flags on loss gradients).
             float dm = 0.f;
             const IO mp0 = Mu[(gid - 1) * Tape<M>::MP4];
-            const float xm = fmaxf((float)fabs(lam[0]), (float)fabs(mp0));
+            const float xm = fmaxf(gmx, fmaxf((float)fabs(lam[0]), (float)fabs(mp0)));
 #pragma unroll
             for (int i = 0; i < M; ++i) {
                 const IO mp = Mu[(gid - 1) * Tape<M>::MP4 + i];
