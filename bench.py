@@ -57,7 +57,7 @@ CONFIGS = {
                            encoder_params=6_100_000),
     # config 5 as BASELINE.json states it: the FULL GOLF HpN synthesiser step
     # on the GPU -- oscillator x4 + decimator, shaped noise, H(z) and the
-    # paper's C(z) LP in one grouped launch, global FIR, the prime-size MSS
+    # paper's C(z) LP in one frame-rate launch, global FIR, the prime-size MSS
     # loss and the backward to every frame parameter (decoder.py, §8(f)
     # ranks 3-4) -- 32 items per GPU, encoder all-reduce stand-in overlapped
     "hpn_full_b32_t48000": dict(kind="decoder", B=32, T=48000, M=22, hop=240, baseline_cfg=5,
@@ -374,7 +374,7 @@ def parity_decoder(item):
     L = dmod.mss_loss(y, torch.tensor(target, device=dev))
     L.sum().backward()
     errs = [oracle.gradcheck_error(y.detach().cpu().numpy()[0], ry),
-            abs(float(L[0]) - rL) / max(abs(rL), 1e-12)]
+            abs(float(L.detach()[0]) - rL) / max(abs(rL), 1e-12)]
     errs += [oracle.gradcheck_error(p[k].grad.cpu().numpy()[0], rg[k]) for k in rg]
     return max(errs)
 
@@ -481,14 +481,20 @@ def run_b200(args, cfg, rank, world, dist):
         if dist is not None:
             grad = torch.randn(cfg["encoder_params"], device=dev)
         e, A, g = noise_d, params_d, target_d  # (host copies for e2e: see below)
+        # the whole step -- render, loss, backward -- captured once in a CUDA
+        # graph over these static buffers (decoder.GraphedStep) and replayed:
+        # every kernel of the step runs each replay, with no host work
+        gstep = dmod.GraphedStep(dec, params_d, noise_d, target_d,
+                                 torch.tensor(f0, dtype=torch.float64, device=dev), c_frames)
 
         def step(e=noise_d, A=params_d, g=target_d):
-            for t_ in A.values():
-                t_.grad = None
-            y = dec.render(A, n_out, e, f0, c_frames)
-            L = dmod.mss_loss(y, g)
-            pdist.overlapped_allreduce(grad, dist, lambda: L.sum().backward())
+            y, L = gstep.replay()
+            if dist is not None:  # the encoder all-reduce stand-in (after the graph)
+                dist.all_reduce(grad)
             return y, L, A["reflection_raw"].grad
+
+        def eager_step():  # the same step without the graph (per-kernel profiling pass)
+            gstep._run()
     elif kind == "tvsplit":
         from paper_2406_05128_b200 import longseq
 
@@ -551,6 +557,8 @@ def run_b200(args, cfg, rank, world, dist):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = lib.tvlp_launch_count() - n0
+    if kind == "decoder":  # replays: the launches captured in the graph, per step
+        launches = gstep.launches * args.steps
     refined = lib.tvlp_refined_sequences() - r0
     ms = pdist.max_over_ranks(ev0.elapsed_time(ev1) / args.steps, dist, dev)
     nonfinite_seen = lpc.check_nonfinite(dev)
@@ -581,7 +589,7 @@ def run_b200(args, cfg, rank, world, dist):
     N.profile_dump()
     lib.tvlp_profile_enable(1)
     for _ in range(args.steps):
-        step()
+        (eager_step if kind == "decoder" else step)()
     torch.cuda.synchronize()
     lib.tvlp_profile_enable(0)
     prof = N.profile_dump()
@@ -716,6 +724,7 @@ def run_b200(args, cfg, rank, world, dist):
                    "kind": kind, "B_per_gpu": B, "T": T, "M": M,
                    "global_B": B_glob, "parallelism": f"batch-shard x{world}",
                    "shard_of": args.shard_of if (strong and world == 1 and args.shard_of > 1) else None,
+                   "cuda_graph": kind == "decoder",
                    "carry_precision": lpc.carry_precision(),
                    "subchunk": int(lib.tvlp_subchunk_len(2 * B if kind == "hpn" else B, T, M)) if kind in ("tv", "hpn", "tvf") else None,
                    "l2": "inputs larger than L2"},

@@ -55,11 +55,20 @@ def reflection_to_lpc(k):
     rows = kt.numel() // M
     lib = N.load()
     a = torch.empty_like(kt)
-    bad = torch.zeros(1, dtype=torch.int32, device=conv.device)
+    # |k| >= 1 is reported like non-finite LP inputs: at once for numpy callers,
+    # through the device flag (lpc.check_nonfinite) for CUDA tensors -- no
+    # host sync inside a training step or a CUDA-graph capture
+    from . import lpc as _lpc
+
+    vmode = _lpc._mode(conv.numpy)
+    if torch.cuda.is_current_stream_capturing():
+        vmode = "lazy" if vmode != "off" else vmode
+    bad = (torch.zeros(1, dtype=torch.int32, device=conv.device) if vmode == "eager"
+           else _lpc._flag(conv.device, vmode))
     with N.on_device(conv.device):
         N.check(lib.tvlp_reflection_to_lpc(N.dtype_code(kt.dtype), N.ptr(kt), N.ptr(a), rows, M,
                                            N.ptr(bad), N.stream_ptr(conv.device)))
-    if int(bad.item()) != 0:
+    if vmode == "eager" and int(bad.item()) != 0:
         raise ValueError("reflection coefficients must satisfy |k| < 1")
     return conv.out(a)
 

@@ -18,7 +18,8 @@ def main():
     F = (n_out - 1) // hop + 1
     dev = torch.device("cuda", 0)
     dec = decoder.Decoder(torch.tensor(g["tables"], dtype=torch.float32, device=dev), hop=hop,
-                          fs=float(g["fs"]), mode="sf")
+                          fs=float(g["fs"]), mode=(sys.argv[2] if len(sys.argv) > 2 else "sf"),
+                          c_lp=len(sys.argv) > 2 and sys.argv[2] == "hpn")
     rng = np.random.default_rng(0)
     shapes = {"reflection_raw": (B, F, 22), "table_pos_raw": (B, F), "voiced_gain_raw": (B, F),
               "noise_gain_raw": (B, F), "h_gain_raw": (B, F),
@@ -30,8 +31,12 @@ def main():
     noise = torch.randn(B, n_out, device=dev)
     target = torch.randn(B, n_out, device=dev)
 
+    cf = (torch.tensor(decoder.stable_c_frames(B, F), dtype=torch.float32, device=dev)
+          if dec.c_lp else None)
+    f0 = torch.tensor(f0, dtype=torch.float64, device=dev)
+
     def step():
-        y = dec.render(p, n_out, noise, f0)
+        y = dec.render(p, n_out, noise, f0, cf)
         decoder.mss_loss(y, target).sum().backward()
 
     for _ in range(3):
@@ -41,7 +46,7 @@ def main():
                                             torch.profiler.ProfilerActivity.CUDA]) as prof:
         step()
         torch.cuda.synchronize()
-    print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25))
+    print(prof.key_averages().table(sort_by="self_cuda_time_total", row_limit=30))
 
 
 if __name__ == "__main__":
