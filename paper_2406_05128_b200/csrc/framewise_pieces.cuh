@@ -26,7 +26,9 @@
 // The adjoint of a TI all-pole filter is the same all-pole filter on
 // reversed time (ge(k) = g(k) - sum_i a_i ge(k+i), lpc.py:176-195), so the
 // backward runs passes 1 and carry on the reversed pieces with the same
-// impulse response; its pass 2 is the push-form adjoint (as k_fw_backward),
+// impulse response (the forward saves its tail per frame in the caller's
+// aux buffer, so the backward's pass 1 runs one chain); its pass 2 is the
+// push-form adjoint (as k_fw_backward),
 // which also accumulates ga[c] = sum_k ge(k) s(k-1-c) against the saved
 // frame outputs and writes gew = window * ge.
 //
@@ -36,6 +38,10 @@
 // carry adds one rounding level), so the plans that must stay bit-identical
 // to lp_forward_ti (one rectangular frame) keep those kernels.
 
+// TVLP_FW_P: pieces per frame (4; 8 is faster but its longer fp32 carry
+// chain misses the parity bar on a resonant golden frame).  TVLP_FW_CARRY64:
+// 1 = the carry's dot products in fp64, 2 = only its exit sums (both pass
+// at P=8 and are slower than P=4 in fp32: measured).
 #ifndef TVLP_FW_P
 #define TVLP_FW_P 4
 #endif
