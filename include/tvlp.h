@@ -234,6 +234,39 @@ int tvlp_framewise_backward_ex(int32_t dtype, const void* grad_out, const void* 
                                int32_t M, int32_t frame_size, int32_t hop, void* workspace,
                                size_t workspace_bytes, void* stream);
 
+/* The decoder pieces around the LP, float32.
+ *
+ * tvlp_wavetable_osc: the wavetable oscillator of source.py:224-318
+ * (oscillator_phase -> upsample_linear(pos, hop*os) -> wavetable_read ->
+ * decimate_fir) in one kernel; replaces the four taped ops of
+ * source.py:294-318 (wavetable_osc).  f0_frames [B, F] float64 (validated by
+ * the caller: 0 <= f0 < fs/2, source.py:230-233), pos_frames [B, F] table
+ * positions (clipped to [0, K-1] inside), tables [K, L], taps [ntaps] (the
+ * odd-length decimation lowpass, design_lowpass), sig [B, n_out];
+ * F = (n_out*os - 1) / (hop*os) + 1; os = 4 (the reference default).
+ * tvlp_wavetable_osc_vjp: grad_pos [B, F] from grad_sig [B, n_out] (f0 is not
+ * differentiated, source.py:301-303); workspace: 2*B*F floats. */
+int tvlp_wavetable_osc(const double* f0_frames, const float* pos_frames, const float* tables,
+                       int32_t K, int32_t L, const float* taps, int32_t ntaps, float* sig,
+                       int64_t B, int64_t n_out, int64_t F, int32_t hop, int32_t oversample,
+                       double fs, void* stream);
+int tvlp_wavetable_osc_vjp(const double* f0_frames, const float* pos_frames, const float* tables,
+                           int32_t K, int32_t L, const float* taps, int32_t ntaps,
+                           const float* grad_sig, float* grad_pos, float* workspace, int64_t B,
+                           int64_t n_out, int64_t F, int32_t hop, int32_t oversample, double fs,
+                           void* stream);
+/* The per-item causal global FIR (source.py:445-466, _fw_global_fir /
+ * _vjp_global_fir): y[b, n] = sum_{k<m} taps[b, k] x[b, n-k]; x, y [B, n],
+ * taps [B, m], 1 <= m <= 1024.  The VJP writes grad_x [B, n] and/or
+ * grad_taps [B, m] (either nullable); workspace: tvlp_global_fir_workspace
+ * bytes (the per-tile tap partials, reduced in a fixed order). */
+int tvlp_global_fir(const float* x, const float* taps, float* y, int64_t B, int64_t n, int32_t m,
+                    void* stream);
+size_t tvlp_global_fir_workspace(int64_t B, int64_t n, int32_t m);
+int tvlp_global_fir_vjp(const float* grad_y, const float* x, const float* taps, float* grad_x,
+                        float* grad_taps, void* workspace, size_t workspace_bytes, int64_t B,
+                        int64_t n, int32_t m, void* stream);
+
 /* Instrumentation (bench.py): number of kernels this library has launched,
  * and optional CUDA-event timing of every launch (off by default; when on,
  * each launch is bracketed by two events on its stream).  tvlp_profile_dump

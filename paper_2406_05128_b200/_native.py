@@ -89,6 +89,13 @@ _SIGS = [
      [_I32, _P, _P, _P, _D, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _P, _SZ, _P]),
     ("tvlp_framewise_backward_ex", ctypes.c_int,
      [_I32, _P, _P, _P, _D, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _P, _SZ, _P]),
+    ("tvlp_wavetable_osc", ctypes.c_int,
+     [_P, _P, _P, _I32, _I32, _P, _I32, _P, _I64, _I64, _I64, _I32, _I32, _D, _P]),
+    ("tvlp_wavetable_osc_vjp", ctypes.c_int,
+     [_P, _P, _P, _I32, _I32, _P, _I32, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _D, _P]),
+    ("tvlp_global_fir", ctypes.c_int, [_P, _P, _P, _I64, _I64, _I32, _P]),
+    ("tvlp_global_fir_workspace", _SZ, [_I64, _I64, _I32]),
+    ("tvlp_global_fir_vjp", ctypes.c_int, [_P, _P, _P, _P, _P, _P, _SZ, _I64, _I64, _I32, _P]),
     ("tvlp_launch_count", _I64, []),
     ("tvlp_refined_sequences", _I64, []),
     ("tvlp_profile_enable", None, [_I32]),
@@ -128,7 +135,8 @@ def load(path=None):
 
 
 _PURE = ("tvlp_workspace_bytes", "tvlp_carry_elems", "tvlp_max_order",
-         "tvlp_framewise_aux_elems", "tvlp_framewise_nframes", "tvlp_subchunk_len")
+         "tvlp_framewise_aux_elems", "tvlp_framewise_nframes", "tvlp_subchunk_len",
+         "tvlp_global_fir_workspace")
 
 
 def on_device(device):

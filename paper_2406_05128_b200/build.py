@@ -21,7 +21,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libtvlp_b200.so")
 OBJDIR = os.path.join(LIBDIR, "obj")
-UNITS = ["scan_kernels.cu", "chain_kernels.cu", "framewise.cu", "stepup.cu", "capi.cu"]
+UNITS = ["scan_kernels.cu", "chain_kernels.cu", "framewise.cu", "stepup.cu",
+         "decoder_kernels.cu", "capi.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -11,6 +11,7 @@
 
 #include "../../include/tvlp.h"
 #include "chain_launch.cuh"
+#include "decoder_launch.cuh"
 #include "framewise_launch.cuh"
 #include "lp_scan.cuh"
 
@@ -154,6 +155,11 @@ const int kGroup = env_int("TVLP_CARRY_GROUP", 32);
 // single-level "auto" refinement folded into the re-apply launch (1) or as a
 // separate per-sequence refine kernel before it (0)
 const int kFusedRefine = env_int("TVLP_FUSED_REFINE", 1);
+// frame-rate rows in the chained forward (k_fwd_chain<..., FR>): correct but
+// measured slower than basis -> carry -> apply at config 5 (88 vs 79 us; the
+// interpolating cursor costs registers: 255/thread); the chained adjoint with
+// frame-rate rows is the faster one (74 vs 87 us) and is the default
+const int kFrFwdChain = env_int("TVLP_FR_FWD_CHAIN", 0);
 struct Levels {
     int L = 1;
     int64_t n[8] = {};
@@ -458,10 +464,11 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
     // hierarchical chains are always checked: their group products are fp32)
     const bool hier = h.lv.L > 1;
     const bool refine = sizeof(IO) == 4 && (prec == kPrecAuto || hier);
-    // the chained single-pass forward (chain.cuh): fp32 I/O, sample-rate rows,
-    // one carry level, fp32 chains
+    // the chained single-pass forward (chain.cuh): fp32 I/O, sample-rate rows
+    // or frame-rate rows interpolated in the kernels, one carry level, fp32
+    // chains
     const bool f32 = std::is_same<IO, float>::value;
-    const bool chain = f32 && !frames && !reuse_tape && !hier &&
+    const bool chain = f32 && (!frames || (native_fr && kFrFwdChain)) && !reuse_tape && !hier &&
                        (prec == kPrecAuto || prec == kPrecF32Chains) && chain_supported(p.Mp);
     IO* xend = (refine || (f32 && need) || chain) ? static_cast<IO*>(c.take(nsc * mp * sz)) : nullptr;
     void* ctl = (f32 && (need || chain)) ? c.take(chain_ctl_bytes(p.B, p.nsub, p.Mp)) : nullptr;
@@ -521,7 +528,8 @@ int forward_impl(bool ti, const void* e, const void* A, const void* zi, void* s,
         if (chain) {
             ChainFwdCall cc{ti, 1, {}, p.Mp, phiz, fflags, xin, xend,
                             nonfinite, ctl, prec == kPrecAuto ? 1 : 0, g};
-            cc.grp[0] = ChainGroup{e_p, A_p, zi_p, s_p, p.B};
+            cc.grp[0] = ChainGroup{e_p, frames ? nullptr : A_p, zi_p, s_p, p.B};
+            cc.fr = frames ? fr : nullptr;
             TVLP_RUN("basis", 2, st, (launch_fwd_chain(p.Mp, cc, st, 0)));
             TVLP_RUN("fwd_chain", 1, st, (launch_fwd_chain(p.Mp, cc, st, 1)));
             if (packed) TVLP_CK(unpack<IO>(ps, s, p.B, p.T, 1, p.Tp, 1, st));
@@ -626,7 +634,7 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
     // the chained single-pass adjoint (chain.cuh): fp32, sample-rate rows, one
     // carry level, the forward's tape, no segment boundary terms
     const bool f32 = std::is_same<IO, float>::value;
-    const bool chain = f32 && !frames && carry != nullptr && !hier && !mu_in && !grad_zi &&
+    const bool chain = f32 && (!frames || native_fr) && carry != nullptr && !hier && !mu_in && !grad_zi &&
                        (prec == kPrecAuto || prec == kPrecF32Chains) && chain_supported(p.Mp);
     IO* kout = (refine || grad_zi || need || chain) ? static_cast<IO*>(c.take(nsc * mp * sz))
                                                     : nullptr;
@@ -700,7 +708,8 @@ int backward_impl(bool ti, const void* gs, const void* A, const void* s, const v
             const int* inherit = reinterpret_cast<const int*>(carry + tape_body(p));
             ChainBwdCall cc{ti, 1, {}, h.tape, inherit, nu, mu, kout, ctl,
                             prec == kPrecAuto ? 1 : 0, g};
-            cc.grp[0] = ChainGroup{gs_p, A_p, nullptr, ge_p, p.B};
+            cc.grp[0] = ChainGroup{gs_p, frames ? nullptr : A_p, nullptr, ge_p, p.B};
+            cc.fr = frk;
             TVLP_RUN("adjoint_zs", 2, st, (launch_bwd_chain(p.Mp, cc, st, 0)));
             TVLP_RUN("bwd_chain", 1, st, (launch_bwd_chain(p.Mp, cc, st, 1)));
             chained = true;
@@ -1065,6 +1074,94 @@ int tvlp_last_cuda_error(void) { return g_last_cuda; }
 int32_t tvlp_max_order(void) { return kMaxOrder; }
 
 int64_t tvlp_launch_count(void) { return g_launches.load(); }
+
+// ---------------------------------------------------------------- decoder pieces
+static int osc_geo(const double* f0, const float* pos, const float* tab, int32_t K, int32_t L,
+                   const float* taps, int32_t nt, int64_t B, int64_t n_out, int64_t F,
+                   int32_t hop, int32_t os, double fs, OscGeo* g) {
+    if (!f0 || !pos || !tab || !taps || K < 1 || L < 2 || nt < 1 || (nt % 2) == 0 || B < 0 ||
+        n_out < 1 || hop < 1 || os != 4 || !(fs > 0.0))
+        return TVLP_ERR_ARG;
+    const int64_t n_os = n_out * os, hop_os = (int64_t)hop * os;
+    if (F != (n_os - 1) / hop_os + 1 || hop_os > (1 << 20) || nt > 4096) return TVLP_ERR_ARG;
+    *g = OscGeo{B, n_out, F, n_os, hop, (int)hop_os, K, L, nt, (nt - 1) / 2, 1.0 / (fs * os),
+                1.0 / (double)hop_os, 1.0f / (float)hop_os};
+    return TVLP_OK;
+}
+
+int tvlp_wavetable_osc(const double* f0_frames, const float* pos_frames, const float* tables,
+                       int32_t K, int32_t L, const float* taps, int32_t ntaps, float* sig,
+                       int64_t B, int64_t n_out, int64_t F, int32_t hop, int32_t oversample,
+                       double fs, void* stream) {
+    OscGeo g;
+    int rc = osc_geo(f0_frames, pos_frames, tables, K, L, taps, ntaps, B, n_out, F, hop,
+                     oversample, fs, &g);
+    if (rc != TVLP_OK) return rc;
+    if (!sig) return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("osc_fwd", 1, st, [&] {
+        return launch_osc_fwd(f0_frames, pos_frames, tables, taps, sig, g, oversample, st);
+    }));
+    return TVLP_OK;
+}
+
+int tvlp_wavetable_osc_vjp(const double* f0_frames, const float* pos_frames, const float* tables,
+                           int32_t K, int32_t L, const float* taps, int32_t ntaps,
+                           const float* grad_sig, float* grad_pos, float* workspace, int64_t B,
+                           int64_t n_out, int64_t F, int32_t hop, int32_t oversample, double fs,
+                           void* stream) {
+    OscGeo g;
+    int rc = osc_geo(f0_frames, pos_frames, tables, K, L, taps, ntaps, B, n_out, F, hop,
+                     oversample, fs, &g);
+    if (rc != TVLP_OK) return rc;
+    if (!grad_sig || !grad_pos || !workspace) return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("osc_vjp", 2, st, [&] {
+        return launch_osc_vjp(f0_frames, pos_frames, tables, taps, grad_sig, workspace, grad_pos,
+                              g, oversample, st);
+    }));
+    return TVLP_OK;
+}
+
+int tvlp_global_fir(const float* x, const float* taps, float* y, int64_t B, int64_t n, int32_t m,
+                    void* stream) {
+    if (!x || !taps || !y || B < 0 || n < 0 || m < 1 || m > 1024) return TVLP_ERR_ARG;
+    if (B == 0 || n == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("global_fir", 1, st, [&] { return launch_fir(x, taps, y, B, n, m, false, st); }));
+    return TVLP_OK;
+}
+
+size_t tvlp_global_fir_workspace(int64_t B, int64_t n, int32_t m) {
+    if (B < 0 || n < 0 || m < 1) return 0;
+    return fir_taps_part_elems(B, n, m) * sizeof(float);
+}
+
+int tvlp_global_fir_vjp(const float* grad_y, const float* x, const float* taps, float* grad_x,
+                        float* grad_taps, void* workspace, size_t workspace_bytes, int64_t B,
+                        int64_t n, int32_t m, void* stream) {
+    if (!grad_y || !x || !taps || B < 0 || n < 0 || m < 1 || m > 1024) return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        if (grad_taps) TVLP_CK(cudaMemsetAsync(grad_taps, 0, B * m * sizeof(float), st));
+        return TVLP_OK;
+    }
+    if (grad_x)
+        TVLP_CK(tracked("global_fir_vjp_x", 1, st,
+                        [&] { return launch_fir(grad_y, taps, grad_x, B, n, m, true, st); }));
+    if (grad_taps) {
+        if (!workspace || workspace_bytes < tvlp_global_fir_workspace(B, n, m))
+            return TVLP_ERR_WORKSPACE;
+        TVLP_CK(tracked("global_fir_vjp_taps", 2, st, [&] {
+            return launch_fir_taps(grad_y, x, static_cast<float*>(workspace), grad_taps, B, n, m,
+                                   st);
+        }));
+    }
+    return TVLP_OK;
+}
 
 int64_t tvlp_refined_sequences(void) {
     return (int64_t)(refined_sequences() + chain_refined_sequences());

@@ -195,11 +195,16 @@ struct UnitLane {
 // Lanes l < L re-run the recursion of sub-chunk g0 + l from xin[l] (shared,
 // rows of MP4), write s through the unit's output box, and return the end
 // state in `xe` (registers, x[i] = s(t1 - i)).
-template <int M, int U, int NST, bool TI>
+// FR: frame-rate rows interpolated in registers by
+// a FrameCursor (lp_scan.cuh) instead of streamed; fs the frame source, fb the
+// sequence within it, tl0 the time of the unit's first sub-chunk.
+template <int M, int U, int NST, bool TI, bool FR = false>
 __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int64_t g0, int L,
                                               int nwin, unsigned char* sm, uint64_t* bars,
                                               const float* xin, float (&xe)[M], bool& finite,
-                                              const float* ati) {
+                                              const float* ati,
+                                              const FrameSrc<float>* fs = nullptr, int64_t fb = 0,
+                                              int64_t tl0 = 0) {
     using S = UnitLane<M, U, NST>;
     constexpr int W = S::W;
     constexpr int MR = (M + W - 1) / W * W;
@@ -208,7 +213,10 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
     const int lane = threadIdx.x & 31;
     const int ln = lane < U ? lane : U - 1;  // lanes past the unit read a valid row, never write
     const bool active = lane < L;
-    const uint32_t tx = TI ? (uint32_t)L * S::XROW * 4u : S::tx(L);
+    const uint32_t tx = (TI || FR) ? (uint32_t)L * S::XROW * 4u : S::tx(L);
+    FrameCursor<float, FR ? M : 1> cur;
+    const float inv_hop = FR ? 1.f / (float)fs->hop : 0.f;
+    const int64_t tlane = tl0 + (int64_t)lane * (nwin * W);  // this lane's sub-chunk start
     const uint64_t pol = policy_evict_first();
     float ar[TI ? M : 1];  // TI: the sequence's constant row
     if constexpr (TI) {
@@ -225,7 +233,8 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
             const int st = k % NST;
             unsigned char* base = sm + st * S::STAGE;
             mbar_arrive_expect_tx(&bars[st], tx);
-            if (!TI) tma_load_2d_hint(base, &mp.A[which], k * W * M, (int)g0, &bars[st], pol);
+            if (!TI && !FR)
+                tma_load_2d_hint(base, &mp.A[which], k * W * M, (int)g0, &bars[st], pol);
             tma_load_2d_hint(base + S::A_BYTES, &mp.X[which], k * W, (int)g0, &bars[st], pol);
         }
     };
@@ -250,17 +259,22 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
                 float ev[W], ov[W];
 #pragma unroll
                 for (int u = 0; u < W; ++u) ev[u] = er[u];
+                if constexpr (FR) cur.window(*fs, fb, tlane + (int64_t)k * W);
                 // rows are loaded one step ahead (issued before this step's
                 // output store, so no shared-memory ordering holds them back)
                 float an[M];
-                if constexpr (!TI) load_row_at<float, M>(Ar, an, (ln * S::AROW) * 4);
+                if constexpr (!TI && !FR) load_row_at<float, M>(Ar, an, (ln * S::AROW) * 4);
 #pragma unroll
                 for (int u = 0; u < W; ++u) {
                     const int pos = w * W + u;
                     float a[M];
+                    if constexpr (FR) {
+                        cur.row(*fs, inv_hop, u, a);
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < M; ++i) a[i] = TI ? ar[TI ? i : 0] : an[i];
-                    if (!TI && u + 1 < W)
+                        for (int i = 0; i < M; ++i) a[i] = TI ? ar[TI ? i : 0] : an[i];
+                    }
+                    if (!TI && !FR && u + 1 < W)
                         load_row_at<float, M>(Ar + (u + 1) * M, an, (ln * S::AROW + (u + 1) * M) * 4);
                     float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
 #pragma unroll
@@ -299,16 +313,21 @@ __device__ __forceinline__ void unit_fwd_pass(const UnitMaps& mp, int which, int
 // MODE 0: zero-state adjoint of sub-chunk g0 + l (lam starts at 0), returns
 // nu_l in lam.  MODE 1: from lam (the carry into the sub-chunk from the
 // right), writes grad_e through the unit's output box; returns the carry-out.
-template <int M, int U, int NST, int MODE, bool TI>
+template <int M, int U, int NST, int MODE, bool TI, bool FR = false>
 __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int64_t g0, int L,
                                               int nwin, unsigned char* sm, uint64_t* bars,
                                               float (&lam)[M], const float* ati,
-                                              float* gmax = nullptr) {
+                                              float* gmax = nullptr,
+                                              const FrameSrc<float>* fs = nullptr, int64_t fb = 0,
+                                              int64_t tl0 = 0) {
     using S = UnitLane<M, U, NST>;
     constexpr int W = S::W;
     const int lane = threadIdx.x & 31;
     const int ln = lane < U ? lane : U - 1;  // lanes past the unit read a valid row, never write
-    const uint32_t tx = TI ? (uint32_t)L * S::XROW * 4u : S::tx(L);
+    const uint32_t tx = (TI || FR) ? (uint32_t)L * S::XROW * 4u : S::tx(L);
+    FrameCursor<float, FR ? M : 1> cur;
+    const float inv_hop = FR ? 1.f / (float)fs->hop : 0.f;
+    const int64_t tlane = tl0 + (int64_t)lane * (nwin * W);  // this lane's sub-chunk start
     const uint64_t pol = MODE == 0 ? policy_evict_last() : policy_evict_first();
     float ar[TI ? M : 1];  // TI: the sequence's constant row
     if constexpr (TI) {
@@ -326,7 +345,8 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
             unsigned char* base = sm + st * S::STAGE;
             const int wr = nwin - 1 - k;
             mbar_arrive_expect_tx(&bars[st], tx);
-            if (!TI) tma_load_2d_hint(base, &mp.A[which], wr * W * M, (int)g0, &bars[st], pol);
+            if (!TI && !FR)
+                tma_load_2d_hint(base, &mp.A[which], wr * W * M, (int)g0, &bars[st], pol);
             tma_load_2d_hint(base + S::A_BYTES, &mp.X[which], wr * W, (int)g0, &bars[st], pol);
         }
     };
@@ -343,17 +363,22 @@ __device__ __forceinline__ void unit_adj_pass(const UnitMaps& mp, int which, int
         float gv[W], ov[W];
 #pragma unroll
         for (int u = 0; u < W; ++u) gv[u] = xr[u];
+        if constexpr (FR) cur.window(*fs, fb, tlane + (int64_t)(nwin - 1 - k) * W);
         // rows are loaded one step ahead (issued before this step's output
         // store, so no shared-memory ordering holds them back)
         float an[M];
-        if constexpr (!TI)
+        if constexpr (!TI && !FR)
             load_row_at<float, M>(Ar + (W - 1) * M, an, (ln * S::AROW + (W - 1) * M) * 4);
 #pragma unroll
         for (int u = W - 1; u >= 0; --u) {
             float a[M];
+            if constexpr (FR) {
+                cur.row(*fs, inv_hop, u, a);
+            } else {
 #pragma unroll
-            for (int i = 0; i < M; ++i) a[i] = TI ? ar[TI ? i : 0] : an[i];
-            if (!TI && u > 0)
+                for (int i = 0; i < M; ++i) a[i] = TI ? ar[TI ? i : 0] : an[i];
+            }
+            if (!TI && !FR && u > 0)
                 load_row_at<float, M>(Ar + (u - 1) * M, an, (ln * S::AROW + (u - 1) * M) * 4);
             const float l0 = lam[0] + gv[u];
             ov[u] = l0;
@@ -461,6 +486,7 @@ struct GroupIdx {
 
 struct ChainFwdArgs {
     UnitMaps mp[kMaxGroups];  // A, e, s lane views of each group
+    FrameSrc<float> fs;       // FR: the frame rows (one group)
     GroupIdx gi;
     const float* Ag[kMaxGroups];  // TI: the constant rows [B_g][Mp] of each group
     const float* zig[kMaxGroups]; // nullable initial states [B_g][zs]
@@ -487,6 +513,7 @@ struct ChainFwdArgs {
 
 struct ChainBwdArgs {
     UnitMaps mp[kMaxGroups];  // A, g_s, g_e lane views of each group
+    FrameSrc<float> fs;       // FR: the frame rows (one group)
     GroupIdx gi;
     const float* Ag[kMaxGroups];  // TI: the constant rows [B_g][Mp]
     CUtensorMap Tw;        // carry tape, box [8][M][MP4] from row 0 (W rows)
@@ -554,7 +581,7 @@ struct BwdChainSmem {
 // detection threshold (tol) is far too loose a stopping point.  One warp.
 constexpr int kRefineIters = 4;
 constexpr float kRefineTarget = 3e-7f;
-template <int M, int NST, bool TI>
+template <int M, int NST, bool TI, bool FR>
 __device__ bool refine_sequence_fwd(const ChainFwdArgs& a, int64_t b, unsigned char* sm,
                                     uint64_t* bars, float* xs, float* xb, bool force,
                                     float xmax) {
@@ -600,8 +627,9 @@ __device__ bool refine_sequence_fwd(const ChainFwdArgs& a, int64_t b, unsigned c
             __syncwarp();
             float xe[M];
             bool fin = true;
-            unit_fwd_pass<M, U, NST, TI>(a.mp[grp], L == U ? 0 : 1, vbase + (int64_t)ru * U, L, nwin,
-                                         sm, bars, xs, xe, fin, arow);
+            unit_fwd_pass<M, U, NST, TI, FR>(a.mp[grp], L == U ? 0 : 1, vbase + (int64_t)ru * U, L,
+                                             nwin, sm, bars, xs, xe, fin, arow, &a.fs,
+                                             b - a.gi.gB0[grp], (int64_t)ru * U * a.g.Ls);
             if (lane < L) {
                 const bool has_next = ru * U + lane + 1 < nsub;
 #pragma unroll
@@ -626,7 +654,7 @@ __device__ bool refine_sequence_fwd(const ChainFwdArgs& a, int64_t b, unsigned c
 // Backward: e_{j-1} = Phi_j^T e_j + d_j, d_j = K_j - Mu_{j-1} (k_refine_bwd),
 // Mu += e; then the adjoint re-application of every unit of the sequence,
 // repeated like the forward.
-template <int M, int NST, bool TI>
+template <int M, int NST, bool TI, bool FR>
 __device__ bool refine_sequence_bwd(const ChainBwdArgs& a, int64_t b, unsigned char* sm,
                                     uint64_t* bars, float* xb, bool force, float xmax) {
     using TP = Tape<M>;
@@ -669,8 +697,9 @@ __device__ bool refine_sequence_bwd(const ChainBwdArgs& a, int64_t b, unsigned c
             float lam[M];
 #pragma unroll
             for (int i = 0; i < M; ++i) lam[i] = lane < L ? a.Mu[(g0 + lane) * MP4 + i] : 0.f;
-            unit_adj_pass<M, U, NST, 1, TI>(a.mp[grp], L == U ? 0 : 1, vbase + (int64_t)ru * U, L,
-                                            nwin, sm, bars, lam, arow);
+            unit_adj_pass<M, U, NST, 1, TI, FR>(a.mp[grp], L == U ? 0 : 1, vbase + (int64_t)ru * U, L,
+                                                nwin, sm, bars, lam, arow, nullptr, &a.fs,
+                                                b - a.gi.gB0[grp], (int64_t)ru * U * a.g.Ls);
             if (lane < L) {
                 const bool has_prev = ru * U + lane > 0;
                 const float* prev = a.Mu + (g0 + lane - 1) * MP4;
@@ -759,7 +788,7 @@ k_adj_zs_units(const __grid_constant__ ChainBwdArgs a) {
 }
 
 // ---------------------------------------------------------------- forward kernel
-template <int M, int NWB, int NST, bool TI>
+template <int M, int NWB, int NST, bool TI, bool FR = false>
 __global__ void __launch_bounds__((NWB + 1) * 32, NWB > 0 ? 1 : 2)
 k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
     grid_dep_wait();
@@ -859,8 +888,9 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
         tt[3] = gtime();
         // 5. re-run the unit's sub-chunks from their carried-in states
         float xe[M];
-        unit_fwd_pass<M, U, NST, TI>(a.mp[grp], L == U ? 0 : 1, r0, L, nwin, sa, abars, xs, xe,
-                                     finite, TI ? a.Ag[grp] + bl * M : nullptr);
+        unit_fwd_pass<M, U, NST, TI, FR>(a.mp[grp], L == U ? 0 : 1, r0, L, nwin, sa, abars, xs, xe,
+                                         finite, TI ? a.Ag[grp] + bl * M : nullptr, &a.fs, bl,
+                                         (int64_t)ru * U * a.g.Ls);
         tt[4] = gtime();
         trace_rec(a.tr, (NWB > 0 ? (unsigned)(B * ((nsub + BC::S - 1) / BC::S)) : 0u) + t, 2, t, tt);
         // 6. boundary defects (precision "auto")
@@ -899,7 +929,7 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
                 const float xmax = __uint_as_float(ld_acquire_u32(&a.dstat[3 * b + 1]));
                 // defects above tol are refined (the boundary-defect check)
                 if (dmax > a.tol * xmax) {
-                    const bool done = refine_sequence_fwd<M, NST, TI>(
+                    const bool done = refine_sequence_fwd<M, NST, TI, FR>(
                         a, b, sa, abars, xs, xb, dmax > a.tol * xmax, xmax);
                     if (done && lane == 0) {
                         a.fflags[b] = 1;
@@ -917,7 +947,7 @@ k_fwd_chain(const __grid_constant__ ChainFwdArgs a) {
 }
 
 // ---------------------------------------------------------------- backward kernel
-template <int M, int NST, bool ZS, bool TI>
+template <int M, int NST, bool ZS, bool TI, bool FR = false>
 __global__ void __launch_bounds__(32)
 k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
     grid_dep_wait();
@@ -969,7 +999,8 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
             // 1. zero-state adjoint -> nu
 #pragma unroll
             for (int i = 0; i < M; ++i) lam[i] = 0.f;
-            unit_adj_pass<M, U, NST, 0, TI>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow);
+            unit_adj_pass<M, U, NST, 0, TI, FR>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow,
+                                                nullptr, &a.fs, bl, (int64_t)ru * U * a.g.Ls);
             if (lane < L) {
 #pragma unroll
                 for (int i = 0; i < M; ++i) nus[lane * MP4 + i] = lam[i];
@@ -993,7 +1024,8 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
         if (lane < M) nus[lane] = mu;
         __syncwarp();
         float gmx = 0.f;
-        unit_adj_pass<M, U, NST, 1, TI>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow, &gmx);
+        unit_adj_pass<M, U, NST, 1, TI, FR>(a.mp[grp], which, r0, L, nwin, sl, bars, lam, arow,
+                                            &gmx, &a.fs, bl, (int64_t)ru * U * a.g.Ls);
         tt[4] = gtime();
         trace_rec(a.tr, t, 3, t, tt);
         if (a.refine) {
@@ -1034,7 +1066,7 @@ k_bwd_chain(const __grid_constant__ ChainBwdArgs a) {
                                  (a.inherit != nullptr && a.inherit[b] != 0);
                 if (bad) {
                     const bool done =
-                        refine_sequence_bwd<M, NST, TI>(a, b, sl, bars, xb, bad, xmax);
+                        refine_sequence_bwd<M, NST, TI, FR>(a, b, sl, bars, xb, bad, xmax);
                     if (done && lane == 0) atomicAdd(&g_chain_refined, 1ull);
                 }
             }

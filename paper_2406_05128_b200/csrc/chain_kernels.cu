@@ -193,7 +193,9 @@ cudaError_t fwd_chain_impl(const ChainFwdCall& c, cudaStream_t st, int phase) {
     constexpr int NWB = TVLP_CHAIN_BASIS_WARPS, NST = TVLP_CHAIN_FWD_STAGES;
     using SM = FwdChainSmem<M, NWB, NST>;
     constexpr int MP4 = Tape<M>::MP4;
-    auto k = k_fwd_chain<M, NWB, NST, TI && NWB == 0>;
+    const bool fr = c.fr != nullptr;  // frame-rate rows (TV, one group)
+    auto k = fr ? k_fwd_chain<M, NWB, NST, false, true> : k_fwd_chain<M, NWB, NST, TI && NWB == 0>;
+    if (fr && (TI || c.ng != 1 || NWB > 0)) return cudaErrorInvalidValue;
     cudaError_t err = set_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
     if (c.ng < 1 || c.ng > kMaxGroups || (NWB > 0 && c.ng != 1)) return cudaErrorInvalidValue;
@@ -207,7 +209,7 @@ cudaError_t fwd_chain_impl(const ChainFwdCall& c, cudaStream_t st, int phase) {
         if (err != cudaSuccess || NWB > 0) return err;
         if (c.ng == 1)
             return launch_basis<float>(M, TI, kPrecF32Chains, c.grp[0].x, c.grp[0].A, c.tape, c.g,
-                                       st);
+                                       st, c.fr);
         // groups: one launch over all of them (each lane picks its group)
         using BC = Basis4Cfg<M, TI>;
         auto kb = k_basis4_groups<M, TI>;
@@ -230,12 +232,13 @@ cudaError_t fwd_chain_impl(const ChainFwdCall& c, cudaStream_t st, int phase) {
     a.gi = group_index(c.ng, c.grp);
     for (int i = 0; i < c.ng; ++i) {
         const ScanArgs gg = group_args(c.g, c.grp[i].B);
-        err = unit_maps<M, SM::U, NST>(a.mp[i], TI ? nullptr : c.grp[i].A, c.grp[i].x, c.grp[i].y,
-                                       gg, u);
+        err = unit_maps<M, SM::U, NST>(a.mp[i], (TI || fr) ? nullptr : c.grp[i].A, c.grp[i].x,
+                                       c.grp[i].y, gg, u);
         if (err != cudaSuccess) return err;
         a.Ag[i] = c.grp[i].A;
         a.zig[i] = c.grp[i].zi;
     }
+    if (fr) a.fs = *c.fr;
     err = view_tapes(&a.Tz, c.tape, M, MP4, Tape<M>::SIZE, (uint64_t)c.g.B * c.g.nsub, M + 1);
     if (err != cudaSuccess) return err;
     a.e = c.grp[0].x;
@@ -278,7 +281,9 @@ cudaError_t bwd_chain_impl(const ChainBwdCall& c, cudaStream_t st, int phase) {
     constexpr bool ZS = TVLP_CHAIN_BWD_ZS != 0;
     using SM = BwdChainSmem<M, NST, ZS>;
     constexpr int MP4 = Tape<M>::MP4;
-    auto k = k_bwd_chain<M, NST, ZS, TI>;
+    const bool fr = c.fr != nullptr;  // frame-rate rows (TV, one group)
+    auto k = fr ? k_bwd_chain<M, NST, ZS, false, true> : k_bwd_chain<M, NST, ZS, TI>;
+    if (fr && (TI || c.ng != 1)) return cudaErrorInvalidValue;
     cudaError_t err = set_smem(k, SM::BYTES);
     if (err != cudaSuccess) return err;
     if (c.ng < 1 || c.ng > kMaxGroups) return cudaErrorInvalidValue;
@@ -293,7 +298,7 @@ cudaError_t bwd_chain_impl(const ChainBwdCall& c, cudaStream_t st, int phase) {
             // group; for several, one launch of unit warps over all of them
             if (c.ng == 1)
                 return launch_adjoint<float>(M, TI, 0, c.grp[0].x, c.grp[0].A, nullptr, c.Nu,
-                                             nullptr, nullptr, nullptr, c.g, st);
+                                             nullptr, nullptr, nullptr, c.g, st, c.fr);
             constexpr int UZ = 32, NZ = 3;
             const UnitGeo uz = chain_units_n(c.g.nsub, UZ);
             ChainBwdArgs z;
@@ -321,11 +326,12 @@ cudaError_t bwd_chain_impl(const ChainBwdCall& c, cudaStream_t st, int phase) {
     std::memset(&a, 0, sizeof(a));
     a.gi = group_index(c.ng, c.grp);
     for (int i = 0; i < c.ng; ++i) {
-        err = unit_maps<M, SM::U, NST>(a.mp[i], TI ? nullptr : c.grp[i].A, c.grp[i].x, c.grp[i].y,
-                                       group_args(c.g, c.grp[i].B), u);
+        err = unit_maps<M, SM::U, NST>(a.mp[i], (TI || fr) ? nullptr : c.grp[i].A, c.grp[i].x,
+                                       c.grp[i].y, group_args(c.g, c.grp[i].B), u);
         if (err != cudaSuccess) return err;
         a.Ag[i] = c.grp[i].A;
     }
+    if (fr) a.fs = *c.fr;
     err = view_tapes(&a.Tw, c.tape, M, MP4, Tape<M>::SIZE, (uint64_t)c.g.B * c.g.nsub, M);
     if (err != cudaSuccess) return err;
     a.Nu = c.Nu;

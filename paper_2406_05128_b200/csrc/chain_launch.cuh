@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "scan_launch.cuh"
+
 namespace tvlp {
 
 struct ScanArgs;
@@ -41,6 +43,7 @@ struct ChainFwdCall {
     void* ctl;         // chain_ctl_bytes() of workspace (zeroed by the launcher)
     int refine;
     const ScanArgs& g; // g.B: the total over the groups
+    const FrameSrc<float>* fr = nullptr;  // frame-rate rows interpolated in the kernels
 };
 
 struct ChainBwdCall {
@@ -56,6 +59,7 @@ struct ChainBwdCall {
     void* ctl;
     int refine;
     const ScanArgs& g;
+    const FrameSrc<float>* fr = nullptr;  // frame-rate rows interpolated in the kernels
 };
 
 UnitGeo chain_units(int nsub, bool fwd);

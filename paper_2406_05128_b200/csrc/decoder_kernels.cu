@@ -1,0 +1,500 @@
+// decoder_kernels.cu -- the two decoder pieces around the LP that profiled
+// hottest in the config-5 step (torch + cuDNN took
+// ~2.6 of its 6.2 ms: a float64 cumsum, table gathers, the x4 decimation
+// conv and its dgrad, the depthwise global FIR and its backward), float32:
+//
+//  * the wavetable oscillator (source.py:224-318): the table phase in float64
+//    (the frame-rate f0 track is linear inside a frame, so its running sum is a
+//    per-frame prefix plus a closed-form quadratic -- no sequential scan), the
+//    bilinear table read and the x`OS` windowed-sinc decimation in ONE kernel:
+//    the oversampled track only ever lives in shared memory.  Its VJP to the
+//    table-position frames (the only trainable input; f0 is not
+//    differentiated, source.py:301-303) recomputes the row difference and
+//    folds the transposed decimation, the read's VJP and the upsample VJP
+//    (params.py:135-145) into per-frame block sums, then one 2-term combine.
+//  * the per-item causal global FIR (source.py:445-466, y[n] = sum_k h[k]
+//    x[n-k]) and its VJP (grad_x: the correlation with h; grad_h[k] = sum_n
+//    g[n] x[n-k], per-tile partials reduced in a fixed order).
+//
+// Roofline: all of it is a few hundred MB of HBM per step and < 2 GFLOP of
+// FFMA; the kernels are sized so neither the gathers nor shared memory
+// bandwidth dominate (register-blocked FIR tiles: 31 LDS per 128 FFMA).
+#include "common.cuh"
+#include "decoder_launch.cuh"
+
+namespace tvlp {
+
+// ---------------------------------------------------------------- oscillator
+
+// sum over frame g's hop_os samples of the linear f0 track (params.py:107-117:
+// w = n / hop_os, the last frame held)
+__device__ __forceinline__ double frame_sum(const double* f0, int64_t F, int64_t g, int hop_os) {
+    const double a = f0[g], b = g + 1 < F ? f0[g + 1] : a;
+    return (double)hop_os * a + (b - a) * (0.5 * (double)(hop_os - 1));
+}
+
+// sum_{h < g} frame_sum(h), by one full warp
+__device__ double frame_prefix(const double* f0, int64_t F, int64_t g, int hop_os) {
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+#pragma unroll 8
+    for (int64_t h = lane; h < g; h += 32) s += frame_sum(f0, F, h, hop_os);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// phase (periods, mod 1, rounded to float32 like the torch path's .to(f32))
+// of oversampled sample n inside frame g whose prefix is P
+__device__ __forceinline__ float osc_phase(const double* f0, const OscGeo& g_, int64_t fr,
+                                           int n, double P) {
+    const double a = f0[fr];
+    const double d = fr + 1 < g_.F ? f0[fr + 1] - a : 0.0;
+    const double nn = (double)n;
+    const double cum = P + (nn + 1.0) * a + d * (nn * (nn + 1.0) * 0.5) * g_.inv_hop;
+    const double ph = cum * g_.inv_rate;
+    return (float)(ph - floor(ph));
+}
+
+// bilinear read (source.py:241-262, decoder._WavetableRead) -> (out, high - low)
+__device__ __forceinline__ float2 table_read(const float* __restrict__ tab, int K, int L,
+                                             float pos, float ph) {
+    const float p = fminf(fmaxf(pos, 0.f), (float)(K - 1));
+    const int r0 = min((int)floorf(p), K - 1);
+    const int r1 = min(r0 + 1, K - 1);
+    const float wr = __fsub_rn(p, (float)r0);
+    const float x = __fmul_rn(ph, (float)L);
+    const float fx = floorf(x);
+    int i0 = (int)fx;  // x in [0, L]: the phase is in [0, 1]
+    if (i0 >= L) i0 -= L;
+    const int i1 = i0 + 1 == L ? 0 : i0 + 1;
+    const float wi = __fsub_rn(x, fx), wi1 = __fsub_rn(1.f, wi);
+    const float low = __fadd_rn(__fmul_rn(wi1, __ldg(tab + r0 * L + i0)),
+                                __fmul_rn(wi, __ldg(tab + r0 * L + i1)));
+    const float high = __fadd_rn(__fmul_rn(wi1, __ldg(tab + r1 * L + i0)),
+                                 __fmul_rn(wi, __ldg(tab + r1 * L + i1)));
+    return make_float2(__fadd_rn(__fmul_rn(__fsub_rn(1.f, wr), low), __fmul_rn(wr, high)),
+                       __fsub_rn(high, low));
+}
+
+// the upsampled position track (decoder._Upsample forward)
+__device__ __forceinline__ float pos_track(const float* pos, const OscGeo& g_, int64_t fr, int n) {
+    const float w = fr == g_.F - 1 ? 0.f : __fmul_rn((float)n, g_.inv_hop_f);
+    const float a = pos[fr], b = fr + 1 < g_.F ? pos[fr + 1] : a;
+    return __fadd_rn(__fmul_rn(__fsub_rn(1.f, w), a), __fmul_rn(w, b));
+}
+
+constexpr int kOscThreads = 256;
+
+__host__ __device__ __forceinline__ int osc_taps_u4(int nt, int os) {
+    return ((nt + os - 1) / os + 3) & ~3;
+}
+// polyphase columns of one CTA's span: outputs t < hop read columns t + u, u < U4
+__host__ __device__ __forceinline__ int osc_span_cols(int hop, int u4) { return hop + u4; }
+
+// frames one CTA's oversampled span (at most NR samples) can touch
+__host__ __device__ __forceinline__ int osc_span_frames(int NR, int hop_os) {
+    return (NR / hop_os + 3) & ~1;  // even: the float rows after it stay 16-byte aligned
+}
+
+// One CTA per (frame f, item b): output samples [f*hop, f*hop + hop) need the
+// oversampled samples [OS*m0 + gd - (nt-1), OS*(m1-1) + gd]; they are computed
+// into shared memory in polyphase order (raw[r][v] = sample OS*v + r of the
+// span) so the decimation dot reads consecutive words across the warp.
+template <int OS>
+__global__ void __launch_bounds__(kOscThreads)
+k_osc_fwd(const double* __restrict__ f0, const float* __restrict__ pos,
+          const float* __restrict__ tab, const float* __restrict__ taps, float* __restrict__ sig,
+          OscGeo g) {
+    extern __shared__ __align__(16) unsigned char osc_sm[];
+    grid_dep_wait();
+    const int64_t f = blockIdx.x, b = blockIdx.y;
+    const int64_t m0 = f * g.hop;
+    const int nm = (int)min((int64_t)g.hop, g.n_out - m0);
+    if (nm <= 0) return;
+    const int64_t ilo = OS * m0 + g.gd - (g.nt - 1);
+    const int NR = OS * (nm - 1) + g.nt;
+    const int NRmax = OS * (g.hop - 1) + g.nt;
+    const int U4 = osc_taps_u4(g.nt, OS);           // taps per phase, padded to 4
+    const int NVp = osc_span_cols(g.hop, U4);        // columns per phase (zero padded)
+    double* Pf = reinterpret_cast<double*>(osc_sm);
+    float* hq = reinterpret_cast<float*>(Pf + osc_span_frames(NRmax, g.hop_os));  // [OS][U4]
+    float* raw = hq + OS * U4;                                                     // [OS][NVp]
+    const double* f0b = f0 + b * g.F;
+    const float* posb = pos + b * g.F;
+    const int64_t ia = ilo > 0 ? ilo : (int64_t)0, ib = min((int64_t)ilo + NR, g.n_os) - 1;
+    const int64_t gl = ia / g.hop_os, gh = ib / g.hop_os;
+    TVLP_ASSERT(gh - gl + 1 <= osc_span_frames(NRmax, g.hop_os));
+    if (threadIdx.x < 32) {
+        const double P0 = frame_prefix(f0b, g.F, gl, g.hop_os);
+        if (threadIdx.x == 0) {
+            double P = P0;
+            for (int64_t h = gl; h <= gh; ++h) {
+                Pf[h - gl] = P;
+                P += frame_sum(f0b, g.F, h, g.hop_os);
+            }
+        }
+    }
+    // polyphase taps: hq[r][u] = h[nt-1-(OS u + r)] (0 past the end)
+    for (int j = threadIdx.x; j < OS * U4; j += blockDim.x) {
+        const int r = j / U4, u = j % U4, q = OS * u + r;
+        hq[j] = q < g.nt ? taps[g.nt - 1 - q] : 0.f;
+    }
+    __syncthreads();
+    const int64_t gbase = gl * g.hop_os;
+    for (int idx = threadIdx.x; idx < OS * NVp; idx += blockDim.x) {
+        const int64_t i = ilo + idx;
+        float v = 0.f;
+        if (idx < NR && i >= 0 && i < g.n_os) {
+            const int loc = (int)(i - gbase);
+            const int k = loc / g.hop_os;
+            const int n = loc - k * g.hop_os;
+            const float ph = osc_phase(f0b, g, gl + k, n, Pf[k]);
+            v = table_read(tab, g.K, g.L, pos_track(posb, g, gl + k, n), ph).x;
+        }
+        raw[(idx % OS) * NVp + idx / OS] = v;
+    }
+    __syncthreads();
+    // sig[m0 + t] = sum_j h[j] raw_full[gd + OS(m0+t) - j] = sum_q h[nt-1-q] span[OS t + q]
+    //             = sum_r sum_u hq[r][u] raw[r][t + u]
+    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int r = 0; r < OS; ++r) {
+            const float* hr = hq + r * U4;
+            const float* xr = raw + r * NVp + t;
+            for (int u = 0; u < U4; u += 4) {
+                const float4 h4 = *reinterpret_cast<const float4*>(hr + u);
+                acc[0] = fmaf(h4.x, xr[u], acc[0]);
+                acc[1] = fmaf(h4.y, xr[u + 1], acc[1]);
+                acc[2] = fmaf(h4.z, xr[u + 2], acc[2]);
+                acc[3] = fmaf(h4.w, xr[u + 3], acc[3]);
+            }
+        }
+        sig[b * g.n_out + m0 + t] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    }
+}
+
+// VJP: one CTA per (frame f, item b) over the frame's oversampled samples i:
+// gr[i] = sum_m g[m] h[gd + OS m - i] (the transposed decimation,
+// source.py:285-291), times the row difference, reduced into the two block
+// sums of the upsample VJP: part[b][f] = (sum (1-w) gr*d, sum w gr*d).
+template <int OS>
+__global__ void __launch_bounds__(kOscThreads)
+k_osc_vjp(const double* __restrict__ f0, const float* __restrict__ pos,
+          const float* __restrict__ tab, const float* __restrict__ taps,
+          const float* __restrict__ gsig, float* __restrict__ part, OscGeo g) {
+    extern __shared__ __align__(16) unsigned char osc_sm[];
+    __shared__ float red[2][kOscThreads / 32];
+    __shared__ double Psh;
+    grid_dep_wait();
+    const int64_t f = blockIdx.x, b = blockIdx.y;
+    const int64_t i0 = f * g.hop_os;
+    const int ni = (int)min((int64_t)g.hop_os, g.n_os - i0);
+    const int U4 = osc_taps_u4(g.nt, OS);
+    // [OS][U4 + 4]: hp[j0][u] = h[j0 + OS u]; the lanes of a warp read OS rows
+    // at once, so rows are skewed by 4 words (distinct banks for LDS.128)
+    const int HS = U4 + 4;
+    float* hp = reinterpret_cast<float*>(osc_sm);
+    float* gs = hp + OS * HS;
+    const double* f0b = f0 + b * g.F;
+    const float* posb = pos + b * g.F;
+    // m range: floor((i0 - gd) / OS) .. (i0 + ni - 1 - gd + nt - 1) / OS
+    const int64_t d0 = i0 - g.gd;
+    const int64_t mb = d0 >= 0 ? d0 / OS : -((-d0 + OS - 1) / OS);
+    const int NG = (int)((i0 + ni - 1 - g.gd + g.nt - 1 - mb * OS) / OS) + 1;
+    if (threadIdx.x < 32) {
+        const double P = frame_prefix(f0b, g.F, f, g.hop_os);
+        if (threadIdx.x == 0) Psh = P;
+    }
+    for (int j = threadIdx.x; j < OS * U4; j += blockDim.x) {
+        const int q = (j / U4) + OS * (j % U4);
+        hp[(j / U4) * HS + j % U4] = q < g.nt ? taps[q] : 0.f;
+    }
+    for (int v = threadIdx.x; v < NG + U4; v += blockDim.x) {
+        const int64_t m = mb + v;
+        gs[v] = (m >= 0 && m < g.n_out) ? gsig[b * g.n_out + m] : 0.f;
+    }
+    __syncthreads();
+    const double P = Psh;
+    float sa = 0.f, sb = 0.f;
+    for (int n = threadIdx.x; n < ni; n += blockDim.x) {
+        const int64_t d = i0 + n - g.gd;
+        const int64_t mf = d >= 0 ? (d + OS - 1) / OS : -((-d) / OS);  // ceil(d / OS)
+        const int j0 = (int)(mf * OS - d);                               // in [0, OS)
+        const int v0 = (int)(mf - mb);
+        float acc = 0.f;
+        const float* hr = hp + j0 * HS;
+        const float* gr = gs + v0;
+        float a4[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int u = 0; u < U4; u += 4) {
+            const float4 h4 = *reinterpret_cast<const float4*>(hr + u);
+            a4[0] = fmaf(h4.x, gr[u], a4[0]);
+            a4[1] = fmaf(h4.y, gr[u + 1], a4[1]);
+            a4[2] = fmaf(h4.z, gr[u + 2], a4[2]);
+            a4[3] = fmaf(h4.w, gr[u + 3], a4[3]);
+        }
+        acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+        const float ph = osc_phase(f0b, g, f, n, P);
+        const float dl = table_read(tab, g.K, g.L, pos_track(posb, g, f, n), ph).y;
+        const float gp = __fmul_rn(acc, dl);
+        const float w = f == g.F - 1 ? 0.f : __fmul_rn((float)n, g.inv_hop_f);
+        sa = fmaf(__fsub_rn(1.f, w), gp, sa);
+        sb = fmaf(w, gp, sb);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][wid] = sa;
+        red[1][wid] = sb;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float a = 0.f, c = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += red[0][w];
+            c += red[1][w];
+        }
+        part[(b * g.F + f) * 2 + 0] = a;
+        part[(b * g.F + f) * 2 + 1] = c;
+    }
+}
+
+// grad_pos[b][f] = part[b][f].a + part[b][f-1].b  (decoder._Upsample backward)
+__global__ void k_osc_combine(const float* __restrict__ part, float* __restrict__ gpos,
+                              int64_t B, int64_t F) {
+    grid_dep_wait();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= B * F) return;
+    const int64_t f = r % F;
+    gpos[r] = part[2 * r] + (f > 0 ? part[2 * (r - 1) + 1] : 0.f);
+}
+
+inline size_t osc_fwd_smem(const OscGeo& g, int os) {
+    const int NR = os * (g.hop - 1) + g.nt;
+    const int u4 = osc_taps_u4(g.nt, os);
+    return osc_span_frames(NR, g.hop_os) * sizeof(double) +
+           ((size_t)os * u4 + (size_t)os * osc_span_cols(g.hop, u4)) * sizeof(float);
+}
+inline size_t osc_vjp_smem(const OscGeo& g, int os) {
+    const int u4 = osc_taps_u4(g.nt, os);
+    const int NG = (g.hop_os + g.nt + 2 * os) / os + 2 + u4;
+    return ((size_t)os * (u4 + 4) + (size_t)NG) * sizeof(float);
+}
+
+// ---------------------------------------------------------------- global FIR
+constexpr int kFirThreads = 128;
+constexpr int kFirJ = 16;                        // outputs per thread
+constexpr int kFirTile = kFirThreads * kFirJ;    // 2048 outputs per CTA
+constexpr int kFirKB = 8;                        // taps per register block
+constexpr int kFirMaxTaps = 1024;
+
+// shared-memory skew: one pad word per 16 (thread t's rows start 17t apart:
+// conflict-free across the warp)
+__device__ __forceinline__ int skew(int y) { return y + (y >> 4); }
+
+// ADJ = false: y[n] = sum_k h[k] x[n-k]          (x[<0] = 0)
+// ADJ = true:  y[n] = sum_k h[k] x[n+k]          (x[>=n] = 0)  -- grad_x
+template <bool ADJ>
+__global__ void __launch_bounds__(kFirThreads)
+k_fir(const float* __restrict__ x, const float* __restrict__ taps, float* __restrict__ y,
+      int64_t n, int m) {
+    extern __shared__ __align__(16) float fir_sm[];
+    grid_dep_wait();
+    const int mp = (m + kFirKB - 1) / kFirKB * kFirKB;
+    const int64_t b = blockIdx.y, n0 = (int64_t)blockIdx.x * kFirTile;
+    float* hs = fir_sm;           // [mp]
+    float* xs = fir_sm + mp;      // skewed [kFirTile + mp]
+    const float* xb = x + b * n;
+    const float* hb = taps + b * m;
+    for (int k = threadIdx.x; k < mp; k += blockDim.x) hs[k] = k < m ? hb[k] : 0.f;
+    const int NX = kFirTile + mp;
+    const int64_t s0 = ADJ ? n0 : n0 - (mp - 1);   // first staged sample
+    for (int e = threadIdx.x; e < NX; e += blockDim.x) {
+        const int64_t idx = s0 + e;
+        xs[skew(e)] = (idx >= 0 && idx < n) ? xb[idx] : 0.f;
+    }
+    __syncthreads();
+    const int base = threadIdx.x * kFirJ;
+    float acc[kFirJ];
+#pragma unroll
+    for (int j = 0; j < kFirJ; ++j) acc[j] = 0.f;
+    for (int kb = 0; kb < mp; kb += kFirKB) {
+        float hv[kFirKB];
+#pragma unroll
+        for (int kk = 0; kk < kFirKB; ++kk) hv[kk] = hs[kb + kk];
+        float xr[kFirJ + kFirKB - 1];
+        // fwd: staged index of x[n0+base+j-k] = base + j - k + mp - 1, k = kb + kk
+        //      = (base + mp - 1 - kb - (KB-1)) + (j - kk + KB - 1)
+        // adj: staged index of x[n0+base+j+k] = base + kb + (j + kk)
+        const int e0 = ADJ ? base + kb : base + mp - kb - kFirKB;
+#pragma unroll
+        for (int e = 0; e < kFirJ + kFirKB - 1; ++e) xr[e] = xs[skew(e0 + e)];
+#pragma unroll
+        for (int kk = 0; kk < kFirKB; ++kk)
+#pragma unroll
+            for (int j = 0; j < kFirJ; ++j)
+                acc[j] = fmaf(hv[kk], xr[ADJ ? j + kk : j - kk + kFirKB - 1], acc[j]);
+    }
+    float* yb = y + b * n + n0 + base;
+    if (n0 + base + kFirJ <= n && ((reinterpret_cast<uintptr_t>(yb) & 15) == 0)) {
+#pragma unroll
+        for (int j = 0; j < kFirJ; j += 4)
+            *reinterpret_cast<float4*>(yb + j) = make_float4(acc[j], acc[j + 1], acc[j + 2],
+                                                             acc[j + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kFirJ; ++j)
+            if (n0 + base + j < n) yb[j] = acc[j];
+    }
+}
+
+// grad_h partials: part[b][tile][k] = sum_{n in tile} g[n] x[n-k].  Thread t:
+// taps [16 kb, 16 kb + 16) (kb = t % 8) over n-slice t / 8 of 128 samples; the
+// 16 slices are summed in shared memory in a fixed order.  (m <= 128 per pass
+// over k; larger m loops the k window.)
+constexpr int kTapJ = 16, kTapSlices = kFirThreads / 8, kTapSlice = kFirTile / kTapSlices;
+__global__ void __launch_bounds__(kFirThreads)
+k_fir_taps_part(const float* __restrict__ g, const float* __restrict__ x, float* __restrict__ part,
+                int64_t n, int m, int ntiles) {
+    extern __shared__ __align__(16) float fir_sm[];
+    grid_dep_wait();
+    const int64_t b = blockIdx.y, n0 = (int64_t)blockIdx.x * kFirTile;
+    const int mw = 128;                       // k window per pass
+    float* gs = fir_sm;                       // skewed [kFirTile]
+    float* xs = gs + skew(kFirTile) + 1;      // skewed [kFirTile + mw]
+    float* red = xs + skew(kFirTile + mw) + 1;  // [kTapSlices][mw]
+    const int kb = threadIdx.x % 8, sl = threadIdx.x / 8;
+    for (int e = threadIdx.x; e < kFirTile; e += blockDim.x) {
+        const int64_t idx = n0 + e;
+        gs[skew(e)] = idx < n ? g[b * n + idx] : 0.f;
+    }
+    for (int k0 = 0; k0 < m; k0 += mw) {
+        __syncthreads();
+        // staged x[n0 - k0 - mw + e], e in [0, kFirTile + mw)
+        for (int e = threadIdx.x; e < kFirTile + mw; e += blockDim.x) {
+            const int64_t idx = n0 - k0 - mw + e;
+            xs[skew(e)] = (idx >= 0 && idx < n) ? x[b * n + idx] : 0.f;
+        }
+        __syncthreads();
+        float acc[kTapJ];
+#pragma unroll
+        for (int j = 0; j < kTapJ; ++j) acc[j] = 0.f;
+        for (int s = 0; s < kTapSlice; s += 8) {
+            const int nl = sl * kTapSlice + s;   // local n of this 8-block
+            float gv[8], xr[8 + kTapJ - 1];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) gv[q] = gs[skew(nl + q)];
+            // x[n - k] for n = nl + q, k = k0 + 16 kb + j: staged e = nl + q - 16 kb - j + mw
+            const int e0 = nl + mw - 16 * kb - (kTapJ - 1);
+#pragma unroll
+            for (int e = 0; e < 8 + kTapJ - 1; ++e) xr[e] = xs[skew(e0 + e)];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int j = 0; j < kTapJ; ++j)
+                    acc[j] = fmaf(gv[q], xr[q - j + kTapJ - 1], acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < kTapJ; ++j) red[sl * mw + 16 * kb + j] = acc[j];
+        __syncthreads();
+        for (int k = threadIdx.x; k < mw; k += blockDim.x) {
+            float s = 0.f;
+            for (int q = 0; q < kTapSlices; ++q) s += red[q * mw + k];
+            if (k0 + k < m) part[(b * ntiles + blockIdx.x) * (int64_t)m + k0 + k] = s;
+        }
+    }
+}
+
+__global__ void k_fir_taps_reduce(const float* __restrict__ part, float* __restrict__ gh,
+                                  int64_t B, int m, int ntiles) {
+    grid_dep_wait();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= B * m) return;
+    const int64_t b = r / m, k = r % m;
+    float s = 0.f;
+    for (int t = 0; t < ntiles; ++t) s += part[(b * ntiles + t) * (int64_t)m + k];
+    gh[r] = s;
+}
+
+// ---------------------------------------------------------------- launchers
+namespace {
+template <typename K>
+cudaError_t allow_smem(K kernel, size_t bytes) {
+    return bytes > 48 * 1024 ? cudaFuncSetAttribute(kernel,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)bytes)
+                             : cudaSuccess;
+}
+}  // namespace
+
+cudaError_t launch_osc_fwd(const double* f0, const float* pos, const float* tab,
+                           const float* taps, float* sig, const OscGeo& g, int os,
+                           cudaStream_t st) {
+    if (os != 4) return cudaErrorInvalidValue;
+    const size_t sm = osc_fwd_smem(g, os);
+    cudaError_t e = allow_smem(k_osc_fwd<4>, sm);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(k_osc_fwd<4>, dim3((unsigned)g.F, (unsigned)g.B), kOscThreads, sm, st, f0, pos,
+                   tab, taps, sig, g);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_osc_vjp(const double* f0, const float* pos, const float* tab,
+                           const float* taps, const float* gsig, float* part, float* gpos,
+                           const OscGeo& g, int os, cudaStream_t st) {
+    if (os != 4) return cudaErrorInvalidValue;
+    const size_t sm = osc_vjp_smem(g, os);
+    cudaError_t e = allow_smem(k_osc_vjp<4>, sm);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(k_osc_vjp<4>, dim3((unsigned)g.F, (unsigned)g.B), kOscThreads, sm, st, f0, pos,
+                   tab, taps, gsig, part, g);
+    if (e != cudaSuccess) return e;
+    const int64_t rows = g.B * g.F;
+    e = launch_pdl(k_osc_combine, dim3((unsigned)((rows + 255) / 256)), 256, 0, st,
+                   (const float*)part, gpos, g.B, g.F);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+int fir_tiles(int64_t n) { return (int)((n + kFirTile - 1) / kFirTile); }
+
+cudaError_t launch_fir(const float* x, const float* taps, float* y, int64_t B, int64_t n, int m,
+                       bool adj, cudaStream_t st) {
+    if (m < 1 || m > kFirMaxTaps) return cudaErrorInvalidValue;
+    const int mp = (m + kFirKB - 1) / kFirKB * kFirKB;
+    const size_t sm = (mp + (kFirTile + mp) + (kFirTile + mp) / 16 + 1) * sizeof(float);
+    const dim3 grid((unsigned)fir_tiles(n), (unsigned)B);
+    cudaError_t e;
+    if (adj) {
+        e = allow_smem(k_fir<true>, sm);
+        if (e == cudaSuccess) e = launch_pdl(k_fir<true>, grid, kFirThreads, sm, st, x, taps, y, n, m);
+    } else {
+        e = allow_smem(k_fir<false>, sm);
+        if (e == cudaSuccess) e = launch_pdl(k_fir<false>, grid, kFirThreads, sm, st, x, taps, y, n, m);
+    }
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+size_t fir_taps_part_elems(int64_t B, int64_t n, int m) { return (size_t)B * fir_tiles(n) * m; }
+
+cudaError_t launch_fir_taps(const float* g, const float* x, float* part, float* gh, int64_t B,
+                            int64_t n, int m, cudaStream_t st) {
+    if (m < 1 || m > kFirMaxTaps) return cudaErrorInvalidValue;
+    const int nt = fir_tiles(n), mw = 128;
+    const size_t sm = ((kFirTile + kFirTile / 16 + 1) + (kFirTile + mw + (kFirTile + mw) / 16 + 1) +
+                       kTapSlices * mw) * sizeof(float);
+    cudaError_t e = allow_smem(k_fir_taps_part, sm);
+    if (e == cudaSuccess)
+        e = launch_pdl(k_fir_taps_part, dim3((unsigned)nt, (unsigned)B), kFirThreads, sm, st, g, x,
+                       part, n, m, nt);
+    if (e == cudaSuccess)
+        e = launch_pdl(k_fir_taps_reduce, dim3((unsigned)((B * m + 255) / 256)), 256, 0, st,
+                       (const float*)part, gh, B, m, nt);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+}  // namespace tvlp

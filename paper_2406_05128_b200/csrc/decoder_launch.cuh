@@ -1,0 +1,28 @@
+// decoder_launch.cuh -- launchers of decoder_kernels.cu (the oscillator and
+// the global FIR around the LP; include/tvlp.h tvlp_wavetable_osc*,
+// tvlp_global_fir*).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tvlp {
+
+struct OscGeo {
+    int64_t B, n_out, F, n_os;
+    int hop, hop_os, K, L, nt, gd;
+    double inv_rate;  // 1 / (fs * oversample)
+    double inv_hop;   // 1 / hop_os
+    float inv_hop_f;
+};
+cudaError_t launch_osc_fwd(const double* f0, const float* pos, const float* tab,
+                           const float* taps, float* sig, const OscGeo& g, int os,
+                           cudaStream_t st);
+cudaError_t launch_osc_vjp(const double* f0, const float* pos, const float* tab,
+                           const float* taps, const float* gsig, float* part, float* gpos,
+                           const OscGeo& g, int os, cudaStream_t st);
+cudaError_t launch_fir(const float* x, const float* taps, float* y, int64_t B, int64_t n, int m,
+                       bool adj, cudaStream_t st);
+size_t fir_taps_part_elems(int64_t B, int64_t n, int m);
+cudaError_t launch_fir_taps(const float* g, const float* x, float* part, float* gh, int64_t B,
+                            int64_t n, int m, cudaStream_t st);
+}  // namespace tvlp

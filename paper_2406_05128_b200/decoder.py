@@ -14,8 +14,11 @@ decoders on a numpy tape (pkg/src/tvlp/synth.py:217-275) from these pieces:
 
 Here they are batched torch operations on CUDA tensors (cuFFT/cuDNN
 library kernels -- SURVEY.md §8(f): "torch/cuFFT first, fuse only if
-profiled hot"), differentiated by torch autograd; the LP filters are this
-package's sm_100a kernels (the fused upsample+LP ``autograd.lp_tv_frames``
+profiled hot"), differentiated by torch autograd, except the two pieces that
+profiled hot in the float32 decoder step: the oscillator (phase, table read,
+decimation) and the global FIR run on this package's kernels
+(csrc/decoder_kernels.cu; ``wavetable_osc``, ``global_fir``); the LP filters
+are this package's sm_100a kernels (the fused upsample+LP ``autograd.lp_tv_frames``
 and the grouped pair ``autograd.lp_tv_grouped`` for a C(z) LP).
 Every op follows the reference's arithmetic order closely enough that the
 float64 decoder matches the reference tape to ~1e-12 (tests/test_decoder_gpu.py).
@@ -31,11 +34,12 @@ import numpy as np
 import torch
 import torch.nn.functional as TF
 
+from . import _native as N
 from . import autograd as ag
 
 __all__ = [
     "NOISE_BINS", "FIR_TAPS", "design_lowpass", "oscillator_phase", "upsample_linear",
-    "wavetable_read", "decimate_fir", "fir_from_logmag", "shape_noise", "generate_noise",
+    "wavetable_read", "decimate_fir", "wavetable_osc", "fir_from_logmag", "shape_noise", "generate_noise",
     "global_fir", "stft_mag", "mss_loss", "Decoder",
 ]
 
@@ -150,6 +154,22 @@ def oscillator_phase(f0_frames, hop, n_out, fs, oversample, device=None):
     """Per-sample table phase (periods, mod 1) at the oversampled rate
     (source.py:224-238): float64 cumulative sum, on ``device`` (default: the
     device of ``f0_frames``; host arrays -> CPU)."""
+    f0_frames = _checked_f0(f0_frames, fs, device)
+    n_os = n_out * oversample
+    f0 = upsample_linear(f0_frames, hop * oversample, n_os)
+    return torch.remainder(torch.cumsum(f0 / (fs * oversample), dim=-1), 1.0)
+
+
+def _b200_pieces(t):
+    """The float32 CUDA decoder runs the oscillator and the global FIR on
+    csrc/decoder_kernels.cu; float64 (the reference-parity runs) and CPU
+    tensors compose the torch pieces."""
+    return t.is_cuda and t.dtype == torch.float32
+
+
+def _checked_f0(f0_frames, fs, device=None):
+    """f0 frames as float64 [B, F] on ``device``, validated like
+    source.py:230-233."""
     f0_frames = torch.as_tensor(f0_frames, dtype=torch.float64, device=device)
     if f0_frames.dim() == 1:
         f0_frames = f0_frames[None]
@@ -160,9 +180,71 @@ def oscillator_phase(f0_frames, hop, n_out, fs, oversample, device=None):
         if bool((f0_frames >= fs / 2.0).any()):
             raise ValueError("f0 at or above the output Nyquist frequency")
         raise ValueError("f0 must be nonnegative")
-    n_os = n_out * oversample
-    f0 = upsample_linear(f0_frames, hop * oversample, n_os)
-    return torch.remainder(torch.cumsum(f0 / (fs * oversample), dim=-1), 1.0)
+    return f0_frames
+
+
+class _WavetableOscB200(torch.autograd.Function):
+    """The oscillator subgraph of source.py:294-318 (oscillator_phase ->
+    upsample_linear(pos) -> wavetable_read -> decimate_fir) as one kernel
+    (tvlp_wavetable_osc: the x4 track never leaves shared memory) and its VJP
+    to the table-position frames (tvlp_wavetable_osc_vjp).  float32, the phase
+    in float64."""
+
+    @staticmethod
+    def forward(ctx, pos, f0, tables, taps, hop, n_out, fs):
+        lib = N.load()
+        B, F = pos.shape
+        K, L = tables.shape
+        sig = torch.empty((B, n_out), dtype=torch.float32, device=pos.device)
+        with N.on_device(pos.device):
+            N.check(lib.tvlp_wavetable_osc(N.ptr(f0), N.ptr(pos), N.ptr(tables), K, L, N.ptr(taps),
+                                           taps.shape[0], N.ptr(sig), B, n_out, F, hop, 4,
+                                           float(fs), N.stream_ptr(pos.device)))
+        ctx.save_for_backward(pos, f0, tables, taps)
+        ctx.cfg = (hop, n_out, float(fs))
+        return sig
+
+    @staticmethod
+    def backward(ctx, g):
+        pos, f0, tables, taps = ctx.saved_tensors
+        hop, n_out, fs = ctx.cfg
+        lib = N.load()
+        B, F = pos.shape
+        K, L = tables.shape
+        g = g.contiguous()
+        gpos = torch.empty_like(pos)
+        ws = torch.empty(2 * B * F, dtype=torch.float32, device=pos.device)
+        with N.on_device(pos.device):
+            N.check(lib.tvlp_wavetable_osc_vjp(N.ptr(f0), N.ptr(pos), N.ptr(tables), K, L,
+                                               N.ptr(taps), taps.shape[0], N.ptr(g), N.ptr(gpos),
+                                               N.ptr(ws), B, n_out, F, hop, 4, fs,
+                                               N.stream_ptr(pos.device)))
+        return gpos, None, None, None, None, None, None
+
+
+def wavetable_osc(pos, f0_frames, tables, hop, n_out, fs, oversample=4, taps=None):
+    """The oscillator's decimated signal [B, n_out] before the gain
+    (source.py:294-316) from table-position frames pos [B, F] (already in
+    [0, K-1] units) and f0 frames [B, F].  float32 CUDA tensors at the
+    reference's oversample 4 run the fused kernels; anything else composes
+    the taped pieces (oscillator_phase, upsample_linear, wavetable_read,
+    decimate_fir) in torch."""
+    if taps is None:
+        taps = _on_device(("lowpass", oversample),
+                          lambda: torch.as_tensor(_lowpass_np(127, 0.45, oversample).copy()),
+                          pos.device, pos.dtype)
+    if _b200_pieces(pos) and oversample == 4:
+        f0 = _checked_f0(f0_frames, fs, pos.device)
+        if f0.shape != pos.shape:
+            raise ValueError(f"f0 frames {tuple(f0.shape)} must match positions {tuple(pos.shape)}")
+        return _WavetableOscB200.apply(pos.contiguous(), f0.contiguous(),
+                                       tables.to(torch.float32).contiguous(),
+                                       taps.to(torch.float32).contiguous(), hop, n_out, fs)
+    phase = oscillator_phase(f0_frames, hop, n_out, fs, oversample,
+                             device=pos.device).to(pos.dtype)
+    pos_track = upsample_linear(pos, hop * oversample, n_out * oversample)
+    raw = wavetable_read(pos_track, tables.to(pos.dtype), phase)
+    return decimate_fir(raw, taps, oversample, n_out) if oversample > 1 else raw
 
 
 class _WavetableRead(torch.autograd.Function):
@@ -281,10 +363,47 @@ def shape_noise(logmag, noise, plan):
     return out[:, :n_out] / plan._cola_cached()
 
 
+class _GlobalFIRB200(torch.autograd.Function):
+    """source.py:445-466 on the kernels of csrc/decoder_kernels.cu
+    (tvlp_global_fir / tvlp_global_fir_vjp), float32."""
+
+    @staticmethod
+    def forward(ctx, x, taps):
+        lib = N.load()
+        Bn, n = x.shape
+        y = torch.empty_like(x)
+        with N.on_device(x.device):
+            N.check(lib.tvlp_global_fir(N.ptr(x), N.ptr(taps), N.ptr(y), Bn, n, taps.shape[-1],
+                                        N.stream_ptr(x.device)))
+        ctx.save_for_backward(x, taps)
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        x, taps = ctx.saved_tensors
+        lib = N.load()
+        Bn, n = x.shape
+        m = taps.shape[-1]
+        g = g.contiguous()
+        gx = torch.empty_like(x) if ctx.needs_input_grad[0] else None
+        gt = torch.empty_like(taps) if ctx.needs_input_grad[1] else None
+        nb = lib.tvlp_global_fir_workspace(Bn, n, m)
+        ws = torch.empty(max(nb, 4) // 4, dtype=torch.float32, device=x.device)
+        with N.on_device(x.device):
+            N.check(lib.tvlp_global_fir_vjp(N.ptr(g), N.ptr(x), N.ptr(taps),
+                                            N.ptr(gx) if gx is not None else None,
+                                            N.ptr(gt) if gt is not None else None,
+                                            N.ptr(ws), nb, Bn, n, m, N.stream_ptr(x.device)))
+        return gx, gt
+
+
 def global_fir(x, taps):
-    """source.py:445-459: causal same-length convolution, x [B, n], taps [B, m]."""
+    """source.py:445-459: causal same-length convolution, x [B, n], taps [B, m]
+    (float32 CUDA tensors: the kernels of csrc/decoder_kernels.cu)."""
     Bn, n = x.shape
     m = taps.shape[-1]
+    if _b200_pieces(x) and taps.dtype == torch.float32 and 1 <= m <= 1024 and taps.shape == (Bn, m):
+        return _GlobalFIRB200.apply(x.contiguous(), taps.contiguous())
     xp = TF.pad(x, (m - 1, 0))
     # grouped conv: one filter per item (the taps are per-item parameters)
     y = TF.conv1d(xp[None], taps.flip(-1)[:, None], groups=Bn)
@@ -361,17 +480,7 @@ class Decoder:
         pos = torch.sigmoid(p["table_pos_raw"]) * (K - 1)
         vgain = torch.exp(p["voiced_gain_raw"])
         # oscillator (source.py:294-314)
-        phase = oscillator_phase(f0_frames, hop, n_out, self.fs, self.oversample,
-                                 device=pos.device).to(pos.dtype)
-        pos_track = upsample_linear(pos, hop * self.oversample, n_out * self.oversample)
-        raw = wavetable_read(pos_track, self.tables.to(pos.dtype), phase)
-        if self.oversample > 1:
-            taps = _on_device(("lowpass", self.oversample),
-                              lambda: torch.as_tensor(_lowpass_np(127, 0.45, self.oversample).copy()),
-                              pos.device, pos.dtype)
-            sig = decimate_fir(raw, taps, self.oversample, n_out)
-        else:
-            sig = raw
+        sig = wavetable_osc(pos, f0_frames, self.tables, hop, n_out, self.fs, self.oversample)
         osc = sig * upsample_linear(vgain, hop, T1)
         noise_unit = shape_noise(p["noise_logmag"], noise.to(pos.dtype), self._plan())
         noise_s = noise_unit * upsample_linear(torch.exp(p["noise_gain_raw"]), hop, T1)

@@ -186,6 +186,22 @@ def test_tv_frames_exact_plan_all_items():
     assert max(max(x) for x in errs) < TOL32, errs
 
 
+@pytest.mark.skipif(os.environ.get("TVLP_FR_FWD_CHAIN") == "1", reason="already in the child")
+def test_tv_frames_chained_forward_knob():
+    """The chained forward with frame-rate rows (TVLP_FR_FWD_CHAIN=1, off by
+    default: measured slower) at the same exact plan, in a child process (the
+    knob is read once per process)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_parity_bench_gpu.py"),
+                        "-k", "test_tv_frames_exact_plan_all_items"],
+                       env=dict(os.environ, TVLP_FR_FWD_CHAIN="1"), cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "1 passed" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_framewise_exact_all_items():
     """Config 2 (bench framewise_b32_t48000): all 32 items."""
     from paper_2406_05128_b200 import params
