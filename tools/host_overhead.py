@@ -56,6 +56,13 @@ def main():
         lpc._backward(False, g1, A1, s, None, c)
 
     measure("tv B=8", tv8)
+    e4, A4, g4 = data.d1_batch_torch(0, 4, 24000, 22, device="cuda")
+
+    def tv4():
+        s, c = lpc._forward(False, e4, A4, None, return_carry=True)
+        lpc._backward(False, g4, A4, s, None, c)
+
+    measure("tv B=4 T=24000 (config 1)", tv4)
 
 
 if __name__ == "__main__":
