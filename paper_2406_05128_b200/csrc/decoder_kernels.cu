@@ -425,6 +425,7 @@ __global__ void k_fir_taps_reduce(const float* __restrict__ part, float* __restr
 namespace {
 template <typename K>
 cudaError_t allow_smem(K kernel, size_t bytes) {
+    if (bytes > 227 * 1024) return cudaErrorInvalidValue;  // (very long hops)
     return bytes > 48 * 1024 ? cudaFuncSetAttribute(kernel,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     (int)bytes)

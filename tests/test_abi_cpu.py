@@ -89,6 +89,41 @@ def test_abi_queries_frames_and_split():
     assert lib.tvlp_segment_transition(0, None, 1, 100, 3, None, None, 0, None) == 1
 
 
+def test_abi_decoder_entry_points_validate_before_launch():
+    """tvlp_wavetable_osc* / tvlp_global_fir*: argument checks and the
+    workspace query (no kernel launches: B = 0 or rejected arguments)."""
+    import ctypes
+    lib = N.load()
+    fake = ctypes.c_void_p(256)          # never dereferenced: rejected or B = 0
+    n_out, hop = 48001, 240
+    F = (n_out * 4 - 1) // (hop * 4) + 1
+    ok = (fake, fake, fake, 9, 512, fake, 127)
+    # valid geometry with B = 0: nothing to do
+    assert lib.tvlp_wavetable_osc(*ok, fake, 0, n_out, F, hop, 4, 48000.0, None) == 0
+    assert lib.tvlp_wavetable_osc_vjp(*ok, fake, fake, fake, 0, n_out, F, hop, 4, 48000.0,
+                                      None) == 0
+    bad = [
+        dict(F=F + 1), dict(os=2), dict(nt=128), dict(fs=0.0), dict(K=0), dict(L=1),
+    ]
+    for b in bad:
+        args = dict(K=9, L=512, nt=127, F=F, os=4, fs=48000.0)
+        args.update(b)
+        assert lib.tvlp_wavetable_osc(fake, fake, fake, args["K"], args["L"], fake, args["nt"],
+                                      fake, 2, n_out, args["F"], hop, args["os"], args["fs"],
+                                      None) == 1, b
+    assert lib.tvlp_wavetable_osc(None, fake, fake, 9, 512, fake, 127, fake, 2, n_out, F, hop, 4,
+                                  48000.0, None) == 1
+    assert lib.tvlp_wavetable_osc_vjp(*ok, None, fake, fake, 2, n_out, F, hop, 4, 48000.0,
+                                      None) == 1
+    # global FIR: taps 1..1024; workspace = B x tiles(n) x m floats
+    assert lib.tvlp_global_fir(fake, fake, fake, 2, 5000, 0, None) == 1
+    assert lib.tvlp_global_fir(fake, fake, fake, 2, 5000, 1025, None) == 1
+    assert lib.tvlp_global_fir(fake, fake, fake, 0, 5000, 128, None) == 0
+    assert lib.tvlp_global_fir_workspace(2, 5000, 128) == 2 * 3 * 128 * 4
+    assert lib.tvlp_global_fir_workspace(4, 48001, 128) == 4 * 24 * 128 * 4
+    assert lib.tvlp_global_fir_vjp(fake, fake, fake, None, fake, None, 0, 2, 5000, 128, None) == 3
+
+
 def test_longseq_combine_algebra():
     """The fold of the time split on small matrices (CPU torch): forward
     states and backward adjoints against a direct composition."""
