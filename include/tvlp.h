@@ -267,6 +267,19 @@ int tvlp_global_fir_vjp(const float* grad_y, const float* x, const float* taps, 
                         float* grad_taps, void* workspace, size_t workspace_bytes, int64_t B,
                         int64_t n, int32_t m, void* stream);
 
+/* One FFT size of the multi-resolution spectral loss (loss.py:105-126) from
+ * one-sided spectra (the caller's FFTs): X (signal) and Y (target) complex
+ * [B][n] as interleaved float pairs, n = frames x bins per item.
+ * term[b] = ||(|X|-|Y|)|| / max(||Y||, 1e-12) + mean |log(|X|+eps) -
+ * log(|Y|+eps)|; aux [B][4] keeps what the VJP needs; workspace:
+ * tvlp_mss_terms_workspace bytes.  The VJP writes grad_X (complex [B][n])
+ * from grad_term [B] (the stft_mag VJP's phase mask, loss.py:71-73). */
+size_t tvlp_mss_terms_workspace(int64_t B, int64_t n);
+int tvlp_mss_terms(const float* X, const float* Y, int64_t B, int64_t n, float eps, float* term,
+                   float* aux, void* workspace, size_t workspace_bytes, void* stream);
+int tvlp_mss_terms_vjp(const float* X, const float* Y, const float* aux, const float* grad_term,
+                       float* grad_X, int64_t B, int64_t n, float eps, void* stream);
+
 /* Instrumentation (bench.py): number of kernels this library has launched,
  * and optional CUDA-event timing of every launch (off by default; when on,
  * each launch is bracketed by two events on its stream).  tvlp_profile_dump

@@ -96,6 +96,9 @@ _SIGS = [
     ("tvlp_global_fir", ctypes.c_int, [_P, _P, _P, _I64, _I64, _I32, _P]),
     ("tvlp_global_fir_workspace", _SZ, [_I64, _I64, _I32]),
     ("tvlp_global_fir_vjp", ctypes.c_int, [_P, _P, _P, _P, _P, _P, _SZ, _I64, _I64, _I32, _P]),
+    ("tvlp_mss_terms_workspace", _SZ, [_I64, _I64]),
+    ("tvlp_mss_terms", ctypes.c_int, [_P, _P, _I64, _I64, ctypes.c_float, _P, _P, _P, _SZ, _P]),
+    ("tvlp_mss_terms_vjp", ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, ctypes.c_float, _P]),
     ("tvlp_launch_count", _I64, []),
     ("tvlp_refined_sequences", _I64, []),
     ("tvlp_profile_enable", None, [_I32]),
@@ -136,7 +139,7 @@ def load(path=None):
 
 _PURE = ("tvlp_workspace_bytes", "tvlp_carry_elems", "tvlp_max_order",
          "tvlp_framewise_aux_elems", "tvlp_framewise_nframes", "tvlp_subchunk_len",
-         "tvlp_global_fir_workspace")
+         "tvlp_global_fir_workspace", "tvlp_mss_terms_workspace")
 
 
 def on_device(device):

@@ -1130,7 +1130,35 @@ int tvlp_global_fir(const float* x, const float* taps, float* y, int64_t B, int6
     if (!x || !taps || !y || B < 0 || n < 0 || m < 1 || m > 1024) return TVLP_ERR_ARG;
     if (B == 0 || n == 0) return TVLP_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    TVLP_CK(tracked("global_fir", 1, st, [&] { return launch_fir(x, taps, y, B, n, m, false, st); }));
+    TVLP_CK(tracked("global_fir", 1, st, [&] { return launch_fir(x, taps, y, B, n, m, false, 0, st); }));
+    return TVLP_OK;
+}
+
+size_t tvlp_mss_terms_workspace(int64_t B, int64_t n) {
+    if (B < 0 || n < 1) return 0;
+    return mss_part_floats(B, n) * sizeof(float);
+}
+
+int tvlp_mss_terms(const float* X, const float* Y, int64_t B, int64_t n, float eps, float* term,
+                   float* aux, void* workspace, size_t workspace_bytes, void* stream) {
+    if (!X || !Y || !term || !aux || B < 0 || n < 1 || !(eps >= 0.f)) return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    if (!workspace || workspace_bytes < tvlp_mss_terms_workspace(B, n)) return TVLP_ERR_WORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("mss_terms", 2, st, [&] {
+        return launch_mss_terms(X, Y, B, n, eps, term, aux, static_cast<float*>(workspace), st);
+    }));
+    return TVLP_OK;
+}
+
+int tvlp_mss_terms_vjp(const float* X, const float* Y, const float* aux, const float* grad_term,
+                       float* grad_X, int64_t B, int64_t n, float eps, void* stream) {
+    if (!X || !Y || !aux || !grad_term || !grad_X || B < 0 || n < 1) return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("mss_terms_vjp", 1, st, [&] {
+        return launch_mss_terms_vjp(X, Y, aux, grad_term, B, n, eps, grad_X, st);
+    }));
     return TVLP_OK;
 }
 
@@ -1151,13 +1179,13 @@ int tvlp_global_fir_vjp(const float* grad_y, const float* x, const float* taps, 
     }
     if (grad_x)
         TVLP_CK(tracked("global_fir_vjp_x", 1, st,
-                        [&] { return launch_fir(grad_y, taps, grad_x, B, n, m, true, st); }));
+                        [&] { return launch_fir(grad_y, taps, grad_x, B, n, m, true, 0, st); }));
     if (grad_taps) {
         if (!workspace || workspace_bytes < tvlp_global_fir_workspace(B, n, m))
             return TVLP_ERR_WORKSPACE;
         TVLP_CK(tracked("global_fir_vjp_taps", 2, st, [&] {
             return launch_fir_taps(grad_y, x, static_cast<float*>(workspace), grad_taps, B, n, m,
-                                   st);
+                                   0, st);
         }));
     }
     return TVLP_OK;

@@ -19,6 +19,8 @@
 // Roofline: all of it is a few hundred MB of HBM per step and < 2 GFLOP of
 // FFMA; the kernels are sized so neither the gathers nor shared memory
 // bandwidth dominate (register-blocked FIR tiles: 31 LDS per 128 FFMA).
+#include <algorithm>
+
 #include "common.cuh"
 #include "decoder_launch.cuh"
 
@@ -286,110 +288,120 @@ inline size_t osc_vjp_smem(const OscGeo& g, int os) {
     return ((size_t)os * (u4 + 4) + (size_t)NG) * sizeof(float);
 }
 
-// ---------------------------------------------------------------- global FIR
+// ---------------------------------------------------------------- FIR rows
+// Per-row FIRs: the decoder's global FIR (source.py:445-466, one 128-tap
+// filter per item) and the noise shaping's frame FIRs (source.py:367-428,
+// one 510-tap filter per 960-sample frame) share these kernels:
+//   y[n] = sum_{k<m} h[k] x[n + off - k],  n in [0, ny),  x = 0 outside [0, nx)
+// (global FIR: off 0, nx = ny = n; noise frames: off = the FIR's 255-sample
+// delay, nx = ny = frame size), its adjoint to x (ADJ, off 0) and the tap
+// gradient grad_h[k] = sum_n g[n] x[n + off - k].
 constexpr int kFirThreads = 128;
-constexpr int kFirJ = 16;                        // outputs per thread
-constexpr int kFirTile = kFirThreads * kFirJ;    // 2048 outputs per CTA
 constexpr int kFirKB = 8;                        // taps per register block
 constexpr int kFirMaxTaps = 1024;
+template <int J>
+struct FirTile {
+    static constexpr int TILE = kFirThreads * J;  // outputs per CTA (J = 16: 2048, 8: 1024)
+};
 
 // shared-memory skew: one pad word per 16 (thread t's rows start 17t apart:
 // conflict-free across the warp)
 __device__ __forceinline__ int skew(int y) { return y + (y >> 4); }
 
-// ADJ = false: y[n] = sum_k h[k] x[n-k]          (x[<0] = 0)
-// ADJ = true:  y[n] = sum_k h[k] x[n+k]          (x[>=n] = 0)  -- grad_x
-template <bool ADJ>
+template <bool ADJ, int J>
 __global__ void __launch_bounds__(kFirThreads)
 k_fir(const float* __restrict__ x, const float* __restrict__ taps, float* __restrict__ y,
-      int64_t n, int m) {
+      int64_t n, int m, int off) {
     extern __shared__ __align__(16) float fir_sm[];
     grid_dep_wait();
+    constexpr int TILE = FirTile<J>::TILE;
     const int mp = (m + kFirKB - 1) / kFirKB * kFirKB;
-    const int64_t b = blockIdx.y, n0 = (int64_t)blockIdx.x * kFirTile;
+    const int64_t b = blockIdx.y, n0 = (int64_t)blockIdx.x * TILE;
     float* hs = fir_sm;           // [mp]
-    float* xs = fir_sm + mp;      // skewed [kFirTile + mp]
+    float* xs = fir_sm + mp;      // skewed [TILE + mp]
     const float* xb = x + b * n;
     const float* hb = taps + b * m;
     for (int k = threadIdx.x; k < mp; k += blockDim.x) hs[k] = k < m ? hb[k] : 0.f;
-    const int NX = kFirTile + mp;
-    const int64_t s0 = ADJ ? n0 : n0 - (mp - 1);   // first staged sample
+    const int NX = TILE + mp;
+    const int64_t s0 = ADJ ? n0 : n0 + off - (mp - 1);   // first staged sample
     for (int e = threadIdx.x; e < NX; e += blockDim.x) {
         const int64_t idx = s0 + e;
         xs[skew(e)] = (idx >= 0 && idx < n) ? xb[idx] : 0.f;
     }
     __syncthreads();
-    const int base = threadIdx.x * kFirJ;
-    float acc[kFirJ];
+    const int base = threadIdx.x * J;
+    float acc[J];
 #pragma unroll
-    for (int j = 0; j < kFirJ; ++j) acc[j] = 0.f;
+    for (int j = 0; j < J; ++j) acc[j] = 0.f;
     for (int kb = 0; kb < mp; kb += kFirKB) {
         float hv[kFirKB];
 #pragma unroll
         for (int kk = 0; kk < kFirKB; ++kk) hv[kk] = hs[kb + kk];
-        float xr[kFirJ + kFirKB - 1];
-        // fwd: staged index of x[n0+base+j-k] = base + j - k + mp - 1, k = kb + kk
-        //      = (base + mp - 1 - kb - (KB-1)) + (j - kk + KB - 1)
+        float xr[J + kFirKB - 1];
+        // fwd: staged index of x[n0+base+j+off-k] = base + j - k + mp - 1, k = kb + kk
+        //      = (base + mp - kb - KB) + (j - kk + KB - 1)
         // adj: staged index of x[n0+base+j+k] = base + kb + (j + kk)
         const int e0 = ADJ ? base + kb : base + mp - kb - kFirKB;
 #pragma unroll
-        for (int e = 0; e < kFirJ + kFirKB - 1; ++e) xr[e] = xs[skew(e0 + e)];
+        for (int e = 0; e < J + kFirKB - 1; ++e) xr[e] = xs[skew(e0 + e)];
 #pragma unroll
         for (int kk = 0; kk < kFirKB; ++kk)
 #pragma unroll
-            for (int j = 0; j < kFirJ; ++j)
+            for (int j = 0; j < J; ++j)
                 acc[j] = fmaf(hv[kk], xr[ADJ ? j + kk : j - kk + kFirKB - 1], acc[j]);
     }
     float* yb = y + b * n + n0 + base;
-    if (n0 + base + kFirJ <= n && ((reinterpret_cast<uintptr_t>(yb) & 15) == 0)) {
+    if (n0 + base + J <= n && ((reinterpret_cast<uintptr_t>(yb) & 15) == 0)) {
 #pragma unroll
-        for (int j = 0; j < kFirJ; j += 4)
+        for (int j = 0; j < J; j += 4)
             *reinterpret_cast<float4*>(yb + j) = make_float4(acc[j], acc[j + 1], acc[j + 2],
                                                              acc[j + 3]);
     } else {
 #pragma unroll
-        for (int j = 0; j < kFirJ; ++j)
+        for (int j = 0; j < J; ++j)
             if (n0 + base + j < n) yb[j] = acc[j];
     }
 }
 
-// grad_h partials: part[b][tile][k] = sum_{n in tile} g[n] x[n-k].  Thread t:
-// taps [16 kb, 16 kb + 16) (kb = t % 8) over n-slice t / 8 of 128 samples; the
-// 16 slices are summed in shared memory in a fixed order.  (m <= 128 per pass
-// over k; larger m loops the k window.)
-constexpr int kTapJ = 16, kTapSlices = kFirThreads / 8, kTapSlice = kFirTile / kTapSlices;
+// grad_h partials: part[b][tile][k] = sum_{n in tile} g[n] x[n + off - k].
+// Thread t: taps [16 kb, 16 kb + 16) (kb = t % 8) over n-slice t / 8 of
+// TILE/16 samples; the 16 slices are summed in shared memory in a fixed
+// order; taps beyond 128 loop the k window.
+constexpr int kTapJ = 16, kTapSlices = kFirThreads / 8, kTapWin = 128;
+template <int J>
 __global__ void __launch_bounds__(kFirThreads)
 k_fir_taps_part(const float* __restrict__ g, const float* __restrict__ x, float* __restrict__ part,
-                int64_t n, int m, int ntiles) {
+                int64_t n, int m, int off, int ntiles) {
     extern __shared__ __align__(16) float fir_sm[];
     grid_dep_wait();
-    const int64_t b = blockIdx.y, n0 = (int64_t)blockIdx.x * kFirTile;
-    const int mw = 128;                       // k window per pass
-    float* gs = fir_sm;                       // skewed [kFirTile]
-    float* xs = gs + skew(kFirTile) + 1;      // skewed [kFirTile + mw]
-    float* red = xs + skew(kFirTile + mw) + 1;  // [kTapSlices][mw]
+    constexpr int TILE = FirTile<J>::TILE, SLICE = TILE / kTapSlices;
+    const int64_t b = blockIdx.y, n0 = (int64_t)blockIdx.x * TILE;
+    const int mw = kTapWin;
+    float* gs = fir_sm;                       // skewed [TILE]
+    float* xs = gs + skew(TILE) + 1;          // skewed [TILE + mw]
+    float* red = xs + skew(TILE + mw) + 1;    // [kTapSlices][mw]
     const int kb = threadIdx.x % 8, sl = threadIdx.x / 8;
-    for (int e = threadIdx.x; e < kFirTile; e += blockDim.x) {
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
         const int64_t idx = n0 + e;
         gs[skew(e)] = idx < n ? g[b * n + idx] : 0.f;
     }
     for (int k0 = 0; k0 < m; k0 += mw) {
         __syncthreads();
-        // staged x[n0 - k0 - mw + e], e in [0, kFirTile + mw)
-        for (int e = threadIdx.x; e < kFirTile + mw; e += blockDim.x) {
-            const int64_t idx = n0 - k0 - mw + e;
+        // staged x[n0 + off - k0 - mw + e], e in [0, TILE + mw)
+        for (int e = threadIdx.x; e < TILE + mw; e += blockDim.x) {
+            const int64_t idx = n0 + off - k0 - mw + e;
             xs[skew(e)] = (idx >= 0 && idx < n) ? x[b * n + idx] : 0.f;
         }
         __syncthreads();
         float acc[kTapJ];
 #pragma unroll
         for (int j = 0; j < kTapJ; ++j) acc[j] = 0.f;
-        for (int s = 0; s < kTapSlice; s += 8) {
-            const int nl = sl * kTapSlice + s;   // local n of this 8-block
+        for (int s = 0; s < SLICE; s += 8) {
+            const int nl = sl * SLICE + s;   // local n of this 8-block
             float gv[8], xr[8 + kTapJ - 1];
 #pragma unroll
             for (int q = 0; q < 8; ++q) gv[q] = gs[skew(nl + q)];
-            // x[n - k] for n = nl + q, k = k0 + 16 kb + j: staged e = nl + q - 16 kb - j + mw
+            // x[n + off - k] for n = n0 + nl + q, k = k0 + 16 kb + j: staged e = nl + q - 16 kb - j + mw
             const int e0 = nl + mw - 16 * kb - (kTapJ - 1);
 #pragma unroll
             for (int e = 0; e < 8 + kTapJ - 1; ++e) xr[e] = xs[skew(e0 + e)];
@@ -461,40 +473,180 @@ cudaError_t launch_osc_vjp(const double* f0, const float* pos, const float* tab,
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-int fir_tiles(int64_t n) { return (int)((n + kFirTile - 1) / kFirTile); }
+// rows up to 1024 samples (the noise frames) use the 1024-output tile
+int fir_j(int64_t n) { return n <= 1024 ? 8 : 16; }
+int fir_tiles(int64_t n) {
+    const int tile = kFirThreads * fir_j(n);
+    return (int)((n + tile - 1) / tile);
+}
+
+template <bool ADJ, int J>
+cudaError_t launch_fir_j(const float* x, const float* taps, float* y, int64_t B, int64_t n, int m,
+                         int off, cudaStream_t st) {
+    const int mp = (m + kFirKB - 1) / kFirKB * kFirKB;
+    const int NX = FirTile<J>::TILE + mp;
+    const size_t sm = (mp + NX + NX / 16 + 1) * sizeof(float);
+    cudaError_t e = allow_smem(k_fir<ADJ, J>, sm);
+    if (e == cudaSuccess)
+        e = launch_pdl(k_fir<ADJ, J>, dim3((unsigned)fir_tiles(n), (unsigned)B), kFirThreads, sm,
+                       st, x, taps, y, n, m, off);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
 
 cudaError_t launch_fir(const float* x, const float* taps, float* y, int64_t B, int64_t n, int m,
-                       bool adj, cudaStream_t st) {
-    if (m < 1 || m > kFirMaxTaps) return cudaErrorInvalidValue;
-    const int mp = (m + kFirKB - 1) / kFirKB * kFirKB;
-    const size_t sm = (mp + (kFirTile + mp) + (kFirTile + mp) / 16 + 1) * sizeof(float);
-    const dim3 grid((unsigned)fir_tiles(n), (unsigned)B);
-    cudaError_t e;
-    if (adj) {
-        e = allow_smem(k_fir<true>, sm);
-        if (e == cudaSuccess) e = launch_pdl(k_fir<true>, grid, kFirThreads, sm, st, x, taps, y, n, m);
-    } else {
-        e = allow_smem(k_fir<false>, sm);
-        if (e == cudaSuccess) e = launch_pdl(k_fir<false>, grid, kFirThreads, sm, st, x, taps, y, n, m);
-    }
-    return e != cudaSuccess ? e : cudaGetLastError();
+                       bool adj, int off, cudaStream_t st) {
+    if (m < 1 || m > kFirMaxTaps || (adj && off != 0)) return cudaErrorInvalidValue;
+    if (fir_j(n) == 8)
+        return adj ? launch_fir_j<true, 8>(x, taps, y, B, n, m, off, st)
+                   : launch_fir_j<false, 8>(x, taps, y, B, n, m, off, st);
+    return adj ? launch_fir_j<true, 16>(x, taps, y, B, n, m, off, st)
+               : launch_fir_j<false, 16>(x, taps, y, B, n, m, off, st);
 }
 
 size_t fir_taps_part_elems(int64_t B, int64_t n, int m) { return (size_t)B * fir_tiles(n) * m; }
 
-cudaError_t launch_fir_taps(const float* g, const float* x, float* part, float* gh, int64_t B,
-                            int64_t n, int m, cudaStream_t st) {
-    if (m < 1 || m > kFirMaxTaps) return cudaErrorInvalidValue;
-    const int nt = fir_tiles(n), mw = 128;
-    const size_t sm = ((kFirTile + kFirTile / 16 + 1) + (kFirTile + mw + (kFirTile + mw) / 16 + 1) +
-                       kTapSlices * mw) * sizeof(float);
-    cudaError_t e = allow_smem(k_fir_taps_part, sm);
+template <int J>
+cudaError_t launch_fir_taps_j(const float* g, const float* x, float* part, int64_t B, int64_t n,
+                              int m, int off, cudaStream_t st) {
+    constexpr int TILE = FirTile<J>::TILE;
+    const size_t sm = ((TILE + TILE / 16 + 1) + (TILE + kTapWin + (TILE + kTapWin) / 16 + 1) +
+                       kTapSlices * kTapWin) * sizeof(float);
+    cudaError_t e = allow_smem(k_fir_taps_part<J>, sm);
     if (e == cudaSuccess)
-        e = launch_pdl(k_fir_taps_part, dim3((unsigned)nt, (unsigned)B), kFirThreads, sm, st, g, x,
-                       part, n, m, nt);
+        e = launch_pdl(k_fir_taps_part<J>, dim3((unsigned)fir_tiles(n), (unsigned)B), kFirThreads,
+                       sm, st, g, x, part, n, m, off, fir_tiles(n));
+    return e;
+}
+
+cudaError_t launch_fir_taps(const float* g, const float* x, float* part, float* gh, int64_t B,
+                            int64_t n, int m, int off, cudaStream_t st) {
+    if (m < 1 || m > kFirMaxTaps) return cudaErrorInvalidValue;
+    cudaError_t e = fir_j(n) == 8 ? launch_fir_taps_j<8>(g, x, part, B, n, m, off, st)
+                                  : launch_fir_taps_j<16>(g, x, part, B, n, m, off, st);
     if (e == cudaSuccess)
         e = launch_pdl(k_fir_taps_reduce, dim3((unsigned)((B * m + 255) / 256)), 256, 0, st,
-                       (const float*)part, gh, B, m, nt);
+                       (const float*)part, gh, B, m, fir_tiles(n));
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- MSS loss terms
+// One FFT size of the multi-resolution spectral loss (loss.py:105-126) from
+// the one-sided spectra X (signal, differentiated) and Y (target), complex
+// [B][n] interleaved (n = frames x bins per item):
+//   term_b = sqrt(sum (|X|-|Y|)^2) / max(sqrt(sum |Y|^2), 1e-12)
+//          + mean |log(|X| + eps) - log(|Y| + eps)|
+// and its VJP to X: g_b [ (|X|-|Y|) / (sqrt(S1) ynorm) + sgn(lx - ly) /
+// (n (|X| + eps)) ] X / |X|  (0 where |X| = 0, like the reference's phase
+// mask, loss.py:71-73).  Replaces ~25 elementwise passes of the torch graph
+// (magnitudes, the two norms, logs, the absolute mean and their backward) by
+// one reduction pass and one gradient pass.
+constexpr int kMssThreads = 256;
+
+__device__ __forceinline__ float mss_mag(float2 z) { return sqrtf(z.x * z.x + z.y * z.y); }
+
+__global__ void __launch_bounds__(kMssThreads)
+k_mss_reduce(const float2* __restrict__ X, const float2* __restrict__ Y, int64_t n, float eps,
+             float* __restrict__ part, int nchunk) {
+    grid_dep_wait();
+    const int64_t b = blockIdx.y;
+    const int64_t lo = n * blockIdx.x / nchunk, hi = n * (blockIdx.x + 1) / nchunk;
+    const float2* xb = X + b * n;
+    const float2* yb = Y + b * n;
+    float s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const float mx = mss_mag(xb[i]), my = mss_mag(yb[i]);
+        const float d = mx - my;
+        s1 = fmaf(d, d, s1);
+        s2 = fmaf(my, my, s2);
+        s3 += fabsf(logf(mx + eps) - logf(my + eps));
+    }
+    __shared__ float red[3][kMssThreads / 32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][w] = s1;
+        red[1][w] = s2;
+        red[2][w] = s3;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        float t = 0.f;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[threadIdx.x][k];
+        part[(b * nchunk + blockIdx.x) * 3 + threadIdx.x] = t;
+    }
+}
+
+// per item, chunks summed in a fixed order (double): term[b]; aux[b] =
+// (sqrt(S1), ynorm, n, 0) for the VJP
+__global__ void k_mss_finish(const float* __restrict__ part, int nchunk, int64_t B, int64_t n,
+                             float* __restrict__ term, float* __restrict__ aux) {
+    grid_dep_wait();
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int c = 0; c < nchunk; ++c) {
+        const float* q = part + (b * nchunk + c) * 3;
+        s1 += q[0];
+        s2 += q[1];
+        s3 += q[2];
+    }
+    const double r1 = sqrt(s1), yn = fmax(sqrt(s2), 1e-12);
+    term[b] = (float)(r1 / yn + s3 / (double)n);
+    aux[b * 4 + 0] = (float)r1;
+    aux[b * 4 + 1] = (float)yn;
+    aux[b * 4 + 2] = (float)n;
+    aux[b * 4 + 3] = 0.f;
+}
+
+__global__ void __launch_bounds__(kMssThreads)
+k_mss_grad(const float2* __restrict__ X, const float2* __restrict__ Y,
+           const float* __restrict__ aux, const float* __restrict__ gterm, int64_t B, int64_t n,
+           float eps, float2* __restrict__ gX) {
+    grid_dep_wait();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * n) return;
+    const int64_t b = i / n;
+    const float g = gterm[b];
+    const float r1 = aux[b * 4 + 0], yn = aux[b * 4 + 1];
+    const float2 x = X[i];
+    const float mx = mss_mag(x), my = mss_mag(Y[i]);
+    const float dl = logf(mx + eps) - logf(my + eps);
+    const float sg = dl > 0.f ? 1.f : (dl < 0.f ? -1.f : 0.f);
+    float gm = sg / ((float)n * (mx + eps));
+    if (r1 > 0.f) gm += (mx - my) / (r1 * yn);
+    gm *= g;
+    gX[i] = mx > 0.f ? make_float2(gm * x.x / mx, gm * x.y / mx) : make_float2(0.f, 0.f);
+}
+
+int mss_chunks(int64_t n) { return (int)std::min<int64_t>(64, std::max<int64_t>(1, n / 4096)); }
+
+size_t mss_part_floats(int64_t B, int64_t n) { return (size_t)B * mss_chunks(n) * 3; }
+
+cudaError_t launch_mss_terms(const float* X, const float* Y, int64_t B, int64_t n, float eps,
+                             float* term, float* aux, float* part, cudaStream_t st) {
+    const int nc = mss_chunks(n);
+    cudaError_t e = launch_pdl(k_mss_reduce, dim3((unsigned)nc, (unsigned)B), kMssThreads, 0, st,
+                               reinterpret_cast<const float2*>(X),
+                               reinterpret_cast<const float2*>(Y), n, eps, part, nc);
+    if (e == cudaSuccess)
+        e = launch_pdl(k_mss_finish, dim3((unsigned)((B + 127) / 128)), 128, 0, st,
+                       (const float*)part, nc, B, n, term, aux);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_mss_terms_vjp(const float* X, const float* Y, const float* aux,
+                                 const float* gterm, int64_t B, int64_t n, float eps, float* gX,
+                                 cudaStream_t st) {
+    const int64_t tot = B * n;
+    cudaError_t e = launch_pdl(k_mss_grad, dim3((unsigned)((tot + kMssThreads - 1) / kMssThreads)),
+                               kMssThreads, 0, st, reinterpret_cast<const float2*>(X),
+                               reinterpret_cast<const float2*>(Y), aux, gterm, B, n, eps,
+                               reinterpret_cast<float2*>(gX));
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 

@@ -21,8 +21,15 @@ cudaError_t launch_osc_vjp(const double* f0, const float* pos, const float* tab,
                            const float* taps, const float* gsig, float* part, float* gpos,
                            const OscGeo& g, int os, cudaStream_t st);
 cudaError_t launch_fir(const float* x, const float* taps, float* y, int64_t B, int64_t n, int m,
-                       bool adj, cudaStream_t st);
+                       bool adj, int off, cudaStream_t st);
 size_t fir_taps_part_elems(int64_t B, int64_t n, int m);
 cudaError_t launch_fir_taps(const float* g, const float* x, float* part, float* gh, int64_t B,
-                            int64_t n, int m, cudaStream_t st);
+                            int64_t n, int m, int off, cudaStream_t st);
+int mss_chunks(int64_t n);
+size_t mss_part_floats(int64_t B, int64_t n);
+cudaError_t launch_mss_terms(const float* X, const float* Y, int64_t B, int64_t n, float eps,
+                             float* term, float* aux, float* part, cudaStream_t st);
+cudaError_t launch_mss_terms_vjp(const float* X, const float* Y, const float* aux,
+                                 const float* gterm, int64_t B, int64_t n, float eps, float* gX,
+                                 cudaStream_t st);
 }  // namespace tvlp

@@ -425,9 +425,68 @@ def stft_mag(x, size, hop=None, window=None):
     return torch.abs(torch.fft.rfft(frames, dim=-1))
 
 
+def _spectrum(x, size, hop):
+    """The one-sided spectra of stft_mag's frames (before the magnitude)."""
+    window = _on_device(("hann_periodic", size),
+                        lambda: 0.5 - 0.5 * torch.cos(2.0 * math.pi * torch.arange(
+                            size, dtype=torch.float64) / size), x.device, x.dtype)
+    xp = TF.pad(x[:, None], (size // 2, size // 2), mode="reflect")[:, 0]
+    return torch.fft.rfft(xp.unfold(-1, size, hop) * window, dim=-1)
+
+
+class _MSSTermsB200(torch.autograd.Function):
+    """One FFT size's loss terms from the spectra (tvlp_mss_terms /
+    tvlp_mss_terms_vjp, csrc/decoder_kernels.cu): magnitudes, both norms, the
+    log-magnitude mean and their VJP in two passes instead of the ~25
+    elementwise ops of the torch graph; the FFTs stay cuFFT."""
+
+    @staticmethod
+    def forward(ctx, X, Y, eps):
+        lib = N.load()
+        X, Y = X.contiguous(), Y.contiguous()
+        B = X.shape[0]
+        n = X.numel() // B
+        term = torch.empty(B, dtype=torch.float32, device=X.device)
+        aux = torch.empty(B * 4, dtype=torch.float32, device=X.device)
+        nb = lib.tvlp_mss_terms_workspace(B, n)
+        ws = torch.empty(max(nb, 4) // 4, dtype=torch.float32, device=X.device)
+        with N.on_device(X.device):
+            N.check(lib.tvlp_mss_terms(N.ptr(X), N.ptr(Y), B, n, float(eps), N.ptr(term),
+                                       N.ptr(aux), N.ptr(ws), nb, N.stream_ptr(X.device)))
+        ctx.save_for_backward(X, Y, aux)
+        ctx.eps = float(eps)
+        return term
+
+    @staticmethod
+    def backward(ctx, g):
+        X, Y, aux = ctx.saved_tensors
+        lib = N.load()
+        B = X.shape[0]
+        n = X.numel() // B
+        g = g.contiguous()
+        gX = torch.empty_like(X)
+        with N.on_device(X.device):
+            N.check(lib.tvlp_mss_terms_vjp(N.ptr(X), N.ptr(Y), N.ptr(aux), N.ptr(g), N.ptr(gX), B,
+                                           n, ctx.eps, N.stream_ptr(X.device)))
+        return gX, None, None
+
+
 def mss_loss(x, y, fft_sizes=DEFAULT_FFT_SIZES, eps=LOG_EPS):
     """loss.py:105-126, per item: mean over sizes of spectral convergence +
-    mean |log-magnitude difference|; returns [B] losses."""
+    mean |log-magnitude difference|; returns [B] losses.  float32 CUDA
+    signals compute the terms on tvlp_mss_terms (the spectra on cuFFT)."""
+    if _b200_pieces(x) and x.dim() == 2 and y.shape == x.shape:
+        total = 0.0
+        yd = y.detach().to(x.dtype)
+        for size in fft_sizes:
+            hop = -(-size // 4)
+            if x.shape[-1] < size:
+                raise ValueError(f"signal of length {x.shape[-1]} is shorter than one "
+                                 f"{size}-sample frame")
+            with torch.no_grad():
+                Y = _spectrum(yd, size, hop)
+            total = total + _MSSTermsB200.apply(_spectrum(x, size, hop), Y, eps)
+        return total / len(fft_sizes)
     total = 0.0
     for size in fft_sizes:
         hop = -(-size // 4)

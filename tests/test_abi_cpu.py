@@ -90,8 +90,9 @@ def test_abi_queries_frames_and_split():
 
 
 def test_abi_decoder_entry_points_validate_before_launch():
-    """tvlp_wavetable_osc* / tvlp_global_fir*: argument checks and the
-    workspace query (no kernel launches: B = 0 or rejected arguments)."""
+    """tvlp_wavetable_osc* / tvlp_global_fir* / tvlp_mss_terms*: argument
+    checks and the workspace queries (no kernel launches: B = 0 or rejected
+    arguments)."""
     import ctypes
     lib = N.load()
     fake = ctypes.c_void_p(256)          # never dereferenced: rejected or B = 0
@@ -122,6 +123,13 @@ def test_abi_decoder_entry_points_validate_before_launch():
     assert lib.tvlp_global_fir_workspace(2, 5000, 128) == 2 * 3 * 128 * 4
     assert lib.tvlp_global_fir_workspace(4, 48001, 128) == 4 * 24 * 128 * 4
     assert lib.tvlp_global_fir_vjp(fake, fake, fake, None, fake, None, 0, 2, 5000, 128, None) == 3
+    # MSS loss terms: per-item partials (64 chunks at most) of three sums
+    assert lib.tvlp_mss_terms_workspace(32, 96000) == 32 * (96000 // 4096) * 3 * 4
+    assert lib.tvlp_mss_terms_workspace(2, 10 ** 7) == 2 * 64 * 3 * 4
+    assert lib.tvlp_mss_terms(None, fake, 2, 100, 1e-8, fake, fake, fake, 4096, None) == 1
+    assert lib.tvlp_mss_terms(fake, fake, 2, 100, 1e-8, fake, fake, None, 0, None) == 3
+    assert lib.tvlp_mss_terms(fake, fake, 0, 100, 1e-8, fake, fake, None, 0, None) == 0
+    assert lib.tvlp_mss_terms_vjp(fake, fake, fake, None, fake, 2, 100, 1e-8, None) == 1
 
 
 def test_longseq_combine_algebra():

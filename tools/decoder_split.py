@@ -14,6 +14,7 @@ from paper_2406_05128_b200.params import FramePlan  # noqa: E402
 
 
 def timeit(fn, n=20):
+    """(eager us, CUDA-graph replay us) per call."""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -23,7 +24,24 @@ def timeit(fn, n=20):
         fn()
     b.record()
     torch.cuda.synchronize()
-    return round(a.elapsed_time(b) / n * 1e3, 1)
+    eager = round(a.elapsed_time(b) / n * 1e3, 1)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    g.replay()
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(n):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return eager, round(a.elapsed_time(b) / n * 1e3, 1)
 
 
 def main():
