@@ -267,6 +267,17 @@ int tvlp_global_fir_vjp(const float* grad_y, const float* x, const float* taps, 
                         float* grad_taps, void* workspace, size_t workspace_bytes, int64_t B,
                         int64_t n, int32_t m, void* stream);
 
+/* stft_mag's framing (loss.py:46-63): x [B, n] reflect-padded by N/2, frames
+ * of N samples every `hop`, times window [N] -> frames [B, nframes, N]
+ * (nframes = tvlp_stft_nframes(n, N, hop); 0 = invalid: n < N or
+ * N/2 >= n); the VJP overlap-adds the windowed frame gradients back through
+ * the pads (loss.py:81-86), times `scale`. */
+int64_t tvlp_stft_nframes(int64_t n, int32_t N, int32_t hop);
+int tvlp_stft_frames(const float* x, const float* window, float* frames, int64_t B, int64_t n,
+                     int32_t N, int32_t hop, void* stream);
+int tvlp_stft_frames_vjp(const float* grad_frames, const float* window, float* grad_x, int64_t B,
+                         int64_t n, int32_t N, int32_t hop, float scale, void* stream);
+
 /* One FFT size of the multi-resolution spectral loss (loss.py:105-126) from
  * one-sided spectra (the caller's FFTs): X (signal) and Y (target) complex
  * [B][n] as interleaved float pairs, n = frames x bins per item.

@@ -96,6 +96,10 @@ _SIGS = [
     ("tvlp_global_fir", ctypes.c_int, [_P, _P, _P, _I64, _I64, _I32, _P]),
     ("tvlp_global_fir_workspace", _SZ, [_I64, _I64, _I32]),
     ("tvlp_global_fir_vjp", ctypes.c_int, [_P, _P, _P, _P, _P, _P, _SZ, _I64, _I64, _I32, _P]),
+    ("tvlp_stft_nframes", _I64, [_I64, _I32, _I32]),
+    ("tvlp_stft_frames", ctypes.c_int, [_P, _P, _P, _I64, _I64, _I32, _I32, _P]),
+    ("tvlp_stft_frames_vjp", ctypes.c_int,
+     [_P, _P, _P, _I64, _I64, _I32, _I32, ctypes.c_float, _P]),
     ("tvlp_mss_terms_workspace", _SZ, [_I64, _I64]),
     ("tvlp_mss_terms", ctypes.c_int, [_P, _P, _I64, _I64, ctypes.c_float, _P, _P, _P, _SZ, _P]),
     ("tvlp_mss_terms_vjp", ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, ctypes.c_float, _P]),
@@ -139,7 +143,7 @@ def load(path=None):
 
 _PURE = ("tvlp_workspace_bytes", "tvlp_carry_elems", "tvlp_max_order",
          "tvlp_framewise_aux_elems", "tvlp_framewise_nframes", "tvlp_subchunk_len",
-         "tvlp_global_fir_workspace", "tvlp_mss_terms_workspace")
+         "tvlp_global_fir_workspace", "tvlp_mss_terms_workspace", "tvlp_stft_nframes")
 
 
 def on_device(device):

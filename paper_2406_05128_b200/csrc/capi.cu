@@ -1134,6 +1134,33 @@ int tvlp_global_fir(const float* x, const float* taps, float* y, int64_t B, int6
     return TVLP_OK;
 }
 
+int64_t tvlp_stft_nframes(int64_t n, int32_t N, int32_t hop) {
+    if (n < 1 || N < 2 || hop < 1 || n < N || N / 2 >= n) return 0;
+    return 1 + (n + 2 * (N / 2) - N) / hop;
+}
+
+int tvlp_stft_frames(const float* x, const float* window, float* frames, int64_t B, int64_t n,
+                     int32_t N, int32_t hop, void* stream) {
+    if (!x || !window || !frames || B < 0 || tvlp_stft_nframes(n, N, hop) == 0) return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("stft_frames", 1, st,
+                    [&] { return launch_stft_frames(x, window, frames, B, n, N, hop, st); }));
+    return TVLP_OK;
+}
+
+int tvlp_stft_frames_vjp(const float* grad_frames, const float* window, float* grad_x, int64_t B,
+                         int64_t n, int32_t N, int32_t hop, float scale, void* stream) {
+    if (!grad_frames || !window || !grad_x || B < 0 || tvlp_stft_nframes(n, N, hop) == 0)
+        return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("stft_frames_vjp", 1, st, [&] {
+        return launch_stft_frames_vjp(grad_frames, window, grad_x, B, n, N, hop, scale, st);
+    }));
+    return TVLP_OK;
+}
+
 size_t tvlp_mss_terms_workspace(int64_t B, int64_t n) {
     if (B < 0 || n < 1) return 0;
     return mss_part_floats(B, n) * sizeof(float);

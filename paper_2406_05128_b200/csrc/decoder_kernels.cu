@@ -650,4 +650,82 @@ cudaError_t launch_mss_terms_vjp(const float* X, const float* Y, const float* au
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- STFT frames
+// stft_mag's framing (loss.py:46-63): reflect-padded by N/2, frames of N at
+// `hop`, times the window -- one pass writing the FFT input (the torch graph
+// pads, unfolds and multiplies: three), and its adjoint: each signal sample
+// gathers, in a fixed order, the windowed frame gradients of the padded
+// positions that map to it (itself and its reflections in the pads,
+// loss.py:81-86), scaled by `scale` (the caller's inverse-FFT normalisation).
+__device__ __forceinline__ int64_t reflect_index(int64_t i, int64_t n) {
+    if (i < 0) i = -i;
+    if (i >= n) i = 2 * (n - 1) - i;
+    return i;
+}
+
+__global__ void k_stft_frames(const float* __restrict__ x, const float* __restrict__ win,
+                              float* __restrict__ fr, int64_t B, int64_t n, int N, int hop,
+                              int64_t nfr) {
+    grid_dep_wait();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = nfr * N;
+    if (i >= B * per) return;
+    const int64_t b = i / per, r = i - b * per;
+    const int64_t f = r / N;
+    const int j = (int)(r - f * N);
+    const int64_t t = reflect_index(f * hop + j - N / 2, n);
+    fr[i] = x[b * n + t] * win[j];
+}
+
+// grad of padded position p: sum over frames f with 0 <= p - f hop < N
+__device__ __forceinline__ float stft_pad_grad(const float* __restrict__ gfb,
+                                               const float* __restrict__ win, int64_t p, int N,
+                                               int hop, int64_t nfr) {
+    int64_t f1 = p / hop;
+    if (f1 > nfr - 1) f1 = nfr - 1;
+    int64_t f0 = p - (N - 1);
+    f0 = f0 <= 0 ? 0 : (f0 + hop - 1) / hop;
+    float s = 0.f;
+    for (int64_t f = f0; f <= f1; ++f) {
+        const int j = (int)(p - f * hop);
+        s = fmaf(gfb[f * N + j], win[j], s);
+    }
+    return s;
+}
+
+__global__ void k_stft_frames_vjp(const float* __restrict__ gfr, const float* __restrict__ win,
+                                  float* __restrict__ gx, int64_t B, int64_t n, int N, int hop,
+                                  int64_t nfr, float scale) {
+    grid_dep_wait();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * n) return;
+    const int64_t b = i / n, t = i - b * n;
+    const int64_t pad = N / 2;
+    const float* gfb = gfr + b * nfr * N;
+    // padded positions mapping to t: t + pad; pad - t (left mirror, 1 <= t <= pad);
+    // pad + 2(n-1) - t (right mirror, n-1-pad <= t <= n-2)
+    float s = stft_pad_grad(gfb, win, t + pad, N, hop, nfr);
+    if (t >= 1 && t <= pad) s += stft_pad_grad(gfb, win, pad - t, N, hop, nfr);
+    if (t <= n - 2 && t >= n - 1 - pad) s += stft_pad_grad(gfb, win, pad + 2 * (n - 1) - t, N, hop, nfr);
+    gx[i] = s * scale;
+}
+
+cudaError_t launch_stft_frames(const float* x, const float* win, float* fr, int64_t B, int64_t n,
+                               int N, int hop, cudaStream_t st) {
+    const int64_t nfr = 1 + (n + 2 * (N / 2) - N) / hop;
+    const int64_t tot = B * nfr * N;
+    cudaError_t e = launch_pdl(k_stft_frames, dim3((unsigned)((tot + 255) / 256)), 256, 0, st, x,
+                               win, fr, B, n, N, hop, nfr);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_stft_frames_vjp(const float* gfr, const float* win, float* gx, int64_t B,
+                                   int64_t n, int N, int hop, float scale, cudaStream_t st) {
+    const int64_t nfr = 1 + (n + 2 * (N / 2) - N) / hop;
+    const int64_t tot = B * n;
+    cudaError_t e = launch_pdl(k_stft_frames_vjp, dim3((unsigned)((tot + 255) / 256)), 256, 0, st,
+                               gfr, win, gx, B, n, N, hop, nfr, scale);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace tvlp

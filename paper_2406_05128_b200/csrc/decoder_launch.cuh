@@ -32,4 +32,8 @@ cudaError_t launch_mss_terms(const float* X, const float* Y, int64_t B, int64_t 
 cudaError_t launch_mss_terms_vjp(const float* X, const float* Y, const float* aux,
                                  const float* gterm, int64_t B, int64_t n, float eps, float* gX,
                                  cudaStream_t st);
+cudaError_t launch_stft_frames(const float* x, const float* win, float* fr, int64_t B, int64_t n,
+                               int N, int hop, cudaStream_t st);
+cudaError_t launch_stft_frames_vjp(const float* gfr, const float* win, float* gx, int64_t B,
+                                   int64_t n, int N, int hop, float scale, cudaStream_t st);
 }  // namespace tvlp

@@ -425,13 +425,47 @@ def stft_mag(x, size, hop=None, window=None):
     return torch.abs(torch.fft.rfft(frames, dim=-1))
 
 
-def _spectrum(x, size, hop):
-    """The one-sided spectra of stft_mag's frames (before the magnitude)."""
-    window = _on_device(("hann_periodic", size),
-                        lambda: 0.5 - 0.5 * torch.cos(2.0 * math.pi * torch.arange(
-                            size, dtype=torch.float64) / size), x.device, x.dtype)
-    xp = TF.pad(x[:, None], (size // 2, size // 2), mode="reflect")[:, 0]
-    return torch.fft.rfft(xp.unfold(-1, size, hop) * window, dim=-1)
+def _hann_periodic(size, device, dtype):
+    return _on_device(("hann_periodic", size),
+                      lambda: 0.5 - 0.5 * torch.cos(2.0 * math.pi * torch.arange(
+                          size, dtype=torch.float64) / size), device, dtype)
+
+
+class _SpectrumB200(torch.autograd.Function):
+    """One-sided spectra of stft_mag's windowed, reflect-padded frames
+    (loss.py:46-63): the framing on tvlp_stft_frames, the DFT on cuFFT; the
+    VJP is the reference's adjoint (loss.py:74-86): one c2r inverse FFT of
+    the one-sided gradient (bins >= 1 halved: irfft doubles them) and
+    tvlp_stft_frames_vjp's windowed overlap-add through the pads."""
+
+    @staticmethod
+    def forward(ctx, x, size, hop):
+        lib = N.load()
+        x = x.contiguous()
+        B, n = x.shape
+        nfr = lib.tvlp_stft_nframes(n, size, hop)
+        win = _hann_periodic(size, x.device, x.dtype)
+        fr = torch.empty((B, nfr, size), dtype=x.dtype, device=x.device)
+        with N.on_device(x.device):
+            N.check(lib.tvlp_stft_frames(N.ptr(x), N.ptr(win), N.ptr(fr), B, n, size, hop,
+                                         N.stream_ptr(x.device)))
+        ctx.cfg = (B, n, size, hop)
+        return torch.fft.rfft(fr, dim=-1)
+
+    @staticmethod
+    def backward(ctx, gX):
+        B, n, size, hop = ctx.cfg
+        lib = N.load()
+        half = _on_device(("rfft_adjoint_scale", size), lambda: torch.tensor(
+            [1.0] + [0.5] * ((size - 1) // 2) + ([1.0] if size % 2 == 0 else [])),
+            gX.device, torch.float32)
+        gfr = torch.fft.irfft(gX * half, n=size, dim=-1).contiguous()
+        win = _hann_periodic(size, gX.device, torch.float32)
+        gx = torch.empty((B, n), dtype=torch.float32, device=gX.device)
+        with N.on_device(gX.device):
+            N.check(lib.tvlp_stft_frames_vjp(N.ptr(gfr), N.ptr(win), N.ptr(gx), B, n, size, hop,
+                                             float(size), N.stream_ptr(gX.device)))
+        return gx, None, None
 
 
 class _MSSTermsB200(torch.autograd.Function):
@@ -484,8 +518,8 @@ def mss_loss(x, y, fft_sizes=DEFAULT_FFT_SIZES, eps=LOG_EPS):
                 raise ValueError(f"signal of length {x.shape[-1]} is shorter than one "
                                  f"{size}-sample frame")
             with torch.no_grad():
-                Y = _spectrum(yd, size, hop)
-            total = total + _MSSTermsB200.apply(_spectrum(x, size, hop), Y, eps)
+                Y = _SpectrumB200.apply(yd, size, hop)
+            total = total + _MSSTermsB200.apply(_SpectrumB200.apply(x, size, hop), Y, eps)
         return total / len(fft_sizes)
     total = 0.0
     for size in fft_sizes:
