@@ -267,6 +267,21 @@ int tvlp_global_fir_vjp(const float* grad_y, const float* x, const float* taps, 
                         float* grad_taps, void* workspace, size_t workspace_bytes, int64_t B,
                         int64_t n, int32_t m, void* stream);
 
+/* shape_noise's framing and overlap-add (source.py:367-428) for hop-spaced
+ * frames: frame i starts at sample start0 + i hop (samples outside [0, n)
+ * read as 0 / are dropped).  tvlp_noise_frames: frames [B, nframes, nfft] =
+ * noise [B, n] times window [size], zero-padded to nfft (the FFT input).
+ * tvlp_frame_ola: out [B, n] = scale * sum over frames of y [B, nframes, ld]
+ * read from column `delay` on (adjoint = 0), or its adjoint (adjoint = 1:
+ * y is the output gradient [B, n], out the frame gradient [B, nframes, ld],
+ * zero outside the read columns).  Fixed-order gathers, no atomics. */
+int tvlp_noise_frames(const float* noise, const float* window, float* frames, int64_t B,
+                      int64_t n, int64_t nframes, int32_t size, int32_t nfft, int64_t start0,
+                      int32_t hop, void* stream);
+int tvlp_frame_ola(const float* y, float* out, int64_t B, int64_t n, int64_t nframes, int32_t size,
+                   int32_t ld, int32_t delay, int64_t start0, int32_t hop, float scale,
+                   int32_t adjoint, void* stream);
+
 /* stft_mag's framing (loss.py:46-63): x [B, n] reflect-padded by N/2, frames
  * of N samples every `hop`, times window [N] -> frames [B, nframes, N]
  * (nframes = tvlp_stft_nframes(n, N, hop); 0 = invalid: n < N or

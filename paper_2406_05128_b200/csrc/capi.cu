@@ -1134,6 +1134,39 @@ int tvlp_global_fir(const float* x, const float* taps, float* y, int64_t B, int6
     return TVLP_OK;
 }
 
+static bool noise_geo_ok(int64_t B, int64_t n, int64_t nfr, int32_t size, int32_t ld,
+                         int32_t delay, int32_t hop) {
+    return B >= 0 && n >= 1 && nfr >= 1 && size >= 1 && hop >= 1 && delay >= 0 &&
+           ld >= size + delay;
+}
+
+int tvlp_noise_frames(const float* noise, const float* window, float* frames, int64_t B,
+                      int64_t n, int64_t nframes, int32_t size, int32_t nfft, int64_t start0,
+                      int32_t hop, void* stream) {
+    if (!noise || !window || !frames || !noise_geo_ok(B, n, nframes, size, nfft, 0, hop))
+        return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("noise_frames", 1, st, [&] {
+        return launch_noise_frames(noise, window, frames, B, n, nframes, size, nfft, start0, hop,
+                                   st);
+    }));
+    return TVLP_OK;
+}
+
+int tvlp_frame_ola(const float* y, float* out, int64_t B, int64_t n, int64_t nframes, int32_t size,
+                   int32_t ld, int32_t delay, int64_t start0, int32_t hop, float scale,
+                   int32_t adjoint, void* stream) {
+    if (!y || !out || !noise_geo_ok(B, n, nframes, size, ld, delay, hop)) return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked(adjoint ? "frame_ola_vjp" : "frame_ola", 1, st, [&] {
+        return launch_frame_ola(y, out, B, n, nframes, size, ld, delay, start0, hop, scale,
+                                adjoint != 0, st);
+    }));
+    return TVLP_OK;
+}
+
 int64_t tvlp_stft_nframes(int64_t n, int32_t N, int32_t hop) {
     if (n < 1 || N < 2 || hop < 1 || n < N || N / 2 >= n) return 0;
     return 1 + (n + 2 * (N / 2) - N) / hop;

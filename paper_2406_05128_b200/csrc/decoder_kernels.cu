@@ -728,4 +728,84 @@ cudaError_t launch_stft_frames_vjp(const float* gfr, const float* win, float* gx
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- noise frames
+// shape_noise's framing and overlap-add (source.py:367-428) for hop-spaced
+// frames (frame i starts at sample s_i = start0 + i hop; samples outside
+// [0, n) are zero / dropped):
+//   frames[b][i][j] = noise[b][s_i + j] win[j] for j < size, 0 up to nfft
+//     (the FFT input, zero-padded in the same pass);
+//   out[b][t] = inv_cola sum_{i: 0 <= t - s_i < size} y[b][i][t - s_i + delay]
+//     (a fixed-order gather: no scatter, no atomics) and its adjoint.
+__global__ void k_noise_frames(const float* __restrict__ noise, const float* __restrict__ win,
+                               float* __restrict__ fr, int64_t B, int64_t n, int64_t nfr,
+                               int size, int nfft, int64_t start0, int hop) {
+    grid_dep_wait();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = nfr * nfft;
+    if (i >= B * per) return;
+    const int64_t b = i / per, r = i - b * per;
+    const int64_t f = r / nfft;
+    const int j = (int)(r - f * nfft);
+    const int64_t t = start0 + f * hop + j;
+    fr[i] = (j < size && t >= 0 && t < n) ? noise[b * n + t] * win[j] : 0.f;
+}
+
+__global__ void k_frame_ola(const float* __restrict__ y, float* __restrict__ out, int64_t B,
+                            int64_t n, int64_t nfr, int size, int ld, int delay, int64_t start0,
+                            int hop, float inv_cola) {
+    grid_dep_wait();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * n) return;
+    const int64_t b = i / n, t = i - b * n;
+    // frames with 0 <= t - start0 - f hop < size
+    const int64_t u = t - start0;
+    int64_t f1 = u / hop;
+    if (f1 > nfr - 1) f1 = nfr - 1;
+    int64_t f0 = u - (size - 1);
+    f0 = f0 <= 0 ? 0 : (f0 + hop - 1) / hop;
+    float s = 0.f;
+    const float* yb = y + b * nfr * ld;
+    for (int64_t f = f0; f <= f1; ++f) s += yb[f * ld + (u - f * hop) + delay];
+    out[i] = s * inv_cola;
+}
+
+__global__ void k_frame_ola_vjp(const float* __restrict__ g, float* __restrict__ gy, int64_t B,
+                                int64_t n, int64_t nfr, int size, int ld, int delay,
+                                int64_t start0, int hop, float inv_cola) {
+    grid_dep_wait();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = nfr * ld;
+    if (i >= B * per) return;
+    const int64_t b = i / per, r = i - b * per;
+    const int64_t f = r / ld;
+    const int j = (int)(r - f * ld) - delay;
+    const int64_t t = start0 + f * hop + j;
+    gy[i] = (j >= 0 && j < size && t >= 0 && t < n) ? g[b * n + t] * inv_cola : 0.f;
+}
+
+cudaError_t launch_noise_frames(const float* noise, const float* win, float* fr, int64_t B,
+                                int64_t n, int64_t nfr, int size, int nfft, int64_t start0, int hop,
+                                cudaStream_t st) {
+    const int64_t tot = B * nfr * nfft;
+    cudaError_t e = launch_pdl(k_noise_frames, dim3((unsigned)((tot + 255) / 256)), 256, 0, st,
+                               noise, win, fr, B, n, nfr, size, nfft, start0, hop);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_frame_ola(const float* y, float* out, int64_t B, int64_t n, int64_t nfr,
+                             int size, int ld, int delay, int64_t start0, int hop, float inv_cola,
+                             bool adj, cudaStream_t st) {
+    cudaError_t e;
+    if (!adj) {
+        const int64_t tot = B * n;
+        e = launch_pdl(k_frame_ola, dim3((unsigned)((tot + 255) / 256)), 256, 0, st, y, out, B, n,
+                       nfr, size, ld, delay, start0, hop, inv_cola);
+    } else {
+        const int64_t tot = B * nfr * ld;
+        e = launch_pdl(k_frame_ola_vjp, dim3((unsigned)((tot + 255) / 256)), 256, 0, st, y, out, B,
+                       n, nfr, size, ld, delay, start0, hop, inv_cola);
+    }
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace tvlp

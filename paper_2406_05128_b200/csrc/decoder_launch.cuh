@@ -36,4 +36,10 @@ cudaError_t launch_stft_frames(const float* x, const float* win, float* fr, int6
                                int N, int hop, cudaStream_t st);
 cudaError_t launch_stft_frames_vjp(const float* gfr, const float* win, float* gx, int64_t B,
                                    int64_t n, int N, int hop, float scale, cudaStream_t st);
+cudaError_t launch_noise_frames(const float* noise, const float* win, float* fr, int64_t B,
+                                int64_t n, int64_t nfr, int size, int nfft, int64_t start0, int hop,
+                                cudaStream_t st);
+cudaError_t launch_frame_ola(const float* y, float* out, int64_t B, int64_t n, int64_t nfr,
+                             int size, int ld, int delay, int64_t start0, int hop, float inv_cola,
+                             bool adj, cudaStream_t st);
 }  // namespace tvlp

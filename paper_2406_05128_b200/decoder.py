@@ -330,6 +330,41 @@ def _frame_index_host(plan, n_out, F):
     return torch.as_tensor(np.array(rows)), torch.as_tensor(np.stack(idx))
 
 
+def _frame_starts(plan, n_out, F):
+    """Sample index of frame 0's window start: plan.iter_frames yields every
+    frame from -n_lead_in to F - 1 at hop spacing (params.py:163-171)."""
+    return -plan.n_lead_in() * plan.hop
+
+
+class _FrameOLAB200(torch.autograd.Function):
+    """shape_noise's overlap-add of the filtered frames, read from the FIR's
+    delay on, / COLA (source.py:418-428), as a fixed-order gather
+    (tvlp_frame_ola) and its adjoint."""
+
+    @staticmethod
+    def forward(ctx, y, n_out, size, delay, start0, hop, scale):
+        lib = N.load()
+        y = y.contiguous()
+        Bn, nfr, ld = y.shape
+        out = torch.empty((Bn, n_out), dtype=y.dtype, device=y.device)
+        with N.on_device(y.device):
+            N.check(lib.tvlp_frame_ola(N.ptr(y), N.ptr(out), Bn, n_out, nfr, size, ld, delay,
+                                       start0, hop, scale, 0, N.stream_ptr(y.device)))
+        ctx.cfg = (Bn, nfr, ld, n_out, size, delay, start0, hop, scale)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        Bn, nfr, ld, n_out, size, delay, start0, hop, scale = ctx.cfg
+        lib = N.load()
+        g = g.contiguous()
+        gy = torch.empty((Bn, nfr, ld), dtype=g.dtype, device=g.device)
+        with N.on_device(g.device):
+            N.check(lib.tvlp_frame_ola(N.ptr(g), N.ptr(gy), Bn, n_out, nfr, size, ld, delay,
+                                       start0, hop, scale, 1, N.stream_ptr(g.device)))
+        return gy, None, None, None, None, None, None
+
+
 def shape_noise(logmag, noise, plan):
     """source.py:367-428 for [B, F, 256] log-magnitudes and [B, n_out] unit
     noise: each windowed noise frame convolved with its frame's FIR (the
@@ -346,11 +381,27 @@ def shape_noise(logmag, noise, plan):
     rows, idx = _frame_index(plan, n_out, F, dev)
     fir = fir_from_logmag(logmag)                                 # [B, F, 510]
     win = plan._window_tensor(dt, dev)
+    n_fir = fir.shape[-1]
+    nfft = 1 << (size + n_fir - 2).bit_length()
+    start0 = _frame_starts(plan, n_out, F)
+    if (_b200_pieces(logmag) and noise.dtype == dt and not noise.requires_grad
+            and rows.shape[0] == plan.n_lead_in() + F):
+        # framing (+ zero pad to nfft) and the overlap-add on the kernels of
+        # csrc/decoder_kernels.cu; the spectra stay cuFFT
+        lib = N.load()
+        noise = noise.contiguous()
+        nfr = rows.shape[0]
+        segs = torch.empty((Bn, nfr, nfft), dtype=dt, device=dev)
+        with N.on_device(dev):
+            N.check(lib.tvlp_noise_frames(N.ptr(noise), N.ptr(win), N.ptr(segs), Bn, n_out, nfr,
+                                          size, nfft, start0, plan.hop, N.stream_ptr(dev)))
+        spec = torch.fft.rfft(segs) * torch.fft.rfft(fir[:, rows], n=nfft)
+        y = torch.fft.irfft(spec, n=nfft)                         # [B, nfr, nfft]
+        return _FrameOLAB200.apply(y, n_out, size, delay, start0, plan.hop,
+                                   1.0 / plan._cola_cached())
     valid = idx >= 0
     segs = torch.where(valid, noise[:, idx.clamp(min=0)], torch.zeros((), dtype=dt, device=dev))
     segs = segs * win                                            # [B, nfr, size]
-    n_fir = fir.shape[-1]
-    nfft = 1 << (size + n_fir - 2).bit_length()
     spec = torch.fft.rfft(segs, n=nfft) * torch.fft.rfft(fir[:, rows], n=nfft)
     y = torch.fft.irfft(spec, n=nfft)[..., delay:delay + size]   # [B, nfr, size]
     out = torch.zeros((Bn, n_out + 1), dtype=dt, device=dev)     # (slot n_out: padding)
