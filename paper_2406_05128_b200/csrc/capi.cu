@@ -1136,8 +1136,9 @@ int tvlp_global_fir(const float* x, const float* taps, float* y, int64_t B, int6
 
 static bool noise_geo_ok(int64_t B, int64_t n, int64_t nfr, int32_t size, int32_t ld,
                          int32_t delay, int32_t hop) {
-    return B >= 0 && n >= 1 && nfr >= 1 && size >= 1 && hop >= 1 && delay >= 0 &&
-           ld >= size + delay;
+    // (grid y covers one item's samples / one frame row in blocks of 256)
+    return B >= 0 && n >= 1 && n <= (1 << 24) && nfr >= 1 && size >= 1 && hop >= 1 &&
+           delay >= 0 && ld >= size + delay && ld <= (1 << 24);
 }
 
 int tvlp_noise_frames(const float* noise, const float* window, float* frames, int64_t B,
@@ -1168,7 +1169,7 @@ int tvlp_frame_ola(const float* y, float* out, int64_t B, int64_t n, int64_t nfr
 }
 
 int64_t tvlp_stft_nframes(int64_t n, int32_t N, int32_t hop) {
-    if (n < 1 || N < 2 || hop < 1 || n < N || N / 2 >= n) return 0;
+    if (n < 1 || n > (1 << 24) || N < 2 || hop < 1 || n < N || N / 2 >= n) return 0;
     return 1 + (n + 2 * (N / 2) - N) / hop;
 }
 
@@ -1201,7 +1202,8 @@ size_t tvlp_mss_terms_workspace(int64_t B, int64_t n) {
 
 int tvlp_mss_terms(const float* X, const float* Y, int64_t B, int64_t n, float eps, float* term,
                    float* aux, void* workspace, size_t workspace_bytes, void* stream) {
-    if (!X || !Y || !term || !aux || B < 0 || n < 1 || !(eps >= 0.f)) return TVLP_ERR_ARG;
+    if (!X || !Y || !term || !aux || B < 0 || n < 1 || n > (1 << 24) || !(eps >= 0.f))
+        return TVLP_ERR_ARG;
     if (B == 0) return TVLP_OK;
     if (!workspace || workspace_bytes < tvlp_mss_terms_workspace(B, n)) return TVLP_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1213,7 +1215,8 @@ int tvlp_mss_terms(const float* X, const float* Y, int64_t B, int64_t n, float e
 
 int tvlp_mss_terms_vjp(const float* X, const float* Y, const float* aux, const float* grad_term,
                        float* grad_X, int64_t B, int64_t n, float eps, void* stream) {
-    if (!X || !Y || !aux || !grad_term || !grad_X || B < 0 || n < 1) return TVLP_ERR_ARG;
+    if (!X || !Y || !aux || !grad_term || !grad_X || B < 0 || n < 1 || n > (1 << 24))
+        return TVLP_ERR_ARG;
     if (B == 0) return TVLP_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     TVLP_CK(tracked("mss_terms_vjp", 1, st, [&] {

@@ -608,9 +608,10 @@ k_mss_grad(const float2* __restrict__ X, const float2* __restrict__ Y,
            const float* __restrict__ aux, const float* __restrict__ gterm, int64_t B, int64_t n,
            float eps, float2* __restrict__ gX) {
     grid_dep_wait();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= B * n) return;
-    const int64_t b = i / n;
+    const int64_t b = blockIdx.x;   // grid: (items, element blocks): no 64-bit division
+    const int64_t k = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int64_t i = b * n + k;
     const float g = gterm[b];
     const float r1 = aux[b * 4 + 0], yn = aux[b * 4 + 1];
     const float2 x = X[i];
@@ -642,8 +643,8 @@ cudaError_t launch_mss_terms(const float* X, const float* Y, int64_t B, int64_t 
 cudaError_t launch_mss_terms_vjp(const float* X, const float* Y, const float* aux,
                                  const float* gterm, int64_t B, int64_t n, float eps, float* gX,
                                  cudaStream_t st) {
-    const int64_t tot = B * n;
-    cudaError_t e = launch_pdl(k_mss_grad, dim3((unsigned)((tot + kMssThreads - 1) / kMssThreads)),
+    cudaError_t e = launch_pdl(k_mss_grad,
+                               dim3((unsigned)B, (unsigned)((n + kMssThreads - 1) / kMssThreads)),
                                kMssThreads, 0, st, reinterpret_cast<const float2*>(X),
                                reinterpret_cast<const float2*>(Y), aux, gterm, B, n, eps,
                                reinterpret_cast<float2*>(gX));
@@ -663,32 +664,31 @@ __device__ __forceinline__ int64_t reflect_index(int64_t i, int64_t n) {
     return i;
 }
 
+// grid: (frame rows b * nfr + f, column blocks) -- no 64-bit division per element
 __global__ void k_stft_frames(const float* __restrict__ x, const float* __restrict__ win,
                               float* __restrict__ fr, int64_t B, int64_t n, int N, int hop,
                               int64_t nfr) {
     grid_dep_wait();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t per = nfr * N;
-    if (i >= B * per) return;
-    const int64_t b = i / per, r = i - b * per;
-    const int64_t f = r / N;
-    const int j = (int)(r - f * N);
+    const int j = blockIdx.y * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    const int64_t row = blockIdx.x;
+    const int64_t b = row / nfr, f = row - b * nfr;
     const int64_t t = reflect_index(f * hop + j - N / 2, n);
-    fr[i] = x[b * n + t] * win[j];
+    fr[row * N + j] = x[b * n + t] * win[j];
 }
 
 // grad of padded position p: sum over frames f with 0 <= p - f hop < N
 __device__ __forceinline__ float stft_pad_grad(const float* __restrict__ gfb,
-                                               const float* __restrict__ win, int64_t p, int N,
-                                               int hop, int64_t nfr) {
-    int64_t f1 = p / hop;
+                                               const float* __restrict__ win, int p, int N,
+                                               int hop, int nfr) {
+    int f1 = p / hop;
     if (f1 > nfr - 1) f1 = nfr - 1;
-    int64_t f0 = p - (N - 1);
+    int f0 = p - (N - 1);
     f0 = f0 <= 0 ? 0 : (f0 + hop - 1) / hop;
     float s = 0.f;
-    for (int64_t f = f0; f <= f1; ++f) {
-        const int j = (int)(p - f * hop);
-        s = fmaf(gfb[f * N + j], win[j], s);
+    for (int f = f0; f <= f1; ++f) {
+        const int j = p - f * hop;
+        s = fmaf(gfb[(int64_t)f * N + j], win[j], s);
     }
     return s;
 }
@@ -697,34 +697,34 @@ __global__ void k_stft_frames_vjp(const float* __restrict__ gfr, const float* __
                                   float* __restrict__ gx, int64_t B, int64_t n, int N, int hop,
                                   int64_t nfr, float scale) {
     grid_dep_wait();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= B * n) return;
-    const int64_t b = i / n, t = i - b * n;
-    const int64_t pad = N / 2;
+    const int64_t b = blockIdx.x;
+    const int t = blockIdx.y * blockDim.x + threadIdx.x;   // (n < 2^31: 32-bit index math)
+    if (t >= n) return;
+    const int64_t i = b * n + t;
+    const int pad = N / 2, nn = (int)n, nf = (int)nfr;
     const float* gfb = gfr + b * nfr * N;
     // padded positions mapping to t: t + pad; pad - t (left mirror, 1 <= t <= pad);
     // pad + 2(n-1) - t (right mirror, n-1-pad <= t <= n-2)
-    float s = stft_pad_grad(gfb, win, t + pad, N, hop, nfr);
-    if (t >= 1 && t <= pad) s += stft_pad_grad(gfb, win, pad - t, N, hop, nfr);
-    if (t <= n - 2 && t >= n - 1 - pad) s += stft_pad_grad(gfb, win, pad + 2 * (n - 1) - t, N, hop, nfr);
+    float s = stft_pad_grad(gfb, win, t + pad, N, hop, nf);
+    if (t >= 1 && t <= pad) s += stft_pad_grad(gfb, win, pad - t, N, hop, nf);
+    if (t <= nn - 2 && t >= nn - 1 - pad)
+        s += stft_pad_grad(gfb, win, pad + 2 * (nn - 1) - t, N, hop, nf);
     gx[i] = s * scale;
 }
 
 cudaError_t launch_stft_frames(const float* x, const float* win, float* fr, int64_t B, int64_t n,
                                int N, int hop, cudaStream_t st) {
     const int64_t nfr = 1 + (n + 2 * (N / 2) - N) / hop;
-    const int64_t tot = B * nfr * N;
-    cudaError_t e = launch_pdl(k_stft_frames, dim3((unsigned)((tot + 255) / 256)), 256, 0, st, x,
-                               win, fr, B, n, N, hop, nfr);
+    cudaError_t e = launch_pdl(k_stft_frames, dim3((unsigned)(B * nfr), (unsigned)((N + 255) / 256)),
+                               256, 0, st, x, win, fr, B, n, N, hop, nfr);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_stft_frames_vjp(const float* gfr, const float* win, float* gx, int64_t B,
                                    int64_t n, int N, int hop, float scale, cudaStream_t st) {
     const int64_t nfr = 1 + (n + 2 * (N / 2) - N) / hop;
-    const int64_t tot = B * n;
-    cudaError_t e = launch_pdl(k_stft_frames_vjp, dim3((unsigned)((tot + 255) / 256)), 256, 0, st,
-                               gfr, win, gx, B, n, N, hop, nfr, scale);
+    cudaError_t e = launch_pdl(k_stft_frames_vjp, dim3((unsigned)B, (unsigned)((n + 255) / 256)),
+                               256, 0, st, gfr, win, gx, B, n, N, hop, nfr, scale);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -740,23 +740,22 @@ __global__ void k_noise_frames(const float* __restrict__ noise, const float* __r
                                float* __restrict__ fr, int64_t B, int64_t n, int64_t nfr,
                                int size, int nfft, int64_t start0, int hop) {
     grid_dep_wait();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t per = nfr * nfft;
-    if (i >= B * per) return;
-    const int64_t b = i / per, r = i - b * per;
-    const int64_t f = r / nfft;
-    const int j = (int)(r - f * nfft);
+    const int j = blockIdx.y * blockDim.x + threadIdx.x;   // grid: (frame rows, columns)
+    if (j >= nfft) return;
+    const int64_t row = blockIdx.x;
+    const int64_t b = row / nfr, f = row - b * nfr;
     const int64_t t = start0 + f * hop + j;
-    fr[i] = (j < size && t >= 0 && t < n) ? noise[b * n + t] * win[j] : 0.f;
+    fr[row * nfft + j] = (j < size && t >= 0 && t < n) ? noise[b * n + t] * win[j] : 0.f;
 }
 
 __global__ void k_frame_ola(const float* __restrict__ y, float* __restrict__ out, int64_t B,
                             int64_t n, int64_t nfr, int size, int ld, int delay, int64_t start0,
                             int hop, float inv_cola) {
     grid_dep_wait();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= B * n) return;
-    const int64_t b = i / n, t = i - b * n;
+    const int64_t b = blockIdx.x;                            // grid: (items, samples)
+    const int64_t t = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int64_t i = b * n + t;
     // frames with 0 <= t - start0 - f hop < size
     const int64_t u = t - start0;
     int64_t f1 = u / hop;
@@ -773,22 +772,21 @@ __global__ void k_frame_ola_vjp(const float* __restrict__ g, float* __restrict__
                                 int64_t n, int64_t nfr, int size, int ld, int delay,
                                 int64_t start0, int hop, float inv_cola) {
     grid_dep_wait();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t per = nfr * ld;
-    if (i >= B * per) return;
-    const int64_t b = i / per, r = i - b * per;
-    const int64_t f = r / ld;
-    const int j = (int)(r - f * ld) - delay;
+    const int jc = blockIdx.y * blockDim.x + threadIdx.x;  // grid: (frame rows, columns)
+    if (jc >= ld) return;
+    const int64_t row = blockIdx.x;
+    const int64_t b = row / nfr, f = row - b * nfr;
+    const int j = jc - delay;
     const int64_t t = start0 + f * hop + j;
-    gy[i] = (j >= 0 && j < size && t >= 0 && t < n) ? g[b * n + t] * inv_cola : 0.f;
+    gy[row * ld + jc] = (j >= 0 && j < size && t >= 0 && t < n) ? g[b * n + t] * inv_cola : 0.f;
 }
 
 cudaError_t launch_noise_frames(const float* noise, const float* win, float* fr, int64_t B,
                                 int64_t n, int64_t nfr, int size, int nfft, int64_t start0, int hop,
                                 cudaStream_t st) {
-    const int64_t tot = B * nfr * nfft;
-    cudaError_t e = launch_pdl(k_noise_frames, dim3((unsigned)((tot + 255) / 256)), 256, 0, st,
-                               noise, win, fr, B, n, nfr, size, nfft, start0, hop);
+    cudaError_t e = launch_pdl(k_noise_frames,
+                               dim3((unsigned)(B * nfr), (unsigned)((nfft + 255) / 256)), 256, 0,
+                               st, noise, win, fr, B, n, nfr, size, nfft, start0, hop);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -796,15 +794,12 @@ cudaError_t launch_frame_ola(const float* y, float* out, int64_t B, int64_t n, i
                              int size, int ld, int delay, int64_t start0, int hop, float inv_cola,
                              bool adj, cudaStream_t st) {
     cudaError_t e;
-    if (!adj) {
-        const int64_t tot = B * n;
-        e = launch_pdl(k_frame_ola, dim3((unsigned)((tot + 255) / 256)), 256, 0, st, y, out, B, n,
-                       nfr, size, ld, delay, start0, hop, inv_cola);
-    } else {
-        const int64_t tot = B * nfr * ld;
-        e = launch_pdl(k_frame_ola_vjp, dim3((unsigned)((tot + 255) / 256)), 256, 0, st, y, out, B,
-                       n, nfr, size, ld, delay, start0, hop, inv_cola);
-    }
+    if (!adj)
+        e = launch_pdl(k_frame_ola, dim3((unsigned)B, (unsigned)((n + 255) / 256)), 256, 0, st, y,
+                       out, B, n, nfr, size, ld, delay, start0, hop, inv_cola);
+    else
+        e = launch_pdl(k_frame_ola_vjp, dim3((unsigned)(B * nfr), (unsigned)((ld + 255) / 256)),
+                       256, 0, st, y, out, B, n, nfr, size, ld, delay, start0, hop, inv_cola);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
