@@ -584,6 +584,46 @@ def mss_loss(x, y, fft_sizes=DEFAULT_FFT_SIZES, eps=LOG_EPS):
     return total / len(fft_sizes)
 
 
+class _StackPad(torch.autograd.Function):
+    """Rows of [B_i, T] tensors stacked into one [sum B_i, Tp] buffer, zero
+    past T (one copy, like torch.cat); the VJP slices the gradient back."""
+
+    @staticmethod
+    def forward(ctx, Tp, *xs):
+        T = xs[0].shape[1]
+        out = xs[0].new_empty((sum(x.shape[0] for x in xs), Tp))
+        r = 0
+        for x in xs:
+            out[r:r + x.shape[0], :T].copy_(x)
+            r += x.shape[0]
+        out[:, T:].zero_()
+        ctx.rows = [x.shape[0] for x in xs]
+        ctx.T = T
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        outs, r = [], 0
+        for n in ctx.rows:
+            outs.append(g[r:r + n, :ctx.T])
+            r += n
+        return (None, *outs)
+
+
+def _lp_frames(xs, frames, hop):
+    """The frame-rate LP (autograd.lp_tv_frames) of the rows of ``xs`` stacked
+    as one batch.  The signals are laid out at a length Tp >= T that is a
+    multiple of the hop with the same frame count (48001 -> 48240 at hop 240,
+    zeros after T; the causal filter's first T outputs and, with a zero
+    gradient on the tail, their VJP are unchanged), so the C ABI finds a
+    sub-chunk plan without its pack/unpack copies; the output is [:, :T]."""
+    T = xs[0].shape[1]
+    Tp = -(-T // hop) * hop
+    if Tp == T or (Tp - 1) // hop != (T - 1) // hop:
+        return ag.lp_tv_frames(xs[0] if len(xs) == 1 else torch.cat(xs), frames, hop)
+    return ag.lp_tv_frames(_StackPad.apply(Tp, *xs), frames, hop)[:, :T]
+
+
 @dataclass
 class Decoder:
     """The reference decoder graph (synth.py:217-275) in torch on the GPU.
@@ -633,7 +673,7 @@ class Decoder:
             if self.framewise:
                 s = ag.framewise(hgain * (osc + noise_s), a_frames, self._plan())
             else:
-                s = ag.lp_tv_frames(hgain * (osc + noise_s), a_frames, hop)
+                s = _lp_frames([hgain * (osc + noise_s)], a_frames, hop)
             return global_fir(s, p["fir_taps"])
         if self.c_lp:
             # H(z) on the glottal source and C(z) on the noise in ONE launch
@@ -643,10 +683,10 @@ class Decoder:
             # sample-rate grouped entry point, lp_tv_grouped, serves callers
             # that hold [B, T, M] tracks)
             Bn = osc.shape[0]
-            sc = ag.lp_tv_frames(torch.cat([hgain * osc, noise_s]),
-                                 torch.cat([a_frames, c_frames.to(a_frames.dtype)]), hop)
+            sc = _lp_frames([hgain * osc, noise_s],
+                            torch.cat([a_frames, c_frames.to(a_frames.dtype)]), hop)
             return global_fir(sc[:Bn] + sc[Bn:], p["fir_taps"])
-        s = ag.lp_tv_frames(hgain * osc, a_frames, hop)
+        s = _lp_frames([hgain * osc], a_frames, hop)
         return global_fir(s + noise_s, p["fir_taps"])
 
 
