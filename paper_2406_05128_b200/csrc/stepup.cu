@@ -30,8 +30,13 @@ __device__ __forceinline__ double np_pairwise(const double* x, int n) {
 }
 
 // a_m = [a_{m-1} + k_{m-1} * reverse(a_{m-1}), k_{m-1}]  (params.py:43-53)
+// one thread per row, 32 per CTA: the rows spread over every SM (at 128 per
+// CTA a decoder step's 6.4 k rows sat on 51 SMs, and the VJP's per-thread
+// stage arrays -- 3.5 KB of local memory each -- thrashed their L1)
+constexpr int kStepThreads = 32;
+
 template <typename IO>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kStepThreads)
 k_step_up(const IO* __restrict__ k, IO* __restrict__ a, int64_t rows, int M,
           int* __restrict__ bad) {
     grid_dep_wait();
@@ -55,7 +60,7 @@ k_step_up(const IO* __restrict__ k, IO* __restrict__ a, int64_t rows, int M,
 // params.py:74-84: g = grad_a; for m = M..2: grad_k[m-1] = g[m-1] +
 // sum(g[:m-1] * reverse(stage_{m-1})); g = g[:m-1] + k[m-1] * reverse(g[:m-1]).
 template <typename IO>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kStepThreads)
 k_step_up_vjp(const IO* __restrict__ grad_a, const IO* __restrict__ k, IO* __restrict__ grad_k,
               int64_t rows, int M) {
     grid_dep_wait();
@@ -91,14 +96,16 @@ k_step_up_vjp(const IO* __restrict__ grad_a, const IO* __restrict__ k, IO* __res
 template <typename IO>
 cudaError_t launch_step_up(const IO* k, IO* a, int64_t rows, int M, int* bad, cudaStream_t st) {
     if (M < 1 || M > kStepMax) return cudaErrorInvalidValue;
-    launch_pdl(k_step_up<IO>, (unsigned)((rows + 127) / 128), 128, 0, st, k, a, rows, M, bad);
+    launch_pdl(k_step_up<IO>, (unsigned)((rows + kStepThreads - 1) / kStepThreads), kStepThreads,
+               0, st, k, a, rows, M, bad);
     return cudaGetLastError();
 }
 template <typename IO>
 cudaError_t launch_step_up_vjp(const IO* ga, const IO* k, IO* gk, int64_t rows, int M,
                                cudaStream_t st) {
     if (M < 1 || M > kStepMax) return cudaErrorInvalidValue;
-    launch_pdl(k_step_up_vjp<IO>, (unsigned)((rows + 127) / 128), 128, 0, st, ga, k, gk, rows, M);
+    launch_pdl(k_step_up_vjp<IO>, (unsigned)((rows + kStepThreads - 1) / kStepThreads),
+               kStepThreads, 0, st, ga, k, gk, rows, M);
     return cudaGetLastError();
 }
 template cudaError_t launch_step_up<float>(const float*, float*, int64_t, int, int*, cudaStream_t);
