@@ -1137,8 +1137,8 @@ int tvlp_global_fir(const float* x, const float* taps, float* y, int64_t B, int6
 static bool noise_geo_ok(int64_t B, int64_t n, int64_t nfr, int32_t size, int32_t ld,
                          int32_t delay, int32_t hop) {
     // (grid y covers one item's samples / one frame row in blocks of 256)
-    return B >= 0 && n >= 1 && n <= (1 << 24) && nfr >= 1 && size >= 1 && hop >= 1 &&
-           delay >= 0 && ld >= size + delay && ld <= (1 << 24);
+    return B >= 0 && B <= 65535 && n >= 1 && n <= (1 << 24) && nfr >= 1 && nfr < (1 << 30) &&
+           size >= 1 && hop >= 1 && delay >= 0 && ld >= size + delay && ld <= (1 << 24);
 }
 
 int tvlp_noise_frames(const float* noise, const float* window, float* frames, int64_t B,
@@ -1175,7 +1175,8 @@ int64_t tvlp_stft_nframes(int64_t n, int32_t N, int32_t hop) {
 
 int tvlp_stft_frames(const float* x, const float* window, float* frames, int64_t B, int64_t n,
                      int32_t N, int32_t hop, void* stream) {
-    if (!x || !window || !frames || B < 0 || tvlp_stft_nframes(n, N, hop) == 0) return TVLP_ERR_ARG;
+    if (!x || !window || !frames || B < 0 || B > 65535 || tvlp_stft_nframes(n, N, hop) == 0)
+        return TVLP_ERR_ARG;
     if (B == 0) return TVLP_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     TVLP_CK(tracked("stft_frames", 1, st,

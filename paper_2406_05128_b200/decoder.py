@@ -14,10 +14,12 @@ decoders on a numpy tape (pkg/src/tvlp/synth.py:217-275) from these pieces:
 
 Here they are batched torch operations on CUDA tensors (cuFFT/cuDNN
 library kernels -- SURVEY.md §8(f): "torch/cuFFT first, fuse only if
-profiled hot"), differentiated by torch autograd, except the two pieces that
-profiled hot in the float32 decoder step: the oscillator (phase, table read,
-decimation) and the global FIR run on this package's kernels
-(csrc/decoder_kernels.cu; ``wavetable_osc``, ``global_fir``); the LP filters
+profiled hot"), differentiated by torch autograd, except the pieces that
+profiled hot in the float32 decoder step, which run on this package's
+kernels (csrc/decoder_kernels.cu): the oscillator (phase, table read,
+decimation; ``wavetable_osc``), the global FIR (``global_fir``), the noise
+shaping's framing and overlap-add (``shape_noise``) and the MSS loss's
+framing and loss terms (``mss_loss``; its spectra stay cuFFT); the LP filters
 are this package's sm_100a kernels (the fused upsample+LP ``autograd.lp_tv_frames``
 and the grouped pair ``autograd.lp_tv_grouped`` for a C(z) LP).
 Every op follows the reference's arithmetic order closely enough that the
