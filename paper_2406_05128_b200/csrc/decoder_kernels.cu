@@ -552,13 +552,33 @@ k_mss_reduce(const float2* __restrict__ X, const float2* __restrict__ Y, int64_t
     const int64_t lo = n * blockIdx.x / nchunk, hi = n * (blockIdx.x + 1) / nchunk;
     const float2* xb = X + b * n;
     const float2* yb = Y + b * n;
+    // four independent elements per iteration (the loop was latency-bound:
+    // IPC 1.1 with one dependent load pair in flight per thread)
     float s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int64_t step = blockDim.x;
+    int64_t i = lo + threadIdx.x;
+    for (; i + 3 * step < hi; i += 4 * step) {
+        float2 xv[4], yv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            xv[u] = xb[i + u * step];
+            yv[u] = yb[i + u * step];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float mx = mss_mag(xv[u]), my = mss_mag(yv[u]);
+            const float d = mx - my;
+            s1 = fmaf(d, d, s1);
+            s2 = fmaf(my, my, s2);
+            s3 += fabsf(__logf(mx + eps) - __logf(my + eps));  // (MUFU: ~1e-6 absolute)
+        }
+    }
+    for (; i < hi; i += step) {
         const float mx = mss_mag(xb[i]), my = mss_mag(yb[i]);
         const float d = mx - my;
         s1 = fmaf(d, d, s1);
         s2 = fmaf(my, my, s2);
-        s3 += fabsf(__logf(mx + eps) - __logf(my + eps));  // (MUFU: ~1e-6 absolute)
+        s3 += fabsf(__logf(mx + eps) - __logf(my + eps));
     }
     __shared__ float red[3][kMssThreads / 32];
 #pragma unroll
@@ -608,20 +628,30 @@ k_mss_grad(const float2* __restrict__ X, const float2* __restrict__ Y,
            const float* __restrict__ aux, const float* __restrict__ gterm, int64_t B, int64_t n,
            float eps, float2* __restrict__ gX) {
     grid_dep_wait();
-    const int64_t b = blockIdx.x;   // grid: (items, element blocks): no 64-bit division
-    const int64_t k = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const int64_t i = b * n + k;
+    const int64_t b = blockIdx.x;   // grid: (items, element blocks of 4 x 256): no division
     const float g = gterm[b];
     const float r1 = aux[b * 4 + 0], yn = aux[b * 4 + 1];
-    const float2 x = X[i];
-    const float mx = mss_mag(x), my = mss_mag(Y[i]);
-    const float dl = __logf(mx + eps) - __logf(my + eps);
-    const float sg = dl > 0.f ? 1.f : (dl < 0.f ? -1.f : 0.f);
-    float gm = sg / ((float)n * (mx + eps));
-    if (r1 > 0.f) gm += (mx - my) / (r1 * yn);
-    gm *= g;
-    gX[i] = mx > 0.f ? make_float2(gm * x.x / mx, gm * x.y / mx) : make_float2(0.f, 0.f);
+    // per-item factors; two reciprocals per element instead of four divisions
+    const float c_la = g / (float)n, c_sc = r1 > 0.f ? g / (r1 * yn) : 0.f;
+    const int64_t k0 = (int64_t)blockIdx.y * 4 * blockDim.x + threadIdx.x;
+    float2 xv[4], yv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {   // four independent elements in flight
+        const int64_t k = k0 + u * blockDim.x;
+        xv[u] = k < n ? X[b * n + k] : make_float2(0.f, 0.f);
+        yv[u] = k < n ? Y[b * n + k] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t k = k0 + u * blockDim.x;
+        if (k >= n) break;
+        const float mx = mss_mag(xv[u]), my = mss_mag(yv[u]);
+        const float dl = __logf(mx + eps) - __logf(my + eps);
+        const float sg = dl > 0.f ? 1.f : (dl < 0.f ? -1.f : 0.f);
+        const float gm = fmaf(c_sc, mx - my, c_la * sg * __frcp_rn(mx + eps));
+        const float q = mx > 0.f ? gm * __frcp_rn(mx) : 0.f;
+        gX[b * n + k] = make_float2(q * xv[u].x, q * xv[u].y);
+    }
 }
 
 int mss_chunks(int64_t n) { return (int)std::min<int64_t>(64, std::max<int64_t>(1, n / 4096)); }
@@ -644,7 +674,7 @@ cudaError_t launch_mss_terms_vjp(const float* X, const float* Y, const float* au
                                  const float* gterm, int64_t B, int64_t n, float eps, float* gX,
                                  cudaStream_t st) {
     cudaError_t e = launch_pdl(k_mss_grad,
-                               dim3((unsigned)B, (unsigned)((n + kMssThreads - 1) / kMssThreads)),
+                               dim3((unsigned)B, (unsigned)((n + 4 * kMssThreads - 1) / (4 * kMssThreads))),
                                kMssThreads, 0, st, reinterpret_cast<const float2*>(X),
                                reinterpret_cast<const float2*>(Y), aux, gterm, B, n, eps,
                                reinterpret_cast<float2*>(gX));
