@@ -282,6 +282,17 @@ int tvlp_frame_ola(const float* y, float* out, int64_t B, int64_t n, int64_t nfr
                    int32_t ld, int32_t delay, int64_t start0, int32_t hop, float scale,
                    int32_t adjoint, void* stream);
 
+/* The noise shaping's FFT-convolution product (source.py:404-412):
+ * P[b][i] = S[b][i] * H[b][rows[i]] over K complex bins (interleaved float
+ * pairs; S [B, nframes, K], H [B, F, K], rows [nframes] device int32,
+ * nondecreasing), and its VJP to H: grad_H[b][f] = sum over the frames i
+ * with rows[i] = f (i in [first[f], first[f+1]), first [F+1]) of
+ * grad_P[b][i] * conj(S[b][i]), in frame order. */
+int tvlp_spectra_mul(const float* S, const float* H, const int32_t* rows, float* P, int64_t B,
+                     int64_t nframes, int64_t F, int32_t K, void* stream);
+int tvlp_spectra_mul_vjp(const float* grad_P, const float* S, const int32_t* first, float* grad_H,
+                         int64_t B, int64_t nframes, int64_t F, int32_t K, void* stream);
+
 /* stft_mag's framing (loss.py:46-63): x [B, n] reflect-padded by N/2, frames
  * of N samples every `hop`, times window [N] -> frames [B, nframes, N]
  * (nframes = tvlp_stft_nframes(n, N, hop); 0 = invalid: n < N or

@@ -1168,6 +1168,30 @@ int tvlp_frame_ola(const float* y, float* out, int64_t B, int64_t n, int64_t nfr
     return TVLP_OK;
 }
 
+int tvlp_spectra_mul(const float* S, const float* H, const int32_t* rows, float* P, int64_t B,
+                     int64_t nframes, int64_t F, int32_t K, void* stream) {
+    if (!S || !H || !rows || !P || B < 0 || B > 65535 || nframes < 1 || F < 1 || K < 1)
+        return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("spectra_mul", 1, st, [&] {
+        return launch_spec_mul(S, H, rows, nullptr, P, B, nframes, F, K, false, st);
+    }));
+    return TVLP_OK;
+}
+
+int tvlp_spectra_mul_vjp(const float* grad_P, const float* S, const int32_t* first, float* grad_H,
+                         int64_t B, int64_t nframes, int64_t F, int32_t K, void* stream) {
+    if (!grad_P || !S || !first || !grad_H || B < 0 || B > 65535 || nframes < 1 || F < 1 || K < 1)
+        return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("spectra_mul_vjp", 1, st, [&] {
+        return launch_spec_mul(grad_P, S, nullptr, first, grad_H, B, nframes, F, K, true, st);
+    }));
+    return TVLP_OK;
+}
+
 int64_t tvlp_stft_nframes(int64_t n, int32_t N, int32_t hop) {
     if (n < 1 || n > (1 << 24) || N < 2 || hop < 1 || n < N || N / 2 >= n) return 0;
     return 1 + (n + 2 * (N / 2) - N) / hop;

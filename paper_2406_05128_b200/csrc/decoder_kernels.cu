@@ -843,4 +843,58 @@ cudaError_t launch_frame_ola(const float* y, float* out, int64_t B, int64_t n, i
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- noise spectra
+// The frame FIRs' spectra applied to the noise frames' spectra
+// (source.py:404-412, FFT convolution): P[b][i] = S[b][i] * H[b][rows[i]]
+// (complex, K bins; rows[i] = the frame's FIR row, lead-in frames share row
+// 0) without materialising H[:, rows]; the VJP to H sums, in frame order,
+// gP * conj(S) over the frames that use each row (rows is nondecreasing, so
+// row f's frames are the contiguous range first[f] .. first[f+1]-1).
+__global__ void k_spec_mul(const float2* __restrict__ S, const float2* __restrict__ H,
+                           const int* __restrict__ rows, float2* __restrict__ P, int64_t nfr,
+                           int64_t F, int K) {
+    grid_dep_wait();
+    const int64_t i = blockIdx.x, b = blockIdx.z;        // grid: (frames, bins, items)
+    const int k = blockIdx.y * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const float2 s = S[(b * nfr + i) * K + k];
+    const float2 h = H[(b * F + rows[i]) * K + k];
+    P[(b * nfr + i) * K + k] = make_float2(s.x * h.x - s.y * h.y, s.x * h.y + s.y * h.x);
+}
+
+__global__ void k_spec_mul_vjp(const float2* __restrict__ gP, const float2* __restrict__ S,
+                               const int* __restrict__ first, float2* __restrict__ gH,
+                               int64_t nfr, int64_t F, int K) {
+    grid_dep_wait();
+    const int64_t f = blockIdx.x, b = blockIdx.z;        // grid: (rows, bins, items)
+    const int k = blockIdx.y * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int i = first[f]; i < first[f + 1]; ++i) {
+        const float2 g = gP[(b * nfr + i) * K + k];
+        const float2 s = S[(b * nfr + i) * K + k];
+        // g * conj(s)
+        acc.x += g.x * s.x + g.y * s.y;
+        acc.y += g.y * s.x - g.x * s.y;
+    }
+    gH[(b * F + f) * K + k] = acc;
+}
+
+cudaError_t launch_spec_mul(const float* S, const float* H, const int* rows, const int* first,
+                            float* out, int64_t B, int64_t nfr, int64_t F, int K, bool adj,
+                            cudaStream_t st) {
+    cudaError_t e;
+    if (!adj)
+        e = launch_pdl(k_spec_mul, dim3((unsigned)nfr, (unsigned)((K + 255) / 256), (unsigned)B),
+                       256, 0, st, reinterpret_cast<const float2*>(S),
+                       reinterpret_cast<const float2*>(H), rows, reinterpret_cast<float2*>(out), nfr,
+                       F, K);
+    else  // S: the output gradient gP, H: the noise spectra S
+        e = launch_pdl(k_spec_mul_vjp, dim3((unsigned)F, (unsigned)((K + 255) / 256), (unsigned)B),
+                       256, 0, st, reinterpret_cast<const float2*>(S),
+                       reinterpret_cast<const float2*>(H), first, reinterpret_cast<float2*>(out),
+                       nfr, F, K);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace tvlp

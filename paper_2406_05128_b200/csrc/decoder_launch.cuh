@@ -42,4 +42,7 @@ cudaError_t launch_noise_frames(const float* noise, const float* win, float* fr,
 cudaError_t launch_frame_ola(const float* y, float* out, int64_t B, int64_t n, int64_t nfr,
                              int size, int ld, int delay, int64_t start0, int hop, float inv_cola,
                              bool adj, cudaStream_t st);
+cudaError_t launch_spec_mul(const float* S, const float* H, const int* rows, const int* first,
+                            float* out, int64_t B, int64_t nfr, int64_t F, int K, bool adj,
+                            cudaStream_t st);
 }  // namespace tvlp

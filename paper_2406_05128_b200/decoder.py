@@ -338,6 +338,51 @@ def _frame_starts(plan, n_out, F):
     return -plan.n_lead_in() * plan.hop
 
 
+def _row_ranges(plan, n_out, F, device):
+    """int32 FIR row of every frame (nondecreasing: lead-in frames share row
+    0) and, per row, the first frame using it ([F + 1])."""
+    key = ("rowranges", plan.frame_size, plan.hop, n_out, F)
+
+    def build(which):
+        rows = np.asarray(_frame_index_host(plan, n_out, F)[0], dtype=np.int64)
+        if which == 0:
+            return torch.as_tensor(rows.astype(np.int32))
+        return torch.as_tensor(np.searchsorted(rows, np.arange(F + 1)).astype(np.int32))
+    return (_on_device(key + (0,), lambda: build(0), device, None),
+            _on_device(key + (1,), lambda: build(1), device, None))
+
+
+class _SpecMulB200(torch.autograd.Function):
+    """S[b, i] * H[b, rows[i]] (the FFT-convolution product of shape_noise,
+    source.py:404-412) on tvlp_spectra_mul without gathering H's rows; the
+    VJP to H (the noise spectra S carry no gradient) on tvlp_spectra_mul_vjp."""
+
+    @staticmethod
+    def forward(ctx, S, H, rows, first):
+        lib = N.load()
+        S, H = S.contiguous(), H.contiguous()
+        Bn, nfr, K = S.shape
+        P = torch.empty_like(S)
+        with N.on_device(S.device):
+            N.check(lib.tvlp_spectra_mul(N.ptr(S), N.ptr(H), N.ptr(rows), N.ptr(P), Bn, nfr,
+                                         H.shape[1], K, N.stream_ptr(S.device)))
+        ctx.save_for_backward(S, first)
+        ctx.F = H.shape[1]
+        return P
+
+    @staticmethod
+    def backward(ctx, gP):
+        S, first = ctx.saved_tensors
+        lib = N.load()
+        gP = gP.contiguous()
+        Bn, nfr, K = S.shape
+        gH = torch.empty((Bn, ctx.F, K), dtype=S.dtype, device=S.device)
+        with N.on_device(S.device):
+            N.check(lib.tvlp_spectra_mul_vjp(N.ptr(gP), N.ptr(S), N.ptr(first), N.ptr(gH), Bn, nfr,
+                                             ctx.F, K, N.stream_ptr(S.device)))
+        return None, gH, None, None
+
+
 class _FrameOLAB200(torch.autograd.Function):
     """shape_noise's overlap-add of the filtered frames, read from the FIR's
     delay on, / COLA (source.py:418-428), as a fixed-order gather
@@ -397,7 +442,9 @@ def shape_noise(logmag, noise, plan):
         with N.on_device(dev):
             N.check(lib.tvlp_noise_frames(N.ptr(noise), N.ptr(win), N.ptr(segs), Bn, n_out, nfr,
                                           size, nfft, start0, plan.hop, N.stream_ptr(dev)))
-        spec = torch.fft.rfft(segs) * torch.fft.rfft(fir[:, rows], n=nfft)
+        rows32, first32 = _row_ranges(plan, n_out, F, dev)
+        spec = _SpecMulB200.apply(torch.fft.rfft(segs), torch.fft.rfft(fir, n=nfft), rows32,
+                                  first32)
         y = torch.fft.irfft(spec, n=nfft)                         # [B, nfr, nfft]
         return _FrameOLAB200.apply(y, n_out, size, delay, start0, plan.hop,
                                    1.0 / plan._cola_cached())
