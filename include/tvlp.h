@@ -297,12 +297,16 @@ int tvlp_spectra_mul_vjp(const float* grad_P, const float* S, const int32_t* fir
  * of N samples every `hop`, times window [N] -> frames [B, nframes, N]
  * (nframes = tvlp_stft_nframes(n, N, hop); 0 = invalid: n < N or
  * N/2 >= n); the VJP overlap-adds the windowed frame gradients back through
- * the pads (loss.py:81-86), times `scale`. */
+ * the pads (loss.py:81-86), each frame's value taken as scale * grad_frames +
+ * dc_scale * dc[frame * dc_stride] (dc nullable: the one-sided spectrum's DC
+ * correction when grad_frames is a plain inverse FFT of the spectrum's
+ * gradient, odd N). */
 int64_t tvlp_stft_nframes(int64_t n, int32_t N, int32_t hop);
 int tvlp_stft_frames(const float* x, const float* window, float* frames, int64_t B, int64_t n,
                      int32_t N, int32_t hop, void* stream);
 int tvlp_stft_frames_vjp(const float* grad_frames, const float* window, float* grad_x, int64_t B,
-                         int64_t n, int32_t N, int32_t hop, float scale, void* stream);
+                         int64_t n, int32_t N, int32_t hop, float scale, const float* dc,
+                         int64_t dc_stride, float dc_scale, void* stream);
 
 /* One FFT size of the multi-resolution spectral loss (loss.py:105-126) from
  * one-sided spectra (the caller's FFTs): X (signal) and Y (target) complex

@@ -104,7 +104,7 @@ _SIGS = [
     ("tvlp_stft_nframes", _I64, [_I64, _I32, _I32]),
     ("tvlp_stft_frames", ctypes.c_int, [_P, _P, _P, _I64, _I64, _I32, _I32, _P]),
     ("tvlp_stft_frames_vjp", ctypes.c_int,
-     [_P, _P, _P, _I64, _I64, _I32, _I32, ctypes.c_float, _P]),
+     [_P, _P, _P, _I64, _I64, _I32, _I32, ctypes.c_float, _P, _I64, ctypes.c_float, _P]),
     ("tvlp_mss_terms_workspace", _SZ, [_I64, _I64]),
     ("tvlp_mss_terms", ctypes.c_int, [_P, _P, _I64, _I64, ctypes.c_float, _P, _P, _P, _SZ, _P]),
     ("tvlp_mss_terms_vjp", ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, ctypes.c_float, _P]),

@@ -1209,13 +1209,16 @@ int tvlp_stft_frames(const float* x, const float* window, float* frames, int64_t
 }
 
 int tvlp_stft_frames_vjp(const float* grad_frames, const float* window, float* grad_x, int64_t B,
-                         int64_t n, int32_t N, int32_t hop, float scale, void* stream) {
-    if (!grad_frames || !window || !grad_x || B < 0 || tvlp_stft_nframes(n, N, hop) == 0)
+                         int64_t n, int32_t N, int32_t hop, float scale, const float* dc,
+                         int64_t dc_stride, float dc_scale, void* stream) {
+    if (!grad_frames || !window || !grad_x || B < 0 || tvlp_stft_nframes(n, N, hop) == 0 ||
+        (dc && dc_stride < 1))
         return TVLP_ERR_ARG;
     if (B == 0) return TVLP_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     TVLP_CK(tracked("stft_frames_vjp", 1, st, [&] {
-        return launch_stft_frames_vjp(grad_frames, window, grad_x, B, n, N, hop, scale, st);
+        return launch_stft_frames_vjp(grad_frames, window, grad_x, B, n, N, hop, scale, dc,
+                                      dc_stride, dc_scale, st);
     }));
     return TVLP_OK;
 }

@@ -711,9 +711,12 @@ __global__ void k_stft_frames(const float* __restrict__ x, const float* __restri
     }
 }
 
-// grad of padded position p: sum over frames f with 0 <= p - f hop < N
+// grad of padded position p: sum over frames f with 0 <= p - f hop < N of
+// win[j] (scale gframe[f][j] + dc_scale dc[f])  (dc: nullable per-frame term)
 __device__ __forceinline__ float stft_pad_grad(const float* __restrict__ gfb,
-                                               const float* __restrict__ win, int p, int N,
+                                               const float* __restrict__ win,
+                                               const float* __restrict__ dcb, int64_t dcs,
+                                               float scale, float dc_scale, int p, int N,
                                                int hop, int nfr) {
     int f1 = p / hop;
     if (f1 > nfr - 1) f1 = nfr - 1;
@@ -722,14 +725,17 @@ __device__ __forceinline__ float stft_pad_grad(const float* __restrict__ gfb,
     float s = 0.f;
     for (int f = f0; f <= f1; ++f) {
         const int j = p - f * hop;
-        s = fmaf(gfb[(int64_t)f * N + j], win[j], s);
+        float v = gfb[(int64_t)f * N + j] * scale;
+        if (dcb != nullptr) v = fmaf(dc_scale, dcb[f * dcs], v);
+        s = fmaf(v, win[j], s);
     }
     return s;
 }
 
 __global__ void k_stft_frames_vjp(const float* __restrict__ gfr, const float* __restrict__ win,
                                   float* __restrict__ gx, int64_t B, int64_t n, int N, int hop,
-                                  int64_t nfr, float scale) {
+                                  int64_t nfr, float scale, const float* __restrict__ dc,
+                                  int64_t dcs, float dc_scale) {
     grid_dep_wait();
     const int64_t b = blockIdx.x;
     const int t = blockIdx.y * blockDim.x + threadIdx.x;   // (n < 2^31: 32-bit index math)
@@ -737,13 +743,16 @@ __global__ void k_stft_frames_vjp(const float* __restrict__ gfr, const float* __
     const int64_t i = b * n + t;
     const int pad = N / 2, nn = (int)n, nf = (int)nfr;
     const float* gfb = gfr + b * nfr * N;
+    const float* dcb = dc == nullptr ? nullptr : dc + b * nfr * dcs;
     // padded positions mapping to t: t + pad; pad - t (left mirror, 1 <= t <= pad);
     // pad + 2(n-1) - t (right mirror, n-1-pad <= t <= n-2)
-    float s = stft_pad_grad(gfb, win, t + pad, N, hop, nf);
-    if (t >= 1 && t <= pad) s += stft_pad_grad(gfb, win, pad - t, N, hop, nf);
+    float s = stft_pad_grad(gfb, win, dcb, dcs, scale, dc_scale, t + pad, N, hop, nf);
+    if (t >= 1 && t <= pad)
+        s += stft_pad_grad(gfb, win, dcb, dcs, scale, dc_scale, pad - t, N, hop, nf);
     if (t <= nn - 2 && t >= nn - 1 - pad)
-        s += stft_pad_grad(gfb, win, pad + 2 * (nn - 1) - t, N, hop, nf);
-    gx[i] = s * scale;
+        s += stft_pad_grad(gfb, win, dcb, dcs, scale, dc_scale, pad + 2 * (nn - 1) - t, N, hop,
+                           nf);
+    gx[i] = s;
 }
 
 cudaError_t launch_stft_frames(const float* x, const float* win, float* fr, int64_t B, int64_t n,
@@ -755,10 +764,12 @@ cudaError_t launch_stft_frames(const float* x, const float* win, float* fr, int6
 }
 
 cudaError_t launch_stft_frames_vjp(const float* gfr, const float* win, float* gx, int64_t B,
-                                   int64_t n, int N, int hop, float scale, cudaStream_t st) {
+                                   int64_t n, int N, int hop, float scale, const float* dc,
+                                   int64_t dcs, float dc_scale, cudaStream_t st) {
     const int64_t nfr = 1 + (n + 2 * (N / 2) - N) / hop;
     cudaError_t e = launch_pdl(k_stft_frames_vjp, dim3((unsigned)B, (unsigned)((n + 255) / 256)),
-                               256, 0, st, gfr, win, gx, B, n, N, hop, nfr, scale);
+                               256, 0, st, gfr, win, gx, B, n, N, hop, nfr, scale, dc, dcs,
+                               dc_scale);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 

@@ -35,7 +35,8 @@ cudaError_t launch_mss_terms_vjp(const float* X, const float* Y, const float* au
 cudaError_t launch_stft_frames(const float* x, const float* win, float* fr, int64_t B, int64_t n,
                                int N, int hop, cudaStream_t st);
 cudaError_t launch_stft_frames_vjp(const float* gfr, const float* win, float* gx, int64_t B,
-                                   int64_t n, int N, int hop, float scale, cudaStream_t st);
+                                   int64_t n, int N, int hop, float scale, const float* dc,
+                                   int64_t dcs, float dc_scale, cudaStream_t st);
 cudaError_t launch_noise_frames(const float* noise, const float* win, float* fr, int64_t B,
                                 int64_t n, int64_t nfr, int size, int nfft, int64_t start0, int hop,
                                 cudaStream_t st);

@@ -556,15 +556,27 @@ class _SpectrumB200(torch.autograd.Function):
     def backward(ctx, gX):
         B, n, size, hop = ctx.cfg
         lib = N.load()
-        half = _on_device(("rfft_adjoint_scale", size), lambda: torch.tensor(
-            [1.0] + [0.5] * ((size - 1) // 2) + ([1.0] if size % 2 == 0 else [])),
-            gX.device, torch.float32)
-        gfr = torch.fft.irfft(gX * half, n=size, dim=-1).contiguous()
+        gX = gX.contiguous()
         win = _hann_periodic(size, gX.device, torch.float32)
         gx = torch.empty((B, n), dtype=torch.float32, device=gX.device)
+        if size % 2:
+            # odd N: sum_k Re(g_k e^{i theta}) over the one-sided bins is
+            # (N/2) irfft(g) + Re(g_0)/2 (irfft doubles bins >= 1), so the
+            # inverse FFT takes the gradient as is and the DC term rides in
+            # the overlap-add kernel
+            gfr = torch.fft.irfft(gX, n=size, dim=-1).contiguous()
+            dc = torch.view_as_real(gX)[..., 0, 0]             # Re(g_0) per frame (view)
+            with N.on_device(gX.device):
+                N.check(lib.tvlp_stft_frames_vjp(N.ptr(gfr), N.ptr(win), N.ptr(gx), B, n, size,
+                                                 hop, 0.5 * size, N.ptr(dc), 2 * gX.shape[-1],
+                                                 0.5, N.stream_ptr(gX.device)))
+            return gx, None, None
+        half = _on_device(("rfft_adjoint_scale", size), lambda: torch.tensor(
+            [1.0] + [0.5] * ((size - 1) // 2) + [1.0]), gX.device, torch.float32)
+        gfr = torch.fft.irfft(gX * half, n=size, dim=-1).contiguous()
         with N.on_device(gX.device):
             N.check(lib.tvlp_stft_frames_vjp(N.ptr(gfr), N.ptr(win), N.ptr(gx), B, n, size, hop,
-                                             float(size), N.stream_ptr(gX.device)))
+                                             float(size), None, 0, 0.0, N.stream_ptr(gX.device)))
         return gx, None, None
 
 
