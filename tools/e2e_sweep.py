@@ -20,7 +20,7 @@ for ch in (2, 4, 8, 16, 32, 64):
     print("chunks", ch, round(a.elapsed_time(b) / 5, 3), "ms")
 
 # copy-only pipeline (same streams/events, no kernels)
-bufs = stream._buffers(torch.device("cuda", 0), B, T, M, torch.float32, B // 8, False)
+bufs = stream._buffers(torch.device("cuda", 0), B, T, M, torch.float32, [B // 8], False)
 h2d, comp, d2h = stream._streams(torch.device("cuda", 0), 3)
 def copies(n):
     main = torch.cuda.current_stream()
