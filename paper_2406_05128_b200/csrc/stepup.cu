@@ -93,6 +93,59 @@ k_step_up_vjp(const IO* __restrict__ grad_a, const IO* __restrict__ k, IO* __res
     for (int i = 0; i < M; ++i) grad_k[r * M + i] = (IO)gk[i];
 }
 
+// float32 rows (the decoder): one warp per row, lane i holds component i in
+// float64 registers; the reversed-coefficient reads are warp shuffles, the
+// VJP's stage vectors stay in registers (no 3.5 KB local array per row) and
+// its dot products are warp sums (not numpy's pairwise order: the float64
+// entry point keeps the bit-exact kernel above).
+__global__ void __launch_bounds__(128)
+k_step_up_vjp_warp(const float* __restrict__ grad_a, const float* __restrict__ k,
+                   float* __restrict__ grad_k, int64_t rows, int M) {
+    grid_dep_wait();
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const float* kr = k + r * M;
+    const double kl = lane < M ? (double)kr[lane] : 0.0;
+    // forward: stage m-1 (length m-1) kept per lane: st[m] = component `lane` of
+    // the stage entering step m (valid for lane < m - 1)
+    double st[kStepMax];
+    const double k0 = __shfl_sync(0xffffffffu, kl, 0);
+    double cur = lane == 0 ? k0 : 0.0;
+#pragma unroll
+    for (int m = 2; m <= kStepMax; ++m) {
+        if (m > M) break;
+        st[m - 2] = cur;
+        const double km = __shfl_sync(0xffffffffu, kl, m - 1);
+        const int src = m - 2 - lane;
+        const double rev = __shfl_sync(0xffffffffu, cur, src >= 0 ? src : 0);
+        double nxt = cur;
+        if (lane < m - 1) nxt = __dadd_rn(cur, __dmul_rn(km, rev));
+        else if (lane == m - 1) nxt = km;
+        cur = nxt;
+    }
+    double g = lane < M ? (double)grad_a[r * M + lane] : 0.0;
+    double gk = 0.0;
+#pragma unroll
+    for (int m = kStepMax; m >= 2; --m) {
+        if (m > M) continue;
+        // gk[m-1] = g[m-1] + sum_{i < m-1} g[i] * stage[m-2-i]
+        const int src = m - 2 - lane;
+        const double prev = __shfl_sync(0xffffffffu, st[m - 2], src >= 0 ? src : 0);
+        double prod = lane < m - 1 ? g * prev : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
+        const double gm1 = __shfl_sync(0xffffffffu, g, m - 1);
+        if (lane == m - 1) gk = gm1 + prod;
+        // g[i] <- g[i] + k[m-1] g[m-2-i] for i < m-1
+        const double km = __shfl_sync(0xffffffffu, kl, m - 1);
+        const double rev = __shfl_sync(0xffffffffu, g, src >= 0 ? src : 0);
+        if (lane < m - 1) g = __dadd_rn(g, __dmul_rn(km, rev));
+    }
+    if (lane == 0) gk = g;
+    if (lane < M) grad_k[r * M + lane] = (float)gk;
+}
+
 template <typename IO>
 cudaError_t launch_step_up(const IO* k, IO* a, int64_t rows, int M, int* bad, cudaStream_t st) {
     if (M < 1 || M > kStepMax) return cudaErrorInvalidValue;
@@ -104,6 +157,11 @@ template <typename IO>
 cudaError_t launch_step_up_vjp(const IO* ga, const IO* k, IO* gk, int64_t rows, int M,
                                cudaStream_t st) {
     if (M < 1 || M > kStepMax) return cudaErrorInvalidValue;
+    if constexpr (std::is_same<IO, float>::value) {
+        launch_pdl(k_step_up_vjp_warp, (unsigned)((rows * 32 + 127) / 128), 128, 0, st, ga, k, gk,
+                   rows, M);
+        return cudaGetLastError();
+    }
     launch_pdl(k_step_up_vjp<IO>, (unsigned)((rows + kStepThreads - 1) / kStepThreads),
                kStepThreads, 0, st, ga, k, gk, rows, M);
     return cudaGetLastError();

@@ -656,3 +656,22 @@ def test_long_sequence_frames_and_ti():
     rge, rga = oracle.lp_backward_ti(g[0].astype(np.float64), a[0].astype(np.float64), rs)
     errs = (_err(_np(s)[0], rs), _err(_np(ge)[0], rge), _err(_np(ga)[0], rga))
     assert max(errs) < 1e-5, errs
+
+
+@pytest.mark.parametrize("M", [1, 2, 5, 22, 30])
+def test_reflection_vjp_float32_warp_kernel(M):
+    """float32 step-up VJP (one warp per row, warp-sum dot products) against
+    the bit-exact float64 kernel on the same rows."""
+    from paper_2406_05128_b200 import params
+
+    rng = np.random.default_rng(M)
+    k = rng.uniform(-0.95, 0.95, (257, M))
+    ga = rng.standard_normal((257, M))
+    ref = params.reflection_to_lpc_vjp(torch.tensor(ga, device="cuda"),
+                                       torch.tensor(k, device="cuda")).cpu().numpy()
+    got = params.reflection_to_lpc_vjp(torch.tensor(ga, dtype=torch.float32, device="cuda"),
+                                       torch.tensor(k, dtype=torch.float32, device="cuda"))
+    assert got.dtype == torch.float32
+    got = got.cpu().numpy()
+    for r in range(257):
+        assert oracle.gradcheck_error(got[r], ref[r]) < 1e-5, r
