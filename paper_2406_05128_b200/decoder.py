@@ -127,6 +127,18 @@ class _Upsample(torch.autograd.Function):
     def backward(ctx, g):
         F, hop, T1, nd = ctx.shape
         Bn = g.shape[0]
+        if nd == 2 and F > 1 and _b200_pieces(g):
+            # float32 CUDA: the F-1 full blocks' two weighted sums as ONE thin
+            # GEMM over a view of g (no pad copy, no weighted temporaries);
+            # the last (held, w = 0) block is a plain sum
+            g = g.contiguous()
+            wm = _on_device(("upsample_w2", hop), lambda: torch.stack(
+                [1.0 - torch.arange(hop, dtype=torch.float64) / hop,
+                 torch.arange(hop, dtype=torch.float64) / hop], dim=1), g.device, g.dtype)
+            ab = torch.matmul(g[:, :(F - 1) * hop].reshape(Bn, F - 1, hop), wm)   # [B, F-1, 2]
+            gf = torch.cat([ab[..., 0], g[:, (F - 1) * hop:].sum(dim=1, keepdim=True)], dim=1)
+            gf[:, 1:] += ab[..., 1]
+            return gf, None, None
         w = _block_weights(F, hop, g.device, g.dtype)
         pad = F * hop - T1
         if nd == 3:
