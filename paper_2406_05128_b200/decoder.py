@@ -102,6 +102,13 @@ def _block_weights(F, hop, device, dtype):
     return w
 
 
+def _upsample_w2(hop, device, dtype):
+    """[hop, 2]: the interpolation weights (1 - j/hop, j/hop) of one block."""
+    return _on_device(("upsample_w2", hop), lambda: torch.stack(
+        [1.0 - torch.arange(hop, dtype=torch.float64) / hop,
+         torch.arange(hop, dtype=torch.float64) / hop], dim=1), device, dtype)
+
+
 class _Upsample(torch.autograd.Function):
     """params.py:120-145 as dense block arithmetic: forward
     (1 - w) frames[f] + w frames[f + 1] over [F, hop] blocks (bit-identical to
@@ -111,8 +118,16 @@ class _Upsample(torch.autograd.Function):
     @staticmethod
     def forward(ctx, frames, hop, T1):
         Bn, F = frames.shape[:2]
-        w = _block_weights(F, hop, frames.device, frames.dtype)
         nxt = torch.cat([frames[:, 1:], frames[:, -1:]], dim=1)
+        ctx.shape = (F, hop, T1, frames.dim())
+        if frames.dim() == 2 and _b200_pieces(frames):
+            # float32 CUDA: [a, b] x [(1 - w), w]^T for every block as one thin
+            # GEMM (K = 2) writing the track once; the held last block has
+            # b = a, so it needs no w = 0 special case (a (1 - w) + a w)
+            out = torch.matmul(torch.stack([frames, nxt], dim=-1),
+                               _upsample_w2(hop, frames.device, frames.dtype).t())
+            return out.reshape(Bn, F * hop)[:, :T1]
+        w = _block_weights(F, hop, frames.device, frames.dtype)
         if frames.dim() == 3:
             w = w[..., None]
             out = (1.0 - w) * frames[:, :, None] + w * nxt[:, :, None]   # [B, F, hop, D]
@@ -132,10 +147,8 @@ class _Upsample(torch.autograd.Function):
             # GEMM over a view of g (no pad copy, no weighted temporaries);
             # the last (held, w = 0) block is a plain sum
             g = g.contiguous()
-            wm = _on_device(("upsample_w2", hop), lambda: torch.stack(
-                [1.0 - torch.arange(hop, dtype=torch.float64) / hop,
-                 torch.arange(hop, dtype=torch.float64) / hop], dim=1), g.device, g.dtype)
-            ab = torch.matmul(g[:, :(F - 1) * hop].reshape(Bn, F - 1, hop), wm)   # [B, F-1, 2]
+            ab = torch.matmul(g[:, :(F - 1) * hop].reshape(Bn, F - 1, hop),
+                              _upsample_w2(hop, g.device, g.dtype))            # [B, F-1, 2]
             gf = torch.cat([ab[..., 0], g[:, (F - 1) * hop:].sum(dim=1, keepdim=True)], dim=1)
             gf[:, 1:] += ab[..., 1]
             return gf, None, None
