@@ -1784,9 +1784,11 @@ k_grad_frames(const FrameSrc<IO> fs, const IO* __restrict__ ge, const IO* __rest
     // support of frames fbase..fbase+K-1: t in [(fbase-1) hop, (fbase+K) hop)
     const int64_t tlo = (fbase - 1) * hop;
     const int span = (kFramesPerCta + 1) * hop;
-    IO* p0 = reinterpret_cast<IO*>(gf_smem);  // (1-w(t)) (-grad_e(t)), t = tlo + i
-    IO* p1 = p0 + span;                        // w(t) (-grad_e(t))
-    IO* ss = p1 + span;                        // s(tlo - LAG + i)
+    // -grad_e(t), t = tlo + i (the interval weights (1 - w), w are applied in
+    // the reduction: two staged arrays instead of three keep the grid in one
+    // wave -- 12 CTAs per SM instead of 8 at hop 240)
+    IO* gn = reinterpret_cast<IO*>(gf_smem);
+    IO* ss = gn + span;                        // s(tlo - LAG + i)
     const IO* gb = ge + b * T;
     const IO* sb = s + b * T;
     const IO inv_hop = (IO)1 / (IO)hop;
@@ -1821,12 +1823,7 @@ k_grad_frames(const FrameSrc<IO> fs, const IO* __restrict__ ge, const IO* __rest
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const int i = i0 + j * blockDim.x;
-            if (i < span) {
-                const int q = i / hop;  // frame fbase - 1 + q, offset i - q hop
-                const IO w = (fbase - 1 + q < fs.nF - 1) ? (IO)(i - q * hop) * inv_hop : (IO)0;
-                p0[i] = ((IO)1 - w) * v[j];
-                p1[i] = w * v[j];
-            }
+            if (i < span) gn[i] = v[j];
         }
     }
     __syncthreads();
@@ -1837,7 +1834,10 @@ k_grad_frames(const FrameSrc<IO> fs, const IO* __restrict__ ge, const IO* __rest
     // part 0: t in [f hop, (f+1) hop) -> local i = (k+1) hop + r, weight p0
     // part 1: t in [(f-1) hop, f hop) -> local i = k hop + r, weight p1 (f >= 1)
     const int i0 = (k + 1 - part) * hop;
-    const IO* pw = part == 0 ? p0 : p1;
+    // the interval's weight of frame f: part 0 (its own interval, frame f):
+    // 1 - w, w = r / hop (0 in the held last interval); part 1 (interval of
+    // frame f - 1, never the last): w -- the same products as staging them
+    const bool held = part == 0 && !(f < fs.nF - 1);
     IO acc[4] = {(IO)0, (IO)0, (IO)0, (IO)0};
     if (f < fs.nF && (part == 0 || f >= 1)) {
         // x[j] = s(t - 1 - c0 - j) at the current t (ss index LAG + i - 1 - c0 - j)
@@ -1845,7 +1845,8 @@ k_grad_frames(const FrameSrc<IO> fs, const IO* __restrict__ ge, const IO* __rest
         IO x0 = sp[0], x1 = sp[-1], x2 = sp[-2], x3 = sp[-3];
 #pragma unroll 4
         for (int r = 0; r < hop; ++r) {
-            const IO pv = pw[i0 + r];
+            const IO w = held ? (IO)0 : (IO)r * inv_hop;
+            const IO pv = (part == 0 ? (IO)1 - w : w) * gn[i0 + r];
             acc[0] = fma(pv, x0, acc[0]);
             acc[1] = fma(pv, x1, acc[1]);
             acc[2] = fma(pv, x2, acc[2]);

@@ -386,7 +386,7 @@ template <typename IO>
 cudaError_t launch_grad_frames(const FrameSrc<IO>& fr, const IO* ge, const IO* s, const IO* zi,
                                int Mzi, IO* gF, int64_t B, int64_t T, cudaStream_t st) {
     if (fr.Mf > 32) return cudaErrorInvalidValue;
-    const size_t sm = (size_t)(3 * (kFramesPerCta + 1) * fr.hop + 32) * sizeof(IO);
+    const size_t sm = (size_t)(2 * (kFramesPerCta + 1) * fr.hop + 32) * sizeof(IO);
     if (sm > 200 * 1024) return cudaErrorInvalidValue;
     auto k = k_grad_frames<IO>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
