@@ -84,16 +84,6 @@ def design_lowpass(num_taps=127, cutoff=0.45, oversample=4):
     return _lowpass_np(num_taps, cutoff, oversample).copy()
 
 
-def _weights(F, hop, T1, device, dtype):
-    """params.py:107-117 on the device: anchors f0, f1 and weights for T1 samples."""
-    t = torch.arange(T1, device=device)
-    f0 = torch.div(t, hop, rounding_mode="floor")
-    w = (t - f0 * hop).to(dtype) / float(hop)
-    f1 = torch.clamp(f0 + 1, max=F - 1)
-    w = torch.where(f0 == F - 1, torch.zeros_like(w), w)
-    return f0, f1, w
-
-
 def _block_weights(F, hop, device, dtype):
     """The same weights as [F, hop] blocks (block f covers t = f*hop + j):
     j / hop, and 0 in the last block (params.py:113-115)."""
