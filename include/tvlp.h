@@ -293,6 +293,22 @@ int tvlp_spectra_mul(const float* S, const float* H, const int32_t* rows, float*
 int tvlp_spectra_mul_vjp(const float* grad_P, const float* S, const int32_t* first, float* grad_H,
                          int64_t B, int64_t nframes, int64_t F, int32_t K, void* stream);
 
+/* The HpN decoder's two LP inputs in one pass (synth.py:264-273 with the
+ * paper's C(z) LP; decoder.Decoder.render): out [2B, Tp] = rows
+ * h_gain(t) (sig(t) voiced_gain(t)) then noise(t) noise_gain(t), zero from T1
+ * to Tp, the gains [B, F] upsampled at `hop` (params.py:107-132; F = (T1-1)/hop
+ * + 1, T1 <= Tp <= F hop); sig, noise [B, T1].  The VJP writes grad_sig,
+ * grad_noise [B, T1] and the three gain-frame gradients [B, F]; workspace:
+ * 6 B F floats. */
+int tvlp_source_pair(const float* sig, const float* noise, const float* voiced_gain,
+                     const float* noise_gain, const float* h_gain, float* out, int64_t B,
+                     int64_t T1, int64_t F, int32_t hop, int64_t Tp, void* stream);
+int tvlp_source_pair_vjp(const float* grad_out, const float* sig, const float* noise,
+                         const float* voiced_gain, const float* noise_gain, const float* h_gain,
+                         float* grad_sig, float* grad_noise, float* grad_voiced_gain,
+                         float* grad_noise_gain, float* grad_h_gain, float* workspace, int64_t B,
+                         int64_t T1, int64_t F, int32_t hop, int64_t Tp, void* stream);
+
 /* stft_mag's framing (loss.py:46-63): x [B, n] reflect-padded by N/2, frames
  * of N samples every `hop`, times window [N] -> frames [B, nframes, N]
  * (nframes = tvlp_stft_nframes(n, N, hop); 0 = invalid: n < N or

@@ -101,6 +101,9 @@ _SIGS = [
      [_P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _I64, _I32, ctypes.c_float, _I32, _P]),
     ("tvlp_spectra_mul", ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _I32, _P]),
     ("tvlp_spectra_mul_vjp", ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _I32, _P]),
+    ("tvlp_source_pair", ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I64, _P]),
+    ("tvlp_source_pair_vjp", ctypes.c_int,
+     [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I64, _P]),
     ("tvlp_stft_nframes", _I64, [_I64, _I32, _I32]),
     ("tvlp_stft_frames", ctypes.c_int, [_P, _P, _P, _I64, _I64, _I32, _I32, _P]),
     ("tvlp_stft_frames_vjp", ctypes.c_int,

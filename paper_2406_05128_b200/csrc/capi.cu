@@ -1192,6 +1192,45 @@ int tvlp_spectra_mul_vjp(const float* grad_P, const float* S, const int32_t* fir
     return TVLP_OK;
 }
 
+static bool source_geo_ok(int64_t B, int64_t T1, int64_t F, int32_t hop, int64_t Tp) {
+    return B >= 0 && B <= 65535 && T1 >= 1 && hop >= 1 && F == (T1 - 1) / hop + 1 &&
+           Tp >= T1 && Tp <= F * hop;
+}
+
+int tvlp_source_pair(const float* sig, const float* noise, const float* voiced_gain,
+                     const float* noise_gain, const float* h_gain, float* out, int64_t B,
+                     int64_t T1, int64_t F, int32_t hop, int64_t Tp, void* stream) {
+    if (!sig || !noise || !voiced_gain || !noise_gain || !h_gain || !out ||
+        !source_geo_ok(B, T1, F, hop, Tp))
+        return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("source_pair", 1, st, [&] {
+        return launch_source_pair(sig, noise, voiced_gain, noise_gain, h_gain, out, B, T1, F, hop,
+                                  Tp, st);
+    }));
+    return TVLP_OK;
+}
+
+int tvlp_source_pair_vjp(const float* grad_out, const float* sig, const float* noise,
+                         const float* voiced_gain, const float* noise_gain, const float* h_gain,
+                         float* grad_sig, float* grad_noise, float* grad_voiced_gain,
+                         float* grad_noise_gain, float* grad_h_gain, float* workspace, int64_t B,
+                         int64_t T1, int64_t F, int32_t hop, int64_t Tp, void* stream) {
+    if (!grad_out || !sig || !noise || !voiced_gain || !noise_gain || !h_gain || !grad_sig ||
+        !grad_noise || !grad_voiced_gain || !grad_noise_gain || !grad_h_gain || !workspace ||
+        !source_geo_ok(B, T1, F, hop, Tp))
+        return TVLP_ERR_ARG;
+    if (B == 0) return TVLP_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TVLP_CK(tracked("source_pair_vjp", 2, st, [&] {
+        return launch_source_pair_vjp(grad_out, sig, noise, voiced_gain, noise_gain, h_gain,
+                                      grad_sig, grad_noise, grad_voiced_gain, grad_noise_gain,
+                                      grad_h_gain, workspace, B, T1, F, hop, Tp, st);
+    }));
+    return TVLP_OK;
+}
+
 int64_t tvlp_stft_nframes(int64_t n, int32_t N, int32_t hop) {
     if (n < 1 || n > (1 << 24) || N < 2 || hop < 1 || n < N || N / 2 >= n) return 0;
     return 1 + (n + 2 * (N / 2) - N) / hop;

@@ -908,4 +908,131 @@ cudaError_t launch_spec_mul(const float* S, const float* H, const int* rows, con
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- HpN source pair
+// The HpN decoder's two LP inputs (synth.py:264-273 with the paper's C(z),
+// decoder.Decoder.render) in one pass: rows b < B: H(t) (sig(t) V(t)), rows
+// B + b: noise(t) G(t), zero from T1 to Tp = F hop, where V, G, H are the
+// upsampled gain frames (params.py:107-132: w = j / hop, held last frame) --
+// instead of three upsampled tracks, three products and the stacking copy.
+// The VJP writes grad_sig, grad_noise and, per (item, frame block), the six
+// weighted block sums of the three gain tracks' gradients; a combine adds
+// each frame's two intervals (params.py:135-145).
+struct GainPair {
+    float a, d;  // frame value and slope to the next frame (0 in the last)
+};
+
+__device__ __forceinline__ float gain_at(const float* __restrict__ fr, int64_t F, int64_t f,
+                                         float w) {
+    const float a = fr[f];
+    const float b = f + 1 < F ? fr[f + 1] : a;
+    return __fadd_rn(__fmul_rn(__fsub_rn(1.f, w), a), __fmul_rn(w, b));
+}
+
+__global__ void k_source_pair(const float* __restrict__ sig, const float* __restrict__ noise,
+                              const float* __restrict__ vg, const float* __restrict__ ng,
+                              const float* __restrict__ hg, float* __restrict__ out, int64_t B,
+                              int64_t T1, int64_t F, int hop, int64_t Tp) {
+    grid_dep_wait();
+    const int64_t f = blockIdx.x, b = blockIdx.y;   // grid: (frame blocks, items)
+    const float inv_hop = 1.f / (float)hop;
+    for (int j = threadIdx.x; j < hop; j += blockDim.x) {
+        const int64_t t = f * hop + j;
+        if (t >= Tp) break;
+        float o0 = 0.f, o1 = 0.f;
+        if (t < T1) {
+            const float w = f == F - 1 ? 0.f : __fmul_rn((float)j, inv_hop);
+            const float V = gain_at(vg + b * F, F, f, w), H = gain_at(hg + b * F, F, f, w);
+            const float G = gain_at(ng + b * F, F, f, w);
+            o0 = __fmul_rn(H, __fmul_rn(sig[b * T1 + t], V));
+            o1 = __fmul_rn(noise[b * T1 + t], G);
+        }
+        out[b * Tp + t] = o0;
+        out[(B + b) * Tp + t] = o1;
+    }
+}
+
+__global__ void k_source_pair_vjp(const float* __restrict__ g, const float* __restrict__ sig,
+                                  const float* __restrict__ noise, const float* __restrict__ vg,
+                                  const float* __restrict__ ng, const float* __restrict__ hg,
+                                  float* __restrict__ gsig, float* __restrict__ gnoise,
+                                  float* __restrict__ part, int64_t B, int64_t T1, int64_t F,
+                                  int hop, int64_t Tp) {
+    grid_dep_wait();
+    const int64_t f = blockIdx.x, b = blockIdx.y;
+    const float inv_hop = 1.f / (float)hop;
+    float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // (1-w), w sums of dV, dH, dG
+    for (int j = threadIdx.x; j < hop; j += blockDim.x) {
+        const int64_t t = f * hop + j;
+        if (t >= T1) break;
+        const float w = f == F - 1 ? 0.f : __fmul_rn((float)j, inv_hop);
+        const float V = gain_at(vg + b * F, F, f, w), H = gain_at(hg + b * F, F, f, w);
+        const float G = gain_at(ng + b * F, F, f, w);
+        const float gt = g[b * Tp + t], gb = g[(B + b) * Tp + t];
+        const float sv = sig[b * T1 + t], nv = noise[b * T1 + t];
+        const float sV = __fmul_rn(sv, V);
+        gsig[b * T1 + t] = __fmul_rn(__fmul_rn(gt, H), V);
+        gnoise[b * T1 + t] = __fmul_rn(gb, G);
+        const float dV = __fmul_rn(__fmul_rn(gt, H), sv), dH = __fmul_rn(gt, sV);
+        const float dG = __fmul_rn(gb, nv);
+        const float w1 = __fsub_rn(1.f, w);
+        acc[0] = fmaf(w1, dV, acc[0]);
+        acc[1] = fmaf(w, dV, acc[1]);
+        acc[2] = fmaf(w1, dH, acc[2]);
+        acc[3] = fmaf(w, dH, acc[3]);
+        acc[4] = fmaf(w1, dG, acc[4]);
+        acc[5] = fmaf(w, dG, acc[5]);
+    }
+    __shared__ float red[6][8];
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) red[q][wid] = acc[q];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        float tsum = 0.f;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tsum += red[threadIdx.x][k];
+        part[(b * F + f) * 6 + threadIdx.x] = tsum;
+    }
+}
+
+// grad of gain frames: X[b][f] = part[b][f].(1-w)X + part[b][f-1].wX
+__global__ void k_source_pair_combine(const float* __restrict__ part, float* __restrict__ gv,
+                                      float* __restrict__ gh, float* __restrict__ gn, int64_t B,
+                                      int64_t F) {
+    grid_dep_wait();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= B * F) return;
+    const int64_t f = r % F;
+    const float* p = part + r * 6;
+    const float* q = f > 0 ? part + (r - 1) * 6 : nullptr;
+    gv[r] = p[0] + (q ? q[1] : 0.f);
+    gh[r] = p[2] + (q ? q[3] : 0.f);
+    gn[r] = p[4] + (q ? q[5] : 0.f);
+}
+
+cudaError_t launch_source_pair(const float* sig, const float* noise, const float* vg,
+                               const float* ng, const float* hg, float* out, int64_t B, int64_t T1,
+                               int64_t F, int hop, int64_t Tp, cudaStream_t st) {
+    cudaError_t e = launch_pdl(k_source_pair, dim3((unsigned)F, (unsigned)B), 256, 0, st, sig, noise,
+                               vg, ng, hg, out, B, T1, F, hop, Tp);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_source_pair_vjp(const float* g, const float* sig, const float* noise,
+                                   const float* vg, const float* ng, const float* hg, float* gsig,
+                                   float* gnoise, float* gvg, float* gng, float* ghg, float* part,
+                                   int64_t B, int64_t T1, int64_t F, int hop, int64_t Tp,
+                                   cudaStream_t st) {
+    cudaError_t e = launch_pdl(k_source_pair_vjp, dim3((unsigned)F, (unsigned)B), 256, 0, st, g, sig,
+                               noise, vg, ng, hg, gsig, gnoise, part, B, T1, F, hop, Tp);
+    if (e == cudaSuccess)
+        e = launch_pdl(k_source_pair_combine, dim3((unsigned)((B * F + 255) / 256)), 256, 0, st,
+                       (const float*)part, gvg, ghg, gng, B, F);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace tvlp

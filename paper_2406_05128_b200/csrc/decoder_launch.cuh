@@ -46,4 +46,12 @@ cudaError_t launch_frame_ola(const float* y, float* out, int64_t B, int64_t n, i
 cudaError_t launch_spec_mul(const float* S, const float* H, const int* rows, const int* first,
                             float* out, int64_t B, int64_t nfr, int64_t F, int K, bool adj,
                             cudaStream_t st);
+cudaError_t launch_source_pair(const float* sig, const float* noise, const float* vg,
+                               const float* ng, const float* hg, float* out, int64_t B, int64_t T1,
+                               int64_t F, int hop, int64_t Tp, cudaStream_t st);
+cudaError_t launch_source_pair_vjp(const float* g, const float* sig, const float* noise,
+                                   const float* vg, const float* ng, const float* hg, float* gsig,
+                                   float* gnoise, float* gvg, float* gng, float* ghg, float* part,
+                                   int64_t B, int64_t T1, int64_t F, int hop, int64_t Tp,
+                                   cudaStream_t st);
 }  // namespace tvlp

@@ -660,6 +660,46 @@ def mss_loss(x, y, fft_sizes=DEFAULT_FFT_SIZES, eps=LOG_EPS):
     return total / len(fft_sizes)
 
 
+class _SourcePairB200(torch.autograd.Function):
+    """The HpN LP pair's inputs [2B, Tp] -- H (sig V) over N G, zero past T1
+    -- in one kernel (tvlp_source_pair) from the gain FRAMES, and the VJP to
+    sig, noise and the three gain frame tensors (tvlp_source_pair_vjp)."""
+
+    @staticmethod
+    def forward(ctx, sig, noise, vg, ng, hg, hop, Tp):
+        lib = N.load()
+        sig, noise = sig.contiguous(), noise.contiguous()
+        vg, ng, hg = vg.contiguous(), ng.contiguous(), hg.contiguous()
+        Bn, T1 = sig.shape
+        F = vg.shape[1]
+        out = torch.empty((2 * Bn, Tp), dtype=sig.dtype, device=sig.device)
+        with N.on_device(sig.device):
+            N.check(lib.tvlp_source_pair(N.ptr(sig), N.ptr(noise), N.ptr(vg), N.ptr(ng), N.ptr(hg),
+                                         N.ptr(out), Bn, T1, F, hop, Tp,
+                                         N.stream_ptr(sig.device)))
+        ctx.save_for_backward(sig, noise, vg, ng, hg)
+        ctx.cfg = (hop, Tp)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        sig, noise, vg, ng, hg = ctx.saved_tensors
+        hop, Tp = ctx.cfg
+        lib = N.load()
+        g = g.contiguous()
+        Bn, T1 = sig.shape
+        F = vg.shape[1]
+        gs, gn = torch.empty_like(sig), torch.empty_like(noise)
+        gv, gng, gh = torch.empty_like(vg), torch.empty_like(ng), torch.empty_like(hg)
+        ws = torch.empty(6 * Bn * F, dtype=torch.float32, device=sig.device)
+        with N.on_device(sig.device):
+            N.check(lib.tvlp_source_pair_vjp(N.ptr(g), N.ptr(sig), N.ptr(noise), N.ptr(vg),
+                                             N.ptr(ng), N.ptr(hg), N.ptr(gs), N.ptr(gn), N.ptr(gv),
+                                             N.ptr(gng), N.ptr(gh), N.ptr(ws), Bn, T1, F, hop, Tp,
+                                             N.stream_ptr(sig.device)))
+        return gs, gn, gv, gng, gh, None, None
+
+
 class _StackPad(torch.autograd.Function):
     """Rows of [B_i, T] tensors stacked into one [sum B_i, Tp] buffer, zero
     past T (one copy, like torch.cat); the VJP slices the gradient back."""
@@ -741,8 +781,18 @@ class Decoder:
         vgain = torch.exp(p["voiced_gain_raw"])
         # oscillator (source.py:294-314)
         sig = wavetable_osc(pos, f0_frames, self.tables, hop, n_out, self.fs, self.oversample)
-        osc = sig * upsample_linear(vgain, hop, T1)
         noise_unit = shape_noise(p["noise_logmag"], noise.to(pos.dtype), self._plan())
+        if self.mode == "hpn" and self.c_lp and _b200_pieces(sig):
+            Tp = -(-T1 // hop) * hop
+            if (Tp - 1) // hop == (T1 - 1) // hop:
+                # both LP inputs, gains applied, in one kernel (no gain tracks)
+                Bn = sig.shape[0]
+                e2 = _SourcePairB200.apply(sig, noise_unit, vgain, torch.exp(p["noise_gain_raw"]),
+                                           torch.exp(p["h_gain_raw"]), hop, Tp)
+                sc = ag.lp_tv_frames(e2, torch.cat([a_frames, c_frames.to(a_frames.dtype)]),
+                                     hop)[:, :T1]
+                return global_fir(sc[:Bn] + sc[Bn:], p["fir_taps"])
+        osc = sig * upsample_linear(vgain, hop, T1)
         noise_s = noise_unit * upsample_linear(torch.exp(p["noise_gain_raw"]), hop, T1)
         hgain = upsample_linear(torch.exp(p["h_gain_raw"]), hop, T1)
         if self.mode == "sf":
