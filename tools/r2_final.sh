@@ -17,5 +17,5 @@ bash tools/r2_profiles.sh
 timeout 900 python tools/integration_e2e.py > gpurun_out/${p}_integration_e2e.jsonl 2> gpurun_out/${p}_integration_e2e.err
 timeout 600 python tools/decoder_bench.py 32 > gpurun_out/${p}_decoder_bench.jsonl 2> gpurun_out/${p}_decoder_bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__throughput.avg.pct_of_peak_sustained_elapsed,sm__warps_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active \
-  --clock-control none -k regex:"k_osc|k_fir" -c 12 --csv --log-file gpurun_out/${p}_ncu_decoder_kernels.csv \
+  --clock-control none -k regex:"k_osc|k_fir|k_mss|k_stft|k_noise|k_frame_ola|k_step|k_spec|k_source" -c 60 --csv --log-file gpurun_out/${p}_ncu_decoder_kernels.csv \
   python tools/decoder_prof.py 32 hpn > gpurun_out/${p}_ncu_decoder.log 2>&1
