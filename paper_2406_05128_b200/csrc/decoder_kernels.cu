@@ -1,7 +1,10 @@
-// decoder_kernels.cu -- the two decoder pieces around the LP that profiled
-// hottest in the config-5 step (torch + cuDNN took
-// ~2.6 of its 6.2 ms: a float64 cumsum, table gathers, the x4 decimation
-// conv and its dgrad, the depthwise global FIR and its backward), float32:
+// decoder_kernels.cu -- the decoder pieces around the LP that profiled hot
+// in the config-5 step, float32.
+// First the two that took ~2.6 of the torch step's 6.2 ms (a float64
+// cumsum, table gathers, the x4 decimation conv and its dgrad, the depthwise
+// global FIR and its backward); further down the MSS framing and loss
+// terms, the noise shaping's framing / overlap-add / spectra product and the
+// HpN source pair:
 //
 //  * the wavetable oscillator (source.py:224-318): the table phase in float64
 //    (the frame-rate f0 track is linear inside a frame, so its running sum is a
@@ -917,10 +920,6 @@ cudaError_t launch_spec_mul(const float* S, const float* H, const int* rows, con
 // The VJP writes grad_sig, grad_noise and, per (item, frame block), the six
 // weighted block sums of the three gain tracks' gradients; a combine adds
 // each frame's two intervals (params.py:135-145).
-struct GainPair {
-    float a, d;  // frame value and slope to the next frame (0 in the last)
-};
-
 __device__ __forceinline__ float gain_at(const float* __restrict__ fr, int64_t F, int64_t f,
                                          float w) {
     const float a = fr[f];
