@@ -667,17 +667,67 @@ def run_b200(args, cfg, rank, world, dist):
         h2d = sum(x.numel() * x.element_size() for x in list(ph.values()) + [nh, th])
         d2h = sum(x.numel() * x.element_size() for x in list(gh_.values()) + [yh, lh])
 
-        def e2e_step():
-            with torch.no_grad():
+        # every step copies its inputs up and its results down, on a second
+        # stream through device staging buffers so the copies overlap the
+        # neighbouring steps' graph replays: step i+1's inputs land while step
+        # i replays, step i's results drain while step i+1 replays (double-
+        # buffered); e2e_flush() joins the copy stream before the clock stops
+        cstream = torch.cuda.Stream(dev)
+        s_in = {k: torch.empty_like(v, device=dev) for k, v in ph.items()}
+        s_n, s_t = torch.empty_like(e), torch.empty_like(g)
+        s_out = [({k: torch.empty_like(A[k]) for k in ph}, torch.empty_like(gstep.y),
+                  torch.empty_like(gstep.loss)) for _ in range(2)]
+        pipe = {"i": 0, "in_ready": None, "drained": [None, None]}
+
+        def stage_inputs():
+            with torch.cuda.stream(cstream):
                 for k, v in ph.items():
-                    A[k].copy_(v, non_blocking=True)
-                e.copy_(nh, non_blocking=True)
-                g.copy_(th, non_blocking=True)
+                    s_in[k].copy_(v, non_blocking=True)
+                s_n.copy_(nh, non_blocking=True)
+                s_t.copy_(th, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cstream)
+            return ev
+
+        def e2e_step():
+            main = torch.cuda.current_stream(dev)
+            if pipe["in_ready"] is None:
+                pipe["in_ready"] = stage_inputs()
+            main.wait_event(pipe["in_ready"])
+            with torch.no_grad():
+                for k in ph:
+                    A[k].copy_(s_in[k])
+                e.copy_(s_n)
+                g.copy_(s_t)
+            consumed = torch.cuda.Event()
+            consumed.record(main)
+            cstream.wait_event(consumed)
+            pipe["in_ready"] = stage_inputs()          # the next step's inputs
             y, L, _ = step()
-            yh.copy_(y.detach(), non_blocking=True)
-            lh.copy_(L.detach(), non_blocking=True)
-            for k in ph:
-                gh_[k].copy_(A[k].grad, non_blocking=True)
+            j = pipe["i"] % 2
+            if pipe["drained"][j] is not None:
+                main.wait_event(pipe["drained"][j])
+            og, oy, ol = s_out[j]
+            with torch.no_grad():
+                oy.copy_(y.detach())
+                ol.copy_(L.detach())
+                for k in ph:
+                    og[k].copy_(A[k].grad)
+            ready = torch.cuda.Event()
+            ready.record(main)
+            cstream.wait_event(ready)
+            with torch.cuda.stream(cstream):
+                yh.copy_(oy, non_blocking=True)
+                lh.copy_(ol, non_blocking=True)
+                for k in ph:
+                    gh_[k].copy_(og[k], non_blocking=True)
+                drained = torch.cuda.Event()
+                drained.record(cstream)
+            pipe["drained"][j] = drained
+            pipe["i"] += 1
+
+        def e2e_flush():
+            torch.cuda.current_stream(dev).wait_stream(cstream)
     elif kind == "hpn":
         eh, Ah, gh = (torch.cat([y.cpu() for y in x]).pin_memory() for x in (e, A, g))
         oh = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (eh, eh, Ah)]
@@ -709,12 +759,17 @@ def run_b200(args, cfg, rank, world, dist):
             for o, r in zip(oh, res):
                 o.copy_(r, non_blocking=True)
 
+    if kind != "decoder":
+        def e2e_flush():
+            pass
     for _ in range(max(1, args.warmup)):
         e2e_step()
+    e2e_flush()
     barrier()
     ev0.record(stream)
     for _ in range(args.steps):
         e2e_step()
+    e2e_flush()
     ev1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = pdist.max_over_ranks(ev0.elapsed_time(ev1) / args.steps, dist, dev)
