@@ -800,7 +800,12 @@ def run_b200(args, cfg, rank, world, dist):
         "kernels": per_kernel,
         "e2e": {"value": round(samples / (e2e_ms * 1e-3), 1), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": round(e2e_ms, 3)},
+                "ms_per_step": round(e2e_ms, 3),
+                "copies": ("every step's inputs up and results down on a second stream "
+                           "(double-buffered device staging), overlapping the neighbouring "
+                           "steps' graph replays" if kind == "decoder" else
+                           "pipelined host API (chunks overlap kernels and both copy directions)"
+                           if kind in ("tv", "hpn") else "serial around each step")},
         "gpu_launches": int(launches),
         "nonfinite_outputs": bool(nonfinite_seen),
         "refined_sequences": int(refined),
