@@ -672,7 +672,8 @@ def run_b200(args, cfg, rank, world, dist):
         # neighbouring steps' graph replays: step i+1's inputs land while step
         # i replays, step i's results drain while step i+1 replays (double-
         # buffered); e2e_flush() joins the copy stream before the clock stops
-        cstream = torch.cuda.Stream(dev)
+        cstream = torch.cuda.Stream(dev)    # host -> device
+        dstream = torch.cuda.Stream(dev)    # device -> host (the other copy engine)
         s_in = {k: torch.empty_like(v, device=dev) for k, v in ph.items()}
         s_n, s_t = torch.empty_like(e), torch.empty_like(g)
         s_out = [({k: torch.empty_like(A[k]) for k in ph}, torch.empty_like(gstep.y),
@@ -715,19 +716,20 @@ def run_b200(args, cfg, rank, world, dist):
                     og[k].copy_(A[k].grad)
             ready = torch.cuda.Event()
             ready.record(main)
-            cstream.wait_event(ready)
-            with torch.cuda.stream(cstream):
+            dstream.wait_event(ready)
+            with torch.cuda.stream(dstream):
                 yh.copy_(oy, non_blocking=True)
                 lh.copy_(ol, non_blocking=True)
                 for k in ph:
                     gh_[k].copy_(og[k], non_blocking=True)
                 drained = torch.cuda.Event()
-                drained.record(cstream)
+                drained.record(dstream)
             pipe["drained"][j] = drained
             pipe["i"] += 1
 
         def e2e_flush():
             torch.cuda.current_stream(dev).wait_stream(cstream)
+            torch.cuda.current_stream(dev).wait_stream(dstream)
     elif kind == "hpn":
         eh, Ah, gh = (torch.cat([y.cpu() for y in x]).pin_memory() for x in (e, A, g))
         oh = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (eh, eh, Ah)]
@@ -751,15 +753,50 @@ def run_b200(args, cfg, rank, world, dist):
             if allreduce is not None:
                 allreduce().wait()
     else:
-        def e2e_step():
-            ed = eh.to(dev, non_blocking=True)
-            Ad = Ah.to(dev, non_blocking=True)
-            gd = gh.to(dev, non_blocking=True)
-            res = step(ed, Ad, gd)
-            for o, r in zip(oh, res):
-                o.copy_(r, non_blocking=True)
+        # every step copies its own inputs up and results down on a second
+        # stream: the next step's inputs land in the other device buffer set
+        # while this step runs, and this step's results drain while the next
+        # one runs (results are fresh tensors, held by the allocator until then)
+        cstream2 = torch.cuda.Stream(dev)   # host -> device
+        dstream2 = torch.cuda.Stream(dev)   # device -> host (the other copy engine)
+        bufs_in = [tuple(torch.empty(x.shape, dtype=x.dtype, device=dev) for x in (eh, Ah, gh))
+                   for _ in range(2)]
+        pipe2 = {"i": 0, "ready": [None, None], "free": [None, None]}
 
-    if kind != "decoder":
+        def stage(j):
+            with torch.cuda.stream(cstream2):
+                if pipe2["free"][j] is not None:
+                    cstream2.wait_event(pipe2["free"][j])
+                for d, h in zip(bufs_in[j], (eh, Ah, gh)):
+                    d.copy_(h, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cstream2)
+            pipe2["ready"][j] = ev
+
+        def e2e_step():
+            main = torch.cuda.current_stream(dev)
+            j = pipe2["i"] % 2
+            if pipe2["ready"][j] is None:
+                stage(j)
+            stage(1 - j)                                  # the next step's inputs
+            main.wait_event(pipe2["ready"][j])
+            res = step(*bufs_in[j])
+            done = torch.cuda.Event()
+            done.record(main)
+            pipe2["free"][j] = done
+            pipe2["ready"][j] = None
+            dstream2.wait_event(done)
+            with torch.cuda.stream(dstream2):
+                for o, r in zip(oh, res):
+                    o.copy_(r, non_blocking=True)
+                    r.record_stream(dstream2)             # not reused before the copy drains
+            pipe2["i"] += 1
+
+        def e2e_flush():
+            torch.cuda.current_stream(dev).wait_stream(cstream2)
+            torch.cuda.current_stream(dev).wait_stream(dstream2)
+
+    if kind in ("tv", "hpn"):
         def e2e_flush():
             pass
     for _ in range(max(1, args.warmup)):
@@ -805,7 +842,9 @@ def run_b200(args, cfg, rank, world, dist):
                            "(double-buffered device staging), overlapping the neighbouring "
                            "steps' graph replays" if kind == "decoder" else
                            "pipelined host API (chunks overlap kernels and both copy directions)"
-                           if kind in ("tv", "hpn") else "serial around each step")},
+                           if kind in ("tv", "hpn") else
+                           "every step's inputs up and results down on a second stream, "
+                           "overlapping the neighbouring steps")},
         "gpu_launches": int(launches),
         "nonfinite_outputs": bool(nonfinite_seen),
         "refined_sequences": int(refined),
